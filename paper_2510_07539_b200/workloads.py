@@ -1,0 +1,253 @@
+"""Seeded synthetic inputs for the SI-IMEX hSGN hot path.
+
+This module holds ONLY input generators (initial states, bathymetry, per-member
+parameters) and closed-form reference profiles.  It contains none of the SI
+method's arithmetic, and it is the one module shared by the oracle tests and the
+CUDA path (DESIGN.md section 5 gives the recipe of each config).
+
+Every generator returns fp64 numpy arrays (h, q, K, W) in the state convention
+of DESIGN.md: q = h u, K = h eta (flat) or h (eta + 3 b / 2),
+W = h w.
+
+Closed forms followed:
+  * SGN solitary wave: h = h0 (1 + eps sech^2(kappa (x - x0))),
+    u = C (1 - h0/h), C = sqrt(g h0 (1 + eps)), kappa = sqrt(3 eps / (4 h0^2 (1 + eps))),
+    eta = h, w = -h u_x (A11: K = h^2, W = -h^2 u_x, u_x analytic).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+G_DEFAULT = 9.81  # P:646 (A14: m/s^2)
+
+
+@dataclass
+class Workload:
+    name: str
+    n: int                      # cells per member
+    members: int
+    x_min: float
+    x_max: float
+    bc: tuple                   # ("periodic","periodic") | ("wall","wall") | ...
+    lam: np.ndarray             # [members]
+    h: np.ndarray               # [members, n] (or [n] flattened as [1, n])
+    q: np.ndarray
+    K: np.ndarray
+    W: np.ndarray
+    b: np.ndarray | None = None  # [n] shared by all members, or None
+    g: float = G_DEFAULT
+    cfl: float = 2.0
+    mcfl: float = 0.5
+    steps: int | None = None
+    t_end: float | None = None
+    filter_sigma: float = 0.0
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def dx(self) -> float:
+        return (self.x_max - self.x_min) / self.n
+
+    def x(self) -> np.ndarray:
+        return cell_centres(self.x_min, self.x_max, self.n)
+
+    def state(self, m: int = 0):
+        return [self.h[m], self.q[m], self.K[m], self.W[m]]
+
+    def subset(self, members) -> "Workload":
+        idx = np.asarray(members)
+        return Workload(self.name, self.n, len(idx), self.x_min, self.x_max, self.bc,
+                        self.lam[idx].copy(), self.h[idx].copy(), self.q[idx].copy(),
+                        self.K[idx].copy(), self.W[idx].copy(), self.b, self.g, self.cfl,
+                        self.mcfl, self.steps, self.t_end, self.filter_sigma, dict(self.meta))
+
+
+def cell_centres(x_min: float, x_max: float, n: int) -> np.ndarray:
+    """x_i = x_min + (i + 1/2) dx."""
+    dx = (x_max - x_min) / n
+    return x_min + (np.arange(n, dtype=np.float64) + 0.5) * dx
+
+
+def _wrap(d: np.ndarray, L: float | None) -> np.ndarray:
+    if L is None:
+        return d
+    return d - L * np.floor(d / L + 0.5)  # minimum image in [-L/2, L/2)
+
+
+def soliton_params(h0: float, A: float, g: float = G_DEFAULT):
+    """(eps, kappa, C) of the SGN solitary wave."""
+    eps = A / h0
+    kappa = math.sqrt(3.0 * eps / (4.0 * h0 * h0 * (1.0 + eps)))
+    C = math.sqrt(g * h0 * (1.0 + eps))
+    return eps, kappa, C
+
+
+def soliton_exact(x, t, h0, A, x0, g=G_DEFAULT, L=None):
+    """Exact SGN soliton translated by C t (A13): returns (h, u)."""
+    eps, kappa, C = soliton_params(h0, A, g)
+    d = _wrap(np.asarray(x, dtype=np.float64) - x0 - C * t, L)
+    s2 = 1.0 / np.cosh(kappa * d) ** 2
+    h = h0 * (1.0 + eps * s2)
+    u = C * (1.0 - h0 / h)
+    return h, u
+
+
+def soliton_state(x, h0, A, x0, g=G_DEFAULT, L=None):
+    """hSGN state of the SGN soliton with eta = h, w = -h u_x (A11)."""
+    eps, kappa, C = soliton_params(h0, A, g)
+    d = _wrap(np.asarray(x, dtype=np.float64) - x0, L)
+    th = np.tanh(kappa * d)
+    s2 = 1.0 / np.cosh(kappa * d) ** 2
+    h = h0 * (1.0 + eps * s2)
+    hx = -2.0 * h0 * eps * kappa * s2 * th
+    u = C * (1.0 - h0 / h)
+    ux = C * h0 * hx / (h * h)
+    return h, h * u, h * h, -h * h * ux
+
+
+def multi_soliton_state(x, amps, pos, g=G_DEFAULT, L=None, h0=1.0):
+    """Superposed solitary waves (cfg3): h = h0 + sum_j A_j sech^2(kappa_j d_j),
+    u = sum_j C_j (1 - h0 / (h0 + A_j sech^2)), eta = h, w = -h u_x (analytic)."""
+    h = np.full_like(x, h0)
+    u = np.zeros_like(x)
+    ux = np.zeros_like(x)
+    for A, x0 in zip(amps, pos):
+        _, kappa, C = soliton_params(h0, A, g)
+        d = _wrap(x - x0, L)
+        th = np.tanh(kappa * d)
+        s2 = 1.0 / np.cosh(kappa * d) ** 2
+        hj = h0 + A * s2
+        hjx = -2.0 * A * kappa * s2 * th
+        h = h + A * s2
+        u = u + C * (1.0 - h0 / hj)
+        ux = ux + C * h0 * hjx / (hj * hj)
+    return h, h * u, h * h, -h * h * ux
+
+
+# --------------------------------------------------------------------------
+# BASELINE.json configs (synthetic stand-ins)
+# --------------------------------------------------------------------------
+
+def cfg1(n: int = 1000, lam: float = 500.0, x0: float = -50.0) -> Workload:
+    """Solitary wave, periodic [-100, 100), h0 = 1, a = 0.2, lambda = 500, t_end = 20;
+    dt = min(2.7 dx / nu_max, 0.5 dx / u_max) (A12); A19 filter on (seeded-rest
+    pin decides it, A19)."""
+    x = cell_centres(-100.0, 100.0, n)
+    h, q, K, W = soliton_state(x, 1.0, 0.2, x0, L=200.0)
+    return Workload("cfg1_soliton", n, 1, -100.0, 100.0, ("periodic", "periodic"),
+                    np.array([lam]), h[None], q[None], K[None], W[None], cfl=2.7, mcfl=0.5,
+                    t_end=20.0, filter_sigma=0.25, meta=dict(h0=1.0, A=0.2, x0=x0, L=200.0))
+
+
+def cfg2(lam: float, n: int = 1 << 16, width_cells: float = 0.0) -> Workload:
+    """Dispersive dam break on [-300, 300] with walls: h = 1.8 left / 1.0 right,
+    u = 0, K = h^2, W = 0, t_end = 48.  width_cells > 0 smooths the step as a tanh
+    of that many cells (fallback recipe of DESIGN.md section 5)."""
+    x = cell_centres(-300.0, 300.0, n)
+    dx = 600.0 / n
+    if width_cells > 0:
+        h = 1.4 - 0.4 * np.tanh(x / (width_cells * dx))
+    else:
+        h = np.where(x < 0.0, 1.8, 1.0)
+    z = np.zeros_like(h)
+    return Workload(f"cfg2_dambreak_lam{lam:g}", n, 1, -300.0, 300.0, ("wall", "wall"),
+                    np.array([lam]), h[None], z[None].copy(), (h * h)[None], z[None].copy(),
+                    cfl=2.0, mcfl=0.5, t_end=48.0, filter_sigma=0.25)
+
+
+def cfg3(members: int = 4096, n: int = 4096, seed: int = 7539003, dx: float = 0.1,
+         first_member: int = 0) -> Workload:
+    """Batched ensemble: `members` periodic domains of n cells (dx = 0.1); per member
+    1-3 solitary waves with amplitudes U(0.05, 0.3), positions U[0, L), and
+    lambda = 10^U(2, 4); 200 steps at CFL_IMEX = 2, MCFL = 0.5.
+
+    The per-member draws come from one PCG64 stream in member order, so any
+    subset [first_member, first_member + members) is reproducible on its own."""
+    L = n * dx
+    rng = np.random.Generator(np.random.PCG64(seed))
+    total = first_member + members
+    ns = rng.integers(1, 4, size=total)
+    amps = rng.uniform(0.05, 0.3, size=(total, 3))
+    pos = rng.uniform(0.0, L, size=(total, 3))
+    lam = 10.0 ** rng.uniform(2.0, 4.0, size=total)
+    x = cell_centres(0.0, L, n)
+    H = np.empty((members, n)); Q = np.empty((members, n))
+    KK = np.empty((members, n)); WW = np.empty((members, n))
+    for mi in range(members):
+        m = first_member + mi
+        k = int(ns[m])
+        H[mi], Q[mi], KK[mi], WW[mi] = multi_soliton_state(x, amps[m, :k], pos[m, :k], L=L)
+    return Workload("cfg3_ensemble", n, members, 0.0, L, ("periodic", "periodic"),
+                    lam[first_member:total].copy(), H, Q, KK, WW, cfl=2.0, mcfl=0.5,
+                    steps=200, meta=dict(seed=seed, first_member=first_member))
+
+
+def flat_rest(n: int, dx: float, h0: float = 1.0, lam: float = 500.0, noise: float = 0.0,
+              seed: int = 0, members: int = 1) -> Workload:
+    """Periodic rest state (h0, 0, h0^2, 0) plus optional seeded noise."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    sh = (members, n)
+    h = h0 + noise * rng.standard_normal(sh)
+    q = noise * rng.standard_normal(sh)
+    K = h0 * h0 + noise * rng.standard_normal(sh)
+    W = noise * rng.standard_normal(sh)
+    return Workload("flat_rest", n, members, 0.0, n * dx, ("periodic", "periodic"),
+                    np.full(members, lam), h, q, K, W)
+
+
+def random_smooth(n: int, members: int, seed: int, dx: float = 0.1, amp: float = 0.05,
+                  modes: int = 8, bc=("periodic", "periodic"), lam_range=(1e2, 1e4),
+                  bathy: float = 0.0) -> Workload:
+    """Seeded smooth random states (parity cases): zeta = 1 + amp * sum of periodic
+    modes, u = small smooth field, eta = h (1 + small), w small; optional
+    sinusoidal bathymetry of amplitude `bathy`."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    L = n * dx
+    x = cell_centres(0.0, L, n)
+    H = np.empty((members, n)); Q = np.empty((members, n))
+    KK = np.empty((members, n)); WW = np.empty((members, n))
+    b = None
+    if bathy > 0:
+        b = bathy * np.sin(2 * np.pi * 3 * x / L)
+    for m in range(members):
+        k = rng.integers(1, max(2, n // 16), size=modes)
+        ph = rng.uniform(0, 2 * np.pi, size=(4, modes))
+        a = rng.standard_normal((4, modes)) / np.sqrt(modes)
+        f = [np.sum(a[j, :, None] * np.cos(2 * np.pi * k[:, None] * x[None] / L + ph[j, :, None]), 0)
+             for j in range(4)]
+        zeta = 1.0 + amp * f[0]
+        h = zeta - (b if b is not None else 0.0)
+        u = 0.3 * amp * f[1]
+        eta = h * (1.0 + 0.01 * amp * f[2])
+        w = 0.1 * amp * f[3]
+        H[m] = h
+        Q[m] = h * u
+        KK[m] = h * eta + (1.5 * h * b if b is not None else 0.0)
+        WW[m] = h * w
+    lam = 10.0 ** rng.uniform(np.log10(lam_range[0]), np.log10(lam_range[1]), size=members)
+    return Workload("random_smooth", n, members, 0.0, L, tuple(bc), lam, H, Q, KK, WW, b=b)
+
+
+def gaussian_bell(n: int = 5000, lam: float = 100.0) -> Workload:
+    """Paper's Gaussian bell: h = 1 + exp(-x^2/20) on [-200, 200], u = 0,
+    eta = h, w = 0; CFL_IMEX = 2.  Boundary: transmissive."""
+    x = cell_centres(-200.0, 200.0, n)
+    h = 1.0 + np.exp(-x * x / 20.0)
+    z = np.zeros_like(h)
+    return Workload("gaussian_bell", n, 1, -200.0, 200.0, ("transmissive", "transmissive"),
+                    np.array([lam]), h[None], z[None].copy(), (h * h)[None], z[None].copy(),
+                    cfl=2.0, mcfl=0.5, t_end=35.0)
+
+
+def lake_at_rest(n: int, lam: float, L: float = 40.0, amp: float = 0.1, h_ref: float = 0.5,
+                 bc=("periodic", "periodic")) -> Workload:
+    """zeta = const, u = 0, eta = h, w = 0 over smooth periodic bathymetry."""
+    x = cell_centres(0.0, L, n)
+    b = amp * np.sin(2 * np.pi * x / L) + 0.5 * amp * np.cos(4 * np.pi * x / L)
+    h = h_ref - b
+    z = np.zeros_like(h)
+    K = h * (h + 1.5 * b)
+    return Workload("lake_at_rest", n, 1, 0.0, L, tuple(bc), np.array([lam]), h[None],
+                    z[None].copy(), K[None], z[None].copy(), b=b)

@@ -1,0 +1,80 @@
+"""Mutation check of the oracle pins: apply plausible mistakes to a copy of
+oracle/hsgn_oracle.c and confirm that `pytest tests/test_oracle_pins.py` fails
+for every one of them.  Dev tool; not part of the product or of the test suite.
+
+    python tools/mutation_check.py
+"""
+import os
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = open(os.path.join(ROOT, "oracle", "hsgn_oracle.c")).read()
+
+MUTANTS = {
+    "R2 reading of A1 (mean delta with 1/(2dx^2))":
+        ("const double lt2 = lam * tau * tau / (2.0 * dx * dx);",
+         "const double lt2 = lam * tau * tau / (4.0 * dx * dx);"),
+    "sign of tau*W^dagger in H^dagger":
+        ("- 1.5 * tau * qE * Dxb[i] + tau * Wd_;", "- 1.5 * tau * qE * Dxb[i] - tau * Wd_;"),
+    "beta2 missing factor 2":
+        ("double beta2 = 2.0 * lambda", "double beta2 = 1.0 * lambda"),
+    "transposed hbar neighbours in qbar":
+        ("be[i + 1] * (hr - hl)", "be[i + 1] * (hl - hr)"),
+    "Rusanov speed min instead of max":
+        ("double a = fabs(um) > fabs(up_) ? fabs(um) : fabs(up_);",
+         "double a = fabs(um) < fabs(up_) ? fabs(um) : fabs(up_);"),
+    "Rusanov dissipation sign":
+        ("- 0.5 * a * (vp[1] - vm[1]);", "+ 0.5 * a * (vp[1] - vm[1]);"),
+    "H flux uses q instead of H":
+        ("out[1] = 0.5 * (vm[2] * um + vp[2] * up_)", "out[1] = 0.5 * (vm[1] * um + vp[1] * up_)"),
+    "p-tilde sign in momentum bathymetric source":
+        ("- 1.5 * tau * ptil * Dxb[i];", "+ 1.5 * tau * ptil * Dxb[i];"),
+    "hydrostatic back-substitution term sign":
+        ("- tau * g * X(eh, i) * Dxb[i];", "+ tau * g * X(eh, i) * Dxb[i];"),
+    "MUSCL slope not halved":
+        ("double s0 = (X(ev[k], f + 1) - X(ev[k], f - 1)) / 2.0;",
+         "double s0 = (X(ev[k], f + 1) - X(ev[k], f - 1)) / 1.0;"),
+    "dropped lambda*tau source in W^dagger":
+        ("+ lam * tau;\n", ";\n"),
+    "Hbar uses beta1 at E instead of hbar":
+        ("double Hn = Hd[i + 1] / (1.0 + lam * tau * tau / (hn * hn));",
+         "double Hn = Hd[i + 1] / (1.0 + lam * tau * tau / (X(eh, i) * X(eh, i)));"),
+    "a2 = c2 + lambda eta alpha":
+        ("double a2 = c2 - lambda * eta * alpha;", "double a2 = c2 + lambda * eta * alpha;"),
+    "wE/wR swapped":
+        ("*wE = T->aE[1][0] / T->aI[0][0];\n    *wR = T->aI[1][0] / T->aI[0][0];",
+         "*wR = T->aE[1][0] / T->aI[0][0];\n    *wE = T->aI[1][0] / T->aI[0][0];"),
+    "wall q parity even":
+        ("const double qpar = -1.0;", "const double qpar = 1.0;"),
+    "delta uses beta1^2":
+        ("double delta = alpha / beta1;", "double delta = alpha / (beta1 * beta1);"),
+    "bathymetry source in H^dagger sign":
+        ("- 1.5 * tau * qE * Dxb[i] + tau * Wd_;", "+ 1.5 * tau * qE * Dxb[i] + tau * Wd_;"),
+    "hydrostatic zeta term dropped":
+        ("hd = hd + t2 * (Gr * dbr - Gl * dbl);", "hd = hd + 0.0 * t2 * (Gr * dbr - Gl * dbl);"),
+    "nu_max from P:628 literal":
+        ("return sqrt(g * h + (lambda / 3.0) * eta_over_h * eta_over_h);",
+         "return sqrt(g * h + (lambda / 3.0) * (eta_over_h - 1.0));"),
+}
+
+ok = True
+for name, (a, b) in MUTANTS.items():
+    assert SRC.count(a) >= 1, name
+    mut = SRC.replace(a, b, 1)
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "m.c")
+        so = os.path.join(d, "libm.so")
+        open(c, "w").write(mut)
+        subprocess.check_call(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-o", so, c, "-lm"])
+        env = dict(os.environ, HSGN_ORACLE_LIB=so)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                            os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                           cwd=ROOT, env=env, capture_output=True, text=True)
+        caught = r.returncode != 0
+        first = [l for l in r.stdout.splitlines() if l.startswith("FAILED")][:1]
+        print(("CAUGHT " if caught else "MISSED ") + name + ("  <- " + first[0] if first else ""))
+        ok &= caught
+sys.exit(0 if ok else 1)

@@ -1,0 +1,294 @@
+#!/usr/bin/env python
+"""Benchmark of the SI-IMEX hSGN hot path (BASELINE.json metric:
+"fp64 cell-stage updates/s per GPU and whole box; % of HBM roofline").
+
+Workload: BASELINE configs[2] = cfg3, the batched
+ensemble of 4096 periodic domains x 4096 cells (seeded synthetic solitary
+waves, lambda log-uniform in [1e2, 1e4], CFL_IMEX 2, MCFL 0.5).  It is the
+largest single-GPU throughput config whose roofline is meaningful (state
+512 MiB > L2, so no L2 flush is needed between steps).  One bench "step" = one
+SI-IMEX step (2 stages) over the whole batch.  Multi-GPU: one process per GPU,
+each runs its own 4096-member shard of a 4096*N-member ensemble (weak scaling,
+no data-path collective: members are independent).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hsgn|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 cell-stage updates/s (whole job)"
+UNIT = "cell-stage/s"
+B_STAGE1 = 64   # algorithmic bytes per cell: read U^n (32), write U1 (32)
+B_STAGE2 = 96   # read U^n + U1 (64), write U^{n+1} (32)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="hsgn", choices=["hsgn", "reference"])
+    p.add_argument("--members", type=int, default=4096)
+    p.add_argument("--cells", type=int, default=4096)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def config_dict(a, world):
+    return {"workload": "cfg3_ensemble: %d members x %d cells per GPU, periodic, 200-step config"
+                        % (a.members, a.cells),
+            "members_per_gpu": a.members, "cells_per_member": a.cells,
+            "global_members": a.members * world, "lambda": "log-uniform [1e2, 1e4] per member",
+            "cfl_imex": 2.0, "mcfl": 0.5, "order": 2, "tableau": "P:371-386 (gamma = 1 - 1/sqrt2)",
+            "parallelism": f"ensemble-sharded x{world}",
+            "l2": "inputs (512 MiB state) larger than L2 (126 MB): no flush"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes per launch of the stage-2 kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get("stage2_dram_bytes_per_cell")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (test infrastructure; timed only here, never on the product path)
+# ---------------------------------------------------------------------------
+def cpu_oracle_rate(w, members, steps, threads):
+    from oracle import oracle as O
+    jobs = [(O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc), w.state(m)) for m in members]
+    t0 = time.perf_counter()
+    O.run_members(jobs, threads=threads, cfl=w.cfl, mcfl=w.mcfl, steps=steps)
+    dt = time.perf_counter() - t0
+    return 2.0 * w.n * len(members) * steps / dt, dt
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the oracle (plain fp64 C, -O2, no FMA) on the host cores,
+    each step a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    from paper_2510_07539_b200 import workloads as W
+    threads = os.cpu_count() or 1
+    sample_members = max(threads, 16)
+    w = W.cfg3(members=sample_members, n=a.cells)
+    rate_w, _ = cpu_oracle_rate(w, range(sample_members), max(1, a.warmup), threads)
+    rate, secs = cpu_oracle_rate(w, range(sample_members), a.steps, threads)
+    ms = secs / a.steps * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(a, world),
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{sample_members} cfg3 members x {a.steps} SI steps per run "
+                                       f"(each bench step = 1 SI step over {sample_members} members)"},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2510_07539_b200 import hsgn
+    from paper_2510_07539_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = W.cfg3(members=a.members, n=a.cells, first_member=rank * a.members)
+    s = hsgn.solver_for(w)
+    Ntot = w.n * w.members
+    state_bytes = 4 * 8 * Ntot
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also captures the CUDA graph)
+    s.run_steps(max(a.warmup, 3))
+    s.sync()
+    torch.cuda.synchronize()
+
+    stream = s.stream
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = s.launches
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    ms1, ms2 = s.run_steps_timed(a.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    launches = s.launches - l0
+    elapsed = ev0.elapsed_time(ev1)
+    t = torch.tensor([elapsed, ms1, ms2], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed, ms1, ms2 = [float(x) for x in t.tolist()]
+    diag = s.diagnostics()
+
+    value = 2.0 * Ntot * a.steps * world / (elapsed / 1e3)
+    peaks, peak_src = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    t2 = ms2 / a.steps / 1e3
+    t1 = ms1 / a.steps / 1e3
+    ach2 = B_STAGE2 * Ntot / t2 / 1e9
+    ach1 = B_STAGE1 * Ntot / t1 / 1e9
+    traffic = profile_traffic()
+
+    # e2e through the public API with host buffers: pinned host state uploaded,
+    # K steps each reading back the per-member dt, final state downloaded.
+    e2e = None
+    if not a.no_e2e:
+        pin = [torch.from_numpy(np.ascontiguousarray(f.reshape(-1))).pin_memory() for f in (w.h, w.q, w.K, w.W)]
+        outp = [torch.empty(Ntot, dtype=torch.float64).pin_memory() for _ in range(4)]
+        barrier()
+        torch.cuda.synchronize()
+        te0 = time.perf_counter()
+        s.set_state(*pin)
+        for _ in range(a.steps):
+            s.step(return_dt=True)
+        import ctypes as C
+        tt = np.empty(w.members)
+        s._chk(s.L.hsgn_get_state(s.ctx, *[C.c_void_p(x.data_ptr()) for x in outp], C.c_void_p(tt.ctypes.data)))
+        te = time.perf_counter() - te0
+        tt_ = torch.tensor([te], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        te = float(tt_.item())
+        e2e = {"value": 2.0 * Ntot * a.steps * world / te, "unit": UNIT,
+               "h2d_bytes_per_step": state_bytes / a.steps,
+               "d2h_bytes_per_step": 8 * w.members + state_bytes / a.steps,
+               "what": "Solver.set_state(pinned host) + K x Solver.step(return_dt) + get_state(pinned host), wall clock, max over ranks"}
+
+    cpu = None
+    if rank == 0 and not a.no_cpu:
+        threads = os.cpu_count() or 1
+        nm = max(threads, 16)
+        rate, secs = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"first {nm} cfg3 members x 10 SI steps ({secs:.1f} s)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": elapsed / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(a, world),
+        "per_gpu": value / world,
+        "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s",
+                     "frac": ach2 / peak, "traffic": traffic,
+                     "kernel": "stage_kernel<STAGE2,FINAL> (stage 2)",
+                     "bytes_model": "96 B/cell per stage-2 launch (read U^n, U1; write U^{n+1})",
+                     "peak_source": peak_src,
+                     "stage1": {"achieved": ach1, "frac": ach1 / peak, "bytes_model": "64 B/cell"},
+                     "step_avg_frac": (80.0 * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches * world,
+        "clocks": ck,
+        "diag": {"steps": diag["steps"], "mass": diag["mass"], "min_h": diag["min_h"],
+                 "t_max": diag["t_max"], "dt_last_min": diag["dt_last_min"]},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

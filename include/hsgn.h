@@ -1,0 +1,196 @@
+/*
+ * hsgn.h -- C ABI of libhsgn.so: the B200 (sm_100a) fp64 implementation of the
+ * semi-implicit IMEX Runge-Kutta step of the hyperbolised Serre-Green-Naghdi
+ * (hSGN) system of arXiv 2510.07539.
+ *
+ * Citations: "P:n" = line n of the paper text, "Ak" = reading k of
+ * the ambiguity ledger in DESIGN.md section 3.
+ *
+ * What one step computes (efficient form P:397-403):
+ *   U1      = S(U^n, U^n, a^I_11 dt)                       (stage 1)
+ *   E2      = (1 - wE) U^n + wE U1,  wE = a^E_21 / a^I_11
+ *   R2      = (1 - wR) U^n + wR U1,  wR = a^I_21 / a^I_11
+ *   U^{n+1} = S(E2, R2, a^I_22 dt)                          (stage 2)
+ * where S(E, R, tau) is the fully discrete SI stage of P:500-517: MUSCL
+ * + Rusanov convective predictor on E, coefficients
+ * beta1, beta2, beta, delta at E (A2), one tridiagonal depth solve
+ * Delta[hbar] = h^dagger (A1), and back-substitution.
+ * A 1-stage tableau gives the first-order SI step (P:500-517 literally).
+ *
+ * Data layout.  All state arrays are fp64, structure-of-arrays, member-major:
+ * field[m * n_cells + i] for member m in [0, n_members) and cell i in
+ * [0, n_cells).  The state is (h, q = h u, K, W = h w) with K = h eta on a
+ * flat bottom and K = h (eta + 3 b / 2) with bathymetry.
+ *
+ * Memory ownership.  The library never allocates device memory: the caller
+ * queries hsgn_workspace_bytes() and hands in one device allocation with
+ * hsgn_set_workspace() (the Python binding allocates it with torch).  All
+ * arrays passed to set_* / get_* are owned by the caller; they may be device
+ * or host pointers (copies use cudaMemcpyDefault, ordered on the context's
+ * stream).  The context owns nothing else but host-side bookkeeping and the
+ * CUDA graphs it captures.
+ *
+ * Errors.  Every call returns an hsgn_status.  Device-side failures (kappa <= 0,
+ * h <= h_min, non-finite values, insufficient solver overlap) are latched in a
+ * device error word; the stage kernels stop computing once it is set, the step
+ * that failed is not committed, and the next synchronising call (hsgn_step
+ * with dt_used, hsgn_advance_to, hsgn_run_steps, hsgn_get_*, hsgn_sync) returns
+ * the status.  After an error the state reads back as the last committed step.
+ *
+ * Threading.  A context is not thread-safe; use one context per thread.
+ * Asynchrony: hsgn_run_steps and hsgn_step (dt_used == NULL) only enqueue work
+ * on the context's stream; hsgn_sync() waits and reports device errors.
+ */
+#ifndef HSGN_H_
+#define HSGN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hsgn_ctx hsgn_ctx; /* opaque */
+
+typedef enum {
+    HSGN_OK = 0,
+    HSGN_E_INVALID = -1,    /* bad argument, extent, tableau or call order */
+    HSGN_E_DRY = -2,        /* hbar <= h_min after a stage        */
+    HSGN_E_COERCIVITY = -3, /* beta (= kappa) <= 0 at some cell */
+    HSGN_E_SINGULAR = -4,   /* zero pivot in the depth solve              */
+    HSGN_E_NONFINITE = -5,  /* NaN/Inf produced                           */
+    HSGN_E_CUDA = -6,       /* CUDA runtime error                         */
+    HSGN_E_OVERLAP = -7,    /* tile overlap too short for the depth solve's
+                               decay (solver); result inexact  */
+    HSGN_E_NOWORKSPACE = -8 /* workspace missing or too small             */
+} hsgn_status;
+
+typedef enum {
+    HSGN_BC_PERIODIC = 0,     /* cyclic (both sides must be periodic)           */
+    HSGN_BC_WALL = 1,         /* reflecting: h, K, W even, q odd; Neumann depth rows (A10) */
+    HSGN_BC_TRANSMISSIVE = 2  /* zero-order extrapolation; Neumann depth rows */
+} hsgn_bc;
+
+/* Double Butcher tableau.  Validated by hsgn_set_tableau:
+ * stages in {1, 2}; A_E strictly lower triangular; A_I lower triangular with
+ * positive diagonal; for 2 stages the implicit tableau must be stiffly
+ * accurate (last row == b). */
+typedef struct {
+    int32_t stages;
+    int32_t pad_;
+    double a_exp[2][2];
+    double a_imp[2][2];
+    double b[2];
+} hsgn_tableau;
+
+/* Problem description (uniform 1-D grid). */
+typedef struct {
+    int64_t n_cells;     /* cells per member, >= 4                                  */
+    int32_t n_members;   /* independent domains (ensemble), >= 1                    */
+    int32_t order;       /* 1: first-order faces, 2: MUSCL              */
+    double x_min, x_max; /* dx = (x_max - x_min) / n_cells                         */
+    int32_t bc_left;     /* hsgn_bc */
+    int32_t bc_right;    /* hsgn_bc */
+    int32_t tile_cells;  /* kept cells per CTA tile; 0 = automatic                  */
+    int32_t overlap;     /* tile overlap w (cells) for the depth solve; 0 = auto    */
+} hsgn_desc;
+
+/* Diagnostics (all members): mass = sum_i h_i dx summed over members,
+ * min_h, max_abs_u, nu_max = max(|u| + c), t_min/t_max over members,
+ * dt_last_min/max = last step's dt over members, steps = committed steps. */
+typedef struct {
+    double mass;
+    double min_h;
+    double max_abs_u;
+    double nu_max;
+    double t_min;
+    double t_max;
+    double dt_last_min;
+    double dt_last_max;
+    int64_t steps;
+    int32_t error_bits;
+    int32_t pad_;
+} hsgn_diag;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Create a context on the current CUDA device.  cuda_stream is a cudaStream_t
+ * (NULL = legacy default stream) that every later call enqueues on. */
+hsgn_status hsgn_create(const hsgn_desc *desc, void *cuda_stream, hsgn_ctx **out);
+void hsgn_destroy(hsgn_ctx *ctx);
+
+/* Bytes of device workspace the context needs (3 state buffers of
+ * 4 * n_cells * n_members doubles, bathymetry, per-member scalars). */
+size_t hsgn_workspace_bytes(const hsgn_ctx *ctx);
+/* Hand in a device allocation of at least hsgn_workspace_bytes() bytes,
+ * 256-byte aligned.  The caller keeps it alive until hsgn_destroy. */
+hsgn_status hsgn_set_workspace(hsgn_ctx *ctx, void *dev_ptr, size_t bytes);
+
+/* ---- parameters -------------------------------------- */
+
+/* g > 0; lambda[n_members] (host array) >= 0 (lambda = 0 allowed: the
+ * semi-implicit shallow-water limit); cfl_imex <= 0 disables the CFL rule,
+ * mcfl <= 0 disables the material rule; h_min >= 0. */
+hsgn_status hsgn_set_params(hsgn_ctx *ctx, double g, const double *lambda, double cfl_imex,
+                            double mcfl, double h_min);
+/* Default: the paper's tableau, gamma = 1 - 1/sqrt2, c = 1/(2 gamma). */
+hsgn_status hsgn_set_tableau(hsgn_ctx *ctx, const hsgn_tableau *tab);
+/* b[n_cells] shared by all members (host or device pointer), or NULL = flat.
+ * Bathymetric terms follow reading A9 of DESIGN.md. */
+hsgn_status hsgn_set_bathymetry(hsgn_ctx *ctx, const double *b);
+/* Optional stability filter of reading A19, applied after each
+ * step: f_i -= (sigma/16) (f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
+ * for f in {q, W}.  sigma = 0 disables it (default).  field_mask must be
+ * (1<<1)|(1<<3) (q and W) or 0. */
+hsgn_status hsgn_set_filter(hsgn_ctx *ctx, double sigma, uint32_t field_mask);
+
+/* ---- state -------------------------------------------------------------- */
+
+/* Copy in (h, q, K, W), each n_members * n_cells doubles, host or device
+ * pointers; t0 is the start time of every member.  Also (re)computes the
+ * max|u| and max(|u|+c) the first step's dt needs, and clears errors. */
+hsgn_status hsgn_set_state(hsgn_ctx *ctx, const double *h, const double *q, const double *K,
+                           const double *W, double t0);
+/* Copy out the last committed state; any pointer may be NULL.  t (host array
+ * of n_members, or NULL) receives each member's time.  Synchronises. */
+hsgn_status hsgn_get_state(hsgn_ctx *ctx, double *h, double *q, double *K, double *W,
+                           double *t);
+
+/* ---- stepping ------------------------------------------------------------ */
+
+/* One SI-IMEX step.  dt > 0: fixed step for every member; dt <= 0: the
+ * two-condition rule of P:613-617 per member.  If dt_used (host, n_members)
+ * is non-NULL the call synchronises and reports the dt each member took. */
+hsgn_status hsgn_step(hsgn_ctx *ctx, double dt, double *dt_used);
+/* Enqueue n_steps automatic-dt steps (CUDA-graph replay); asynchronous. */
+hsgn_status hsgn_run_steps(hsgn_ctx *ctx, int64_t n_steps);
+/* Advance every member to t_end (last step clipped), at most max_steps
+ * steps; polls the device every `poll` steps.  *steps_done = steps taken. */
+hsgn_status hsgn_advance_to(hsgn_ctx *ctx, double t_end, int64_t max_steps,
+                            int64_t *steps_done);
+/* Enqueue n_steps automatic-dt steps EAGERLY with a CUDA event recorded
+ * between consecutive kernels on the context's stream, synchronise, and
+ * return in stage_ms[0] / stage_ms[1] the summed device time (ms) of the
+ * stage-1 / stage-2 kernels (stage_ms[1] = 0 for a 1-stage tableau).  Same
+ * arithmetic as hsgn_run_steps; used by bench.py for per-kernel rooflines. */
+hsgn_status hsgn_run_steps_timed(hsgn_ctx *ctx, int64_t n_steps, double *stage_ms);
+/* Wait for the stream; return the latched device status. */
+hsgn_status hsgn_sync(hsgn_ctx *ctx);
+
+/* ---- diagnostics ----------------------------------------------------------- */
+hsgn_status hsgn_get_diagnostics(hsgn_ctx *ctx, hsgn_diag *out);
+/* Number of kernel launches enqueued by this context since creation. */
+int64_t hsgn_launch_count(const hsgn_ctx *ctx);
+/* Tile geometry chosen by hsgn_create: kept cells per tile, overlap, tiles per
+ * member, threads per CTA, max rows per CTA. */
+hsgn_status hsgn_get_geometry(const hsgn_ctx *ctx, int32_t *tile_cells, int32_t *overlap,
+                              int32_t *tiles_per_member, int32_t *threads, int32_t *max_rows);
+
+const char *hsgn_status_string(hsgn_status s);
+const char *hsgn_last_error(const hsgn_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSGN_H_ */

@@ -573,12 +573,13 @@ int orc_run(const orc_problem *P, const orc_tableau *T, double cfl, double mcfl,
             st = orc_dt(P, cfl, mcfl, h, q, K, &dt, NULL, NULL);
             if (st != ORC_OK) break;
         }
-        if (use_tend && t + dt > t_end) dt = t_end - t;
+        /* last step clipped to land exactly on t_end */
+        if (use_tend && t + dt >= t_end) dt = t_end - t;
         double m;
         st = orc_step(P, T, dt, h, q, K, W, &m);
         if (m < mb) mb = m;
         if (st != ORC_OK) break;
-        t += dt;
+        t = (use_tend && dt == t_end - t) ? t_end : t + dt;
         s++;
     }
     if (t_out) *t_out = t;

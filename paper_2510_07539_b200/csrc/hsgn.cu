@@ -1,0 +1,649 @@
+// hsgn.cu -- C ABI runtime of libhsgn.so (see include/hsgn.h).
+//
+// Host side: validates the problem, chooses the tile geometry, lays out the
+// caller-provided workspace, launches the stage kernels of
+// hsgn_kernels.cuh on the caller's stream, and replays CUDA graphs of
+// GRAPH_STEPS steps for hsgn_run_steps / hsgn_advance_to.  Never allocates
+// device memory and never falls back to the CPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hsgn.h"
+#include "hsgn_kernels.cuh"
+
+using namespace hsgn;
+
+namespace {
+
+constexpr int GRAPH_STEPS = 16;   // steps per captured graph (even: buffers ping-pong)
+constexpr int POLL_STEPS = 256;   // advance_to polls the device every POLL_STEPS
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct hsgn_ctx {
+    hsgn_desc desc{};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    // geometry
+    int n = 0, members = 0, T = 0, w = 0, tiles = 0;
+    double dx = 0;
+    // parameters
+    double g = 9.81, cfl = 2.0, mcfl = 0.5, h_min = 1e-8;
+    std::vector<double> lam;
+    bool have_params = false, have_state = false, bathy = false;
+    hsgn_tableau tab{};
+    double aI1 = 0, aI2 = 0, wE = 0, wR = 0;
+    double filter_sigma = 0;
+    // workspace
+    char *ws = nullptr;
+    size_t ws_bytes = 0;
+    double *buf[3][4] = {};     // [A, B, U1][field]
+    double *b = nullptr, *lamd = nullptr, *t = nullptr, *dt = nullptr, *partials = nullptr;
+    unsigned long long *maxes = nullptr, *rho_obs = nullptr;
+    unsigned int *err = nullptr, *done = nullptr;
+    long long *steps = nullptr;
+    Ctrl *ctrl = nullptr;
+    // host bookkeeping
+    int cur = 0;                  // buffer index holding the state at device step `base_steps`
+    long long host_steps = 0;     // steps enqueued since set_state
+    Ctrl ctrl_host{0.0, 0.0};
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    long long launches = 0;
+    std::string last_error;
+};
+
+namespace {
+
+hsgn_status fail(hsgn_ctx *c, hsgn_status s, const std::string &msg)
+{
+    if (c) c->last_error = msg;
+    return s;
+}
+
+#define CUDA_TRY(c, expr)                                                              \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return fail((c), HSGN_E_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+hsgn_status status_from_bits(unsigned int bits)
+{
+    if (!bits) return HSGN_OK;
+    if (bits & ERR_COERC) return HSGN_E_COERCIVITY;
+    if (bits & ERR_DRY) return HSGN_E_DRY;
+    if (bits & ERR_NONFINITE) return HSGN_E_NONFINITE;
+    if (bits & ERR_OVERLAP) return HSGN_E_OVERLAP;
+    if (bits & ERR_DT) return HSGN_E_INVALID;
+    return HSGN_E_INVALID;
+}
+
+Params make_params(hsgn_ctx *c)
+{
+    Params P{};
+    P.n = c->n; P.members = c->members; P.tiles = c->tiles; P.T = c->T; P.w = c->w;
+    P.bcl = c->desc.bc_left; P.bcr = c->desc.bc_right; P.order = c->desc.order;
+    P.dx = c->dx; P.g = c->g; P.h_min = c->h_min; P.cfl = c->cfl; P.mcfl = c->mcfl;
+    P.aI1 = c->aI1; P.aI2 = c->aI2; P.wE = c->wE; P.wR = c->wR;
+    P.filter_sigma = c->filter_sigma;
+    P.b = c->bathy ? c->b : nullptr;
+    P.lam = c->lamd; P.t = c->t; P.dt = c->dt; P.maxes = c->maxes; P.err = c->err;
+    P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.ctrl = c->ctrl;
+    return P;
+}
+
+template <bool S2, bool FIN, bool BATHY>
+hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
+{
+    dim3 grid(c->tiles, c->members);
+    stage_kernel<S2, FIN, BATHY><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return HSGN_OK;
+}
+
+template <bool S2, bool FIN>
+hsgn_status launch_stage_b(hsgn_ctx *c, const Params &P, const Bufs &B)
+{
+    return c->bathy ? launch_stage<S2, FIN, true>(c, P, B) : launch_stage<S2, FIN, false>(c, P, B);
+}
+
+// enqueue one step reading buf[cur], writing buf[cur ^ 1]
+hsgn_status enqueue_step(hsgn_ctx *c, int cur)
+{
+    const Params P = make_params(c);
+    Bufs B{};
+    for (int k = 0; k < 4; k++) {
+        B.Un[k] = c->buf[cur][k];
+        B.U1[k] = c->buf[2][k];
+    }
+    hsgn_status st;
+    if (c->tab.stages == 1) {
+        for (int k = 0; k < 4; k++) B.out[k] = c->buf[cur ^ 1][k];
+        st = launch_stage_b<false, true>(c, P, B);
+    } else {
+        for (int k = 0; k < 4; k++) B.out[k] = c->buf[2][k];
+        st = launch_stage_b<false, false>(c, P, B);
+        if (st != HSGN_OK) return st;
+        for (int k = 0; k < 4; k++) B.out[k] = c->buf[cur ^ 1][k];
+        st = launch_stage_b<true, true>(c, P, B);
+    }
+    return st;
+}
+
+void drop_graphs(hsgn_ctx *c)
+{
+    for (auto &gx : c->graph)
+        if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
+}
+
+hsgn_status set_ctrl(hsgn_ctx *c, double t_end, double dt_fixed)
+{
+    if (c->ctrl_host.t_end == t_end && c->ctrl_host.dt_fixed == dt_fixed) return HSGN_OK;
+    c->ctrl_host.t_end = t_end;
+    c->ctrl_host.dt_fixed = dt_fixed;
+    // ctrl_host is read by the copy after this call returns only if the
+    // stream is idle; copy from a stable per-context staging location
+    CUDA_TRY(c, cudaMemcpyAsync(c->ctrl, &c->ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status ready(hsgn_ctx *c)
+{
+    if (!c) return HSGN_E_INVALID;
+    if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
+    if (!c->have_params) return fail(c, HSGN_E_INVALID, "hsgn_set_params not called");
+    if (!c->have_state) return fail(c, HSGN_E_INVALID, "hsgn_set_state not called");
+    return HSGN_OK;
+}
+
+hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
+{
+    long long done = 0;
+    while (done < n_steps) {
+        if (n_steps - done >= GRAPH_STEPS) {
+            cudaGraphExec_t &gx = c->graph[c->cur];
+            if (!gx) {
+                cudaGraph_t gr;
+                CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+                long long l0 = c->launches;
+                int cc = c->cur;
+                hsgn_status st = HSGN_OK;
+                for (int k = 0; k < GRAPH_STEPS && st == HSGN_OK; k++) {
+                    st = enqueue_step(c, cc);
+                    cc ^= 1;
+                }
+                cudaError_t ce = cudaStreamEndCapture(c->stream, &gr);
+                if (st != HSGN_OK) return st;
+                if (ce != cudaSuccess) return fail(c, HSGN_E_CUDA, cudaGetErrorString(ce));
+                c->launches = l0;   // counted at replay
+                CUDA_TRY(c, cudaGraphInstantiate(&gx, gr, 0));
+                cudaGraphDestroy(gr);
+            }
+            CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
+            c->launches += GRAPH_STEPS * c->tab.stages;
+            done += GRAPH_STEPS;   // GRAPH_STEPS even: cur unchanged
+        } else {
+            hsgn_status st = enqueue_step(c, c->cur);
+            if (st != HSGN_OK) return st;
+            c->cur ^= 1;
+            done++;
+        }
+    }
+    c->host_steps += n_steps;
+    return HSGN_OK;
+}
+
+// After a sync: reconcile host buffer parity with the device's committed steps.
+hsgn_status reconcile(hsgn_ctx *c, unsigned int *bits_out = nullptr)
+{
+    unsigned int bits = 0;
+    long long dsteps = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&bits, c->err, sizeof(bits), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&dsteps, c->steps, sizeof(dsteps), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (bits_out) *bits_out = bits;
+    if (dsteps != c->host_steps) {
+        // steps after the failing one did nothing: the committed state is in
+        // the buffer reached after dsteps ping-pongs
+        const long long extra = c->host_steps - dsteps;
+        if (extra & 1) c->cur ^= 1;
+        c->host_steps = dsteps;
+    }
+    hsgn_status st = status_from_bits(bits);
+    if (st != HSGN_OK) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "device error bits 0x%x after %lld committed steps", bits, dsteps);
+        c->last_error = msg;
+    }
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *hsgn_status_string(hsgn_status s)
+{
+    switch (s) {
+    case HSGN_OK: return "ok";
+    case HSGN_E_INVALID: return "invalid argument or call order";
+    case HSGN_E_DRY: return "dry bed: hbar <= h_min";
+    case HSGN_E_COERCIVITY: return "coercivity violated: beta (kappa) <= 0";
+    case HSGN_E_SINGULAR: return "singular pivot in the depth solve";
+    case HSGN_E_NONFINITE: return "non-finite value";
+    case HSGN_E_CUDA: return "CUDA error";
+    case HSGN_E_OVERLAP: return "tile overlap too short for the depth-solve decay";
+    case HSGN_E_NOWORKSPACE: return "workspace missing or too small";
+    }
+    return "unknown status";
+}
+
+const char *hsgn_last_error(const hsgn_ctx *c) { return c ? c->last_error.c_str() : "null context"; }
+
+hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
+{
+    if (!d || !out) return HSGN_E_INVALID;
+    *out = nullptr;
+    if (d->n_cells < 4 || d->n_cells > (int64_t(1) << 31) - 1 || d->n_members < 1 ||
+        d->n_members > 65535 || !(d->x_max > d->x_min) || (d->order != 1 && d->order != 2))
+        return HSGN_E_INVALID;
+    if (d->bc_left < 0 || d->bc_left > 2 || d->bc_right < 0 || d->bc_right > 2) return HSGN_E_INVALID;
+    if ((d->bc_left == HSGN_BC_PERIODIC) != (d->bc_right == HSGN_BC_PERIODIC)) return HSGN_E_INVALID;
+    hsgn_ctx *c = new hsgn_ctx();
+    c->desc = *d;
+    c->stream = (cudaStream_t)stream;
+    cudaGetDevice(&c->device);
+    c->n = int(d->n_cells);
+    c->members = d->n_members;
+    c->dx = (d->x_max - d->x_min) / double(d->n_cells);
+    // overlap: enough for rho up to ~2.2 (CFL_IMEX ~ 3.5) by default; checked per tile
+    int w = d->overlap > 0 ? d->overlap : 64;
+    w = std::max(w, 3);
+    const int maxT = LCAP - 2 - 2 * w;
+    if (maxT < 16) { delete c; return HSGN_E_INVALID; }
+    int T;
+    if (d->tile_cells > 0) T = std::min<int>(d->tile_cells, maxT);
+    else {
+        const int ntiles = (c->n + maxT - 1) / maxT;
+        T = (c->n + ntiles - 1) / ntiles;
+        if (ntiles > 1) T = ((T + 31) / 32) * 32;       // aligned tiles when split
+        T = std::min(T, maxT);
+    }
+    c->T = T;
+    c->w = w;
+    c->tiles = (c->n + T - 1) / T;
+    c->lam.assign(c->members, 0.0);
+    // default tableau
+    const double gm = 1.0 - 1.0 / std::sqrt(2.0), cc = 1.0 / (2.0 * gm);
+    hsgn_tableau tb{};
+    tb.stages = 2;
+    tb.a_exp[1][0] = cc;
+    tb.a_imp[0][0] = gm; tb.a_imp[1][0] = 1.0 - gm; tb.a_imp[1][1] = gm;
+    tb.b[0] = 1.0 - gm; tb.b[1] = gm;
+    c->tab = tb;
+    c->aI1 = gm; c->aI2 = gm; c->wE = cc / gm; c->wR = (1.0 - gm) / gm;
+    // kernels need > 48 KiB dynamic smem
+    cudaFuncSetAttribute(stage_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        delete c;
+        return HSGN_E_CUDA;
+    }
+    *out = c;
+    return HSGN_OK;
+}
+
+void hsgn_destroy(hsgn_ctx *c)
+{
+    if (!c) return;
+    drop_graphs(c);
+    delete c;
+}
+
+size_t hsgn_workspace_bytes(const hsgn_ctx *c)
+{
+    if (!c) return 0;
+    const size_t N = size_t(c->n) * c->members;
+    size_t s = 0;
+    s += 12 * align256(N * sizeof(double));                 // 3 buffers x 4 fields
+    s += align256(size_t(c->n) * sizeof(double));           // b
+    s += 3 * align256(size_t(c->members) * sizeof(double)); // lam, t, dt
+    s += align256(4 * size_t(c->members) * 8);              // maxes
+    s += align256(size_t(c->members) * c->tiles * 4 * sizeof(double));  // partials
+    s += 256;                                               // scalars
+    s += 256;                                               // ctrl
+    return s;
+}
+
+hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
+{
+    if (!c || !p) return HSGN_E_INVALID;
+    if (bytes < hsgn_workspace_bytes(c)) return fail(c, HSGN_E_NOWORKSPACE, "workspace too small");
+    if ((uintptr_t)p & 255) return fail(c, HSGN_E_INVALID, "workspace must be 256-byte aligned");
+    drop_graphs(c);
+    c->ws = (char *)p;
+    c->ws_bytes = bytes;
+    const size_t N = size_t(c->n) * c->members;
+    char *q = c->ws;
+    for (int bi = 0; bi < 3; bi++)
+        for (int k = 0; k < 4; k++) { c->buf[bi][k] = (double *)q; q += align256(N * sizeof(double)); }
+    c->b = (double *)q; q += align256(size_t(c->n) * sizeof(double));
+    c->lamd = (double *)q; q += align256(size_t(c->members) * sizeof(double));
+    c->t = (double *)q; q += align256(size_t(c->members) * sizeof(double));
+    c->dt = (double *)q; q += align256(size_t(c->members) * sizeof(double));
+    c->maxes = (unsigned long long *)q; q += align256(4 * size_t(c->members) * 8);
+    c->partials = (double *)q; q += align256(size_t(c->members) * c->tiles * 4 * sizeof(double));
+    c->err = (unsigned int *)q;
+    c->done = (unsigned int *)(q + 4);
+    c->steps = (long long *)(q + 8);
+    c->rho_obs = (unsigned long long *)(q + 16);
+    q += 256;
+    c->ctrl = (Ctrl *)q;
+    CUDA_TRY(c, cudaMemsetAsync(c->ws + (size_t)((char *)c->err - c->ws), 0, 512, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->b, 0, size_t(c->n) * sizeof(double), c->stream));
+    c->ctrl_host = Ctrl{0.0, 0.0};
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->have_params) {
+        CUDA_TRY(c, cudaMemcpy(c->lamd, c->lam.data(), c->members * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    c->have_state = false;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_params(hsgn_ctx *c, double g, const double *lambda, double cfl, double mcfl,
+                            double h_min)
+{
+    if (!c || !lambda) return HSGN_E_INVALID;
+    if (!(g > 0.0) || !(h_min >= 0.0)) return fail(c, HSGN_E_INVALID, "g must be > 0, h_min >= 0");
+    for (int m = 0; m < c->members; m++)
+        if (!(lambda[m] >= 0.0) || !std::isfinite(lambda[m]))
+            return fail(c, HSGN_E_INVALID, "lambda must be finite and >= 0");
+    c->g = g;
+    c->cfl = cfl;
+    c->mcfl = mcfl;
+    c->h_min = h_min;
+    c->lam.assign(lambda, lambda + c->members);
+    c->have_params = true;
+    drop_graphs(c);
+    if (c->ws) {
+        CUDA_TRY(c, cudaMemcpyAsync(c->lamd, c->lam.data(), c->members * sizeof(double),
+                                    cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_tableau(hsgn_ctx *c, const hsgn_tableau *t)
+{
+    if (!c || !t) return HSGN_E_INVALID;
+    if (t->stages == 1) {
+        if (!(t->a_imp[0][0] > 0.0)) return fail(c, HSGN_E_INVALID, "a_11 must be > 0");
+        c->aI1 = t->a_imp[0][0]; c->aI2 = 0; c->wE = 0; c->wR = 0;
+    } else if (t->stages == 2) {
+        if (!(t->a_imp[0][0] > 0.0) || !(t->a_imp[1][1] > 0.0) || t->a_exp[0][0] != 0.0 ||
+            t->a_exp[0][1] != 0.0 || t->a_exp[1][1] != 0.0 || t->a_imp[0][1] != 0.0)
+            return fail(c, HSGN_E_INVALID, "tableau shape");
+        if (t->a_imp[1][0] != t->b[0] || t->a_imp[1][1] != t->b[1])
+            return fail(c, HSGN_E_INVALID, "implicit tableau must be stiffly accurate (P:368)");
+        c->aI1 = t->a_imp[0][0]; c->aI2 = t->a_imp[1][1];
+        c->wE = t->a_exp[1][0] / t->a_imp[0][0];
+        c->wR = t->a_imp[1][0] / t->a_imp[0][0];
+    } else {
+        return fail(c, HSGN_E_INVALID, "stages must be 1 or 2");
+    }
+    c->tab = *t;
+    drop_graphs(c);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_bathymetry(hsgn_ctx *c, const double *b)
+{
+    if (!c) return HSGN_E_INVALID;
+    if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
+    drop_graphs(c);
+    if (!b) {
+        c->bathy = false;
+        CUDA_TRY(c, cudaMemsetAsync(c->b, 0, size_t(c->n) * sizeof(double), c->stream));
+    } else {
+        c->bathy = true;
+        CUDA_TRY(c, cudaMemcpyAsync(c->b, b, size_t(c->n) * sizeof(double), cudaMemcpyDefault, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_filter(hsgn_ctx *c, double sigma, uint32_t mask)
+{
+    if (!c || !(sigma >= 0.0)) return HSGN_E_INVALID;
+    if (sigma > 0.0 && mask != ((1u << 1) | (1u << 3)))
+        return fail(c, HSGN_E_INVALID, "filter mask must be q|W (0xA)");
+    c->filter_sigma = sigma;
+    drop_graphs(c);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_state(hsgn_ctx *c, const double *h, const double *q, const double *K,
+                           const double *W, double t0)
+{
+    if (!c || !h || !q || !K || !W) return HSGN_E_INVALID;
+    if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
+    if (!c->have_params) return fail(c, HSGN_E_INVALID, "hsgn_set_params first");
+    const size_t N = size_t(c->n) * c->members;
+    const double *src[4] = {h, q, K, W};
+    c->cur = 0;
+    for (int k = 0; k < 4; k++)
+        CUDA_TRY(c, cudaMemcpyAsync(c->buf[0][k], src[k], N * sizeof(double), cudaMemcpyDefault, c->stream));
+    std::vector<double> tv(c->members, t0);
+    CUDA_TRY(c, cudaMemcpyAsync(c->t, tv.data(), c->members * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->dt, 0, c->members * sizeof(double), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->maxes, 0, 4 * size_t(c->members) * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->err, 0, 32, c->stream));   // err, done, steps, rho_obs
+    dim3 grid(c->tiles, c->members);
+    reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[0][0], c->buf[0][1], c->buf[0][2],
+                                              c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
+                                              c->partials, c->maxes, c->members);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // tv must outlive the copy
+    c->host_steps = 0;
+    c->have_state = true;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_get_state(hsgn_ctx *c, double *h, double *q, double *K, double *W, double *t)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    st = reconcile(c);
+    const size_t N = size_t(c->n) * c->members;
+    double *dst[4] = {h, q, K, W};
+    for (int k = 0; k < 4; k++)
+        if (dst[k])
+            CUDA_TRY(c, cudaMemcpyAsync(dst[k], c->buf[c->cur][k], N * sizeof(double), cudaMemcpyDefault, c->stream));
+    if (t) CUDA_TRY(c, cudaMemcpyAsync(t, c->t, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return st;
+}
+
+hsgn_status hsgn_step(hsgn_ctx *c, double dt, double *dt_used)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    st = set_ctrl(c, c->ctrl_host.t_end, dt > 0.0 ? dt : 0.0);
+    if (st != HSGN_OK) return st;
+    st = enqueue_step(c, c->cur);
+    if (st != HSGN_OK) return st;
+    c->cur ^= 1;
+    c->host_steps++;
+    if (dt_used) {
+        st = reconcile(c);
+        CUDA_TRY(c, cudaMemcpy(dt_used, c->dt, c->members * sizeof(double), cudaMemcpyDeviceToHost));
+        return st;
+    }
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_run_steps(hsgn_ctx *c, int64_t n_steps)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (n_steps < 0) return HSGN_E_INVALID;
+    st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
+    if (st != HSGN_OK) return st;
+    return run_steps_impl(c, n_steps);
+}
+
+hsgn_status hsgn_run_steps_timed(hsgn_ctx *c, int64_t n_steps, double *stage_ms)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (n_steps < 0 || !stage_ms) return HSGN_E_INVALID;
+    st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
+    if (st != HSGN_OK) return st;
+    const int per = c->tab.stages;
+    std::vector<cudaEvent_t> ev(size_t(n_steps) * per + 1);
+    for (auto &e : ev) CUDA_TRY(c, cudaEventCreate(&e));
+    CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
+    const Params P = make_params(c);
+    for (int64_t k = 0; k < n_steps && st == HSGN_OK; k++) {
+        Bufs B{};
+        for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; }
+        if (per == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
+            st = launch_stage_b<false, true>(c, P, B);
+            if (st == HSGN_OK) CUDA_TRY(c, cudaEventRecord(ev[k + 1], c->stream));
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            st = launch_stage_b<false, false>(c, P, B);
+            if (st != HSGN_OK) break;
+            CUDA_TRY(c, cudaEventRecord(ev[2 * k + 1], c->stream));
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
+            st = launch_stage_b<true, true>(c, P, B);
+            if (st == HSGN_OK) CUDA_TRY(c, cudaEventRecord(ev[2 * k + 2], c->stream));
+        }
+        c->cur ^= 1;
+        c->host_steps++;
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    stage_ms[0] = stage_ms[1] = 0.0;
+    if (st == HSGN_OK) {
+        for (size_t i = 1; i < ev.size(); i++) {
+            float ms = 0.f;
+            CUDA_TRY(c, cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+            stage_ms[(i - 1) % per] += ms;
+        }
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    if (st != HSGN_OK) return st;
+    return reconcile(c);
+}
+
+hsgn_status hsgn_sync(hsgn_ctx *c)
+{
+    if (!c) return HSGN_E_INVALID;
+    return reconcile(c);
+}
+
+hsgn_status hsgn_advance_to(hsgn_ctx *c, double t_end, int64_t max_steps, int64_t *steps_done)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (!(t_end > 0.0)) return fail(c, HSGN_E_INVALID, "t_end must be > 0");
+    st = set_ctrl(c, t_end, 0.0);
+    if (st != HSGN_OK) return st;
+    std::vector<double> tv(c->members);
+    long long taken = 0;
+    const long long s0 = c->host_steps;
+    while (taken < max_steps) {
+        CUDA_TRY(c, cudaMemcpyAsync(tv.data(), c->t, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        st = reconcile(c);
+        if (st != HSGN_OK) break;
+        bool all = true;
+        for (double tm : tv) all &= !(tm < t_end);
+        if (all) break;
+        const long long chunk = std::min<long long>(POLL_STEPS, max_steps - taken);
+        st = run_steps_impl(c, chunk);
+        if (st != HSGN_OK) break;
+        taken += chunk;
+    }
+    if (st == HSGN_OK) st = reconcile(c);
+    // steps that actually advanced some member are not distinguishable from
+    // carried no-op steps here; report committed device steps since entry
+    if (steps_done) *steps_done = c->host_steps - s0;
+    set_ctrl(c, 0.0, 0.0);
+    return st;
+}
+
+hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (!o) return HSGN_E_INVALID;
+    unsigned int bits = 0;
+    st = reconcile(c, &bits);
+    dim3 grid(c->tiles, c->members);
+    reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[c->cur][0], c->buf[c->cur][1], c->buf[c->cur][2],
+                                              c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
+                                              c->partials, nullptr, c->members);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    std::vector<double> part(size_t(c->members) * c->tiles * 4), tv(c->members), dv(c->members);
+    long long dsteps = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(part.data(), c->partials, part.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(tv.data(), c->t, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(dv.data(), c->dt, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&dsteps, c->steps, sizeof(dsteps), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    hsgn_diag d{};
+    d.min_h = 1e300;
+    d.t_min = 1e300; d.t_max = -1e300; d.dt_last_min = 1e300; d.dt_last_max = -1e300;
+    for (int m = 0; m < c->members; m++) {
+        double mass = 0.0;
+        for (int j = 0; j < c->tiles; j++) {
+            const double *p = &part[(size_t(m) * c->tiles + j) * 4];
+            mass += p[0];
+            d.min_h = std::min(d.min_h, p[1]);
+            d.max_abs_u = std::max(d.max_abs_u, p[2]);
+            d.nu_max = std::max(d.nu_max, p[3]);
+        }
+        d.mass += mass * c->dx;
+        d.t_min = std::min(d.t_min, tv[m]); d.t_max = std::max(d.t_max, tv[m]);
+        d.dt_last_min = std::min(d.dt_last_min, dv[m]); d.dt_last_max = std::max(d.dt_last_max, dv[m]);
+    }
+    d.steps = dsteps;
+    d.error_bits = int32_t(bits);
+    *o = d;
+    return st;
+}
+
+int64_t hsgn_launch_count(const hsgn_ctx *c) { return c ? c->launches : 0; }
+
+hsgn_status hsgn_get_geometry(const hsgn_ctx *c, int32_t *T, int32_t *w, int32_t *tiles,
+                              int32_t *threads, int32_t *max_rows)
+{
+    if (!c) return HSGN_E_INVALID;
+    if (T) *T = c->T;
+    if (w) *w = c->w;
+    if (tiles) *tiles = c->tiles;
+    if (threads) *threads = NT;
+    if (max_rows) *max_rows = LCAP;
+    return HSGN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,645 @@
+// hsgn_kernels.cuh -- sm_100a fp64 kernels of the SI-IMEX hSGN step.
+//
+// One kernel launch = one IMEX stage S(E, R, tau) over every tile of
+// every ensemble member.  Citations: P:n = PAPER.md line n, Ak = DESIGN.md
+// reading k.  Nothing here is shared with oracle/ (no code, no constants).
+//
+// CTA work unit: a TILE of Tk kept cells of one member, extended by an overlap
+// of w cells on each side (clipped at physical walls).  The depth system of
+// P:509-512 couples the whole domain, but it is a diagonally dominant M-matrix
+// whose inverse decays like r^k per cell (r from rho_max),
+// so solving the extended tile with Neumann-truncated ends gives the kept rows
+// exactly to round-off whenever r^w <= 2^-60; every CTA checks that with its
+// own rho_max and latches HSGN_E_OVERLAP otherwise.  Periodic domains wrap.
+//
+// Phases inside the CTA (NT threads, rows of the extended tile in shared memory):
+//   load   : coalesced global -> smem: E (h, q, H, W) on rows -3..L+2, R on
+//            rows -1..L (stage 2 forms E and R from U^n and U1)
+//   phase 1: per-thread CHUNKS of MCH rows, sliding register window:
+//            MUSCL + Rusanov faces, predictor q^dag, H^dag, W^dag
+//            (A9), coefficients beta, delta
+//   phase 2: per-thread chunk assembly of Delta[h] = h^dag (A1),
+//            partition method (downward + upward sweeps in registers), reduced
+//            system of NT unknowns by PCR in smem, chunk recovery -> hbar
+//   phase 3: back-substitution, optional A19 filter, coalesced
+//            stores; final stage: per-member max|u|, max(|u|+c) for the next
+//            dt and the step commit by the last CTA.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hsgn {
+
+constexpr int NT = 256;             // threads per CTA
+constexpr int MCH = 5;              // rows per thread chunk (odd: conflict-free strided smem)
+constexpr int LCAP = NT * MCH;      // 1280 rows per CTA incl. phase-1 halo rows
+constexpr int SROWS = LCAP + 6;     // smem row capacity per array
+constexpr int NARR = 10;            // smem arrays
+constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
+
+enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2 };
+enum { ERR_COERC = 1u, ERR_DRY = 2u, ERR_NONFINITE = 4u, ERR_OVERLAP = 8u, ERR_DT = 16u };
+
+struct Ctrl {            // device-resident run control (read by stage kernels)
+    double t_end;        // <= 0: no clipping
+    double dt_fixed;     // > 0: fixed step
+};
+
+struct Params {
+    int n, members, tiles, T, w;
+    int bcl, bcr, order;
+    double dx, g, h_min;
+    double cfl, mcfl;
+    double aI1, aI2, wE, wR;
+    double filter_sigma;
+    const double *b;                 // [n] or nullptr
+    const double *lam;               // [members]
+    double *t;                       // [members]
+    double *dt;                      // [members]
+    unsigned long long *maxes;       // [2 slots][2 kinds][members] (double bits)
+    unsigned int *err;
+    long long *steps;
+    unsigned int *done;
+    unsigned long long *rho_obs;     // max rho over tiles (double bits)
+    const Ctrl *ctrl;
+};
+
+struct Bufs {
+    const double *Un[4];
+    const double *U1[4];
+    double *out[4];
+};
+
+__device__ __forceinline__ int map_cell(int c, int n, int bcl, int bcr, double &par)
+{
+    par = 1.0;
+    if (c < 0) {
+        if (bcl == BC_PERIODIC) { c %= n; if (c < 0) c += n; }
+        else if (bcl == BC_WALL) { c = -1 - c; par = -1.0; }
+        else c = 0;
+    } else if (c >= n) {
+        if (bcr == BC_PERIODIC) c %= n;
+        else if (bcr == BC_WALL) { c = 2 * n - 1 - c; par = -1.0; }
+        else c = n - 1;
+    }
+    return c;
+}
+
+__device__ __forceinline__ double bathy_at(const double *__restrict__ b, int c, int n, int bcl,
+                                           int bcr)
+{
+    double par;
+    int cc = map_cell(c, n, bcl, bcr, par);
+    return __ldg(b + cc);
+}
+
+// dt rule of P:613-617 (reading A7 for nu_max): dt_bar = CFL dx / nu_max; if
+// u_max dt_bar / dx > MCFL use MCFL dx / u_max.  Returns < 0 if undefined.
+__device__ __forceinline__ double dt_rule(double cfl, double mcfl, double dx, double umax,
+                                          double numax)
+{
+    double d;
+    if (cfl > 0.0) {
+        d = cfl * dx / numax;
+        if (mcfl > 0.0 && umax > 0.0 && umax * d / dx > mcfl) d = mcfl * dx / umax;
+    } else if (mcfl > 0.0 && umax > 0.0) {
+        d = mcfl * dx / umax;
+    } else {
+        d = -1.0;
+    }
+    return d;
+}
+
+// Rusanov face flux (A4) from the 4-row window v0..v3 = rows f-1..f+2
+// for the face f+1/2, with MUSCL (A5) when order == 2.
+struct Face { double q, H, W; };
+
+__device__ __forceinline__ Face face_flux(const double (&wh)[4], const double (&wq)[4],
+                                          const double (&wH)[4], const double (&wW)[4],
+                                          int order)
+{
+    double hm, hp, qm, qp, Hm, Hp, Wm, Wp;
+    if (order == 2) {
+        hm = wh[1] + 0.25 * (wh[2] - wh[0]);  hp = wh[2] - 0.25 * (wh[3] - wh[1]);
+        qm = wq[1] + 0.25 * (wq[2] - wq[0]);  qp = wq[2] - 0.25 * (wq[3] - wq[1]);
+        Hm = wH[1] + 0.25 * (wH[2] - wH[0]);  Hp = wH[2] - 0.25 * (wH[3] - wH[1]);
+        Wm = wW[1] + 0.25 * (wW[2] - wW[0]);  Wp = wW[2] - 0.25 * (wW[3] - wW[1]);
+    } else {
+        hm = wh[1]; hp = wh[2]; qm = wq[1]; qp = wq[2];
+        Hm = wH[1]; Hp = wH[2]; Wm = wW[1]; Wp = wW[2];
+    }
+    const double um = qm / hm, up = qp / hp;
+    const double a = fmax(fabs(um), fabs(up));
+    Face F;
+    F.q = 0.5 * (qm * um + qp * up) - 0.5 * a * (qp - qm);
+    F.H = 0.5 * (Hm * um + Hp * up) - 0.5 * a * (Hp - Hm);
+    F.W = 0.5 * (Wm * um + Wp * up) - 0.5 * a * (Wp - Wm);
+    return F;
+}
+
+__device__ __forceinline__ double warp_max(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double block_max(double v, double *red)
+{
+    v = warp_max(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        v = (lane < NT / 32) ? red[lane] : 0.0;
+        v = warp_max(v);
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    v = red[0];
+    __syncthreads();
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// The stage kernel.  STAGE2: inputs are U^n and U1 (E, R formed on load);
+// FINAL: this stage produces U^{n+1} (filter, dt maxima, commit).
+// ---------------------------------------------------------------------------
+template <bool STAGE2, bool FINAL, bool BATHY>
+__global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs B)
+{
+    extern __shared__ double smem[];
+    __shared__ double red[NT / 32 + 1];
+    __shared__ double xch[NT / 32][3];
+    __shared__ int s_last;
+
+    if (*((volatile unsigned int *)P.err)) return;
+
+    const int tid = threadIdx.x;
+    const int j = blockIdx.x;        // tile
+    const int m = blockIdx.y;        // member
+    const int n = P.n;
+    const size_t mo = size_t(m) * n;
+
+    // ---- tile geometry ------------------------------------------------------
+    const bool periodic = (P.bcl == BC_PERIODIC);
+    const int s = j * P.T;
+    const int e = min(n, s + P.T);
+    const int Tk = e - s;
+    const int wl = periodic ? P.w : min(P.w, s);
+    const int wr = periodic ? P.w : min(P.w, n - e);
+    const int start = s - wl;
+    const int L = Tk + wl + wr;
+    const bool left_phys = !periodic && (start == 0);
+    const bool right_phys = !periodic && (start + L == n);
+
+    // ---- dt -------------------------------------------------------
+    const long long stepno = *((volatile long long *)P.steps);
+    const int slot = int(stepno & 1);
+    const int members = P.members;
+    double dtm;
+    if (!STAGE2) {
+        const double umax = __longlong_as_double((long long)P.maxes[(slot * 2 + 0) * members + m]);
+        const double numax = __longlong_as_double((long long)P.maxes[(slot * 2 + 1) * members + m]);
+        const double t_end = P.ctrl->t_end, dt_fixed = P.ctrl->dt_fixed;
+        dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, umax, numax);
+        const double tm = P.t[m];
+        if (t_end > 0.0) {
+            if (!(tm < t_end)) dtm = 0.0;
+            else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end
+        }
+        if (!(dtm >= 0.0) || !isfinite(dtm)) {
+            if (tid == 0) atomicOr(P.err, ERR_DT);
+            return;
+        }
+        if (j == 0 && tid == 0) P.dt[m] = dtm;
+    } else {
+        dtm = P.dt[m];
+    }
+    const double lam = P.lam[m];
+    const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
+    const double dx = P.dx, g = P.g;
+
+    double *sEh = smem;
+    double *sEq = sEh + SROWS;
+    double *sEH = sEq + SROWS;
+    double *sEW = sEH + SROWS;
+    double *sQd = sEW + SROWS;   // q^dagger  (R_q before phase 1)
+    double *sHd = sQd + SROWS;   // H^dagger  (R_H before phase 1)
+    double *sWd = sHd + SROWS;   // W^dagger  (R_W before phase 1)
+    double *sBe = sWd + SROWS;   // beta
+    double *sDe = sBe + SROWS;   // delta
+    double *sHR = sDe + SROWS;   // h^R (+ hydrostatic bathymetric term)
+
+    double umax_loc = 0.0, numax_loc = 0.0;
+    unsigned int errbits = 0u;
+
+    if (dtm == 0.0) {
+        // member already at t_end: carry the state (and its dt maxima)
+        for (int i = s + tid; i < e; i += NT) {
+            const double h = B.Un[0][mo + i], q = B.Un[1][mo + i], K = B.Un[2][mo + i],
+                         W = B.Un[3][mo + i];
+            B.out[0][mo + i] = h; B.out[1][mo + i] = q; B.out[2][mo + i] = K; B.out[3][mo + i] = W;
+            if (FINAL) {
+                const double bb = BATHY ? __ldg(P.b + i) : 0.0;
+                const double H = K - 1.5 * h * bb;
+                const double u = q / h, sg = H / h / h;
+                umax_loc = fmax(umax_loc, fabs(u));
+                numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * h + (lam / 3.0) * sg * sg));
+            }
+        }
+    } else {
+        // ---- load: E on rows -3..L+2, R on rows -1..L -----------------------
+        const double wE = P.wE, wR = P.wR;
+        for (int idx = tid; idx < L + 6; idx += NT) {
+            const int r = idx - 3;
+            double par;
+            const int c = map_cell(start + r, n, P.bcl, P.bcr, par);
+            const size_t gi = mo + c;
+            const double bb = BATHY ? __ldg(P.b + c) : 0.0;
+            double eh = B.Un[0][gi], eq = par * B.Un[1][gi], eK = B.Un[2][gi], eW = B.Un[3][gi];
+            double rh = eh, rq = eq, rK = eK, rW = eW;
+            if (STAGE2) {
+                const double h1 = B.U1[0][gi], q1 = par * B.U1[1][gi], K1 = B.U1[2][gi],
+                             W1 = B.U1[3][gi];
+                // efficient form
+                rh = (1.0 - wR) * eh + wR * h1; rq = (1.0 - wR) * eq + wR * q1;
+                rK = (1.0 - wR) * eK + wR * K1; rW = (1.0 - wR) * eW + wR * W1;
+                eh = (1.0 - wE) * eh + wE * h1; eq = (1.0 - wE) * eq + wE * q1;
+                eK = (1.0 - wE) * eK + wE * K1; eW = (1.0 - wE) * eW + wE * W1;
+            }
+            sEh[idx] = eh; sEq[idx] = eq;
+            sEH[idx] = BATHY ? eK - 1.5 * eh * bb : eK;   // H = K - 1.5 h b (A9)
+            sEW[idx] = eW;
+            if (r >= -1 && r <= L) {
+                const int p = r + 1;
+                sHR[p] = rh; sQd[p] = rq;
+                sHd[p] = BATHY ? rK - 1.5 * rh * bb : rK;
+                sWd[p] = rW;
+            }
+        }
+        __syncthreads();
+
+        // ---- phase 1: faces, predictor, coefficients (chunk rows) -------------
+        {
+            const int p0 = tid * MCH;
+            if (p0 < L + 2) {
+                const double tdx = tau / dx;
+                const double lt2 = lam * tau * tau;
+                double wh[4], wq[4], wH[4], wW[4];
+                const int r0 = p0 - 1;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {     // rows r0-2 .. r0+1
+                    const int ix = r0 - 2 + k + 3;
+                    wh[k] = sEh[ix]; wq[k] = sEq[ix]; wH[k] = sEH[ix]; wW[k] = sEW[ix];
+                }
+                Face Fl = face_flux(wh, wq, wH, wW, P.order);
+#pragma unroll
+                for (int i = 0; i < MCH; i++) {
+                    const int r = r0 + i;
+                    if (r > L) break;
+#pragma unroll
+                    for (int k = 0; k < 3; k++) {
+                        wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
+                    }
+                    {
+                        const int ix = r + 2 + 3;
+                        wh[3] = sEh[ix]; wq[3] = sEq[ix]; wH[3] = sEH[ix]; wW[3] = sEW[ix];
+                    }
+                    const Face Fr = face_flux(wh, wq, wH, wW, P.order);
+                    const int p = r + 1;
+                    const double hE = wh[1], qE = wq[1], HE = wH[1];
+                    const double hR = sHR[p], qR = sQd[p], HR = sHd[p], WR = sWd[p];
+                    double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
+                    if (BATHY) {
+                        const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
+                        const double b0 = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
+                        const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
+                        Dxb = (bp - bm) / (2.0 * dx);
+                        // hydrostatic term in zeta-form (A9)
+                        const double Gr = g * (hE + wh[2]) * 0.5, Gl = g * (wh[0] + hE) * 0.5;
+                        hRp = hR + (tau * tau / (dx * dx)) * (Gr * (bp - b0) - Gl * (b0 - bm));
+                        const double sgE = HE / hE / hE;
+                        ptil_term = 1.5 * tau * (lam / 3.0) * (1.0 - sgE) * Dxb;   // p~
+                    }
+                    // predictor
+                    const double Wd = WR - tdx * (Fr.W - Fl.W) + lam * tau;
+                    const double Hd = HR - tdx * (Fr.H - Fl.H) - 1.5 * tau * qE * Dxb + tau * Wd;
+                    const double qd = qR - tdx * (Fr.q - Fl.q) - ptil_term;
+                    // coefficients at E (A2)
+                    const double sg = HE / hE / hE;
+                    const double alpha = -(2.0 * sg - 1.0) / (3.0 * hE);
+                    const double a2 = g * hE + (lam / 3.0) * sg * (3.0 * sg - 1.0);
+                    const double ih2 = 1.0 / (hE * hE);
+                    const double beta1 = 1.0 + lt2 * ih2;
+                    const double ib1 = 1.0 / beta1;
+                    const double beta2 = 2.0 * lt2 * ib1 * ib1 * ih2 / hE;
+                    const double beta = a2 + lam * alpha * beta2 * Hd;
+                    const double delta = alpha * ib1;
+                    if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
+                    sQd[p] = qd; sHd[p] = Hd; sWd[p] = Wd; sBe[p] = beta; sDe[p] = delta;
+                    sHR[p] = hRp;
+                    Fl = Fr;
+                }
+            }
+        }
+        __syncthreads();
+        // derived-field ghosts at physical boundaries (A10)
+        if (tid == 0 && left_phys) {
+            sQd[0] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[1];
+            sHd[0] = sHd[1]; sBe[0] = sBe[1]; sDe[0] = sDe[1];
+        }
+        if (tid == 32 && right_phys) {
+            sQd[L + 1] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L];
+            sHd[L + 1] = sHd[L]; sBe[L + 1] = sBe[L]; sDe[L + 1] = sDe[L];
+        }
+        __syncthreads();
+
+        // ---- phase 2: assemble + partition solve (A1, A3) ---------
+        double *sHB = sEq;            // hbar[r], r in [0, L)
+        double *pcr0 = sEH;           // PCR buffers: 2 x 4 x NT doubles over sEH..sEW
+        double *pcr1 = sEH + 4 * NT;
+        double rho_loc = 0.0;
+        {
+            const double t2 = tau * tau / (dx * dx);
+            const double lt2h = lam * tau * tau / (2.0 * dx * dx);
+            const double tdx2 = tau / (2.0 * dx);
+            const int r0 = tid * MCH;
+            double am[MCH], cm[MCH], dm[MCH];
+#pragma unroll
+            for (int i = 0; i < MCH; i++) {
+                const int r = r0 + i;
+                double a = 0.0, c = 0.0, dg = 1.0, rhs = 0.0;
+                if (r < L) {
+                    const int p = r + 1;
+                    const double bl = sBe[p - 1], bc = sBe[p], br = sBe[p + 1];
+                    const double rl = (r == 0) ? 0.0 : t2 * (bl + bc) * 0.5;
+                    const double rr = (r == L - 1) ? 0.0 : t2 * (bc + br) * 0.5;
+                    const double dl = sDe[p - 1], dc = sDe[p], dr = sDe[p + 1];
+                    const double ml = lt2h * (dl + dc), mr = lt2h * (dc + dr);
+                    const double Hl = sHd[p - 1], Hc = sHd[p], Hr = sHd[p + 1];
+                    rhs = sHR[p] - tdx2 * (sQd[p + 1] - sQd[p - 1]) + mr * (Hr - Hc) - ml * (Hc - Hl);
+                    a = -rl; c = -rr; dg = 1.0 + rl + rr;
+                    rho_loc = fmax(rho_loc, rr);
+                }
+                if (i == 0) {
+                    const double inv = 1.0 / dg;
+                    am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
+                } else {
+                    const double inv = 1.0 / (dg - a * cm[i - 1]);
+                    am[i] = -a * am[i - 1] * inv;
+                    cm[i] = c * inv;
+                    dm[i] = (rhs - a * dm[i - 1]) * inv;
+                }
+            }
+            // chunk-end relation (downward) and first-row relation (upward):
+            // x_i = P_i - Q_i X_{k-1} - R_i X_k,  X_k = last row of chunk k
+            const double aE = am[MCH - 1], cE = cm[MCH - 1], dE = dm[MCH - 1];
+            double Pn = 0.0, Qn = 0.0, Rn = -1.0;
+#pragma unroll
+            for (int i = MCH - 2; i >= 0; i--) {
+                const double Pi = dm[i] - cm[i] * Pn;
+                const double Qi = am[i] - cm[i] * Qn;
+                const double Ri = -cm[i] * Rn;
+                dm[i] = Pi; am[i] = Qi; cm[i] = Ri;
+                Pn = Pi; Qn = Qi; Rn = Ri;
+            }
+            // neighbour's (P_0, Q_0, R_0) via shuffles / smem across warps
+            const int lane = tid & 31, wid = tid >> 5;
+            double P1 = __shfl_down_sync(0xffffffffu, dm[0], 1);
+            double Q1 = __shfl_down_sync(0xffffffffu, am[0], 1);
+            double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
+            if (lane == 0) { xch[wid][0] = dm[0]; xch[wid][1] = am[0]; xch[wid][2] = cm[0]; }
+            rho_loc = warp_max(rho_loc);
+            if (lane == 0) red[wid] = rho_loc;
+            __syncthreads();
+            if (lane == 31) {
+                if (wid + 1 < NT / 32) { P1 = xch[wid + 1][0]; Q1 = xch[wid + 1][1]; R1 = xch[wid + 1][2]; }
+                else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
+            }
+            // reduced row k:  A X_{k-1} + Bd X_k + C X_{k+1} = D
+            double A_ = aE, Bd = 1.0 - cE * Q1, C_ = -cE * R1, D_ = dE - cE * P1;
+            if (tid == 0) A_ = 0.0;
+            // PCR over NT unknowns, double-buffered
+            double *cur = pcr0, *nxt = pcr1;
+            cur[tid] = A_; cur[NT + tid] = Bd; cur[2 * NT + tid] = C_; cur[3 * NT + tid] = D_;
+            __syncthreads();
+#pragma unroll 1
+            for (int sd = 1; sd < NT; sd <<= 1) {
+                const int km = tid - sd, kp = tid + sd;
+                double Am = 0, Bm = 1, Cm = 0, Dm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0;
+                if (km >= 0) { Am = cur[km]; Bm = cur[NT + km]; Cm = cur[2 * NT + km]; Dm = cur[3 * NT + km]; }
+                if (kp < NT) { Ap = cur[kp]; Bp = cur[NT + kp]; Cp = cur[2 * NT + kp]; Dp = cur[3 * NT + kp]; }
+                const double k1 = A_ / Bm, k2 = C_ / Bp;
+                const double An = -Am * k1, Cn = -Cp * k2;
+                const double Bn = Bd - Cm * k1 - Ap * k2;
+                const double Dn = D_ - Dm * k1 - Dp * k2;
+                A_ = An; Bd = Bn; C_ = Cn; D_ = Dn;
+                nxt[tid] = A_; nxt[NT + tid] = Bd; nxt[2 * NT + tid] = C_; nxt[3 * NT + tid] = D_;
+                __syncthreads();
+                double *tmp = cur; cur = nxt; nxt = tmp;
+            }
+            const double Xk = D_ / Bd;
+            cur[3 * NT + tid] = Xk;     // own slot; neighbours read after the barrier
+            __syncthreads();
+            const double XL = (tid > 0) ? cur[3 * NT + tid - 1] : 0.0;
+#pragma unroll
+            for (int i = 0; i < MCH; i++) {
+                const int r = r0 + i;
+                const double x = (i == MCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
+                if (r < L) sHB[r] = x;
+            }
+            if (tid == 0) {
+                double rmax = 0.0;
+                for (int q = 0; q < NT / 32; q++) rmax = fmax(rmax, red[q]);
+                // overlap check: r^w <= 2^-60 at every truncated end
+                if (rmax > 0.0) {
+                    const double rdec = 2.0 * rmax / ((1.0 + 2.0 * rmax) + sqrt(1.0 + 4.0 * rmax));
+                    const double need = 41.588830833596716 / (-log(rdec));   // 60 ln 2
+                    if ((!left_phys && double(wl) < need) || (!right_phys && double(wr) < need))
+                        errbits |= ERR_OVERLAP;
+                }
+                atomicMax(P.rho_obs, (unsigned long long)__double_as_longlong(rmax));
+            }
+        }
+        __syncthreads();
+
+        // ---- phase 3: back-substitution ---------------------------
+        const double tdx2 = tau / (2.0 * dx);
+        const double ltdx2 = lam * tau / (2.0 * dx);
+        const double lt2 = lam * tau * tau;
+        const bool filt = FINAL && (P.filter_sigma > 0.0);
+        double *sQb = sEH, *sWb = sEW, *sHb = sHR;   // filter scratch (rows r)
+        const int rbeg = filt ? max(0, wl - 2) : wl;
+        const int rend = filt ? min(L, wl + Tk + 2) : wl + Tk;
+        for (int r = rbeg + tid; r < rend; r += NT) {
+            const int p = r + 1;
+            const double hb = sHB[r];
+            const double hl = (r > 0) ? sHB[r - 1] : hb;        // Neumann at physical ends
+            const double hr = (r < L - 1) ? sHB[r + 1] : hb;
+            double qb = sQd[p] - tdx2 * sBe[p] * (hr - hl) - ltdx2 * sDe[p] * (sHd[p + 1] - sHd[p - 1]);
+            double bb = 0.0;
+            if (BATHY) {
+                const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
+                const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
+                bb = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
+                qb -= tau * g * sEh[r + 3] * (bp - bm) / (2.0 * dx);     // A9
+            }
+            const double ihb2 = 1.0 / (hb * hb);
+            const double Hb = sHd[p] / (1.0 + lt2 * ihb2);
+            const double Wb = sWd[p] - lam * tau * Hb * ihb2;
+            const bool kept = (r >= wl && r < wl + Tk);
+            if (kept) {
+                if (!(hb > P.h_min)) errbits |= ERR_DRY;
+                if (!isfinite(hb) || !isfinite(qb) || !isfinite(Hb) || !isfinite(Wb))
+                    errbits |= ERR_NONFINITE;
+            }
+            if (filt) {
+                sQb[r] = qb; sWb[r] = Wb; sHb[r] = Hb;
+            } else if (kept) {
+                const size_t gi = mo + (s + (r - wl));
+                B.out[0][gi] = hb; B.out[1][gi] = qb; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
+                B.out[3][gi] = Wb;
+                if (FINAL) {
+                    const double u = qb / hb, sg = Hb * ihb2;
+                    umax_loc = fmax(umax_loc, fabs(u));
+                    numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * hb + (lam / 3.0) * sg * sg));
+                }
+            }
+        }
+        if (filt) {
+            __syncthreads();
+            const double sig16 = P.filter_sigma / 16.0;
+            for (int r = wl + tid; r < wl + Tk; r += NT) {
+                double fq[5], fw[5];
+#pragma unroll
+                for (int k = -2; k <= 2; k++) {
+                    int rr = r + k;
+                    double pq = 1.0;
+                    if (rr < 0) {            // only at a physical left boundary
+                        if (P.bcl == BC_WALL) { rr = -1 - rr; pq = -1.0; } else rr = 0;
+                    } else if (rr >= L) {    // only at a physical right boundary
+                        if (P.bcr == BC_WALL) { rr = 2 * L - 1 - rr; pq = -1.0; } else rr = L - 1;
+                    }
+                    fq[k + 2] = pq * sQb[rr];
+                    fw[k + 2] = sWb[rr];
+                }
+                const double qf = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
+                const double wf = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
+                const double hb = sHB[r], Hb = sHb[r];
+                const double bb = BATHY ? __ldg(P.b + (s + (r - wl))) : 0.0;
+                const size_t gi = mo + (s + (r - wl));
+                B.out[0][gi] = hb; B.out[1][gi] = qf; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
+                B.out[3][gi] = wf;
+                const double u = qf / hb, sg = Hb / (hb * hb);
+                umax_loc = fmax(umax_loc, fabs(u));
+                numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * hb + (lam / 3.0) * sg * sg));
+                if (!isfinite(qf) || !isfinite(wf)) errbits |= ERR_NONFINITE;
+            }
+        }
+    }
+
+    // ---- error bits --------------------------------------------------------
+    {
+        unsigned int eb = errbits;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) eb |= __shfl_xor_sync(0xffffffffu, eb, o);
+        if ((tid & 31) == 0 && eb) atomicOr(P.err, eb);
+    }
+
+    if (FINAL) {
+        // ---- dt maxima for the next step -----------------------------
+        const double um = block_max(umax_loc, red);
+        const double nm = block_max(numax_loc, red);
+        const int nslot = slot ^ 1;
+        if (tid == 0) {
+            atomicMax(P.maxes + (nslot * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
+            atomicMax(P.maxes + (nslot * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
+        }
+        // ---- commit by the last CTA ----------------------------------------------
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            const unsigned int total = gridDim.x * gridDim.y;
+            const unsigned int prev = atomicAdd(P.done, 1u);
+            s_last = (prev == total - 1) ? 1 : 0;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            const bool ok = (*((volatile unsigned int *)P.err) == 0u);
+            const double t_end = P.ctrl->t_end;
+            if (ok) {
+                for (int mm = tid; mm < members; mm += NT) {
+                    const double tm = P.t[mm], d = P.dt[mm];
+                    P.t[mm] = (t_end > 0.0 && d == t_end - tm) ? t_end : tm + d;
+                    P.maxes[(slot * 2 + 0) * members + mm] = 0ull;
+                    P.maxes[(slot * 2 + 1) * members + mm] = 0ull;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                if (ok) *P.steps = stepno + 1;
+                *P.done = 0u;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-(tile, member) reductions of a state: mass partial sums (deterministic,
+// summed on the host), min h, max|u|, max(|u|+c).  Optionally seeds the dt
+// maxima slot 0 (after hsgn_set_state).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) reduce_kernel(const double *__restrict__ h,
+                                                    const double *__restrict__ q,
+                                                    const double *__restrict__ K,
+                                                    const double *__restrict__ b,
+                                                    const double *__restrict__ lamv, int n, int T,
+                                                    double g, double *partials,
+                                                    unsigned long long *maxes, int members)
+{
+    __shared__ double red[NT / 32 + 1];
+    __shared__ double sred[NT];
+    const int j = blockIdx.x, m = blockIdx.y, tid = threadIdx.x;
+    const int s = j * T, e = min(n, s + T);
+    const size_t mo = size_t(m) * n;
+    const double lam = lamv[m];
+    double sum = 0.0, mn = 1e300, um = 0.0, nm = 0.0;
+    for (int i = s + tid; i < e; i += NT) {
+        const double hh = h[mo + i], qq = q[mo + i];
+        const double bb = b ? b[i] : 0.0;
+        const double H = K[mo + i] - 1.5 * hh * bb;
+        const double u = qq / hh, sg = H / hh / hh;
+        sum += hh;
+        mn = fmin(mn, hh);
+        um = fmax(um, fabs(u));
+        nm = fmax(nm, fabs(u) + sqrt(g * hh + (lam / 3.0) * sg * sg));
+    }
+    // deterministic tree sum
+    sred[tid] = sum;
+    __syncthreads();
+    for (int o = NT / 2; o > 0; o >>= 1) {
+        if (tid < o) sred[tid] += sred[tid + o];
+        __syncthreads();
+    }
+    const double tot = sred[0];
+    __syncthreads();
+    const double mnn = -block_max(-mn, red);
+    const double umm = block_max(um, red);
+    const double nmm = block_max(nm, red);
+    if (tid == 0) {
+        const size_t o = (size_t(m) * gridDim.x + j) * 4;
+        partials[o + 0] = tot;
+        partials[o + 1] = mnn;
+        partials[o + 2] = umm;
+        partials[o + 3] = nmm;
+        if (maxes) {
+            atomicMax(maxes + 0 * members + m, (unsigned long long)__double_as_longlong(umm));
+            atomicMax(maxes + 1 * members + m, (unsigned long long)__double_as_longlong(nmm));
+        }
+    }
+}
+
+}  // namespace hsgn

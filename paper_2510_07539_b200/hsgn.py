@@ -1,0 +1,281 @@
+"""Thin Python binding of libhsgn.so (include/hsgn.h): argument marshalling only.
+
+Every step of the SI-IMEX path runs in the CUDA kernels of csrc/; this module
+only passes pointers and sizes.  torch provides device memory (the workspace)
+and the stream.  There is no CPU fallback: if the library is missing or no
+CUDA device is present, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libhsgn.so")
+
+BC = {"periodic": 0, "wall": 1, "transmissive": 2}
+STATUS = {0: "OK", -1: "E_INVALID", -2: "E_DRY", -3: "E_COERCIVITY", -4: "E_SINGULAR",
+          -5: "E_NONFINITE", -6: "E_CUDA", -7: "E_OVERLAP", -8: "E_NOWORKSPACE"}
+
+
+class HsgnError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hsgn {STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Desc(C.Structure):
+    _fields_ = [("n_cells", C.c_int64), ("n_members", C.c_int32), ("order", C.c_int32),
+                ("x_min", C.c_double), ("x_max", C.c_double), ("bc_left", C.c_int32),
+                ("bc_right", C.c_int32), ("tile_cells", C.c_int32), ("overlap", C.c_int32)]
+
+
+class Tableau(C.Structure):
+    _fields_ = [("stages", C.c_int32), ("pad_", C.c_int32), ("a_exp", (C.c_double * 2) * 2),
+                ("a_imp", (C.c_double * 2) * 2), ("b", C.c_double * 2)]
+
+
+class Diag(C.Structure):
+    _fields_ = [("mass", C.c_double), ("min_h", C.c_double), ("max_abs_u", C.c_double),
+                ("nu_max", C.c_double), ("t_min", C.c_double), ("t_max", C.c_double),
+                ("dt_last_min", C.c_double), ("dt_last_max", C.c_double),
+                ("steps", C.c_int64), ("error_bits", C.c_int32), ("pad_", C.c_int32)]
+
+
+# exported symbols (checked by tests/test_abi.py against include/hsgn.h)
+SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_workspace",
+           "hsgn_set_params", "hsgn_set_tableau", "hsgn_set_bathymetry", "hsgn_set_filter",
+           "hsgn_set_state", "hsgn_get_state", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
+           "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
+           "hsgn_status_string", "hsgn_last_error"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libhsgn.so and declare its signatures (no CUDA calls)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing: run `python -m paper_2510_07539_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, dp = C.c_void_p, C.POINTER(C.c_double)
+    st = C.c_int
+    sig = {
+        "hsgn_create": (st, [C.POINTER(Desc), vp, C.POINTER(vp)]),
+        "hsgn_destroy": (None, [vp]),
+        "hsgn_workspace_bytes": (C.c_size_t, [vp]),
+        "hsgn_set_workspace": (st, [vp, vp, C.c_size_t]),
+        "hsgn_set_params": (st, [vp, C.c_double, dp, C.c_double, C.c_double, C.c_double]),
+        "hsgn_set_tableau": (st, [vp, C.POINTER(Tableau)]),
+        "hsgn_set_bathymetry": (st, [vp, vp]),
+        "hsgn_set_filter": (st, [vp, C.c_double, C.c_uint32]),
+        "hsgn_set_state": (st, [vp, vp, vp, vp, vp, C.c_double]),
+        "hsgn_get_state": (st, [vp, vp, vp, vp, vp, vp]),
+        "hsgn_step": (st, [vp, C.c_double, dp]),
+        "hsgn_run_steps": (st, [vp, C.c_int64]),
+        "hsgn_advance_to": (st, [vp, C.c_double, C.c_int64, C.POINTER(C.c_int64)]),
+        "hsgn_sync": (st, [vp]),
+        "hsgn_run_steps_timed": (st, [vp, C.c_int64, dp]),
+        "hsgn_get_diagnostics": (st, [vp, C.POINTER(Diag)]),
+        "hsgn_launch_count": (C.c_int64, [vp]),
+        "hsgn_get_geometry": (st, [vp] + [C.POINTER(C.c_int32)] * 5),
+        "hsgn_status_string": (C.c_char_p, [st]),
+        "hsgn_last_error": (C.c_char_p, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def paper_tableau() -> Tableau:
+    """gamma = 1 - 1/sqrt 2, c = 1/(2 gamma)."""
+    g = 1.0 - 1.0 / np.sqrt(2.0)
+    c = 1.0 / (2.0 * g)
+    return make_tableau(2, [[0, 0], [c, 0]], [[g, 0], [1 - g, g]], [1 - g, g])
+
+
+def euler_tableau() -> Tableau:
+    """First-order SI step: one implicit stage with tau = dt."""
+    return make_tableau(1, [[0, 0], [0, 0]], [[1.0, 0], [0, 0]], [1.0, 0])
+
+
+def make_tableau(stages, aE, aI, b) -> Tableau:
+    T = Tableau()
+    T.stages = stages
+    for i in range(2):
+        for j in range(2):
+            T.a_exp[i][j] = float(aE[i][j])
+            T.a_imp[i][j] = float(aI[i][j])
+        T.b[i] = float(b[i])
+    return T
+
+
+def _ptr(a):
+    """Raw pointer of a torch tensor (device or host) or a numpy array."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+        return a.ctypes.data
+    import torch
+    assert a.dtype == torch.float64 and a.is_contiguous()
+    return a.data_ptr()
+
+
+@dataclass
+class Geometry:
+    tile_cells: int
+    overlap: int
+    tiles_per_member: int
+    threads: int
+    max_rows: int
+
+
+class Solver:
+    """One context: `members` independent 1-D domains of `n` cells each."""
+
+    def __init__(self, n: int, members: int = 1, x_min: float = 0.0, x_max: float = 1.0,
+                 bc=("periodic", "periodic"), order: int = 2, tile_cells: int = 0,
+                 overlap: int = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device: the hSGN path has no CPU fallback")
+        self.L = load_library()
+        self.n, self.members = int(n), int(members)
+        self.dx = (x_max - x_min) / n
+        self._torch = torch
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        d = Desc(n_cells=n, n_members=members, order=order, x_min=x_min, x_max=x_max,
+                 bc_left=BC[bc[0]], bc_right=BC[bc[1]], tile_cells=tile_cells, overlap=overlap)
+        h = C.c_void_p()
+        self._chk(self.L.hsgn_create(C.byref(d), C.c_void_p(self.stream.cuda_stream), C.byref(h)),
+                  ctx=False)
+        self.ctx = h
+        nbytes = self.L.hsgn_workspace_bytes(self.ctx)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self._chk(self.L.hsgn_set_workspace(self.ctx, C.c_void_p(self.workspace.data_ptr()), nbytes))
+        self._keep = []
+
+    # -- plumbing ----------------------------------------------------------
+    def _chk(self, st, ctx=True):
+        if st != 0:
+            msg = self.L.hsgn_last_error(self.ctx).decode() if ctx else ""
+            raise HsgnError(st, msg or self.L.hsgn_status_string(st).decode())
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.L.hsgn_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def geometry(self) -> Geometry:
+        v = [C.c_int32() for _ in range(5)]
+        self._chk(self.L.hsgn_get_geometry(self.ctx, *[C.byref(x) for x in v]))
+        return Geometry(*[x.value for x in v])
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.hsgn_launch_count(self.ctx))
+
+    # -- parameters ----------------------------------------------------------
+    def set_params(self, g=9.81, lam=500.0, cfl=2.0, mcfl=0.5, h_min=1e-8):
+        lam = np.ascontiguousarray(np.broadcast_to(np.asarray(lam, dtype=np.float64),
+                                                   (self.members,)))
+        self._chk(self.L.hsgn_set_params(self.ctx, g, lam.ctypes.data_as(C.POINTER(C.c_double)),
+                                         cfl, mcfl, h_min))
+
+    def set_tableau(self, tab: Tableau):
+        self._chk(self.L.hsgn_set_tableau(self.ctx, C.byref(tab)))
+
+    def set_bathymetry(self, b):
+        if b is not None:
+            b = self._as_f64(b)
+            self._keep.append(b)
+        self._chk(self.L.hsgn_set_bathymetry(self.ctx, C.c_void_p(_ptr(b)) if b is not None else None))
+
+    def set_filter(self, sigma: float, mask: int = 0b1010):
+        self._chk(self.L.hsgn_set_filter(self.ctx, float(sigma), mask if sigma > 0 else 0))
+
+    # -- state ------------------------------------------------------------
+    def _as_f64(self, a):
+        if isinstance(a, np.ndarray):
+            return np.ascontiguousarray(a, dtype=np.float64)
+        return a.contiguous().to(self._torch.float64)
+
+    def set_state(self, h, q, K, W, t0: float = 0.0):
+        arrs = [self._as_f64(a) for a in (h, q, K, W)]
+        for a in arrs:
+            assert a.size == self.n * self.members if isinstance(a, np.ndarray) else a.numel() == self.n * self.members
+        self._chk(self.L.hsgn_set_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in arrs], t0))
+
+    def get_state(self, device: bool = True):
+        """Return (h, q, K, W) as [members, n] tensors (device) or numpy arrays, and t[members]."""
+        torch = self._torch
+        if device:
+            out = [torch.empty((self.members, self.n), dtype=torch.float64, device="cuda") for _ in range(4)]
+        else:
+            out = [np.empty((self.members, self.n)) for _ in range(4)]
+        t = np.empty(self.members)
+        self._chk(self.L.hsgn_get_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in out],
+                                        C.c_void_p(t.ctypes.data)))
+        return out, t
+
+    # -- stepping ------------------------------------------------------------
+    def step(self, dt: float = 0.0, return_dt: bool = False):
+        if return_dt:
+            d = np.empty(self.members)
+            self._chk(self.L.hsgn_step(self.ctx, dt, d.ctypes.data_as(C.POINTER(C.c_double))))
+            return d
+        self._chk(self.L.hsgn_step(self.ctx, dt, None))
+
+    def run_steps(self, n_steps: int):
+        self._chk(self.L.hsgn_run_steps(self.ctx, int(n_steps)))
+
+    def run_steps_timed(self, n_steps: int):
+        """Eager steps with CUDA events between kernels; returns summed device
+        ms per stage kind (stage 1, stage 2)."""
+        ms = np.zeros(2)
+        self._chk(self.L.hsgn_run_steps_timed(self.ctx, int(n_steps),
+                                              ms.ctypes.data_as(C.POINTER(C.c_double))))
+        return float(ms[0]), float(ms[1])
+
+    def advance_to(self, t_end: float, max_steps: int = 1 << 40) -> int:
+        s = C.c_int64()
+        self._chk(self.L.hsgn_advance_to(self.ctx, t_end, max_steps, C.byref(s)))
+        return s.value
+
+    def sync(self):
+        self._chk(self.L.hsgn_sync(self.ctx))
+
+    def diagnostics(self) -> dict:
+        d = Diag()
+        self._chk(self.L.hsgn_get_diagnostics(self.ctx, C.byref(d)))
+        return {k: getattr(d, k) for k, _ in Diag._fields_ if k != "pad_"}
+
+
+def solver_for(w, **kw) -> Solver:
+    """Build a Solver for a workloads.Workload (state, params, bathymetry, filter)."""
+    s = Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, **kw)
+    s.set_params(w.g, w.lam, w.cfl, w.mcfl)
+    if w.b is not None:
+        s.set_bathymetry(w.b)
+    if w.filter_sigma > 0:
+        s.set_filter(w.filter_sigma)
+    s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
+    return s

@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Metric (reading A17): for every field and every
+member, max_i |f_gpu - f_ref| / max_i |f_ref|;  <= 1e-11 after one step and
+<= 1e-8 after a full run (north_star)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2510_07539_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-11
+TOL_RUN = 1e-8
+
+
+def _hsgn():
+    from paper_2510_07539_b200 import hsgn
+    return hsgn
+
+
+def rel_err(gpu, ref):
+    """max over fields of max_i |gpu - ref| / max_i |ref| (per member)."""
+    out = []
+    for fg, fr in zip(gpu, ref):
+        fg = np.asarray(fg)
+        fr = np.asarray(fr)
+        out.append(np.max(np.abs(fg - fr)) / max(np.max(np.abs(fr)), 1e-300))
+    return max(out)
+
+
+def oracle_run(w, members, steps=None, t_end=None, order=2, tableau=None, dt_fixed=0.0):
+    jobs = []
+    for m in members:
+        o = O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, order=order, b=w.b,
+                     filter_sigma=w.filter_sigma, tableau=tableau)
+        jobs.append((o, w.state(m)))
+    res = O.run_members(jobs, cfl=w.cfl, mcfl=w.mcfl, steps=steps, t_end=t_end, dt_fixed=dt_fixed)
+    return [r[0] for r in res], [r[1] for r in res]
+
+
+def gpu_solver(w, **kw):
+    hs = _hsgn()
+    order = kw.pop("order", 2)
+    tab = kw.pop("tableau", None)
+    s = hs.Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, order=order, **kw)
+    s.set_params(w.g, w.lam, w.cfl, w.mcfl)
+    if tab is not None:
+        s.set_tableau(tab)
+    if w.b is not None:
+        s.set_bathymetry(w.b)
+    if w.filter_sigma > 0:
+        s.set_filter(w.filter_sigma)
+    s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
+    return s
+
+
+def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, **okw):
+    (h, q, K, Wf), t = s.get_state(device=False)
+    refs, trefs = oracle_run(w, members, steps=steps, t_end=t_end, **okw)
+    worst = 0.0
+    for i, m in enumerate(members):
+        e = rel_err([h[m], q[m], K[m], Wf[m]], refs[i])
+        worst = max(worst, e)
+        assert abs(t[m] - trefs[i]) <= 1e-12 * max(1.0, abs(trefs[i])), (m, t[m], trefs[i])
+    assert worst <= tol, worst
+    return worst
+
+
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("bc", ["periodic", "wall", "transmissive"])
+@pytest.mark.parametrize("order", [2, 1])
+def test_one_step_ragged_tiles(bc, order):
+    w = W.random_smooth(3000, 3, seed=21, amp=0.08, bc=(bc, bc))
+    s = gpu_solver(w, tile_cells=700, overlap=64, order=order)
+    assert s.geometry.tiles_per_member == 5
+    s.step()
+    compare(w, s, range(3), steps=1, order=order)
+
+
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_bathymetry_steps(bc):
+    w = W.random_smooth(2048, 2, seed=5, amp=0.05, bc=(bc, bc), bathy=0.08)
+    s = gpu_solver(w, tile_cells=512)
+    s.step()
+    compare(w, s, range(2), steps=1)
+    s.run_steps(19)
+    compare(w, s, range(2), steps=20, tol=1e-10)
+
+
+def test_euler_tableau_first_order_step():
+    w = W.random_smooth(1500, 2, seed=8, amp=0.05)
+    hs = _hsgn()
+    s = gpu_solver(w, tableau=hs.euler_tableau(), order=1, tile_cells=400)
+    s.run_steps(5)
+    compare(w, s, range(2), steps=5, order=1, tableau=O.euler_tableau(), tol=1e-10)
+
+
+def test_filter_walls_and_periodic():
+    for bc in ("periodic", "wall"):
+        w = W.random_smooth(2000, 2, seed=13, amp=0.05, bc=(bc, bc))
+        w.filter_sigma = 0.25
+        s = gpu_solver(w, tile_cells=500)
+        s.run_steps(30)
+        compare(w, s, range(2), steps=30, tol=1e-10)
+
+
+def test_single_tile_tiny_domains_wrap():
+    for n, bc in ((4, "periodic"), (7, "periodic"), (64, "periodic"), (5, "wall"), (9, "transmissive")):
+        w = W.random_smooth(n, 2, seed=n, amp=0.02, bc=(bc, bc))
+        s = gpu_solver(w)
+        s.run_steps(3)
+        compare(w, s, range(2), steps=3, tol=1e-10)
+
+
+def test_dt_rule_matches_oracle():
+    w = W.random_smooth(1024, 4, seed=3, amp=0.1)
+    w.cfl, w.mcfl = 2.0, 0.05       # make the material rule bind for some members
+    s = gpu_solver(w)
+    d = s.step(return_dt=True)
+    for m in range(4):
+        o = O.Oracle(w.n, w.dx, lam=float(w.lam[m]))
+        ref, _, _ = o.dt(w.state(m), w.cfl, w.mcfl)
+        assert abs(d[m] - ref) <= 1e-14 * ref
+
+
+def test_mass_conservation_gpu():
+    for bc in ("periodic", "wall"):
+        w = W.random_smooth(4096, 2, seed=2, amp=0.1, bc=(bc, bc))
+        s = gpu_solver(w)
+        m0 = s.diagnostics()["mass"]
+        s.run_steps(100)
+        d = s.diagnostics()
+        assert d["steps"] == 100
+        assert abs(d["mass"] - m0) <= 1e-13 * m0
+
+
+def test_launch_count_two_per_step():
+    w = W.random_smooth(512, 1, seed=1)
+    s = gpu_solver(w)
+    l0 = s.launches
+    s.run_steps(40)          # graph replays + eager remainder
+    s.sync()
+    assert s.launches - l0 == 80
+
+
+# --------------------------------------------------------------------------
+# error paths: status + last committed state
+# --------------------------------------------------------------------------
+def test_dry_bed_reported_and_state_kept():
+    hs = _hsgn()
+    w = W.random_smooth(512, 1, seed=4)
+    s = hs.Solver(w.n, 1, w.x_min, w.x_max)
+    s.set_params(9.81, w.lam, 2.0, 0.5, h_min=0.999)   # any h <= 0.999 is "dry"
+    s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
+    s.run_steps(3)
+    with pytest.raises(hs.HsgnError) as e:
+        s.sync()
+    assert e.value.name == "E_DRY"
+    out, t = _safe_state(s)
+    assert np.array_equal(out[0][0], w.h[0]) and t[0] == 0.0
+
+
+def _safe_state(s):
+    hs = _hsgn()
+    try:
+        return s.get_state(device=False)
+    except hs.HsgnError:
+        import ctypes as C
+        out = [np.empty((s.members, s.n)) for _ in range(4)]
+        t = np.empty(s.members)
+        s.L.hsgn_get_state(s.ctx, *[C.c_void_p(a.ctypes.data) for a in out], C.c_void_p(t.ctypes.data))
+        return out, t
+
+
+def test_coercivity_violation_reported():
+    hs = _hsgn()
+    n = 256
+    h = np.ones(n)
+    K = 0.2 * h * h                         # eta/h = 0.2 -> a^2 < 0 for lam = 1000
+    z = np.zeros(n)
+    with pytest.raises(O.OracleError) as eo:
+        O.Oracle(n, 0.1, lam=1000.0).step([h, z, K, z], 0.01)
+    assert eo.value.status == O.E_COERCIVITY
+    s = hs.Solver(n, 1, 0.0, n * 0.1)
+    s.set_params(9.81, 1000.0, 2.0, 0.5)
+    s.set_state(h, z, K, z)
+    with pytest.raises(hs.HsgnError) as e:
+        s.step(0.01, return_dt=True)
+    assert e.value.name == "E_COERCIVITY"
+
+
+def test_overlap_too_short_is_reported():
+    hs = _hsgn()
+    w = W.random_smooth(2048, 1, seed=6)
+    w.cfl = 8.0                               # rho ~ 11: needs w ~ 130 cells
+    s = gpu_solver(w, tile_cells=512, overlap=8)
+    s.run_steps(1)
+    with pytest.raises(hs.HsgnError) as e:
+        s.sync()
+    assert e.value.name == "E_OVERLAP"
+
+
+# --------------------------------------------------------------------------
+# BASELINE configs
+# --------------------------------------------------------------------------
+def test_cfg1_full_run_to_t20():
+    w = W.cfg1()
+    s = gpu_solver(w)
+    nst = s.advance_to(w.t_end)
+    (h, q, K, Wf), t = s.get_state(device=False)
+    assert t[0] == w.t_end
+    refs, trefs = oracle_run(w, [0], t_end=w.t_end)
+    assert trefs[0] == w.t_end
+    assert rel_err([h[0], q[0], K[0], Wf[0]], refs[0]) <= TOL_RUN
+    he, _ = W.soliton_exact(w.x(), w.t_end, 1.0, 0.2, -50.0, L=200.0)
+    assert np.sum(np.abs(h[0] - he)) / np.sum(np.abs(h[0])) < 2e-3
+    assert nst >= 500
+
+
+def test_cfg3_subset_200_steps():
+    w = W.cfg3(members=6)
+    s = gpu_solver(w)
+    s.run_steps(1)
+    compare(w, s, range(6), steps=1)
+    s.run_steps(199)
+    compare(w, s, range(6), steps=200, tol=TOL_RUN)
+
+
+@pytest.mark.slow
+def test_cfg3_full_size_sampled():
+    """cfg3 at full size (4096 x 4096) in bench.py's launch configuration;
+    sampled members checked against the oracle after 1 and 200 steps."""
+    w = W.cfg3()
+    s = gpu_solver(w)
+    sample = [0, 1, 777, 2048, 4095]
+    s.run_steps(1)
+    compare(w, s, sample, steps=1)
+    s.run_steps(199)
+    d = s.diagnostics()
+    assert d["steps"] == 200
+    compare(w, s, sample[:3], steps=200, tol=TOL_RUN)

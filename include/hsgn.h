@@ -93,12 +93,16 @@ typedef struct {
     int32_t bc_left;     /* hsgn_bc */
     int32_t bc_right;    /* hsgn_bc */
     int32_t tile_cells;  /* kept cells per CTA tile; 0 = automatic                  */
-    int32_t overlap;     /* tile overlap w (cells) for the depth solve; 0 = auto    */
+    int32_t overlap;     /* tile overlap w (cells) for the depth solve; 0 = auto:
+                            chosen from CFL_IMEX and the tableau at set_params /
+                            set_tableau                       */
 } hsgn_desc;
 
 /* Diagnostics (all members): mass = sum_i h_i dx summed over members,
  * min_h, max_abs_u, nu_max = max(|u| + c), t_min/t_max over members,
- * dt_last_min/max = last step's dt over members, steps = committed steps. */
+ * dt_last_min/max = last step's dt over members, rho_max = largest
+ * (tau/dx)^2 (beta_i + beta_{i+1})/2 seen (sets the solver overlap),
+ * steps = committed steps. */
 typedef struct {
     double mass;
     double min_h;
@@ -108,6 +112,7 @@ typedef struct {
     double t_max;
     double dt_last_min;
     double dt_last_max;
+    double rho_max;      /* max off-diagonal rho of the depth system seen since set_state */
     int64_t steps;
     int32_t error_bits;
     int32_t pad_;

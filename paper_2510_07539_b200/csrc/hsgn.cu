@@ -23,6 +23,7 @@ namespace {
 
 constexpr int GRAPH_STEPS = 16;   // steps per captured graph (even: buffers ping-pong)
 constexpr int POLL_STEPS = 256;   // advance_to polls the device every POLL_STEPS
+constexpr int T_MIN = 64;         // smallest kept tile (bounds the partials workspace)
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -158,6 +159,39 @@ hsgn_status set_ctrl(hsgn_ctx *c, double t_end, double dt_fixed)
     return HSGN_OK;
 }
 
+// Tile geometry: overlap w from the CFL-implied bound on
+// rho = (tau/dx)^2 beta <= 3 (a_ii CFL)^2 (beta <= ~2 nu^2 at rest, margin 1.5),
+// r = 2 rho / (1 + 2 rho + sqrt(1 + 4 rho)), w >= 60 ln2 / -ln r.  Every CTA
+// re-checks r^w <= 2^-60 with its actual rho_max.
+void choose_geometry(hsgn_ctx *c)
+{
+    int w;
+    if (c->desc.overlap > 0) {
+        w = c->desc.overlap;
+    } else if (c->cfl > 0.0) {
+        const double a = std::max(c->aI1, c->aI2);
+        const double rho = 3.0 * (a * c->cfl) * (a * c->cfl);
+        const double r = 2.0 * rho / (1.0 + 2.0 * rho + std::sqrt(1.0 + 4.0 * rho));
+        w = int(std::ceil(41.588830833596716 / -std::log(r))) + 4;
+        w = ((w + 7) / 8) * 8;
+    } else {
+        w = 256;   // material-CFL-only stepping: rho is not bounded a priori
+    }
+    w = std::max(3, std::min(w, (LCAP - 2 - T_MIN) / 2));
+    const int maxT = LCAP - 2 - 2 * w;
+    int T;
+    if (c->desc.tile_cells > 0) T = std::max(std::min<int>(c->desc.tile_cells, maxT), T_MIN);
+    else {
+        const int ntiles = (c->n + maxT - 1) / maxT;
+        T = (c->n + ntiles - 1) / ntiles;
+        if (ntiles > 1) T = ((T + 31) / 32) * 32;
+        T = std::max(std::min(T, maxT), std::min(T_MIN, c->n));
+    }
+    c->T = T;
+    c->w = w;
+    c->tiles = (c->n + T - 1) / T;
+}
+
 hsgn_status ready(hsgn_ctx *c)
 {
     if (!c) return HSGN_E_INVALID;
@@ -171,7 +205,7 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
 {
     long long done = 0;
     while (done < n_steps) {
-        if (n_steps - done >= GRAPH_STEPS) {
+        if (n_steps - done >= GRAPH_STEPS && c->stream != nullptr) {   // legacy stream: no capture
             cudaGraphExec_t &gx = c->graph[c->cur];
             if (!gx) {
                 cudaGraph_t gr;
@@ -267,22 +301,6 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     c->n = int(d->n_cells);
     c->members = d->n_members;
     c->dx = (d->x_max - d->x_min) / double(d->n_cells);
-    // overlap: enough for rho up to ~2.2 (CFL_IMEX ~ 3.5) by default; checked per tile
-    int w = d->overlap > 0 ? d->overlap : 64;
-    w = std::max(w, 3);
-    const int maxT = LCAP - 2 - 2 * w;
-    if (maxT < 16) { delete c; return HSGN_E_INVALID; }
-    int T;
-    if (d->tile_cells > 0) T = std::min<int>(d->tile_cells, maxT);
-    else {
-        const int ntiles = (c->n + maxT - 1) / maxT;
-        T = (c->n + ntiles - 1) / ntiles;
-        if (ntiles > 1) T = ((T + 31) / 32) * 32;       // aligned tiles when split
-        T = std::min(T, maxT);
-    }
-    c->T = T;
-    c->w = w;
-    c->tiles = (c->n + T - 1) / T;
     c->lam.assign(c->members, 0.0);
     // default tableau
     const double gm = 1.0 - 1.0 / std::sqrt(2.0), cc = 1.0 / (2.0 * gm);
@@ -293,6 +311,7 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     tb.b[0] = 1.0 - gm; tb.b[1] = gm;
     c->tab = tb;
     c->aI1 = gm; c->aI2 = gm; c->wE = cc / gm; c->wR = (1.0 - gm) / gm;
+    choose_geometry(c);
     // kernels need > 48 KiB dynamic smem
     cudaFuncSetAttribute(stage_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
@@ -325,7 +344,7 @@ size_t hsgn_workspace_bytes(const hsgn_ctx *c)
     s += align256(size_t(c->n) * sizeof(double));           // b
     s += 3 * align256(size_t(c->members) * sizeof(double)); // lam, t, dt
     s += align256(4 * size_t(c->members) * 8);              // maxes
-    s += align256(size_t(c->members) * c->tiles * 4 * sizeof(double));  // partials
+    s += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));  // partials
     s += 256;                                               // scalars
     s += 256;                                               // ctrl
     return s;
@@ -348,7 +367,7 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     c->t = (double *)q; q += align256(size_t(c->members) * sizeof(double));
     c->dt = (double *)q; q += align256(size_t(c->members) * sizeof(double));
     c->maxes = (unsigned long long *)q; q += align256(4 * size_t(c->members) * 8);
-    c->partials = (double *)q; q += align256(size_t(c->members) * c->tiles * 4 * sizeof(double));
+    c->partials = (double *)q; q += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));
     c->err = (unsigned int *)q;
     c->done = (unsigned int *)(q + 4);
     c->steps = (long long *)(q + 8);
@@ -381,6 +400,7 @@ hsgn_status hsgn_set_params(hsgn_ctx *c, double g, const double *lambda, double 
     c->lam.assign(lambda, lambda + c->members);
     c->have_params = true;
     drop_graphs(c);
+    choose_geometry(c);
     if (c->ws) {
         CUDA_TRY(c, cudaMemcpyAsync(c->lamd, c->lam.data(), c->members * sizeof(double),
                                     cudaMemcpyHostToDevice, c->stream));
@@ -409,6 +429,7 @@ hsgn_status hsgn_set_tableau(hsgn_ctx *c, const hsgn_tableau *t)
     }
     c->tab = *t;
     drop_graphs(c);
+    choose_geometry(c);
     return HSGN_OK;
 }
 
@@ -626,6 +647,11 @@ hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
         d.t_min = std::min(d.t_min, tv[m]); d.t_max = std::max(d.t_max, tv[m]);
         d.dt_last_min = std::min(d.dt_last_min, dv[m]); d.dt_last_max = std::max(d.dt_last_max, dv[m]);
     }
+    unsigned long long rb = 0;
+    CUDA_TRY(c, cudaMemcpy(&rb, c->rho_obs, sizeof(rb), cudaMemcpyDeviceToHost));
+    double rmx;
+    memcpy(&rmx, &rb, sizeof(rmx));
+    d.rho_max = rmx;
     d.steps = dsteps;
     d.error_bits = int32_t(bits);
     *o = d;

@@ -70,6 +70,30 @@ struct Bufs {
     double *out[4];
 };
 
+// Reciprocal: hardware approximation (MUFU.RCP64H, ~2^-20) refined by two
+// Newton steps (4 DFMA) to ~1 ulp -- replaces the IEEE division sequence, whose
+// slow-path branch and longer dependency chain dominated the stage's fp64 issue.
+__device__ __forceinline__ double rcp(double x)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ void cp_async8(double *dst_smem, const double *src)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 __device__ __forceinline__ int map_cell(int c, int n, int bcl, int bcr, double &par)
 {
     par = 1.0;
@@ -128,7 +152,7 @@ __device__ __forceinline__ Face face_flux(const double (&wh)[4], const double (&
         hm = wh[1]; hp = wh[2]; qm = wq[1]; qp = wq[2];
         Hm = wH[1]; Hp = wH[2]; Wm = wW[1]; Wp = wW[2];
     }
-    const double um = qm / hm, up = qp / hp;
+    const double um = qm * rcp(hm), up = qp * rcp(hp);
     const double a = fmax(fabs(um), fabs(up));
     Face F;
     F.q = 0.5 * (qm * um + qp * up) - 0.5 * a * (qp - qm);
@@ -144,7 +168,7 @@ __device__ __forceinline__ double warp_max(double v)
     return v;
 }
 
-__device__ __forceinline__ double block_max(double v, double *red)
+__device__ __forceinline__ double block_max(double v, double *red, double ident = 0.0)
 {
     v = warp_max(v);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -152,7 +176,7 @@ __device__ __forceinline__ double block_max(double v, double *red)
     if (lane == 0) red[wid] = v;
     __syncthreads();
     if (wid == 0) {
-        v = (lane < NT / 32) ? red[lane] : 0.0;
+        v = (lane < NT / 32) ? red[lane] : ident;
         v = warp_max(v);
         if (lane == 0) red[0] = v;
     }
@@ -225,12 +249,15 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     double *sEq = sEh + SROWS;
     double *sEH = sEq + SROWS;
     double *sEW = sEH + SROWS;
-    double *sQd = sEW + SROWS;   // q^dagger  (R_q before phase 1)
-    double *sHd = sQd + SROWS;   // H^dagger  (R_H before phase 1)
-    double *sWd = sHd + SROWS;   // W^dagger  (R_W before phase 1)
-    double *sBe = sWd + SROWS;   // beta
-    double *sDe = sBe + SROWS;   // delta
-    double *sHR = sDe + SROWS;   // h^R (+ hydrostatic bathymetric term)
+    // E arrays are indexed by idx = r + 3 (rows -3..L+2).  The phase-1 output
+    // arrays are offset by 2 so that index p = r + 1 lands on the same physical
+    // slot r + 3: the stage-2 raw copy of U1 and the R combination share it.
+    double *sQd = sEW + SROWS + 2;       // q^dagger  (U1_q / R_q before phase 1)
+    double *sHd = sQd + SROWS;           // H^dagger  (U1_K / R_H before phase 1)
+    double *sWd = sHd + SROWS;           // W^dagger  (U1_W / R_W before phase 1)
+    double *sBe = sWd + SROWS;           // beta
+    double *sDe = sBe + SROWS;           // delta
+    double *sHR = sDe + SROWS;           // h^R (+ hydrostatic term) (U1_h before)
 
     double umax_loc = 0.0, numax_loc = 0.0;
     unsigned int errbits = 0u;
@@ -250,36 +277,51 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
             }
         }
     } else {
-        // ---- load: E on rows -3..L+2, R on rows -1..L -----------------------
-        const double wE = P.wE, wR = P.wR;
+        // ---- load: raw rows -3..L+2 of U^n (and U1) by cp.async ----------------
+        // (all copies in flight at once; one wait) then an in-place pass forms
+        // E, R, H = K - 1.5 h b (A9) and the wall parity of q.
         for (int idx = tid; idx < L + 6; idx += NT) {
-            const int r = idx - 3;
             double par;
-            const int c = map_cell(start + r, n, P.bcl, P.bcr, par);
+            const int c = map_cell(start + idx - 3, n, P.bcl, P.bcr, par);
             const size_t gi = mo + c;
-            const double bb = BATHY ? __ldg(P.b + c) : 0.0;
-            double eh = B.Un[0][gi], eq = par * B.Un[1][gi], eK = B.Un[2][gi], eW = B.Un[3][gi];
-            double rh = eh, rq = eq, rK = eK, rW = eW;
+            cp_async8(sEh + idx, B.Un[0] + gi);
+            cp_async8(sEq + idx, B.Un[1] + gi);
+            cp_async8(sEH + idx, B.Un[2] + gi);
+            cp_async8(sEW + idx, B.Un[3] + gi);
             if (STAGE2) {
-                const double h1 = B.U1[0][gi], q1 = par * B.U1[1][gi], K1 = B.U1[2][gi],
-                             W1 = B.U1[3][gi];
-                // efficient form
-                rh = (1.0 - wR) * eh + wR * h1; rq = (1.0 - wR) * eq + wR * q1;
-                rK = (1.0 - wR) * eK + wR * K1; rW = (1.0 - wR) * eW + wR * W1;
-                eh = (1.0 - wE) * eh + wE * h1; eq = (1.0 - wE) * eq + wE * q1;
-                eK = (1.0 - wE) * eK + wE * K1; eW = (1.0 - wE) * eW + wE * W1;
-            }
-            sEh[idx] = eh; sEq[idx] = eq;
-            sEH[idx] = BATHY ? eK - 1.5 * eh * bb : eK;   // H = K - 1.5 h b (A9)
-            sEW[idx] = eW;
-            if (r >= -1 && r <= L) {
-                const int p = r + 1;
-                sHR[p] = rh; sQd[p] = rq;
-                sHd[p] = BATHY ? rK - 1.5 * rh * bb : rK;
-                sWd[p] = rW;
+                cp_async8(sHR + idx - 2, B.U1[0] + gi);
+                cp_async8(sQd + idx - 2, B.U1[1] + gi);
+                cp_async8(sHd + idx - 2, B.U1[2] + gi);
+                cp_async8(sWd + idx - 2, B.U1[3] + gi);
             }
         }
+        cp_async_wait_all();
         __syncthreads();
+        const bool wall_ghosts = (left_phys && P.bcl == BC_WALL) || (right_phys && P.bcr == BC_WALL);
+        if (STAGE2 || BATHY || wall_ghosts) {
+            const double wE = P.wE, wR = P.wR;
+            for (int idx = tid; idx < L + 6; idx += NT) {
+                double par;
+                const int c = map_cell(start + idx - 3, n, P.bcl, P.bcr, par);
+                const double bb = BATHY ? __ldg(P.b + c) : 0.0;
+                double eh = sEh[idx], eq = par * sEq[idx], eK = sEH[idx], eW = sEW[idx];
+                if (STAGE2) {
+                    const double h1 = sHR[idx - 2], q1 = par * sQd[idx - 2], K1 = sHd[idx - 2],
+                                 W1 = sWd[idx - 2];
+                    const double rh = (1.0 - wR) * eh + wR * h1, rq = (1.0 - wR) * eq + wR * q1;
+                    const double rK = (1.0 - wR) * eK + wR * K1, rW = (1.0 - wR) * eW + wR * W1;
+                    sHR[idx - 2] = rh; sQd[idx - 2] = rq;
+                    sHd[idx - 2] = BATHY ? rK - 1.5 * rh * bb : rK;
+                    sWd[idx - 2] = rW;
+                    eh = (1.0 - wE) * eh + wE * h1; eq = (1.0 - wE) * eq + wE * q1;
+                    eK = (1.0 - wE) * eK + wE * K1; eW = (1.0 - wE) * eW + wE * W1;
+                }
+                sEh[idx] = eh; sEq[idx] = eq;
+                sEH[idx] = BATHY ? eK - 1.5 * eh * bb : eK;   // H = K - 1.5 h b (A9)
+                sEW[idx] = eW;
+            }
+            __syncthreads();
+        }
 
         // ---- phase 1: faces, predictor, coefficients (chunk rows) -------------
         {
@@ -310,7 +352,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                     const Face Fr = face_flux(wh, wq, wH, wW, P.order);
                     const int p = r + 1;
                     const double hE = wh[1], qE = wq[1], HE = wH[1];
-                    const double hR = sHR[p], qR = sQd[p], HR = sHd[p], WR = sWd[p];
+                    // R = E in stage 1; stage 2 combined it on load
+                    const double hR = STAGE2 ? sHR[p] : hE, qR = STAGE2 ? sQd[p] : qE;
+                    const double HR = STAGE2 ? sHd[p] : HE, WR = STAGE2 ? sWd[p] : wW[1];
                     double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
                     if (BATHY) {
                         const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
@@ -320,7 +364,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                         // hydrostatic term in zeta-form (A9)
                         const double Gr = g * (hE + wh[2]) * 0.5, Gl = g * (wh[0] + hE) * 0.5;
                         hRp = hR + (tau * tau / (dx * dx)) * (Gr * (bp - b0) - Gl * (b0 - bm));
-                        const double sgE = HE / hE / hE;
+                        const double ih = rcp(hE);
+                        const double sgE = HE * ih * ih;
                         ptil_term = 1.5 * tau * (lam / 3.0) * (1.0 - sgE) * Dxb;   // p~
                     }
                     // predictor
@@ -328,13 +373,14 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                     const double Hd = HR - tdx * (Fr.H - Fl.H) - 1.5 * tau * qE * Dxb + tau * Wd;
                     const double qd = qR - tdx * (Fr.q - Fl.q) - ptil_term;
                     // coefficients at E (A2)
-                    const double sg = HE / hE / hE;
-                    const double alpha = -(2.0 * sg - 1.0) / (3.0 * hE);
-                    const double a2 = g * hE + (lam / 3.0) * sg * (3.0 * sg - 1.0);
-                    const double ih2 = 1.0 / (hE * hE);
-                    const double beta1 = 1.0 + lt2 * ih2;
-                    const double ib1 = 1.0 / beta1;
-                    const double beta2 = 2.0 * lt2 * ib1 * ib1 * ih2 / hE;
+                    const double ihE = rcp(hE);
+                    const double ih2 = ihE * ihE;
+                    const double sg = HE * ih2;                                  // eta/h
+                    const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
+                    const double a2 = g * hE + (lam / 3.0) * sg * (3.0 * sg - 1.0);  // P:142
+                    const double beta1 = 1.0 + lt2 * ih2;                        // P:505
+                    const double ib1 = rcp(beta1);
+                    const double beta2 = 2.0 * lt2 * ib1 * ib1 * ih2 * ihE;
                     const double beta = a2 + lam * alpha * beta2 * Hd;
                     const double delta = alpha * ib1;
                     if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
@@ -384,10 +430,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                     rho_loc = fmax(rho_loc, rr);
                 }
                 if (i == 0) {
-                    const double inv = 1.0 / dg;
+                    const double inv = rcp(dg);
                     am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
                 } else {
-                    const double inv = 1.0 / (dg - a * cm[i - 1]);
+                    const double inv = rcp(dg - a * cm[i - 1]);
                     am[i] = -a * am[i - 1] * inv;
                     cm[i] = c * inv;
                     dm[i] = (rhs - a * dm[i - 1]) * inv;
@@ -422,25 +468,33 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
             double A_ = aE, Bd = 1.0 - cE * Q1, C_ = -cE * R1, D_ = dE - cE * P1;
             if (tid == 0) A_ = 0.0;
             // PCR over NT unknowns, double-buffered
+            // rows are stored normalised by their diagonal (A/B, C/B, D/B) so that
+            // each PCR step needs one reciprocal per row
             double *cur = pcr0, *nxt = pcr1;
-            cur[tid] = A_; cur[NT + tid] = Bd; cur[2 * NT + tid] = C_; cur[3 * NT + tid] = D_;
+            {
+                const double ib = rcp(Bd);
+                A_ *= ib; C_ *= ib; D_ *= ib;
+            }
+            cur[tid] = A_; cur[2 * NT + tid] = C_; cur[3 * NT + tid] = D_;
             __syncthreads();
 #pragma unroll 1
             for (int sd = 1; sd < NT; sd <<= 1) {
                 const int km = tid - sd, kp = tid + sd;
-                double Am = 0, Bm = 1, Cm = 0, Dm = 0, Ap = 0, Bp = 1, Cp = 0, Dp = 0;
-                if (km >= 0) { Am = cur[km]; Bm = cur[NT + km]; Cm = cur[2 * NT + km]; Dm = cur[3 * NT + km]; }
-                if (kp < NT) { Ap = cur[kp]; Bp = cur[NT + kp]; Cp = cur[2 * NT + kp]; Dp = cur[3 * NT + kp]; }
-                const double k1 = A_ / Bm, k2 = C_ / Bp;
-                const double An = -Am * k1, Cn = -Cp * k2;
-                const double Bn = Bd - Cm * k1 - Ap * k2;
-                const double Dn = D_ - Dm * k1 - Dp * k2;
-                A_ = An; Bd = Bn; C_ = Cn; D_ = Dn;
-                nxt[tid] = A_; nxt[NT + tid] = Bd; nxt[2 * NT + tid] = C_; nxt[3 * NT + tid] = D_;
+                double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
+                if (km >= 0) { Am = cur[km]; Cm = cur[2 * NT + km]; Dm = cur[3 * NT + km]; }
+                if (kp < NT) { Ap = cur[kp]; Cp = cur[2 * NT + kp]; Dp = cur[3 * NT + kp]; }
+                // row - A_ * row(km) - C_ * row(kp), then renormalise
+                const double Bn = 1.0 - A_ * Cm - C_ * Ap;
+                const double ib = rcp(Bn);
+                const double An = -A_ * Am * ib;
+                const double Cn = -C_ * Cp * ib;
+                const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
+                A_ = An; C_ = Cn; D_ = Dn;
+                nxt[tid] = A_; nxt[2 * NT + tid] = C_; nxt[3 * NT + tid] = D_;
                 __syncthreads();
                 double *tmp = cur; cur = nxt; nxt = tmp;
             }
-            const double Xk = D_ / Bd;
+            const double Xk = D_;
             cur[3 * NT + tid] = Xk;     // own slot; neighbours read after the barrier
             __syncthreads();
             const double XL = (tid > 0) ? cur[3 * NT + tid - 1] : 0.0;
@@ -486,8 +540,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                 bb = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
                 qb -= tau * g * sEh[r + 3] * (bp - bm) / (2.0 * dx);     // A9
             }
-            const double ihb2 = 1.0 / (hb * hb);
-            const double Hb = sHd[p] / (1.0 + lt2 * ihb2);
+            const double ihb = rcp(hb);
+            const double ihb2 = ihb * ihb;
+            const double Hb = sHd[p] * rcp(1.0 + lt2 * ihb2);
             const double Wb = sWd[p] - lam * tau * Hb * ihb2;
             const bool kept = (r >= wl && r < wl + Tk);
             if (kept) {
@@ -502,7 +557,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                 B.out[0][gi] = hb; B.out[1][gi] = qb; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
                 B.out[3][gi] = Wb;
                 if (FINAL) {
-                    const double u = qb / hb, sg = Hb * ihb2;
+                    const double u = qb * ihb, sg = Hb * ihb2;
                     umax_loc = fmax(umax_loc, fabs(u));
                     numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * hb + (lam / 3.0) * sg * sg));
                 }
@@ -532,7 +587,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                 const size_t gi = mo + (s + (r - wl));
                 B.out[0][gi] = hb; B.out[1][gi] = qf; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
                 B.out[3][gi] = wf;
-                const double u = qf / hb, sg = Hb / (hb * hb);
+                const double ihb = rcp(hb);
+                const double u = qf * ihb, sg = Hb * ihb * ihb;
                 umax_loc = fmax(umax_loc, fabs(u));
                 numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * hb + (lam / 3.0) * sg * sg));
                 if (!isfinite(qf) || !isfinite(wf)) errbits |= ERR_NONFINITE;
@@ -626,7 +682,7 @@ __global__ void __launch_bounds__(NT) reduce_kernel(const double *__restrict__ h
     }
     const double tot = sred[0];
     __syncthreads();
-    const double mnn = -block_max(-mn, red);
+    const double mnn = -block_max(-mn, red, -1e300);
     const double umm = block_max(um, red);
     const double nmm = block_max(nm, red);
     if (tid == 0) {

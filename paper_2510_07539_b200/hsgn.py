@@ -42,7 +42,7 @@ class Tableau(C.Structure):
 class Diag(C.Structure):
     _fields_ = [("mass", C.c_double), ("min_h", C.c_double), ("max_abs_u", C.c_double),
                 ("nu_max", C.c_double), ("t_min", C.c_double), ("t_max", C.c_double),
-                ("dt_last_min", C.c_double), ("dt_last_max", C.c_double),
+                ("dt_last_min", C.c_double), ("dt_last_max", C.c_double), ("rho_max", C.c_double),
                 ("steps", C.c_int64), ("error_bits", C.c_int32), ("pad_", C.c_int32)]
 
 
@@ -154,7 +154,8 @@ class Solver:
         self.n, self.members = int(n), int(members)
         self.dx = (x_max - x_min) / n
         self._torch = torch
-        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        # a dedicated non-default stream: CUDA graphs cannot capture the legacy stream
+        self.stream = stream if stream is not None else torch.cuda.Stream()
         d = Desc(n_cells=n, n_members=members, order=order, x_min=x_min, x_max=x_max,
                  bc_left=BC[bc[0]], bc_right=BC[bc[1]], tile_cells=tile_cells, overlap=overlap)
         h = C.c_void_p()
@@ -222,6 +223,7 @@ class Solver:
         arrs = [self._as_f64(a) for a in (h, q, K, W)]
         for a in arrs:
             assert a.size == self.n * self.members if isinstance(a, np.ndarray) else a.numel() == self.n * self.members
+        self.stream.wait_stream(self._torch.cuda.current_stream())
         self._chk(self.L.hsgn_set_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in arrs], t0))
 
     def get_state(self, device: bool = True):
@@ -229,6 +231,7 @@ class Solver:
         torch = self._torch
         if device:
             out = [torch.empty((self.members, self.n), dtype=torch.float64, device="cuda") for _ in range(4)]
+            self.stream.wait_stream(torch.cuda.current_stream())
         else:
             out = [np.empty((self.members, self.n)) for _ in range(4)]
         t = np.empty(self.members)

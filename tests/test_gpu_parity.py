@@ -64,7 +64,8 @@ def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, **okw):
     for i, m in enumerate(members):
         e = rel_err([h[m], q[m], K[m], Wf[m]], refs[i])
         worst = max(worst, e)
-        assert abs(t[m] - trefs[i]) <= 1e-12 * max(1.0, abs(trefs[i])), (m, t[m], trefs[i])
+        # t accumulates dt's computed from states that agree to ~tol
+        assert abs(t[m] - trefs[i]) <= max(tol, 1e-13) * max(1.0, abs(trefs[i])), (m, t[m], trefs[i])
     assert worst <= tol, worst
     return worst
 
@@ -94,6 +95,7 @@ def test_euler_tableau_first_order_step():
     w = W.random_smooth(1500, 2, seed=8, amp=0.05)
     hs = _hsgn()
     s = gpu_solver(w, tableau=hs.euler_tableau(), order=1, tile_cells=400)
+    assert s.geometry.overlap >= 100       # auto overlap follows tau = dt (rho ~ 4x larger)
     s.run_steps(5)
     compare(w, s, range(2), steps=5, order=1, tableau=O.euler_tableau(), tol=1e-10)
 
@@ -133,7 +135,7 @@ def test_mass_conservation_gpu():
         m0 = s.diagnostics()["mass"]
         s.run_steps(100)
         d = s.diagnostics()
-        assert d["steps"] == 100
+        assert d["steps"] == 100, d
         assert abs(d["mass"] - m0) <= 1e-13 * m0
 
 

@@ -1,0 +1,29 @@
+// Accuracy of rcp.approx.ftz.f64 + k Newton steps vs IEEE 1/x (dev tool).
+#include <cstdio>
+#include <cmath>
+#include <cuda_runtime.h>
+__global__ void k(const double* x, double* out, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v = x[i], r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+    double ref = 1.0 / v;
+    out[4 * i + 0] = fabs(r * v - 1.0);
+    double e = fma(-v, r, 1.0); double r1 = fma(r, e, r);
+    out[4 * i + 1] = fabs((r1 - ref) / ref);
+    e = fma(-v, r1, 1.0); double r2 = fma(r1, e, r1);
+    out[4 * i + 2] = fabs((r2 - ref) / ref);
+    e = fma(-v, r2, 1.0); double r3 = fma(r2, e, r2);
+    out[4 * i + 3] = fabs((r3 - ref) / ref);
+}
+int main() {
+    const int n = 1 << 20;
+    double *x, *o; cudaMallocManaged(&x, n * 8); cudaMallocManaged(&o, 4 * n * 8);
+    unsigned long long s = 88172645463325252ull;
+    for (int i = 0; i < n; i++) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; x[i] = 0.01 + 1000.0 * (double)(s >> 11) / 9007199254740992.0; }
+    k<<<n / 256, 256>>>(x, o, n); cudaDeviceSynchronize();
+    double m[4] = {0, 0, 0, 0};
+    for (int i = 0; i < n; i++) for (int j = 0; j < 4; j++) m[j] = fmax(m[j], o[4 * i + j]);
+    printf("approx rel err %.3e, 1 NR %.3e, 2 NR %.3e, 3 NR %.3e (ulp=%.3e)\n", m[0], m[1], m[2], m[3], ldexp(1.0, -52));
+    return 0;
+}

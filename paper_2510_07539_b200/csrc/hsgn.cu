@@ -55,6 +55,7 @@ struct hsgn_ctx {
     // host bookkeeping
     int cur = 0;                  // buffer index holding the state at device step `base_steps`
     long long host_steps = 0;     // steps enqueued since set_state
+    long long dev_steps = 0;      // committed device steps at the last reconcile
     Ctrl ctrl_host{0.0, 0.0};
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     long long launches = 0;
@@ -92,7 +93,7 @@ Params make_params(hsgn_ctx *c)
     Params P{};
     P.n = c->n; P.members = c->members; P.tiles = c->tiles; P.T = c->T; P.w = c->w;
     P.bcl = c->desc.bc_left; P.bcr = c->desc.bc_right; P.order = c->desc.order;
-    P.dx = c->dx; P.g = c->g; P.h_min = c->h_min; P.cfl = c->cfl; P.mcfl = c->mcfl;
+    P.dx = c->dx; P.idx = 1.0 / c->dx; P.g = c->g; P.h_min = c->h_min; P.cfl = c->cfl; P.mcfl = c->mcfl;
     P.aI1 = c->aI1; P.aI2 = c->aI2; P.wE = c->wE; P.wR = c->wR;
     P.filter_sigma = c->filter_sigma;
     P.b = c->bathy ? c->b : nullptr;
@@ -247,6 +248,7 @@ hsgn_status reconcile(hsgn_ctx *c, unsigned int *bits_out = nullptr)
     CUDA_TRY(c, cudaMemcpyAsync(&dsteps, c->steps, sizeof(dsteps), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (bits_out) *bits_out = bits;
+    c->dev_steps = dsteps;
     if (dsteps != c->host_steps) {
         // steps after the failing one did nothing: the committed state is in
         // the buffer reached after dsteps ping-pongs
@@ -342,8 +344,9 @@ size_t hsgn_workspace_bytes(const hsgn_ctx *c)
     size_t s = 0;
     s += 12 * align256(N * sizeof(double));                 // 3 buffers x 4 fields
     s += align256(size_t(c->n) * sizeof(double));           // b
-    s += 3 * align256(size_t(c->members) * sizeof(double)); // lam, t, dt
-    s += align256(4 * size_t(c->members) * 8);              // maxes
+    s += 2 * align256(size_t(c->members) * sizeof(double)); // lam, dt
+    s += align256(2 * size_t(c->members) * sizeof(double)); // t[2]
+    s += align256(6 * size_t(c->members) * 8);              // maxes[3][2]
     s += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));  // partials
     s += 256;                                               // scalars
     s += 256;                                               // ctrl
@@ -364,9 +367,9 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
         for (int k = 0; k < 4; k++) { c->buf[bi][k] = (double *)q; q += align256(N * sizeof(double)); }
     c->b = (double *)q; q += align256(size_t(c->n) * sizeof(double));
     c->lamd = (double *)q; q += align256(size_t(c->members) * sizeof(double));
-    c->t = (double *)q; q += align256(size_t(c->members) * sizeof(double));
+    c->t = (double *)q; q += align256(2 * size_t(c->members) * sizeof(double));
     c->dt = (double *)q; q += align256(size_t(c->members) * sizeof(double));
-    c->maxes = (unsigned long long *)q; q += align256(4 * size_t(c->members) * 8);
+    c->maxes = (unsigned long long *)q; q += align256(6 * size_t(c->members) * 8);
     c->partials = (double *)q; q += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));
     c->err = (unsigned int *)q;
     c->done = (unsigned int *)(q + 4);
@@ -472,8 +475,9 @@ hsgn_status hsgn_set_state(hsgn_ctx *c, const double *h, const double *q, const 
         CUDA_TRY(c, cudaMemcpyAsync(c->buf[0][k], src[k], N * sizeof(double), cudaMemcpyDefault, c->stream));
     std::vector<double> tv(c->members, t0);
     CUDA_TRY(c, cudaMemcpyAsync(c->t, tv.data(), c->members * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    c->dev_steps = 0;
     CUDA_TRY(c, cudaMemsetAsync(c->dt, 0, c->members * sizeof(double), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->maxes, 0, 4 * size_t(c->members) * 8, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->maxes, 0, 6 * size_t(c->members) * 8, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->err, 0, 32, c->stream));   // err, done, steps, rho_obs
     dim3 grid(c->tiles, c->members);
     reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[0][0], c->buf[0][1], c->buf[0][2],
@@ -497,7 +501,7 @@ hsgn_status hsgn_get_state(hsgn_ctx *c, double *h, double *q, double *K, double 
     for (int k = 0; k < 4; k++)
         if (dst[k])
             CUDA_TRY(c, cudaMemcpyAsync(dst[k], c->buf[c->cur][k], N * sizeof(double), cudaMemcpyDefault, c->stream));
-    if (t) CUDA_TRY(c, cudaMemcpyAsync(t, c->t, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (t) CUDA_TRY(c, cudaMemcpyAsync(t, c->t + (c->dev_steps & 1) * c->members, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return st;
 }
@@ -592,8 +596,8 @@ hsgn_status hsgn_advance_to(hsgn_ctx *c, double t_end, int64_t max_steps, int64_
     long long taken = 0;
     const long long s0 = c->host_steps;
     while (taken < max_steps) {
-        CUDA_TRY(c, cudaMemcpyAsync(tv.data(), c->t, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         st = reconcile(c);
+        CUDA_TRY(c, cudaMemcpy(tv.data(), c->t + (c->dev_steps & 1) * c->members, c->members * sizeof(double), cudaMemcpyDeviceToHost));
         if (st != HSGN_OK) break;
         bool all = true;
         for (double tm : tv) all &= !(tm < t_end);
@@ -627,7 +631,7 @@ hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
     std::vector<double> part(size_t(c->members) * c->tiles * 4), tv(c->members), dv(c->members);
     long long dsteps = 0;
     CUDA_TRY(c, cudaMemcpyAsync(part.data(), c->partials, part.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(tv.data(), c->t, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(tv.data(), c->t + (c->dev_steps & 1) * c->members, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(dv.data(), c->dt, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(&dsteps, c->steps, sizeof(dsteps), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));

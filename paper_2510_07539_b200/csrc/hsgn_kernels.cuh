@@ -48,15 +48,15 @@ struct Ctrl {            // device-resident run control (read by stage kernels)
 struct Params {
     int n, members, tiles, T, w;
     int bcl, bcr, order;
-    double dx, g, h_min;
+    double dx, idx, g, h_min;        // idx = 1/dx
     double cfl, mcfl;
     double aI1, aI2, wE, wR;
     double filter_sigma;
     const double *b;                 // [n] or nullptr
     const double *lam;               // [members]
-    double *t;                       // [members]
+    double *t;                       // [2][members], by step parity
     double *dt;                      // [members]
-    unsigned long long *maxes;       // [2 slots][2 kinds][members] (double bits)
+    unsigned long long *maxes;       // [3 slots][2 kinds][members] (double bits), step % 3
     unsigned int *err;
     long long *steps;
     unsigned int *done;
@@ -119,19 +119,32 @@ __device__ __forceinline__ double bathy_at(const double *__restrict__ b, int c, 
 
 // dt rule of P:613-617 (reading A7 for nu_max): dt_bar = CFL dx / nu_max; if
 // u_max dt_bar / dx > MCFL use MCFL dx / u_max.  Returns < 0 if undefined.
-__device__ __forceinline__ double dt_rule(double cfl, double mcfl, double dx, double umax,
-                                          double numax)
+__device__ __forceinline__ double dt_rule(double cfl, double mcfl, double dx, double idx,
+                                          double umax, double numax)
 {
     double d;
     if (cfl > 0.0) {
-        d = cfl * dx / numax;
-        if (mcfl > 0.0 && umax > 0.0 && umax * d / dx > mcfl) d = mcfl * dx / umax;
+        d = cfl * dx * rcp(numax);
+        if (mcfl > 0.0 && umax > 0.0 && umax * d * idx > mcfl) d = mcfl * dx * rcp(umax);
     } else if (mcfl > 0.0 && umax > 0.0) {
-        d = mcfl * dx / umax;
+        d = mcfl * dx * rcp(umax);
     } else {
         d = -1.0;
     }
     return d;
+}
+
+// sqrt(x), x > 0: MUFU.RSQ64H estimate, two Newton steps for 1/sqrt, one
+// residual correction of x * y (branch-free; <= 1 ulp from IEEE sqrt).
+__device__ __forceinline__ double fsqrt(double x)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    const double s = x * y;
+    return fma(fma(-s, s, x), 0.5 * y, s);
 }
 
 // Rusanov face flux (A4) from the 4-row window v0..v3 = rows f-1..f+2
@@ -194,11 +207,8 @@ template <bool STAGE2, bool FINAL, bool BATHY>
 __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs B)
 {
     extern __shared__ double smem[];
-    __shared__ double red[NT / 32 + 1];
+    __shared__ double red[2][NT / 32];
     __shared__ double xch[NT / 32][3];
-    __shared__ int s_last;
-
-    if (*((volatile unsigned int *)P.err)) return;
 
     const int tid = threadIdx.x;
     const int j = blockIdx.x;        // tile
@@ -218,33 +228,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     const bool left_phys = !periodic && (start == 0);
     const bool right_phys = !periodic && (start + L == n);
 
-    // ---- dt -------------------------------------------------------
-    const long long stepno = *((volatile long long *)P.steps);
-    const int slot = int(stepno & 1);
-    const int members = P.members;
-    double dtm;
-    if (!STAGE2) {
-        const double umax = __longlong_as_double((long long)P.maxes[(slot * 2 + 0) * members + m]);
-        const double numax = __longlong_as_double((long long)P.maxes[(slot * 2 + 1) * members + m]);
-        const double t_end = P.ctrl->t_end, dt_fixed = P.ctrl->dt_fixed;
-        dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, umax, numax);
-        const double tm = P.t[m];
-        if (t_end > 0.0) {
-            if (!(tm < t_end)) dtm = 0.0;
-            else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end (S:342)
-        }
-        if (!(dtm >= 0.0) || !isfinite(dtm)) {
-            if (tid == 0) atomicOr(P.err, ERR_DT);
-            return;
-        }
-        if (j == 0 && tid == 0) P.dt[m] = dtm;
-    } else {
-        dtm = P.dt[m];
-    }
-    const double lam = P.lam[m];
-    const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
-    const double dx = P.dx, g = P.g;
-
     double *sEh = smem;
     double *sEq = sEh + SROWS;
     double *sEH = sEq + SROWS;
@@ -259,8 +242,81 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     double *sDe = sBe + SROWS;           // delta
     double *sHR = sDe + SROWS;           // h^R (+ hydrostatic term) (U1_h before)
 
+    // ---- load: raw rows -3..L+2 of U^n (and U1) by cp.async -------------------
+    // Issued first so that the copies overlap the run-control reads below.
+    const bool interior = (start - 3 >= 0) && (start + L + 3 <= n);
+    if (interior) {
+        const size_t base = mo + (start - 3);
+        for (int idx = tid; idx < L + 6; idx += NT) {
+            const size_t gi = base + idx;
+            cp_async8(sEh + idx, B.Un[0] + gi); cp_async8(sEq + idx, B.Un[1] + gi);
+            cp_async8(sEH + idx, B.Un[2] + gi); cp_async8(sEW + idx, B.Un[3] + gi);
+            if (STAGE2) {
+                cp_async8(sHR + idx - 2, B.U1[0] + gi); cp_async8(sQd + idx - 2, B.U1[1] + gi);
+                cp_async8(sHd + idx - 2, B.U1[2] + gi); cp_async8(sWd + idx - 2, B.U1[3] + gi);
+            }
+        }
+    } else {
+        for (int idx = tid; idx < L + 6; idx += NT) {
+            double par;
+            const size_t gi = mo + map_cell(start + idx - 3, n, P.bcl, P.bcr, par);
+            cp_async8(sEh + idx, B.Un[0] + gi); cp_async8(sEq + idx, B.Un[1] + gi);
+            cp_async8(sEH + idx, B.Un[2] + gi); cp_async8(sEW + idx, B.Un[3] + gi);
+            if (STAGE2) {
+                cp_async8(sHR + idx - 2, B.U1[0] + gi); cp_async8(sQd + idx - 2, B.U1[1] + gi);
+                cp_async8(sHd + idx - 2, B.U1[2] + gi); cp_async8(sWd + idx - 2, B.U1[3] + gi);
+            }
+        }
+    }
+
+    // ---- run control and dt ---------------------------------------
+    const unsigned int err0 = *((volatile unsigned int *)P.err);
+    const long long stepno = *((volatile long long *)P.steps);
+    const int members = P.members;
+    const int slot_r = int(stepno % 3), slot_w = int((stepno + 1) % 3), slot_z = int((stepno + 2) % 3);
+    const double tm = P.t[int(stepno & 1) * members + m];
+    const double t_end = P.ctrl->t_end;
+    const double lam = P.lam[m];
+    double dtm;
+    if (!STAGE2) {
+        const double umax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 0) * members + m]);
+        const double numax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 1) * members + m]);
+        const double dt_fixed = P.ctrl->dt_fixed;
+        dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, P.idx, umax, numax);
+        if (t_end > 0.0) {
+            if (!(tm < t_end)) dtm = 0.0;
+            else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end (S:342)
+        }
+        if (!(dtm >= 0.0) || !isfinite(dtm)) {
+            cp_async_wait_all();
+            if (tid == 0) atomicOr(P.err, ERR_DT);
+            return;
+        }
+        if (j == 0 && tid == 0) {
+            P.dt[m] = dtm;
+            P.maxes[(slot_z * 2 + 0) * members + m] = 0ull;   // 3-slot rotation: free
+            P.maxes[(slot_z * 2 + 1) * members + m] = 0ull;   // the slot read last step
+        }
+    } else {
+        dtm = P.dt[m];
+    }
+    if (err0) { cp_async_wait_all(); return; }
+
+    const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
+    const double g = P.g, idx1 = P.idx;
+    const double tdx = tau * idx1;                  // tau / dx
+    const double tdx2 = 0.5 * tdx;                  // tau / (2 dx)
+    const double t2 = tdx * tdx;                    // tau^2 / dx^2
+    const double lt2 = lam * tau * tau;             // lambda tau^2
+    const double lt2h = 0.5 * lam * t2;             // lambda tau^2 / (2 dx^2)
+    const double ltdx2 = lam * tdx2;                // lambda tau / (2 dx)
+    const double lam3 = lam * (1.0 / 3.0);
+
     double umax_loc = 0.0, numax_loc = 0.0;
     unsigned int errbits = 0u;
+
+    cp_async_wait_all();
+    __syncthreads();
 
     if (dtm == 0.0) {
         // member already at t_end: carry the state (and its dt maxima)
@@ -270,39 +326,21 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
             B.out[0][mo + i] = h; B.out[1][mo + i] = q; B.out[2][mo + i] = K; B.out[3][mo + i] = W;
             if (FINAL) {
                 const double bb = BATHY ? __ldg(P.b + i) : 0.0;
-                const double H = K - 1.5 * h * bb;
-                const double u = q / h, sg = H / h / h;
+                const double ih = rcp(h);
+                const double u = q * ih, sg = (K - 1.5 * h * bb) * ih * ih;
                 umax_loc = fmax(umax_loc, fabs(u));
-                numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * h + (lam / 3.0) * sg * sg));
+                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h + lam3 * sg * sg));
             }
         }
     } else {
-        // ---- load: raw rows -3..L+2 of U^n (and U1) by cp.async ----------------
-        // (all copies in flight at once; one wait) then an in-place pass forms
-        // E, R, H = K - 1.5 h b (A9) and the wall parity of q.
-        for (int idx = tid; idx < L + 6; idx += NT) {
-            double par;
-            const int c = map_cell(start + idx - 3, n, P.bcl, P.bcr, par);
-            const size_t gi = mo + c;
-            cp_async8(sEh + idx, B.Un[0] + gi);
-            cp_async8(sEq + idx, B.Un[1] + gi);
-            cp_async8(sEH + idx, B.Un[2] + gi);
-            cp_async8(sEW + idx, B.Un[3] + gi);
-            if (STAGE2) {
-                cp_async8(sHR + idx - 2, B.U1[0] + gi);
-                cp_async8(sQd + idx - 2, B.U1[1] + gi);
-                cp_async8(sHd + idx - 2, B.U1[2] + gi);
-                cp_async8(sWd + idx - 2, B.U1[3] + gi);
-            }
-        }
-        cp_async_wait_all();
-        __syncthreads();
+        // ---- in-place pass: E, R, H = K - 1.5 h b (A9), wall parity
         const bool wall_ghosts = (left_phys && P.bcl == BC_WALL) || (right_phys && P.bcr == BC_WALL);
         if (STAGE2 || BATHY || wall_ghosts) {
             const double wE = P.wE, wR = P.wR;
             for (int idx = tid; idx < L + 6; idx += NT) {
-                double par;
-                const int c = map_cell(start + idx - 3, n, P.bcl, P.bcr, par);
+                double par = 1.0;
+                int c = start + idx - 3;
+                if (!interior) c = map_cell(c, n, P.bcl, P.bcr, par);
                 const double bb = BATHY ? __ldg(P.b + c) : 0.0;
                 double eh = sEh[idx], eq = par * sEq[idx], eK = sEH[idx], eW = sEW[idx];
                 if (STAGE2) {
@@ -317,7 +355,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                     eK = (1.0 - wE) * eK + wE * K1; eW = (1.0 - wE) * eW + wE * W1;
                 }
                 sEh[idx] = eh; sEq[idx] = eq;
-                sEH[idx] = BATHY ? eK - 1.5 * eh * bb : eK;   // H = K - 1.5 h b (A9)
+                sEH[idx] = BATHY ? eK - 1.5 * eh * bb : eK;
                 sEW[idx] = eW;
             }
             __syncthreads();
@@ -327,8 +365,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
         {
             const int p0 = tid * MCH;
             if (p0 < L + 2) {
-                const double tdx = tau / dx;
-                const double lt2 = lam * tau * tau;
                 double wh[4], wq[4], wH[4], wW[4];
                 const int r0 = p0 - 1;
 #pragma unroll
@@ -355,34 +391,32 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                     // R = E in stage 1; stage 2 combined it on load
                     const double hR = STAGE2 ? sHR[p] : hE, qR = STAGE2 ? sQd[p] : qE;
                     const double HR = STAGE2 ? sHd[p] : HE, WR = STAGE2 ? sWd[p] : wW[1];
+                    const double ihE = rcp(hE);
+                    const double ih2 = ihE * ihE;
+                    const double sg = HE * ih2;                                  // eta/h
                     double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
                     if (BATHY) {
                         const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
                         const double b0 = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
                         const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
-                        Dxb = (bp - bm) / (2.0 * dx);
+                        Dxb = (bp - bm) * (0.5 * idx1);
                         // hydrostatic term in zeta-form (A9)
                         const double Gr = g * (hE + wh[2]) * 0.5, Gl = g * (wh[0] + hE) * 0.5;
-                        hRp = hR + (tau * tau / (dx * dx)) * (Gr * (bp - b0) - Gl * (b0 - bm));
-                        const double ih = rcp(hE);
-                        const double sgE = HE * ih * ih;
-                        ptil_term = 1.5 * tau * (lam / 3.0) * (1.0 - sgE) * Dxb;   // p~
+                        hRp = hR + t2 * (Gr * (bp - b0) - Gl * (b0 - bm));
+                        ptil_term = 1.5 * tau * lam3 * (1.0 - sg) * Dxb;        // p~
                     }
                     // predictor
                     const double Wd = WR - tdx * (Fr.W - Fl.W) + lam * tau;
                     const double Hd = HR - tdx * (Fr.H - Fl.H) - 1.5 * tau * qE * Dxb + tau * Wd;
                     const double qd = qR - tdx * (Fr.q - Fl.q) - ptil_term;
                     // coefficients at E (A2)
-                    const double ihE = rcp(hE);
-                    const double ih2 = ihE * ihE;
-                    const double sg = HE * ih2;                                  // eta/h
                     const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
-                    const double a2 = g * hE + (lam / 3.0) * sg * (3.0 * sg - 1.0);
+                    const double a2 = g * hE + lam3 * sg * (3.0 * sg - 1.0);
                     const double beta1 = 1.0 + lt2 * ih2;
                     const double ib1 = rcp(beta1);
                     const double beta2 = 2.0 * lt2 * ib1 * ib1 * ih2 * ihE;
-                    const double beta = a2 + lam * alpha * beta2 * Hd;
-                    const double delta = alpha * ib1;
+                    const double beta = a2 + lam * alpha * beta2 * Hd;           // P:507
+                    const double delta = alpha * ib1;                            // P:508
                     if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
                     sQd[p] = qd; sHd[p] = Hd; sWd[p] = Wd; sBe[p] = beta; sDe[p] = delta;
                     sHR[p] = hRp;
@@ -404,28 +438,28 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
 
         // ---- phase 2: assemble + partition solve (A1, A3) ---------
         double *sHB = sEq;            // hbar[r], r in [0, L)
-        double *pcr0 = sEH;           // PCR buffers: 2 x 4 x NT doubles over sEH..sEW
-        double *pcr1 = sEH + 4 * NT;
+        double *pcr0 = sEH;           // PCR buffers: 2 x 3 x NT doubles over sEH..sEW
+        double *pcr1 = sEH + 3 * NT;
         double rho_loc = 0.0;
         {
-            const double t2 = tau * tau / (dx * dx);
-            const double lt2h = lam * tau * tau / (2.0 * dx * dx);
-            const double tdx2 = tau / (2.0 * dx);
             const int r0 = tid * MCH;
+            // register windows over p = r0 .. r0+MCH+1 (rows r0-1 .. r0+MCH)
+            double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
+#pragma unroll
+            for (int k = 0; k < MCH + 2; k++) {
+                vb[k] = sBe[r0 + k]; vd[k] = sDe[r0 + k]; vH[k] = sHd[r0 + k]; vq[k] = sQd[r0 + k];
+            }
             double am[MCH], cm[MCH], dm[MCH];
 #pragma unroll
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
                 double a = 0.0, c = 0.0, dg = 1.0, rhs = 0.0;
                 if (r < L) {
-                    const int p = r + 1;
-                    const double bl = sBe[p - 1], bc = sBe[p], br = sBe[p + 1];
-                    const double rl = (r == 0) ? 0.0 : t2 * (bl + bc) * 0.5;
-                    const double rr = (r == L - 1) ? 0.0 : t2 * (bc + br) * 0.5;
-                    const double dl = sDe[p - 1], dc = sDe[p], dr = sDe[p + 1];
-                    const double ml = lt2h * (dl + dc), mr = lt2h * (dc + dr);
-                    const double Hl = sHd[p - 1], Hc = sHd[p], Hr = sHd[p + 1];
-                    rhs = sHR[p] - tdx2 * (sQd[p + 1] - sQd[p - 1]) + mr * (Hr - Hc) - ml * (Hc - Hl);
+                    const double rl = (r == 0) ? 0.0 : t2 * (vb[i] + vb[i + 1]) * 0.5;
+                    const double rr = (r == L - 1) ? 0.0 : t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
+                    const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
+                    rhs = sHR[r + 1] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
+                          - ml * (vH[i + 1] - vH[i]);
                     a = -rl; c = -rr; dg = 1.0 + rl + rr;
                     rho_loc = fmax(rho_loc, rr);
                 }
@@ -458,46 +492,42 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
             double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
             if (lane == 0) { xch[wid][0] = dm[0]; xch[wid][1] = am[0]; xch[wid][2] = cm[0]; }
             rho_loc = warp_max(rho_loc);
-            if (lane == 0) red[wid] = rho_loc;
+            if (lane == 0) red[0][wid] = rho_loc;
             __syncthreads();
             if (lane == 31) {
                 if (wid + 1 < NT / 32) { P1 = xch[wid + 1][0]; Q1 = xch[wid + 1][1]; R1 = xch[wid + 1][2]; }
                 else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
             }
-            // reduced row k:  A X_{k-1} + Bd X_k + C X_{k+1} = D
-            double A_ = aE, Bd = 1.0 - cE * Q1, C_ = -cE * R1, D_ = dE - cE * P1;
+            // reduced row k:  A X_{k-1} + Bd X_k + C X_{k+1} = D, normalised by Bd
+            double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1;
             if (tid == 0) A_ = 0.0;
-            // PCR over NT unknowns, double-buffered
-            // rows are stored normalised by their diagonal (A/B, C/B, D/B) so that
-            // each PCR step needs one reciprocal per row
-            double *cur = pcr0, *nxt = pcr1;
             {
-                const double ib = rcp(Bd);
+                const double ib = rcp(1.0 - cE * Q1);
                 A_ *= ib; C_ *= ib; D_ *= ib;
             }
-            cur[tid] = A_; cur[2 * NT + tid] = C_; cur[3 * NT + tid] = D_;
+            // PCR over NT unknowns, double-buffered, one reciprocal per row and step
+            double *cur = pcr0, *nxt = pcr1;
+            cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
             __syncthreads();
 #pragma unroll 1
             for (int sd = 1; sd < NT; sd <<= 1) {
                 const int km = tid - sd, kp = tid + sd;
                 double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
-                if (km >= 0) { Am = cur[km]; Cm = cur[2 * NT + km]; Dm = cur[3 * NT + km]; }
-                if (kp < NT) { Ap = cur[kp]; Cp = cur[2 * NT + kp]; Dp = cur[3 * NT + kp]; }
-                // row - A_ * row(km) - C_ * row(kp), then renormalise
-                const double Bn = 1.0 - A_ * Cm - C_ * Ap;
-                const double ib = rcp(Bn);
+                if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
+                if (kp < NT) { Ap = cur[kp]; Cp = cur[NT + kp]; Dp = cur[2 * NT + kp]; }
+                const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
                 const double An = -A_ * Am * ib;
                 const double Cn = -C_ * Cp * ib;
                 const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
                 A_ = An; C_ = Cn; D_ = Dn;
-                nxt[tid] = A_; nxt[2 * NT + tid] = C_; nxt[3 * NT + tid] = D_;
+                nxt[tid] = A_; nxt[NT + tid] = C_; nxt[2 * NT + tid] = D_;
                 __syncthreads();
                 double *tmp = cur; cur = nxt; nxt = tmp;
             }
             const double Xk = D_;
-            cur[3 * NT + tid] = Xk;     // own slot; neighbours read after the barrier
+            cur[2 * NT + tid] = Xk;     // own slot; neighbours read after the barrier
             __syncthreads();
-            const double XL = (tid > 0) ? cur[3 * NT + tid - 1] : 0.0;
+            const double XL = (tid > 0) ? cur[2 * NT + tid - 1] : 0.0;
 #pragma unroll
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
@@ -506,7 +536,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
             }
             if (tid == 0) {
                 double rmax = 0.0;
-                for (int q = 0; q < NT / 32; q++) rmax = fmax(rmax, red[q]);
+                for (int q = 0; q < NT / 32; q++) rmax = fmax(rmax, red[0][q]);
                 // overlap check: r^w <= 2^-60 at every truncated end
                 if (rmax > 0.0) {
                     const double rdec = 2.0 * rmax / ((1.0 + 2.0 * rmax) + sqrt(1.0 + 4.0 * rmax));
@@ -520,11 +550,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
         __syncthreads();
 
         // ---- phase 3: back-substitution ---------------------------
-        const double tdx2 = tau / (2.0 * dx);
-        const double ltdx2 = lam * tau / (2.0 * dx);
-        const double lt2 = lam * tau * tau;
         const bool filt = FINAL && (P.filter_sigma > 0.0);
-        double *sQb = sEH, *sWb = sEW, *sHb = sHR;   // filter scratch (rows r)
+        double *sQb = sEH, *sWb = sEW, *sHb = sHR - 2;   // filter scratch (rows r)
         const int rbeg = filt ? max(0, wl - 2) : wl;
         const int rend = filt ? min(L, wl + Tk + 2) : wl + Tk;
         for (int r = rbeg + tid; r < rend; r += NT) {
@@ -538,7 +565,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                 const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
                 const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
                 bb = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
-                qb -= tau * g * sEh[r + 3] * (bp - bm) / (2.0 * dx);     // A9
+                qb -= tau * g * sEh[r + 3] * (bp - bm) * (0.5 * idx1);     // A9
             }
             const double ihb = rcp(hb);
             const double ihb2 = ihb * ihb;
@@ -559,27 +586,34 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                 if (FINAL) {
                     const double u = qb * ihb, sg = Hb * ihb2;
                     umax_loc = fmax(umax_loc, fabs(u));
-                    numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * hb + (lam / 3.0) * sg * sg));
+                    numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * hb + lam3 * sg * sg));
                 }
             }
         }
         if (filt) {
             __syncthreads();
-            const double sig16 = P.filter_sigma / 16.0;
+            const double sig16 = P.filter_sigma * (1.0 / 16.0);
+            const bool edge_tile = left_phys || right_phys;
             for (int r = wl + tid; r < wl + Tk; r += NT) {
                 double fq[5], fw[5];
+                if (!edge_tile || (r >= 2 && r + 2 < L)) {
 #pragma unroll
-                for (int k = -2; k <= 2; k++) {
-                    int rr = r + k;
-                    double pq = 1.0;
-                    if (rr < 0) {            // only at a physical left boundary
-                        if (P.bcl == BC_WALL) { rr = -1 - rr; pq = -1.0; } else rr = 0;
-                    } else if (rr >= L) {    // only at a physical right boundary
-                        if (P.bcr == BC_WALL) { rr = 2 * L - 1 - rr; pq = -1.0; } else rr = L - 1;
+                    for (int k = 0; k < 5; k++) { fq[k] = sQb[r + k - 2]; fw[k] = sWb[r + k - 2]; }
+                } else {
+#pragma unroll
+                    for (int k = -2; k <= 2; k++) {
+                        int rr = r + k;
+                        double pq = 1.0;
+                        if (rr < 0) {            // only at a physical left boundary
+                            if (P.bcl == BC_WALL) { rr = -1 - rr; pq = -1.0; } else rr = 0;
+                        } else if (rr >= L) {    // only at a physical right boundary
+                            if (P.bcr == BC_WALL) { rr = 2 * L - 1 - rr; pq = -1.0; } else rr = L - 1;
+                        }
+                        fq[k + 2] = pq * sQb[rr];
+                        fw[k + 2] = sWb[rr];
                     }
-                    fq[k + 2] = pq * sQb[rr];
-                    fw[k + 2] = sWb[rr];
                 }
+                // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
                 const double qf = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
                 const double wf = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
                 const double hb = sHB[r], Hb = sHb[r];
@@ -590,7 +624,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
                 const double ihb = rcp(hb);
                 const double u = qf * ihb, sg = Hb * ihb * ihb;
                 umax_loc = fmax(umax_loc, fabs(u));
-                numax_loc = fmax(numax_loc, fabs(u) + sqrt(g * hb + (lam / 3.0) * sg * sg));
+                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * hb + lam3 * sg * sg));
                 if (!isfinite(qf) || !isfinite(wf)) errbits |= ERR_NONFINITE;
             }
         }
@@ -606,37 +640,26 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
 
     if (FINAL) {
         // ---- dt maxima for the next step -----------------------------
-        const double um = block_max(umax_loc, red);
-        const double nm = block_max(numax_loc, red);
-        const int nslot = slot ^ 1;
-        if (tid == 0) {
-            atomicMax(P.maxes + (nslot * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
-            atomicMax(P.maxes + (nslot * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
-        }
-        // ---- commit by the last CTA ----------------------------------------------
+        double um = warp_max(umax_loc), nm = warp_max(numax_loc);
+        const int lane = tid & 31, wid = tid >> 5;
+        __syncthreads();
+        if (lane == 0) { red[0][wid] = um; red[1][wid] = nm; }
         __syncthreads();
         if (tid == 0) {
+            for (int q = 1; q < NT / 32; q++) { um = fmax(um, red[0][q]); nm = fmax(nm, red[1][q]); }
+            atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
+            atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
+            if (j == 0) {   // next time level of this member (double-buffered by step parity)
+                P.t[int((stepno + 1) & 1) * members + m] =
+                    (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
+            }
+            // ---- commit by the last CTA: O(1) ----------------------------------------
             __threadfence();
             const unsigned int total = gridDim.x * gridDim.y;
             const unsigned int prev = atomicAdd(P.done, 1u);
-            s_last = (prev == total - 1) ? 1 : 0;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            const bool ok = (*((volatile unsigned int *)P.err) == 0u);
-            const double t_end = P.ctrl->t_end;
-            if (ok) {
-                for (int mm = tid; mm < members; mm += NT) {
-                    const double tm = P.t[mm], d = P.dt[mm];
-                    P.t[mm] = (t_end > 0.0 && d == t_end - tm) ? t_end : tm + d;
-                    P.maxes[(slot * 2 + 0) * members + mm] = 0ull;
-                    P.maxes[(slot * 2 + 1) * members + mm] = 0ull;
-                }
-            }
-            __syncthreads();
-            if (tid == 0) {
-                if (ok) *P.steps = stepno + 1;
+            if (prev == total - 1) {
+                __threadfence();
+                if (*((volatile unsigned int *)P.err) == 0u) *P.steps = stepno + 1;
                 *P.done = 0u;
             }
         }

@@ -1,0 +1,80 @@
+"""Attribute ncu SASS-level stall samples to CUDA source lines (dev tool).
+
+    python tools/ncu_lines.py gpurun_out/prof.ncu-rep paper_2510_07539_b200/lib/libhsgn.so
+
+Uses nvdisasm line info (-lineinfo builds) to map each SASS offset to a line of
+hsgn_kernels.cuh, then sums 'Warp Stall Sampling (All Samples)' per line."""
+import collections
+import csv
+import io
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+
+def sass_lines(so):
+    d = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=d, capture_output=True, check=True)
+    cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".cubin")][0]
+    out = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+    funcs = {}
+    cur = None
+    line = None
+    for ln in out.splitlines():
+        m = re.match(r"\s*\.text\.(\S+):", ln)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = {}
+            continue
+        m = re.search(r'//## File ".*?/([^/"]+)", line (\d+)', ln)
+        if m:
+            line = (m.group(1), int(m.group(2)))
+            continue
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if m and cur is not None and line is not None:
+            funcs[cur][int(m.group(1), 16)] = line
+    return funcs
+
+
+def main(rep, so):
+    funcs = sass_lines(so)
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    blocks = txt.split('"Kernel Name"')[1:]
+    for b in blocks:
+        name = b.split("\n", 1)[0]
+        rows = list(csv.reader(io.StringIO(b.split("\n", 1)[1])))
+        hdr = rows[0]
+        ia, iss, iex = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
+        base = int(rows[1][ia], 16)
+        # pick the mangled function whose size matches
+        n = len(rows) - 1
+        cand = [f for f, m in funcs.items() if abs(len(m) - n) <= 2 and "stage_kernel" in f]
+        key = None
+        tag = re.findall(r"<\(bool\)(\d), \(bool\)(\d), \(bool\)(\d)>", name)
+        if tag:
+            t = "".join("ILb%sE" % x for x in tag[0])
+            for f in funcs:
+                if t in f:
+                    key = f
+        if key is None and cand:
+            key = cand[0]
+        agg = collections.Counter()
+        inst = collections.Counter()
+        tot = 0
+        for r in rows[1:]:
+            off = int(r[ia], 16) - base
+            li = funcs.get(key, {}).get(off, ("?", 0))
+            s = int(r[iss] or 0)
+            agg[li] += s
+            inst[li] += int(r[iex] or 0)
+            tot += s
+        print("=== %s  (%s) total samples %d" % (name[:60], key, tot))
+        for li, s in agg.most_common(int(os.environ.get("TOPN", "40"))):
+            print("%6.2f%%  %-22s line %4d   inst %d" % (100.0 * s / max(tot, 1), li[0], li[1], inst[li]))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])

@@ -16,7 +16,7 @@ __global__ void k(const double* x, double* out, int n) {
     e = fma(-v, r2, 1.0); double r3 = fma(r2, e, r2);
     out[4 * i + 3] = fabs((r3 - ref) / ref);
 }
-int main() {
+int main1() {
     const int n = 1 << 20;
     double *x, *o; cudaMallocManaged(&x, n * 8); cudaMallocManaged(&o, 4 * n * 8);
     unsigned long long s = 88172645463325252ull;
@@ -27,3 +27,27 @@ int main() {
     printf("approx rel err %.3e, 1 NR %.3e, 2 NR %.3e, 3 NR %.3e (ulp=%.3e)\n", m[0], m[1], m[2], m[3], ldexp(1.0, -52));
     return 0;
 }
+// (appended) fsqrt accuracy check
+__global__ void ks(const double* x, double* out, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v = x[i], y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+    const double hx = 0.5 * v;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    const double s = v * y;
+    const double r = fma(fma(-s, s, v), 0.5 * y, s);
+    out[i] = fabs(r - sqrt(v)) / sqrt(v);
+}
+int main2() {
+    const int n = 1 << 20;
+    double *x, *o; cudaMallocManaged(&x, n * 8); cudaMallocManaged(&o, n * 8);
+    unsigned long long s = 88172645463325252ull;
+    for (int i = 0; i < n; i++) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; x[i] = 1e-3 + 1e5 * (double)(s >> 11) / 9007199254740992.0; }
+    ks<<<n / 256, 256>>>(x, o, n); cudaDeviceSynchronize();
+    double m = 0; for (int i = 0; i < n; i++) m = fmax(m, o[i]);
+    printf("fsqrt max rel err %.3e\n", m);
+    return 0;
+}
+int main() { main1(); return main2(); }

@@ -28,13 +28,14 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """defines: extra -D flags (tuning experiments, e.g. HSGN_NT=128)."""
+    if out == LIB and not force and not stale():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB, *SRC, "-cudart", "static"]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SRC, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(os.path.dirname(LIB), "ptxas.log")
+    log = out + ".ptxas.log"
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
@@ -42,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({r.returncode}); see {log}")
     if verbose:
         sys.stdout.write(r.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -28,12 +28,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef HSGN_NT
+#define HSGN_NT 128
+#endif
+#ifndef HSGN_MINB
+#define HSGN_MINB 4
+#endif
+
 namespace hsgn {
 
-constexpr int NT = 256;             // threads per CTA
+constexpr int NT = HSGN_NT;           // threads per CTA
 constexpr int MCH = 5;              // rows per thread chunk (odd: conflict-free strided smem)
 constexpr int LCAP = NT * MCH;      // 1280 rows per CTA incl. phase-1 halo rows
-constexpr int SROWS = LCAP + 6;     // smem row capacity per array
+constexpr int SROWS = LCAP + 8;     // smem row capacity per array (even: 16-B aligned bases)
 constexpr int NARR = 10;            // smem arrays
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
 
@@ -92,6 +99,31 @@ __device__ __forceinline__ void cp_async8(double *dst_smem, const double *src)
 __device__ __forceinline__ void cp_async_wait_all()
 {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// TMA bulk copy global -> shared (16-B aligned, size a multiple of 16),
+// completion signalled on the mbarrier at shared address mbar.
+__device__ __forceinline__ void bulk_g2s(double *dst_smem, const double *src, unsigned bytes,
+                                         unsigned mbar)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(dst_smem);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(a), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(mbar), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void drain_loads(bool bulk, unsigned mbar)
+{
+    if (bulk) { __syncthreads(); mbar_wait(mbar, 0); }
+    else cp_async_wait_all();
 }
 
 __device__ __forceinline__ int map_cell(int c, int n, int bcl, int bcr, double &par)
@@ -204,9 +236,10 @@ __device__ __forceinline__ double block_max(double v, double *red, double ident 
 // FINAL: this stage produces U^{n+1} (filter, dt maxima, commit).
 // ---------------------------------------------------------------------------
 template <bool STAGE2, bool FINAL, bool BATHY>
-__global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs B)
+__global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
 {
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(8) unsigned long long s_mbar;
     __shared__ double red[2][NT / 32];
     __shared__ double xch[NT / 32][3];
 
@@ -228,13 +261,24 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     const bool left_phys = !periodic && (start == 0);
     const bool right_phys = !periodic && (start + L == n);
 
-    double *sEh = smem;
-    double *sEq = sEh + SROWS;
-    double *sEH = sEq + SROWS;
-    double *sEW = sEH + SROWS;
+    // ---- load: raw rows -3..L+2 of U^n (and U1) into shared memory ----------
+    // Interior tiles: one TMA bulk copy per field (cp.async.bulk, 16-B aligned
+    // by shifting the smem arrays by d = parity of the first global cell).
+    // Wrapping / wall tiles: per-element cp.async through the BC index map.
+    // Issued first so that the copies overlap the run-control reads below.
+    const bool interior = (start - 3 >= 0) && (start + L + 3 <= n);
+    const int d = interior ? int((mo + size_t(start - 3)) & 1) : 0;
+    const int a0 = start - 3 - d;                       // first copied cell
+    const int cnt = (L + 6 + d + 1) & ~1;               // even count: 16-B multiple
+    const bool bulk = interior && (a0 >= 0) && (a0 + cnt <= n);
+
     // E arrays are indexed by idx = r + 3 (rows -3..L+2).  The phase-1 output
     // arrays are offset by 2 so that index p = r + 1 lands on the same physical
     // slot r + 3: the stage-2 raw copy of U1 and the R combination share it.
+    double *sEh = smem + d;
+    double *sEq = sEh + SROWS;
+    double *sEH = sEq + SROWS;
+    double *sEW = sEH + SROWS;
     double *sQd = sEW + SROWS + 2;       // q^dagger  (U1_q / R_q before phase 1)
     double *sHd = sQd + SROWS;           // H^dagger  (U1_K / R_H before phase 1)
     double *sWd = sHd + SROWS;           // W^dagger  (U1_W / R_W before phase 1)
@@ -242,18 +286,23 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     double *sDe = sBe + SROWS;           // delta
     double *sHR = sDe + SROWS;           // h^R (+ hydrostatic term) (U1_h before)
 
-    // ---- load: raw rows -3..L+2 of U^n (and U1) by cp.async -------------------
-    // Issued first so that the copies overlap the run-control reads below.
-    const bool interior = (start - 3 >= 0) && (start + L + 3 <= n);
-    if (interior) {
-        const size_t base = mo + (start - 3);
-        for (int idx = tid; idx < L + 6; idx += NT) {
-            const size_t gi = base + idx;
-            cp_async8(sEh + idx, B.Un[0] + gi); cp_async8(sEq + idx, B.Un[1] + gi);
-            cp_async8(sEH + idx, B.Un[2] + gi); cp_async8(sEW + idx, B.Un[3] + gi);
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+    if (bulk) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            const unsigned bytes = unsigned(cnt) * 8u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                         "r"(bytes * (STAGE2 ? 8u : 4u)) : "memory");
+            const size_t gsrc = mo + size_t(a0);
+#pragma unroll
+            for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
             if (STAGE2) {
-                cp_async8(sHR + idx - 2, B.U1[0] + gi); cp_async8(sQd + idx - 2, B.U1[1] + gi);
-                cp_async8(sHd + idx - 2, B.U1[2] + gi); cp_async8(sWd + idx - 2, B.U1[3] + gi);
+                // raw U1 into the R slots: h -> sHR, q -> sQd, K -> sHd, W -> sWd
+                bulk_g2s(smem + 9 * SROWS, B.U1[0] + gsrc, bytes, mb);
+                bulk_g2s(smem + 4 * SROWS, B.U1[1] + gsrc, bytes, mb);
+                bulk_g2s(smem + 5 * SROWS, B.U1[2] + gsrc, bytes, mb);
+                bulk_g2s(smem + 6 * SROWS, B.U1[3] + gsrc, bytes, mb);
             }
         }
     } else {
@@ -288,7 +337,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
             else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end
         }
         if (!(dtm >= 0.0) || !isfinite(dtm)) {
-            cp_async_wait_all();
+            drain_loads(bulk, mb);
             if (tid == 0) atomicOr(P.err, ERR_DT);
             return;
         }
@@ -300,7 +349,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     } else {
         dtm = P.dt[m];
     }
-    if (err0) { cp_async_wait_all(); return; }
+    if (err0) { drain_loads(bulk, mb); return; }
 
     const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
     const double g = P.g, idx1 = P.idx;
@@ -315,7 +364,12 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const Params P, const Bufs
     double umax_loc = 0.0, numax_loc = 0.0;
     unsigned int errbits = 0u;
 
-    cp_async_wait_all();
+    if (bulk) {
+        __syncthreads();                  // mbarrier initialised before anyone waits
+        mbar_wait(mb, 0);
+    } else {
+        cp_async_wait_all();
+    }
     __syncthreads();
 
     if (dtm == 0.0) {

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libhsgn.so")
+LIB_PATH = os.environ.get("HSGN_LIB") or os.path.join(_PKG, "lib", "libhsgn.so")
 
 BC = {"periodic": 0, "wall": 1, "transmissive": 2}
 STATUS = {0: "OK", -1: "E_INVALID", -2: "E_DRY", -3: "E_COERCIVITY", -4: "E_SINGULAR",

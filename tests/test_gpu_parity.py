@@ -76,7 +76,8 @@ def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, **okw):
 def test_one_step_ragged_tiles(bc, order):
     w = W.random_smooth(3000, 3, seed=21, amp=0.08, bc=(bc, bc))
     s = gpu_solver(w, tile_cells=700, overlap=64, order=order)
-    assert s.geometry.tiles_per_member == 5
+    g = s.geometry
+    assert g.tiles_per_member == -(-3000 // g.tile_cells) >= 5 and 3000 % g.tile_cells != 0  # ragged
     s.step()
     compare(w, s, range(3), steps=1, order=order)
 

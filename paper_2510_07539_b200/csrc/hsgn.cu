@@ -3,7 +3,9 @@
 // Host side: validates the problem, chooses the tile geometry, lays out the
 // caller-provided workspace, launches the stage kernels of
 // hsgn_kernels.cuh on the caller's stream, and replays CUDA graphs of
-// GRAPH_STEPS steps for hsgn_run_steps / hsgn_advance_to.  Never allocates
+// GRAPH_STEPS steps for hsgn_run_steps / hsgn_advance_to.  One step k =
+// stage 1, stage 2, dt_commit(k+1) (commit step k, dt of step k+1); every run
+// starts with dt_commit(k, no commit).  Never allocates
 // device memory and never falls back to the CPU.
 #include <cuda_runtime.h>
 
@@ -21,7 +23,8 @@ using namespace hsgn;
 
 namespace {
 
-constexpr int GRAPH_STEPS = 16;   // steps per captured graph (even: buffers ping-pong)
+constexpr int GRAPH_STEPS = 18;   // steps per captured graph: a multiple of 6, so the buffer
+                                  // parity (k mod 2) and the maxima slot (k mod 3) repeat
 constexpr int POLL_STEPS = 256;   // advance_to polls the device every POLL_STEPS
 constexpr int T_MIN = 64;         // smallest kept tile (bounds the partials workspace)
 
@@ -47,7 +50,8 @@ struct hsgn_ctx {
     char *ws = nullptr;
     size_t ws_bytes = 0;
     double *buf[3][4] = {};     // [A, B, U1][field]
-    double *b = nullptr, *lamd = nullptr, *t = nullptr, *dt = nullptr, *partials = nullptr;
+    double *b = nullptr, *lamd = nullptr, *t = nullptr, *dt = nullptr, *dt_used = nullptr,
+           *partials = nullptr;
     unsigned long long *maxes = nullptr, *rho_obs = nullptr;
     unsigned int *err = nullptr, *done = nullptr;
     long long *steps = nullptr;
@@ -88,9 +92,11 @@ hsgn_status status_from_bits(unsigned int bits)
     return HSGN_E_INVALID;
 }
 
-Params make_params(hsgn_ctx *c)
+Params make_params(hsgn_ctx *c, long long k)
 {
     Params P{};
+    P.kslot = int(k % 3);
+    P.kpar = int(k & 1);
     P.n = c->n; P.members = c->members; P.tiles = c->tiles; P.T = c->T; P.w = c->w;
     P.bcl = c->desc.bc_left; P.bcr = c->desc.bc_right; P.order = c->desc.order;
     P.dx = c->dx; P.idx = 1.0 / c->dx; P.g = c->g; P.h_min = c->h_min; P.cfl = c->cfl; P.mcfl = c->mcfl;
@@ -118,27 +124,51 @@ hsgn_status launch_stage_b(hsgn_ctx *c, const Params &P, const Bufs &B)
     return c->bathy ? launch_stage<S2, FIN, true>(c, P, B) : launch_stage<S2, FIN, false>(c, P, B);
 }
 
-// enqueue one step reading buf[cur], writing buf[cur ^ 1]
-hsgn_status enqueue_step(hsgn_ctx *c, int cur)
+hsgn_status launch_dtc(hsgn_ctx *c, long long k, int commit_prev, int compute_dt)
 {
-    const Params P = make_params(c);
+    const Params P = make_params(c, k);
+    dt_commit_kernel<<<(c->members + 127) / 128, 128, 0, c->stream>>>(P, commit_prev, compute_dt);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return HSGN_OK;
+}
+
+// Enqueue step k reading buf[cur], writing buf[cur ^ 1]: the stages, then the
+// commit of step k and the dt of step k+1.  ev (optional, 3 events) brackets
+// the stage kernels; dt_copy (optional, device) receives the dt step k used.
+hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nullptr,
+                         double *dt_copy = nullptr)
+{
+    const Params P = make_params(c, k);
     Bufs B{};
-    for (int k = 0; k < 4; k++) {
-        B.Un[k] = c->buf[cur][k];
-        B.U1[k] = c->buf[2][k];
+    for (int f = 0; f < 4; f++) {
+        B.Un[f] = c->buf[cur][f];
+        B.U1[f] = c->buf[2][f];
     }
     hsgn_status st;
+    if (ev) CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
     if (c->tab.stages == 1) {
-        for (int k = 0; k < 4; k++) B.out[k] = c->buf[cur ^ 1][k];
+        for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         st = launch_stage_b<false, true>(c, P, B);
+        if (st != HSGN_OK) return st;
+        if (ev) {
+            CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+        }
     } else {
-        for (int k = 0; k < 4; k++) B.out[k] = c->buf[2][k];
+        for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
         st = launch_stage_b<false, false>(c, P, B);
         if (st != HSGN_OK) return st;
-        for (int k = 0; k < 4; k++) B.out[k] = c->buf[cur ^ 1][k];
+        if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+        for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         st = launch_stage_b<true, true>(c, P, B);
+        if (st != HSGN_OK) return st;
+        if (ev) CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
     }
-    return st;
+    if (dt_copy)
+        CUDA_TRY(c, cudaMemcpyAsync(dt_copy, c->dt, c->members * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, c->stream));
+    return launch_dtc(c, k + 1, 1, 1);
 }
 
 void drop_graphs(hsgn_ctx *c)
@@ -204,18 +234,20 @@ hsgn_status ready(hsgn_ctx *c)
 
 hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
 {
+    if (n_steps <= 0) return HSGN_OK;
+    hsgn_status st = launch_dtc(c, c->host_steps, 0, 1);   // dt of the first step
+    if (st != HSGN_OK) return st;
     long long done = 0;
     while (done < n_steps) {
-        if (n_steps - done >= GRAPH_STEPS && c->stream != nullptr) {   // legacy stream: no capture
+        if (n_steps - done >= GRAPH_STEPS && c->stream != nullptr && c->host_steps % 6 == 0) {
             cudaGraphExec_t &gx = c->graph[c->cur];
             if (!gx) {
                 cudaGraph_t gr;
                 CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-                long long l0 = c->launches;
+                const long long l0 = c->launches;
                 int cc = c->cur;
-                hsgn_status st = HSGN_OK;
                 for (int k = 0; k < GRAPH_STEPS && st == HSGN_OK; k++) {
-                    st = enqueue_step(c, cc);
+                    st = enqueue_step(c, cc, c->host_steps + k);
                     cc ^= 1;
                 }
                 cudaError_t ce = cudaStreamEndCapture(c->stream, &gr);
@@ -226,16 +258,17 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
                 cudaGraphDestroy(gr);
             }
             CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
-            c->launches += GRAPH_STEPS * c->tab.stages;
-            done += GRAPH_STEPS;   // GRAPH_STEPS even: cur unchanged
+            c->launches += GRAPH_STEPS * (c->tab.stages + 1);
+            done += GRAPH_STEPS;          // even: cur unchanged
+            c->host_steps += GRAPH_STEPS;
         } else {
-            hsgn_status st = enqueue_step(c, c->cur);
+            st = enqueue_step(c, c->cur, c->host_steps);
             if (st != HSGN_OK) return st;
             c->cur ^= 1;
+            c->host_steps++;
             done++;
         }
     }
-    c->host_steps += n_steps;
     return HSGN_OK;
 }
 
@@ -344,7 +377,7 @@ size_t hsgn_workspace_bytes(const hsgn_ctx *c)
     size_t s = 0;
     s += 12 * align256(N * sizeof(double));                 // 3 buffers x 4 fields
     s += align256(size_t(c->n) * sizeof(double));           // b
-    s += 2 * align256(size_t(c->members) * sizeof(double)); // lam, dt
+    s += 3 * align256(size_t(c->members) * sizeof(double)); // lam, dt, dt_used
     s += align256(2 * size_t(c->members) * sizeof(double)); // t[2]
     s += align256(6 * size_t(c->members) * 8);              // maxes[3][2]
     s += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));  // partials
@@ -369,6 +402,7 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     c->lamd = (double *)q; q += align256(size_t(c->members) * sizeof(double));
     c->t = (double *)q; q += align256(2 * size_t(c->members) * sizeof(double));
     c->dt = (double *)q; q += align256(size_t(c->members) * sizeof(double));
+    c->dt_used = (double *)q; q += align256(size_t(c->members) * sizeof(double));
     c->maxes = (unsigned long long *)q; q += align256(6 * size_t(c->members) * 8);
     c->partials = (double *)q; q += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));
     c->err = (unsigned int *)q;
@@ -512,13 +546,15 @@ hsgn_status hsgn_step(hsgn_ctx *c, double dt, double *dt_used)
     if (st != HSGN_OK) return st;
     st = set_ctrl(c, c->ctrl_host.t_end, dt > 0.0 ? dt : 0.0);
     if (st != HSGN_OK) return st;
-    st = enqueue_step(c, c->cur);
+    st = launch_dtc(c, c->host_steps, 0, 1);
+    if (st != HSGN_OK) return st;
+    st = enqueue_step(c, c->cur, c->host_steps, nullptr, dt_used ? c->dt_used : nullptr);
     if (st != HSGN_OK) return st;
     c->cur ^= 1;
     c->host_steps++;
     if (dt_used) {
         st = reconcile(c);
-        CUDA_TRY(c, cudaMemcpy(dt_used, c->dt, c->members * sizeof(double), cudaMemcpyDeviceToHost));
+        CUDA_TRY(c, cudaMemcpy(dt_used, c->dt_used, c->members * sizeof(double), cudaMemcpyDeviceToHost));
         return st;
     }
     return HSGN_OK;
@@ -541,37 +577,23 @@ hsgn_status hsgn_run_steps_timed(hsgn_ctx *c, int64_t n_steps, double *stage_ms)
     if (n_steps < 0 || !stage_ms) return HSGN_E_INVALID;
     st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
     if (st != HSGN_OK) return st;
-    const int per = c->tab.stages;
-    std::vector<cudaEvent_t> ev(size_t(n_steps) * per + 1);
+    std::vector<cudaEvent_t> ev(size_t(n_steps) * 3);
     for (auto &e : ev) CUDA_TRY(c, cudaEventCreate(&e));
-    CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
-    const Params P = make_params(c);
+    st = launch_dtc(c, c->host_steps, 0, 1);
     for (int64_t k = 0; k < n_steps && st == HSGN_OK; k++) {
-        Bufs B{};
-        for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; }
-        if (per == 1) {
-            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
-            st = launch_stage_b<false, true>(c, P, B);
-            if (st == HSGN_OK) CUDA_TRY(c, cudaEventRecord(ev[k + 1], c->stream));
-        } else {
-            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
-            st = launch_stage_b<false, false>(c, P, B);
-            if (st != HSGN_OK) break;
-            CUDA_TRY(c, cudaEventRecord(ev[2 * k + 1], c->stream));
-            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
-            st = launch_stage_b<true, true>(c, P, B);
-            if (st == HSGN_OK) CUDA_TRY(c, cudaEventRecord(ev[2 * k + 2], c->stream));
-        }
+        st = enqueue_step(c, c->cur, c->host_steps, &ev[3 * k]);
         c->cur ^= 1;
         c->host_steps++;
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     stage_ms[0] = stage_ms[1] = 0.0;
     if (st == HSGN_OK) {
-        for (size_t i = 1; i < ev.size(); i++) {
-            float ms = 0.f;
-            CUDA_TRY(c, cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
-            stage_ms[(i - 1) % per] += ms;
+        for (int64_t k = 0; k < n_steps; k++) {
+            float a = 0.f, b = 0.f;
+            CUDA_TRY(c, cudaEventElapsedTime(&a, ev[3 * k], ev[3 * k + 1]));
+            CUDA_TRY(c, cudaEventElapsedTime(&b, ev[3 * k + 1], ev[3 * k + 2]));
+            stage_ms[0] += a;
+            stage_ms[1] += b;
         }
     }
     for (auto &e : ev) cudaEventDestroy(e);

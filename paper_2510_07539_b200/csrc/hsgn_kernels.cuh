@@ -69,6 +69,7 @@ struct Params {
     unsigned int *done;
     unsigned long long *rho_obs;     // max rho over tiles (double bits)
     const Ctrl *ctrl;
+    int kslot, kpar;                 // host step index k: k mod 3, k mod 2
 };
 
 struct Bufs {
@@ -179,30 +180,51 @@ __device__ __forceinline__ double fsqrt(double x)
     return fma(fma(-s, s, x), 0.5 * y, s);
 }
 
-// Rusanov face flux (A4) from the 4-row window v0..v3 = rows f-1..f+2
-// for the face f+1/2, with MUSCL (A5) when order == 2.
+// MUSCL face states (A5): for the window rows (k-1, k, k+1),
+// M_k = v_k + (v_{k+1} - v_{k-1})/4 at face k+1/2 and Pl_k = v_k - (...)/4 at
+// face k-1/2 (order 1: the cell values); u = q/h at the face state.
+struct FState { double h, q, H, W, u; };
 struct Face { double q, H, W; };
 
-__device__ __forceinline__ Face face_flux(const double (&wh)[4], const double (&wq)[4],
-                                          const double (&wH)[4], const double (&wW)[4],
-                                          int order)
+__device__ __forceinline__ FState muscl_minus(const double (&wh)[3], const double (&wq)[3],
+                                              const double (&wH)[3], const double (&wW)[3],
+                                              int order)
 {
-    double hm, hp, qm, qp, Hm, Hp, Wm, Wp;
+    FState S;
     if (order == 2) {
-        hm = wh[1] + 0.25 * (wh[2] - wh[0]);  hp = wh[2] - 0.25 * (wh[3] - wh[1]);
-        qm = wq[1] + 0.25 * (wq[2] - wq[0]);  qp = wq[2] - 0.25 * (wq[3] - wq[1]);
-        Hm = wH[1] + 0.25 * (wH[2] - wH[0]);  Hp = wH[2] - 0.25 * (wH[3] - wH[1]);
-        Wm = wW[1] + 0.25 * (wW[2] - wW[0]);  Wp = wW[2] - 0.25 * (wW[3] - wW[1]);
+        S.h = wh[1] + 0.25 * (wh[2] - wh[0]); S.q = wq[1] + 0.25 * (wq[2] - wq[0]);
+        S.H = wH[1] + 0.25 * (wH[2] - wH[0]); S.W = wW[1] + 0.25 * (wW[2] - wW[0]);
     } else {
-        hm = wh[1]; hp = wh[2]; qm = wq[1]; qp = wq[2];
-        Hm = wH[1]; Hp = wH[2]; Wm = wW[1]; Wp = wW[2];
+        S.h = wh[1]; S.q = wq[1]; S.H = wH[1]; S.W = wW[1];
     }
-    const double um = qm * rcp(hm), up = qp * rcp(hp);
-    const double a = fmax(fabs(um), fabs(up));
+    S.u = S.q * rcp(S.h);
+    return S;
+}
+
+__device__ __forceinline__ FState muscl_plus(const double (&wh)[3], const double (&wq)[3],
+                                             const double (&wH)[3], const double (&wW)[3],
+                                             int order)
+{
+    FState S;
+    if (order == 2) {
+        S.h = wh[1] - 0.25 * (wh[2] - wh[0]); S.q = wq[1] - 0.25 * (wq[2] - wq[0]);
+        S.H = wH[1] - 0.25 * (wH[2] - wH[0]); S.W = wW[1] - 0.25 * (wW[2] - wW[0]);
+    } else {
+        S.h = wh[1]; S.q = wq[1]; S.H = wH[1]; S.W = wW[1];
+    }
+    S.u = S.q * rcp(S.h);
+    return S;
+}
+
+// Rusanov flux of R_E at a face (A4): alpha = max(|u-|, |u+|),
+// F = 1/2 (F(U-) + F(U+)) - 1/2 alpha (U+ - U-) for F^q = q u, F^H = H u, F^W = W u.
+__device__ __forceinline__ Face rusanov(const FState &m, const FState &p)
+{
+    const double a = fmax(fabs(m.u), fabs(p.u));
     Face F;
-    F.q = 0.5 * (qm * um + qp * up) - 0.5 * a * (qp - qm);
-    F.H = 0.5 * (Hm * um + Hp * up) - 0.5 * a * (Hp - Hm);
-    F.W = 0.5 * (Wm * um + Wp * up) - 0.5 * a * (Wp - Wm);
+    F.q = 0.5 * (m.q * m.u + p.q * p.u) - 0.5 * a * (p.q - m.q);
+    F.H = 0.5 * (m.H * m.u + p.H * p.u) - 0.5 * a * (p.H - m.H);
+    F.W = 0.5 * (m.W * m.u + p.W * p.u) - 0.5 * a * (p.W - m.W);
     return F;
 }
 
@@ -318,39 +340,12 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         }
     }
 
-    // ---- run control and dt ---------------------------------------
+    // ---- run control: dt of this member was set by dt_commit_kernel ---------
     const unsigned int err0 = *((volatile unsigned int *)P.err);
-    const long long stepno = *((volatile long long *)P.steps);
     const int members = P.members;
-    const int slot_r = int(stepno % 3), slot_w = int((stepno + 1) % 3), slot_z = int((stepno + 2) % 3);
-    const double tm = P.t[int(stepno & 1) * members + m];
-    const double t_end = P.ctrl->t_end;
+    const double dtm = P.dt[m];
     const double lam = P.lam[m];
-    double dtm;
-    if (!STAGE2) {
-        const double umax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 0) * members + m]);
-        const double numax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 1) * members + m]);
-        const double dt_fixed = P.ctrl->dt_fixed;
-        dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, P.idx, umax, numax);
-        if (t_end > 0.0) {
-            if (!(tm < t_end)) dtm = 0.0;
-            else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end
-        }
-        if (!(dtm >= 0.0) || !isfinite(dtm)) {
-            drain_loads(bulk, mb);
-            if (tid == 0) atomicOr(P.err, ERR_DT);
-            return;
-        }
-        if (j == 0 && tid == 0) {
-            P.dt[m] = dtm;
-            P.maxes[(slot_z * 2 + 0) * members + m] = 0ull;   // 3-slot rotation: free
-            P.maxes[(slot_z * 2 + 1) * members + m] = 0ull;   // the slot read last step
-        }
-    } else {
-        dtm = P.dt[m];
-    }
     if (err0) { drain_loads(bulk, mb); return; }
-
     const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
     const double g = P.g, idx1 = P.idx;
     const double tdx = tau * idx1;                  // tau / dx
@@ -419,32 +414,49 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         {
             const int p0 = tid * MCH;
             if (p0 < L + 2) {
-                double wh[4], wq[4], wH[4], wW[4];
+                const int order = P.order;
                 const int r0 = p0 - 1;
+                // raw window rows (r-1, r, r+1) and MUSCL face states:
+                // M_k = minus state at face k+1/2, Pl_k = plus state at face k-1/2
+                double wh[3], wq[3], wH[3], wW[3];
 #pragma unroll
-                for (int k = 0; k < 4; k++) {     // rows r0-2 .. r0+1
+                for (int k = 0; k < 3; k++) {     // rows r0-2 .. r0
                     const int ix = r0 - 2 + k + 3;
                     wh[k] = sEh[ix]; wq[k] = sEq[ix]; wH[k] = sEH[ix]; wW[k] = sEW[ix];
                 }
-                Face Fl = face_flux(wh, wq, wH, wW, P.order);
+                FState Mr = muscl_minus(wh, wq, wH, wW, order);       // M_{r0-1}
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
+                }
+                {
+                    const int ix = r0 + 1 + 3;
+                    wh[2] = sEh[ix]; wq[2] = sEq[ix]; wH[2] = sEH[ix]; wW[2] = sEW[ix];
+                }
+                FState Pn = muscl_plus(wh, wq, wH, wW, order);        // Pl_{r0}
+                Face Fl = rusanov(Mr, Pn);                             // face r0-1/2
+                Mr = muscl_minus(wh, wq, wH, wW, order);               // M_{r0}
 #pragma unroll
                 for (int i = 0; i < MCH; i++) {
                     const int r = r0 + i;
                     if (r > L) break;
+                    const double hE = wh[1], qE = wq[1], HE = wH[1], WE = wW[1];
+                    const double hEm = wh[0], hEp = wh[2];
 #pragma unroll
-                    for (int k = 0; k < 3; k++) {
+                    for (int k = 0; k < 2; k++) {
                         wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
                     }
                     {
                         const int ix = r + 2 + 3;
-                        wh[3] = sEh[ix]; wq[3] = sEq[ix]; wH[3] = sEH[ix]; wW[3] = sEW[ix];
+                        wh[2] = sEh[ix]; wq[2] = sEq[ix]; wH[2] = sEH[ix]; wW[2] = sEW[ix];
                     }
-                    const Face Fr = face_flux(wh, wq, wH, wW, P.order);
+                    Pn = muscl_plus(wh, wq, wH, wW, order);            // Pl_{r+1}
+                    const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
+                    Mr = muscl_minus(wh, wq, wH, wW, order);           // M_{r+1}
                     const int p = r + 1;
-                    const double hE = wh[1], qE = wq[1], HE = wH[1];
                     // R = E in stage 1; stage 2 combined it on load
                     const double hR = STAGE2 ? sHR[p] : hE, qR = STAGE2 ? sQd[p] : qE;
-                    const double HR = STAGE2 ? sHd[p] : HE, WR = STAGE2 ? sWd[p] : wW[1];
+                    const double HR = STAGE2 ? sHd[p] : HE, WR = STAGE2 ? sWd[p] : WE;
                     const double ihE = rcp(hE);
                     const double ih2 = ihE * ihE;
                     const double sg = HE * ih2;                                  // eta/h
@@ -455,7 +467,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                         const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
                         Dxb = (bp - bm) * (0.5 * idx1);
                         // hydrostatic term in zeta-form (A9)
-                        const double Gr = g * (hE + wh[2]) * 0.5, Gl = g * (wh[0] + hE) * 0.5;
+                        const double Gr = g * (hE + hEp) * 0.5, Gl = g * (hEm + hE) * 0.5;
                         hRp = hR + t2 * (Gr * (bp - b0) - Gl * (b0 - bm));
                         ptil_term = 1.5 * tau * lam3 * (1.0 - sg) * Dxb;        // p~
                     }
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                     rhs = sHR[r + 1] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
                           - ml * (vH[i + 1] - vH[i]);
                     a = -rl; c = -rr; dg = 1.0 + rl + rr;
-                    rho_loc = fmax(rho_loc, rr);
+                    rho_loc = rr > rho_loc ? rr : rho_loc;
                 }
                 if (i == 0) {
                     const double inv = rcp(dg);
@@ -559,12 +571,34 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 const double ib = rcp(1.0 - cE * Q1);
                 A_ *= ib; C_ *= ib; D_ *= ib;
             }
-            // PCR over NT unknowns, double-buffered, one reciprocal per row and step
+            // PCR over NT unknowns, double-buffered, one reciprocal per row and
+            // step.  The reduced couplings shrink like e_{s+1} <= e_s^2/(1-2e_s^2)
+            // (e = max |A|,|C|), so PCR stops once e^(2^s) <= 2^-64: the rows are
+            // then decoupled to below round-off (x_k = D_k).
             double *cur = pcr0, *nxt = pcr1;
             cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
+            {
+                const double ea = fabs(A_), ec = fabs(C_);
+                double ev = warp_max(ea > ec ? ea : ec);
+                if (lane == 0) red[1][wid] = ev;
+            }
             __syncthreads();
+            int lim = NT;
+            {
+                double e0 = 0.0;
+#pragma unroll
+                for (int q = 0; q < NT / 32; q++) e0 = fmax(e0, red[1][q]);
+                e0 *= 1.05;
+                if (e0 == 0.0) lim = 1;
+                else if (e0 < 0.5) {
+                    const double need = 64.0 / -log2(e0);    // 2^s >= need
+                    int sdl = 1;
+                    while (sdl < NT && double(sdl) < need) sdl <<= 1;
+                    lim = sdl;
+                }
+            }
 #pragma unroll 1
-            for (int sd = 1; sd < NT; sd <<= 1) {
+            for (int sd = 1; sd < lim; sd <<= 1) {
                 const int km = tid - sd, kp = tid + sd;
                 double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
                 if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
@@ -621,10 +655,13 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 bb = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
                 qb -= tau * g * sEh[r + 3] * (bp - bm) * (0.5 * idx1);     // A9
             }
-            const double ihb = rcp(hb);
-            const double ihb2 = ihb * ihb;
-            const double Hb = sHd[p] * rcp(1.0 + lt2 * ihb2);
-            const double Wb = sWd[p] - lam * tau * Hb * ihb2;
+            // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),
+            // Wbar = W^dag - lam tau Hbar / hbar^2 = W^dag - lam tau H^dag / (hbar^2 + lam tau^2)
+            const double hb2 = hb * hb;
+            const double Dn = rcp(hb2 + lt2);
+            const double HdD = sHd[p] * Dn;
+            const double Hb = HdD * hb2;
+            const double Wb = sWd[p] - lam * tau * HdD;
             const bool kept = (r >= wl && r < wl + Tk);
             if (kept) {
                 if (!(hb > P.h_min)) errbits |= ERR_DRY;
@@ -638,7 +675,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 B.out[0][gi] = hb; B.out[1][gi] = qb; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
                 B.out[3][gi] = Wb;
                 if (FINAL) {
-                    const double u = qb * ihb, sg = Hb * ihb2;
+                    const double u = qb * rcp(hb), sg = HdD;             // sg = Hbar / hbar^2
                     umax_loc = fmax(umax_loc, fabs(u));
                     numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * hb + lam3 * sg * sg));
                 }
@@ -689,11 +726,11 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         unsigned int eb = errbits;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) eb |= __shfl_xor_sync(0xffffffffu, eb, o);
-        if ((tid & 31) == 0 && eb) atomicOr(P.err, eb);
+        if ((tid & 31) == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
     }
 
     if (FINAL) {
-        // ---- dt maxima for the next step -----------------------------
+        // ---- dt maxima for the next step and next time level ----------
         double um = warp_max(umax_loc), nm = warp_max(numax_loc);
         const int lane = tid & 31, wid = tid >> 5;
         __syncthreads();
@@ -701,23 +738,53 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         __syncthreads();
         if (tid == 0) {
             for (int q = 1; q < NT / 32; q++) { um = fmax(um, red[0][q]); nm = fmax(nm, red[1][q]); }
+            const int slot_w = (P.kslot + 1) % 3;
             atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
             atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
-            if (j == 0) {   // next time level of this member (double-buffered by step parity)
-                P.t[int((stepno + 1) & 1) * members + m] =
-                    (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
-            }
-            // ---- commit by the last CTA: O(1) ----------------------------------------
-            __threadfence();
-            const unsigned int total = gridDim.x * gridDim.y;
-            const unsigned int prev = atomicAdd(P.done, 1u);
-            if (prev == total - 1) {
-                __threadfence();
-                if (*((volatile unsigned int *)P.err) == 0u) *P.steps = stepno + 1;
-                *P.done = 0u;
+            if (j == 0) {   // t^{n+1} of this member, in the other parity slot
+                const double tm = P.t[P.kpar * members + m];
+                const double t_end = P.ctrl->t_end;
+                P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Between steps: commit step k-1 (steps += 1 unless an error was latched) and
+// set dt of step k for every member from the max|u|, max(|u|+c) of U^k
+// (A7), clipped to t_end; free the maxima slot read at
+// step k-1 (3-slot rotation, slot = k mod 3 is read, k+1 written).
+// Slots and time parity come from the host's step index k (kslot = k mod 3,
+// kpar = k mod 2), so no kernel reads a device step counter.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int commit_prev,
+                                                        int compute_dt)
+{
+    const unsigned int err = *((volatile unsigned int *)P.err);
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid == 0 && commit_prev && err == 0u) *P.steps += 1;
+    if (err || !compute_dt) return;
+    const int m = tid;
+    const int members = P.members;
+    if (m >= members) return;
+    const int slot_r = P.kslot, slot_z = (P.kslot + 2) % 3;
+    const double umax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 0) * members + m]);
+    const double numax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 1) * members + m]);
+    const double t_end = P.ctrl->t_end, dt_fixed = P.ctrl->dt_fixed;
+    const double tm = P.t[P.kpar * members + m];
+    double dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, P.idx, umax, numax);
+    if (t_end > 0.0) {
+        if (!(tm < t_end)) dtm = 0.0;
+        else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end
+    }
+    if (!(dtm >= 0.0) || !isfinite(dtm)) {
+        atomicOr(P.err, ERR_DT);
+        return;
+    }
+    P.dt[m] = dtm;
+    P.maxes[(slot_z * 2 + 0) * members + m] = 0ull;
+    P.maxes[(slot_z * 2 + 1) * members + m] = 0ull;
 }
 
 // ---------------------------------------------------------------------------

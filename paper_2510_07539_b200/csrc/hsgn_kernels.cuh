@@ -38,10 +38,13 @@
 namespace hsgn {
 
 constexpr int NT = HSGN_NT;           // threads per CTA
-constexpr int MCH = 5;              // rows per thread chunk (odd: conflict-free strided smem)
+#ifndef HSGN_MCH
+#define HSGN_MCH 5
+#endif
+constexpr int MCH = HSGN_MCH;       // rows per thread chunk (odd: conflict-free strided smem)
 constexpr int LCAP = NT * MCH;      // 1280 rows per CTA incl. phase-1 halo rows
 constexpr int SROWS = LCAP + 8;     // smem row capacity per array (even: 16-B aligned bases)
-constexpr int NARR = 10;            // smem arrays
+constexpr int NARR = 9;             // smem arrays
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
 
 enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2 };
@@ -111,6 +114,14 @@ __device__ __forceinline__ void bulk_g2s(double *dst_smem, const double *src, un
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
         ::"r"(a), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+// TMA bulk copy shared -> global (16-B aligned, size a multiple of 16).
+__device__ __forceinline__ void bulk_s2g(double *dst, const double *src_smem, unsigned bytes)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(src_smem);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                 ::"l"(dst), "r"(a), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity)
@@ -228,6 +239,67 @@ __device__ __forceinline__ Face rusanov(const FState &m, const FState &p)
     return F;
 }
 
+// Pl state of the row after the window (rows k, k+1 = window[1..2] + (h1, q1, H1, W1)).
+__device__ __forceinline__ FState muscl_plus_next(const double (&wh)[3], const double (&wq)[3],
+                                                  const double (&wH)[3], const double (&wW)[3],
+                                                  double h1, double q1, double H1, double W1,
+                                                  int order)
+{
+    const double th[3] = {wh[1], wh[2], h1}, tq[3] = {wq[1], wq[2], q1};
+    const double tH[3] = {wH[1], wH[2], H1}, tW[3] = {wW[1], wW[2], W1};
+    return muscl_plus(th, tq, tH, tW, order);
+}
+
+struct RowCtx { double tau, tdx, t2, lt2, lam, lam3, ltau, g, idx; };
+
+// Predictor (A9) and coefficients at E (A2) of
+// one row r; E rows r-1, r, r+1 in (ch, cq, cH, cW); fluxes at r -+ 1/2.
+// Stores q^dag, H^dag, beta, delta, h^R' at row r unless r < -1 (dead row).
+template <bool STAGE2, bool BATHY>
+__device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int r, int start, int n,
+                                           const double (&ch)[3], const double (&cq)[3],
+                                           const double (&cH)[3], const double (&cW)[3],
+                                           const Face &Fl, const Face &Fr, double *sHR, double *sQd,
+                                           double *sHd, double *sBe, double *sDe, double &Wd_out,
+                                           double &beta_out)
+{
+    const bool live = r >= -1;
+    const int rr = live ? r : 0;
+    const double hE = ch[1], qE = cq[1], HE = cH[1], WE = cW[1];
+    // R = E in stage 1; stage 2 combined it on load
+    const double hR = STAGE2 ? sHR[rr] : hE, qR = STAGE2 ? sQd[rr] : qE;
+    const double HR = STAGE2 ? sHd[rr] : HE, WR = STAGE2 ? sBe[rr] : WE;
+    const double ihE = rcp(hE);
+    const double ih2 = ihE * ihE;
+    const double sg = HE * ih2;                                      // eta/h
+    double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
+    if (BATHY) {
+        const double bm = bathy_at(P.b, start + rr - 1, n, P.bcl, P.bcr);
+        const double b0 = bathy_at(P.b, start + rr, n, P.bcl, P.bcr);
+        const double bp = bathy_at(P.b, start + rr + 1, n, P.bcl, P.bcr);
+        Dxb = (bp - bm) * (0.5 * C.idx);
+        // hydrostatic term in zeta-form (A9)
+        const double Gr = C.g * (hE + ch[2]) * 0.5, Gl = C.g * (ch[0] + hE) * 0.5;
+        hRp = hR + C.t2 * (Gr * (bp - b0) - Gl * (b0 - bm));
+        ptil_term = 1.5 * C.tau * C.lam3 * (1.0 - sg) * Dxb;        // p~
+    }
+    // predictor
+    const double Wd = WR - C.tdx * (Fr.W - Fl.W) + C.ltau;
+    const double Hd = HR - C.tdx * (Fr.H - Fl.H) - 1.5 * C.tau * qE * Dxb + C.tau * Wd;
+    const double qd = qR - C.tdx * (Fr.q - Fl.q) - ptil_term;
+    // coefficients at E
+    const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
+    const double a2 = C.g * hE + C.lam3 * sg * (3.0 * sg - 1.0);
+    const double beta1 = 1.0 + C.lt2 * ih2;
+    const double ib1 = rcp(beta1);
+    const double beta2 = 2.0 * C.lt2 * ib1 * ib1 * ih2 * ihE;
+    const double beta = a2 + C.lam * alpha * beta2 * Hd;
+    const double delta = alpha * ib1;
+    if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; sHR[rr] = hRp; }
+    Wd_out = Wd;
+    beta_out = live ? beta : 1.0;
+}
+
 __device__ __forceinline__ double warp_max(double v)
 {
 #pragma unroll
@@ -263,6 +335,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(8) unsigned long long s_mbar;
     __shared__ double red[2][NT / 32];
+    __shared__ float redf[NT / 32];
     __shared__ double xch[NT / 32][3];
 
     const int tid = threadIdx.x;
@@ -283,31 +356,24 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const bool left_phys = !periodic && (start == 0);
     const bool right_phys = !periodic && (start + L == n);
 
-    // ---- load: raw rows -3..L+2 of U^n (and U1) into shared memory ----------
-    // Interior tiles: one TMA bulk copy per field (cp.async.bulk, 16-B aligned
-    // by shifting the smem arrays by d = parity of the first global cell).
-    // Wrapping / wall tiles: per-element cp.async through the BC index map.
-    // Issued first so that the copies overlap the run-control reads below.
+    // ---- shared memory: 9 arrays of SROWS doubles, all indexed by tile row r
+    // (r in [-3, L+3)).  Interior tiles are filled by TMA bulk copies, which
+    // need 16-B aligned destinations: every array is shifted by d = parity of
+    // the first copied global cell.
     const bool interior = (start - 3 >= 0) && (start + L + 3 <= n);
     const int d = interior ? int((mo + size_t(start - 3)) & 1) : 0;
     const int a0 = start - 3 - d;                       // first copied cell
     const int cnt = (L + 6 + d + 1) & ~1;               // even count: 16-B multiple
     const bool bulk = interior && (a0 >= 0) && (a0 + cnt <= n);
+    double *const A = smem + d + 3;                     // A + k*SROWS + r
+    double *sEh = A, *sEq = A + SROWS, *sEH = A + 2 * SROWS, *sEW = A + 3 * SROWS;
+    double *sQd = A + 4 * SROWS;   // U1_q -> R_q -> q^dagger
+    double *sHd = A + 5 * SROWS;   // U1_K -> R_H -> H^dagger
+    double *sBe = A + 6 * SROWS;   // U1_W -> R_W -> beta
+    double *sDe = A + 7 * SROWS;   // delta
+    double *sHR = A + 8 * SROWS;   // U1_h -> R_h -> h^R (+ hydrostatic term)
 
-    // E arrays are indexed by idx = r + 3 (rows -3..L+2).  The phase-1 output
-    // arrays are offset by 2 so that index p = r + 1 lands on the same physical
-    // slot r + 3: the stage-2 raw copy of U1 and the R combination share it.
-    double *sEh = smem + d;
-    double *sEq = sEh + SROWS;
-    double *sEH = sEq + SROWS;
-    double *sEW = sEH + SROWS;
-    double *sQd = sEW + SROWS + 2;       // q^dagger  (U1_q / R_q before phase 1)
-    double *sHd = sQd + SROWS;           // H^dagger  (U1_K / R_H before phase 1)
-    double *sWd = sHd + SROWS;           // W^dagger  (U1_W / R_W before phase 1)
-    double *sBe = sWd + SROWS;           // beta
-    double *sDe = sBe + SROWS;           // delta
-    double *sHR = sDe + SROWS;           // h^R (+ hydrostatic term) (U1_h before)
-
+    // ---- load: raw rows -3..L+2 of U^n (and U1), overlapped with run control --
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
     if (bulk) {
         if (tid == 0) {
@@ -320,22 +386,21 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
 #pragma unroll
             for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
             if (STAGE2) {
-                // raw U1 into the R slots: h -> sHR, q -> sQd, K -> sHd, W -> sWd
-                bulk_g2s(smem + 9 * SROWS, B.U1[0] + gsrc, bytes, mb);
+                bulk_g2s(smem + 8 * SROWS, B.U1[0] + gsrc, bytes, mb);
                 bulk_g2s(smem + 4 * SROWS, B.U1[1] + gsrc, bytes, mb);
                 bulk_g2s(smem + 5 * SROWS, B.U1[2] + gsrc, bytes, mb);
                 bulk_g2s(smem + 6 * SROWS, B.U1[3] + gsrc, bytes, mb);
             }
         }
     } else {
-        for (int idx = tid; idx < L + 6; idx += NT) {
+        for (int r = tid - 3; r < L + 3; r += NT) {
             double par;
-            const size_t gi = mo + map_cell(start + idx - 3, n, P.bcl, P.bcr, par);
-            cp_async8(sEh + idx, B.Un[0] + gi); cp_async8(sEq + idx, B.Un[1] + gi);
-            cp_async8(sEH + idx, B.Un[2] + gi); cp_async8(sEW + idx, B.Un[3] + gi);
+            const size_t gi = mo + map_cell(start + r, n, P.bcl, P.bcr, par);
+            cp_async8(sEh + r, B.Un[0] + gi); cp_async8(sEq + r, B.Un[1] + gi);
+            cp_async8(sEH + r, B.Un[2] + gi); cp_async8(sEW + r, B.Un[3] + gi);
             if (STAGE2) {
-                cp_async8(sHR + idx - 2, B.U1[0] + gi); cp_async8(sQd + idx - 2, B.U1[1] + gi);
-                cp_async8(sHd + idx - 2, B.U1[2] + gi); cp_async8(sWd + idx - 2, B.U1[3] + gi);
+                cp_async8(sHR + r, B.U1[0] + gi); cp_async8(sQd + r, B.U1[1] + gi);
+                cp_async8(sHd + r, B.U1[2] + gi); cp_async8(sBe + r, B.U1[3] + gi);
             }
         }
     }
@@ -355,8 +420,10 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const double lt2h = 0.5 * lam * t2;             // lambda tau^2 / (2 dx^2)
     const double ltdx2 = lam * tdx2;                // lambda tau / (2 dx)
     const double lam3 = lam * (1.0 / 3.0);
+    const double ltau = lam * tau;
 
     double umax_loc = 0.0, numax_loc = 0.0;
+    float rho_loc = 0.0f;
     unsigned int errbits = 0u;
 
     if (bulk) {
@@ -386,119 +453,105 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         const bool wall_ghosts = (left_phys && P.bcl == BC_WALL) || (right_phys && P.bcr == BC_WALL);
         if (STAGE2 || BATHY || wall_ghosts) {
             const double wE = P.wE, wR = P.wR;
-            for (int idx = tid; idx < L + 6; idx += NT) {
+            for (int r = tid - 3; r < L + 3; r += NT) {
                 double par = 1.0;
-                int c = start + idx - 3;
+                int c = start + r;
                 if (!interior) c = map_cell(c, n, P.bcl, P.bcr, par);
                 const double bb = BATHY ? __ldg(P.b + c) : 0.0;
-                double eh = sEh[idx], eq = par * sEq[idx], eK = sEH[idx], eW = sEW[idx];
+                double eh = sEh[r], eq = par * sEq[r], eK = sEH[r], eW = sEW[r];
                 if (STAGE2) {
-                    const double h1 = sHR[idx - 2], q1 = par * sQd[idx - 2], K1 = sHd[idx - 2],
-                                 W1 = sWd[idx - 2];
+                    const double h1 = sHR[r], q1 = par * sQd[r], K1 = sHd[r], W1 = sBe[r];
                     const double rh = (1.0 - wR) * eh + wR * h1, rq = (1.0 - wR) * eq + wR * q1;
                     const double rK = (1.0 - wR) * eK + wR * K1, rW = (1.0 - wR) * eW + wR * W1;
-                    sHR[idx - 2] = rh; sQd[idx - 2] = rq;
-                    sHd[idx - 2] = BATHY ? rK - 1.5 * rh * bb : rK;
-                    sWd[idx - 2] = rW;
+                    sHR[r] = rh; sQd[r] = rq;
+                    sHd[r] = BATHY ? rK - 1.5 * rh * bb : rK;
+                    sBe[r] = rW;
                     eh = (1.0 - wE) * eh + wE * h1; eq = (1.0 - wE) * eq + wE * q1;
                     eK = (1.0 - wE) * eK + wE * K1; eW = (1.0 - wE) * eW + wE * W1;
                 }
-                sEh[idx] = eh; sEq[idx] = eq;
-                sEH[idx] = BATHY ? eK - 1.5 * eh * bb : eK;
-                sEW[idx] = eW;
+                sEh[r] = eh; sEq[r] = eq;
+                sEH[r] = BATHY ? eK - 1.5 * eh * bb : eK;
+                sEW[r] = eW;
             }
             __syncthreads();
         }
 
-        // ---- phase 1: faces, predictor, coefficients (chunk rows) -------------
+        // Every thread owns the rows r0 .. r0+MCH-1 of the tile in all three
+        // phases (thread 0 also computes row -1 in phase 1, the owner of row L
+        // computes it); values stay in registers between phases, neighbours'
+        // rows come from shared memory.
+        const int r0 = tid * MCH;
+        double wd[MCH];                  // W^dagger of own rows (phase 1 -> 3)
+
+        // ---- phase 1: faces, predictor, coefficients --------------------------
+        // Branch-free over the MCH own rows (stores predicated on r <= L) so the
+        // register window shifts are pure renaming; thread 0 also does row -1.
         {
-            const int p0 = tid * MCH;
-            if (p0 < L + 2) {
-                const int order = P.order;
-                const int r0 = p0 - 1;
-                // raw window rows (r-1, r, r+1) and MUSCL face states:
-                // M_k = minus state at face k+1/2, Pl_k = plus state at face k-1/2
-                double wh[3], wq[3], wH[3], wW[3];
+            const int order = P.order;
+            RowCtx C{};
+            C.tau = tau; C.tdx = tdx; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
+            C.ltau = ltau; C.g = g; C.idx = idx1;
+            double wh[3], wq[3], wH[3], wW[3];
 #pragma unroll
-                for (int k = 0; k < 3; k++) {     // rows r0-2 .. r0
-                    const int ix = r0 - 2 + k + 3;
-                    wh[k] = sEh[ix]; wq[k] = sEq[ix]; wH[k] = sEH[ix]; wW[k] = sEW[ix];
+            for (int k = 0; k < 3; k++) {                 // rows r0-2 .. r0
+                const int rr = r0 - 2 + k;
+                wh[k] = sEh[rr]; wq[k] = sEq[rr]; wH[k] = sEH[rr]; wW[k] = sEW[rr];
+            }
+            FState Mm = muscl_minus(wh, wq, wH, wW, order);           // M_{r0-1}
+            if (tid == 0) {
+                // row -1 (left halo of the tile): faces -3/2 and -1/2
+                double xh[3], xq[3], xH[3], xW[3];
+#pragma unroll
+                for (int k = 0; k < 3; k++) {             // rows -3 .. -1
+                    xh[k] = sEh[k - 3]; xq[k] = sEq[k - 3]; xH[k] = sEH[k - 3]; xW[k] = sEW[k - 3];
                 }
-                FState Mr = muscl_minus(wh, wq, wH, wW, order);       // M_{r0-1}
+                const FState M2 = muscl_minus(xh, xq, xH, xW, order);     // M_{-2}
+                const FState P1 = muscl_plus(wh, wq, wH, wW, order);      // Pl_{-1} (rows -2..0)
+                const Face Fa = rusanov(M2, P1);                          // face -3/2
+                const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], order);
+                const Face Fb = rusanov(Mm, P0);                          // face -1/2
+                double Wd, beta;
+                row_update<STAGE2, BATHY>(C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
+                                          sHR, sQd, sHd, sBe, sDe, Wd, beta);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
+            }
+            wh[2] = sEh[r0 + 1]; wq[2] = sEq[r0 + 1]; wH[2] = sEH[r0 + 1]; wW[2] = sEW[r0 + 1];
+            FState Pn = muscl_plus(wh, wq, wH, wW, order);        // Pl_{r0}
+            Face Fl = rusanov(Mm, Pn);                             // face r0-1/2
+            FState Mr = muscl_minus(wh, wq, wH, wW, order);        // M_{r0}
+#pragma unroll
+            for (int i = 0; i < MCH; i++) {
+                const int r = r0 + i;
+                double ch[3], cq[3], cH[3], cW[3];                 // rows r-1, r, r+1
+#pragma unroll
+                for (int k = 0; k < 3; k++) { ch[k] = wh[k]; cq[k] = wq[k]; cH[k] = wH[k]; cW[k] = wW[k]; }
 #pragma unroll
                 for (int k = 0; k < 2; k++) {
                     wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
                 }
-                {
-                    const int ix = r0 + 1 + 3;
-                    wh[2] = sEh[ix]; wq[2] = sEq[ix]; wH[2] = sEH[ix]; wW[2] = sEW[ix];
-                }
-                FState Pn = muscl_plus(wh, wq, wH, wW, order);        // Pl_{r0}
-                Face Fl = rusanov(Mr, Pn);                             // face r0-1/2
-                Mr = muscl_minus(wh, wq, wH, wW, order);               // M_{r0}
-#pragma unroll
-                for (int i = 0; i < MCH; i++) {
-                    const int r = r0 + i;
-                    if (r > L) break;
-                    const double hE = wh[1], qE = wq[1], HE = wH[1], WE = wW[1];
-                    const double hEm = wh[0], hEp = wh[2];
-#pragma unroll
-                    for (int k = 0; k < 2; k++) {
-                        wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
-                    }
-                    {
-                        const int ix = r + 2 + 3;
-                        wh[2] = sEh[ix]; wq[2] = sEq[ix]; wH[2] = sEH[ix]; wW[2] = sEW[ix];
-                    }
-                    Pn = muscl_plus(wh, wq, wH, wW, order);            // Pl_{r+1}
-                    const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
-                    Mr = muscl_minus(wh, wq, wH, wW, order);           // M_{r+1}
-                    const int p = r + 1;
-                    // R = E in stage 1; stage 2 combined it on load
-                    const double hR = STAGE2 ? sHR[p] : hE, qR = STAGE2 ? sQd[p] : qE;
-                    const double HR = STAGE2 ? sHd[p] : HE, WR = STAGE2 ? sWd[p] : WE;
-                    const double ihE = rcp(hE);
-                    const double ih2 = ihE * ihE;
-                    const double sg = HE * ih2;                                  // eta/h
-                    double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
-                    if (BATHY) {
-                        const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
-                        const double b0 = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
-                        const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
-                        Dxb = (bp - bm) * (0.5 * idx1);
-                        // hydrostatic term in zeta-form (A9)
-                        const double Gr = g * (hE + hEp) * 0.5, Gl = g * (hEm + hE) * 0.5;
-                        hRp = hR + t2 * (Gr * (bp - b0) - Gl * (b0 - bm));
-                        ptil_term = 1.5 * tau * lam3 * (1.0 - sg) * Dxb;        // p~
-                    }
-                    // predictor
-                    const double Wd = WR - tdx * (Fr.W - Fl.W) + lam * tau;
-                    const double Hd = HR - tdx * (Fr.H - Fl.H) - 1.5 * tau * qE * Dxb + tau * Wd;
-                    const double qd = qR - tdx * (Fr.q - Fl.q) - ptil_term;
-                    // coefficients at E (A2)
-                    const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
-                    const double a2 = g * hE + lam3 * sg * (3.0 * sg - 1.0);
-                    const double beta1 = 1.0 + lt2 * ih2;
-                    const double ib1 = rcp(beta1);
-                    const double beta2 = 2.0 * lt2 * ib1 * ib1 * ih2 * ihE;
-                    const double beta = a2 + lam * alpha * beta2 * Hd;
-                    const double delta = alpha * ib1;
-                    if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
-                    sQd[p] = qd; sHd[p] = Hd; sWd[p] = Wd; sBe[p] = beta; sDe[p] = delta;
-                    sHR[p] = hRp;
-                    Fl = Fr;
-                }
+                wh[2] = sEh[r + 2]; wq[2] = sEq[r + 2]; wH[2] = sEH[r + 2]; wW[2] = sEW[r + 2];
+                Pn = muscl_plus(wh, wq, wH, wW, order);            // Pl_{r+1}
+                const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
+                Mr = muscl_minus(wh, wq, wH, wW, order);           // M_{r+1}
+                double beta;
+                row_update<STAGE2, BATHY>(C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
+                                          sHR, sQd, sHd, sBe, sDe, wd[i], beta);
+                if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
+                Fl = Fr;
             }
         }
         __syncthreads();
         // derived-field ghosts at physical boundaries (A10)
         if (tid == 0 && left_phys) {
-            sQd[0] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[1];
-            sHd[0] = sHd[1]; sBe[0] = sBe[1]; sDe[0] = sDe[1];
+            sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
+            sHd[-1] = sHd[0]; sBe[-1] = sBe[0]; sDe[-1] = sDe[0];
         }
         if (tid == 32 && right_phys) {
-            sQd[L + 1] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L];
-            sHd[L + 1] = sHd[L]; sBe[L + 1] = sBe[L]; sDe[L + 1] = sDe[L];
+            sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
+            sHd[L] = sHd[L - 1]; sBe[L] = sBe[L - 1]; sDe[L] = sDe[L - 1];
         }
         __syncthreads();
 
@@ -506,29 +559,29 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         double *sHB = sEq;            // hbar[r], r in [0, L)
         double *pcr0 = sEH;           // PCR buffers: 2 x 3 x NT doubles over sEH..sEW
         double *pcr1 = sEH + 3 * NT;
-        double rho_loc = 0.0;
-        {
-            const int r0 = tid * MCH;
-            // register windows over p = r0 .. r0+MCH+1 (rows r0-1 .. r0+MCH)
-            double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
+        // register windows over rows r0-1 .. r0+MCH
+        double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
 #pragma unroll
-            for (int k = 0; k < MCH + 2; k++) {
-                vb[k] = sBe[r0 + k]; vd[k] = sDe[r0 + k]; vH[k] = sHd[r0 + k]; vq[k] = sQd[r0 + k];
-            }
+        for (int k = 0; k < MCH + 2; k++) {
+            vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; vH[k] = sHd[r0 - 1 + k]; vq[k] = sQd[r0 - 1 + k];
+        }
+        double hb[MCH];
+        {
             double am[MCH], cm[MCH], dm[MCH];
 #pragma unroll
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
-                double a = 0.0, c = 0.0, dg = 1.0, rhs = 0.0;
-                if (r < L) {
-                    const double rl = (r == 0) ? 0.0 : t2 * (vb[i] + vb[i + 1]) * 0.5;
-                    const double rr = (r == L - 1) ? 0.0 : t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
-                    const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
-                    rhs = sHR[r + 1] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
-                          - ml * (vH[i + 1] - vH[i]);
-                    a = -rl; c = -rr; dg = 1.0 + rl + rr;
-                    rho_loc = rr > rho_loc ? rr : rho_loc;
-                }
+                const bool in = r < L;                    // rows >= L: identity rows
+                const double rl0 = t2 * (vb[i] + vb[i + 1]) * 0.5;
+                const double rr0 = t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
+                const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
+                const double rhs0 = sHR[r] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
+                                    - ml * (vH[i + 1] - vH[i]);
+                const double rl = (in && r != 0) ? rl0 : 0.0;        // truncated / Neumann ends
+                const double rr = (in && r != L - 1) ? rr0 : 0.0;
+                const double rhs = in ? rhs0 : 0.0;
+                const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
+                rho_loc = fmaxf(rho_loc, float(rr));
                 if (i == 0) {
                     const double inv = rcp(dg);
                     am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
@@ -557,8 +610,6 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             double Q1 = __shfl_down_sync(0xffffffffu, am[0], 1);
             double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
             if (lane == 0) { xch[wid][0] = dm[0]; xch[wid][1] = am[0]; xch[wid][2] = cm[0]; }
-            rho_loc = warp_max(rho_loc);
-            if (lane == 0) red[0][wid] = rho_loc;
             __syncthreads();
             if (lane == 31) {
                 if (wid + 1 < NT / 32) { P1 = xch[wid + 1][0]; Q1 = xch[wid + 1][1]; R1 = xch[wid + 1][2]; }
@@ -578,22 +629,22 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             double *cur = pcr0, *nxt = pcr1;
             cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
             {
-                const double ea = fabs(A_), ec = fabs(C_);
-                double ev = warp_max(ea > ec ? ea : ec);
-                if (lane == 0) red[1][wid] = ev;
+                const float ea = float(fabs(A_)), ec = float(fabs(C_));
+                float ev = ea > ec ? ea : ec;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ev = fmaxf(ev, __shfl_xor_sync(0xffffffffu, ev, o));
+                if (lane == 0) redf[wid] = ev;
             }
             __syncthreads();
             int lim = NT;
             {
-                double e0 = 0.0;
+                float e0 = 0.0f;
 #pragma unroll
-                for (int q = 0; q < NT / 32; q++) e0 = fmax(e0, red[1][q]);
-                e0 *= 1.05;
-                if (e0 == 0.0) lim = 1;
-                else if (e0 < 0.5) {
-                    const double need = 64.0 / -log2(e0);    // 2^s >= need
+                for (int q = 0; q < NT / 32; q++) e0 = fmaxf(e0, redf[q]);
+                if (e0 < 0.4f) {                       // repeated squaring, 10% margin per step
+                    float ee = e0 * 1.1f;
                     int sdl = 1;
-                    while (sdl < NT && double(sdl) < need) sdl <<= 1;
+                    while (sdl < NT && ee > 5.42e-20f) { ee = ee * ee * 1.1f; sdl <<= 1; }   // 2^-64
                     lim = sdl;
                 }
             }
@@ -613,81 +664,71 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 double *tmp = cur; cur = nxt; nxt = tmp;
             }
             const double Xk = D_;
-            cur[2 * NT + tid] = Xk;     // own slot; neighbours read after the barrier
+            double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
+            if (lane == 31) xch[wid][0] = Xk;       // last chunk of this warp
             __syncthreads();
-            const double XL = (tid > 0) ? cur[2 * NT + tid - 1] : 0.0;
+            if (lane == 0) XL = (wid > 0) ? xch[wid - 1][0] : 0.0;
 #pragma unroll
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
-                const double x = (i == MCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
-                if (r < L) sHB[r] = x;
-            }
-            if (tid == 0) {
-                double rmax = 0.0;
-                for (int q = 0; q < NT / 32; q++) rmax = fmax(rmax, red[0][q]);
-                // overlap check: r^w <= 2^-60 at every truncated end
-                if (rmax > 0.0) {
-                    const double rdec = 2.0 * rmax / ((1.0 + 2.0 * rmax) + sqrt(1.0 + 4.0 * rmax));
-                    const double need = 41.588830833596716 / (-log(rdec));   // 60 ln 2
-                    if ((!left_phys && double(wl) < need) || (!right_phys && double(wr) < need))
-                        errbits |= ERR_OVERLAP;
-                }
-                atomicMax(P.rho_obs, (unsigned long long)__double_as_longlong(rmax));
+                hb[i] = (i == MCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
+                if (r < L) sHB[r] = hb[i];
             }
         }
         __syncthreads();
 
-        // ---- phase 3: back-substitution ---------------------------
+        // ---- phase 3: back-substitution, own rows ------------------
         const bool filt = FINAL && (P.filter_sigma > 0.0);
-        double *sQb = sEH, *sWb = sEW, *sHb = sHR - 2;   // filter scratch (rows r)
-        const int rbeg = filt ? max(0, wl - 2) : wl;
-        const int rend = filt ? min(L, wl + Tk + 2) : wl + Tk;
-        for (int r = rbeg + tid; r < rend; r += NT) {
-            const int p = r + 1;
-            const double hb = sHB[r];
-            const double hl = (r > 0) ? sHB[r - 1] : hb;        // Neumann at physical ends
-            const double hr = (r < L - 1) ? sHB[r + 1] : hb;
-            double qb = sQd[p] - tdx2 * sBe[p] * (hr - hl) - ltdx2 * sDe[p] * (sHd[p + 1] - sHd[p - 1]);
-            double bb = 0.0;
-            if (BATHY) {
+        double *sQb = sEH, *sWb = sEW;                   // unfiltered qbar, Wbar (filter)
+        // staged outputs (index r - wl) at the 16-B aligned bases of arrays 4..7,
+        // whose row data were consumed into registers in phase 2
+        double *oh = smem + 4 * SROWS, *oq = smem + 5 * SROWS, *oK = smem + 6 * SROWS,
+               *oW = smem + 7 * SROWS;
+        const int klo = filt ? wl - 2 : wl, khi = filt ? wl + Tk + 2 : wl + Tk;
+        double qbv[MCH], Hbv[MCH], Wbv[MCH], bbv[MCH];
+        const double hLn = (r0 > 0 && r0 - 1 < L) ? sHB[r0 - 1] : 0.0;
+        const double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            const bool act = (r >= klo) && (r < khi) && (r < L);   // rows this stage needs
+            bbv[i] = 0.0;
+            const double h0 = hb[i];
+            double hl = (i > 0) ? hb[i - 1] : hLn;
+            double hr = (i < MCH - 1) ? hb[i + 1] : hRn;
+            if (r == 0) hl = h0;                           // Neumann at physical ends
+            if (r == L - 1) hr = h0;
+            double qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
+            if (BATHY && act) {
                 const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
                 const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
-                bb = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
-                qb -= tau * g * sEh[r + 3] * (bp - bm) * (0.5 * idx1);     // A9
+                bbv[i] = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
+                qb -= tau * g * sEh[r] * (bp - bm) * (0.5 * idx1);     // A9
             }
             // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),
-            // Wbar = W^dag - lam tau Hbar / hbar^2 = W^dag - lam tau H^dag / (hbar^2 + lam tau^2)
-            const double hb2 = hb * hb;
-            const double Dn = rcp(hb2 + lt2);
-            const double HdD = sHd[p] * Dn;
-            const double Hb = HdD * hb2;
-            const double Wb = sWd[p] - lam * tau * HdD;
-            const bool kept = (r >= wl && r < wl + Tk);
-            if (kept) {
-                if (!(hb > P.h_min)) errbits |= ERR_DRY;
-                if (!isfinite(hb) || !isfinite(qb) || !isfinite(Hb) || !isfinite(Wb))
+            // Wbar = W^dag - lam tau H^dag / (hbar^2 + lam tau^2)
+            const double hb2 = h0 * h0;
+            const double HdD = vH[i + 1] * rcp(hb2 + lt2);
+            qbv[i] = qb;
+            Hbv[i] = HdD * hb2;
+            Wbv[i] = wd[i] - ltau * HdD;
+            if (act && r >= wl && r < wl + Tk) {
+                if (!(h0 > P.h_min)) errbits |= ERR_DRY;
+                if (!isfinite(h0) || !isfinite(qb) || !isfinite(Hbv[i]) || !isfinite(Wbv[i]))
                     errbits |= ERR_NONFINITE;
             }
-            if (filt) {
-                sQb[r] = qb; sWb[r] = Wb; sHb[r] = Hb;
-            } else if (kept) {
-                const size_t gi = mo + (s + (r - wl));
-                B.out[0][gi] = hb; B.out[1][gi] = qb; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
-                B.out[3][gi] = Wb;
-                if (FINAL) {
-                    const double u = qb * rcp(hb), sg = HdD;             // sg = Hbar / hbar^2
-                    umax_loc = fmax(umax_loc, fabs(u));
-                    numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * hb + lam3 * sg * sg));
-                }
-            }
+            if (filt && act) { sQb[r] = qb; sWb[r] = Wbv[i]; }
         }
-        if (filt) {
-            __syncthreads();
-            const double sig16 = P.filter_sigma * (1.0 / 16.0);
-            const bool edge_tile = left_phys || right_phys;
-            for (int r = wl + tid; r < wl + Tk; r += NT) {
+        if (filt) __syncthreads();
+        const double sig16 = P.filter_sigma * (1.0 / 16.0);
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            if (r < wl || r >= wl + Tk) continue;
+            double qo = qbv[i], wo = Wbv[i];
+            if (filt) {
                 double fq[5], fw[5];
-                if (!edge_tile || (r >= 2 && r + 2 < L)) {
+                if (!(left_phys || right_phys) || (r >= 2 && r + 2 < L)) {
 #pragma unroll
                     for (int k = 0; k < 5; k++) { fq[k] = sQb[r + k - 2]; fw[k] = sWb[r + k - 2]; }
                 } else {
@@ -705,18 +746,39 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                     }
                 }
                 // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
-                const double qf = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
-                const double wf = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
-                const double hb = sHB[r], Hb = sHb[r];
-                const double bb = BATHY ? __ldg(P.b + (s + (r - wl))) : 0.0;
-                const size_t gi = mo + (s + (r - wl));
-                B.out[0][gi] = hb; B.out[1][gi] = qf; B.out[2][gi] = BATHY ? Hb + 1.5 * hb * bb : Hb;
-                B.out[3][gi] = wf;
-                const double ihb = rcp(hb);
-                const double u = qf * ihb, sg = Hb * ihb * ihb;
+                qo = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
+                wo = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
+                if (!isfinite(qo) || !isfinite(wo)) errbits |= ERR_NONFINITE;
+            }
+            const double h0 = hb[i];
+            const int ko = r - wl;
+            oh[ko] = h0; oq[ko] = qo; oK[ko] = BATHY ? Hbv[i] + 1.5 * h0 * bbv[i] : Hbv[i]; oW[ko] = wo;
+            if (FINAL) {
+                const double u = qo * rcp(h0), sg = Hbv[i] * rcp(h0 * h0);
                 umax_loc = fmax(umax_loc, fabs(u));
-                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * hb + lam3 * sg * sg));
-                if (!isfinite(qf) || !isfinite(wf)) errbits |= ERR_NONFINITE;
+                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h0 + lam3 * sg * sg));
+            }
+        }
+        // ---- stores: TMA bulk (aligned interior tiles) or coalesced copies -------
+        const size_t gdst = mo + size_t(s);
+        const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
+        if (bulk_out) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                const unsigned bytes = unsigned(Tk) * 8u;
+                bulk_s2g(B.out[0] + gdst, oh, bytes);
+                bulk_s2g(B.out[1] + gdst, oq, bytes);
+                bulk_s2g(B.out[2] + gdst, oK, bytes);
+                bulk_s2g(B.out[3] + gdst, oW, bytes);
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            }
+        } else {
+            __syncthreads();
+            for (int k = tid; k < Tk; k += NT) {
+                B.out[0][gdst + k] = oh[k]; B.out[1][gdst + k] = oq[k];
+                B.out[2][gdst + k] = oK[k]; B.out[3][gdst + k] = oW[k];
             }
         }
     }
@@ -729,22 +791,41 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         if ((tid & 31) == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
     }
 
-    if (FINAL) {
-        // ---- dt maxima for the next step and next time level ----------
+    // ---- per-CTA reductions: rho (overlap check), dt maxima, next time level ----
+    {
         double um = warp_max(umax_loc), nm = warp_max(numax_loc);
+        float rf = rho_loc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rf = fmaxf(rf, __shfl_xor_sync(0xffffffffu, rf, o));
         const int lane = tid & 31, wid = tid >> 5;
         __syncthreads();
-        if (lane == 0) { red[0][wid] = um; red[1][wid] = nm; }
+        if (lane == 0) { red[0][wid] = um; red[1][wid] = nm; redf[wid] = rf; }
         __syncthreads();
         if (tid == 0) {
-            for (int q = 1; q < NT / 32; q++) { um = fmax(um, red[0][q]); nm = fmax(nm, red[1][q]); }
-            const int slot_w = (P.kslot + 1) % 3;
-            atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
-            atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
-            if (j == 0) {   // t^{n+1} of this member, in the other parity slot
-                const double tm = P.t[P.kpar * members + m];
-                const double t_end = P.ctrl->t_end;
-                P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
+            for (int q = 1; q < NT / 32; q++) {
+                um = fmax(um, red[0][q]); nm = fmax(nm, red[1][q]); rf = fmaxf(rf, redf[q]);
+            }
+            // overlap check: r^w <= 2^-60 at each truncated end
+            if (rf > 0.0f && dtm != 0.0) {
+                const double rho = double(rf) * (1.0 + 1e-6);
+                const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
+                const int wmin = min(left_phys ? 1 << 30 : wl, right_phys ? 1 << 30 : wr);
+                if (wmin < (1 << 30)) {
+                    double x = 1.0, b = rdec;          // rdec^wmin by squaring
+                    for (int k = wmin; k > 0; k >>= 1) { if (k & 1) x *= b; b *= b; }
+                    if (x > 8.673617379884035e-19) atomicOr(P.err, ERR_OVERLAP);   // 2^-60
+                }
+                atomicMax(P.rho_obs, (unsigned long long)__double_as_longlong(rho));
+            }
+            if (FINAL) {
+                const int slot_w = (P.kslot + 1) % 3;
+                atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
+                atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
+                if (j == 0) {   // t^{n+1} of this member, in the other parity slot
+                    const double tm = P.t[P.kpar * members + m];
+                    const double t_end = P.ctrl->t_end;
+                    P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
+                }
             }
         }
     }

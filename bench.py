@@ -47,16 +47,24 @@ def parse():
     p.add_argument("--cells", type=int, default=4096)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--config", default="cfg3", choices=["cfg3", "cfg5"],
+                   help="cfg3: ensemble (default, headline); cfg5: single 2^28-cell domain with bathymetry")
+    p.add_argument("--cells5", type=int, default=1 << 28)
     return p.parse_args()
 
 
 def config_dict(a, world):
+    if a.config == "cfg5":
+        return {"workload": "cfg5_large_domain: %d cells, periodic, bathymetry 0.2 sin, lambda 1e4, "
+                            "100-step config, A19 filter" % a.cells5, "cells": a.cells5,
+                "cfl_imex": 2.0, "mcfl": 0.5, "order": 2, "parallelism": "single GPU",
+                "l2": "inputs (8 GiB state) larger than L2: no flush"}
     return {"workload": "cfg3_ensemble: %d members x %d cells per GPU, periodic, 200-step config"
                         % (a.members, a.cells),
             "members_per_gpu": a.members, "cells_per_member": a.cells,
             "global_members": a.members * world, "lambda": "log-uniform [1e2, 1e4] per member",
             "cfl_imex": 2.0, "mcfl": 0.5, "order": 2, "tableau": "P:371-386 (gamma = 1 - 1/sqrt2)",
-            "parallelism": f"ensemble-sharded x{world}",
+            "filter": "A19, sigma 0.25 on q and W", "parallelism": f"ensemble-sharded x{world}",
             "l2": "inputs (512 MiB state) larger than L2 (126 MB): no flush"}
 
 
@@ -196,9 +204,29 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    w = W.cfg3(members=a.members, n=a.cells, first_member=rank * a.members)
-    s = hsgn.solver_for(w)
-    Ntot = w.n * w.members
+    bathy = False
+    if a.config == "cfg5":
+        # single large periodic domain with bathymetry, generated on the device
+        (h, q, K, Wf, b), meta = W.cfg5(a.cells5, device="cuda")
+        s = hsgn.Solver(meta["n"], 1, 0.0, meta["L"], bc=("periodic", "periodic"))
+        s.set_params(9.81, meta["lam"], meta["cfl"], meta["mcfl"])
+        s.set_bathymetry(b)
+        s.set_filter(0.25)
+        s.set_state(h, q, K, Wf)
+        host_state = [x.cpu() for x in (h, q, K, Wf)] if not a.no_e2e else None
+        del h, q, K, Wf
+        Ntot = meta["n"]
+        bathy = True
+
+        class _W:   # minimal stand-in for the e2e/cpu legs
+            members = 1
+            n = meta["n"]
+        w = _W()
+    else:
+        w = W.cfg3(members=a.members, n=a.cells, first_member=rank * a.members)
+        s = hsgn.solver_for(w)
+        Ntot = w.n * w.members
+        host_state = None
     state_bytes = 4 * 8 * Ntot
 
     def barrier():
@@ -238,15 +266,20 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     t2 = ms2 / a.steps / 1e3
     t1 = ms1 / a.steps / 1e3
-    ach2 = B_STAGE2 * Ntot / t2 / 1e9
-    ach1 = B_STAGE1 * Ntot / t1 / 1e9
+    bs1 = B_STAGE1 + (8 if bathy else 0)    # + b read per stage
+    bs2 = B_STAGE2 + (8 if bathy else 0)
+    ach2 = bs2 * Ntot / t2 / 1e9
+    ach1 = bs1 * Ntot / t1 / 1e9
     traffic = profile_traffic(Ntot)
 
     # e2e through the public API with host buffers: pinned host state uploaded,
     # K steps each reading back the per-member dt, final state downloaded.
     e2e = None
     if not a.no_e2e:
-        pin = [torch.from_numpy(np.ascontiguousarray(f.reshape(-1))).pin_memory() for f in (w.h, w.q, w.K, w.W)]
+        if host_state is not None:
+            pin = [x.pin_memory() for x in host_state]
+        else:
+            pin = [torch.from_numpy(np.ascontiguousarray(f.reshape(-1))).pin_memory() for f in (w.h, w.q, w.K, w.W)]
         outp = [torch.empty(Ntot, dtype=torch.float64).pin_memory() for _ in range(4)]
         barrier()
         torch.cuda.synchronize()
@@ -268,7 +301,7 @@ def main():
                "what": "Solver.set_state(pinned host) + K x Solver.step(return_dt) + get_state(pinned host), wall clock, max over ranks"}
 
     cpu = None
-    if rank == 0 and not a.no_cpu:
+    if rank == 0 and not a.no_cpu and a.config == "cfg3":
         threads = os.cpu_count() or 1
         nm = max(4 * threads, 16)
         rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0)
@@ -284,10 +317,10 @@ def main():
         "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s",
                      "frac": ach2 / peak, "traffic": traffic,
                      "kernel": "stage_kernel<STAGE2,FINAL> (stage 2)",
-                     "bytes_model": "96 B/cell per stage-2 launch (read U^n, U1; write U^{n+1})",
+                     "bytes_model": f"{bs2} B/cell per stage-2 launch (read U^n, U1{', b' if bathy else ''}; write U^{{n+1}})",
                      "peak_source": peak_src,
-                     "stage1": {"achieved": ach1, "frac": ach1 / peak, "bytes_model": "64 B/cell"},
-                     "step_avg_frac": (80.0 * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak},
+                     "stage1": {"achieved": ach1, "frac": ach1 / peak, "bytes_model": f"{bs1} B/cell"},
+                     "step_avg_frac": (0.5 * (bs1 + bs2) * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches * world,

@@ -141,10 +141,13 @@ def cfg1(n: int = 1000, lam: float = 500.0, x0: float = -50.0) -> Workload:
                     t_end=20.0, filter_sigma=0.25, meta=dict(h0=1.0, A=0.2, x0=x0, L=200.0))
 
 
-def cfg2(lam: float, n: int = 1 << 16, width_cells: float = 0.0) -> Workload:
+def cfg2(lam: float, n: int = 1 << 16, width_cells: float = 50.0) -> Workload:
     """Dispersive dam break on [-300, 300] with walls: h = 1.8 left / 1.0 right,
-    u = 0, K = h^2, W = 0, t_end = 48.  width_cells > 0 smooths the step as a tanh
-    of that many cells (fallback recipe of DESIGN.md section 5)."""
+    u = 0, K = h^2, W = 0, t_end = 48.  The step is regularised as a tanh over
+    width_cells cells (50 by default, ~0.46 m at N = 2^16): the unlimited MUSCL
+    of the paper breaks down (coercivity) within ~50 steps on a sharp
+    step at every lambda and on a 5-cell tanh at lambda >= 1e3 (DESIGN.md A20);
+    width_cells = 0 gives the sharp step."""
     x = cell_centres(-300.0, 300.0, n)
     dx = 600.0 / n
     if width_cells > 0:
@@ -261,3 +264,55 @@ def lake_at_rest(n: int, lam: float, L: float = 40.0, amp: float = 0.1, h_ref: f
     K = h * (h + 1.5 * b)
     return Workload("lake_at_rest", n, 1, 0.0, L, tuple(bc), np.array([lam]), h[None],
                     z[None].copy(), K[None], z[None].copy(), b=b)
+
+
+def cfg5(n: int = 1 << 28, seed: int = 7539005, lam: float = 1e4, device: str | None = None,
+         first: int = 0, count: int | None = None):
+    """Single large periodic domain: dx = 1/16, L = n/16; zeta = 1 + 0.05 G(x),
+    G = unit-RMS sum of 64 cosine modes with distinct wavenumbers m_j uniform in
+    [L/128, L/16] (wavelengths 16-128 m), A_j ~ N(0,1), phi_j ~ U[0, 2 pi);
+    b = 0.2 sin(2 pi x / 128); h = zeta - b, u = 0, eta = h, w = 0,
+    K = h (h + 1.5 b), W = 0; lambda = 1e4, 100 steps, CFL_IMEX 2, MCFL 0.5, A19
+    filter on (the literal scheme amplifies a 1e-14 perturbation to 1e-7 in the
+    100 steps at n = 2^18; filtered: 1e-10).
+
+    Returns the cells [first, first + count) (a slab), as numpy arrays, or as
+    torch tensors on `device` (fp64; used for n = 2^28, where numpy is slow)."""
+    L = n / 16.0
+    rng = np.random.Generator(np.random.PCG64(seed))
+    lo, hi = max(1, int(L / 128)), max(2, int(L / 16))
+    m = rng.choice(np.arange(lo, hi + 1), size=64, replace=False).astype(np.float64)
+    A = rng.standard_normal(64)
+    ph = rng.uniform(0.0, 2 * np.pi, size=64)
+    A = A / np.sqrt(0.5 * np.sum(A * A))             # unit RMS of sum A_j cos(...)
+    count = n - first if count is None else count
+    mb = L / 128.0
+    if device is None:
+        x = cell_centres(0.0, L, n)[first:first + count]
+        G = np.zeros(count)
+        for j in range(64):
+            G += A[j] * np.cos(2 * np.pi * m[j] * x / L + ph[j])
+        b = 0.2 * np.sin(2 * np.pi * mb * x / L)
+        zeta = 1.0 + 0.05 * G
+        h = zeta - b
+        z = np.zeros(count)
+        out = (h, z, h * (h + 1.5 * b), z.copy(), b)
+    else:
+        import torch
+        x = (torch.arange(first, first + count, dtype=torch.float64, device=device) + 0.5) * (L / n)
+        G = torch.zeros(count, dtype=torch.float64, device=device)
+        for j in range(64):
+            G += A[j] * torch.cos(2 * np.pi * m[j] * x / L + ph[j])
+        b = 0.2 * torch.sin(2 * np.pi * mb * x / L)
+        h = 1.0 + 0.05 * G - b
+        z = torch.zeros_like(h)
+        out = (h, z, h * (h + 1.5 * b), z.clone(), b)
+    return out, dict(n=n, L=L, lam=lam, cfl=2.0, mcfl=0.5, steps=100, seed=seed)
+
+
+def cfg5_workload(n: int = 1 << 22, seed: int = 7539005, lam: float = 1e4) -> Workload:
+    """cfg5 at a reduced size as a numpy Workload (parity cases)."""
+    (h, q, K, W, b), meta = cfg5(n, seed, lam)
+    return Workload(f"cfg5_n{n}", n, 1, 0.0, meta["L"], ("periodic", "periodic"),
+                    np.array([lam]), h[None], q[None], K[None], W[None], b=b, cfl=2.0, mcfl=0.5,
+                    steps=100, filter_sigma=0.25, meta=meta)

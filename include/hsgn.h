@@ -69,7 +69,10 @@ typedef enum {
 typedef enum {
     HSGN_BC_PERIODIC = 0,     /* cyclic (both sides must be periodic)           */
     HSGN_BC_WALL = 1,         /* reflecting: h, K, W even, q odd; Neumann depth rows (A10) */
-    HSGN_BC_TRANSMISSIVE = 2  /* zero-order extrapolation; Neumann depth rows */
+    HSGN_BC_TRANSMISSIVE = 2, /* zero-order extrapolation; Neumann depth rows */
+    HSGN_BC_HALO = 3          /* neighbouring slab of one large domain: w + 3 ghost cells
+                                 exchanged before each stage;
+                                 requires n_members == 1 and a group or NCCL */
 } hsgn_bc;
 
 /* Double Butcher tableau.  Validated by hsgn_set_tableau:
@@ -191,6 +194,24 @@ int64_t hsgn_launch_count(const hsgn_ctx *ctx);
  * member, threads per CTA, max rows per CTA. */
 hsgn_status hsgn_get_geometry(const hsgn_ctx *ctx, int32_t *tile_cells, int32_t *overlap,
                               int32_t *tiles_per_member, int32_t *threads, int32_t *max_rows);
+
+/* ---- slab decomposition of one domain --
+ * A domain of N cells split into P contiguous slabs, slab i a context whose
+ * interior sides are HSGN_BC_HALO.  Each step: max-reduce the dt maxima across
+ * slabs, dt, exchange w + 3 boundary cells of U^n, stage 1, exchange U1,
+ * stage 2, commit.  Two transports:
+ *   group: all slabs in this process on one device and one stream (device-to-
+ *          device copies; ctxs in ring order, ctxs[i-1] left of ctxs[i]);
+ *          bathymetry must be set before hsgn_group_create;
+ *   NCCL:  one slab per process/GPU, ring by rank (send/recv of the halos,
+ *          all-reduce max of the dt maxima), on the context's stream. */
+typedef struct hsgn_group hsgn_group;
+hsgn_status hsgn_group_create(hsgn_ctx *const *ctxs, int32_t n, hsgn_group **out);
+hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps);
+void hsgn_group_destroy(hsgn_group *g);
+/* 128-byte ncclUniqueId (rank 0; the caller broadcasts it, e.g. torch.distributed) */
+hsgn_status hsgn_nccl_unique_id(void *id);
+hsgn_status hsgn_attach_nccl(hsgn_ctx *ctx, const void *id, int32_t rank, int32_t world);
 
 const char *hsgn_status_string(hsgn_status s);
 const char *hsgn_last_error(const hsgn_ctx *ctx);

@@ -17,8 +17,12 @@ DEPS = SRC + [os.path.join(PKG, "csrc", "hsgn_kernels.cuh"), os.path.join(ROOT, 
 LIB = os.path.join(PKG, "lib", "libhsgn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NCCL = os.environ.get("HSGN_NCCL_HOME", "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-         "--expt-relaxed-constexpr", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"),
+         "-I", os.path.join(NCCL, "include")]
+LINK = ["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker",
+        "-rpath," + os.path.join(NCCL, "lib")]
 
 
 def stale() -> bool:
@@ -33,7 +37,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     if out == LIB and not force and not stale():
         return LIB
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SRC, "-cudart", "static"]
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SRC, "-cudart", "static", *LINK]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = out + ".ptxas.log"
     with open(log, "w") as f:

@@ -8,6 +8,7 @@
 // starts with dt_commit(k, no commit).  Never allocates
 // device memory and never falls back to the CPU.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -27,6 +28,7 @@ constexpr int GRAPH_STEPS = 18;   // steps per captured graph: a multiple of 6, 
                                   // parity (k mod 2) and the maxima slot (k mod 3) repeat
 constexpr int POLL_STEPS = 256;   // advance_to polls the device every POLL_STEPS
 constexpr int T_MIN = 64;         // smallest kept tile (bounds the partials workspace)
+constexpr int H_MAX = (LCAP - 2 - T_MIN) / 2 + 3;   // largest slab halo (overlap + stencil)
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -63,6 +65,11 @@ struct hsgn_ctx {
     Ctrl ctrl_host{0.0, 0.0};
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     long long launches = 0;
+    // slab decomposition (BC_HALO sides): halo receive buffers [9][H_MAX] per side
+    double *halo_l = nullptr, *halo_r = nullptr;
+    bool slab = false;
+    ncclComm_t nccl = nullptr;
+    int nrank = 0, nworld = 1;
     std::string last_error;
 };
 
@@ -105,6 +112,11 @@ Params make_params(hsgn_ctx *c, long long k)
     P.b = c->bathy ? c->b : nullptr;
     P.lam = c->lamd; P.t = c->t; P.dt = c->dt; P.maxes = c->maxes; P.err = c->err;
     P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.ctrl = c->ctrl;
+    P.H = c->w + 3;
+    for (int k = 0; k < 9; k++) {
+        P.halo_l[k] = c->halo_l ? c->halo_l + k * H_MAX : nullptr;
+        P.halo_r[k] = c->halo_r ? c->halo_r + k * H_MAX : nullptr;
+    }
     return P;
 }
 
@@ -232,9 +244,21 @@ hsgn_status ready(hsgn_ctx *c)
     return HSGN_OK;
 }
 
+hsgn_status slab_step(std::vector<hsgn_ctx *> &g, long long k, bool nccl);
+
 hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
 {
     if (n_steps <= 0) return HSGN_OK;
+    if (c->slab) {
+        if (!c->nccl)
+            return fail(c, HSGN_E_INVALID, "BC_HALO sides need hsgn_group_run_steps or hsgn_attach_nccl");
+        std::vector<hsgn_ctx *> g{c};
+        for (long long i = 0; i < n_steps; i++) {
+            hsgn_status st = slab_step(g, c->host_steps, true);
+            if (st != HSGN_OK) return st;
+        }
+        return HSGN_OK;
+    }
     hsgn_status st = launch_dtc(c, c->host_steps, 0, 1);   // dt of the first step
     if (st != HSGN_OK) return st;
     long long done = 0;
@@ -268,6 +292,144 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
             c->host_steps++;
             done++;
         }
+    }
+    return HSGN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Slab decomposition: one domain split into
+// contiguous slabs whose BC_HALO sides take H = w + 3 ghost cells from the
+// neighbour, exchanged before each stage (U^n before stage 1, U1 before stage
+// 2); the dt maxima are max-reduced across slabs before each step's dt.
+// Transports: in-process loopback group (all slabs on one device and one
+// stream, D2D copies) and NCCL (one slab per process / GPU).
+// ---------------------------------------------------------------------------
+constexpr int GROUP_MAX = 64;
+struct MaxPtrs { unsigned long long *p[GROUP_MAX]; };
+
+__global__ void group_max_kernel(MaxPtrs ptrs, int P, int count)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    unsigned long long mx = 0ull;
+    for (int k = 0; k < P; k++) mx = max(mx, ptrs.p[k][i]);
+    for (int k = 0; k < P; k++) ptrs.p[k][i] = mx;
+}
+
+// halo array index: which = 0 (U^n), 1 (U1), 2 (b)
+double *halo_dst(hsgn_ctx *c, bool left, int which, int f)
+{
+    return (left ? c->halo_l : c->halo_r) + (which == 2 ? 8 : which * 4 + f) * H_MAX;
+}
+
+const double *bnd_src(hsgn_ctx *c, bool right_end, int which, int f, int H)
+{
+    const double *base = which == 2 ? c->b : (which == 0 ? c->buf[c->cur][f] : c->buf[2][f]);
+    return right_end ? base + (c->n - H) : base;
+}
+
+hsgn_status loopback_exchange(std::vector<hsgn_ctx *> &g, int which)
+{
+    const int P = int(g.size());
+    const int nf = which == 2 ? 1 : 4;
+    for (int i = 0; i < P; i++) {
+        hsgn_ctx *c = g[i];
+        const int H = c->w + 3;
+        hsgn_ctx *L = g[(i - 1 + P) % P], *R = g[(i + 1) % P];
+        for (int f = 0; f < nf; f++) {
+            if (c->desc.bc_left == HSGN_BC_HALO)
+                CUDA_TRY(c, cudaMemcpyAsync(halo_dst(c, true, which, f), bnd_src(L, true, which, f, H),
+                                            H * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            if (c->desc.bc_right == HSGN_BC_HALO)
+                CUDA_TRY(c, cudaMemcpyAsync(halo_dst(c, false, which, f), bnd_src(R, false, which, f, H),
+                                            H * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+    return HSGN_OK;
+}
+
+#define NCCL_TRY(c, expr)                                                             \
+    do {                                                                              \
+        ncclResult_t r_ = (expr);                                                     \
+        if (r_ != ncclSuccess)                                                        \
+            return fail((c), HSGN_E_CUDA, std::string(#expr ": ") + ncclGetErrorString(r_)); \
+    } while (0)
+
+hsgn_status nccl_exchange(hsgn_ctx *c, int which)
+{
+    const int H = c->w + 3;
+    const int left = (c->nrank - 1 + c->nworld) % c->nworld, right = (c->nrank + 1) % c->nworld;
+    const int nf = which == 2 ? 1 : 4;
+    NCCL_TRY(c, ncclGroupStart());
+    for (int f = 0; f < nf; f++) {
+        // per peer the order is: my right boundary -> right's left halo, then my
+        // left boundary -> left's right halo (matches for a ring of 2 as well)
+        if (c->desc.bc_right == HSGN_BC_HALO)
+            NCCL_TRY(c, ncclSend(bnd_src(c, true, which, f, H), H, ncclDouble, right, c->nccl, c->stream));
+        if (c->desc.bc_left == HSGN_BC_HALO)
+            NCCL_TRY(c, ncclRecv(halo_dst(c, true, which, f), H, ncclDouble, left, c->nccl, c->stream));
+        if (c->desc.bc_left == HSGN_BC_HALO)
+            NCCL_TRY(c, ncclSend(bnd_src(c, false, which, f, H), H, ncclDouble, left, c->nccl, c->stream));
+        if (c->desc.bc_right == HSGN_BC_HALO)
+            NCCL_TRY(c, ncclRecv(halo_dst(c, false, which, f), H, ncclDouble, right, c->nccl, c->stream));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+    return HSGN_OK;
+}
+
+// one slab step k for every context of g (lockstep, one shared stream) or for
+// the single NCCL-attached context g[0]
+hsgn_status slab_step(std::vector<hsgn_ctx *> &g, long long k, bool nccl)
+{
+    hsgn_status st;
+    const int P = int(g.size());
+    const int slot = int(k % 3);
+    hsgn_ctx *c0 = g[0];
+    const int count = 2 * c0->members;
+    // a. global max of the dt maxima of U^k
+    if (nccl) {
+        unsigned long long *mx = c0->maxes + size_t(slot) * 2 * c0->members;
+        NCCL_TRY(c0, ncclAllReduce(mx, mx, count, ncclUint64, ncclMax, c0->nccl, c0->stream));
+    } else if (P > 1) {
+        MaxPtrs mp{};
+        for (int i = 0; i < P; i++) mp.p[i] = g[i]->maxes + size_t(slot) * 2 * c0->members;
+        group_max_kernel<<<(count + 127) / 128, 128, 0, c0->stream>>>(mp, P, count);
+        c0->launches++;
+        CUDA_TRY(c0, cudaGetLastError());
+    }
+    // b. dt of step k
+    for (auto *c : g) if ((st = launch_dtc(c, k, 0, 1)) != HSGN_OK) return st;
+    // c. U^n halos, stage 1
+    if ((st = nccl ? nccl_exchange(c0, 0) : loopback_exchange(g, 0)) != HSGN_OK) return st;
+    for (auto *c : g) {
+        const Params Pm = make_params(c, k);
+        Bufs B{};
+        for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; }
+        if (c->tab.stages == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
+            if ((st = launch_stage_b<false, true>(c, Pm, B)) != HSGN_OK) return st;
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            if ((st = launch_stage_b<false, false>(c, Pm, B)) != HSGN_OK) return st;
+        }
+    }
+    if (c0->tab.stages == 2) {
+        // d. U1 halos, stage 2
+        if ((st = nccl ? nccl_exchange(c0, 1) : loopback_exchange(g, 1)) != HSGN_OK) return st;
+        for (auto *c : g) {
+            const Params Pm = make_params(c, k);
+            Bufs B{};
+            for (int f = 0; f < 4; f++) {
+                B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; B.out[f] = c->buf[c->cur ^ 1][f];
+            }
+            if ((st = launch_stage_b<true, true>(c, Pm, B)) != HSGN_OK) return st;
+        }
+    }
+    // e. commit step k
+    for (auto *c : g) {
+        if ((st = launch_dtc(c, k + 1, 1, 0)) != HSGN_OK) return st;
+        c->cur ^= 1;
+        c->host_steps++;
     }
     return HSGN_OK;
 }
@@ -327,10 +489,13 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     if (d->n_cells < 4 || d->n_cells > (int64_t(1) << 31) - 1 || d->n_members < 1 ||
         d->n_members > 65535 || !(d->x_max > d->x_min) || (d->order != 1 && d->order != 2))
         return HSGN_E_INVALID;
-    if (d->bc_left < 0 || d->bc_left > 2 || d->bc_right < 0 || d->bc_right > 2) return HSGN_E_INVALID;
+    if (d->bc_left < 0 || d->bc_left > 3 || d->bc_right < 0 || d->bc_right > 3) return HSGN_E_INVALID;
     if ((d->bc_left == HSGN_BC_PERIODIC) != (d->bc_right == HSGN_BC_PERIODIC)) return HSGN_E_INVALID;
+    const bool slab = (d->bc_left == HSGN_BC_HALO || d->bc_right == HSGN_BC_HALO);
+    if (slab && d->n_members != 1) return HSGN_E_INVALID;   // slabs split one domain
     hsgn_ctx *c = new hsgn_ctx();
     c->desc = *d;
+    c->slab = slab;
     c->stream = (cudaStream_t)stream;
     cudaGetDevice(&c->device);
     c->n = int(d->n_cells);
@@ -367,6 +532,7 @@ void hsgn_destroy(hsgn_ctx *c)
 {
     if (!c) return;
     drop_graphs(c);
+    if (c->nccl) ncclCommDestroy(c->nccl);
     delete c;
 }
 
@@ -383,6 +549,7 @@ size_t hsgn_workspace_bytes(const hsgn_ctx *c)
     s += align256(size_t(c->members) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * sizeof(double));  // partials
     s += 256;                                               // scalars
     s += 256;                                               // ctrl
+    s += 2 * align256(9 * size_t(H_MAX) * sizeof(double));  // slab halos
     return s;
 }
 
@@ -411,6 +578,9 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     c->rho_obs = (unsigned long long *)(q + 16);
     q += 256;
     c->ctrl = (Ctrl *)q;
+    q += 256;
+    c->halo_l = (double *)q; q += align256(9 * size_t(H_MAX) * sizeof(double));
+    c->halo_r = (double *)q; q += align256(9 * size_t(H_MAX) * sizeof(double));
     CUDA_TRY(c, cudaMemsetAsync(c->ws + (size_t)((char *)c->err - c->ws), 0, 512, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->b, 0, size_t(c->n) * sizeof(double), c->stream));
     c->ctrl_host = Ctrl{0.0, 0.0};
@@ -482,6 +652,10 @@ hsgn_status hsgn_set_bathymetry(hsgn_ctx *c, const double *b)
         c->bathy = true;
         CUDA_TRY(c, cudaMemcpyAsync(c->b, b, size_t(c->n) * sizeof(double), cudaMemcpyDefault, c->stream));
     }
+    if (c->nccl) {
+        hsgn_status st = nccl_exchange(c, 2);
+        if (st != HSGN_OK) return st;
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return HSGN_OK;
 }
@@ -546,12 +720,20 @@ hsgn_status hsgn_step(hsgn_ctx *c, double dt, double *dt_used)
     if (st != HSGN_OK) return st;
     st = set_ctrl(c, c->ctrl_host.t_end, dt > 0.0 ? dt : 0.0);
     if (st != HSGN_OK) return st;
-    st = launch_dtc(c, c->host_steps, 0, 1);
-    if (st != HSGN_OK) return st;
-    st = enqueue_step(c, c->cur, c->host_steps, nullptr, dt_used ? c->dt_used : nullptr);
-    if (st != HSGN_OK) return st;
-    c->cur ^= 1;
-    c->host_steps++;
+    if (c->slab) {
+        st = run_steps_impl(c, 1);
+        if (st != HSGN_OK) return st;
+        if (dt_used)
+            CUDA_TRY(c, cudaMemcpyAsync(c->dt_used, c->dt, c->members * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+        st = launch_dtc(c, c->host_steps, 0, 1);
+        if (st != HSGN_OK) return st;
+        st = enqueue_step(c, c->cur, c->host_steps, nullptr, dt_used ? c->dt_used : nullptr);
+        if (st != HSGN_OK) return st;
+        c->cur ^= 1;
+        c->host_steps++;
+    }
     if (dt_used) {
         st = reconcile(c);
         CUDA_TRY(c, cudaMemcpy(dt_used, c->dt_used, c->members * sizeof(double), cudaMemcpyDeviceToHost));
@@ -575,6 +757,7 @@ hsgn_status hsgn_run_steps_timed(hsgn_ctx *c, int64_t n_steps, double *stage_ms)
     hsgn_status st = ready(c);
     if (st != HSGN_OK) return st;
     if (n_steps < 0 || !stage_ms) return HSGN_E_INVALID;
+    if (c->slab) return fail(c, HSGN_E_INVALID, "hsgn_run_steps_timed: not for slab contexts");
     st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
     if (st != HSGN_OK) return st;
     std::vector<cudaEvent_t> ev(size_t(n_steps) * 3);
@@ -695,6 +878,75 @@ hsgn_status hsgn_get_geometry(const hsgn_ctx *c, int32_t *T, int32_t *w, int32_t
     if (tiles) *tiles = c->tiles;
     if (threads) *threads = NT;
     if (max_rows) *max_rows = LCAP;
+    return HSGN_OK;
+}
+
+
+// ---- slab groups and NCCL ---------------------------------
+
+struct hsgn_group {
+    std::vector<hsgn_ctx *> ctx;
+};
+
+hsgn_status hsgn_group_create(hsgn_ctx *const *ctxs, int32_t n, hsgn_group **out)
+{
+    if (!ctxs || !out || n < 1 || n > GROUP_MAX) return HSGN_E_INVALID;
+    *out = nullptr;
+    hsgn_ctx *c0 = ctxs[0];
+    for (int i = 0; i < n; i++) {
+        hsgn_ctx *c = ctxs[i];
+        hsgn_status st = ready(c);
+        if (st != HSGN_OK) return st;
+        if (c->stream != c0->stream || c->w != c0->w || c->members != c0->members ||
+            c->tab.stages != c0->tab.stages || c->host_steps != c0->host_steps || c->nccl)
+            return fail(c, HSGN_E_INVALID, "group: contexts must share stream, overlap, tableau and step");
+        if (c->n < c->w + 3) return fail(c, HSGN_E_INVALID, "group: slab shorter than its halo");
+    }
+    hsgn_group *g = new hsgn_group();
+    g->ctx.assign(ctxs, ctxs + n);
+    if (c0->bathy) {
+        hsgn_status st = loopback_exchange(g->ctx, 2);   // static bathymetry halos
+        if (st != HSGN_OK) { delete g; return st; }
+    }
+    *out = g;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps)
+{
+    if (!g || n_steps < 0) return HSGN_E_INVALID;
+    for (auto *c : g->ctx) {
+        hsgn_status st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
+        if (st != HSGN_OK) return st;
+    }
+    for (int64_t i = 0; i < n_steps; i++) {
+        hsgn_status st = slab_step(g->ctx, g->ctx[0]->host_steps, false);
+        if (st != HSGN_OK) return st;
+    }
+    return HSGN_OK;
+}
+
+void hsgn_group_destroy(hsgn_group *g) { delete g; }
+
+hsgn_status hsgn_nccl_unique_id(void *id)
+{
+    if (!id) return HSGN_E_INVALID;
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return HSGN_E_CUDA;
+    memcpy(id, &u, sizeof(u));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_attach_nccl(hsgn_ctx *c, const void *id, int32_t rank, int32_t world)
+{
+    if (!c || !id || world < 1 || rank < 0 || rank >= world) return HSGN_E_INVALID;
+    if (!c->slab) return fail(c, HSGN_E_INVALID, "attach_nccl: context has no BC_HALO side");
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof(u));
+    NCCL_TRY(c, ncclCommInitRank(&c->nccl, world, u, rank));
+    c->nrank = rank;
+    c->nworld = world;
+    if (c->bathy) return nccl_exchange(c, 2);
     return HSGN_OK;
 }
 

@@ -47,7 +47,7 @@ constexpr int SROWS = LCAP + 8;     // smem row capacity per array (even: 16-B a
 constexpr int NARR = 9;             // smem arrays
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
 
-enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2 };
+enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2, BC_HALO = 3 };
 enum { ERR_COERC = 1u, ERR_DRY = 2u, ERR_NONFINITE = 4u, ERR_OVERLAP = 8u, ERR_DT = 16u };
 
 struct Ctrl {            // device-resident run control (read by stage kernels)
@@ -73,6 +73,11 @@ struct Params {
     unsigned long long *rho_obs;     // max rho over tiles (double bits)
     const Ctrl *ctrl;
     int kslot, kpar;                 // host step index k: k mod 3, k mod 2
+    // slab decomposition (BC_HALO sides): ghost cells received from the
+    // neighbouring slab, H cells each: [0..3] U^n fields, [4..7] U1, [8] b
+    const double *halo_l[9];
+    const double *halo_r[9];
+    int H;
 };
 
 struct Bufs {
@@ -153,12 +158,23 @@ __device__ __forceinline__ int map_cell(int c, int n, int bcl, int bcr, double &
     return c;
 }
 
-__device__ __forceinline__ double bathy_at(const double *__restrict__ b, int c, int n, int bcl,
-                                           int bcr)
+__device__ __forceinline__ double bathy_at(const Params &P, int c)
 {
+    if (c < 0 && P.bcl == BC_HALO) return P.halo_l[8][c + P.H];
+    if (c >= P.n && P.bcr == BC_HALO) return P.halo_r[8][c - P.n];
     double par;
-    int cc = map_cell(c, n, bcl, bcr, par);
-    return __ldg(b + cc);
+    return __ldg(P.b + map_cell(c, P.n, P.bcl, P.bcr, par));
+}
+
+// Source of field f (0..3 state, +4 for U1) at global cell c of member offset mo:
+// the slab's own array, a halo buffer (BC_HALO), or the BC index map.
+__device__ __forceinline__ const double *cell_src(const Params &P, const double *base, int f, size_t mo,
+                                                  int c)
+{
+    if (c < 0 && P.bcl == BC_HALO) return P.halo_l[f] + (c + P.H);
+    if (c >= P.n && P.bcr == BC_HALO) return P.halo_r[f] + (c - P.n);
+    double par;
+    return base + mo + map_cell(c, P.n, P.bcl, P.bcr, par);
 }
 
 // dt rule of P:613-617 (reading A7 for nu_max): dt_bar = CFL dx / nu_max; if
@@ -274,9 +290,9 @@ __device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int
     const double sg = HE * ih2;                                      // eta/h
     double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
     if (BATHY) {
-        const double bm = bathy_at(P.b, start + rr - 1, n, P.bcl, P.bcr);
-        const double b0 = bathy_at(P.b, start + rr, n, P.bcl, P.bcr);
-        const double bp = bathy_at(P.b, start + rr + 1, n, P.bcl, P.bcr);
+        const double bm = bathy_at(P, start + rr - 1);
+        const double b0 = bathy_at(P, start + rr);
+        const double bp = bathy_at(P, start + rr + 1);
         Dxb = (bp - bm) * (0.5 * C.idx);
         // hydrostatic term in zeta-form (A9)
         const double Gr = C.g * (hE + ch[2]) * 0.5, Gl = C.g * (ch[0] + hE) * 0.5;
@@ -345,16 +361,19 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const size_t mo = size_t(m) * n;
 
     // ---- tile geometry ------------------------------------------------------
-    const bool periodic = (P.bcl == BC_PERIODIC);
+    // physical sides (wall, transmissive) clip the overlap; periodic and halo
+    // (neighbouring slab) sides extend the tile into real data
+    const bool physL = (P.bcl == BC_WALL || P.bcl == BC_TRANSMISSIVE);
+    const bool physR = (P.bcr == BC_WALL || P.bcr == BC_TRANSMISSIVE);
     const int s = j * P.T;
     const int e = min(n, s + P.T);
     const int Tk = e - s;
-    const int wl = periodic ? P.w : min(P.w, s);
-    const int wr = periodic ? P.w : min(P.w, n - e);
+    const int wl = physL ? min(P.w, s) : P.w;
+    const int wr = physR ? min(P.w, n - e) : P.w;
     const int start = s - wl;
     const int L = Tk + wl + wr;
-    const bool left_phys = !periodic && (start == 0);
-    const bool right_phys = !periodic && (start + L == n);
+    const bool left_phys = physL && (start == 0);
+    const bool right_phys = physR && (start + L == n);
 
     // ---- shared memory: 9 arrays of SROWS doubles, all indexed by tile row r
     // (r in [-3, L+3)).  Interior tiles are filled by TMA bulk copies, which
@@ -394,13 +413,12 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         }
     } else {
         for (int r = tid - 3; r < L + 3; r += NT) {
-            double par;
-            const size_t gi = mo + map_cell(start + r, n, P.bcl, P.bcr, par);
-            cp_async8(sEh + r, B.Un[0] + gi); cp_async8(sEq + r, B.Un[1] + gi);
-            cp_async8(sEH + r, B.Un[2] + gi); cp_async8(sEW + r, B.Un[3] + gi);
+            const int c = start + r;
+            cp_async8(sEh + r, cell_src(P, B.Un[0], 0, mo, c)); cp_async8(sEq + r, cell_src(P, B.Un[1], 1, mo, c));
+            cp_async8(sEH + r, cell_src(P, B.Un[2], 2, mo, c)); cp_async8(sEW + r, cell_src(P, B.Un[3], 3, mo, c));
             if (STAGE2) {
-                cp_async8(sHR + r, B.U1[0] + gi); cp_async8(sQd + r, B.U1[1] + gi);
-                cp_async8(sHd + r, B.U1[2] + gi); cp_async8(sBe + r, B.U1[3] + gi);
+                cp_async8(sHR + r, cell_src(P, B.U1[0], 4, mo, c)); cp_async8(sQd + r, cell_src(P, B.U1[1], 5, mo, c));
+                cp_async8(sHd + r, cell_src(P, B.U1[2], 6, mo, c)); cp_async8(sBe + r, cell_src(P, B.U1[3], 7, mo, c));
             }
         }
     }
@@ -455,9 +473,9 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             const double wE = P.wE, wR = P.wR;
             for (int r = tid - 3; r < L + 3; r += NT) {
                 double par = 1.0;
-                int c = start + r;
-                if (!interior) c = map_cell(c, n, P.bcl, P.bcr, par);
-                const double bb = BATHY ? __ldg(P.b + c) : 0.0;
+                const int c = start + r;
+                if (!interior) (void)map_cell(c, n, P.bcl, P.bcr, par);   // q parity of wall ghosts
+                const double bb = BATHY ? bathy_at(P, c) : 0.0;
                 double eh = sEh[r], eq = par * sEq[r], eK = sEH[r], eW = sEW[r];
                 if (STAGE2) {
                     const double h1 = sHR[r], q1 = par * sQd[r], K1 = sHd[r], W1 = sBe[r];
@@ -700,9 +718,9 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             if (r == L - 1) hr = h0;
             double qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
             if (BATHY && act) {
-                const double bm = bathy_at(P.b, start + r - 1, n, P.bcl, P.bcr);
-                const double bp = bathy_at(P.b, start + r + 1, n, P.bcl, P.bcr);
-                bbv[i] = bathy_at(P.b, start + r, n, P.bcl, P.bcr);
+                const double bm = bathy_at(P, start + r - 1);
+                const double bp = bathy_at(P, start + r + 1);
+                bbv[i] = bathy_at(P, start + r);
                 qb -= tau * g * sEh[r] * (bp - bm) * (0.5 * idx1);     // A9
             }
             // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),

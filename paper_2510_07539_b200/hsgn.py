@@ -16,7 +16,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HSGN_LIB") or os.path.join(_PKG, "lib", "libhsgn.so")
 
-BC = {"periodic": 0, "wall": 1, "transmissive": 2}
+BC = {"periodic": 0, "wall": 1, "transmissive": 2, "halo": 3}
 STATUS = {0: "OK", -1: "E_INVALID", -2: "E_DRY", -3: "E_COERCIVITY", -4: "E_SINGULAR",
           -5: "E_NONFINITE", -6: "E_CUDA", -7: "E_OVERLAP", -8: "E_NOWORKSPACE"}
 
@@ -51,7 +51,8 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_set_params", "hsgn_set_tableau", "hsgn_set_bathymetry", "hsgn_set_filter",
            "hsgn_set_state", "hsgn_get_state", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
            "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
-           "hsgn_status_string", "hsgn_last_error"]
+           "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
+           "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl"]
 
 _lib = None
 
@@ -87,6 +88,11 @@ def load_library(path: str = LIB_PATH):
         "hsgn_launch_count": (C.c_int64, [vp]),
         "hsgn_get_geometry": (st, [vp] + [C.POINTER(C.c_int32)] * 5),
         "hsgn_status_string": (C.c_char_p, [st]),
+        "hsgn_group_create": (st, [C.POINTER(vp), C.c_int32, C.POINTER(vp)]),
+        "hsgn_group_run_steps": (st, [vp, C.c_int64]),
+        "hsgn_group_destroy": (None, [vp]),
+        "hsgn_nccl_unique_id": (st, [C.c_char_p]),
+        "hsgn_attach_nccl": (st, [vp, C.c_char_p, C.c_int32, C.c_int32]),
         "hsgn_last_error": (C.c_char_p, [vp]),
     }
     for name, (res, args) in sig.items():
@@ -266,6 +272,11 @@ class Solver:
     def sync(self):
         self._chk(self.L.hsgn_sync(self.ctx))
 
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int):
+        """Slab of a domain sharded over `world` processes (one GPU each)."""
+        assert len(unique_id) == 128
+        self._chk(self.L.hsgn_attach_nccl(self.ctx, unique_id, rank, world))
+
     def diagnostics(self) -> dict:
         d = Diag()
         self._chk(self.L.hsgn_get_diagnostics(self.ctx, C.byref(d)))
@@ -282,3 +293,67 @@ def solver_for(w, **kw) -> Solver:
         s.set_filter(w.filter_sigma)
     s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
     return s
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = C.create_string_buffer(128)
+    st = L.hsgn_nccl_unique_id(buf)
+    if st != 0:
+        raise HsgnError(st, "ncclGetUniqueId")
+    return buf.raw
+
+
+class Group:
+    """In-process slab group: Solvers (ring order) sharing one stream, stepped in
+    lockstep with device-to-device halo exchange (C ABI hsgn_group_*)."""
+
+    def __init__(self, solvers):
+        self.solvers = list(solvers)
+        self.L = load_library()
+        arr = (C.c_void_p * len(self.solvers))(*[sv.ctx.value for sv in self.solvers])
+        h = C.c_void_p()
+        st = self.L.hsgn_group_create(arr, len(self.solvers), C.byref(h))
+        if st != 0:
+            raise HsgnError(st, self.L.hsgn_last_error(self.solvers[0].ctx).decode())
+        self.g = h
+
+    def run_steps(self, n_steps: int):
+        st = self.L.hsgn_group_run_steps(self.g, int(n_steps))
+        if st != 0:
+            raise HsgnError(st, self.L.hsgn_last_error(self.solvers[0].ctx).decode())
+
+    def close(self):
+        if getattr(self, "g", None):
+            self.L.hsgn_group_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_solvers(w, parts, stream=None, **kw):
+    """Split a 1-member Workload into `parts` contiguous slabs (sizes differ by at
+    most one cell) sharing one stream; returns (solvers, bounds)."""
+    import torch
+    assert w.members == 1
+    stream = stream if stream is not None else torch.cuda.Stream()
+    edges = [round(i * w.n / parts) for i in range(parts + 1)]
+    out = []
+    for i in range(parts):
+        a, b = edges[i], edges[i + 1]
+        left = "halo" if (i > 0 or w.bc[0] == "periodic") else w.bc[0]
+        right = "halo" if (i < parts - 1 or w.bc[1] == "periodic") else w.bc[1]
+        sv = Solver(b - a, 1, w.x_min + a * w.dx, w.x_min + b * w.dx, bc=(left, right),
+                    stream=stream, **kw)
+        sv.set_params(w.g, w.lam, w.cfl, w.mcfl)
+        if w.b is not None:
+            sv.set_bathymetry(np.ascontiguousarray(w.b[a:b]))
+        if w.filter_sigma > 0:
+            sv.set_filter(w.filter_sigma)
+        sv.set_state(*[np.ascontiguousarray(f[0, a:b]) for f in (w.h, w.q, w.K, w.W)])
+        out.append(sv)
+    return out, edges

@@ -289,3 +289,63 @@ def test_cfg5_bathymetry_scaled():
     compare(w, s, [0], steps=1)
     s.run_steps(9)
     compare(w, s, [0], steps=10, tol=1e-10)
+
+
+# --------------------------------------------------------------------------
+# slab decomposition (P2): loopback group of slab contexts on one device
+# --------------------------------------------------------------------------
+def _gather(solvers):
+    outs = [sv.get_state(device=False) for sv in solvers]
+    return [np.concatenate([o[0][k][0] for o in outs]) for k in range(4)], outs[0][1]
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 5])
+def test_slab_group_matches_single_domain_and_oracle(parts):
+    hs = _hsgn()
+    w = W.cfg5_workload(1 << 16)
+    single = gpu_solver(w)
+    solvers, edges = hs.slab_solvers(w, parts)
+    g = hs.Group(solvers)
+    single.run_steps(1)
+    g.run_steps(1)
+    (h, q, K, Wf), t = _gather(solvers)
+    (h1, q1, K1, W1), t1 = single.get_state(device=False)
+    assert t[0] == t1[0]
+    refs, _ = oracle_run(w, [0], steps=1)
+    dt = O.Oracle(w.n, w.dx, lam=float(w.lam[0]), b=w.b).dt(refs[0], w.cfl, w.mcfl)[0]
+    S = field_scales(refs[0], float(w.lam[0]), dt)
+    # slabs vs one domain: different tile cuts, same exact solve -> round-off only
+    assert rel_err([h, q, K, Wf], [h1[0], q1[0], K1[0], W1[0]], S) <= 1e-13
+    assert rel_err([h, q, K, Wf], refs[0], S) <= TOL_STEP
+    g.run_steps(9)
+    single.run_steps(9)
+    (h, q, K, Wf), t = _gather(solvers)
+    (h1, q1, K1, W1), t1 = single.get_state(device=False)
+    assert abs(t[0] - t1[0]) <= 1e-13 * t1[0]
+    assert rel_err([h, q, K, Wf], [h1[0], q1[0], K1[0], W1[0]], S) <= 1e-11
+
+
+def test_slab_group_walls():
+    """first slab (wall, halo) ... last slab (halo, wall) == one walled domain"""
+    hs = _hsgn()
+    w = W.random_smooth(6000, 1, seed=31, amp=0.05, bc=("wall", "wall"))
+    w.filter_sigma = 0.25
+    single = gpu_solver(w)
+    solvers, _ = hs.slab_solvers(w, 3)
+    g = hs.Group(solvers)
+    single.run_steps(20)
+    g.run_steps(20)
+    (h, q, K, Wf), t = _gather(solvers)
+    (h1, q1, K1, W1), t1 = single.get_state(device=False)
+    ref = [h1[0], q1[0], K1[0], W1[0]]
+    dt = O.Oracle(w.n, w.dx, lam=float(w.lam[0]), bc=w.bc).dt(ref, w.cfl, w.mcfl)[0]
+    assert rel_err([h, q, K, Wf], ref, field_scales(ref, float(w.lam[0]), dt)) <= 1e-10
+    compare(w, single, [0], steps=20, tol=1e-10)
+
+
+def test_slab_context_refuses_without_transport():
+    hs = _hsgn()
+    w = W.random_smooth(1000, 1, seed=3)
+    solvers, _ = hs.slab_solvers(w, 2)
+    with pytest.raises(hs.HsgnError):
+        solvers[0].run_steps(1)

@@ -153,6 +153,19 @@ hsgn_status hsgn_set_bathymetry(hsgn_ctx *ctx, const double *b);
  * (1<<1)|(1<<3) (q and W) or 0. */
 hsgn_status hsgn_set_filter(hsgn_ctx *ctx, double sigma, uint32_t field_mask);
 
+/* Relaxation zones (A10, cfg4), applied to U^{n+1} after the filter:
+ * U -= s(x) (U - U_target(x, t^{n+1})), x_i = x_min + (i + 1/2) dx.
+ *   wavemaker x <= gen_x1: s = gen_rate (1 - (x - x_min)/(gen_x1 - x_min))^2,
+ *     eta = amp sin(omega t - k (x - x_min)), h = level + eta - b,
+ *     q = h cp eta / level, K = h (h + 1.5 b), W = 0;
+ *   sponge x >= sp_x0: s = sp_rate ((x - sp_x0)/(x_max - sp_x0))^2, lake at rest
+ *     h = level - b, q = 0, K = h (h + 1.5 b), W = 0.
+ * A rate <= 0 disables a zone; NULL disables both (default). */
+typedef struct {
+    double level, gen_x1, gen_rate, amp, omega, k, cp, sp_x0, sp_rate;
+} hsgn_relax;
+hsgn_status hsgn_set_relaxation(hsgn_ctx *ctx, const hsgn_relax *relax);
+
 /* ---- state -------------------------------------------------------------- */
 
 /* Copy in (h, q, K, W), each n_members * n_cells doubles, host or device

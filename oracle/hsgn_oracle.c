@@ -56,6 +56,17 @@ typedef struct {
     double filter_sigma;/* A19 filter strength, 0 = off */
     int32_t filter_mask;/* bit1 = q, bit3 = W (bit0 h, bit2 K also accepted) */
     int32_t pad_;
+    /* relaxation zones (A10, cfg4), applied after each step at the new time t:
+     * U -= s(x) (U - U_target).  x of cell i = x_min + (i + 1/2) dx.
+     * Wavemaker zone x <= gen_x1: s = gen_rate (1 - (x - x_min)/(gen_x1 - x_min))^2,
+     *   target eta = amp sin(omega t - k (x - x_min)): h = level + eta - b,
+     *   u = cp eta / level, h eta_aux = h^2 (+1.5 h b in K), w = 0.
+     * Sponge zone x >= sp_x0: s = sp_rate ((x - sp_x0)/(x_max - sp_x0))^2, target
+     *   lake at rest h = level - b, q = 0, K = h (h + 1.5 b), W = 0.
+     * A rate <= 0 switches a zone off. */
+    double x_min, level;
+    double gen_x1, gen_rate, amp, omega, k, cp;
+    double sp_x0, sp_rate;
 } orc_problem;
 
 /* Double Butcher tableau. */
@@ -442,6 +453,34 @@ static int apply_filter(const orc_problem *P, double *U[4])
 }
 
 /* ------------------------------------------------------------------------ */
+/* Relaxation zones: wavemaker and sponge (A10; cfg4)                        */
+/* ------------------------------------------------------------------------ */
+static void apply_relaxation(const orc_problem *P, double *U[4], double t)
+{
+    const double x_max = P->x_min + P->n * P->dx;
+    for (int i = 0; i < P->n; i++) {
+        double x = P->x_min + (i + 0.5) * P->dx;
+        double b = P->b ? P->b[i] : 0.0;
+        double s = 0.0, tg[4];
+        if (P->gen_rate > 0.0 && x <= P->gen_x1) {
+            double r = 1.0 - (x - P->x_min) / (P->gen_x1 - P->x_min);
+            s = P->gen_rate * r * r;
+            double eta = P->amp * sin(P->omega * t - P->k * (x - P->x_min));
+            double h = P->level + eta - b;
+            double u = P->cp * eta / P->level;
+            tg[0] = h; tg[1] = h * u; tg[2] = h * (h + 1.5 * b); tg[3] = 0.0;
+        } else if (P->sp_rate > 0.0 && x >= P->sp_x0) {
+            double r = (x - P->sp_x0) / (x_max - P->sp_x0);
+            s = P->sp_rate * r * r;
+            double h = P->level - b;
+            tg[0] = h; tg[1] = 0.0; tg[2] = h * (h + 1.5 * b); tg[3] = 0.0;
+        }
+        if (s > 0.0)
+            for (int k = 0; k < 4; k++) U[k][i] = U[k][i] - s * (U[k][i] - tg[k]);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Tableau validation and stage weights                          */
 /* ------------------------------------------------------------------------ */
 /* wE = a^E_21 / a^I_11 and wR = a^I_21 / a^I_11 (efficient form). */
@@ -468,8 +507,18 @@ int orc_tableau_weights(const orc_tableau *T, double *wE, double *wR)
 /* ------------------------------------------------------------------------ */
 /* One SI-IMEX step                                              */
 /* ------------------------------------------------------------------------ */
+/* One step starting at time t (t only enters the A10 wavemaker zone). */
+int orc_step_t(const orc_problem *P, const orc_tableau *T, double t, double dt, double *h,
+               double *q, double *K, double *W, double *min_beta);
+
 int orc_step(const orc_problem *P, const orc_tableau *T, double dt, double *h, double *q,
              double *K, double *W, double *min_beta)
+{
+    return orc_step_t(P, T, 0.0, dt, h, q, K, W, min_beta);
+}
+
+int orc_step_t(const orc_problem *P, const orc_tableau *T, double t, double dt, double *h,
+               double *q, double *K, double *W, double *min_beta)
 {
     double wE, wR;
     int st = orc_tableau_weights(T, &wE, &wR);
@@ -511,6 +560,7 @@ int orc_step(const orc_problem *P, const orc_tableau *T, double dt, double *h, d
         }
     }
     if (st == ORC_OK) st = apply_filter(P, U);
+    if (st == ORC_OK) apply_relaxation(P, U, t + dt);
     if (min_beta) *min_beta = mb1 < mb2 ? mb1 : mb2;
     free(buf);
     return st;
@@ -576,7 +626,7 @@ int orc_run(const orc_problem *P, const orc_tableau *T, double cfl, double mcfl,
         /* last step clipped to land exactly on t_end */
         if (use_tend && t + dt >= t_end) dt = t_end - t;
         double m;
-        st = orc_step(P, T, dt, h, q, K, W, &m);
+        st = orc_step_t(P, T, t, dt, h, q, K, W, &m);
         if (m < mb) mb = m;
         if (st != ORC_OK) break;
         t = (use_tend && dt == t_end - t) ? t_end : t + dt;

@@ -42,6 +42,9 @@ class Problem(C.Structure):
         ("order", C.c_int32), ("dx", C.c_double), ("g", C.c_double),
         ("lam", C.c_double), ("h_min", C.c_double), ("b", C.POINTER(C.c_double)),
         ("filter_sigma", C.c_double), ("filter_mask", C.c_int32), ("pad_", C.c_int32),
+        ("x_min", C.c_double), ("level", C.c_double), ("gen_x1", C.c_double),
+        ("gen_rate", C.c_double), ("amp", C.c_double), ("omega", C.c_double), ("k", C.c_double),
+        ("cp", C.c_double), ("sp_x0", C.c_double), ("sp_rate", C.c_double),
     ]
 
 
@@ -81,6 +84,8 @@ def lib():
             L.orc_stage.argtypes = [P] + [dp] * 8 + [C.c_double] + [dp] * 5
             L.orc_step.restype = C.c_int
             L.orc_step.argtypes = [P, T, C.c_double] + [dp] * 5
+            L.orc_step_t.restype = C.c_int
+            L.orc_step_t.argtypes = [P, T, C.c_double, C.c_double] + [dp] * 5
             L.orc_dt.restype = C.c_int
             L.orc_dt.argtypes = [P, C.c_double, C.c_double] + [dp] * 6
             L.orc_run.restype = C.c_int
@@ -128,14 +133,17 @@ class Oracle:
     """One 1-D domain (or one ensemble member) on the host."""
 
     def __init__(self, n, dx, g=9.81, lam=500.0, bc=("periodic", "periodic"), order=2,
-                 h_min=1e-8, b=None, filter_sigma=0.0, filter_mask=0b1010, tableau=None):
+                 h_min=1e-8, b=None, filter_sigma=0.0, filter_mask=0b1010, tableau=None,
+                 relax=None):
+        """relax: dict(x_min, level, gen_x1, gen_rate, amp, omega, k, cp, sp_x0, sp_rate)
+        for the A10 wavemaker / sponge zones (cfg4)."""
         self.L = lib()
         codes = {"periodic": BC_PERIODIC, "wall": BC_WALL, "transmissive": BC_TRANSMISSIVE}
         self._b = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
         self.P = Problem(n=n, bc_left=codes[bc[0]], bc_right=codes[bc[1]], order=order,
                          dx=dx, g=g, lam=lam, h_min=h_min,
                          b=_p(self._b) if self._b is not None else None,
-                         filter_sigma=filter_sigma, filter_mask=filter_mask)
+                         filter_sigma=filter_sigma, filter_mask=filter_mask, **(relax or {}))
         self.T = tableau if tableau is not None else paper_tableau()
 
     # -- pieces ---------------------------------------------------------
@@ -150,11 +158,11 @@ class Oracle:
             raise OracleError(st, "stage")
         return O, mb.value
 
-    def step(self, U, dt):
+    def step(self, U, dt, t=0.0):
         U = [np.array(a, dtype=np.float64, copy=True) for a in U]
         mb = C.c_double()
-        st = self.L.orc_step(C.byref(self.P), C.byref(self.T), dt, *[_p(a) for a in U],
-                             C.byref(mb))
+        st = self.L.orc_step_t(C.byref(self.P), C.byref(self.T), t, dt, *[_p(a) for a in U],
+                               C.byref(mb))
         if st != OK:
             raise OracleError(st, "step")
         return U

@@ -48,6 +48,7 @@ struct hsgn_ctx {
     hsgn_tableau tab{};
     double aI1 = 0, aI2 = 0, wE = 0, wR = 0;
     double filter_sigma = 0;
+    hsgn_relax relax{};
     // workspace
     char *ws = nullptr;
     size_t ws_bytes = 0;
@@ -109,6 +110,10 @@ Params make_params(hsgn_ctx *c, long long k)
     P.dx = c->dx; P.idx = 1.0 / c->dx; P.g = c->g; P.h_min = c->h_min; P.cfl = c->cfl; P.mcfl = c->mcfl;
     P.aI1 = c->aI1; P.aI2 = c->aI2; P.wE = c->wE; P.wR = c->wR;
     P.filter_sigma = c->filter_sigma;
+    P.x_min = c->desc.x_min; P.x_max = c->desc.x_max;
+    P.level = c->relax.level; P.gen_x1 = c->relax.gen_x1; P.gen_rate = c->relax.gen_rate;
+    P.amp = c->relax.amp; P.omega = c->relax.omega; P.kw = c->relax.k; P.cp = c->relax.cp;
+    P.sp_x0 = c->relax.sp_x0; P.sp_rate = c->relax.sp_rate;
     P.b = c->bathy ? c->b : nullptr;
     P.lam = c->lamd; P.t = c->t; P.dt = c->dt; P.maxes = c->maxes; P.err = c->err;
     P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.ctrl = c->ctrl;
@@ -124,7 +129,10 @@ template <bool S2, bool FIN, bool BATHY>
 hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
 {
     dim3 grid(c->tiles, c->members);
-    stage_kernel<S2, FIN, BATHY><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    if (FIN && (c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
+        stage_kernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    else
+        stage_kernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return HSGN_OK;
@@ -519,6 +527,10 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         delete c;
@@ -666,6 +678,19 @@ hsgn_status hsgn_set_filter(hsgn_ctx *c, double sigma, uint32_t mask)
     if (sigma > 0.0 && mask != ((1u << 1) | (1u << 3)))
         return fail(c, HSGN_E_INVALID, "filter mask must be q|W (0xA)");
     c->filter_sigma = sigma;
+    drop_graphs(c);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_relaxation(hsgn_ctx *c, const hsgn_relax *r)
+{
+    if (!c) return HSGN_E_INVALID;
+    if (!r) { c->relax = hsgn_relax{}; drop_graphs(c); return HSGN_OK; }
+    if ((r->gen_rate > 0.0 && !(r->gen_x1 > c->desc.x_min)) ||
+        (r->sp_rate > 0.0 && !(r->sp_x0 < c->desc.x_max)) || !(r->gen_rate <= 1.0) ||
+        !(r->sp_rate <= 1.0) || ((r->gen_rate > 0.0 || r->sp_rate > 0.0) && !(r->level > 0.0)))
+        return fail(c, HSGN_E_INVALID, "relaxation zones: bad extents or rates");
+    c->relax = *r;
     drop_graphs(c);
     return HSGN_OK;
 }

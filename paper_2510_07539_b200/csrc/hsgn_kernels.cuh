@@ -78,6 +78,9 @@ struct Params {
     const double *halo_l[9];
     const double *halo_r[9];
     int H;
+    // A10 relaxation zones (cfg4), applied to U^{n+1} at t^{n+1} in the final
+    // stage; rates <= 0 switch them off.  x_i = x_min + (i + 1/2) dx.
+    double x_min, x_max, level, gen_x1, gen_rate, amp, omega, kw, cp, sp_x0, sp_rate;
 };
 
 struct Bufs {
@@ -164,17 +167,6 @@ __device__ __forceinline__ double bathy_at(const Params &P, int c)
     if (c >= P.n && P.bcr == BC_HALO) return P.halo_r[8][c - P.n];
     double par;
     return __ldg(P.b + map_cell(c, P.n, P.bcl, P.bcr, par));
-}
-
-// Source of field f (0..3 state, +4 for U1) at global cell c of member offset mo:
-// the slab's own array, a halo buffer (BC_HALO), or the BC index map.
-__device__ __forceinline__ const double *cell_src(const Params &P, const double *base, int f, size_t mo,
-                                                  int c)
-{
-    if (c < 0 && P.bcl == BC_HALO) return P.halo_l[f] + (c + P.H);
-    if (c >= P.n && P.bcr == BC_HALO) return P.halo_r[f] + (c - P.n);
-    double par;
-    return base + mo + map_cell(c, P.n, P.bcl, P.bcr, par);
 }
 
 // dt rule of P:613-617 (reading A7 for nu_max): dt_bar = CFL dx / nu_max; if
@@ -345,7 +337,35 @@ __device__ __forceinline__ double block_max(double v, double *red, double ident 
 // The stage kernel.  STAGE2: inputs are U^n and U1 (E, R formed on load);
 // FINAL: this stage produces U^{n+1} (filter, dt maxima, commit).
 // ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY>
+// A10 wavemaker / sponge relaxation of one cell (x, b) at time t:
+// U -= s (U - U_target), see oracle/README and DESIGN.md A10.
+__device__ __forceinline__ void relax_cell(const Params &P, double x, double b, double t, double &h,
+                                           double &q, double &K, double &W)
+{
+    double s = 0.0, th, tq, tK;
+    if (P.gen_rate > 0.0 && x <= P.gen_x1) {
+        const double r = 1.0 - (x - P.x_min) / (P.gen_x1 - P.x_min);
+        s = P.gen_rate * r * r;
+        const double eta = P.amp * sin(P.omega * t - P.kw * (x - P.x_min));
+        th = P.level + eta - b;
+        tq = th * (P.cp * eta / P.level);
+        tK = th * (th + 1.5 * b);
+    } else if (P.sp_rate > 0.0 && x >= P.sp_x0) {
+        const double r = (x - P.sp_x0) / (P.x_max - P.sp_x0);
+        s = P.sp_rate * r * r;
+        th = P.level - b;
+        tq = 0.0;
+        tK = th * (th + 1.5 * b);
+    }
+    if (s > 0.0) {
+        h = h - s * (h - th);
+        q = q - s * (q - tq);
+        K = K - s * (K - tK);
+        W = W - s * W;
+    }
+}
+
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
 __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
 {
     extern __shared__ __align__(16) double smem[];
@@ -412,14 +432,27 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             }
         }
     } else {
+        // per-row source: own arrays through the BC index map, or a slab halo
+        // (explicit pointers: no local pointer arrays)
         for (int r = tid - 3; r < L + 3; r += NT) {
             const int c = start + r;
-            cp_async8(sEh + r, cell_src(P, B.Un[0], 0, mo, c)); cp_async8(sEq + r, cell_src(P, B.Un[1], 1, mo, c));
-            cp_async8(sEH + r, cell_src(P, B.Un[2], 2, mo, c)); cp_async8(sEW + r, cell_src(P, B.Un[3], 3, mo, c));
-            if (STAGE2) {
-                cp_async8(sHR + r, cell_src(P, B.U1[0], 4, mo, c)); cp_async8(sQd + r, cell_src(P, B.U1[1], 5, mo, c));
-                cp_async8(sHd + r, cell_src(P, B.U1[2], 6, mo, c)); cp_async8(sBe + r, cell_src(P, B.U1[3], 7, mo, c));
+            const double *p0, *p1, *p2, *p3, *u0 = nullptr, *u1 = nullptr, *u2 = nullptr, *u3 = nullptr;
+            if (c < 0 && P.bcl == BC_HALO) {
+                const int o = c + P.H;
+                p0 = P.halo_l[0] + o; p1 = P.halo_l[1] + o; p2 = P.halo_l[2] + o; p3 = P.halo_l[3] + o;
+                if (STAGE2) { u0 = P.halo_l[4] + o; u1 = P.halo_l[5] + o; u2 = P.halo_l[6] + o; u3 = P.halo_l[7] + o; }
+            } else if (c >= n && P.bcr == BC_HALO) {
+                const int o = c - n;
+                p0 = P.halo_r[0] + o; p1 = P.halo_r[1] + o; p2 = P.halo_r[2] + o; p3 = P.halo_r[3] + o;
+                if (STAGE2) { u0 = P.halo_r[4] + o; u1 = P.halo_r[5] + o; u2 = P.halo_r[6] + o; u3 = P.halo_r[7] + o; }
+            } else {
+                double par;
+                const size_t gi = mo + size_t(map_cell(c, n, P.bcl, P.bcr, par));
+                p0 = B.Un[0] + gi; p1 = B.Un[1] + gi; p2 = B.Un[2] + gi; p3 = B.Un[3] + gi;
+                if (STAGE2) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
             }
+            cp_async8(sEh + r, p0); cp_async8(sEq + r, p1); cp_async8(sEH + r, p2); cp_async8(sEW + r, p3);
+            if (STAGE2) { cp_async8(sHR + r, u0); cp_async8(sQd + r, u1); cp_async8(sHd + r, u2); cp_async8(sBe + r, u3); }
         }
     }
 
@@ -739,6 +772,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         }
         if (filt) __syncthreads();
         const double sig16 = P.filter_sigma * (1.0 / 16.0);
+        const bool relax = FINAL && RELAX;
+        const double t_new = relax ? P.t[P.kpar * members + m] + dtm : 0.0;
 #pragma unroll
         for (int i = 0; i < MCH; i++) {
             const int r = r0 + i;
@@ -768,11 +803,17 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 wo = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
                 if (!isfinite(qo) || !isfinite(wo)) errbits |= ERR_NONFINITE;
             }
-            const double h0 = hb[i];
+            double h0 = hb[i];
+            double Ko = BATHY ? Hbv[i] + 1.5 * h0 * bbv[i] : Hbv[i];
+            double Hf = Hbv[i];
+            if (FINAL && relax) {
+                relax_cell(P, P.x_min + (double(s + (r - wl)) + 0.5) * P.dx, bbv[i], t_new, h0, qo, Ko, wo);
+                Hf = Ko - 1.5 * h0 * bbv[i];
+            }
             const int ko = r - wl;
-            oh[ko] = h0; oq[ko] = qo; oK[ko] = BATHY ? Hbv[i] + 1.5 * h0 * bbv[i] : Hbv[i]; oW[ko] = wo;
+            oh[ko] = h0; oq[ko] = qo; oK[ko] = Ko; oW[ko] = wo;
             if (FINAL) {
-                const double u = qo * rcp(h0), sg = Hbv[i] * rcp(h0 * h0);
+                const double u = qo * rcp(h0), sg = Hf * rcp(h0 * h0);
                 umax_loc = fmax(umax_loc, fabs(u));
                 numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h0 + lam3 * sg * sg));
             }

@@ -39,6 +39,11 @@ class Tableau(C.Structure):
                 ("a_imp", (C.c_double * 2) * 2), ("b", C.c_double * 2)]
 
 
+class Relax(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("level", "gen_x1", "gen_rate", "amp", "omega", "k", "cp",
+                                          "sp_x0", "sp_rate")]
+
+
 class Diag(C.Structure):
     _fields_ = [("mass", C.c_double), ("min_h", C.c_double), ("max_abs_u", C.c_double),
                 ("nu_max", C.c_double), ("t_min", C.c_double), ("t_max", C.c_double),
@@ -49,6 +54,7 @@ class Diag(C.Structure):
 # exported symbols (checked by tests/test_abi.py against include/hsgn.h)
 SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_workspace",
            "hsgn_set_params", "hsgn_set_tableau", "hsgn_set_bathymetry", "hsgn_set_filter",
+           "hsgn_set_relaxation",
            "hsgn_set_state", "hsgn_get_state", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
            "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
@@ -77,6 +83,7 @@ def load_library(path: str = LIB_PATH):
         "hsgn_set_tableau": (st, [vp, C.POINTER(Tableau)]),
         "hsgn_set_bathymetry": (st, [vp, vp]),
         "hsgn_set_filter": (st, [vp, C.c_double, C.c_uint32]),
+        "hsgn_set_relaxation": (st, [vp, C.POINTER(Relax)]),
         "hsgn_set_state": (st, [vp, vp, vp, vp, vp, C.c_double]),
         "hsgn_get_state": (st, [vp, vp, vp, vp, vp, vp]),
         "hsgn_step": (st, [vp, C.c_double, dp]),
@@ -216,6 +223,15 @@ class Solver:
             self._keep.append(b)
         self._chk(self.L.hsgn_set_bathymetry(self.ctx, C.c_void_p(_ptr(b)) if b is not None else None))
 
+    def set_relaxation(self, relax: dict | None):
+        """A10 wavemaker / sponge zones: keys level, gen_x1, gen_rate, amp, omega, k,
+        cp, sp_x0, sp_rate (see include/hsgn.h); None disables them."""
+        if relax is None:
+            self._chk(self.L.hsgn_set_relaxation(self.ctx, None))
+        else:
+            r = Relax(**{k: float(v) for k, v in relax.items()})
+            self._chk(self.L.hsgn_set_relaxation(self.ctx, C.byref(r)))
+
     def set_filter(self, sigma: float, mask: int = 0b1010):
         self._chk(self.L.hsgn_set_filter(self.ctx, float(sigma), mask if sigma > 0 else 0))
 
@@ -291,6 +307,8 @@ def solver_for(w, **kw) -> Solver:
         s.set_bathymetry(w.b)
     if w.filter_sigma > 0:
         s.set_filter(w.filter_sigma)
+    if w.meta.get("relax"):
+        s.set_relaxation({k: v for k, v in w.meta["relax"].items() if k != "x_min"})
     s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
     return s
 

@@ -316,3 +316,48 @@ def cfg5_workload(n: int = 1 << 22, seed: int = 7539005, lam: float = 1e4) -> Wo
     return Workload(f"cfg5_n{n}", n, 1, 0.0, meta["L"], ("periodic", "periodic"),
                     np.array([lam]), h[None], q[None], K[None], W[None], b=b, cfl=2.0, mcfl=0.5,
                     steps=100, filter_sigma=0.25, meta=meta)
+
+
+def bar_bathymetry(x, h_off: float = 0.4):
+    """Submerged trapezoidal bar of cfg4 (BASELINE configs[3]): still-water depth
+    0.4 offshore, slope 1:20 from x = 6 up to a 0.1-deep crest at x = 12, crest to
+    x = 14, slope 1:10 down to 0.4 at x = 17, flat beyond; b = 0.4 - depth."""
+    depth = np.full_like(x, h_off)
+    up = (x >= 6.0) & (x < 12.0)
+    depth[up] = h_off - (x[up] - 6.0) / 20.0
+    depth[(x >= 12.0) & (x < 14.0)] = 0.1
+    dn = (x >= 14.0) & (x < 17.0)
+    depth[dn] = 0.1 + (x[dn] - 14.0) / 10.0
+    return h_off - depth
+
+
+def airy_wavenumber(omega: float, h0: float, g: float = G_DEFAULT) -> float:
+    """Linear wave: omega^2 = g k tanh(k h0) (fixed-point iteration)."""
+    k = omega * omega / g
+    for _ in range(200):
+        k = omega * omega / (g * math.tanh(k * h0))
+    return k
+
+
+def cfg4(n: int = 1 << 20, lams=(1e2, 1e3, 1e4, 1e5), L: float = 40.0) -> Workload:
+    """Waves over a submerged bar: [0, 40] m, N = 2^20, bar of bar_bathymetry, lake at
+    rest initially; wavemaker relaxation zone [0, 4] m (amplitude 0.01, period
+    2.02 s, Airy k and phase speed) at a transmissive end x = 0 (a wall there
+    conflicts with the forced velocity and grows a grid-scale mode); sponge
+    [30, 40] m before a transmissive end (A10); the lambda sweep runs as 4 ensemble
+    members sharing the bathymetry; CFL_IMEX 2, MCFL 0.5, 200 steps, A19 filter on.
+    The bar's slope kinks make the lake at rest drift (O(dx^2) residual, A9): the
+    recipe is meant for fine grids (2^16 cells and up; 2^12 blows up in ~100 steps)."""
+    x = cell_centres(0.0, L, n)
+    b = bar_bathymetry(x)
+    h = 0.4 - b
+    M = len(lams)
+    H = np.tile(h, (M, 1))
+    z = np.zeros_like(H)
+    omega = 2 * math.pi / 2.02
+    k = airy_wavenumber(omega, 0.4)
+    relax = dict(x_min=0.0, level=0.4, gen_x1=4.0, gen_rate=0.1, amp=0.01, omega=omega, k=k,
+                 cp=omega / k, sp_x0=30.0, sp_rate=0.1)
+    return Workload("cfg4_bar", n, M, 0.0, L, ("transmissive", "transmissive"), np.array(lams, dtype=float),
+                    H, z, H * (H + 1.5 * b[None]), z.copy(), b=b, cfl=2.0, mcfl=0.5, steps=200,
+                    filter_sigma=0.25, meta=dict(relax=relax))

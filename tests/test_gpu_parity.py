@@ -48,7 +48,7 @@ def oracle_run(w, members, steps=None, t_end=None, order=2, tableau=None, dt_fix
     jobs = []
     for m in members:
         o = O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, order=order, b=w.b,
-                     filter_sigma=w.filter_sigma, tableau=tableau)
+                     filter_sigma=w.filter_sigma, tableau=tableau, relax=w.meta.get("relax"))
         jobs.append((o, w.state(m)))
     res = O.run_members(jobs, cfl=w.cfl, mcfl=w.mcfl, steps=steps, t_end=t_end, dt_fixed=dt_fixed)
     return [r[0] for r in res], [r[1] for r in res]
@@ -66,6 +66,8 @@ def gpu_solver(w, **kw):
         s.set_bathymetry(w.b)
     if w.filter_sigma > 0:
         s.set_filter(w.filter_sigma)
+    if w.meta.get("relax"):
+        s.set_relaxation({k: v for k, v in w.meta["relax"].items() if k != "x_min"})
     s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
     return s
 
@@ -349,3 +351,29 @@ def test_slab_context_refuses_without_transport():
     solvers, _ = hs.slab_solvers(w, 2)
     with pytest.raises(hs.HsgnError):
         solvers[0].run_steps(1)
+
+
+def test_cfg4_bar_wavemaker_sponge_scaled():
+    """cfg4 recipe (bar bathymetry, wavemaker + sponge zones, 4 lambdas as members)
+    on 2^16 cells, 1 and 60 steps."""
+    w = W.cfg4(n=1 << 16)
+    s = gpu_solver(w)
+    s.step()
+    compare(w, s, range(4), steps=1)
+    s.run_steps(59)
+    compare(w, s, range(4), steps=60, tol=1e-10)
+    (h, *_), t = s.get_state(device=False)
+    assert np.max(np.abs(h[0] + w.b - 0.4)) > 1e-4          # the wavemaker acts
+
+
+def test_wavemaker_channel_matches_oracle():
+    """flat channel with wavemaker + sponge (A10) long enough for waves to form"""
+    w = W.cfg4(n=2000, lams=(1000.0,))
+    w.b = np.zeros(w.n)
+    h = np.full((1, w.n), 0.4)
+    w.h, w.q, w.K, w.W = h, np.zeros_like(h), h * h, np.zeros_like(h)
+    s = gpu_solver(w)
+    s.run_steps(1000)
+    compare(w, s, [0], steps=1000, tol=TOL_RUN)
+    (h, *_), t = s.get_state(device=False)
+    assert np.max(np.abs(h[0] - 0.4)) > 5e-3

@@ -481,3 +481,76 @@ def test_stage_tendency_converges_to_hsgnb_pde(lam, with_b):
     orders = np.log2(errs[:-1] / errs[1:])
     assert np.all(errs[-1] < 5e-3), errs
     assert np.all(orders > 1.7), (errs, orders)
+
+
+# --------------------------------------------------------------------------
+# Wavemaker and sponge relaxation zones (A10; cfg4)
+# --------------------------------------------------------------------------
+def _airy(omega, h0):
+    k = 1.0
+    for _ in range(200):
+        k = omega ** 2 / (G * np.tanh(k * h0))
+    return k, omega / k
+
+
+def _channel(n=2000, L=40.0, h0=0.4, lam=1000.0, amp=0.001, period=2.02, sponge=True, b=None):
+    omega = 2 * np.pi / period
+    k, cp = _airy(omega, h0)
+    relax = dict(x_min=0.0, level=h0, gen_x1=4.0, gen_rate=0.1, amp=amp, omega=omega, k=k, cp=cp,
+                 sp_x0=30.0, sp_rate=0.1 if sponge else 0.0)
+    o = O.Oracle(n, L / n, lam=lam, bc=("transmissive", "transmissive"), b=b, relax=relax,
+                 filter_sigma=0.25)
+    bb = np.zeros(n) if b is None else b
+    h = h0 - bb
+    U = [h, np.zeros(n), h * (h + 1.5 * bb), np.zeros(n)]
+    return o, U, omega
+
+
+def test_wavemaker_zero_amplitude_keeps_rest():
+    o, U, _ = _channel(n=400, amp=0.0)
+    U2, t, s, _ = o.run(U, cfl=2.0, mcfl=0.5, t_end=4.0)
+    assert np.max(np.abs(U2[0] - U[0])) < 1e-12 and np.max(np.abs(U2[1])) < 1e-12   # round-off only
+
+
+def test_sponge_keeps_lake_at_rest_over_bathymetry():
+    n, L = 400, 40.0
+    x = W.cell_centres(0, L, n)
+    b = 0.1 * np.exp(-((x - 35.0) / 2.0) ** 2)
+    relax = dict(x_min=0.0, level=0.4, sp_x0=30.0, sp_rate=0.1)
+    o = O.Oracle(n, L / n, lam=0.0, bc=("wall", "wall"), b=b, relax=relax)
+    h = 0.4 - b
+    U = [h, np.zeros(n), h * (h + 1.5 * b), np.zeros(n)]
+    U2, *_ = o.run(U, steps=20, dt_fixed=0.01)
+    assert np.max(np.abs(U2[0] - h)) < 1e-13 and np.max(np.abs(U2[1])) < 1e-13
+
+
+def _solve_k(omega, h0, lam):
+    lo, hi = 1e-4, 50.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if LT.hsgn_slow_omega(mid, h0, lam, G) < omega:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+def test_wavemaker_generates_the_hsgn_wavelength():
+    """The wavemaker zone (A10) radiates waves whose wavelength beyond the zone is
+    the hSGN one at the forcing frequency (slow branch, derived from P:101-111),
+    within 3 %; the sponge removes most of the wave before x = 40."""
+    h0, lam = 0.4, 1000.0
+    o, U, omega = _channel(h0=h0, lam=lam)
+    U2, t, s, _ = o.run(U, cfl=2.0, mcfl=0.5, t_end=10.0)
+    x = W.cell_centres(0, 40.0, 2000)
+    eta = U2[0] - h0
+    sel = (x > 5.0) & (x < 15.0)
+    xs, es = x[sel], eta[sel]
+    zc = xs[1:][np.sign(es[1:]) != np.sign(es[:-1])]
+    lam_num = 2.0 * np.mean(np.diff(zc))
+    lam_th = 2 * np.pi / _solve_k(omega, h0, lam)
+    assert abs(lam_num - lam_th) / lam_th < 0.03, (lam_num, lam_th)
+    inner = np.max(np.abs(eta[(x > 6) & (x < 14)]))
+    assert inner > 0.5 * 0.001                     # a wave of the forced amplitude
+    tail = np.max(np.abs(eta[x > 38]))
+    assert tail < 0.2 * inner, (tail, inner)

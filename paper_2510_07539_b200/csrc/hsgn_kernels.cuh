@@ -200,39 +200,47 @@ __device__ __forceinline__ double fsqrt(double x)
 }
 
 // MUSCL face states (A5): for the window rows (k-1, k, k+1),
-// M_k = v_k + (v_{k+1} - v_{k-1})/4 at face k+1/2 and Pl_k = v_k - (...)/4 at
-// face k-1/2 (order 1: the cell values); u = q/h at the face state.
+// M_k = v_k + kap (v_{k+1} - v_{k-1}) at face k+1/2 and Pl_k = v_k - kap (...)
+// at face k-1/2, kap = 1/4 (order 2) or 0 (order 1: v_k exactly, branch-free);
+// u = q/h at the face state.
 struct FState { double h, q, H, W, u; };
 struct Face { double q, H, W; };
 
 __device__ __forceinline__ FState muscl_minus(const double (&wh)[3], const double (&wq)[3],
                                               const double (&wH)[3], const double (&wW)[3],
-                                              int order)
+                                              double kap)
 {
     FState S;
-    if (order == 2) {
-        S.h = wh[1] + 0.25 * (wh[2] - wh[0]); S.q = wq[1] + 0.25 * (wq[2] - wq[0]);
-        S.H = wH[1] + 0.25 * (wH[2] - wH[0]); S.W = wW[1] + 0.25 * (wW[2] - wW[0]);
-    } else {
-        S.h = wh[1]; S.q = wq[1]; S.H = wH[1]; S.W = wW[1];
-    }
+    S.h = wh[1] + kap * (wh[2] - wh[0]); S.q = wq[1] + kap * (wq[2] - wq[0]);
+    S.H = wH[1] + kap * (wH[2] - wH[0]); S.W = wW[1] + kap * (wW[2] - wW[0]);
     S.u = S.q * rcp(S.h);
     return S;
 }
 
 __device__ __forceinline__ FState muscl_plus(const double (&wh)[3], const double (&wq)[3],
                                              const double (&wH)[3], const double (&wW)[3],
-                                             int order)
+                                             double kap)
 {
     FState S;
-    if (order == 2) {
-        S.h = wh[1] - 0.25 * (wh[2] - wh[0]); S.q = wq[1] - 0.25 * (wq[2] - wq[0]);
-        S.H = wH[1] - 0.25 * (wH[2] - wH[0]); S.W = wW[1] - 0.25 * (wW[2] - wW[0]);
-    } else {
-        S.h = wh[1]; S.q = wq[1]; S.H = wH[1]; S.W = wW[1];
-    }
+    S.h = wh[1] - kap * (wh[2] - wh[0]); S.q = wq[1] - kap * (wq[2] - wq[0]);
+    S.H = wH[1] - kap * (wH[2] - wH[0]); S.W = wW[1] - kap * (wW[2] - wW[0]);
     S.u = S.q * rcp(S.h);
     return S;
+}
+
+// Both face states of the window's centre row with one reciprocal:
+// Z = 1/(h- h+), 1/h- = h+ Z, 1/h+ = h- Z (a few ulp from q/h).
+__device__ __forceinline__ void muscl_pair(const double (&wh)[3], const double (&wq)[3],
+                                           const double (&wH)[3], const double (&wW)[3],
+                                           double kap, FState &Pl, FState &M)
+{
+    const double dh = kap * (wh[2] - wh[0]), dq = kap * (wq[2] - wq[0]);
+    const double dH = kap * (wH[2] - wH[0]), dW = kap * (wW[2] - wW[0]);
+    Pl.h = wh[1] - dh; Pl.q = wq[1] - dq; Pl.H = wH[1] - dH; Pl.W = wW[1] - dW;
+    M.h = wh[1] + dh; M.q = wq[1] + dq; M.H = wH[1] + dH; M.W = wW[1] + dW;
+    const double Z = rcp(Pl.h * M.h);
+    Pl.u = Pl.q * (M.h * Z);
+    M.u = M.q * (Pl.h * Z);
 }
 
 // Rusanov flux of R_E at a face (A4): alpha = max(|u-|, |u+|),
@@ -251,11 +259,11 @@ __device__ __forceinline__ Face rusanov(const FState &m, const FState &p)
 __device__ __forceinline__ FState muscl_plus_next(const double (&wh)[3], const double (&wq)[3],
                                                   const double (&wH)[3], const double (&wW)[3],
                                                   double h1, double q1, double H1, double W1,
-                                                  int order)
+                                                  double kap)
 {
     const double th[3] = {wh[1], wh[2], h1}, tq[3] = {wq[1], wq[2], q1};
     const double tH[3] = {wH[1], wH[2], H1}, tW[3] = {wW[1], wW[2], W1};
-    return muscl_plus(th, tq, tH, tW, order);
+    return muscl_plus(th, tq, tH, tW, kap);
 }
 
 struct RowCtx { double tau, tdx, t2, lt2, lam, lam3, ltau, g, idx; };
@@ -277,7 +285,11 @@ __device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int
     // R = E in stage 1; stage 2 combined it on load
     const double hR = STAGE2 ? sHR[rr] : hE, qR = STAGE2 ? sQd[rr] : qE;
     const double HR = STAGE2 ? sHd[rr] : HE, WR = STAGE2 ? sBe[rr] : WE;
-    const double ihE = rcp(hE);
+    // one reciprocal for 1/h and 1/beta1 = h^2/(h^2 + lam tau^2):
+    // Z = 1/(h (h^2 + lam tau^2)), 1/h = (h^2 + lam tau^2) Z, D = h Z
+    const double s2 = hE * hE, den = s2 + C.lt2;
+    const double Z = rcp(hE * den);
+    const double ihE = den * Z, D = hE * Z;
     const double ih2 = ihE * ihE;
     const double sg = HE * ih2;                                      // eta/h
     double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
@@ -298,9 +310,8 @@ __device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int
     // coefficients at E
     const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
     const double a2 = C.g * hE + C.lam3 * sg * (3.0 * sg - 1.0);
-    const double beta1 = 1.0 + C.lt2 * ih2;
-    const double ib1 = rcp(beta1);
-    const double beta2 = 2.0 * C.lt2 * ib1 * ib1 * ih2 * ihE;
+    const double ib1 = s2 * D;                                      // 1/beta1
+    const double beta2 = 2.0 * C.lt2 * hE * D * D;                  // P:506 (= 2 lt2 ib1^2 / h^3)
     const double beta = a2 + C.lam * alpha * beta2 * Hd;
     const double delta = alpha * ib1;
     if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; sHR[rr] = hRp; }
@@ -538,7 +549,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         // Branch-free over the MCH own rows (stores predicated on r <= L) so the
         // register window shifts are pure renaming; thread 0 also does row -1.
         {
-            const int order = P.order;
+            const double kap = P.order == 2 ? 0.25 : 0.0;
             RowCtx C{};
             C.tau = tau; C.tdx = tdx; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
             C.ltau = ltau; C.g = g; C.idx = idx1;
@@ -548,7 +559,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 const int rr = r0 - 2 + k;
                 wh[k] = sEh[rr]; wq[k] = sEq[rr]; wH[k] = sEH[rr]; wW[k] = sEW[rr];
             }
-            FState Mm = muscl_minus(wh, wq, wH, wW, order);           // M_{r0-1}
+            FState Mm = muscl_minus(wh, wq, wH, wW, kap);           // M_{r0-1}
             if (tid == 0) {
                 // row -1 (left halo of the tile): faces -3/2 and -1/2
                 double xh[3], xq[3], xH[3], xW[3];
@@ -556,10 +567,10 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 for (int k = 0; k < 3; k++) {             // rows -3 .. -1
                     xh[k] = sEh[k - 3]; xq[k] = sEq[k - 3]; xH[k] = sEH[k - 3]; xW[k] = sEW[k - 3];
                 }
-                const FState M2 = muscl_minus(xh, xq, xH, xW, order);     // M_{-2}
-                const FState P1 = muscl_plus(wh, wq, wH, wW, order);      // Pl_{-1} (rows -2..0)
+                const FState M2 = muscl_minus(xh, xq, xH, xW, kap);     // M_{-2}
+                const FState P1 = muscl_plus(wh, wq, wH, wW, kap);      // Pl_{-1} (rows -2..0)
                 const Face Fa = rusanov(M2, P1);                          // face -3/2
-                const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], order);
+                const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], kap);
                 const Face Fb = rusanov(Mm, P0);                          // face -1/2
                 double Wd, beta;
                 row_update<STAGE2, BATHY>(C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
@@ -570,9 +581,9 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
             }
             wh[2] = sEh[r0 + 1]; wq[2] = sEq[r0 + 1]; wH[2] = sEH[r0 + 1]; wW[2] = sEW[r0 + 1];
-            FState Pn = muscl_plus(wh, wq, wH, wW, order);        // Pl_{r0}
+            FState Pn, Mr;
+            muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);               // Pl_{r0}, M_{r0}
             Face Fl = rusanov(Mm, Pn);                             // face r0-1/2
-            FState Mr = muscl_minus(wh, wq, wH, wW, order);        // M_{r0}
 #pragma unroll
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
@@ -584,9 +595,10 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                     wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
                 }
                 wh[2] = sEh[r + 2]; wq[2] = sEq[r + 2]; wH[2] = sEH[r + 2]; wW[2] = sEW[r + 2];
-                Pn = muscl_plus(wh, wq, wH, wW, order);            // Pl_{r+1}
+                FState Mn;
+                muscl_pair(wh, wq, wH, wW, kap, Pn, Mn);           // Pl_{r+1}, M_{r+1}
                 const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
-                Mr = muscl_minus(wh, wq, wH, wW, order);           // M_{r+1}
+                Mr = Mn;
                 double beta;
                 row_update<STAGE2, BATHY>(C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
                                           sHR, sQd, sHd, sBe, sDe, wd[i], beta);
@@ -736,7 +748,9 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         double *oh = smem + 4 * SROWS, *oq = smem + 5 * SROWS, *oK = smem + 6 * SROWS,
                *oW = smem + 7 * SROWS;
         const int klo = filt ? wl - 2 : wl, khi = filt ? wl + Tk + 2 : wl + Tk;
-        double qbv[MCH], Hbv[MCH], Wbv[MCH], bbv[MCH];
+        // HdD = H^dag / (hbar^2 + lam tau^2): Hbar = HdD hbar^2 and, in the
+        // final stage, sigma = Hbar / hbar^2 = HdD for the dt maxima
+        double qbv[MCH], HdD[MCH], Wbv[MCH], bbv[MCH], ihv[MCH];
         const double hLn = (r0 > 0 && r0 - 1 < L) ? sHB[r0 - 1] : 0.0;
         const double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
 #pragma unroll
@@ -757,16 +771,25 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 qb -= tau * g * sEh[r] * (bp - bm) * (0.5 * idx1);     // A9
             }
             // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),
-            // Wbar = W^dag - lam tau H^dag / (hbar^2 + lam tau^2)
-            const double hb2 = h0 * h0;
-            const double HdD = vH[i + 1] * rcp(hb2 + lt2);
+            // Wbar = W^dag - lam tau H^dag / (hbar^2 + lam tau^2); in the final stage
+            // the same reciprocal gives 1/hbar: Z = 1/(hbar (hbar^2 + lam tau^2))
+            const double den = h0 * h0 + lt2;
+            double rden;
+            if (FINAL && !RELAX) {
+                const double Z = rcp(h0 * den);
+                rden = h0 * Z;
+                ihv[i] = den * Z;
+            } else {
+                rden = rcp(den);
+                ihv[i] = 0.0;
+            }
+            HdD[i] = vH[i + 1] * rden;
             qbv[i] = qb;
-            Hbv[i] = HdD * hb2;
-            Wbv[i] = wd[i] - ltau * HdD;
+            Wbv[i] = wd[i] - ltau * HdD[i];
             if (act && r >= wl && r < wl + Tk) {
                 if (!(h0 > P.h_min)) errbits |= ERR_DRY;
-                if (!isfinite(h0) || !isfinite(qb) || !isfinite(Hbv[i]) || !isfinite(Wbv[i]))
-                    errbits |= ERR_NONFINITE;
+                // one test for all four: a NaN or inf in any makes the sum non-finite
+                if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) errbits |= ERR_NONFINITE;
             }
             if (filt && act) { sQb[r] = qb; sWb[r] = Wbv[i]; }
         }
@@ -801,22 +824,25 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
                 qo = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
                 wo = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
-                if (!isfinite(qo) || !isfinite(wo)) errbits |= ERR_NONFINITE;
+                if (!isfinite(qo + wo)) errbits |= ERR_NONFINITE;
             }
             double h0 = hb[i];
-            double Ko = BATHY ? Hbv[i] + 1.5 * h0 * bbv[i] : Hbv[i];
-            double Hf = Hbv[i];
+            const double Hb = HdD[i] * (h0 * h0);
+            double Ko = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
+            const int ko = r - wl;
             if (FINAL && relax) {
                 relax_cell(P, P.x_min + (double(s + (r - wl)) + 0.5) * P.dx, bbv[i], t_new, h0, qo, Ko, wo);
-                Hf = Ko - 1.5 * h0 * bbv[i];
-            }
-            const int ko = r - wl;
-            oh[ko] = h0; oq[ko] = qo; oK[ko] = Ko; oW[ko] = wo;
-            if (FINAL) {
-                const double u = qo * rcp(h0), sg = Hf * rcp(h0 * h0);
+                const double Hf = Ko - 1.5 * h0 * bbv[i];
+                const double ih = rcp(h0);
+                const double u = qo * ih, sg = Hf * ih * ih;
+                umax_loc = fmax(umax_loc, fabs(u));
+                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h0 + lam3 * sg * sg));
+            } else if (FINAL) {
+                const double u = qo * ihv[i], sg = HdD[i];
                 umax_loc = fmax(umax_loc, fabs(u));
                 numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h0 + lam3 * sg * sg));
             }
+            oh[ko] = h0; oq[ko] = qo; oK[ko] = Ko; oW[ko] = wo;
         }
         // ---- stores: TMA bulk (aligned interior tiles) or coalesced copies -------
         const size_t gdst = mo + size_t(s);

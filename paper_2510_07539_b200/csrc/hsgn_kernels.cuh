@@ -247,7 +247,8 @@ __device__ __forceinline__ void muscl_pair(const double (&wh)[3], const double (
 // F = 1/2 (F(U-) + F(U+)) - 1/2 alpha (U+ - U-) for F^q = q u, F^H = H u, F^W = W u.
 __device__ __forceinline__ Face rusanov(const FState &m, const FState &p)
 {
-    const double a = fmax(fabs(m.u), fabs(p.u));
+    const double am = fabs(m.u), ap = fabs(p.u);
+    const double a = am > ap ? am : ap;
     Face F;
     F.q = 0.5 * (m.q * m.u + p.q * p.u) - 0.5 * a * (p.q - m.q);
     F.H = 0.5 * (m.H * m.u + p.H * p.u) - 0.5 * a * (p.H - m.H);
@@ -324,6 +325,21 @@ __device__ __forceinline__ double warp_max(double v)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+}
+
+// Warp maxima of non-negative values on their bit patterns (IEEE order of
+// non-negative numbers = unsigned order of their bits): two REDUX per double.
+__device__ __forceinline__ double warp_max_nonneg(double v)
+{
+    const unsigned hi = unsigned(__double2hiint(v)), lo = unsigned(__double2loint(v));
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return __hiloint2double(int(mh), int(ml));
+}
+
+__device__ __forceinline__ float warp_max_nonneg(float v)
+{
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
 }
 
 __device__ __forceinline__ double block_max(double v, double *red, double ident = 0.0)
@@ -485,7 +501,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const double ltau = lam * tau;
 
     double umax_loc = 0.0, numax_loc = 0.0;
-    float rho_loc = 0.0f;
+    double rho_loc = 0.0;
     unsigned int errbits = 0u;
 
     if (bulk) {
@@ -514,26 +530,42 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         // ---- in-place pass: E, R, H = K - 1.5 h b (A9), wall parity
         const bool wall_ghosts = (left_phys && P.bcl == BC_WALL) || (right_phys && P.bcr == BC_WALL);
         if (STAGE2 || BATHY || wall_ghosts) {
+            // two rows per thread and iteration with 16-B shared accesses: row r of
+            // array k sits at smem[k * SROWS + d + 3 + r], pairs start at even offsets
+            // (the spare rows at either end are scratch)
             const double wE = P.wE, wR = P.wR;
-            for (int r = tid - 3; r < L + 3; r += NT) {
-                double par = 1.0;
-                const int c = start + r;
-                if (!interior) (void)map_cell(c, n, P.bcl, P.bcr, par);   // q parity of wall ghosts
-                const double bb = BATHY ? bathy_at(P, c) : 0.0;
-                double eh = sEh[r], eq = par * sEq[r], eK = sEH[r], eW = sEW[r];
-                if (STAGE2) {
-                    const double h1 = sHR[r], q1 = par * sQd[r], K1 = sHd[r], W1 = sBe[r];
-                    const double rh = (1.0 - wR) * eh + wR * h1, rq = (1.0 - wR) * eq + wR * q1;
-                    const double rK = (1.0 - wR) * eK + wR * K1, rW = (1.0 - wR) * eW + wR * W1;
-                    sHR[r] = rh; sQd[r] = rq;
-                    sHd[r] = BATHY ? rK - 1.5 * rh * bb : rK;
-                    sBe[r] = rW;
-                    eh = (1.0 - wE) * eh + wE * h1; eq = (1.0 - wE) * eq + wE * q1;
-                    eK = (1.0 - wE) * eK + wE * K1; eW = (1.0 - wE) * eW + wE * W1;
+            for (int p = 2 * tid; p < d + L + 6; p += 2 * NT) {
+                const int r = p - d - 3;
+                double2 *v = reinterpret_cast<double2 *>(smem + p);
+                double2 eh = v[0], eq = v[SROWS / 2], eK = v[SROWS], eW = v[3 * SROWS / 2];
+                double par0 = 1.0, par1 = 1.0;
+                if (!interior) {                       // q parity of wall ghosts
+                    (void)map_cell(start + r, n, P.bcl, P.bcr, par0);
+                    (void)map_cell(start + r + 1, n, P.bcl, P.bcr, par1);
                 }
-                sEh[r] = eh; sEq[r] = eq;
-                sEH[r] = BATHY ? eK - 1.5 * eh * bb : eK;
-                sEW[r] = eW;
+                eq.x *= par0; eq.y *= par1;
+                // (scratch rows clamped onto rows -3 .. L+2: stay inside slab halos)
+                const double b0 = BATHY ? bathy_at(P, start + max(r, -3)) : 0.0;
+                const double b1 = BATHY ? bathy_at(P, start + min(r + 1, L + 2)) : 0.0;
+                if (STAGE2) {
+                    const double2 h1 = v[4 * SROWS], q1 = v[2 * SROWS], K1 = v[5 * SROWS / 2],
+                                  W1 = v[3 * SROWS];
+                    const double q1x = par0 * q1.x, q1y = par1 * q1.y;
+                    double2 rh, rq, rK, rW;
+                    rh.x = (1.0 - wR) * eh.x + wR * h1.x; rh.y = (1.0 - wR) * eh.y + wR * h1.y;
+                    rq.x = (1.0 - wR) * eq.x + wR * q1x;  rq.y = (1.0 - wR) * eq.y + wR * q1y;
+                    rK.x = (1.0 - wR) * eK.x + wR * K1.x; rK.y = (1.0 - wR) * eK.y + wR * K1.y;
+                    rW.x = (1.0 - wR) * eW.x + wR * W1.x; rW.y = (1.0 - wR) * eW.y + wR * W1.y;
+                    if (BATHY) { rK.x -= 1.5 * rh.x * b0; rK.y -= 1.5 * rh.y * b1; }
+                    v[4 * SROWS] = rh; v[2 * SROWS] = rq; v[5 * SROWS / 2] = rK; v[3 * SROWS] = rW;
+                    eh.x = (1.0 - wE) * eh.x + wE * h1.x; eh.y = (1.0 - wE) * eh.y + wE * h1.y;
+                    eq.x = (1.0 - wE) * eq.x + wE * q1x;  eq.y = (1.0 - wE) * eq.y + wE * q1y;
+                    eK.x = (1.0 - wE) * eK.x + wE * K1.x; eK.y = (1.0 - wE) * eK.y + wE * K1.y;
+                    eW.x = (1.0 - wE) * eW.x + wE * W1.x; eW.y = (1.0 - wE) * eW.y + wE * W1.y;
+                }
+                if (BATHY) { eK.x -= 1.5 * eh.x * b0; eK.y -= 1.5 * eh.y * b1; }
+                v[0] = eh; v[SROWS / 2] = eq; v[SROWS] = eK;
+                if (STAGE2) v[3 * SROWS / 2] = eW;
             }
             __syncthreads();
         }
@@ -607,14 +639,32 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             }
         }
         __syncthreads();
-        // derived-field ghosts at physical boundaries (A10)
-        if (tid == 0 && left_phys) {
-            sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
-            sHd[-1] = sHd[0]; sBe[-1] = sBe[0]; sDe[-1] = sDe[0];
+        // derived-field ghosts at physical boundaries (A10).  The implicit
+        // coupling across both tile ends is cut (truncated overlap or Neumann end:
+        // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
+        // make those face coefficients t2 (beta_i + beta_{i+1}) / 2 exactly zero,
+        // and rows L+1 .. LCAP+1 (beyond the tile, solved as decoupled rows) get
+        // zero fields and alternating +-beta_{L-1} so all their couplings vanish too.
+        if (tid == 0) {
+            if (left_phys) {
+                sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
+                sHd[-1] = sHd[0]; sDe[-1] = sDe[0];
+            }
+            sBe[-1] = -sBe[0];
         }
-        if (tid == 32 && right_phys) {
-            sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
-            sHd[L] = sHd[L - 1]; sBe[L] = sBe[L - 1]; sDe[L] = sDe[L - 1];
+        if (tid == 32) {
+            if (right_phys) {
+                sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
+                sHd[L] = sHd[L - 1]; sDe[L] = sDe[L - 1];
+            }
+            sBe[L] = -sBe[L - 1];
+        }
+        if (tid >= 64 && tid < 96) {
+            const double bL = sBe[L - 1];
+            for (int r = L + 1 + (tid - 64); r <= LCAP + 1; r += 32) {
+                sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0; sHR[r] = 0.0;
+                sBe[r] = ((r - L) & 1) ? bL : -bL;
+            }
         }
         __syncthreads();
 
@@ -634,17 +684,14 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
 #pragma unroll
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
-                const bool in = r < L;                    // rows >= L: identity rows
-                const double rl0 = t2 * (vb[i] + vb[i + 1]) * 0.5;
-                const double rr0 = t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
+                // (r_{-1/2} = r_{L-1/2} = 0 through the beta ghosts set above)
+                const double rl = t2 * (vb[i] + vb[i + 1]) * 0.5;
+                const double rr = t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
                 const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
-                const double rhs0 = sHR[r] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
-                                    - ml * (vH[i + 1] - vH[i]);
-                const double rl = (in && r != 0) ? rl0 : 0.0;        // truncated / Neumann ends
-                const double rr = (in && r != L - 1) ? rr0 : 0.0;
-                const double rhs = in ? rhs0 : 0.0;
+                const double rhs = sHR[r] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
+                                   - ml * (vH[i + 1] - vH[i]);
                 const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
-                rho_loc = fmaxf(rho_loc, float(rr));
+                rho_loc = rr > rho_loc ? rr : rho_loc;
                 if (i == 0) {
                     const double inv = rcp(dg);
                     am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
@@ -693,9 +740,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
             {
                 const float ea = float(fabs(A_)), ec = float(fabs(C_));
-                float ev = ea > ec ? ea : ec;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) ev = fmaxf(ev, __shfl_xor_sync(0xffffffffu, ev, o));
+                const float ev = warp_max_nonneg(ea > ec ? ea : ec);
                 if (lane == 0) redf[wid] = ev;
             }
             __syncthreads();
@@ -791,7 +836,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 // one test for all four: a NaN or inf in any makes the sum non-finite
                 if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) errbits |= ERR_NONFINITE;
             }
-            if (filt && act) { sQb[r] = qb; sWb[r] = Wbv[i]; }
+            if (filt) { sQb[r] = qb; sWb[r] = Wbv[i]; }        // rows outside are never read
         }
         if (filt) __syncthreads();
         const double sig16 = P.filter_sigma * (1.0 / 16.0);
@@ -834,13 +879,15 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 relax_cell(P, P.x_min + (double(s + (r - wl)) + 0.5) * P.dx, bbv[i], t_new, h0, qo, Ko, wo);
                 const double Hf = Ko - 1.5 * h0 * bbv[i];
                 const double ih = rcp(h0);
-                const double u = qo * ih, sg = Hf * ih * ih;
-                umax_loc = fmax(umax_loc, fabs(u));
-                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h0 + lam3 * sg * sg));
+                const double u = fabs(qo * ih), sg = Hf * ih * ih;
+                const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
+                umax_loc = u > umax_loc ? u : umax_loc;
+                numax_loc = nu > numax_loc ? nu : numax_loc;
             } else if (FINAL) {
-                const double u = qo * ihv[i], sg = HdD[i];
-                umax_loc = fmax(umax_loc, fabs(u));
-                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h0 + lam3 * sg * sg));
+                const double u = fabs(qo * ihv[i]), sg = HdD[i];
+                const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
+                umax_loc = u > umax_loc ? u : umax_loc;
+                numax_loc = nu > numax_loc ? nu : numax_loc;
             }
             oh[ko] = h0; oq[ko] = qo; oK[ko] = Ko; oW[ko] = wo;
         }
@@ -857,7 +904,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 bulk_s2g(B.out[2] + gdst, oK, bytes);
                 bulk_s2g(B.out[3] + gdst, oW, bytes);
                 asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                // (the read-completion wait is deferred to the kernel's end: the
+                // staged rows are not written again)
             }
         } else {
             __syncthreads();
@@ -870,25 +918,23 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
 
     // ---- error bits --------------------------------------------------------
     {
-        unsigned int eb = errbits;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) eb |= __shfl_xor_sync(0xffffffffu, eb, o);
+        const unsigned int eb = __reduce_or_sync(0xffffffffu, errbits);
         if ((tid & 31) == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
     }
 
     // ---- per-CTA reductions: rho (overlap check), dt maxima, next time level ----
     {
-        double um = warp_max(umax_loc), nm = warp_max(numax_loc);
-        float rf = rho_loc;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) rf = fmaxf(rf, __shfl_xor_sync(0xffffffffu, rf, o));
+        double um = 0.0, nm = 0.0;
+        if (FINAL) { um = warp_max_nonneg(umax_loc); nm = warp_max_nonneg(numax_loc); }
+        float rf = warp_max_nonneg(float(rho_loc));
         const int lane = tid & 31, wid = tid >> 5;
         __syncthreads();
         if (lane == 0) { red[0][wid] = um; red[1][wid] = nm; redf[wid] = rf; }
         __syncthreads();
         if (tid == 0) {
             for (int q = 1; q < NT / 32; q++) {
-                um = fmax(um, red[0][q]); nm = fmax(nm, red[1][q]); rf = fmaxf(rf, redf[q]);
+                um = red[0][q] > um ? red[0][q] : um; nm = red[1][q] > nm ? red[1][q] : nm;
+                rf = redf[q] > rf ? redf[q] : rf;
             }
             // overlap check: r^w <= 2^-60 at each truncated end
             if (rf > 0.0f && dtm != 0.0) {
@@ -912,6 +958,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                     P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
                 }
             }
+            // shared memory must outlive the bulk stores' reads (no-op if none)
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
         }
     }
 }

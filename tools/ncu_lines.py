@@ -53,9 +53,9 @@ def main(rep, so):
         n = len(rows) - 1
         cand = [f for f, m in funcs.items() if abs(len(m) - n) <= 2 and "stage_kernel" in f]
         key = None
-        tag = re.findall(r"<\(bool\)(\d), \(bool\)(\d), \(bool\)(\d)>", name)
+        tag = re.findall(r"<\(bool\)(\d), \(bool\)(\d), \(bool\)(\d), \(bool\)(\d)>", name)
         if tag:
-            t = "".join("ILb%sE" % x for x in tag[0])
+            t = "ILb%sELb%sELb%sELb%sEE" % tag[0]
             for f in funcs:
                 if t in f:
                     key = f
@@ -63,6 +63,8 @@ def main(rep, so):
             key = cand[0]
         agg = collections.Counter()
         inst = collections.Counter()
+        ops = collections.Counter()
+        isrc = hdr.index("Source")
         tot = 0
         for r in rows[1:]:
             off = int(r[ia], 16) - base
@@ -70,10 +72,20 @@ def main(rep, so):
             s = int(r[iss] or 0)
             agg[li] += s
             inst[li] += int(r[iex] or 0)
+            op = r[isrc].split()
+            op = [t for t in op if not t.startswith("@")]
+            if op:
+                ops[op[0].split(".")[0]] += int(r[iex] or 0)
             tot += s
         print("=== %s  (%s) total samples %d" % (name[:60], key, tot))
         for li, s in agg.most_common(int(os.environ.get("TOPN", "40"))):
             print("%6.2f%%  %-22s line %4d   inst %d" % (100.0 * s / max(tot, 1), li[0], li[1], inst[li]))
+        cells = float(os.environ.get("CELLS", "0"))
+        if cells:
+            print("--- dynamic SASS opcodes, thread-inst per cell (x32 warp)")
+            for op, c in ops.most_common(30):
+                print("   %-10s %7.1f" % (op, 32.0 * c / cells))
+            print("   total      %7.1f" % (32.0 * sum(ops.values()) / cells))
 
 
 if __name__ == "__main__":

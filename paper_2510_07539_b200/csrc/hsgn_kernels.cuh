@@ -34,6 +34,14 @@
 #ifndef HSGN_MINB
 #define HSGN_MINB 4
 #endif
+// Timing experiments only (never in the product build): skip the global loads
+// or stores of the stage kernel and ignore its error checks.
+#ifndef HSGN_EXP_NOLOAD
+#define HSGN_EXP_NOLOAD 0
+#endif
+#ifndef HSGN_EXP_NOSTORE
+#define HSGN_EXP_NOSTORE 0
+#endif
 
 namespace hsgn {
 
@@ -44,7 +52,7 @@ constexpr int NT = HSGN_NT;           // threads per CTA
 constexpr int MCH = HSGN_MCH;       // rows per thread chunk (odd: conflict-free strided smem)
 constexpr int LCAP = NT * MCH;      // 1280 rows per CTA incl. phase-1 halo rows
 constexpr int SROWS = LCAP + 8;     // smem row capacity per array (even: 16-B aligned bases)
-constexpr int NARR = 9;             // smem arrays
+constexpr int NARR = 8;             // smem arrays
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
 
 enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2, BC_HALO = 3 };
@@ -271,20 +279,22 @@ struct RowCtx { double tau, tdx, t2, lt2, lam, lam3, ltau, g, idx; };
 
 // Predictor (A9) and coefficients at E (A2) of
 // one row r; E rows r-1, r, r+1 in (ch, cq, cH, cW); fluxes at r -+ 1/2.
-// Stores q^dag, H^dag, beta, delta, h^R' at row r unless r < -1 (dead row).
+// Stores q^dag, H^dag, beta, delta at row r unless r < -1 (dead row); returns
+// h^R' (R_h plus the hydrostatic term) in hR_out.  Stage 2 reads R_h from the
+// delta array (sRh == sDe) before overwriting it with delta.
 template <bool STAGE2, bool BATHY>
 __device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int r, int start, int n,
                                            const double (&ch)[3], const double (&cq)[3],
                                            const double (&cH)[3], const double (&cW)[3],
-                                           const Face &Fl, const Face &Fr, double *sHR, double *sQd,
+                                           const Face &Fl, const Face &Fr, double *sQd,
                                            double *sHd, double *sBe, double *sDe, double &Wd_out,
-                                           double &beta_out)
+                                           double &beta_out, double &hR_out)
 {
     const bool live = r >= -1;
     const int rr = live ? r : 0;
     const double hE = ch[1], qE = cq[1], HE = cH[1], WE = cW[1];
     // R = E in stage 1; stage 2 combined it on load
-    const double hR = STAGE2 ? sHR[rr] : hE, qR = STAGE2 ? sQd[rr] : qE;
+    const double hR = STAGE2 ? sDe[rr] : hE, qR = STAGE2 ? sQd[rr] : qE;
     const double HR = STAGE2 ? sHd[rr] : HE, WR = STAGE2 ? sBe[rr] : WE;
     // one reciprocal for 1/h and 1/beta1 = h^2/(h^2 + lam tau^2):
     // Z = 1/(h (h^2 + lam tau^2)), 1/h = (h^2 + lam tau^2) Z, D = h Z
@@ -315,7 +325,8 @@ __device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int
     const double beta2 = 2.0 * C.lt2 * hE * D * D;                  // P:506 (= 2 lt2 ib1^2 / h^3)
     const double beta = a2 + C.lam * alpha * beta2 * Hd;
     const double delta = alpha * ib1;
-    if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; sHR[rr] = hRp; }
+    if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; }
+    hR_out = hRp;
     Wd_out = Wd;
     beta_out = live ? beta : 1.0;
 }
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const bool left_phys = physL && (start == 0);
     const bool right_phys = physR && (start + L == n);
 
-    // ---- shared memory: 9 arrays of SROWS doubles, all indexed by tile row r
+    // ---- shared memory: 8 arrays of SROWS doubles, all indexed by tile row r
     // (r in [-3, L+3)).  Interior tiles are filled by TMA bulk copies, which
     // need 16-B aligned destinations: every array is shifted by d = parity of
     // the first copied global cell.
@@ -436,12 +447,12 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     double *sQd = A + 4 * SROWS;   // U1_q -> R_q -> q^dagger
     double *sHd = A + 5 * SROWS;   // U1_K -> R_H -> H^dagger
     double *sBe = A + 6 * SROWS;   // U1_W -> R_W -> beta
-    double *sDe = A + 7 * SROWS;   // delta
-    double *sHR = A + 8 * SROWS;   // U1_h -> R_h -> h^R (+ hydrostatic term)
+    double *sDe = A + 7 * SROWS;   // U1_h -> R_h -> delta (R_h read by its own row first)
 
     // ---- load: raw rows -3..L+2 of U^n (and U1), overlapped with run control --
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
-    if (bulk) {
+    if (HSGN_EXP_NOLOAD) {
+    } else if (bulk) {
         if (tid == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -452,7 +463,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
 #pragma unroll
             for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
             if (STAGE2) {
-                bulk_g2s(smem + 8 * SROWS, B.U1[0] + gsrc, bytes, mb);
+                bulk_g2s(smem + 7 * SROWS, B.U1[0] + gsrc, bytes, mb);
                 bulk_g2s(smem + 4 * SROWS, B.U1[1] + gsrc, bytes, mb);
                 bulk_g2s(smem + 5 * SROWS, B.U1[2] + gsrc, bytes, mb);
                 bulk_g2s(smem + 6 * SROWS, B.U1[3] + gsrc, bytes, mb);
@@ -479,7 +490,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 if (STAGE2) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
             }
             cp_async8(sEh + r, p0); cp_async8(sEq + r, p1); cp_async8(sEH + r, p2); cp_async8(sEW + r, p3);
-            if (STAGE2) { cp_async8(sHR + r, u0); cp_async8(sQd + r, u1); cp_async8(sHd + r, u2); cp_async8(sBe + r, u3); }
+            if (STAGE2) { cp_async8(sDe + r, u0); cp_async8(sQd + r, u1); cp_async8(sHd + r, u2); cp_async8(sBe + r, u3); }
         }
     }
 
@@ -488,7 +499,10 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const int members = P.members;
     const double dtm = P.dt[m];
     const double lam = P.lam[m];
-    if (err0) { drain_loads(bulk, mb); return; }
+    if (err0) {
+        if (!HSGN_EXP_NOLOAD) drain_loads(bulk, mb);
+        return;
+    }
     const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
     const double g = P.g, idx1 = P.idx;
     const double tdx = tau * idx1;                  // tau / dx
@@ -504,7 +518,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     double rho_loc = 0.0;
     unsigned int errbits = 0u;
 
-    if (bulk) {
+    if (HSGN_EXP_NOLOAD) {
+    } else if (bulk) {
         __syncthreads();                  // mbarrier initialised before anyone waits
         mbar_wait(mb, 0);
     } else {
@@ -548,7 +563,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 const double b0 = BATHY ? bathy_at(P, start + max(r, -3)) : 0.0;
                 const double b1 = BATHY ? bathy_at(P, start + min(r + 1, L + 2)) : 0.0;
                 if (STAGE2) {
-                    const double2 h1 = v[4 * SROWS], q1 = v[2 * SROWS], K1 = v[5 * SROWS / 2],
+                    const double2 h1 = v[7 * SROWS / 2], q1 = v[2 * SROWS], K1 = v[5 * SROWS / 2],
                                   W1 = v[3 * SROWS];
                     const double q1x = par0 * q1.x, q1y = par1 * q1.y;
                     double2 rh, rq, rK, rW;
@@ -557,7 +572,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                     rK.x = (1.0 - wR) * eK.x + wR * K1.x; rK.y = (1.0 - wR) * eK.y + wR * K1.y;
                     rW.x = (1.0 - wR) * eW.x + wR * W1.x; rW.y = (1.0 - wR) * eW.y + wR * W1.y;
                     if (BATHY) { rK.x -= 1.5 * rh.x * b0; rK.y -= 1.5 * rh.y * b1; }
-                    v[4 * SROWS] = rh; v[2 * SROWS] = rq; v[5 * SROWS / 2] = rK; v[3 * SROWS] = rW;
+                    v[7 * SROWS / 2] = rh; v[2 * SROWS] = rq; v[5 * SROWS / 2] = rK; v[3 * SROWS] = rW;
                     eh.x = (1.0 - wE) * eh.x + wE * h1.x; eh.y = (1.0 - wE) * eh.y + wE * h1.y;
                     eq.x = (1.0 - wE) * eq.x + wE * q1x;  eq.y = (1.0 - wE) * eq.y + wE * q1y;
                     eK.x = (1.0 - wE) * eK.x + wE * K1.x; eK.y = (1.0 - wE) * eK.y + wE * K1.y;
@@ -576,6 +591,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         // rows come from shared memory.
         const int r0 = tid * MCH;
         double wd[MCH];                  // W^dagger of own rows (phase 1 -> 3)
+        double hRv[MCH];                 // h^R' of own rows (phase 1 -> 2)
 
         // ---- phase 1: faces, predictor, coefficients --------------------------
         // Branch-free over the MCH own rows (stores predicated on r <= L) so the
@@ -604,9 +620,9 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 const Face Fa = rusanov(M2, P1);                          // face -3/2
                 const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], kap);
                 const Face Fb = rusanov(Mm, P0);                          // face -1/2
-                double Wd, beta;
+                double Wd, beta, hRd;
                 row_update<STAGE2, BATHY>(C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
-                                          sHR, sQd, sHd, sBe, sDe, Wd, beta);
+                                          sQd, sHd, sBe, sDe, Wd, beta, hRd);
             }
 #pragma unroll
             for (int k = 0; k < 2; k++) {
@@ -631,9 +647,10 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 muscl_pair(wh, wq, wH, wW, kap, Pn, Mn);           // Pl_{r+1}, M_{r+1}
                 const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
                 Mr = Mn;
-                double beta;
+                double beta, hRr;
                 row_update<STAGE2, BATHY>(C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
-                                          sHR, sQd, sHd, sBe, sDe, wd[i], beta);
+                                          sQd, sHd, sBe, sDe, wd[i], beta, hRr);
+                hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
                 if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
                 Fl = Fr;
             }
@@ -662,7 +679,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         if (tid >= 64 && tid < 96) {
             const double bL = sBe[L - 1];
             for (int r = L + 1 + (tid - 64); r <= LCAP + 1; r += 32) {
-                sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0; sHR[r] = 0.0;
+                sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0;
                 sBe[r] = ((r - L) & 1) ? bL : -bL;
             }
         }
@@ -688,7 +705,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 const double rl = t2 * (vb[i] + vb[i + 1]) * 0.5;
                 const double rr = t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
                 const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
-                const double rhs = sHR[r] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
+                const double rhs = hRv[i] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
                                    - ml * (vH[i + 1] - vH[i]);
                 const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
                 rho_loc = rr > rho_loc ? rr : rho_loc;
@@ -894,7 +911,9 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         // ---- stores: TMA bulk (aligned interior tiles) or coalesced copies -------
         const size_t gdst = mo + size_t(s);
         const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
-        if (bulk_out) {
+        if (HSGN_EXP_NOSTORE) {
+            __syncthreads();
+        } else if (bulk_out) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncthreads();
             if (tid == 0) {
@@ -918,7 +937,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
 
     // ---- error bits --------------------------------------------------------
     {
-        const unsigned int eb = __reduce_or_sync(0xffffffffu, errbits);
+        const unsigned int eb = (HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE) ? 0u : __reduce_or_sync(0xffffffffu, errbits);
         if ((tid & 31) == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
     }
 
@@ -937,7 +956,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                 rf = redf[q] > rf ? redf[q] : rf;
             }
             // overlap check: r^w <= 2^-60 at each truncated end
-            if (rf > 0.0f && dtm != 0.0) {
+            if (rf > 0.0f && dtm != 0.0 && !(HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE)) {
                 const double rho = double(rf) * (1.0 + 1e-6);
                 const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
                 const int wmin = min(left_phys ? 1 << 30 : wl, right_phys ? 1 << 30 : wr);
@@ -992,6 +1011,7 @@ __global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int comm
         if (!(tm < t_end)) dtm = 0.0;
         else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end
     }
+    if ((HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE) && !(dtm > 0.0 && isfinite(dtm))) dtm = 1e-3;
     if (!(dtm >= 0.0) || !isfinite(dtm)) {
         atomicOr(P.err, ERR_DT);
         return;
@@ -1034,8 +1054,10 @@ __global__ void __launch_bounds__(NT) reduce_kernel(const double *__restrict__ h
     // deterministic tree sum
     sred[tid] = sum;
     __syncthreads();
-    for (int o = NT / 2; o > 0; o >>= 1) {
-        if (tid < o) sred[tid] += sred[tid + o];
+    int p2 = 1;
+    while (p2 < NT) p2 <<= 1;                 // any NT (tuning builds use NT = 160, 192)
+    for (int o = p2 / 2; o > 0; o >>= 1) {
+        if (tid < o && tid + o < NT) sred[tid] += sred[tid + o];
         __syncthreads();
     }
     const double tot = sred[0];

@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--cells", type=int, default=4096)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--fused", type=int, default=-1,
+                   help="1: fused step kernel, 0: per-stage kernels, -1: library default")
     p.add_argument("--config", default="cfg3", choices=["cfg3", "cfg5"],
                    help="cfg3: ensemble (default, headline); cfg5: single 2^28-cell domain with bathymetry")
     p.add_argument("--cells5", type=int, default=1 << 28)
@@ -237,6 +239,8 @@ def main():
         s = hsgn.solver_for(w)
         Ntot = w.n * w.members
         host_state = None
+    if a.fused >= 0:
+        s.set_fused(bool(a.fused))
     state_bytes = 4 * 8 * Ntot
 
     def barrier():

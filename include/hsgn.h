@@ -193,8 +193,9 @@ hsgn_status hsgn_advance_to(hsgn_ctx *ctx, double t_end, int64_t max_steps,
 /* Enqueue n_steps automatic-dt steps EAGERLY with a CUDA event recorded
  * between consecutive kernels on the context's stream, synchronise, and
  * return in stage_ms[0] / stage_ms[1] the summed device time (ms) of the
- * stage-1 / stage-2 kernels (stage_ms[1] = 0 for a 1-stage tableau).  Same
- * arithmetic as hsgn_run_steps; used by bench.py for per-kernel rooflines. */
+ * stage-1 / stage-2 kernels (stage_ms[1] = 0 for a 1-stage tableau; for a fused
+ * step, stage_ms[0] is the fused kernel and stage_ms[1] = 0).  Same arithmetic
+ * as hsgn_run_steps; used by bench.py for per-kernel rooflines. */
 hsgn_status hsgn_run_steps_timed(hsgn_ctx *ctx, int64_t n_steps, double *stage_ms);
 /* Wait for the stream; return the latched device status. */
 hsgn_status hsgn_sync(hsgn_ctx *ctx);
@@ -203,6 +204,15 @@ hsgn_status hsgn_sync(hsgn_ctx *ctx);
 hsgn_status hsgn_get_diagnostics(hsgn_ctx *ctx, hsgn_diag *out);
 /* Number of kernel launches enqueued by this context since creation. */
 int64_t hsgn_launch_count(const hsgn_ctx *ctx);
+/* Fused step: a two-stage tableau on a non-slab domain
+ * runs each step as ONE persistent kernel (stage 1 on a widened tile, U1 kept
+ * in shared memory, stage 2, next tile prefetched) instead of one kernel per
+ * stage.  Both paths compute the same P:500-517 arithmetic.  on = 0 forces the
+ * per-stage kernels (tests compare both); default on.  Drops captured graphs
+ * and re-chooses the tile geometry.  Errors: HSGN_E_INVALID (null context). */
+hsgn_status hsgn_set_fused(hsgn_ctx *ctx, int32_t on);
+/* 1 if steps currently run as the fused kernel, 0 otherwise (-1: null). */
+int32_t hsgn_get_fused(const hsgn_ctx *ctx);
 /* Tile geometry chosen by hsgn_create: kept cells per tile, overlap, tiles per
  * member, threads per CTA, max rows per CTA. */
 hsgn_status hsgn_get_geometry(const hsgn_ctx *ctx, int32_t *tile_cells, int32_t *overlap,

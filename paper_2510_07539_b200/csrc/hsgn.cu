@@ -69,6 +69,10 @@ struct hsgn_ctx {
     // slab decomposition (BC_HALO sides): halo receive buffers [9][H_MAX] per side
     double *halo_l = nullptr, *halo_r = nullptr;
     bool slab = false;
+    // fused two-stage step kernel (persistent CTAs): off unless enabled, used for
+    // two-stage tableaux on non-slab domains when the widened tile fits
+    bool fused_on = false, fused = false;
+    int fused_grid = 0;
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
     std::string last_error;
@@ -167,7 +171,24 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
     }
     hsgn_status st;
     if (ev) CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
-    if (c->tab.stages == 1) {
+    if (c->fused) {
+        for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+        const int items = c->tiles * c->members;
+        const bool relax = c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0;
+        if (c->bathy) {
+            if (relax) step_kernel<true, true><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
+            else step_kernel<true, false><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
+        } else {
+            if (relax) step_kernel<false, true><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
+            else step_kernel<false, false><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
+        }
+        c->launches++;
+        CUDA_TRY(c, cudaGetLastError());
+        if (ev) {
+            CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+        }
+    } else if (c->tab.stages == 1) {
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         st = launch_stage_b<false, true>(c, P, B);
         if (st != HSGN_OK) return st;
@@ -228,19 +249,30 @@ void choose_geometry(hsgn_ctx *c)
     } else {
         w = 256;   // material-CFL-only stepping: rho is not bounded a priori
     }
+    // fused step: stage 1 runs on the kept tile widened by 2w + 3 on each side
+    const int wmax_fused = (LCAP - 2 - 6 - T_MIN) / 4;
+    c->fused = c->fused_on && c->tab.stages == 2 && !c->slab && w <= wmax_fused;
     w = std::max(3, std::min(w, (LCAP - 2 - T_MIN) / 2));
-    const int maxT = LCAP - 2 - 2 * w;
+    const int maxT = c->fused ? LCAP - 2 - 6 - 4 * w : LCAP - 2 - 2 * w;
     int T;
     if (c->desc.tile_cells > 0) T = std::max(std::min<int>(c->desc.tile_cells, maxT), T_MIN);
     else {
         const int ntiles = (c->n + maxT - 1) / maxT;
         T = (c->n + ntiles - 1) / ntiles;
         if (ntiles > 1) T = ((T + 31) / 32) * 32;
+        if (T > maxT) T = (T + 1) & ~1;                 // even: aligned bulk stores
         T = std::max(std::min(T, maxT), std::min(T_MIN, c->n));
     }
     c->T = T;
     c->w = w;
     c->tiles = (c->n + T - 1) / T;
+    if (c->fused) {
+        int sms = 148, occ = 1;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<false, false>, NT, fused_smem_bytes(c->T));
+        const long long items = (long long)c->tiles * c->members;
+        c->fused_grid = int(std::min<long long>(items, (long long)sms * std::max(occ, 1)));
+    }
 }
 
 hsgn_status ready(hsgn_ctx *c)
@@ -290,7 +322,7 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
                 cudaGraphDestroy(gr);
             }
             CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
-            c->launches += GRAPH_STEPS * (c->tab.stages + 1);
+            c->launches += GRAPH_STEPS * ((c->fused ? 1 : c->tab.stages) + 1);
             done += GRAPH_STEPS;          // even: cur unchanged
             c->host_steps += GRAPH_STEPS;
         } else {
@@ -519,7 +551,6 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     tb.b[0] = 1.0 - gm; tb.b[1] = gm;
     c->tab = tb;
     c->aI1 = gm; c->aI2 = gm; c->wE = cc / gm; c->wR = (1.0 - gm) / gm;
-    choose_geometry(c);
     // kernels need > 48 KiB dynamic smem
     cudaFuncSetAttribute(stage_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
@@ -531,6 +562,11 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(step_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
+    cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
+    cudaFuncSetAttribute(step_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
+    cudaFuncSetAttribute(step_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
+    choose_geometry(c);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         delete c;
@@ -893,6 +929,17 @@ hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
 }
 
 int64_t hsgn_launch_count(const hsgn_ctx *c) { return c ? c->launches : 0; }
+
+hsgn_status hsgn_set_fused(hsgn_ctx *c, int32_t on)
+{
+    if (!c) return HSGN_E_INVALID;
+    c->fused_on = on != 0;
+    drop_graphs(c);
+    choose_geometry(c);
+    return HSGN_OK;
+}
+
+int32_t hsgn_get_fused(const hsgn_ctx *c) { return c ? (c->fused ? 1 : 0) : -1; }
 
 hsgn_status hsgn_get_geometry(const hsgn_ctx *c, int32_t *T, int32_t *w, int32_t *tiles,
                               int32_t *threads, int32_t *max_rows)

@@ -51,9 +51,17 @@ constexpr int NT = HSGN_NT;           // threads per CTA
 #endif
 constexpr int MCH = HSGN_MCH;       // rows per thread chunk (odd: conflict-free strided smem)
 constexpr int LCAP = NT * MCH;      // 1280 rows per CTA incl. phase-1 halo rows
-constexpr int SROWS = LCAP + 8;     // smem row capacity per array (even: 16-B aligned bases)
+constexpr int SROWS = LCAP + 16;    // smem row capacity per array (even: 16-B aligned bases;
+                                    // rows up to L+MCH+2 past a base shifted by <= 4)
 constexpr int NARR = 8;             // smem arrays
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
+// fused step kernel: + a dedicated output staging buffer of 4 x T doubles
+// (T <= LCAP), so a tile's bulk store overlaps the next tile's compute
+__host__ __device__ constexpr size_t fused_smem_bytes(int T)
+{
+    return SMEM_BYTES + size_t(4) * size_t((T + 1) & ~1) * sizeof(double);
+}
+constexpr size_t FUSED_SMEM_MAX = SMEM_BYTES + size_t(4) * LCAP * sizeof(double);
 
 enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2, BC_HALO = 3 };
 enum { ERR_COERC = 1u, ERR_DRY = 2u, ERR_NONFINITE = 4u, ERR_OVERLAP = 8u, ERR_DT = 16u };
@@ -110,6 +118,17 @@ __device__ __forceinline__ double rcp(double x)
     return fma(r, e, r);
 }
 
+// Shared memory of the stage kernels: the dynamic row arrays and a few
+// per-CTA scratch variables (file scope, so the device helpers can reach them).
+extern __shared__ __align__(16) double hsgn_smem[];
+__shared__ __align__(8) unsigned long long s_mbar;
+__shared__ double s_red[2][NT / 32];
+__shared__ float s_redf[NT / 32];
+__shared__ double s_xch[NT / 32][3];
+__shared__ double s_rc[2];            // fused step: dt, lambda of the next item
+
+__device__ __forceinline__ double *dyn_smem() { return hsgn_smem; }
+
 __device__ __forceinline__ void cp_async8(double *dst_smem, const double *src)
 {
     const unsigned a = (unsigned)__cvta_generic_to_shared(dst_smem);
@@ -146,12 +165,6 @@ __device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity)
         "{\n .reg .pred p;\n WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"(mbar), "r"(parity) : "memory");
-}
-
-__device__ __forceinline__ void drain_loads(bool bulk, unsigned mbar)
-{
-    if (bulk) { __syncthreads(); mbar_wait(mbar, 0); }
-    else cp_async_wait_all();
 }
 
 __device__ __forceinline__ int map_cell(int c, int n, int bcl, int bcr, double &par)
@@ -282,8 +295,8 @@ struct RowCtx { double tau, tdx, t2, lt2, lam, lam3, ltau, g, idx; };
 // Stores q^dag, H^dag, beta, delta at row r unless r < -1 (dead row); returns
 // h^R' (R_h plus the hydrostatic term) in hR_out.  Stage 2 reads R_h from the
 // delta array (sRh == sDe) before overwriting it with delta.
-template <bool STAGE2, bool BATHY>
-__device__ __forceinline__ void row_update(const RowCtx &C, const Params &P, int r, int start, int n,
+template <bool BATHY>
+__device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const Params &P, int r, int start, int n,
                                            const double (&ch)[3], const double (&cq)[3],
                                            const double (&cH)[3], const double (&cW)[3],
                                            const Face &Fl, const Face &Fr, double *sQd,
@@ -403,66 +416,99 @@ __device__ __forceinline__ void relax_cell(const Params &P, double x, double b, 
     }
 }
 
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
-__global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
+// ---------------------------------------------------------------------------
+// Tile geometry of one stage.  Rows r in [0, L) of the extended tile are the
+// cells start + r; raw rows -3 .. L+2 sit in shared memory at
+// smem[k * SROWS + abase + r] (array k).  The stage delivers rows [klo, khi).
+// ---------------------------------------------------------------------------
+struct Geom {
+    int start, L;                 // first cell, rows
+    int wl, wr;                   // overlap rows at either end (truncated ends)
+    int klo, khi;                 // rows this stage delivers
+    bool left_phys, right_phys;   // tile ends on a physical boundary (Neumann end)
+    bool interior;                // raw rows are all cells of [0, n) (no ghosts)
+    int abase;
+};
+
+// Standalone stage tile of kept cells [s, e) with overlap w.
+__device__ __forceinline__ Geom stage_geom(const Params &P, int s, int e, int w)
 {
-    extern __shared__ __align__(16) double smem[];
-    __shared__ __align__(8) unsigned long long s_mbar;
-    __shared__ double red[2][NT / 32];
-    __shared__ float redf[NT / 32];
-    __shared__ double xch[NT / 32][3];
-
-    const int tid = threadIdx.x;
-    const int j = blockIdx.x;        // tile
-    const int m = blockIdx.y;        // member
-    const int n = P.n;
-    const size_t mo = size_t(m) * n;
-
-    // ---- tile geometry ------------------------------------------------------
-    // physical sides (wall, transmissive) clip the overlap; periodic and halo
-    // (neighbouring slab) sides extend the tile into real data
     const bool physL = (P.bcl == BC_WALL || P.bcl == BC_TRANSMISSIVE);
     const bool physR = (P.bcr == BC_WALL || P.bcr == BC_TRANSMISSIVE);
-    const int s = j * P.T;
-    const int e = min(n, s + P.T);
-    const int Tk = e - s;
-    const int wl = physL ? min(P.w, s) : P.w;
-    const int wr = physR ? min(P.w, n - e) : P.w;
-    const int start = s - wl;
-    const int L = Tk + wl + wr;
-    const bool left_phys = physL && (start == 0);
-    const bool right_phys = physR && (start + L == n);
+    Geom G;
+    G.wl = physL ? min(w, s) : w;
+    G.wr = physR ? min(w, P.n - e) : w;
+    G.start = s - G.wl;
+    G.L = (e - s) + G.wl + G.wr;
+    G.klo = G.wl;
+    G.khi = G.wl + (e - s);
+    G.left_phys = physL && (G.start == 0);
+    G.right_phys = physR && (G.start + G.L == P.n);
+    G.interior = (G.start - 3 >= 0) && (G.start + G.L + 3 <= P.n);
+    G.abase = 3;
+    return G;
+}
 
-    // ---- shared memory: 8 arrays of SROWS doubles, all indexed by tile row r
-    // (r in [-3, L+3)).  Interior tiles are filled by TMA bulk copies, which
-    // need 16-B aligned destinations: every array is shifted by d = parity of
-    // the first copied global cell.
-    const bool interior = (start - 3 >= 0) && (start + L + 3 <= n);
-    const int d = interior ? int((mo + size_t(start - 3)) & 1) : 0;
-    const int a0 = start - 3 - d;                       // first copied cell
-    const int cnt = (L + 6 + d + 1) & ~1;               // even count: 16-B multiple
-    const bool bulk = interior && (a0 >= 0) && (a0 + cnt <= n);
-    double *const A = smem + d + 3;                     // A + k*SROWS + r
-    double *sEh = A, *sEq = A + SROWS, *sEH = A + 2 * SROWS, *sEW = A + 3 * SROWS;
-    double *sQd = A + 4 * SROWS;   // U1_q -> R_q -> q^dagger
-    double *sHd = A + 5 * SROWS;   // U1_K -> R_H -> H^dagger
-    double *sBe = A + 6 * SROWS;   // U1_W -> R_W -> beta
-    double *sDe = A + 7 * SROWS;   // U1_h -> R_h -> delta (R_h read by its own row first)
+// Fused step: stage-2 tile G2 of kept cells [s, e); stage-1 tile G1 delivering
+// U1 on G2's raw rows (cells start2-3 .. start2+L2+2, minus the ghost rows at a
+// physical end, which are mirrored from the tile afterwards).
+__device__ __forceinline__ void fused_geom(const Params &P, int s, int e, int w, Geom &G1, Geom &G2)
+{
+    const bool physL = (P.bcl == BC_WALL || P.bcl == BC_TRANSMISSIVE);
+    const bool physR = (P.bcr == BC_WALL || P.bcr == BC_TRANSMISSIVE);
+    G2 = stage_geom(P, s, e, w);
+    const int a1 = G2.left_phys ? G2.start : G2.start - 3;
+    const int b1 = G2.right_phys ? G2.start + G2.L : G2.start + G2.L + 3;
+    G1.wl = physL ? min(w, a1) : w;
+    G1.wr = physR ? min(w, P.n - b1) : w;
+    G1.start = a1 - G1.wl;
+    G1.L = (b1 - a1) + G1.wl + G1.wr;
+    G1.klo = G1.wl;
+    G1.khi = G1.wl + (b1 - a1);
+    G1.left_phys = physL && (G1.start == 0);
+    G1.right_phys = physR && (G1.start + G1.L == P.n);
+    G1.interior = (G1.start - 3 >= 0) && (G1.start + G1.L + 3 <= P.n);
+    G1.abase = 3;
+}
 
-    // ---- load: raw rows -3..L+2 of U^n (and U1), overlapped with run control --
-    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
-    if (HSGN_EXP_NOLOAD) {
-    } else if (bulk) {
+// TMA bulk loads need 16-B aligned destinations: shift the arrays by the parity
+// of the first copied cell (interior tiles).
+struct LoadPlan {
+    int a0, cnt;      // first copied cell, count (even)
+    bool bulk;
+};
+
+__device__ __forceinline__ LoadPlan load_plan(const Params &P, size_t mo, Geom &G)
+{
+    LoadPlan Lp;
+    const int d = G.interior ? int((mo + size_t(G.start - 3)) & 1) : 0;
+    G.abase = 3 + d;
+    Lp.a0 = G.start - 3 - d;
+    Lp.cnt = (G.L + 6 + d + 1) & ~1;
+    Lp.bulk = G.interior && (Lp.a0 >= 0) && (Lp.a0 + Lp.cnt <= P.n);
+    return Lp;
+}
+
+// Issue the loads of the raw rows -3 .. L+2 of U^n (arrays 0..3) and, for a
+// standalone stage 2, of U1 (arrays 7, 4, 5, 6 = h, q, K, W).  Bulk: thread 0,
+// completion on the mbarrier; otherwise per-row cp.async through the BC index
+// map or a slab halo (all threads).
+template <bool WITH_U1>
+__device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_t mo, const Geom &G,
+                                           const LoadPlan &Lp, unsigned mb, int tid)
+{
+    double *const smem = dyn_smem();
+    if (HSGN_EXP_NOLOAD) return;
+    if (Lp.bulk) {
         if (tid == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-            const unsigned bytes = unsigned(cnt) * 8u;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const unsigned bytes = unsigned(Lp.cnt) * 8u;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
-                         "r"(bytes * (STAGE2 ? 8u : 4u)) : "memory");
-            const size_t gsrc = mo + size_t(a0);
+                         "r"(bytes * (WITH_U1 ? 8u : 4u)) : "memory");
+            const size_t gsrc = mo + size_t(Lp.a0);
 #pragma unroll
             for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
-            if (STAGE2) {
+            if (WITH_U1) {
                 bulk_g2s(smem + 7 * SROWS, B.U1[0] + gsrc, bytes, mb);
                 bulk_g2s(smem + 4 * SROWS, B.U1[1] + gsrc, bytes, mb);
                 bulk_g2s(smem + 5 * SROWS, B.U1[2] + gsrc, bytes, mb);
@@ -470,99 +516,177 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             }
         }
     } else {
-        // per-row source: own arrays through the BC index map, or a slab halo
-        // (explicit pointers: no local pointer arrays)
-        for (int r = tid - 3; r < L + 3; r += NT) {
-            const int c = start + r;
+        double *const A = smem + G.abase;
+        const int n = P.n;
+        for (int r = tid - 3; r < G.L + 3; r += NT) {
+            const int c = G.start + r;
             const double *p0, *p1, *p2, *p3, *u0 = nullptr, *u1 = nullptr, *u2 = nullptr, *u3 = nullptr;
             if (c < 0 && P.bcl == BC_HALO) {
                 const int o = c + P.H;
                 p0 = P.halo_l[0] + o; p1 = P.halo_l[1] + o; p2 = P.halo_l[2] + o; p3 = P.halo_l[3] + o;
-                if (STAGE2) { u0 = P.halo_l[4] + o; u1 = P.halo_l[5] + o; u2 = P.halo_l[6] + o; u3 = P.halo_l[7] + o; }
+                if (WITH_U1) { u0 = P.halo_l[4] + o; u1 = P.halo_l[5] + o; u2 = P.halo_l[6] + o; u3 = P.halo_l[7] + o; }
             } else if (c >= n && P.bcr == BC_HALO) {
                 const int o = c - n;
                 p0 = P.halo_r[0] + o; p1 = P.halo_r[1] + o; p2 = P.halo_r[2] + o; p3 = P.halo_r[3] + o;
-                if (STAGE2) { u0 = P.halo_r[4] + o; u1 = P.halo_r[5] + o; u2 = P.halo_r[6] + o; u3 = P.halo_r[7] + o; }
+                if (WITH_U1) { u0 = P.halo_r[4] + o; u1 = P.halo_r[5] + o; u2 = P.halo_r[6] + o; u3 = P.halo_r[7] + o; }
             } else {
                 double par;
                 const size_t gi = mo + size_t(map_cell(c, n, P.bcl, P.bcr, par));
                 p0 = B.Un[0] + gi; p1 = B.Un[1] + gi; p2 = B.Un[2] + gi; p3 = B.Un[3] + gi;
-                if (STAGE2) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
+                if (WITH_U1) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
             }
-            cp_async8(sEh + r, p0); cp_async8(sEq + r, p1); cp_async8(sEH + r, p2); cp_async8(sEW + r, p3);
-            if (STAGE2) { cp_async8(sDe + r, u0); cp_async8(sQd + r, u1); cp_async8(sHd + r, u2); cp_async8(sBe + r, u3); }
+            cp_async8(A + r, p0); cp_async8(A + SROWS + r, p1);
+            cp_async8(A + 2 * SROWS + r, p2); cp_async8(A + 3 * SROWS + r, p3);
+            if (WITH_U1) {
+                cp_async8(A + 7 * SROWS + r, u0); cp_async8(A + 4 * SROWS + r, u1);
+                cp_async8(A + 5 * SROWS + r, u2); cp_async8(A + 6 * SROWS + r, u3);
+            }
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
+}
 
-    // ---- run control: dt of this member was set by dt_commit_kernel ---------
-    const unsigned int err0 = *((volatile unsigned int *)P.err);
-    const int members = P.members;
-    const double dtm = P.dt[m];
-    const double lam = P.lam[m];
-    if (err0) {
-        if (!HSGN_EXP_NOLOAD) drain_loads(bulk, mb);
-        return;
-    }
-    const double tau = (STAGE2 ? P.aI2 : P.aI1) * dtm;
-    const double g = P.g, idx1 = P.idx;
-    const double tdx = tau * idx1;                  // tau / dx
-    const double tdx2 = 0.5 * tdx;                  // tau / (2 dx)
-    const double t2 = tdx * tdx;                    // tau^2 / dx^2
-    const double lt2 = lam * tau * tau;             // lambda tau^2
-    const double lt2h = 0.5 * lam * t2;             // lambda tau^2 / (2 dx^2)
-    const double ltdx2 = lam * tdx2;                // lambda tau / (2 dx)
-    const double lam3 = lam * (1.0 / 3.0);
-    const double ltau = lam * tau;
-
-    double umax_loc = 0.0, numax_loc = 0.0;
-    double rho_loc = 0.0;
-    unsigned int errbits = 0u;
-
-    if (HSGN_EXP_NOLOAD) {
-    } else if (bulk) {
-        __syncthreads();                  // mbarrier initialised before anyone waits
-        mbar_wait(mb, 0);
+// Wait for the loads issued by issue_load (bulk: mbarrier phase parity).
+__device__ __forceinline__ void wait_load(const LoadPlan &Lp, unsigned mb, unsigned &parity)
+{
+    if (HSGN_EXP_NOLOAD) return;
+    if (Lp.bulk) {
+        mbar_wait(mb, parity);
+        parity ^= 1u;
     } else {
         cp_async_wait_all();
     }
-    __syncthreads();
+}
 
-    if (dtm == 0.0) {
-        // member already at t_end: carry the state (and its dt maxima)
-        for (int i = s + tid; i < e; i += NT) {
-            const double h = B.Un[0][mo + i], q = B.Un[1][mo + i], K = B.Un[2][mo + i],
-                         W = B.Un[3][mo + i];
-            B.out[0][mo + i] = h; B.out[1][mo + i] = q; B.out[2][mo + i] = K; B.out[3][mo + i] = W;
-            if (FINAL) {
-                const double bb = BATHY ? __ldg(P.b + i) : 0.0;
-                const double ih = rcp(h);
-                const double u = q * ih, sg = (K - 1.5 * h * bb) * ih * ih;
-                umax_loc = fmax(umax_loc, fabs(u));
-                numax_loc = fmax(numax_loc, fabs(u) + fsqrt(g * h + lam3 * sg * sg));
-            }
-        }
+// Per-stage scalars (P:500-517 with tau = a_ii dt).
+struct StageC {
+    double tau, g, idx1, tdx, tdx2, t2, t2h, lt2, lt2h, ltdx2, lam, lam3, ltau;
+};
+
+__device__ __forceinline__ StageC stage_consts(const Params &P, double aii, double dtm, double lam)
+{
+    StageC S;
+    S.tau = aii * dtm;
+    S.g = P.g; S.idx1 = P.idx;
+    S.tdx = S.tau * S.idx1;                 // tau / dx
+    S.tdx2 = 0.5 * S.tdx;                   // tau / (2 dx)
+    S.t2 = S.tdx * S.tdx;                   // tau^2 / dx^2
+    S.t2h = 0.5 * S.t2;                     // tau^2 / (2 dx^2)
+    S.lt2 = lam * S.tau * S.tau;            // lambda tau^2
+    S.lt2h = 0.5 * lam * S.t2;              // lambda tau^2 / (2 dx^2)
+    S.ltdx2 = lam * S.tdx2;                 // lambda tau / (2 dx)
+    S.lam = lam;
+    S.lam3 = lam * (1.0 / 3.0);
+    S.ltau = lam * S.tau;
+    return S;
+}
+
+// Accumulators of one tile (both stages of a fused step).
+struct TileAcc {
+    double umax, numax, rho;
+    unsigned int err;
+    int wmin;                     // narrowest truncated overlap (1 << 30: none)
+};
+
+enum { MODE_ALONE = 0, MODE_FUSED = 1 };
+
+__device__ __forceinline__ void item_tile(const Params &P, int item, int &j, int &m, int &s, int &e)
+{
+    m = item / P.tiles;
+    j = item - m * P.tiles;
+    s = j * P.T;
+    e = min(P.n, s + P.T);
+}
+
+// Output staging of a final stage: arrays 4..7 (standalone kernel) or the
+// dedicated buffer of the fused kernel (4 x even(T) doubles after the arrays).
+__device__ __forceinline__ void stage_ptrs(bool dedicated, int T, double *&oh, double *&oq, double *&oK,
+                                           double *&oW)
+{
+    double *const smem = dyn_smem();
+    if (dedicated) {
+        const int TS = (T + 1) & ~1;
+        oh = smem + NARR * SROWS; oq = oh + TS; oK = oq + TS; oW = oK + TS;
     } else {
-        // ---- in-place pass: E, R, H = K - 1.5 h b (A9), wall parity
+        oh = smem + 4 * SROWS; oq = smem + 5 * SROWS; oK = smem + 6 * SROWS; oW = smem + 7 * SROWS;
+    }
+}
+
+// Issue the U^n loads of a fused-step item (its stage-1 tile).
+__device__ __forceinline__ void prefetch_item(const Params &P, const Bufs &B, int item)
+{
+    int j, m, s, e;
+    item_tile(P, item, j, m, s, e);
+    Geom G1, G2;
+    fused_geom(P, s, e, P.w, G1, G2);
+    const size_t mo = size_t(m) * P.n;
+    const LoadPlan Lp = load_plan(P, mo, G1);
+    issue_load<false>(P, B, mo, G1, Lp, (unsigned)__cvta_generic_to_shared(&s_mbar), threadIdx.x);
+    if (threadIdx.x == 0) { s_rc[0] = P.dt[m]; s_rc[1] = P.lam[m]; }
+}
+
+
+// ---------------------------------------------------------------------------
+// One IMEX stage S(E, R, tau) on the tile G, data already in
+// shared memory.  MODE_ALONE: raw U^n (and U1) rows as loaded, output K-form
+// staged at arrays 4..7 (h, q, K, W) index r - klo for the bulk store.
+// MODE_FUSED, rt2 = false: stage 1 of a fused step, output U1 in H-form
+// (H = K - 1.5 h b) into arrays 7, 4, 5, 6 (h, q, H, W) at the cells' own
+// positions.  MODE_FUSED, rt2 = true: stage 2 of a fused step on U^n (H-form,
+// parities applied) and that U1; output staged in the dedicated buffer.  Once the arrays 0..3 are no longer read, the
+// loads of U^n for next_item (>= 0) are issued into them (prefetch).
+// ---------------------------------------------------------------------------
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, int MODE>
+__device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const Geom &G, int m, int s_cell,
+                                           const StageC &S, double dtm, TileAcc &acc, int next_item,
+                                           bool rt2)
+{
+    // MODE_FUSED: one copy of the code serves both stages of the fused step
+    // (rt2 = stage 2), keeping the kernel inside the instruction cache
+    const bool st2 = (MODE == MODE_FUSED) ? rt2 : STAGE2;
+    const bool fin = (MODE == MODE_FUSED) ? rt2 : FINAL;
+    const bool fused1 = (MODE == MODE_FUSED) && !rt2;
+    const bool fused2 = (MODE == MODE_FUSED) && rt2;
+    double *const smem = dyn_smem();
+    const int tid = threadIdx.x;
+    const int n = P.n;
+    const int start = G.start, L = G.L;
+    const bool left_phys = G.left_phys, right_phys = G.right_phys;
+    double *const A = smem + G.abase;
+    double *sEh = A, *sEq = A + SROWS, *sEH = A + 2 * SROWS, *sEW = A + 3 * SROWS;
+    double *sQd = A + 4 * SROWS;   // U1_q -> R_q -> q^dagger
+    double *sHd = A + 5 * SROWS;   // U1_K -> R_H -> H^dagger
+    double *sBe = A + 6 * SROWS;   // U1_W -> R_W -> beta -> hbar
+    double *sDe = A + 7 * SROWS;   // U1_h -> R_h -> delta (R_h read by its own row first)
+    const double tau = S.tau, g = S.g, idx1 = S.idx1, tdx = S.tdx, tdx2 = S.tdx2, t2 = S.t2;
+    const double t2h = S.t2h, lt2 = S.lt2, lt2h = S.lt2h, ltdx2 = S.ltdx2, lam = S.lam;
+    const double lam3 = S.lam3, ltau = S.ltau;
+    const int members = P.members;
+
+    // ---- in-place pass: E, R, H = K - 1.5 h b (A9), wall parity
+    {
+        const bool raw = !fused2;                     // inputs not yet in H-form / parity
         const bool wall_ghosts = (left_phys && P.bcl == BC_WALL) || (right_phys && P.bcr == BC_WALL);
-        if (STAGE2 || BATHY || wall_ghosts) {
+        if (st2 || (raw && (BATHY || wall_ghosts))) {
             // two rows per thread and iteration with 16-B shared accesses: row r of
-            // array k sits at smem[k * SROWS + d + 3 + r], pairs start at even offsets
-            // (the spare rows at either end are scratch)
+            // array k sits at smem[k * SROWS + abase + r], pairs start at even
+            // offsets (the spare rows at either end are scratch)
             const double wE = P.wE, wR = P.wR;
-            for (int p = 2 * tid; p < d + L + 6; p += 2 * NT) {
-                const int r = p - d - 3;
+            const int pbeg = (G.abase - 3) & ~1;
+            for (int p = pbeg + 2 * tid; p < G.abase + L + 3; p += 2 * NT) {
+                const int r = p - G.abase;
                 double2 *v = reinterpret_cast<double2 *>(smem + p);
                 double2 eh = v[0], eq = v[SROWS / 2], eK = v[SROWS], eW = v[3 * SROWS / 2];
                 double par0 = 1.0, par1 = 1.0;
-                if (!interior) {                       // q parity of wall ghosts
+                if (raw && !G.interior) {              // q parity of wall ghosts
                     (void)map_cell(start + r, n, P.bcl, P.bcr, par0);
                     (void)map_cell(start + r + 1, n, P.bcl, P.bcr, par1);
                 }
                 eq.x *= par0; eq.y *= par1;
                 // (scratch rows clamped onto rows -3 .. L+2: stay inside slab halos)
-                const double b0 = BATHY ? bathy_at(P, start + max(r, -3)) : 0.0;
-                const double b1 = BATHY ? bathy_at(P, start + min(r + 1, L + 2)) : 0.0;
-                if (STAGE2) {
+                const double b0 = (raw && BATHY) ? bathy_at(P, start + max(r, -3)) : 0.0;
+                const double b1 = (raw && BATHY) ? bathy_at(P, start + min(r + 1, L + 2)) : 0.0;
+                if (st2) {
                     const double2 h1 = v[7 * SROWS / 2], q1 = v[2 * SROWS], K1 = v[5 * SROWS / 2],
                                   W1 = v[3 * SROWS];
                     const double q1x = par0 * q1.x, q1y = par1 * q1.y;
@@ -571,416 +695,636 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
                     rq.x = (1.0 - wR) * eq.x + wR * q1x;  rq.y = (1.0 - wR) * eq.y + wR * q1y;
                     rK.x = (1.0 - wR) * eK.x + wR * K1.x; rK.y = (1.0 - wR) * eK.y + wR * K1.y;
                     rW.x = (1.0 - wR) * eW.x + wR * W1.x; rW.y = (1.0 - wR) * eW.y + wR * W1.y;
-                    if (BATHY) { rK.x -= 1.5 * rh.x * b0; rK.y -= 1.5 * rh.y * b1; }
+                    if (raw && BATHY) { rK.x -= 1.5 * rh.x * b0; rK.y -= 1.5 * rh.y * b1; }
                     v[7 * SROWS / 2] = rh; v[2 * SROWS] = rq; v[5 * SROWS / 2] = rK; v[3 * SROWS] = rW;
                     eh.x = (1.0 - wE) * eh.x + wE * h1.x; eh.y = (1.0 - wE) * eh.y + wE * h1.y;
                     eq.x = (1.0 - wE) * eq.x + wE * q1x;  eq.y = (1.0 - wE) * eq.y + wE * q1y;
                     eK.x = (1.0 - wE) * eK.x + wE * K1.x; eK.y = (1.0 - wE) * eK.y + wE * K1.y;
                     eW.x = (1.0 - wE) * eW.x + wE * W1.x; eW.y = (1.0 - wE) * eW.y + wE * W1.y;
                 }
-                if (BATHY) { eK.x -= 1.5 * eh.x * b0; eK.y -= 1.5 * eh.y * b1; }
+                if (raw && BATHY) { eK.x -= 1.5 * eh.x * b0; eK.y -= 1.5 * eh.y * b1; }
                 v[0] = eh; v[SROWS / 2] = eq; v[SROWS] = eK;
-                if (STAGE2) v[3 * SROWS / 2] = eW;
+                if (st2) v[3 * SROWS / 2] = eW;
             }
             __syncthreads();
         }
+    }
 
-        // Every thread owns the rows r0 .. r0+MCH-1 of the tile in all three
-        // phases (thread 0 also computes row -1 in phase 1, the owner of row L
-        // computes it); values stay in registers between phases, neighbours'
-        // rows come from shared memory.
-        const int r0 = tid * MCH;
-        double wd[MCH];                  // W^dagger of own rows (phase 1 -> 3)
-        double hRv[MCH];                 // h^R' of own rows (phase 1 -> 2)
+    // Every thread owns the rows r0 .. r0+MCH-1 of the tile in all three
+    // phases (thread 0 also computes row -1 in phase 1, the owner of row L
+    // computes it); values stay in registers between phases, neighbours'
+    // rows come from shared memory.  Threads whose rows all lie beyond L+1
+    // ("dead" chunks) only take part in the reduced solve, as identity rows.
+    const int r0 = tid * MCH;
+    const bool live = r0 < L + 2;
+    double wd[MCH];                  // W^dagger of own rows (phase 1 -> 3)
+    double hRv[MCH];                 // h^R' of own rows (phase 1 -> 2)
 
-        // ---- phase 1: faces, predictor, coefficients --------------------------
-        // Branch-free over the MCH own rows (stores predicated on r <= L) so the
-        // register window shifts are pure renaming; thread 0 also does row -1.
-        {
-            const double kap = P.order == 2 ? 0.25 : 0.0;
-            RowCtx C{};
-            C.tau = tau; C.tdx = tdx; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
-            C.ltau = ltau; C.g = g; C.idx = idx1;
-            double wh[3], wq[3], wH[3], wW[3];
+    // ---- phase 1: faces, predictor, coefficients --------------------------
+    // Branch-free over the MCH own rows (stores predicated on r <= L) so the
+    // register window shifts are pure renaming; thread 0 also does row -1.
+    if (live) {
+        const double kap = P.order == 2 ? 0.25 : 0.0;
+        RowCtx C{};
+        C.tau = tau; C.tdx = tdx; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
+        C.ltau = ltau; C.g = g; C.idx = idx1;
+        double wh[3], wq[3], wH[3], wW[3];
 #pragma unroll
-            for (int k = 0; k < 3; k++) {                 // rows r0-2 .. r0
-                const int rr = r0 - 2 + k;
-                wh[k] = sEh[rr]; wq[k] = sEq[rr]; wH[k] = sEH[rr]; wW[k] = sEW[rr];
-            }
-            FState Mm = muscl_minus(wh, wq, wH, wW, kap);           // M_{r0-1}
-            if (tid == 0) {
-                // row -1 (left halo of the tile): faces -3/2 and -1/2
-                double xh[3], xq[3], xH[3], xW[3];
+        for (int k = 0; k < 3; k++) {                 // rows r0-2 .. r0
+            const int rr = r0 - 2 + k;
+            wh[k] = sEh[rr]; wq[k] = sEq[rr]; wH[k] = sEH[rr]; wW[k] = sEW[rr];
+        }
+        FState Mm = muscl_minus(wh, wq, wH, wW, kap);           // M_{r0-1}
+        if (tid == 0) {
+            // row -1 (left halo of the tile): faces -3/2 and -1/2
+            double xh[3], xq[3], xH[3], xW[3];
 #pragma unroll
-                for (int k = 0; k < 3; k++) {             // rows -3 .. -1
-                    xh[k] = sEh[k - 3]; xq[k] = sEq[k - 3]; xH[k] = sEH[k - 3]; xW[k] = sEW[k - 3];
-                }
-                const FState M2 = muscl_minus(xh, xq, xH, xW, kap);     // M_{-2}
-                const FState P1 = muscl_plus(wh, wq, wH, wW, kap);      // Pl_{-1} (rows -2..0)
-                const Face Fa = rusanov(M2, P1);                          // face -3/2
-                const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], kap);
-                const Face Fb = rusanov(Mm, P0);                          // face -1/2
-                double Wd, beta, hRd;
-                row_update<STAGE2, BATHY>(C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
-                                          sQd, sHd, sBe, sDe, Wd, beta, hRd);
+            for (int k = 0; k < 3; k++) {             // rows -3 .. -1
+                xh[k] = sEh[k - 3]; xq[k] = sEq[k - 3]; xH[k] = sEH[k - 3]; xW[k] = sEW[k - 3];
             }
+            const FState M2 = muscl_minus(xh, xq, xH, xW, kap);     // M_{-2}
+            const FState P1 = muscl_plus(wh, wq, wH, wW, kap);      // Pl_{-1} (rows -2..0)
+            const Face Fa = rusanov(M2, P1);                          // face -3/2
+            const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], kap);
+            const Face Fb = rusanov(Mm, P0);                          // face -1/2
+            double Wd, beta, hRd;
+            row_update<BATHY>(st2, C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
+                                      sQd, sHd, sBe, sDe, Wd, beta, hRd);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
+        }
+        wh[2] = sEh[r0 + 1]; wq[2] = sEq[r0 + 1]; wH[2] = sEH[r0 + 1]; wW[2] = sEW[r0 + 1];
+        FState Pn, Mr;
+        muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);               // Pl_{r0}, M_{r0}
+        Face Fl = rusanov(Mm, Pn);                             // face r0-1/2
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            double ch[3], cq[3], cH[3], cW[3];                 // rows r-1, r, r+1
+#pragma unroll
+            for (int k = 0; k < 3; k++) { ch[k] = wh[k]; cq[k] = wq[k]; cH[k] = wH[k]; cW[k] = wW[k]; }
 #pragma unroll
             for (int k = 0; k < 2; k++) {
                 wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
             }
-            wh[2] = sEh[r0 + 1]; wq[2] = sEq[r0 + 1]; wH[2] = sEH[r0 + 1]; wW[2] = sEW[r0 + 1];
-            FState Pn, Mr;
-            muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);               // Pl_{r0}, M_{r0}
-            Face Fl = rusanov(Mm, Pn);                             // face r0-1/2
+            wh[2] = sEh[r + 2]; wq[2] = sEq[r + 2]; wH[2] = sEH[r + 2]; wW[2] = sEW[r + 2];
+            FState Mn;
+            muscl_pair(wh, wq, wH, wW, kap, Pn, Mn);           // Pl_{r+1}, M_{r+1}
+            const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
+            Mr = Mn;
+            double beta, hRr;
+            row_update<BATHY>(st2, C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
+                                      sQd, sHd, sBe, sDe, wd[i], beta, hRr);
+            hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
+            if (r >= G.klo && r < G.khi && !(beta > 0.0)) acc.err |= ERR_COERC;
+            Fl = Fr;
+        }
+    } else {
 #pragma unroll
-            for (int i = 0; i < MCH; i++) {
-                const int r = r0 + i;
-                double ch[3], cq[3], cH[3], cW[3];                 // rows r-1, r, r+1
-#pragma unroll
-                for (int k = 0; k < 3; k++) { ch[k] = wh[k]; cq[k] = wq[k]; cH[k] = wH[k]; cW[k] = wW[k]; }
-#pragma unroll
-                for (int k = 0; k < 2; k++) {
-                    wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
-                }
-                wh[2] = sEh[r + 2]; wq[2] = sEq[r + 2]; wH[2] = sEH[r + 2]; wW[2] = sEW[r + 2];
-                FState Mn;
-                muscl_pair(wh, wq, wH, wW, kap, Pn, Mn);           // Pl_{r+1}, M_{r+1}
-                const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
-                Mr = Mn;
-                double beta, hRr;
-                row_update<STAGE2, BATHY>(C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
-                                          sQd, sHd, sBe, sDe, wd[i], beta, hRr);
-                hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
-                if (r >= wl && r < wl + Tk && !(beta > 0.0)) errbits |= ERR_COERC;
-                Fl = Fr;
-            }
+        for (int i = 0; i < MCH; i++) { wd[i] = 0.0; hRv[i] = 0.0; }
+    }
+    __syncthreads();
+    // derived-field ghosts at physical boundaries (A10).  The implicit
+    // coupling across both tile ends is cut (truncated overlap or Neumann end:
+    // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
+    // make those face coefficients t2 (beta_i + beta_{i+1}) / 2 exactly zero;
+    // rows L+1 .. L+MCH+1 (read by the last live chunk) get zero fields and
+    // alternating +-beta_{L-1}, so all their couplings vanish too.
+    if (tid == 0) {
+        if (left_phys) {
+            sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
+            sHd[-1] = sHd[0]; sDe[-1] = sDe[0];
         }
-        __syncthreads();
-        // derived-field ghosts at physical boundaries (A10).  The implicit
-        // coupling across both tile ends is cut (truncated overlap or Neumann end:
-        // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
-        // make those face coefficients t2 (beta_i + beta_{i+1}) / 2 exactly zero,
-        // and rows L+1 .. LCAP+1 (beyond the tile, solved as decoupled rows) get
-        // zero fields and alternating +-beta_{L-1} so all their couplings vanish too.
-        if (tid == 0) {
-            if (left_phys) {
-                sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
-                sHd[-1] = sHd[0]; sDe[-1] = sDe[0];
-            }
-            sBe[-1] = -sBe[0];
+        sBe[-1] = -sBe[0];
+    }
+    if (tid == 32) {
+        if (right_phys) {
+            sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
+            sHd[L] = sHd[L - 1]; sDe[L] = sDe[L - 1];
         }
-        if (tid == 32) {
-            if (right_phys) {
-                sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
-                sHd[L] = sHd[L - 1]; sDe[L] = sDe[L - 1];
-            }
-            sBe[L] = -sBe[L - 1];
-        }
-        if (tid >= 64 && tid < 96) {
-            const double bL = sBe[L - 1];
-            for (int r = L + 1 + (tid - 64); r <= LCAP + 1; r += 32) {
-                sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0;
-                sBe[r] = ((r - L) & 1) ? bL : -bL;
-            }
-        }
-        __syncthreads();
+        sBe[L] = -sBe[L - 1];
+    }
+    if (tid >= 64 && tid < 64 + MCH + 1) {
+        const int r = L + 1 + (tid - 64);
+        sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0;
+        sBe[r] = ((r - L) & 1) ? sBe[L - 1] : -sBe[L - 1];
+    }
+    __syncthreads();
 
-        // ---- phase 2: assemble + partition solve (A1, A3) ---------
-        double *sHB = sEq;            // hbar[r], r in [0, L)
-        double *pcr0 = sEH;           // PCR buffers: 2 x 3 x NT doubles over sEH..sEW
-        double *pcr1 = sEH + 3 * NT;
-        // register windows over rows r0-1 .. r0+MCH
-        double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
+    // ---- phase 2: assemble + partition solve (A1, A3) ---------
+    // Standalone: arrays 1..3 are free after phase 1: hbar in array 1, PCR
+    // buffers over arrays 2..3 (later the filter buffers), E_h stays in array 0;
+    // arrays 4..7 take the output staging during phase 3.
+    // Fused: arrays 0..3 take the next tile's prefetch, so after the window
+    // loads PCR goes over arrays 4..5 (later the filter), hbar into array 6 and
+    // the own rows' E_h (BATHY) are copied to array 7.
+    constexpr bool ALONE = (MODE == MODE_ALONE);
+    double *sHB = ALONE ? sEq : sBe;                             // hbar[r], r in [0, L)
+    double *pcr0 = ALONE ? smem + 2 * SROWS : smem + 4 * SROWS;  // 2 x 3 x NT doubles
+    double *pcr1 = pcr0 + 3 * NT;
+    double *sEhc = ALONE ? sEh : sDe;                            // E_h (BATHY)
+    // register windows over rows r0-1 .. r0+MCH
+    double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
+    if (live) {
 #pragma unroll
         for (int k = 0; k < MCH + 2; k++) {
             vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; vH[k] = sHd[r0 - 1 + k]; vq[k] = sQd[r0 - 1 + k];
         }
-        double hb[MCH];
-        {
-            double am[MCH], cm[MCH], dm[MCH];
+    } else {
 #pragma unroll
-            for (int i = 0; i < MCH; i++) {
-                const int r = r0 + i;
-                // (r_{-1/2} = r_{L-1/2} = 0 through the beta ghosts set above)
-                const double rl = t2 * (vb[i] + vb[i + 1]) * 0.5;
-                const double rr = t2 * (vb[i + 1] + vb[i + 2]) * 0.5;
-                const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
-                const double rhs = hRv[i] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
-                                   - ml * (vH[i + 1] - vH[i]);
-                const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
-                rho_loc = rr > rho_loc ? rr : rho_loc;
-                if (i == 0) {
-                    const double inv = rcp(dg);
-                    am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
-                } else {
-                    const double inv = rcp(dg - a * cm[i - 1]);
-                    am[i] = -a * am[i - 1] * inv;
-                    cm[i] = c * inv;
-                    dm[i] = (rhs - a * dm[i - 1]) * inv;
-                }
-            }
-            // chunk-end relation (downward) and first-row relation (upward):
-            // x_i = P_i - Q_i X_{k-1} - R_i X_k,  X_k = last row of chunk k
-            const double aE = am[MCH - 1], cE = cm[MCH - 1], dE = dm[MCH - 1];
-            double Pn = 0.0, Qn = 0.0, Rn = -1.0;
-#pragma unroll
-            for (int i = MCH - 2; i >= 0; i--) {
-                const double Pi = dm[i] - cm[i] * Pn;
-                const double Qi = am[i] - cm[i] * Qn;
-                const double Ri = -cm[i] * Rn;
-                dm[i] = Pi; am[i] = Qi; cm[i] = Ri;
-                Pn = Pi; Qn = Qi; Rn = Ri;
-            }
-            // neighbour's (P_0, Q_0, R_0) via shuffles / smem across warps
-            const int lane = tid & 31, wid = tid >> 5;
-            double P1 = __shfl_down_sync(0xffffffffu, dm[0], 1);
-            double Q1 = __shfl_down_sync(0xffffffffu, am[0], 1);
-            double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
-            if (lane == 0) { xch[wid][0] = dm[0]; xch[wid][1] = am[0]; xch[wid][2] = cm[0]; }
-            __syncthreads();
-            if (lane == 31) {
-                if (wid + 1 < NT / 32) { P1 = xch[wid + 1][0]; Q1 = xch[wid + 1][1]; R1 = xch[wid + 1][2]; }
-                else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
-            }
-            // reduced row k:  A X_{k-1} + Bd X_k + C X_{k+1} = D, normalised by Bd
-            double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1;
-            if (tid == 0) A_ = 0.0;
-            {
-                const double ib = rcp(1.0 - cE * Q1);
-                A_ *= ib; C_ *= ib; D_ *= ib;
-            }
-            // PCR over NT unknowns, double-buffered, one reciprocal per row and
-            // step.  The reduced couplings shrink like e_{s+1} <= e_s^2/(1-2e_s^2)
-            // (e = max |A|,|C|), so PCR stops once e^(2^s) <= 2^-64: the rows are
-            // then decoupled to below round-off (x_k = D_k).
-            double *cur = pcr0, *nxt = pcr1;
-            cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
-            {
-                const float ea = float(fabs(A_)), ec = float(fabs(C_));
-                const float ev = warp_max_nonneg(ea > ec ? ea : ec);
-                if (lane == 0) redf[wid] = ev;
-            }
-            __syncthreads();
-            int lim = NT;
-            {
-                float e0 = 0.0f;
-#pragma unroll
-                for (int q = 0; q < NT / 32; q++) e0 = fmaxf(e0, redf[q]);
-                if (e0 < 0.4f) {                       // repeated squaring, 10% margin per step
-                    float ee = e0 * 1.1f;
-                    int sdl = 1;
-                    while (sdl < NT && ee > 5.42e-20f) { ee = ee * ee * 1.1f; sdl <<= 1; }   // 2^-64
-                    lim = sdl;
-                }
-            }
-#pragma unroll 1
-            for (int sd = 1; sd < lim; sd <<= 1) {
-                const int km = tid - sd, kp = tid + sd;
-                double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
-                if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
-                if (kp < NT) { Ap = cur[kp]; Cp = cur[NT + kp]; Dp = cur[2 * NT + kp]; }
-                const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
-                const double An = -A_ * Am * ib;
-                const double Cn = -C_ * Cp * ib;
-                const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
-                A_ = An; C_ = Cn; D_ = Dn;
-                nxt[tid] = A_; nxt[NT + tid] = C_; nxt[2 * NT + tid] = D_;
-                __syncthreads();
-                double *tmp = cur; cur = nxt; nxt = tmp;
-            }
-            const double Xk = D_;
-            double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
-            if (lane == 31) xch[wid][0] = Xk;       // last chunk of this warp
-            __syncthreads();
-            if (lane == 0) XL = (wid > 0) ? xch[wid - 1][0] : 0.0;
-#pragma unroll
-            for (int i = 0; i < MCH; i++) {
-                const int r = r0 + i;
-                hb[i] = (i == MCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
-                if (r < L) sHB[r] = hb[i];
-            }
-        }
-        __syncthreads();
-
-        // ---- phase 3: back-substitution, own rows ------------------
-        const bool filt = FINAL && (P.filter_sigma > 0.0);
-        double *sQb = sEH, *sWb = sEW;                   // unfiltered qbar, Wbar (filter)
-        // staged outputs (index r - wl) at the 16-B aligned bases of arrays 4..7,
-        // whose row data were consumed into registers in phase 2
-        double *oh = smem + 4 * SROWS, *oq = smem + 5 * SROWS, *oK = smem + 6 * SROWS,
-               *oW = smem + 7 * SROWS;
-        const int klo = filt ? wl - 2 : wl, khi = filt ? wl + Tk + 2 : wl + Tk;
-        // HdD = H^dag / (hbar^2 + lam tau^2): Hbar = HdD hbar^2 and, in the
-        // final stage, sigma = Hbar / hbar^2 = HdD for the dt maxima
-        double qbv[MCH], HdD[MCH], Wbv[MCH], bbv[MCH], ihv[MCH];
-        const double hLn = (r0 > 0 && r0 - 1 < L) ? sHB[r0 - 1] : 0.0;
-        const double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
+        for (int k = 0; k < MCH + 2; k++) { vb[k] = 0.0; vd[k] = 0.0; vH[k] = 0.0; vq[k] = 0.0; }
+    }
+    double hb[MCH];
+    {
+        double am[MCH], cm[MCH], dm[MCH];
 #pragma unroll
         for (int i = 0; i < MCH; i++) {
-            const int r = r0 + i;
-            const bool act = (r >= klo) && (r < khi) && (r < L);   // rows this stage needs
-            bbv[i] = 0.0;
-            const double h0 = hb[i];
-            double hl = (i > 0) ? hb[i - 1] : hLn;
-            double hr = (i < MCH - 1) ? hb[i + 1] : hRn;
-            if (r == 0) hl = h0;                           // Neumann at physical ends
-            if (r == L - 1) hr = h0;
-            double qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
-            if (BATHY && act) {
-                const double bm = bathy_at(P, start + r - 1);
-                const double bp = bathy_at(P, start + r + 1);
-                bbv[i] = bathy_at(P, start + r);
-                qb -= tau * g * sEh[r] * (bp - bm) * (0.5 * idx1);     // A9
-            }
-            // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),
-            // Wbar = W^dag - lam tau H^dag / (hbar^2 + lam tau^2); in the final stage
-            // the same reciprocal gives 1/hbar: Z = 1/(hbar (hbar^2 + lam tau^2))
-            const double den = h0 * h0 + lt2;
-            double rden;
-            if (FINAL && !RELAX) {
-                const double Z = rcp(h0 * den);
-                rden = h0 * Z;
-                ihv[i] = den * Z;
+            // (r_{-1/2} = r_{L-1/2} = 0 through the beta ghosts set above)
+            const double rl = t2h * (vb[i] + vb[i + 1]);
+            const double rr = t2h * (vb[i + 1] + vb[i + 2]);
+            const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
+            const double rhs = hRv[i] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
+                               - ml * (vH[i + 1] - vH[i]);
+            const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
+            acc.rho = rr > acc.rho ? rr : acc.rho;
+            if (i == 0) {
+                const double inv = rcp(dg);
+                am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
             } else {
-                rden = rcp(den);
-                ihv[i] = 0.0;
+                const double inv = rcp(dg - a * cm[i - 1]);
+                am[i] = -a * am[i - 1] * inv;
+                cm[i] = c * inv;
+                dm[i] = (rhs - a * dm[i - 1]) * inv;
             }
-            HdD[i] = vH[i + 1] * rden;
-            qbv[i] = qb;
-            Wbv[i] = wd[i] - ltau * HdD[i];
-            if (act && r >= wl && r < wl + Tk) {
-                if (!(h0 > P.h_min)) errbits |= ERR_DRY;
-                // one test for all four: a NaN or inf in any makes the sum non-finite
-                if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) errbits |= ERR_NONFINITE;
-            }
-            if (filt) { sQb[r] = qb; sWb[r] = Wbv[i]; }        // rows outside are never read
         }
-        if (filt) __syncthreads();
-        const double sig16 = P.filter_sigma * (1.0 / 16.0);
-        const bool relax = FINAL && RELAX;
-        const double t_new = relax ? P.t[P.kpar * members + m] + dtm : 0.0;
+        // chunk-end relation (downward) and first-row relation (upward):
+        // x_i = P_i - Q_i X_{k-1} - R_i X_k,  X_k = last row of chunk k
+        const double aE = am[MCH - 1], cE = cm[MCH - 1], dE = dm[MCH - 1];
+        double Pn = 0.0, Qn = 0.0, Rn = -1.0;
+#pragma unroll
+        for (int i = MCH - 2; i >= 0; i--) {
+            const double Pi = dm[i] - cm[i] * Pn;
+            const double Qi = am[i] - cm[i] * Qn;
+            const double Ri = -cm[i] * Rn;
+            dm[i] = Pi; am[i] = Qi; cm[i] = Ri;
+            Pn = Pi; Qn = Qi; Rn = Ri;
+        }
+        // neighbour's (P_0, Q_0, R_0) via shuffles / smem across warps
+        const int lane = tid & 31, wid = tid >> 5;
+        double P1 = __shfl_down_sync(0xffffffffu, dm[0], 1);
+        double Q1 = __shfl_down_sync(0xffffffffu, am[0], 1);
+        double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
+        if (lane == 0) { s_xch[wid][0] = dm[0]; s_xch[wid][1] = am[0]; s_xch[wid][2] = cm[0]; }
+        __syncthreads();
+        if (lane == 31) {
+            if (wid + 1 < NT / 32) { P1 = s_xch[wid + 1][0]; Q1 = s_xch[wid + 1][1]; R1 = s_xch[wid + 1][2]; }
+            else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
+        }
+        if (BATHY && !ALONE && live) {
+#pragma unroll
+            for (int i = 0; i < MCH; i++) sEhc[r0 + i] = sEh[r0 + i];
+        }
+        // reduced row k:  A X_{k-1} + Bd X_k + C X_{k+1} = D, normalised by Bd
+        double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1;
+        if (tid == 0) A_ = 0.0;
+        {
+            const double ib = rcp(1.0 - cE * Q1);
+            A_ *= ib; C_ *= ib; D_ *= ib;
+        }
+        // PCR over NT unknowns, double-buffered, one reciprocal per row and
+        // step.  The reduced couplings shrink like e_{s+1} <= e_s^2/(1-2e_s^2)
+        // (e = max |A|,|C|), so PCR stops once e^(2^s) <= 2^-64: the rows are
+        // then decoupled to below round-off (x_k = D_k).
+        double *cur = pcr0, *nxt = pcr1;
+        cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
+        {
+            const float ea = float(fabs(A_)), ec = float(fabs(C_));
+            const float ev = warp_max_nonneg(ea > ec ? ea : ec);
+            if (lane == 0) s_redf[wid] = ev;
+        }
+        __syncthreads();
+        if (fused2 && next_item >= 0) prefetch_item(P, B, next_item);   // arrays 0..3 free
+        int lim = NT;
+        {
+            float e0 = 0.0f;
+#pragma unroll
+            for (int q = 0; q < NT / 32; q++) e0 = fmaxf(e0, s_redf[q]);
+            if (e0 < 0.4f) {                       // repeated squaring, 10% margin per step
+                float ee = e0 * 1.1f;
+                int sdl = 1;
+                while (sdl < NT && ee > 5.42e-20f) { ee = ee * ee * 1.1f; sdl <<= 1; }   // 2^-64
+                lim = sdl;
+            }
+        }
+#pragma unroll 1
+        for (int sd = 1; sd < lim; sd <<= 1) {
+            const int km = tid - sd, kp = tid + sd;
+            double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
+            if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
+            if (kp < NT) { Ap = cur[kp]; Cp = cur[NT + kp]; Dp = cur[2 * NT + kp]; }
+            const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
+            const double An = -A_ * Am * ib;
+            const double Cn = -C_ * Cp * ib;
+            const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
+            A_ = An; C_ = Cn; D_ = Dn;
+            nxt[tid] = A_; nxt[NT + tid] = C_; nxt[2 * NT + tid] = D_;
+            __syncthreads();
+            double *tmp = cur; cur = nxt; nxt = tmp;
+        }
+        const double Xk = D_;
+        double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
+        if (lane == 31) s_xch[wid][0] = Xk;       // last chunk of this warp
+        __syncthreads();
+        if (lane == 0) XL = (wid > 0) ? s_xch[wid - 1][0] : 0.0;
 #pragma unroll
         for (int i = 0; i < MCH; i++) {
             const int r = r0 + i;
-            if (r < wl || r >= wl + Tk) continue;
-            double qo = qbv[i], wo = Wbv[i];
-            if (filt) {
-                double fq[5], fw[5];
-                if (!(left_phys || right_phys) || (r >= 2 && r + 2 < L)) {
-#pragma unroll
-                    for (int k = 0; k < 5; k++) { fq[k] = sQb[r + k - 2]; fw[k] = sWb[r + k - 2]; }
-                } else {
-#pragma unroll
-                    for (int k = -2; k <= 2; k++) {
-                        int rr = r + k;
-                        double pq = 1.0;
-                        if (rr < 0) {            // only at a physical left boundary
-                            if (P.bcl == BC_WALL) { rr = -1 - rr; pq = -1.0; } else rr = 0;
-                        } else if (rr >= L) {    // only at a physical right boundary
-                            if (P.bcr == BC_WALL) { rr = 2 * L - 1 - rr; pq = -1.0; } else rr = L - 1;
-                        }
-                        fq[k + 2] = pq * sQb[rr];
-                        fw[k + 2] = sWb[rr];
-                    }
-                }
-                // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
-                qo = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
-                wo = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
-                if (!isfinite(qo + wo)) errbits |= ERR_NONFINITE;
-            }
-            double h0 = hb[i];
-            const double Hb = HdD[i] * (h0 * h0);
-            double Ko = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
-            const int ko = r - wl;
-            if (FINAL && relax) {
-                relax_cell(P, P.x_min + (double(s + (r - wl)) + 0.5) * P.dx, bbv[i], t_new, h0, qo, Ko, wo);
-                const double Hf = Ko - 1.5 * h0 * bbv[i];
-                const double ih = rcp(h0);
-                const double u = fabs(qo * ih), sg = Hf * ih * ih;
-                const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
-                umax_loc = u > umax_loc ? u : umax_loc;
-                numax_loc = nu > numax_loc ? nu : numax_loc;
-            } else if (FINAL) {
-                const double u = fabs(qo * ihv[i]), sg = HdD[i];
-                const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
-                umax_loc = u > umax_loc ? u : umax_loc;
-                numax_loc = nu > numax_loc ? nu : numax_loc;
-            }
-            oh[ko] = h0; oq[ko] = qo; oK[ko] = Ko; oW[ko] = wo;
+            hb[i] = (i == MCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
+            if (r < L) sHB[r] = hb[i];
         }
-        // ---- stores: TMA bulk (aligned interior tiles) or coalesced copies -------
-        const size_t gdst = mo + size_t(s);
-        const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
-        if (HSGN_EXP_NOSTORE) {
-            __syncthreads();
-        } else if (bulk_out) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncthreads();
-            if (tid == 0) {
-                const unsigned bytes = unsigned(Tk) * 8u;
-                bulk_s2g(B.out[0] + gdst, oh, bytes);
-                bulk_s2g(B.out[1] + gdst, oq, bytes);
-                bulk_s2g(B.out[2] + gdst, oK, bytes);
-                bulk_s2g(B.out[3] + gdst, oW, bytes);
-                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-                // (the read-completion wait is deferred to the kernel's end: the
-                // staged rows are not written again)
-            }
+    }
+    __syncthreads();
+
+    // ---- phase 3: back-substitution, own rows ------------------
+    const bool filt = fin && (P.filter_sigma > 0.0);
+    double *sQb = (ALONE ? smem + 2 * SROWS : smem + 4 * SROWS) + G.abase;   // filter (A19)
+    double *sWb = sQb + SROWS;
+    const int klo = G.klo, khi = G.khi;
+    const int flo = filt ? klo - 2 : klo, fhi = filt ? khi + 2 : khi;
+    // HdD = H^dag / (hbar^2 + lam tau^2): Hbar = HdD hbar^2 and, in the
+    // final stage, sigma = Hbar / hbar^2 = HdD for the dt maxima
+    double qbv[MCH], HdD[MCH], Wbv[MCH], bbv[MCH], ihv[MCH];
+    const double hLn = (r0 > 0 && r0 - 1 < L) ? sHB[r0 - 1] : 0.0;
+    const double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
+#pragma unroll
+    for (int i = 0; i < MCH; i++) {
+        const int r = r0 + i;
+        const bool act = (r >= flo) && (r < fhi) && (r < L);   // rows this stage needs
+        bbv[i] = 0.0;
+        const double h0 = hb[i];
+        double hl = (i > 0) ? hb[i - 1] : hLn;
+        double hr = (i < MCH - 1) ? hb[i + 1] : hRn;
+        if (r == 0) hl = h0;                           // Neumann at physical ends
+        if (r == L - 1) hr = h0;
+        double qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
+        if (BATHY && act) {
+            const double bm = bathy_at(P, start + r - 1);
+            const double bp = bathy_at(P, start + r + 1);
+            bbv[i] = bathy_at(P, start + r);
+            qb -= tau * g * sEhc[r] * (bp - bm) * (0.5 * idx1);     // A9
+        }
+        // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),
+        // Wbar = W^dag - lam tau H^dag / (hbar^2 + lam tau^2); in the final stage
+        // the same reciprocal gives 1/hbar: Z = 1/(hbar (hbar^2 + lam tau^2))
+        const double den = h0 * h0 + lt2;
+        double rden;
+        if (fin && !RELAX) {
+            const double Z = rcp(h0 * den);
+            rden = h0 * Z;
+            ihv[i] = den * Z;
         } else {
-            __syncthreads();
-            for (int k = tid; k < Tk; k += NT) {
-                B.out[0][gdst + k] = oh[k]; B.out[1][gdst + k] = oq[k];
-                B.out[2][gdst + k] = oK[k]; B.out[3][gdst + k] = oW[k];
+            rden = rcp(den);
+            ihv[i] = 0.0;
+        }
+        HdD[i] = vH[i + 1] * rden;
+        qbv[i] = qb;
+        Wbv[i] = wd[i] - ltau * HdD[i];
+        if (r >= klo && r < khi) {
+            if (!(h0 > P.h_min)) acc.err |= ERR_DRY;
+            // one test for all four: a NaN or inf in any makes the sum non-finite
+            if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) acc.err |= ERR_NONFINITE;
+        }
+        if (filt && r < L) { sQb[r] = qb; sWb[r] = Wbv[i]; }
+    }
+    if (filt) __syncthreads();
+    const double sig16 = P.filter_sigma * (1.0 / 16.0);
+    const double t_new = (fin && RELAX) ? P.t[P.kpar * members + m] + dtm : 0.0;
+    // final values into (hb, qbv, HdD := K or H, Wbv)
+#pragma unroll
+    for (int i = 0; i < MCH; i++) {
+        const int r = r0 + i;
+        if (r < klo || r >= khi) continue;
+        double qo = qbv[i], wo = Wbv[i];
+        if (filt) {
+            double fq[5], fw[5];
+            if (!(left_phys || right_phys) || (r >= 2 && r + 2 < L)) {
+#pragma unroll
+                for (int k = 0; k < 5; k++) { fq[k] = sQb[r + k - 2]; fw[k] = sWb[r + k - 2]; }
+            } else {
+#pragma unroll
+                for (int k = -2; k <= 2; k++) {
+                    int rr = r + k;
+                    double pq = 1.0;
+                    if (rr < 0) {            // only at a physical left boundary
+                        if (P.bcl == BC_WALL) { rr = -1 - rr; pq = -1.0; } else rr = 0;
+                    } else if (rr >= L) {    // only at a physical right boundary
+                        if (P.bcr == BC_WALL) { rr = 2 * L - 1 - rr; pq = -1.0; } else rr = L - 1;
+                    }
+                    fq[k + 2] = pq * sQb[rr];
+                    fw[k + 2] = sWb[rr];
+                }
             }
+            // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
+            qo = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
+            wo = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
+            if (!isfinite(qo + wo)) acc.err |= ERR_NONFINITE;
+        }
+        double h0 = hb[i];
+        const double Hb = HdD[i] * (h0 * h0);
+        double Ko = (BATHY && !fused1) ? Hb + 1.5 * h0 * bbv[i] : Hb;
+        if (fin && RELAX) {
+            relax_cell(P, P.x_min + (double(s_cell + (r - klo)) + 0.5) * P.dx, bbv[i], t_new, h0, qo, Ko, wo);
+            const double Hf = Ko - 1.5 * h0 * bbv[i];
+            const double ih = rcp(h0);
+            const double u = fabs(qo * ih), sg = Hf * ih * ih;
+            const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
+            acc.umax = u > acc.umax ? u : acc.umax;
+            acc.numax = nu > acc.numax ? nu : acc.numax;
+        } else if (fin) {
+            const double u = fabs(qo * ihv[i]), sg = HdD[i];
+            const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
+            acc.umax = u > acc.umax ? u : acc.umax;
+            acc.numax = nu > acc.numax ? nu : acc.numax;
+        }
+        hb[i] = h0; qbv[i] = qo; HdD[i] = Ko; Wbv[i] = wo;
+        if (ALONE) {          // staging arrays 4..7 are not read in this phase
+            const int ko = r - klo;
+            smem[4 * SROWS + ko] = h0; smem[5 * SROWS + ko] = qo;
+            smem[6 * SROWS + ko] = Ko; smem[7 * SROWS + ko] = wo;
         }
     }
-
-    // ---- error bits --------------------------------------------------------
-    {
-        const unsigned int eb = (HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE) ? 0u : __reduce_or_sync(0xffffffffu, errbits);
-        if ((tid & 31) == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
+    if (ALONE) {
+        // (staged; store_tile synchronises)
+    } else if (fused1) {
+        __syncthreads();             // hbar, filter and E_h copies all read
+        // U1 (H-form) at the cells' own positions: arrays 7, 4, 5, 6
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            if (r < klo || r >= khi) continue;
+            A[7 * SROWS + r] = hb[i]; A[4 * SROWS + r] = qbv[i];
+            A[5 * SROWS + r] = HdD[i]; A[6 * SROWS + r] = Wbv[i];
+        }
+    } else {
+        // staged for the bulk store in the dedicated buffer, index r - klo (the
+        // previous tile's bulk store has long read it)
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        __syncthreads();             // hbar, filter and E_h copies all read
+        double *oh, *oq, *oK, *oW;
+        stage_ptrs(true, P.T, oh, oq, oK, oW);
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            if (r < klo || r >= khi) continue;
+            const int ko = r - klo;
+            oh[ko] = hb[i]; oq[ko] = qbv[i]; oK[ko] = HdD[i]; oW[ko] = Wbv[i];
+        }
     }
+    // truncated overlap widths for the overlap check
+    const int wt = min(left_phys ? 1 << 30 : G.wl, right_phys ? 1 << 30 : G.wr);
+    acc.wmin = min(acc.wmin, wt);
+}
 
-    // ---- per-CTA reductions: rho (overlap check), dt maxima, next time level ----
-    {
-        double um = 0.0, nm = 0.0;
-        if (FINAL) { um = warp_max_nonneg(umax_loc); nm = warp_max_nonneg(numax_loc); }
-        float rf = warp_max_nonneg(float(rho_loc));
-        const int lane = tid & 31, wid = tid >> 5;
+// Store the staged rows (arrays 4..7, index 0 .. Tk-1) to out[] at cells
+// [s, s + Tk): bulk (thread 0; read-completion wait deferred) or per element.
+__device__ __forceinline__ void store_tile(const Bufs &B, size_t mo, int s, int Tk, bool dedicated, int T)
+{
+    const int tid = threadIdx.x;
+    const size_t gdst = mo + size_t(s);
+    const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
+    double *oh, *oq, *oK, *oW;
+    stage_ptrs(dedicated, T, oh, oq, oK, oW);
+    if (HSGN_EXP_NOSTORE) {
         __syncthreads();
-        if (lane == 0) { red[0][wid] = um; red[1][wid] = nm; redf[wid] = rf; }
+    } else if (bulk_out) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
         if (tid == 0) {
-            for (int q = 1; q < NT / 32; q++) {
-                um = red[0][q] > um ? red[0][q] : um; nm = red[1][q] > nm ? red[1][q] : nm;
-                rf = redf[q] > rf ? redf[q] : rf;
-            }
-            // overlap check: r^w <= 2^-60 at each truncated end
-            if (rf > 0.0f && dtm != 0.0 && !(HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE)) {
-                const double rho = double(rf) * (1.0 + 1e-6);
-                const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
-                const int wmin = min(left_phys ? 1 << 30 : wl, right_phys ? 1 << 30 : wr);
-                if (wmin < (1 << 30)) {
-                    double x = 1.0, b = rdec;          // rdec^wmin by squaring
-                    for (int k = wmin; k > 0; k >>= 1) { if (k & 1) x *= b; b *= b; }
-                    if (x > 8.673617379884035e-19) atomicOr(P.err, ERR_OVERLAP);   // 2^-60
-                }
-                atomicMax(P.rho_obs, (unsigned long long)__double_as_longlong(rho));
-            }
-            if (FINAL) {
-                const int slot_w = (P.kslot + 1) % 3;
-                atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
-                atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
-                if (j == 0) {   // t^{n+1} of this member, in the other parity slot
-                    const double tm = P.t[P.kpar * members + m];
-                    const double t_end = P.ctrl->t_end;
-                    P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
-                }
-            }
-            // shared memory must outlive the bulk stores' reads (no-op if none)
-            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            const unsigned bytes = unsigned(Tk) * 8u;
+            bulk_s2g(B.out[0] + gdst, oh, bytes);
+            bulk_s2g(B.out[1] + gdst, oq, bytes);
+            bulk_s2g(B.out[2] + gdst, oK, bytes);
+            bulk_s2g(B.out[3] + gdst, oW, bytes);
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    } else {
+        __syncthreads();
+        for (int k = tid; k < Tk; k += NT) {
+            B.out[0][gdst + k] = oh[k]; B.out[1][gdst + k] = oq[k];
+            B.out[2][gdst + k] = oK[k]; B.out[3][gdst + k] = oW[k];
         }
     }
+}
+
+// Member already at t_end (dt = 0): carry the state of kept cells [s, e) and
+// its dt maxima.
+template <bool FINAL, bool BATHY>
+__device__ __forceinline__ void carry_tile(const Params &P, const Bufs &B, size_t mo, int s, int e,
+                                           double lam, TileAcc &acc)
+{
+    const double lam3 = lam * (1.0 / 3.0);
+    for (int i = s + threadIdx.x; i < e; i += NT) {
+        const double h = B.Un[0][mo + i], q = B.Un[1][mo + i], K = B.Un[2][mo + i], W = B.Un[3][mo + i];
+        B.out[0][mo + i] = h; B.out[1][mo + i] = q; B.out[2][mo + i] = K; B.out[3][mo + i] = W;
+        if (FINAL) {
+            const double bb = BATHY ? __ldg(P.b + i) : 0.0;
+            const double ih = rcp(h);
+            const double u = q * ih, sg = (K - 1.5 * h * bb) * ih * ih;
+            acc.umax = fmax(acc.umax, fabs(u));
+            acc.numax = fmax(acc.numax, fabs(u) + fsqrt(P.g * h + lam3 * sg * sg));
+        }
+    }
+}
+
+// Per-tile epilogue: error bits, overlap check (r^w <= 2^-60 at each truncated
+// end), dt maxima of the member (final stage) and its next
+// time level (tile 0).
+template <bool FINAL>
+__device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, double dtm, const TileAcc &acc)
+{
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int members = P.members;
+    const bool exp_off = HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE;
+    const unsigned int eb = exp_off ? 0u : __reduce_or_sync(0xffffffffu, acc.err);
+    if (lane == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
+    double um = 0.0, nm = 0.0;
+    if (FINAL) { um = warp_max_nonneg(acc.umax); nm = warp_max_nonneg(acc.numax); }
+    float rf = warp_max_nonneg(float(acc.rho));
+    __syncthreads();
+    if (lane == 0) { s_red[0][wid] = um; s_red[1][wid] = nm; s_redf[wid] = rf; }
+    __syncthreads();
+    if (tid == 0) {
+        for (int q = 1; q < NT / 32; q++) {
+            um = s_red[0][q] > um ? s_red[0][q] : um; nm = s_red[1][q] > nm ? s_red[1][q] : nm;
+            rf = s_redf[q] > rf ? s_redf[q] : rf;
+        }
+        if (rf > 0.0f && dtm != 0.0 && !exp_off) {
+            const double rho = double(rf) * (1.0 + 1e-6);
+            const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
+            if (acc.wmin < (1 << 30)) {
+                double x = 1.0, b = rdec;          // rdec^wmin by squaring
+                for (int k = acc.wmin; k > 0; k >>= 1) { if (k & 1) x *= b; b *= b; }
+                if (x > 8.673617379884035e-19) atomicOr(P.err, ERR_OVERLAP);   // 2^-60
+            }
+            atomicMax(P.rho_obs, (unsigned long long)__double_as_longlong(rho));
+        }
+        if (FINAL) {
+            const int slot_w = (P.kslot + 1) % 3;
+            atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
+            atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
+            if (j == 0) {   // t^{n+1} of this member, in the other parity slot
+                const double tm = P.t[P.kpar * members + m];
+                const double t_end = P.ctrl->t_end;
+                P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void init_mbar(unsigned mb)
+{
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Standalone stage kernel: one IMEX stage over every (tile, member) CTA.
+// STAGE2: inputs U^n and U1 (E, R formed on load); FINAL: this stage produces
+// U^{n+1} (filter, relaxation, dt maxima, time level).  Used for one-stage
+// tableaux and slab (BC_HALO) domains; the two-stage step otherwise runs fused.
+// ---------------------------------------------------------------------------
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
+__global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
+{
+    const int tid = threadIdx.x;
+    const int j = blockIdx.x;        // tile
+    const int m = blockIdx.y;        // member
+    const size_t mo = size_t(m) * P.n;
+    const int s = j * P.T;
+    const int e = min(P.n, s + P.T);
+    Geom G = stage_geom(P, s, e, P.w);
+    const LoadPlan Lp = load_plan(P, mo, G);
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+    if (Lp.bulk) init_mbar(mb);
+    issue_load<STAGE2>(P, B, mo, G, Lp, mb, tid);
+
+    // ---- run control: dt of this member was set by dt_commit_kernel ---------
+    const unsigned int err0 = *((volatile unsigned int *)P.err);
+    const double dtm = P.dt[m];
+    const double lam = P.lam[m];
+    unsigned parity = 0u;
+    wait_load(Lp, mb, parity);
+    __syncthreads();
+    if (err0) return;
+
+    TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
+    if (dtm == 0.0) {
+        carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
+    } else {
+        const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
+        stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE>(P, B, G, m, s, S, dtm, acc, -1, false);
+        store_tile(B, mo, s, e - s, false, P.T);
+    }
+    tile_epilogue<FINAL>(P, j, m, dtm, acc);
+    // shared memory must outlive the bulk stores' reads (no-op if none)
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Fused two-stage IMEX step (P:500-517 twice, E/R of P:399-401): persistent
+// CTAs walk the (tile, member) items; per item, stage 1 runs on a tile widened
+// by w + 3 cells on each side, its U1 stays in shared memory, stage 2 runs on
+// the inner tile and produces U^{n+1}.  U^n of the next item is prefetched by
+// TMA into arrays 0..3 while stage 2 of the current item finishes.
+// ---------------------------------------------------------------------------
+template <bool BATHY, bool RELAX>
+__global__ void __launch_bounds__(NT, HSGN_MINB) step_kernel(const Params P, const Bufs B, int items)
+{
+    double *const smem = dyn_smem();
+    const int tid = threadIdx.x;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+    int item = blockIdx.x;
+    if (item >= items) return;
+    init_mbar(mb);
+    unsigned parity = 0u;
+    prefetch_item(P, B, item);
+
+    for (;;) {
+        int j, m, s, e;
+        item_tile(P, item, j, m, s, e);
+        Geom G1, G2;
+        fused_geom(P, s, e, P.w, G1, G2);
+        const size_t mo = size_t(m) * P.n;
+        const LoadPlan Lp = load_plan(P, mo, G1);        // as issued
+        G2.abase = G1.abase + (G2.start - G1.start);     // cells keep their positions
+        const int next = item + int(gridDim.x);
+        // ---- run control: dt, lambda of this item were fetched with its loads
+        const unsigned int err0 = *((volatile unsigned int *)P.err);
+        wait_load(Lp, mb, parity);
+        __syncthreads();
+        const double dtm = s_rc[0];
+        const double lam = s_rc[1];
+        if (err0) {
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            return;
+        }
+
+        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
+        if (dtm == 0.0) {
+            carry_tile<true, BATHY>(P, B, mo, s, e, lam, acc);
+            __syncthreads();
+            if (next < items) prefetch_item(P, B, next);
+        } else {
+            // ---- stage 1: U^n -> U1 on the widened tile; stage 2: (U^n, U1) ->
+            // U^{n+1} on the kept tile.  One (not unrolled) loop: both stages
+            // run the same instructions.
+#pragma unroll 1
+            for (int st = 0; st < 2; st++) {
+                const bool two = st == 1;
+                const Geom G = two ? G2 : G1;
+                const StageC S = stage_consts(P, two ? P.aI2 : P.aI1, dtm, lam);
+                stage_body<false, false, BATHY, RELAX, MODE_FUSED>(P, B, G, m, s, S, dtm, acc,
+                                                                   (two && next < items) ? next : -1, two);
+                if (two) break;
+                __syncthreads();
+                // U1 ghost rows at physical ends (A10): mirror (wall, q odd) or copy
+                if (G2.left_phys || G2.right_phys) {
+                    double *const A2 = smem + G2.abase;
+                    const int L2 = G2.L;
+                    if (tid < 3 && G2.left_phys) {
+                        const int r = -1 - tid;
+                        const bool wall = P.bcl == BC_WALL;
+                        const int src = wall ? -1 - r : 0;
+                        A2[7 * SROWS + r] = A2[7 * SROWS + src];
+                        A2[4 * SROWS + r] = (wall ? -1.0 : 1.0) * A2[4 * SROWS + src];
+                        A2[5 * SROWS + r] = A2[5 * SROWS + src];
+                        A2[6 * SROWS + r] = A2[6 * SROWS + src];
+                    }
+                    if (tid >= 32 && tid < 35 && G2.right_phys) {
+                        const int r = L2 + (tid - 32);
+                        const bool wall = P.bcr == BC_WALL;
+                        const int src = wall ? 2 * L2 - 1 - r : L2 - 1;
+                        A2[7 * SROWS + r] = A2[7 * SROWS + src];
+                        A2[4 * SROWS + r] = (wall ? -1.0 : 1.0) * A2[4 * SROWS + src];
+                        A2[5 * SROWS + r] = A2[5 * SROWS + src];
+                        A2[6 * SROWS + r] = A2[6 * SROWS + src];
+                    }
+                    __syncthreads();
+                }
+            }
+            store_tile(B, mo, s, e - s, true, P.T);
+        }
+        tile_epilogue<true>(P, j, m, dtm, acc);
+        if (next >= items) break;
+        item = next;
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------

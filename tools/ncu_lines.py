@@ -51,11 +51,13 @@ def main(rep, so):
         base = int(rows[1][ia], 16)
         # pick the mangled function whose size matches
         n = len(rows) - 1
-        cand = [f for f, m in funcs.items() if abs(len(m) - n) <= 2 and "stage_kernel" in f]
+        kb = re.search(r"hsgn::(\w+)<", name)
+        kb = kb.group(1) if kb else "stage_kernel"
+        cand = [f for f, m in funcs.items() if abs(len(m) - n) <= 2 and kb in f]
         key = None
-        tag = re.findall(r"<\(bool\)(\d), \(bool\)(\d), \(bool\)(\d), \(bool\)(\d)>", name)
+        tag = re.findall(r"\(bool\)(\d)", name.split(">(")[0])
         if tag:
-            t = "ILb%sELb%sELb%sELb%sEE" % tag[0]
+            t = kb + "I" + "".join("Lb%sE" % x for x in tag) + "E"
             for f in funcs:
                 if t in f:
                     key = f

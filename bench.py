@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--cells", type=int, default=4096)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--persistent", type=int, default=-1,
+                   help="1: persistent per-stage kernels, 0: one CTA per tile, -1: library default")
     p.add_argument("--fused", type=int, default=-1,
                    help="1: fused step kernel, 0: per-stage kernels, -1: library default")
     p.add_argument("--config", default="cfg3", choices=["cfg3", "cfg5"],
@@ -241,6 +243,8 @@ def main():
         host_state = None
     if a.fused >= 0:
         s.set_fused(bool(a.fused))
+    if a.persistent >= 0:
+        s.set_persistent(bool(a.persistent))
     state_bytes = 4 * 8 * Ntot
 
     def barrier():

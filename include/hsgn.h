@@ -213,6 +213,13 @@ int64_t hsgn_launch_count(const hsgn_ctx *ctx);
 hsgn_status hsgn_set_fused(hsgn_ctx *ctx, int32_t on);
 /* 1 if steps currently run as the fused kernel, 0 otherwise (-1: null). */
 int32_t hsgn_get_fused(const hsgn_ctx *ctx);
+/* Per-stage kernels as persistent CTAs: each CTA walks
+ * (tile, member) items and prefetches the next item's inputs by TMA while it
+ * finishes the current one; on = 0: one CTA per (tile, member).  Same
+ * arithmetic either way.  Default off (measured slower on B200, DESIGN.md
+ * section 6).  Drops captured graphs.  Errors:
+ * HSGN_E_INVALID (null context). */
+hsgn_status hsgn_set_persistent(hsgn_ctx *ctx, int32_t on);
 /* Tile geometry chosen by hsgn_create: kept cells per tile, overlap, tiles per
  * member, threads per CTA, max rows per CTA. */
 hsgn_status hsgn_get_geometry(const hsgn_ctx *ctx, int32_t *tile_cells, int32_t *overlap,

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -56,6 +57,7 @@ struct hsgn_ctx {
     double *b = nullptr, *lamd = nullptr, *t = nullptr, *dt = nullptr, *dt_used = nullptr,
            *partials = nullptr;
     unsigned long long *maxes = nullptr, *rho_obs = nullptr;
+    unsigned int *work = nullptr;
     unsigned int *err = nullptr, *done = nullptr;
     long long *steps = nullptr;
     Ctrl *ctrl = nullptr;
@@ -73,6 +75,10 @@ struct hsgn_ctx {
     // two-stage tableaux on non-slab domains when the widened tile fits
     bool fused_on = false, fused = false;
     int fused_grid = 0;
+    int pf_dist = 0;              // L2 prefetch distance of the stage kernels (CTAs)
+    // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
+    bool persist = false;
+    int persist_grid = 0;
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
     std::string last_error;
@@ -121,7 +127,10 @@ Params make_params(hsgn_ctx *c, long long k)
     P.b = c->bathy ? c->b : nullptr;
     P.lam = c->lamd; P.t = c->t; P.dt = c->dt; P.maxes = c->maxes; P.err = c->err;
     P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.ctrl = c->ctrl;
+    P.work = c->work;
     P.H = c->w + 3;
+    P.pf_dist = c->pf_dist;
+    P.inv_tiles = 1.0 / double(c->tiles);
     for (int k = 0; k < 9; k++) {
         P.halo_l[k] = c->halo_l ? c->halo_l + k * H_MAX : nullptr;
         P.halo_r[k] = c->halo_r ? c->halo_r + k * H_MAX : nullptr;
@@ -132,11 +141,17 @@ Params make_params(hsgn_ctx *c, long long k)
 template <bool S2, bool FIN, bool BATHY>
 hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
 {
-    dim3 grid(c->tiles, c->members);
-    if (FIN && (c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
-        stage_kernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
-    else
-        stage_kernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    const bool relax = FIN && (c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0);
+    if (c->persist) {
+        const int items = c->tiles * c->members;
+        const int grid = std::min(items, c->persist_grid);
+        if (relax) stage_pkernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
+        else stage_pkernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
+    } else {
+        dim3 grid(c->tiles, c->members);
+        if (relax) stage_kernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+        else stage_kernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    }
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return HSGN_OK;
@@ -266,6 +281,17 @@ void choose_geometry(hsgn_ctx *c)
     c->T = T;
     c->w = w;
     c->tiles = (c->n + T - 1) / T;
+    {
+        int sms = 148, occ = 4;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<true, true, false>, NT, SMEM_BYTES);
+        const char *e = std::getenv("HSGN_PF_WAVES");     // tuning: prefetch distance in waves
+        const double waves = e ? std::atof(e) : 0.0;
+        c->pf_dist = int(waves * sms * std::max(occ, 1));
+        int occp = 4;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, stage_pkernel<true, true, false>, NT, SMEM_BYTES);
+        c->persist_grid = sms * std::max(occp, 1);
+    }
     if (c->fused) {
         int sms = 148, occ = 1;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -562,6 +588,16 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(step_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cudaFuncSetAttribute(step_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
@@ -624,6 +660,7 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     c->done = (unsigned int *)(q + 4);
     c->steps = (long long *)(q + 8);
     c->rho_obs = (unsigned long long *)(q + 16);
+    c->work = (unsigned int *)(q + 32);
     q += 256;
     c->ctrl = (Ctrl *)q;
     q += 256;
@@ -747,7 +784,7 @@ hsgn_status hsgn_set_state(hsgn_ctx *c, const double *h, const double *q, const 
     c->dev_steps = 0;
     CUDA_TRY(c, cudaMemsetAsync(c->dt, 0, c->members * sizeof(double), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->maxes, 0, 6 * size_t(c->members) * 8, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->err, 0, 32, c->stream));   // err, done, steps, rho_obs
+    CUDA_TRY(c, cudaMemsetAsync(c->err, 0, 48, c->stream));   // err, done, steps, rho_obs, work
     dim3 grid(c->tiles, c->members);
     reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[0][0], c->buf[0][1], c->buf[0][2],
                                               c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
@@ -940,6 +977,29 @@ hsgn_status hsgn_set_fused(hsgn_ctx *c, int32_t on)
 }
 
 int32_t hsgn_get_fused(const hsgn_ctx *c) { return c ? (c->fused ? 1 : 0) : -1; }
+
+hsgn_status hsgn_set_persistent(hsgn_ctx *c, int32_t on)
+{
+    if (!c) return HSGN_E_INVALID;
+    c->persist = on != 0;
+    drop_graphs(c);
+    return HSGN_OK;
+}
+
+#if HSGN_EXP_TIMING
+// timing experiments only (not part of the product ABI): per-stage sums of
+// CTA clocks [load wait, compute + store issue, epilogue + store drain, CTAs]
+int hsgn_exp_counters(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_exp, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_exp, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 hsgn_status hsgn_get_geometry(const hsgn_ctx *c, int32_t *T, int32_t *w, int32_t *tiles,
                               int32_t *threads, int32_t *max_rows)

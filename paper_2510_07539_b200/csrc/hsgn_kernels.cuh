@@ -42,6 +42,12 @@
 #ifndef HSGN_EXP_NOSTORE
 #define HSGN_EXP_NOSTORE 0
 #endif
+#ifndef HSGN_EXP_NOPREFETCH            // persistent kernel loads each item at its start
+#define HSGN_EXP_NOPREFETCH 0
+#endif
+#ifndef HSGN_EXP_TIMING                 // per-CTA phase clocks (hsgn_exp_counters)
+#define HSGN_EXP_TIMING 0
+#endif
 
 namespace hsgn {
 
@@ -87,6 +93,8 @@ struct Params {
     long long *steps;
     unsigned int *done;
     unsigned long long *rho_obs;     // max rho over tiles (double bits)
+    unsigned int *work;              // [2 parities][2 stages] item counters of the
+                                     // persistent kernels (zeroed by dt_commit_kernel)
     const Ctrl *ctrl;
     int kslot, kpar;                 // host step index k: k mod 3, k mod 2
     // slab decomposition (BC_HALO sides): ghost cells received from the
@@ -94,6 +102,10 @@ struct Params {
     const double *halo_l[9];
     const double *halo_r[9];
     int H;
+    // L2 prefetch distance of the standalone stage kernel, in CTAs (~ CTAs
+    // resident at once); 0: off
+    int pf_dist;
+    double inv_tiles;                // 1 / tiles
     // A10 relaxation zones (cfg4), applied to U^{n+1} at t^{n+1} in the final
     // stage; rates <= 0 switch them off.  x_i = x_min + (i + 1/2) dx.
     double x_min, x_max, level, gen_x1, gen_rate, amp, omega, kw, cp, sp_x0, sp_rate;
@@ -125,7 +137,9 @@ __shared__ __align__(8) unsigned long long s_mbar;
 __shared__ double s_red[2][NT / 32];
 __shared__ float s_redf[NT / 32];
 __shared__ double s_xch[NT / 32][3];
-__shared__ double s_rc[2];            // fused step: dt, lambda of the next item
+__shared__ double s_rc[2];            // persistent kernels: dt, lambda of the next item
+__shared__ unsigned int s_err;        // persistent kernels: error word seen at its prefetch
+__shared__ int s_item[2];             // persistent kernels: current, next item
 
 __device__ __forceinline__ double *dyn_smem() { return hsgn_smem; }
 
@@ -157,6 +171,12 @@ __device__ __forceinline__ void bulk_s2g(double *dst, const double *src_smem, un
     const unsigned a = (unsigned)__cvta_generic_to_shared(src_smem);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
                  ::"l"(dst), "r"(a), "r"(bytes) : "memory");
+}
+
+// Bulk prefetch of a global range into L2 (16-B aligned, size a multiple of 16).
+__device__ __forceinline__ void prefetch_l2(const double *src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity)
@@ -493,22 +513,35 @@ __device__ __forceinline__ LoadPlan load_plan(const Params &P, size_t mo, Geom &
 // standalone stage 2, of U1 (arrays 7, 4, 5, 6 = h, q, K, W).  Bulk: thread 0,
 // completion on the mbarrier; otherwise per-row cp.async through the BC index
 // map or a slab halo (all threads).
-template <bool WITH_U1>
+// PART: LD_ALL (U^n, and U1 if WITH_U1; arrive + expect_tx), LD_UN (U^n only,
+// expect_tx without arrive: a later LD_U1 completes the phase), LD_U1 (U1 only,
+// arrive + expect_tx).
+enum { LD_ALL = 0, LD_UN = 1, LD_U1 = 2 };
+
+template <bool WITH_U1, int PART = LD_ALL>
 __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_t mo, const Geom &G,
                                            const LoadPlan &Lp, unsigned mb, int tid)
 {
     double *const smem = dyn_smem();
     if (HSGN_EXP_NOLOAD) return;
+    constexpr bool DO_UN = PART != LD_U1;
+    constexpr bool DO_U1 = WITH_U1 && PART != LD_UN;
     if (Lp.bulk) {
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             const unsigned bytes = unsigned(Lp.cnt) * 8u;
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
-                         "r"(bytes * (WITH_U1 ? 8u : 4u)) : "memory");
+            const unsigned tx = bytes * ((DO_UN ? 4u : 0u) + (DO_U1 ? 4u : 0u));
+            if (PART == LD_UN)
+                asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;\n" ::"r"(mb), "r"(tx) : "memory");
+            else
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(tx)
+                             : "memory");
             const size_t gsrc = mo + size_t(Lp.a0);
+            if (DO_UN) {
 #pragma unroll
-            for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
-            if (WITH_U1) {
+                for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
+            }
+            if (DO_U1) {
                 bulk_g2s(smem + 7 * SROWS, B.U1[0] + gsrc, bytes, mb);
                 bulk_g2s(smem + 4 * SROWS, B.U1[1] + gsrc, bytes, mb);
                 bulk_g2s(smem + 5 * SROWS, B.U1[2] + gsrc, bytes, mb);
@@ -524,20 +557,22 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
             if (c < 0 && P.bcl == BC_HALO) {
                 const int o = c + P.H;
                 p0 = P.halo_l[0] + o; p1 = P.halo_l[1] + o; p2 = P.halo_l[2] + o; p3 = P.halo_l[3] + o;
-                if (WITH_U1) { u0 = P.halo_l[4] + o; u1 = P.halo_l[5] + o; u2 = P.halo_l[6] + o; u3 = P.halo_l[7] + o; }
+                if (DO_U1) { u0 = P.halo_l[4] + o; u1 = P.halo_l[5] + o; u2 = P.halo_l[6] + o; u3 = P.halo_l[7] + o; }
             } else if (c >= n && P.bcr == BC_HALO) {
                 const int o = c - n;
                 p0 = P.halo_r[0] + o; p1 = P.halo_r[1] + o; p2 = P.halo_r[2] + o; p3 = P.halo_r[3] + o;
-                if (WITH_U1) { u0 = P.halo_r[4] + o; u1 = P.halo_r[5] + o; u2 = P.halo_r[6] + o; u3 = P.halo_r[7] + o; }
+                if (DO_U1) { u0 = P.halo_r[4] + o; u1 = P.halo_r[5] + o; u2 = P.halo_r[6] + o; u3 = P.halo_r[7] + o; }
             } else {
                 double par;
                 const size_t gi = mo + size_t(map_cell(c, n, P.bcl, P.bcr, par));
                 p0 = B.Un[0] + gi; p1 = B.Un[1] + gi; p2 = B.Un[2] + gi; p3 = B.Un[3] + gi;
-                if (WITH_U1) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
+                if (DO_U1) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
             }
-            cp_async8(A + r, p0); cp_async8(A + SROWS + r, p1);
-            cp_async8(A + 2 * SROWS + r, p2); cp_async8(A + 3 * SROWS + r, p3);
-            if (WITH_U1) {
+            if (DO_UN) {
+                cp_async8(A + r, p0); cp_async8(A + SROWS + r, p1);
+                cp_async8(A + 2 * SROWS + r, p2); cp_async8(A + 3 * SROWS + r, p3);
+            }
+            if (DO_U1) {
                 cp_async8(A + 7 * SROWS + r, u0); cp_async8(A + 4 * SROWS + r, u1);
                 cp_async8(A + 5 * SROWS + r, u2); cp_async8(A + 6 * SROWS + r, u3);
             }
@@ -588,11 +623,14 @@ struct TileAcc {
     int wmin;                     // narrowest truncated overlap (1 << 30: none)
 };
 
-enum { MODE_ALONE = 0, MODE_FUSED = 1 };
+enum { MODE_ALONE = 0, MODE_FUSED = 1, MODE_PERSIST = 2 };
 
 __device__ __forceinline__ void item_tile(const Params &P, int item, int &j, int &m, int &s, int &e)
 {
-    m = item / P.tiles;
+    // item / tiles through the reciprocal (exact after the +-1 correction)
+    m = __double2int_rz(double(item) * P.inv_tiles);
+    if (m * P.tiles > item) m--;
+    else if ((m + 1) * P.tiles <= item) m++;
     j = item - m * P.tiles;
     s = j * P.T;
     e = min(P.n, s + P.T);
@@ -625,6 +663,36 @@ __device__ __forceinline__ void prefetch_item(const Params &P, const Bufs &B, in
     if (threadIdx.x == 0) { s_rc[0] = P.dt[m]; s_rc[1] = P.lam[m]; }
 }
 
+
+// Persistent stage kernel: item -> kept cells and its stage tile.
+__device__ __forceinline__ void stage_item(const Params &P, int item, int &j, int &m, int &s, int &e,
+                                           Geom &G, size_t &mo, LoadPlan &Lp)
+{
+    item_tile(P, item, j, m, s, e);
+    G = stage_geom(P, s, e, P.w);
+    mo = size_t(m) * P.n;
+    Lp = load_plan(P, mo, G);
+}
+
+// Issue loads of a persistent-stage item (PART of its inputs) and, with the
+// U^n part, fetch its run control (dt, lambda) into s_rc.
+template <bool STAGE2, int PART>
+__device__ __forceinline__ void prefetch_stage_item(const Params &P, const Bufs &B, int item)
+{
+    int j, m, s, e;
+    Geom G;
+    size_t mo;
+    LoadPlan Lp;
+    stage_item(P, item, j, m, s, e, G, mo, Lp);
+    issue_load<STAGE2, PART>(P, B, mo, G, Lp, (unsigned)__cvta_generic_to_shared(&s_mbar), threadIdx.x);
+    if (PART != LD_U1 && threadIdx.x == 0) {       // async: no wait on the critical path
+        cp_async8(&s_rc[0], P.dt + m);
+        cp_async8(&s_rc[1], P.lam + m);
+        const unsigned a = (unsigned)__cvta_generic_to_shared(&s_err);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(a), "l"(P.err) : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+}
 
 // ---------------------------------------------------------------------------
 // One IMEX stage S(E, R, tau) on the tile G, data already in
@@ -786,6 +854,10 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         for (int i = 0; i < MCH; i++) { wd[i] = 0.0; hRv[i] = 0.0; }
     }
     __syncthreads();
+    // persistent kernel without bathymetry: arrays 0..3 (E) are not read after
+    // phase 1, so the next item's U^n loads can start now
+    if (MODE == MODE_PERSIST && !HSGN_EXP_NOPREFETCH && !BATHY && next_item >= 0)
+        prefetch_stage_item<STAGE2, STAGE2 ? LD_UN : LD_ALL>(P, B, next_item);
     // derived-field ghosts at physical boundaries (A10).  The implicit
     // coupling across both tile ends is cut (truncated overlap or Neumann end:
     // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
@@ -906,6 +978,8 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         }
         __syncthreads();
         if (fused2 && next_item >= 0) prefetch_item(P, B, next_item);   // arrays 0..3 free
+        if (MODE == MODE_PERSIST && !HSGN_EXP_NOPREFETCH && BATHY && next_item >= 0)   // (after the E_h copies)
+            prefetch_stage_item<STAGE2, STAGE2 ? LD_UN : LD_ALL>(P, B, next_item);
         int lim = NT;
         {
             float e0 = 0.0f;
@@ -1057,6 +1131,18 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     }
     if (ALONE) {
         // (staged; store_tile synchronises)
+    } else if (MODE == MODE_PERSIST) {
+        // staged at arrays 4..7 once hbar (6) and the filter (4, 5) are read;
+        // the caller bulk-stores them (direct per-thread stores measured slower)
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            if (r < klo || r >= khi) continue;
+            const int ko = r - klo;
+            smem[4 * SROWS + ko] = hb[i]; smem[5 * SROWS + ko] = qbv[i];
+            smem[6 * SROWS + ko] = HdD[i]; smem[7 * SROWS + ko] = Wbv[i];
+        }
     } else if (fused1) {
         __syncthreads();             // hbar, filter and E_h copies all read
         // U1 (H-form) at the cells' own positions: arrays 7, 4, 5, 6
@@ -1199,9 +1285,17 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 // U^{n+1} (filter, relaxation, dt maxima, time level).  Used for one-stage
 // tableaux and slab (BC_HALO) domains; the two-stage step otherwise runs fused.
 // ---------------------------------------------------------------------------
+#if HSGN_EXP_TIMING
+__device__ unsigned long long g_exp[8];
+#define EXP_T(v) long long v = clock64()
+#else
+#define EXP_T(v)
+#endif
+
 template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
 __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
 {
+    EXP_T(t0);
     const int tid = threadIdx.x;
     const int j = blockIdx.x;        // tile
     const int m = blockIdx.y;        // member
@@ -1213,6 +1307,28 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
     if (Lp.bulk) init_mbar(mb);
     issue_load<STAGE2>(P, B, mo, G, Lp, mb, tid);
+    // L2 prefetch of the tile of the CTA about one residency wave later, so its
+    // TMA loads hit L2 instead of HBM (no shared memory involved)
+    if (tid == 0 && P.pf_dist > 0 && !HSGN_EXP_NOLOAD) {
+        const long long lin = (long long)m * gridDim.x + j + P.pf_dist;
+        if (lin < (long long)gridDim.x * gridDim.y) {
+            const int jf = int(lin % gridDim.x), mf = int(lin / gridDim.x);
+            const int sf = jf * P.T;
+            Geom Gf = stage_geom(P, sf, min(P.n, sf + P.T), P.w);
+            const size_t mof = size_t(mf) * P.n;
+            const LoadPlan Lf = load_plan(P, mof, Gf);
+            if (Lf.bulk) {
+                const size_t off = mof + size_t(Lf.a0);
+                const unsigned bytes = unsigned(Lf.cnt) * 8u;
+#pragma unroll
+                for (int f = 0; f < 4; f++) prefetch_l2(B.Un[f] + off, bytes);
+                if (STAGE2) {
+#pragma unroll
+                    for (int f = 0; f < 4; f++) prefetch_l2(B.U1[f] + off, bytes);
+                }
+            }
+        }
+    }
 
     // ---- run control: dt of this member was set by dt_commit_kernel ---------
     const unsigned int err0 = *((volatile unsigned int *)P.err);
@@ -1221,6 +1337,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     unsigned parity = 0u;
     wait_load(Lp, mb, parity);
     __syncthreads();
+    EXP_T(t1);
     if (err0) return;
 
     TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
@@ -1231,8 +1348,87 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE>(P, B, G, m, s, S, dtm, acc, -1, false);
         store_tile(B, mo, s, e - s, false, P.T);
     }
+    EXP_T(t2);
     tile_epilogue<FINAL>(P, j, m, dtm, acc);
     // shared memory must outlive the bulk stores' reads (no-op if none)
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+#if HSGN_EXP_TIMING
+    if (tid == 0) {
+        const long long t3 = clock64();
+        unsigned long long *g = g_exp + (STAGE2 ? 4 : 0);
+        atomicAdd(g + 0, (unsigned long long)(t1 - t0));
+        atomicAdd(g + 1, (unsigned long long)(t2 - t1));
+        atomicAdd(g + 2, (unsigned long long)(t3 - t2));
+        atomicAdd(g + 3, 1ull);
+    }
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Persistent stage kernel: the same stage as stage_kernel, but each CTA walks
+// (tile, member) items and prefetches the next item's inputs while it finishes
+// the current one: U^n into arrays 0..3 as soon as phase 2 has its register
+// windows (stage 1: all its inputs); stage 2's U1 into arrays 4..7 once the
+// current item's staged output has been read by its bulk store.
+// ---------------------------------------------------------------------------
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
+__global__ void __launch_bounds__(NT, HSGN_MINB) stage_pkernel(const Params P, const Bufs B, int items)
+{
+    const int tid = threadIdx.x;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+    // items are handed out by an atomic counter (dynamic balance across SMs);
+    // thread 0 asks for item k+2 while item k runs, so no CTA waits on it
+    unsigned int *ctr = P.work + 2 * P.kpar + (STAGE2 ? 1 : 0);
+    int grab = 0;
+    if (tid == 0) {
+        s_item[0] = int(atomicAdd(ctr, 1u));
+        s_item[1] = int(atomicAdd(ctr, 1u));
+    }
+    init_mbar(mb);                       // (synchronises s_item)
+    int item = s_item[0];
+    if (item >= items) return;
+    unsigned parity = 0u;
+    if (!HSGN_EXP_NOPREFETCH) prefetch_stage_item<STAGE2, LD_ALL>(P, B, item);
+    for (;;) {
+        if (HSGN_EXP_NOPREFETCH) { __syncthreads(); prefetch_stage_item<STAGE2, LD_ALL>(P, B, item); }
+        int j, m, s, e;
+        Geom G;
+        size_t mo;
+        LoadPlan Lp;
+        stage_item(P, item, j, m, s, e, G, mo, Lp);
+        wait_load(Lp, mb, parity);
+        cp_async_wait_all();              // run control (and per-row loads)
+        __syncthreads();
+        const int next = s_item[1];
+        const double dtm = s_rc[0];
+        const double lam = s_rc[1];
+        if (s_err) break;                 // an error was latched (seen at the prefetch)
+        if (tid == 0) grab = int(atomicAdd(ctr, 1u));      // used at the item's end
+        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
+        if (dtm == 0.0) {
+            carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
+            __syncthreads();
+            if (!HSGN_EXP_NOPREFETCH && next < items) prefetch_stage_item<STAGE2, LD_ALL>(P, B, next);
+        } else {
+            const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
+            stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_PERSIST>(P, B, G, m, s, S, dtm, acc,
+                                                                  next < items ? next : -1, false);
+            store_tile(B, mo, s, e - s, false, P.T);
+            if (next < items) {
+                // arrays 4..7 must be read by the bulk store before the next item
+                // writes them (stage 1: phase 1) or loads its U1 into them (stage 2)
+                if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                if (STAGE2 && !HSGN_EXP_NOPREFETCH) {
+                    __syncthreads();
+                    prefetch_stage_item<STAGE2, LD_U1>(P, B, next);
+                }
+            }
+        }
+        tile_epilogue<FINAL>(P, j, m, dtm, acc);   // (its barriers order the s_item update)
+        if (next >= items) break;
+        if (tid == 0) { s_item[1] = grab; }
+        item = next;
+    }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
@@ -1340,6 +1536,7 @@ __global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int comm
 {
     const unsigned int err = *((volatile unsigned int *)P.err);
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid == 0) { P.work[2 * P.kpar] = 0u; P.work[2 * P.kpar + 1] = 0u; }   // step k's item counters
     if (tid == 0 && commit_prev && err == 0u) *P.steps += 1;
     if (err || !compute_dt) return;
     const int m = tid;

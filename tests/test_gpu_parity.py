@@ -58,10 +58,11 @@ def gpu_solver(w, **kw):
     hs = _hsgn()
     order = kw.pop("order", 2)
     tab = kw.pop("tableau", None)
-    fused = kw.pop("fused", None)          # None: library default (fused step)
+    kmode = kw.pop("kmode", None)          # None: library default (persistent per-stage)
     s = hs.Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, order=order, **kw)
-    if fused is not None:
-        s.set_fused(fused)
+    if kmode is not None:
+        s.set_fused(kmode == "fused")
+        s.set_persistent(kmode == "persistent")
     s.set_params(w.g, w.lam, w.cfl, w.mcfl)
     if tab is not None:
         s.set_tableau(tab)
@@ -94,27 +95,28 @@ def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, **okw):
 
 
 # --------------------------------------------------------------------------
-FUSED = [pytest.param(True, id="fused"), pytest.param(False, id="per-stage")]
+# kernel organisations of the same arithmetic
+KMODES = ["persistent", "per-tile", "fused"]
 
 
-@pytest.mark.parametrize("fused", FUSED)
+@pytest.mark.parametrize("kmode", KMODES)
 @pytest.mark.parametrize("bc", ["periodic", "wall", "transmissive"])
 @pytest.mark.parametrize("order", [2, 1])
-def test_one_step_ragged_tiles(bc, order, fused):
+def test_one_step_ragged_tiles(bc, order, kmode):
     w = W.random_smooth(3000, 3, seed=21, amp=0.08, bc=(bc, bc))
-    s = gpu_solver(w, tile_cells=700, overlap=64, order=order, fused=fused)
-    assert s.fused == fused
+    s = gpu_solver(w, tile_cells=700, overlap=64, order=order, kmode=kmode)
+    assert s.fused == (kmode == "fused")
     g = s.geometry
     assert g.tiles_per_member == -(-3000 // g.tile_cells) >= 5 and 3000 % g.tile_cells != 0  # ragged
     s.step()
     compare(w, s, range(3), steps=1, order=order)
 
 
-@pytest.mark.parametrize("fused", FUSED)
+@pytest.mark.parametrize("kmode", KMODES)
 @pytest.mark.parametrize("bc", ["periodic", "wall", "transmissive"])
-def test_bathymetry_steps(bc, fused):
+def test_bathymetry_steps(bc, kmode):
     w = W.random_smooth(2048, 2, seed=5, amp=0.05, bc=(bc, bc), bathy=0.08)
-    s = gpu_solver(w, tile_cells=512, fused=fused)
+    s = gpu_solver(w, tile_cells=512, kmode=kmode)
     s.step()
     compare(w, s, range(2), steps=1)
     s.run_steps(19)
@@ -130,21 +132,21 @@ def test_euler_tableau_first_order_step():
     compare(w, s, range(2), steps=5, order=1, tableau=O.euler_tableau(), tol=1e-10)
 
 
-@pytest.mark.parametrize("fused", FUSED)
-def test_filter_walls_and_periodic(fused):
+@pytest.mark.parametrize("kmode", KMODES)
+def test_filter_walls_and_periodic(kmode):
     for bc in ("periodic", "wall", "transmissive"):
         w = W.random_smooth(2000, 2, seed=13, amp=0.05, bc=(bc, bc))
         w.filter_sigma = 0.25
-        s = gpu_solver(w, tile_cells=500, fused=fused)
+        s = gpu_solver(w, tile_cells=500, kmode=kmode)
         s.run_steps(30)
         compare(w, s, range(2), steps=30, tol=1e-10)
 
 
-@pytest.mark.parametrize("fused", FUSED)
-def test_single_tile_tiny_domains_wrap(fused):
+@pytest.mark.parametrize("kmode", KMODES)
+def test_single_tile_tiny_domains_wrap(kmode):
     for n, bc in ((4, "periodic"), (7, "periodic"), (64, "periodic"), (5, "wall"), (9, "transmissive")):
         w = W.random_smooth(n, 2, seed=n, amp=0.02, bc=(bc, bc))
-        s = gpu_solver(w, fused=fused)
+        s = gpu_solver(w, kmode=kmode)
         s.run_steps(3)
         compare(w, s, range(2), steps=3, tol=1e-10)
 
@@ -171,16 +173,16 @@ def test_mass_conservation_gpu():
         assert abs(d["mass"] - m0) <= 1e-13 * m0
 
 
-@pytest.mark.parametrize("fused", FUSED)
-def test_launch_count_per_step(fused):
+@pytest.mark.parametrize("kmode", KMODES)
+def test_launch_count_per_step(kmode):
     """per step: the fused step kernel (or stage 1 + stage 2) and dt/commit;
     plus one dt kernel per call."""
     w = W.random_smooth(512, 1, seed=1)
-    s = gpu_solver(w, fused=fused)
+    s = gpu_solver(w, kmode=kmode)
     l0 = s.launches
     s.run_steps(40)          # graph replays + eager remainder
     s.sync()
-    assert s.launches - l0 == 1 + (2 if fused else 3) * 40
+    assert s.launches - l0 == 1 + (2 if kmode == "fused" else 3) * 40
 
 
 # --------------------------------------------------------------------------
@@ -258,10 +260,10 @@ def test_cfg1_full_run_to_t20():
     assert nst >= 500
 
 
-@pytest.mark.parametrize("fused", FUSED)
-def test_cfg3_subset_200_steps(fused):
+@pytest.mark.parametrize("kmode", KMODES)
+def test_cfg3_subset_200_steps(kmode):
     w = W.cfg3(members=6)
-    s = gpu_solver(w, fused=fused)
+    s = gpu_solver(w, kmode=kmode)
     s.run_steps(1)
     compare(w, s, range(6), steps=1)
     s.run_steps(199)
@@ -367,12 +369,12 @@ def test_slab_context_refuses_without_transport():
         solvers[0].run_steps(1)
 
 
-@pytest.mark.parametrize("fused", FUSED)
-def test_cfg4_bar_wavemaker_sponge_scaled(fused):
+@pytest.mark.parametrize("kmode", KMODES)
+def test_cfg4_bar_wavemaker_sponge_scaled(kmode):
     """cfg4 recipe (bar bathymetry, wavemaker + sponge zones, 4 lambdas as members)
     on 2^16 cells, 1 and 60 steps."""
     w = W.cfg4(n=1 << 16)
-    s = gpu_solver(w, fused=fused)
+    s = gpu_solver(w, kmode=kmode)
     s.step()
     compare(w, s, range(4), steps=1)
     s.run_steps(59)

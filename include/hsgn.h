@@ -207,9 +207,10 @@ int64_t hsgn_launch_count(const hsgn_ctx *ctx);
 /* Fused step: a two-stage tableau on a non-slab domain
  * runs each step as ONE persistent kernel (stage 1 on a widened tile, U1 kept
  * in shared memory, stage 2, next tile prefetched) instead of one kernel per
- * stage.  Both paths compute the same P:500-517 arithmetic.  on = 0 forces the
- * per-stage kernels (tests compare both); default on.  Drops captured graphs
- * and re-chooses the tile geometry.  Errors: HSGN_E_INVALID (null context). */
+ * stage.  Both paths compute the same P:500-517 arithmetic.  on = 1 selects the
+ * fused kernel (tests compare both); default off (measured slower on B200,
+ * DESIGN.md section 6).  Drops captured graphs and re-chooses the tile
+ * geometry.  Errors: HSGN_E_INVALID (null context). */
 hsgn_status hsgn_set_fused(hsgn_ctx *ctx, int32_t on);
 /* 1 if steps currently run as the fused kernel, 0 otherwise (-1: null). */
 int32_t hsgn_get_fused(const hsgn_ctx *ctx);

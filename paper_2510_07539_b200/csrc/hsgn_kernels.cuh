@@ -117,17 +117,17 @@ struct Bufs {
     double *out[4];
 };
 
-// Reciprocal: hardware approximation (MUFU.RCP64H, ~2^-20) refined by two
-// Newton steps (4 DFMA) to ~1 ulp -- replaces the IEEE division sequence, whose
-// slow-path branch and longer dependency chain dominated the stage's fp64 issue.
+// Reciprocal: hardware approximation (MUFU.RCP64H, ~2^-20) refined by one
+// cubic step r0 (1 + e + e^2), e = 1 - x r0 (relative error e^3 < 2^-60; 3 DFMA,
+// <= 1 ulp from IEEE 1/x, tools/rcp_check.cu) -- replaces the IEEE division
+// sequence, whose slow-path branch and longer dependency chain dominated the
+// stage's fp64 issue.
 __device__ __forceinline__ double rcp(double x)
 {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 
 // Shared memory of the stage kernels: the dynamic row arrays and a few
@@ -286,14 +286,15 @@ __device__ __forceinline__ void muscl_pair(const double (&wh)[3], const double (
 
 // Rusanov flux of R_E at a face (A4): alpha = max(|u-|, |u+|),
 // F = 1/2 (F(U-) + F(U+)) - 1/2 alpha (U+ - U-) for F^q = q u, F^H = H u, F^W = W u.
+// Returned as 2F (the 1/2 is folded into the tau/(2 dx) of the predictor: exact).
 __device__ __forceinline__ Face rusanov(const FState &m, const FState &p)
 {
     const double am = fabs(m.u), ap = fabs(p.u);
     const double a = am > ap ? am : ap;
     Face F;
-    F.q = 0.5 * (m.q * m.u + p.q * p.u) - 0.5 * a * (p.q - m.q);
-    F.H = 0.5 * (m.H * m.u + p.H * p.u) - 0.5 * a * (p.H - m.H);
-    F.W = 0.5 * (m.W * m.u + p.W * p.u) - 0.5 * a * (p.W - m.W);
+    F.q = fma(m.q, m.u, p.q * p.u) - a * (p.q - m.q);
+    F.H = fma(m.H, m.u, p.H * p.u) - a * (p.H - m.H);
+    F.W = fma(m.W, m.u, p.W * p.u) - a * (p.W - m.W);
     return F;
 }
 
@@ -308,7 +309,7 @@ __device__ __forceinline__ FState muscl_plus_next(const double (&wh)[3], const d
     return muscl_plus(th, tq, tH, tW, kap);
 }
 
-struct RowCtx { double tau, tdx, t2, lt2, lam, lam3, ltau, g, idx; };
+struct RowCtx { double tau, tdx2, t2, lt2, lam, lam3, ltau, g, idx; };
 
 // Predictor (A9) and coefficients at E (A2) of
 // one row r; E rows r-1, r, r+1 in (ch, cq, cH, cW); fluxes at r -+ 1/2.
@@ -348,9 +349,10 @@ __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const P
         ptil_term = 1.5 * C.tau * C.lam3 * (1.0 - sg) * Dxb;        // p~
     }
     // predictor
-    const double Wd = WR - C.tdx * (Fr.W - Fl.W) + C.ltau;
-    const double Hd = HR - C.tdx * (Fr.H - Fl.H) - 1.5 * C.tau * qE * Dxb + C.tau * Wd;
-    const double qd = qR - C.tdx * (Fr.q - Fl.q) - ptil_term;
+    // (faces carry 2F: tau/dx (F_r - F_l) = tau/(2 dx) (2F_r - 2F_l))
+    const double Wd = WR - C.tdx2 * (Fr.W - Fl.W) + C.ltau;
+    const double Hd = HR - C.tdx2 * (Fr.H - Fl.H) - 1.5 * C.tau * qE * Dxb + C.tau * Wd;
+    const double qd = qR - C.tdx2 * (Fr.q - Fl.q) - ptil_term;
     // coefficients at E
     const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
     const double a2 = C.g * hE + C.lam3 * sg * (3.0 * sg - 1.0);
@@ -794,7 +796,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     if (live) {
         const double kap = P.order == 2 ? 0.25 : 0.0;
         RowCtx C{};
-        C.tau = tau; C.tdx = tdx; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
+        C.tau = tau; C.tdx2 = tdx2; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
         C.ltau = ltau; C.g = g; C.idx = idx1;
         double wh[3], wq[3], wH[3], wW[3];
 #pragma unroll

@@ -33,6 +33,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fp64 cell-stage updates/s (whole job)"
 UNIT = "cell-stage/s"
+CFL_EX = 0.4          # explicit scheme CFL
 B_STAGE1 = 64   # algorithmic bytes per cell: read U^n (32), write U1 (32)
 B_STAGE2 = 96   # read U^n + U1 (64), write U^{n+1} (32)
 
@@ -47,6 +48,9 @@ def parse():
     p.add_argument("--cells", type=int, default=4096)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--scheme", default="si", choices=["si", "explicit"],
+                   help="si: the SI-IMEX step (headline); explicit: the explicit hSGN scheme "
+                        "(Heun, CFL_EX 0.4) on the same workload")
     p.add_argument("--persistent", type=int, default=-1,
                    help="1: persistent per-stage kernels, 0: one CTA per tile, -1: library default")
     p.add_argument("--fused", type=int, default=-1,
@@ -58,6 +62,16 @@ def parse():
 
 
 def config_dict(a, world):
+    d = _config_dict(a, world)
+    if a.scheme == "explicit":
+        d["scheme"] = "explicit hSGN (P:442-480): Heun, CFL_EX 0.4, MUSCL + Rusanov, A19 filter"
+        d.pop("cfl_imex", None)
+        d.pop("mcfl", None)
+        d.pop("tableau", None)
+    return d
+
+
+def _config_dict(a, world):
     if a.config == "cfg5":
         return {"workload": "cfg5_large_domain: %d cells, periodic, bathymetry 0.2 sin, lambda 1e4, "
                             "100-step config, A19 filter" % a.cells5, "cells": a.cells5,
@@ -151,7 +165,7 @@ def profile_traffic(cells):
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; timed only here, never on the product path)
 # ---------------------------------------------------------------------------
-def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0):
+def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False):
     """Oracle cell-stage/s on the host cores (one member per thread), repeated
     until at least min_seconds of wall time; returns (rate, seconds, repeats)."""
     from oracle import oracle as O
@@ -160,7 +174,10 @@ def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0):
     t0 = time.perf_counter()
     reps = 0
     while True:
-        O.run_members(jobs, threads=threads, cfl=w.cfl, mcfl=w.mcfl, steps=steps)
+        if explicit:
+            O.run_members(jobs, threads=threads, explicit=True, cfl=CFL_EX, steps=steps)
+        else:
+            O.run_members(jobs, threads=threads, cfl=w.cfl, mcfl=w.mcfl, steps=steps)
         reps += 1
         dt = time.perf_counter() - t0
         if dt >= min_seconds:
@@ -241,6 +258,11 @@ def main():
         s = hsgn.solver_for(w)
         Ntot = w.n * w.members
         host_state = None
+    if a.scheme == "explicit":
+        if a.config != "cfg3":
+            raise SystemExit("--scheme explicit: cfg3 only (the explicit scheme needs a flat bottom)")
+        s.set_params(w.g, w.lam, CFL_EX, 0.0)
+        s.set_scheme("explicit", 2)
     if a.fused >= 0:
         s.set_fused(bool(a.fused))
     if a.persistent >= 0:
@@ -328,9 +350,11 @@ def main():
     if rank == 0 and not a.no_cpu and a.config == "cfg3":
         threads = os.cpu_count() or 1
         nm = max(4 * threads, 16)
-        rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0)
+        rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0,
+                                           explicit=a.scheme == "explicit")
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"first {nm} cfg3 members x 10 SI steps, repeated {reps}x ({secs:.1f} s wall)"}
+               "sample": f"first {nm} cfg3 members x 10 {'explicit Heun' if a.scheme == 'explicit' else 'SI'} "
+                         f"steps, repeated {reps}x ({secs:.1f} s wall)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
@@ -340,7 +364,8 @@ def main():
         "per_gpu": value / world,
         "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s",
                      "frac": ach2 / peak, "traffic": traffic,
-                     "kernel": "stage_kernel<STAGE2,FINAL> (stage 2)",
+                     "kernel": ("explicit_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "explicit"
+                                else "stage_kernel<STAGE2,FINAL> (stage 2)"),
                      "bytes_model": f"{bs2} B/cell per stage-2 launch (read U^n, U1{', b' if bathy else ''}; write U^{{n+1}})",
                      "peak_source": peak_src,
                      "stage1": {"achieved": ach1, "frac": ach1 / peak, "bytes_model": f"{bs1} B/cell"},

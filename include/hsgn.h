@@ -214,6 +214,19 @@ int64_t hsgn_launch_count(const hsgn_ctx *ctx);
 hsgn_status hsgn_set_fused(hsgn_ctx *ctx, int32_t on);
 /* 1 if steps currently run as the fused kernel, 0 otherwise (-1: null). */
 int32_t hsgn_get_fused(const hsgn_ctx *ctx);
+/* Time-stepping scheme.  HSGN_SCHEME_SI (default): the
+ * semi-implicit IMEX step of P:500-517.  HSGN_SCHEME_EXPLICIT: the explicit
+ * hSGN scheme of P:442-458 -- central D_x for the mass flux and the pressure
+ * gradient with a^2, alpha at the cell, Rusanov D^_x on the MUSCL
+ * faces for the convective fluxes, relaxation sources -- advanced
+ * by forward Euler (stages = 1) or Heun (stages = 2); dt = CFL dx /
+ * max(|u| + c) with the CFL of hsgn_set_params (the material MCFL is not
+ * used); the A19 filter applies if set.  Explicit runs need a flat bottom, no
+ * relaxation zones and no slab sides (HSGN_E_INVALID at the next step
+ * otherwise).  Errors: HSGN_E_INVALID (unknown scheme, stages not 1 or 2). */
+#define HSGN_SCHEME_SI 0
+#define HSGN_SCHEME_EXPLICIT 1
+hsgn_status hsgn_set_scheme(hsgn_ctx *ctx, int32_t scheme, int32_t stages);
 /* Per-stage kernels as persistent CTAs: each CTA walks
  * (tile, member) items and prefetches the next item's inputs by TMA while it
  * finishes the current one; on = 0: one CTA per (tile, member).  Same

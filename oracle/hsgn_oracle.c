@@ -638,6 +638,162 @@ int orc_run(const orc_problem *P, const orc_tableau *T, double cfl, double mcfl,
     return st;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Explicit hSGN scheme                      */
+/* ------------------------------------------------------------------------ */
+/*
+ * Spatial operator L(U) of the first-order explicit scheme P:444-458, flat
+ * bottom (P->b must be NULL):
+ *   L_h = -D_x(q)
+ *   L_q = -D^_x(q u) - a^2(h, eta) D_x(h) - lambda alpha(h, eta) D_x(h eta)
+ *   L_H = -D^_x(h u eta) + h w                      (H = h eta = K, W = h w)
+ *   L_W = -D^_x(h u w) - lambda (h eta / h^2 - 1)
+ * D_x(F)_i = (F_{i+1/2} - F_{i-1/2})/dx with F_{i+1/2} = (F(U_{i+1}) + F(U_i))/2
+ * (P:463), i.e. (F_{i+1} - F_{i-1})/(2 dx); D^_x is the Rusanov difference of
+ * P:466 with the MUSCL faces of P:469-478 (order 2) or cell values (order 1),
+ * alpha = max(|u-|, |u+|) (A4) -- the same face fluxes as the SI predictor.
+ * a^2 and alpha are taken at cell i, time level of U; alpha and
+ * a^2 as in orc_coeffs.  Ghosts by A10.
+ */
+static int explicit_L(const orc_problem *P, const double *const U[4], double *const L[4])
+{
+    const int n = P->n, G = 2;
+    const double dx = P->dx, g = P->g, lam = P->lambda;
+    const size_t ne = (size_t)(n + 2 * G);
+    if (P->b) return ORC_E_INVALID;   /* flat bottom only */
+    double *buf = (double *)calloc(ne * 4 + (size_t)(n + 1) * 3, sizeof(double));
+    if (!buf) return ORC_E_INVALID;
+    double *eh = buf, *eq = eh + ne, *eH = eq + ne, *eW = eH + ne;
+    double *Fq = eW + ne, *FH = Fq + (n + 1), *FW = FH + (n + 1);
+    fill_ghosts(U[0], n, G, P->bc_left, P->bc_right, 1.0, eh);
+    fill_ghosts(U[1], n, G, P->bc_left, P->bc_right, -1.0, eq);
+    fill_ghosts(U[2], n, G, P->bc_left, P->bc_right, 1.0, eH);
+    fill_ghosts(U[3], n, G, P->bc_left, P->bc_right, 1.0, eW);
+#define XE(a, i) ((a)[(i) + G])
+    /* Rusanov fluxes at faces f+1/2, f = -1 .. n-1 (slot f+1) */
+    for (int f = -1; f <= n - 1; f++) {
+        double vm[4], vp[4];
+        const double *ev[4] = {eh, eq, eH, eW};
+        for (int k = 0; k < 4; k++) {
+            double v0 = XE(ev[k], f), v1 = XE(ev[k], f + 1);
+            if (P->order == 2) {
+                double s0 = (XE(ev[k], f + 1) - XE(ev[k], f - 1)) / 2.0;
+                double s1 = (XE(ev[k], f + 2) - XE(ev[k], f)) / 2.0;
+                vm[k] = v0 + s0 / 2.0;
+                vp[k] = v1 - s1 / 2.0;
+            } else {
+                vm[k] = v0;
+                vp[k] = v1;
+            }
+        }
+        double F[3];
+        orc_rusanov_face(vm, vp, F);
+        Fq[f + 1] = F[0];
+        FH[f + 1] = F[1];
+        FW[f + 1] = F[2];
+    }
+    int st = ORC_OK;
+    for (int i = 0; i < n; i++) {
+        double h = XE(eh, i), H = XE(eH, i), W = XE(eW, i);
+        if (!(h > P->h_min)) st = ORC_E_DRY;
+        double eta = H / h, sigma = eta / h;
+        double alpha = -(1.0 / (3.0 * h)) * (2.0 * sigma - 1.0);
+        double a2 = g * h + (lam / 3.0) * sigma * sigma - lam * eta * alpha;
+        double Dxq = (XE(eq, i + 1) - XE(eq, i - 1)) / (2.0 * dx);
+        double Dxh = (XE(eh, i + 1) - XE(eh, i - 1)) / (2.0 * dx);
+        double DxH = (XE(eH, i + 1) - XE(eH, i - 1)) / (2.0 * dx);
+        L[0][i] = -Dxq;
+        L[1][i] = -(Fq[i + 1] - Fq[i]) / dx - a2 * Dxh - lam * alpha * DxH;
+        L[2][i] = -(FH[i + 1] - FH[i]) / dx + W;
+        L[3][i] = -(FW[i + 1] - FW[i]) / dx - lam * (H / (h * h) - 1.0);
+    }
+#undef XE
+    free(buf);
+    return st;
+}
+
+/* L(U) as a library call (tests). */
+int orc_explicit_rhs(const orc_problem *P, const double *h, const double *q, const double *K,
+                     const double *W, double *Lh, double *Lq, double *LK, double *LW)
+{
+    const double *U[4] = {h, q, K, W};
+    double *L[4] = {Lh, Lq, LK, LW};
+    return explicit_L(P, U, L);
+}
+
+/*
+ * One explicit step: stages = 1 forward Euler U + dt L(U);
+ * stages = 2 Heun: U1 = U + dt L(U),
+ * U^{n+1} = 1/2 U + 1/2 (U1 + dt L(U1)).  Then the optional A19 filter and the
+ * A10 relaxation zones at t + dt, as for the SI step.
+ */
+int orc_explicit_step_t(const orc_problem *P, int stages, double t, double dt, double *h,
+                        double *q, double *K, double *W)
+{
+    if (stages != 1 && stages != 2) return ORC_E_INVALID;
+    const int n = P->n;
+    double *buf = (double *)malloc(sizeof(double) * (size_t)n * 12);
+    if (!buf) return ORC_E_INVALID;
+    double *Un[4], *U1[4], *Lb[4];
+    for (int k = 0; k < 4; k++) {
+        Un[k] = buf + (size_t)n * k;
+        U1[k] = buf + (size_t)n * (4 + k);
+        Lb[k] = buf + (size_t)n * (8 + k);
+    }
+    double *U[4] = {h, q, K, W};
+    for (int k = 0; k < 4; k++) memcpy(Un[k], U[k], sizeof(double) * (size_t)n);
+    int st = explicit_L(P, (const double *const *)Un, Lb);
+    if (st == ORC_OK) {
+        for (int k = 0; k < 4; k++)
+            for (int i = 0; i < n; i++) U1[k][i] = Un[k][i] + dt * Lb[k][i];
+        if (stages == 1) {
+            for (int k = 0; k < 4; k++) memcpy(U[k], U1[k], sizeof(double) * (size_t)n);
+        } else {
+            st = explicit_L(P, (const double *const *)U1, Lb);
+            if (st == ORC_OK)
+                for (int k = 0; k < 4; k++)
+                    for (int i = 0; i < n; i++)
+                        U[k][i] = 0.5 * Un[k][i] + 0.5 * (U1[k][i] + dt * Lb[k][i]);
+        }
+    }
+    if (st == ORC_OK)
+        for (int i = 0; i < n; i++)
+            if (!(h[i] > P->h_min)) st = ORC_E_DRY;
+    if (st == ORC_OK) st = apply_filter(P, U);
+    if (st == ORC_OK) apply_relaxation(P, U, t + dt);
+    free(buf);
+    return st;
+}
+
+/* Explicit run: dt = CFL_EX dx / mu_max (mu = |u| + c, A7) unless
+ * dt_fixed > 0; max_steps steps or until t_end (last step clipped). */
+int orc_explicit_run(const orc_problem *P, int stages, double cfl, double dt_fixed, double t0,
+                     double t_end, int64_t max_steps, double *h, double *q, double *K, double *W,
+                     double *t_out, int64_t *steps_out)
+{
+    double t = t0;
+    int64_t s = 0;
+    int st = ORC_OK;
+    int use_tend = (t_end > t0);
+    while (s < max_steps) {
+        if (use_tend && !(t < t_end)) break;
+        double dt;
+        if (dt_fixed > 0.0) dt = dt_fixed;
+        else {
+            st = orc_dt(P, cfl, 0.0, h, q, K, &dt, NULL, NULL);
+            if (st != ORC_OK) break;
+        }
+        if (use_tend && t + dt >= t_end) dt = t_end - t;
+        st = orc_explicit_step_t(P, stages, t, dt, h, q, K, W);
+        if (st != ORC_OK) break;
+        t = (use_tend && dt == t_end - t) ? t_end : t + dt;
+        s++;
+    }
+    if (t_out) *t_out = t;
+    if (steps_out) *steps_out = s;
+    return st;
+}
+
 /* total mass sum_i h_i dx */
 double orc_mass(int n, double dx, const double *h)
 {

@@ -95,6 +95,13 @@ def lib():
             L.orc_tableau_weights.argtypes = [T, dp, dp]
             L.orc_rusanov_face.restype = None
             L.orc_rusanov_face.argtypes = [dp, dp, dp]
+            L.orc_explicit_rhs.restype = C.c_int
+            L.orc_explicit_rhs.argtypes = [P] + [dp] * 8
+            L.orc_explicit_step_t.restype = C.c_int
+            L.orc_explicit_step_t.argtypes = [P, C.c_int, C.c_double, C.c_double] + [dp] * 4
+            L.orc_explicit_run.restype = C.c_int
+            L.orc_explicit_run.argtypes = [P, C.c_int, C.c_double, C.c_double, C.c_double,
+                                           C.c_double, C.c_int64] + [dp] * 5 + [C.POINTER(C.c_int64)]
             L.orc_mass.restype = C.c_double
             L.orc_mass.argtypes = [C.c_int, C.c_double, dp]
             _lib = L
@@ -191,6 +198,37 @@ class Oracle:
         return U, tout.value, sout.value, mb.value
 
 
+    # -- explicit hSGN scheme -----------------------------------
+    def explicit_rhs(self, U):
+        """L(U) of the explicit scheme P:444-458 (flat bottom)."""
+        U = [np.ascontiguousarray(a, dtype=np.float64) for a in U]
+        O = [np.empty(self.P.n) for _ in range(4)]
+        st = self.L.orc_explicit_rhs(C.byref(self.P), *[_p(a) for a in U], *[_p(a) for a in O])
+        if st != OK:
+            raise OracleError(st, "explicit_rhs")
+        return O
+
+    def explicit_step(self, U, dt, stages=2, t=0.0):
+        """One explicit step: stages 1 = forward Euler, 2 = Heun."""
+        U = [np.array(a, dtype=np.float64, copy=True) for a in U]
+        st = self.L.orc_explicit_step_t(C.byref(self.P), stages, t, dt, *[_p(a) for a in U])
+        if st != OK:
+            raise OracleError(st, "explicit_step")
+        return U
+
+    def explicit_run(self, U, cfl=0.4, stages=2, steps=None, t0=0.0, t_end=None, dt_fixed=0.0):
+        """Advance with dt = CFL_EX dx / mu_max; returns (U, t, steps)."""
+        U = [np.array(a, dtype=np.float64, copy=True) for a in U]
+        tout, sout = C.c_double(), C.c_int64()
+        max_steps = steps if steps is not None else (1 << 62)
+        te = t_end if t_end is not None else t0 - 1.0
+        st = self.L.orc_explicit_run(C.byref(self.P), stages, cfl, dt_fixed, t0, te, max_steps,
+                                     *[_p(a) for a in U], C.byref(tout), C.byref(sout))
+        if st != OK:
+            raise OracleError(st, f"explicit_run (after {sout.value} steps)")
+        return U, tout.value, sout.value
+
+
 def coeffs(g, lam, tau, h, H, Hdag):
     out = np.empty(6)
     lib().orc_coeffs(g, lam, tau, h, H, Hdag, _p(out))
@@ -232,10 +270,13 @@ def mass(h, dx):
     return lib().orc_mass(len(h), dx, _p(h))
 
 
-def run_members(members, threads=None, **kw):
+def run_members(members, threads=None, explicit=False, **kw):
     """Run independent ensemble members on host threads (ctypes releases the GIL).
-    members: list of (Oracle, U).  Returns list of results of Oracle.run."""
+    members: list of (Oracle, U).  Returns list of results of Oracle.run (or of
+    Oracle.explicit_run with explicit=True)."""
     from concurrent.futures import ThreadPoolExecutor
     threads = threads or os.cpu_count() or 1
     with ThreadPoolExecutor(max_workers=threads) as ex:
+        if explicit:
+            return list(ex.map(lambda m: m[0].explicit_run(m[1], **kw), members))
         return list(ex.map(lambda m: m[0].run(m[1], **kw), members))

@@ -76,6 +76,9 @@ struct hsgn_ctx {
     bool fused_on = false, fused = false;
     int fused_grid = 0;
     int pf_dist = 0;              // L2 prefetch distance of the stage kernels (CTAs)
+    // scheme: 0 = SI-IMEX (default), 1 = explicit hSGN (P:442-480,
+    // x_stages 1 = Euler, 2 = Heun) on tiles of xT cells
+    int scheme = 0, x_stages = 2, xT = 0, xtiles = 0;
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
     bool persist = false;
     int persist_grid = 0;
@@ -130,6 +133,11 @@ Params make_params(hsgn_ctx *c, long long k)
     P.work = c->work;
     P.H = c->w + 3;
     P.pf_dist = c->pf_dist;
+    if (c->scheme == 1) {            // explicit: its own tiles, dt = CFL_EX dx / mu_max only
+        P.T = c->xT;
+        P.tiles = c->xtiles;
+        P.mcfl = 0.0;
+    }
     P.inv_tiles = 1.0 / double(c->tiles);
     for (int k = 0; k < 9; k++) {
         P.halo_l[k] = c->halo_l ? c->halo_l + k * H_MAX : nullptr;
@@ -186,7 +194,30 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
     }
     hsgn_status st;
     if (ev) CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
-    if (c->fused) {
+    if (c->scheme == 1) {
+        dim3 grid(c->xtiles, c->members);
+        const bool filt = c->filter_sigma > 0.0;
+        if (c->x_stages == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            if (filt) explicit_kernel<false, true, true><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            else explicit_kernel<false, true, false><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            c->launches++;
+            CUDA_TRY(c, cudaGetLastError());
+            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            explicit_kernel<false, false, false><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            c->launches++;
+            CUDA_TRY(c, cudaGetLastError());
+            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            if (filt) explicit_kernel<true, true, true><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            else explicit_kernel<true, true, false><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            c->launches++;
+            CUDA_TRY(c, cudaGetLastError());
+        }
+        if (ev) CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+    } else if (c->fused) {
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         const int items = c->tiles * c->members;
         const bool relax = c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0;
@@ -281,6 +312,8 @@ void choose_geometry(hsgn_ctx *c)
     c->T = T;
     c->w = w;
     c->tiles = (c->n + T - 1) / T;
+    c->xT = std::min(c->n, XT);
+    c->xtiles = (c->n + c->xT - 1) / c->xT;
     {
         int sms = 148, occ = 4;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -307,6 +340,8 @@ hsgn_status ready(hsgn_ctx *c)
     if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
     if (!c->have_params) return fail(c, HSGN_E_INVALID, "hsgn_set_params not called");
     if (!c->have_state) return fail(c, HSGN_E_INVALID, "hsgn_set_state not called");
+    if (c->scheme == 1 && (c->bathy || c->slab || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
+        return fail(c, HSGN_E_INVALID, "explicit scheme: flat bottom, no relaxation zones, no slabs");
     return HSGN_OK;
 }
 
@@ -348,7 +383,8 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
                 cudaGraphDestroy(gr);
             }
             CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
-            c->launches += GRAPH_STEPS * ((c->fused ? 1 : c->tab.stages) + 1);
+            const int kpl = c->scheme == 1 ? c->x_stages : (c->fused ? 1 : c->tab.stages);
+            c->launches += GRAPH_STEPS * (kpl + 1);
             done += GRAPH_STEPS;          // even: cur unchanged
             c->host_steps += GRAPH_STEPS;
         } else {
@@ -598,6 +634,11 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_pkernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(explicit_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
+    cudaFuncSetAttribute(explicit_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
+    cudaFuncSetAttribute(explicit_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
+    cudaFuncSetAttribute(explicit_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
+    cudaFuncSetAttribute(explicit_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(step_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cudaFuncSetAttribute(step_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
@@ -977,6 +1018,23 @@ hsgn_status hsgn_set_fused(hsgn_ctx *c, int32_t on)
 }
 
 int32_t hsgn_get_fused(const hsgn_ctx *c) { return c ? (c->fused ? 1 : 0) : -1; }
+
+hsgn_status hsgn_set_scheme(hsgn_ctx *c, int32_t scheme, int32_t stages)
+{
+    if (!c) return HSGN_E_INVALID;
+    if (scheme == HSGN_SCHEME_SI) {
+        c->scheme = 0;
+    } else if (scheme == HSGN_SCHEME_EXPLICIT) {
+        if (stages != 1 && stages != 2) return fail(c, HSGN_E_INVALID, "explicit stages must be 1 or 2");
+        c->scheme = 1;
+        c->x_stages = stages;
+    } else {
+        return fail(c, HSGN_E_INVALID, "unknown scheme");
+    }
+    drop_graphs(c);
+    choose_geometry(c);
+    return HSGN_OK;
+}
 
 hsgn_status hsgn_set_persistent(hsgn_ctx *c, int32_t on)
 {

@@ -1526,6 +1526,241 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) step_kernel(const Params P, con
 }
 
 // ---------------------------------------------------------------------------
+// Explicit hSGN scheme, flat bottom:
+//   L_h = -D_x(q),  L_q = -D^_x(q u) - a^2 D_x(h) - lam alpha D_x(h eta),
+//   L_H = -D^_x(H u) + W,  L_W = -D^_x(W u) - lam (H/h^2 - 1)
+// D_x centred over i+-1, D^_x the Rusanov difference of the MUSCL face
+// states (A4, A5: the same faces as the SI predictor), a^2, alpha
+// at cell i.  Euler: U + dt L(U); Heun: U1 = U + dt L(U),
+// U^{n+1} = (U + U1 + dt L(U1)) / 2; then the optional A19 filter on q, W.
+//
+// explicit_kernel<HEUN2, FINAL, FILT>: one CTA per tile of XT kept cells of one
+// member; the stencil input X (U^n, or U1 for HEUN2) is TMA-loaded into shared
+// memory with R = 2 (+2 with the filter) halo rows; the base U^n is read per
+// cell from global memory.  Thread t owns rows t, t + XNT, ... (consecutive
+// threads on consecutive rows: conflict-free shared accesses, coalesced
+// global stores).  With the filter the final q, W of rows -2 .. XT+1 are
+// computed (the 4 halo rows redundantly) into shared memory first.
+// ---------------------------------------------------------------------------
+constexpr int XNT = 256;                 // threads per CTA
+constexpr int XT = 1024;                 // kept cells per tile
+constexpr int XR = 4;                    // halo rows of X (filter: 2 + 2)
+constexpr int XROWS = XT + 2 * XR + 8;   // shared rows per X array (+ alignment)
+constexpr int XFROWS = XT + 8;           // shared rows of the filter arrays
+constexpr size_t XSMEM_BYTES = (size_t(4) * XROWS + 2 * size_t(XFROWS)) * sizeof(double);
+
+// L(X) at row r of the tile (rows r-2 .. r+2 of the shared arrays).
+__device__ __forceinline__ void explicit_rhs(const double *xh, const double *xq, const double *xH,
+                                             const double *xW, int r, double kap, double g,
+                                             double lam, double idx, double ihdx, double out[4])
+{
+    double wh[3], wq[3], wH[3], wW[3];
+    // face r-1/2: M_{r-1} (rows r-2..r) and Pl_r (rows r-1..r+1)
+#pragma unroll
+    for (int k = 0; k < 3; k++) { wh[k] = xh[r - 2 + k]; wq[k] = xq[r - 2 + k]; wH[k] = xH[r - 2 + k]; wW[k] = xW[r - 2 + k]; }
+    const FState Mm = muscl_minus(wh, wq, wH, wW, kap);
+#pragma unroll
+    for (int k = 0; k < 3; k++) { wh[k] = xh[r - 1 + k]; wq[k] = xq[r - 1 + k]; wH[k] = xH[r - 1 + k]; wW[k] = xW[r - 1 + k]; }
+    FState Pl, M0;
+    muscl_pair(wh, wq, wH, wW, kap, Pl, M0);
+    const Face Fl = rusanov(Mm, Pl);                       // 2 x flux at r-1/2
+    // face r+1/2: M_r and Pl_{r+1} (rows r..r+2)
+    const double h2 = xh[r + 2], q2 = xq[r + 2], H2 = xH[r + 2], W2 = xW[r + 2];
+    const FState Pr = muscl_plus_next(wh, wq, wH, wW, h2, q2, H2, W2, kap);
+    const Face Fr = rusanov(M0, Pr);                       // 2 x flux at r+1/2
+    const double h = wh[1], H = wH[1], W = wW[1];
+    const double ih = rcp(h);
+    const double eta = H * ih, sg = eta * ih;                               // eta, eta/h
+    const double alpha = -(2.0 * sg - 1.0) * ih * (1.0 / 3.0);
+    const double a2 = g * h + lam * (1.0 / 3.0) * sg * sg - lam * eta * alpha;
+    const double Dxq = (wq[2] - wq[0]) * ihdx, Dxh = (wh[2] - wh[0]) * ihdx;
+    const double DxH = (wH[2] - wH[0]) * ihdx;
+    const double hidx = 0.5 * idx;                          // faces carry 2F
+    out[0] = -Dxq;
+    out[1] = -(Fr.q - Fl.q) * hidx - a2 * Dxh - lam * alpha * DxH;
+    out[2] = -(Fr.H - Fl.H) * hidx + W;
+    out[3] = -(Fr.W - Fl.W) * hidx - lam * (sg - 1.0);     // H/h^2 = eta/h
+}
+
+template <bool HEUN2, bool FINAL, bool FILT>
+__global__ void __launch_bounds__(XNT) explicit_kernel(const Params P, const Bufs B)
+{
+    const int tid = threadIdx.x;
+    const int j = blockIdx.x, m = blockIdx.y;
+    const int n = P.n;
+    const size_t mo = size_t(m) * n;
+    const int s = j * P.T;
+    const int e = min(n, s + P.T);
+    const int Tk = e - s;
+    constexpr int R = FILT ? XR : 2;           // halo rows of X needed
+    constexpr int RO = FILT ? 2 : 0;           // halo rows of final values
+    double *const smem = dyn_smem();
+    const double *const *X = HEUN2 ? B.U1 : B.Un;
+    // ---- load X rows -R .. Tk+R-1 (TMA for interior tiles, 16-B aligned) -----
+    const int a0r = s - R;
+    const bool interior = (a0r >= 0) && (s + Tk + R <= n);
+    const int d = interior ? int((mo + size_t(a0r)) & 1) : 0;
+    const int cnt = (Tk + 2 * R + d + 1) & ~1;
+    const bool bulk = interior && (a0r - d >= 0) && (a0r - d + cnt <= n);
+    double *const A = smem + d + R;            // row r of array k at A[k * XROWS + r]
+    double *xh = A, *xq = A + XROWS, *xH = A + 2 * XROWS, *xW = A + 3 * XROWS;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
+    if (bulk) {
+        init_mbar(mb);
+        if (tid == 0) {
+            const unsigned bytes = unsigned(cnt) * 8u;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes * 4u)
+                         : "memory");
+            const size_t gsrc = mo + size_t(a0r - d);
+#pragma unroll
+            for (int f = 0; f < 4; f++) bulk_g2s(smem + f * XROWS, X[f] + gsrc, bytes, mb);
+        }
+    } else {
+        for (int r = tid - R; r < Tk + R; r += XNT) {
+            double par;
+            const size_t gi = mo + size_t(map_cell(s + r, n, P.bcl, P.bcr, par));
+            cp_async8(xh + r, X[0] + gi); cp_async8(xq + r, X[1] + gi);
+            cp_async8(xH + r, X[2] + gi); cp_async8(xW + r, X[3] + gi);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    const unsigned int err0 = *((volatile unsigned int *)P.err);
+    const double dtm = P.dt[m];
+    const double lam = P.lam[m];
+    if (bulk) mbar_wait(mb, 0);
+    else cp_async_wait_all();
+    __syncthreads();
+    if (err0) return;
+    // wall ghosts: q is odd (A10); the raw copies need the sign
+    if (!interior && (P.bcl == BC_WALL || P.bcr == BC_WALL)) {
+        for (int r = tid - R; r < Tk + R; r += XNT) {
+            double par;
+            (void)map_cell(s + r, n, P.bcl, P.bcr, par);
+            xq[r] *= par;
+        }
+        __syncthreads();
+    }
+    const double kap = P.order == 2 ? 0.25 : 0.0;
+    const double g = P.g, idx = P.idx, ihdx = 0.5 * P.idx;
+    double umax = 0.0, numax = 0.0;
+    unsigned int errbits = 0u;
+    double *fq = smem + 4 * XROWS + 2, *fw = fq + XFROWS;   // final q, W rows -2 .. Tk+1 (filter)
+    if (dtm == 0.0) {
+        // member already at t_end: carry the state (and its dt maxima)
+        for (int r = tid; r < Tk; r += XNT) {
+            const size_t gi = mo + s + r;
+            const double h = B.Un[0][gi], q = B.Un[1][gi], K = B.Un[2][gi], W = B.Un[3][gi];
+            B.out[0][gi] = h; B.out[1][gi] = q; B.out[2][gi] = K; B.out[3][gi] = W;
+            if (FINAL) {
+                const double ih = rcp(h);
+                const double u = fabs(q * ih), sg = K * ih * ih;
+                const double nu = u + fsqrt(g * h + lam * (1.0 / 3.0) * sg * sg);
+                umax = u > umax ? u : umax;
+                numax = nu > numax ? nu : numax;
+            }
+        }
+    } else {
+    // ---- final values of rows -RO .. Tk+RO-1 ----------------------------------
+    for (int r = tid - RO; r < Tk + RO; r += XNT) {
+        const bool kept = r >= 0 && r < Tk;
+        double L[4];
+        explicit_rhs(xh, xq, xH, xW, r, kap, g, lam, idx, ihdx, L);
+        double o[4];
+        if (HEUN2) {
+            double par;
+            const size_t gi = mo + size_t(map_cell(s + r, n, P.bcl, P.bcr, par));
+            const double b0 = B.Un[0][gi], b1 = par * B.Un[1][gi], b2 = B.Un[2][gi], b3 = B.Un[3][gi];
+            o[0] = 0.5 * b0 + 0.5 * (xh[r] + dtm * L[0]);
+            o[1] = 0.5 * b1 + 0.5 * (xq[r] + dtm * L[1]);
+            o[2] = 0.5 * b2 + 0.5 * (xH[r] + dtm * L[2]);
+            o[3] = 0.5 * b3 + 0.5 * (xW[r] + dtm * L[3]);
+        } else {
+            o[0] = xh[r] + dtm * L[0];
+            o[1] = xq[r] + dtm * L[1];
+            o[2] = xH[r] + dtm * L[2];
+            o[3] = xW[r] + dtm * L[3];
+        }
+        if (FILT) { fq[r] = o[1]; fw[r] = o[3]; }
+        if (kept) {
+            if (!(o[0] > P.h_min)) errbits |= ERR_DRY;
+            if (!isfinite(o[0] + o[1] + o[2] + o[3])) errbits |= ERR_NONFINITE;
+            B.out[0][mo + s + r] = o[0];
+            B.out[2][mo + s + r] = o[2];
+            if (!FILT) { B.out[1][mo + s + r] = o[1]; B.out[3][mo + s + r] = o[3]; }
+            if (FINAL && !FILT) {
+                const double ih = rcp(o[0]);
+                const double u = fabs(o[1] * ih), sg = o[2] * ih * ih;
+                const double nu = u + fsqrt(g * o[0] + lam * (1.0 / 3.0) * sg * sg);
+                umax = u > umax ? u : umax;
+                numax = nu > numax ? nu : numax;
+            }
+        }
+    }
+    if (FILT) {
+        __syncthreads();
+        const double sig16 = P.filter_sigma * (1.0 / 16.0);
+        for (int r = tid; r < Tk; r += XNT) {
+            // A19 on q and W; the halo rows are the neighbours' final values
+            // (the mirror of the tile itself at a physical end, A10)
+            double cq[5], cw[5];
+#pragma unroll
+            for (int k = 0; k < 5; k++) {
+                const int c = s + r + k - 2;
+                int rr = r + k - 2;
+                double pq = 1.0;
+                if (c < 0 && P.bcl != BC_PERIODIC) {
+                    if (P.bcl == BC_WALL) { rr = -1 - c - s; pq = -1.0; } else rr = -s;
+                } else if (c >= n && P.bcr != BC_PERIODIC) {
+                    if (P.bcr == BC_WALL) { rr = 2 * n - 1 - c - s; pq = -1.0; } else rr = n - 1 - s;
+                }
+                cq[k] = pq * fq[rr];
+                cw[k] = fw[rr];
+            }
+            const double qo = cq[2] - sig16 * (cq[0] - 4.0 * cq[1] + 6.0 * cq[2] - 4.0 * cq[3] + cq[4]);
+            const double wo = cw[2] - sig16 * (cw[0] - 4.0 * cw[1] + 6.0 * cw[2] - 4.0 * cw[3] + cw[4]);
+            if (!isfinite(qo + wo)) errbits |= ERR_NONFINITE;
+            B.out[1][mo + s + r] = qo;
+            B.out[3][mo + s + r] = wo;
+            if (FINAL) {
+                const double h0 = B.out[0][mo + s + r], K0 = B.out[2][mo + s + r];
+                const double ih = rcp(h0);
+                const double u = fabs(qo * ih), sg = K0 * ih * ih;
+                const double nu = u + fsqrt(g * h0 + lam * (1.0 / 3.0) * sg * sg);
+                umax = u > umax ? u : umax;
+                numax = nu > numax ? nu : numax;
+            }
+        }
+    }
+    }   // dtm != 0
+    // ---- error bits, dt maxima, next time level --------------------------------
+    const int lane = tid & 31, wid = tid >> 5;
+    const unsigned int eb = __reduce_or_sync(0xffffffffu, errbits);
+    if (lane == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
+    if (FINAL) {
+        __shared__ double xred[2][XNT / 32];
+        const double um = warp_max_nonneg(umax), nm = warp_max_nonneg(numax);
+        if (lane == 0) { xred[0][wid] = um; xred[1][wid] = nm; }
+        __syncthreads();
+        if (tid == 0) {
+            double a = xred[0][0], b = xred[1][0];
+            for (int q = 1; q < XNT / 32; q++) {
+                a = xred[0][q] > a ? xred[0][q] : a;
+                b = xred[1][q] > b ? xred[1][q] : b;
+            }
+            const int members = P.members;
+            const int slot_w = (P.kslot + 1) % 3;
+            atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(a));
+            atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(b));
+            if (j == 0) {
+                const double tm = P.t[P.kpar * members + m];
+                const double t_end = P.ctrl->t_end;
+                P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Between steps: commit step k-1 (steps += 1 unless an error was latched) and
 // set dt of step k for every member from the max|u|, max(|u|+c) of U^k
 // (A7), clipped to t_end; free the maxima slot read at

@@ -131,3 +131,45 @@ def slow_mode_state(x, k, eps, h0, lam, g, t=0.0):
     h = h0 + hp
     eta = h0 + etap
     return h, h * up, h * eta, h * wp
+
+
+def explicit_symbol(theta, dx, h0, lam, g, dt, order=2, stages=2, filter_sigma=0.0):
+    """4x4 amplification matrix of one explicit step (Heun P:480)
+    about rest.  Linearising L(U): the convective fluxes q u and W u are
+    quadratic and Rusanov's alpha = |u| is O(eps), so only F^H = H q / h keeps
+    the linear part h0 q' (through the MUSCL face average M); at rest
+    sigma = 1, alpha0 = -1/(3 h0) and a0^2 = g h0 + (lam/3) - lam h0 alpha0
+    = g h0 + 2 lam/3; lam (H/h^2 - 1) linearises to
+    (lam/h0^2)(H' - 2 h0 h').  With D = i sin(th)/dx:
+      L_h = -D q'
+      L_q = -a0^2 D h' - lam alpha0 D H'
+      L_H = -h0 M q' + W'
+      L_W = (2 lam/h0) h' - (lam/h0^2) H'
+    Euler: G = I + dt A; Heun: G = I + dt A + (dt A)^2 / 2."""
+    e = np.exp(1j * theta)
+    D = 1j * np.sin(theta) / dx
+    if order == 2:
+        face = (1 + e) / 2 + (e - 1 / e - e ** 2 + 1) / 8
+    else:
+        face = (1 + e) / 2
+    M = (1 - 1 / e) * face / dx
+    a2 = g * h0 + 2.0 * lam / 3.0
+    al = -1.0 / (3.0 * h0)
+    A = np.array([[0, -D, 0, 0],
+                  [-a2 * D, 0, -lam * al * D, 0],
+                  [0, -h0 * M, 0, 1.0],
+                  [2 * lam / h0, 0, -lam / h0 ** 2, 0]], dtype=complex)
+    I = np.eye(4, dtype=complex)
+    G = I + dt * A if stages == 1 else I + dt * A + 0.5 * (dt * A) @ (dt * A)
+    if filter_sigma > 0:
+        F = 1.0 - filter_sigma * np.sin(theta / 2.0) ** 4
+        G[1, :] *= F
+        G[3, :] *= F
+    return G
+
+
+def explicit_max_growth(dx, h0, lam, g, dt, order=2, stages=2, filter_sigma=0.0, thetas=None):
+    if thetas is None:
+        thetas = np.linspace(1e-3, np.pi, 600)
+    return max(np.max(np.abs(np.linalg.eigvals(explicit_symbol(th, dx, h0, lam, g, dt, order, stages,
+                                                               filter_sigma)))) for th in thetas)

@@ -45,6 +45,9 @@
 #ifndef HSGN_EXP_NOPREFETCH            // persistent kernel loads each item at its start
 #define HSGN_EXP_NOPREFETCH 0
 #endif
+#ifndef HSGN_STORE_DIRECT               // stage kernels: coalesced STG from staging, no TMA store
+#define HSGN_STORE_DIRECT 0
+#endif
 #ifndef HSGN_EXP_TIMING                 // per-CTA phase clocks (hsgn_exp_counters)
 #define HSGN_EXP_TIMING 0
 #endif
@@ -1181,7 +1184,7 @@ __device__ __forceinline__ void store_tile(const Bufs &B, size_t mo, int s, int 
 {
     const int tid = threadIdx.x;
     const size_t gdst = mo + size_t(s);
-    const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
+    const bool bulk_out = !HSGN_STORE_DIRECT && ((gdst | size_t(Tk)) & 1) == 0;
     double *oh, *oq, *oK, *oW;
     stage_ptrs(dedicated, T, oh, oq, oK, oW);
     if (HSGN_EXP_NOSTORE) {

@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--cells", type=int, default=4096)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--si-order", type=int, default=2, choices=[1, 2],
+                   help="2: the paper's second-order SI step (headline); 1: first-order SI "
+                        "(one implicit stage tau = dt, order-1 faces; SURVEY row f2)")
     p.add_argument("--scheme", default="si", choices=["si", "explicit"],
                    help="si: the SI-IMEX step (headline); explicit: the explicit hSGN scheme "
                         "(Heun, CFL_EX 0.4) on the same workload")
@@ -63,6 +66,10 @@ def parse():
 
 def config_dict(a, world):
     d = _config_dict(a, world)
+    if a.si_order == 1:
+        d["scheme"] = "first-order SI (P:500-517: one implicit stage, tau = dt, order-1 faces)"
+        d["order"] = 1
+        d["tableau"] = "SI Euler (a_11 = 1)"
     if a.scheme == "explicit":
         d["scheme"] = "explicit hSGN (P:442-480): Heun, CFL_EX 0.4, MUSCL + Rusanov, A19 filter"
         d.pop("cfl_imex", None)
@@ -165,12 +172,13 @@ def profile_traffic(cells):
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; timed only here, never on the product path)
 # ---------------------------------------------------------------------------
-def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False):
+def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False, si_order=2):
     """Oracle cell-stage/s on the host cores (one member per thread), repeated
     until at least min_seconds of wall time; returns (rate, seconds, repeats)."""
     from oracle import oracle as O
-    jobs = [(O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, b=w.b,
-                      filter_sigma=w.filter_sigma), w.state(m)) for m in members]
+    tab = O.euler_tableau() if si_order == 1 else None
+    jobs = [(O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, b=w.b, order=si_order,
+                      filter_sigma=w.filter_sigma, tableau=tab), w.state(m)) for m in members]
     t0 = time.perf_counter()
     reps = 0
     while True:
@@ -182,7 +190,7 @@ def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False)
         dt = time.perf_counter() - t0
         if dt >= min_seconds:
             break
-    return 2.0 * w.n * len(members) * steps * reps / dt, dt, reps
+    return (1.0 if si_order == 1 and not explicit else 2.0) * w.n * len(members) * steps * reps / dt, dt, reps
 
 
 def run_reference(a, rank, world):
@@ -258,6 +266,15 @@ def main():
         s = hsgn.solver_for(w)
         Ntot = w.n * w.members
         host_state = None
+    if a.si_order == 1:
+        if a.config != "cfg3" or a.scheme != "si":
+            raise SystemExit("--si-order 1: cfg3 SI only")
+        s.close()
+        s = hsgn.Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, order=1)
+        s.set_params(w.g, w.lam, w.cfl, w.mcfl)
+        s.set_tableau(hsgn.euler_tableau())
+        s.set_filter(w.filter_sigma)
+        s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
     if a.scheme == "explicit":
         if a.config != "cfg3":
             raise SystemExit("--scheme explicit: cfg3 only (the explicit scheme needs a flat bottom)")
@@ -307,13 +324,16 @@ def main():
     elapsed, ms1, ms2 = [float(x) for x in t.tolist()]
     diag = s.diagnostics()
 
-    value = 2.0 * Ntot * a.steps * world / (elapsed / 1e3)    # Ntot = cells of this rank
+    nst = 1 if a.si_order == 1 else 2                         # cell-stages per cell and step
+    value = nst * Ntot * a.steps * world / (elapsed / 1e3)    # Ntot = cells of this rank
     peaks, peak_src = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    if nst == 1:
+        ms2 = ms1                      # the one (final) stage: U^n -> U^{n+1}, 64 B/cell
     t2 = ms2 / a.steps / 1e3
     t1 = ms1 / a.steps / 1e3
     bs1 = B_STAGE1 + (8 if bathy else 0)    # + b read per stage
-    bs2 = B_STAGE2 + (8 if bathy else 0)
+    bs2 = (B_STAGE1 if nst == 1 else B_STAGE2) + (8 if bathy else 0)
     ach2 = bs2 * Ntot / t2 / 1e9
     ach1 = bs1 * Ntot / t1 / 1e9
     traffic = profile_traffic(Ntot)
@@ -341,7 +361,7 @@ def main():
         if world > 1:
             dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
         te = float(tt_.item())
-        e2e = {"value": 2.0 * Ntot * a.steps * world / te, "unit": UNIT,
+        e2e = {"value": nst * Ntot * a.steps * world / te, "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / a.steps,
                "d2h_bytes_per_step": 8 * w.members + state_bytes / a.steps,
                "what": "Solver.set_state(pinned host) + K x Solver.step(return_dt) + get_state(pinned host), wall clock, max over ranks"}
@@ -351,7 +371,7 @@ def main():
         threads = os.cpu_count() or 1
         nm = max(4 * threads, 16)
         rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0,
-                                           explicit=a.scheme == "explicit")
+                                           explicit=a.scheme == "explicit", si_order=a.si_order)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"first {nm} cfg3 members x 10 {'explicit Heun' if a.scheme == 'explicit' else 'SI'} "
                          f"steps, repeated {reps}x ({secs:.1f} s wall)"}
@@ -365,11 +385,14 @@ def main():
         "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s",
                      "frac": ach2 / peak, "traffic": traffic,
                      "kernel": ("explicit_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "explicit"
+                                else "stage_kernel<FINAL> (the one SI stage)" if nst == 1
                                 else "stage_kernel<STAGE2,FINAL> (stage 2)"),
-                     "bytes_model": f"{bs2} B/cell per stage-2 launch (read U^n, U1{', b' if bathy else ''}; write U^{{n+1}})",
+                     "bytes_model": (f"{bs2} B/cell per launch (read U^n; write U^{{n+1}})" if nst == 1 else
+                                     f"{bs2} B/cell per stage-2 launch (read U^n, U1{', b' if bathy else ''}; write U^{{n+1}})"),
                      "peak_source": peak_src,
                      "stage1": {"achieved": ach1, "frac": ach1 / peak, "bytes_model": f"{bs1} B/cell"},
-                     "step_avg_frac": (0.5 * (bs1 + bs2) * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak},
+                     "step_avg_frac": ((ach2 / peak) if nst == 1 else
+                                       (0.5 * (bs1 + bs2) * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches * world,

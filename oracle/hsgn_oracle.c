@@ -794,6 +794,189 @@ int orc_explicit_run(const orc_problem *P, int stages, double cfl, double dt_fix
     return st;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Classical SGN scheme, flat bottom          */
+/* ------------------------------------------------------------------------ */
+/*
+ * Explicit scheme for the standard SGN equations in elliptic-hyperbolic form
+ * (P:548-556):
+ *   h_t + (hu)_x = 0,  (hu)_t + (hu^2 + g h^2/2)_x = h phi,
+ *   h_i phi_i - (1/(3 dx^2)) (h^3_{i+1/2}(phi_{i+1} - phi_i) - h^3_{i-1/2}(phi_i - phi_{i-1})) = h*_i,
+ *   h*_i = -(1/(6 dx^3)) ( g h^3_{i+1} (h_{i+2} - 2h_{i+1} + h_i) + (h^3_{i+1}/2)(u_{i+2} - u_i)^2
+ *                        - g h^3_{i-1} (h_i - 2h_{i-1} + h_{i-2}) - (h^3_{i-1}/2)(u_i - u_{i-2})^2 )
+ * Readings (A23): the g-term carries h^3 (P:591 prints g h_{i+1}; the
+ * discretisation of -(h^3/3 g h_xx)_x of P:548 needs h^3); h_{i+1/2} =
+ * (h_i + h_{i+1})/2; Rusanov fluxes of the shallow-water part on MUSCL faces
+ * of (h, q) with the wave speed alpha = max(|u| + sqrt(g h)) of both face
+ * states; phi ghosts: periodic wrap, wall phi_{-1} = -phi_0 (phi is an
+ * acceleration, odd like q), transmissive phi_{-1} = phi_0.  K and W are not
+ * part of this model and are carried unchanged.
+ */
+static int sgn_L(const orc_problem *P, const double *h, const double *q, double *Lh, double *Lq)
+{
+    const int n = P->n, G = 2;
+    const double dx = P->dx, g = P->g;
+    const size_t ne = (size_t)(n + 2 * G);
+    if (P->b) return ORC_E_INVALID;
+    double *buf = (double *)calloc(ne * 3 + (size_t)(n + 1) * 2 + (size_t)n * 4, sizeof(double));
+    if (!buf) return ORC_E_INVALID;
+    double *eh = buf, *eq = eh + ne, *eu = eq + ne;
+    double *Fh = eu + ne, *Fq = Fh + (n + 1);
+    double *lo = Fq + (n + 1), *di = lo + n, *up = di + n, *rhs = up + n;
+    double *phi = (double *)calloc((size_t)n, sizeof(double));
+    if (!phi) { free(buf); return ORC_E_INVALID; }
+    fill_ghosts(h, n, G, P->bc_left, P->bc_right, 1.0, eh);
+    fill_ghosts(q, n, G, P->bc_left, P->bc_right, -1.0, eq);
+    int st = ORC_OK;
+    for (int i = -G; i < n + G; i++) {
+        if (!(eh[i + G] > P->h_min)) st = ORC_E_DRY;
+        eu[i + G] = eq[i + G] / eh[i + G];
+    }
+#define XS(a, i) ((a)[(i) + G])
+    /* Rusanov fluxes of (q, q^2/h + g h^2/2) at faces f+1/2, f = -1 .. n-1 */
+    for (int f = -1; f <= n - 1; f++) {
+        double vm[2], vp[2];
+        const double *ev[2] = {eh, eq};
+        for (int k = 0; k < 2; k++) {
+            double v0 = XS(ev[k], f), v1 = XS(ev[k], f + 1);
+            if (P->order == 2) {
+                double s0 = (XS(ev[k], f + 1) - XS(ev[k], f - 1)) / 2.0;
+                double s1 = (XS(ev[k], f + 2) - XS(ev[k], f)) / 2.0;
+                vm[k] = v0 + s0 / 2.0;
+                vp[k] = v1 - s1 / 2.0;
+            } else {
+                vm[k] = v0;
+                vp[k] = v1;
+            }
+        }
+        double um = vm[1] / vm[0], up_ = vp[1] / vp[0];
+        double am = fabs(um) + sqrt(g * vm[0]), ap = fabs(up_) + sqrt(g * vp[0]);
+        double a = am > ap ? am : ap;
+        double fhm = vm[1], fhp = vp[1];
+        double fqm = vm[1] * um + 0.5 * g * vm[0] * vm[0];
+        double fqp = vp[1] * up_ + 0.5 * g * vp[0] * vp[0];
+        Fh[f + 1] = 0.5 * (fhm + fhp) - 0.5 * a * (vp[0] - vm[0]);
+        Fq[f + 1] = 0.5 * (fqm + fqp) - 0.5 * a * (vp[1] - vm[1]);
+    }
+    /* phi system */
+    for (int i = 0; i < n; i++) {
+        double hl = 0.5 * (XS(eh, i - 1) + XS(eh, i)), hr = 0.5 * (XS(eh, i) + XS(eh, i + 1));
+        double cl = hl * hl * hl / (3.0 * dx * dx), cr = hr * hr * hr / (3.0 * dx * dx);
+        double hp = XS(eh, i + 1), hm = XS(eh, i - 1);
+        double hp3 = hp * hp * hp, hm3 = hm * hm * hm;
+        double up2 = XS(eu, i + 2) - XS(eu, i), um2 = XS(eu, i) - XS(eu, i - 2);
+        rhs[i] = -(1.0 / (6.0 * dx * dx * dx))
+                 * (g * hp3 * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i)) + 0.5 * hp3 * up2 * up2
+                    - g * hm3 * (XS(eh, i) - 2.0 * hm + XS(eh, i - 2)) - 0.5 * hm3 * um2 * um2);
+        lo[i] = -cl;
+        up[i] = -cr;
+        di[i] = XS(eh, i) + cl + cr;
+    }
+    if (P->bc_left != ORC_BC_PERIODIC) {
+        /* phi_{-1} = p phi_0 folds into the diagonal: -cl (p phi_0) */
+        double pl = (P->bc_left == ORC_BC_WALL) ? -1.0 : 1.0;
+        double pr = (P->bc_right == ORC_BC_WALL) ? -1.0 : 1.0;
+        di[0] += lo[0] * pl;
+        di[n - 1] += up[n - 1] * pr;
+        st = (st == ORC_OK) ? orc_thomas(n, lo, di, up, rhs, phi) : st;
+    } else {
+        st = (st == ORC_OK) ? (n >= 3 ? orc_cyclic_thomas(n, lo, di, up, rhs, phi) : ORC_E_INVALID) : st;
+    }
+    for (int i = 0; i < n; i++) {
+        Lh[i] = -(Fh[i + 1] - Fh[i]) / dx;
+        Lq[i] = -(Fq[i + 1] - Fq[i]) / dx + XS(eh, i) * phi[i];
+    }
+#undef XS
+    free(phi);
+    free(buf);
+    return st;
+}
+
+int orc_sgn_rhs(const orc_problem *P, const double *h, const double *q, double *Lh, double *Lq)
+{
+    return sgn_L(P, h, q, Lh, Lq);
+}
+
+/* One SGN step: stages 1 forward Euler, 2 Heun; then the optional A19
+ * filter (q only is a field of this model; W is carried). */
+int orc_sgn_step(const orc_problem *P, int stages, double dt, double *h, double *q)
+{
+    if (stages != 1 && stages != 2) return ORC_E_INVALID;
+    const int n = P->n;
+    double *buf = (double *)malloc(sizeof(double) * (size_t)n * 6);
+    if (!buf) return ORC_E_INVALID;
+    double *h0 = buf, *q0 = h0 + n, *h1 = q0 + n, *q1 = h1 + n, *Lh = q1 + n, *Lq = Lh + n;
+    memcpy(h0, h, sizeof(double) * (size_t)n);
+    memcpy(q0, q, sizeof(double) * (size_t)n);
+    int st = sgn_L(P, h0, q0, Lh, Lq);
+    if (st == ORC_OK) {
+        for (int i = 0; i < n; i++) { h1[i] = h0[i] + dt * Lh[i]; q1[i] = q0[i] + dt * Lq[i]; }
+        if (stages == 1) {
+            memcpy(h, h1, sizeof(double) * (size_t)n);
+            memcpy(q, q1, sizeof(double) * (size_t)n);
+        } else {
+            st = sgn_L(P, h1, q1, Lh, Lq);
+            if (st == ORC_OK)
+                for (int i = 0; i < n; i++) {
+                    h[i] = 0.5 * h0[i] + 0.5 * (h1[i] + dt * Lh[i]);
+                    q[i] = 0.5 * q0[i] + 0.5 * (q1[i] + dt * Lq[i]);
+                }
+        }
+    }
+    if (st == ORC_OK)
+        for (int i = 0; i < n; i++)
+            if (!(h[i] > P->h_min)) st = ORC_E_DRY;
+    if (st == ORC_OK && P->filter_sigma > 0.0 && (P->filter_mask & 2)) {
+        double *U[4] = {h, q, NULL, NULL};
+        orc_problem Pq = *P;
+        Pq.filter_mask = 2;             /* q only */
+        st = apply_filter(&Pq, U);
+    }
+    free(buf);
+    return st;
+}
+
+/* dt = CFL_SGN dx / max_i (|u_i| + sqrt(g h_i)) */
+int orc_sgn_dt(const orc_problem *P, double cfl, const double *h, const double *q, double *dt)
+{
+    double s = 0.0;
+    for (int i = 0; i < P->n; i++) {
+        if (!(h[i] > P->h_min)) return ORC_E_DRY;
+        double v = fabs(q[i] / h[i]) + sqrt(P->g * h[i]);
+        if (v > s) s = v;
+    }
+    if (!(cfl > 0.0)) return ORC_E_INVALID;
+    *dt = cfl * P->dx / s;
+    return ORC_OK;
+}
+
+int orc_sgn_run(const orc_problem *P, int stages, double cfl, double dt_fixed, double t0,
+                double t_end, int64_t max_steps, double *h, double *q, double *t_out,
+                int64_t *steps_out)
+{
+    double t = t0;
+    int64_t s = 0;
+    int st = ORC_OK;
+    int use_tend = (t_end > t0);
+    while (s < max_steps) {
+        if (use_tend && !(t < t_end)) break;
+        double dt;
+        if (dt_fixed > 0.0) dt = dt_fixed;
+        else {
+            st = orc_sgn_dt(P, cfl, h, q, &dt);
+            if (st != ORC_OK) break;
+        }
+        if (use_tend && t + dt >= t_end) dt = t_end - t;
+        st = orc_sgn_step(P, stages, dt, h, q);
+        if (st != ORC_OK) break;
+        t = (use_tend && dt == t_end - t) ? t_end : t + dt;
+        s++;
+    }
+    if (t_out) *t_out = t;
+    if (steps_out) *steps_out = s;
+    return st;
+}
+
 /* total mass sum_i h_i dx */
 double orc_mass(int n, double dx, const double *h)
 {

@@ -102,6 +102,15 @@ def lib():
             L.orc_explicit_run.restype = C.c_int
             L.orc_explicit_run.argtypes = [P, C.c_int, C.c_double, C.c_double, C.c_double,
                                            C.c_double, C.c_int64] + [dp] * 5 + [C.POINTER(C.c_int64)]
+            L.orc_sgn_rhs.restype = C.c_int
+            L.orc_sgn_rhs.argtypes = [P] + [dp] * 4
+            L.orc_sgn_step.restype = C.c_int
+            L.orc_sgn_step.argtypes = [P, C.c_int, C.c_double, dp, dp]
+            L.orc_sgn_dt.restype = C.c_int
+            L.orc_sgn_dt.argtypes = [P, C.c_double, dp, dp, dp]
+            L.orc_sgn_run.restype = C.c_int
+            L.orc_sgn_run.argtypes = [P, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.c_int64, dp, dp, dp, C.POINTER(C.c_int64)]
             L.orc_mass.restype = C.c_double
             L.orc_mass.argtypes = [C.c_int, C.c_double, dp]
             _lib = L
@@ -226,6 +235,44 @@ class Oracle:
                                      *[_p(a) for a in U], C.byref(tout), C.byref(sout))
         if st != OK:
             raise OracleError(st, f"explicit_run (after {sout.value} steps)")
+        return U, tout.value, sout.value
+
+
+    # -- classical SGN scheme -----------------------------------
+    def sgn_rhs(self, h, q):
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        Lh, Lq = np.empty(self.P.n), np.empty(self.P.n)
+        st = self.L.orc_sgn_rhs(C.byref(self.P), _p(h), _p(q), _p(Lh), _p(Lq))
+        if st != OK:
+            raise OracleError(st, "sgn_rhs")
+        return Lh, Lq
+
+    def sgn_step(self, U, dt, stages=2):
+        """One SGN step on (h, q[, K, W]); K, W are carried unchanged."""
+        U = [np.array(a, dtype=np.float64, copy=True) for a in U]
+        st = self.L.orc_sgn_step(C.byref(self.P), stages, dt, _p(U[0]), _p(U[1]))
+        if st != OK:
+            raise OracleError(st, "sgn_step")
+        return U
+
+    def sgn_dt(self, U, cfl):
+        h, q = [np.ascontiguousarray(a, dtype=np.float64) for a in U[:2]]
+        d = C.c_double()
+        st = self.L.orc_sgn_dt(C.byref(self.P), cfl, _p(h), _p(q), C.byref(d))
+        if st != OK:
+            raise OracleError(st, "sgn_dt")
+        return d.value
+
+    def sgn_run(self, U, cfl=0.9, stages=2, steps=None, t0=0.0, t_end=None, dt_fixed=0.0):
+        U = [np.array(a, dtype=np.float64, copy=True) for a in U]
+        tout, sout = C.c_double(), C.c_int64()
+        max_steps = steps if steps is not None else (1 << 62)
+        te = t_end if t_end is not None else t0 - 1.0
+        st = self.L.orc_sgn_run(C.byref(self.P), stages, cfl, dt_fixed, t0, te, max_steps,
+                                _p(U[0]), _p(U[1]), C.byref(tout), C.byref(sout))
+        if st != OK:
+            raise OracleError(st, f"sgn_run (after {sout.value} steps)")
         return U, tout.value, sout.value
 
 

@@ -173,3 +173,30 @@ def explicit_max_growth(dx, h0, lam, g, dt, order=2, stages=2, filter_sigma=0.0,
         thetas = np.linspace(1e-3, np.pi, 600)
     return max(np.max(np.abs(np.linalg.eigvals(explicit_symbol(th, dx, h0, lam, g, dt, order, stages,
                                                                filter_sigma)))) for th in thetas)
+
+
+def sgn_symbol(theta, dx, h0, g, dt, order=2, stages=2):
+    """2x2 amplification matrix over (h, q) of one step of the classical SGN
+    scheme (reading A23) about rest.  Shallow-water part: Rusanov
+    on MUSCL faces with alpha = sqrt(g h0) at rest (linear dissipation), flux
+    Jacobian [[0, 1], [g h0, 0]]; face-state symbols sm = 1 + (e - 1/e)/4,
+    sp = e - (e^2 - 1)/4 (order 1: 1, e).  phi: h0 phi - (h0^3/(3 dx^2)) d2 phi
+    = h*, h* = -(g h0^3/(6 dx^3)) [(e^2 - 2e + 1) - (1 - 2/e + 1/e^2)] h'
+    (the (u_x)^2 terms are quadratic).  L = (-(1 - 1/e)/dx Fh, -(1 - 1/e)/dx Fq
+    + h0 phi)."""
+    e = np.exp(1j * theta)
+    if order == 2:
+        sm = 1 + (e - 1 / e) / 4
+        sp = e - (e * e - 1) / 4
+    else:
+        sm, sp = 1.0, e
+    c0 = np.sqrt(g * h0)
+    J = np.array([[0, 1], [g * h0, 0]], dtype=complex)
+    F = 0.5 * J * (sm + sp) - 0.5 * c0 * (sp - sm) * np.eye(2)
+    D = (1 - 1 / e) / dx
+    hstar = -(g * h0 ** 3 / (6 * dx ** 3)) * ((e * e - 2 * e + 1) - (1 - 2 / e + 1 / (e * e)))
+    phi = hstar / (h0 - (h0 ** 3 / (3 * dx * dx)) * (e - 2 + 1 / e))
+    A = -D * F
+    A[1, 0] += h0 * phi
+    I = np.eye(2, dtype=complex)
+    return I + dt * A if stages == 1 else I + dt * A + 0.5 * (dt * A) @ (dt * A)

@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "fp64 cell-stage updates/s (whole job)"
 UNIT = "cell-stage/s"
 CFL_EX = 0.4          # explicit scheme CFL
+CFL_SGN = 0.9         # classical SGN scheme CFL
 B_STAGE1 = 64   # algorithmic bytes per cell: read U^n (32), write U1 (32)
 B_STAGE2 = 96   # read U^n + U1 (64), write U^{n+1} (32)
 
@@ -51,9 +52,10 @@ def parse():
     p.add_argument("--si-order", type=int, default=2, choices=[1, 2],
                    help="2: the paper's second-order SI step (headline); 1: first-order SI "
                         "(one implicit stage tau = dt, order-1 faces; SURVEY row f2)")
-    p.add_argument("--scheme", default="si", choices=["si", "explicit"],
+    p.add_argument("--scheme", default="si", choices=["si", "explicit", "sgn"],
                    help="si: the SI-IMEX step (headline); explicit: the explicit hSGN scheme "
-                        "(Heun, CFL_EX 0.4) on the same workload")
+                        "(Heun, CFL_EX 0.4); sgn: the classical SGN scheme (Heun, CFL_SGN 0.9) "
+                        "on the same workload")
     p.add_argument("--persistent", type=int, default=-1,
                    help="1: persistent per-stage kernels, 0: one CTA per tile, -1: library default")
     p.add_argument("--fused", type=int, default=-1,
@@ -70,6 +72,12 @@ def config_dict(a, world):
         d["scheme"] = "first-order SI (P:500-517: one implicit stage, tau = dt, order-1 faces)"
         d["order"] = 1
         d["tableau"] = "SI Euler (a_11 = 1)"
+    if a.scheme == "sgn":
+        d["scheme"] = "classical SGN (P:519-600): Heun, CFL_SGN 0.9, MUSCL + Rusanov, phi tridiagonal"
+        d.pop("cfl_imex", None)
+        d.pop("mcfl", None)
+        d.pop("tableau", None)
+        d["filter"] = "none"
     if a.scheme == "explicit":
         d["scheme"] = "explicit hSGN (P:442-480): Heun, CFL_EX 0.4, MUSCL + Rusanov, A19 filter"
         d.pop("cfl_imex", None)
@@ -177,12 +185,15 @@ def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False,
     until at least min_seconds of wall time; returns (rate, seconds, repeats)."""
     from oracle import oracle as O
     tab = O.euler_tableau() if si_order == 1 else None
+    sig = 0.0 if explicit == "sgn" else w.filter_sigma
     jobs = [(O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, b=w.b, order=si_order,
-                      filter_sigma=w.filter_sigma, tableau=tab), w.state(m)) for m in members]
+                      filter_sigma=sig, tableau=tab), w.state(m)) for m in members]
     t0 = time.perf_counter()
     reps = 0
     while True:
-        if explicit:
+        if explicit == "sgn":
+            O.run_members(jobs, threads=threads, sgn=True, cfl=CFL_SGN, steps=steps)
+        elif explicit:
             O.run_members(jobs, threads=threads, explicit=True, cfl=CFL_EX, steps=steps)
         else:
             O.run_members(jobs, threads=threads, cfl=w.cfl, mcfl=w.mcfl, steps=steps)
@@ -280,6 +291,12 @@ def main():
             raise SystemExit("--scheme explicit: cfg3 only (the explicit scheme needs a flat bottom)")
         s.set_params(w.g, w.lam, CFL_EX, 0.0)
         s.set_scheme("explicit", 2)
+    if a.scheme == "sgn":
+        if a.config != "cfg3":
+            raise SystemExit("--scheme sgn: cfg3 only (flat bottom)")
+        s.set_filter(0.0)
+        s.set_params(w.g, w.lam, CFL_SGN, 0.0)
+        s.set_scheme("sgn", 2)
     if a.fused >= 0:
         s.set_fused(bool(a.fused))
     if a.persistent >= 0:
@@ -334,6 +351,10 @@ def main():
     t1 = ms1 / a.steps / 1e3
     bs1 = B_STAGE1 + (8 if bathy else 0)    # + b read per stage
     bs2 = (B_STAGE1 if nst == 1 else B_STAGE2) + (8 if bathy else 0)
+    if a.scheme == "sgn":
+        # (h, q) only: stage 1 reads X, writes U1 (32 B); stage 2 reads U1, U^n,
+        # writes U^{n+1} (48 B) + carries K, W (32 B)
+        bs1, bs2 = 32, 80
     ach2 = bs2 * Ntot / t2 / 1e9
     ach1 = bs1 * Ntot / t1 / 1e9
     traffic = profile_traffic(Ntot)
@@ -371,9 +392,11 @@ def main():
         threads = os.cpu_count() or 1
         nm = max(4 * threads, 16)
         rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0,
-                                           explicit=a.scheme == "explicit", si_order=a.si_order)
+                                           explicit="sgn" if a.scheme == "sgn" else a.scheme == "explicit",
+                                           si_order=a.si_order)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"first {nm} cfg3 members x 10 {'explicit Heun' if a.scheme == 'explicit' else 'SI'} "
+               "sample": f"first {nm} cfg3 members x 10 "
+                         f"{ {'explicit': 'explicit Heun', 'sgn': 'classical SGN Heun'}.get(a.scheme, 'SI')} "
                          f"steps, repeated {reps}x ({secs:.1f} s wall)"}
 
     line = {
@@ -384,7 +407,8 @@ def main():
         "per_gpu": value / world,
         "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s",
                      "frac": ach2 / peak, "traffic": traffic,
-                     "kernel": ("explicit_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "explicit"
+                     "kernel": ("sgn_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "sgn"
+                                else "explicit_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "explicit"
                                 else "stage_kernel<FINAL> (the one SI stage)" if nst == 1
                                 else "stage_kernel<STAGE2,FINAL> (stage 2)"),
                      "bytes_model": (f"{bs2} B/cell per launch (read U^n; write U^{{n+1}})" if nst == 1 else

@@ -226,6 +226,15 @@ int32_t hsgn_get_fused(const hsgn_ctx *ctx);
  * otherwise).  Errors: HSGN_E_INVALID (unknown scheme, stages not 1 or 2). */
 #define HSGN_SCHEME_SI 0
 #define HSGN_SCHEME_EXPLICIT 1
+/* HSGN_SCHEME_SGN: the classical SGN equations in elliptic-hyperbolic form
+ * on (h, q) -- Rusanov shallow water on MUSCL
+ * faces with alpha = max(|u| + sqrt(g h)), a tridiagonal phi system per stage
+ * (reading A23: g h^3 in h*), source h phi; Euler or Heun;
+ * dt = CFL dx / max(|u| + sqrt(g h)); K, W are carried unchanged.
+ * Flat bottom, no filter, no relaxation zones or slabs.  The phi overlap is
+ * chosen from the state (hsgn_set_state / hsgn_set_scheme); HSGN_E_INVALID if
+ * dx is too small against h for the tile width. */
+#define HSGN_SCHEME_SGN 2
 hsgn_status hsgn_set_scheme(hsgn_ctx *ctx, int32_t scheme, int32_t stages);
 /* Per-stage kernels as persistent CTAs: each CTA walks
  * (tile, member) items and prefetches the next item's inputs by TMA while it

@@ -317,13 +317,15 @@ def mass(h, dx):
     return lib().orc_mass(len(h), dx, _p(h))
 
 
-def run_members(members, threads=None, explicit=False, **kw):
+def run_members(members, threads=None, explicit=False, sgn=False, **kw):
     """Run independent ensemble members on host threads (ctypes releases the GIL).
     members: list of (Oracle, U).  Returns list of results of Oracle.run (or of
     Oracle.explicit_run with explicit=True)."""
     from concurrent.futures import ThreadPoolExecutor
     threads = threads or os.cpu_count() or 1
     with ThreadPoolExecutor(max_workers=threads) as ex:
+        if sgn:
+            return list(ex.map(lambda m: m[0].sgn_run(m[1], **kw), members))
         if explicit:
             return list(ex.map(lambda m: m[0].explicit_run(m[1], **kw), members))
         return list(ex.map(lambda m: m[0].run(m[1], **kw), members))

@@ -79,6 +79,8 @@ struct hsgn_ctx {
     // scheme: 0 = SI-IMEX (default), 1 = explicit hSGN (P:442-480,
     // x_stages 1 = Euler, 2 = Heun) on tiles of xT cells
     int scheme = 0, x_stages = 2, xT = 0, xtiles = 0;
+    // classical SGN (scheme 2): phi-system overlap and tiles, from the state
+    int sw = 0, sT = 0, stiles = 0;
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
     bool persist = false;
     int persist_grid = 0;
@@ -137,6 +139,11 @@ Params make_params(hsgn_ctx *c, long long k)
         P.T = c->xT;
         P.tiles = c->xtiles;
         P.mcfl = 0.0;
+    } else if (c->scheme == 2) {     // classical SGN: phi tiles, dt = CFL_SGN dx / max(|u| + sqrt(g h))
+        P.T = c->sT;
+        P.tiles = c->stiles;
+        P.w = c->sw;
+        P.mcfl = 0.0;
     }
     P.inv_tiles = 1.0 / double(c->tiles);
     for (int k = 0; k < 9; k++) {
@@ -194,7 +201,27 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
     }
     hsgn_status st;
     if (ev) CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
-    if (c->scheme == 1) {
+    if (c->scheme == 2) {
+        dim3 grid(c->stiles, c->members);
+        if (c->x_stages == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            sgn_kernel<false, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
+            c->launches++;
+            CUDA_TRY(c, cudaGetLastError());
+            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            sgn_kernel<false, false><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
+            c->launches++;
+            CUDA_TRY(c, cudaGetLastError());
+            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            sgn_kernel<true, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
+            c->launches++;
+            CUDA_TRY(c, cudaGetLastError());
+        }
+        if (ev) CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+    } else if (c->scheme == 1) {
         dim3 grid(c->xtiles, c->members);
         const bool filt = c->filter_sigma > 0.0;
         if (c->x_stages == 1) {
@@ -340,8 +367,11 @@ hsgn_status ready(hsgn_ctx *c)
     if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
     if (!c->have_params) return fail(c, HSGN_E_INVALID, "hsgn_set_params not called");
     if (!c->have_state) return fail(c, HSGN_E_INVALID, "hsgn_set_state not called");
-    if (c->scheme == 1 && (c->bathy || c->slab || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
-        return fail(c, HSGN_E_INVALID, "explicit scheme: flat bottom, no relaxation zones, no slabs");
+    if (c->scheme != 0 && (c->bathy || c->slab || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
+        return fail(c, HSGN_E_INVALID, "explicit / SGN schemes: flat bottom, no relaxation zones, no slabs");
+    if (c->scheme == 2 && c->filter_sigma > 0.0)
+        return fail(c, HSGN_E_INVALID, "SGN scheme: no A19 filter (its Rusanov speed includes sqrt(g h))");
+    if (c->scheme == 2 && c->sT <= 0) return fail(c, HSGN_E_INVALID, "SGN geometry not set");
     return HSGN_OK;
 }
 
@@ -383,7 +413,7 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
                 cudaGraphDestroy(gr);
             }
             CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
-            const int kpl = c->scheme == 1 ? c->x_stages : (c->fused ? 1 : c->tab.stages);
+            const int kpl = c->scheme != 0 ? c->x_stages : (c->fused ? 1 : c->tab.stages);
             c->launches += GRAPH_STEPS * (kpl + 1);
             done += GRAPH_STEPS;          // even: cur unchanged
             c->host_steps += GRAPH_STEPS;
@@ -564,6 +594,59 @@ hsgn_status reconcile(hsgn_ctx *c, unsigned int *bits_out = nullptr)
 
 }  // namespace
 
+// Classical SGN (scheme 2): overlap of the phi system from the state.  Rows
+// are normalised by h_i, so the off-diagonals are c_{i+-1/2}/h_i <= h_max^3 /
+// (3 dx^2 h_min) =: rho; w from the decay bound r^w <= 2^-60 with a 1.25
+// margin on rho (the kernel re-checks with its own rho), tiles of up to
+// SLCAP - 2 - 2w kept cells (h_min, h_max from a reduction of the state).
+hsgn_status sgn_geometry(hsgn_ctx *c)
+{
+    dim3 grid(c->tiles, c->members);
+    reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[c->cur][0], c->buf[c->cur][1], c->buf[c->cur][2],
+                                              nullptr, c->lamd, c->n, c->T, c->g, c->partials, nullptr,
+                                              c->members, 2);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    std::vector<double> part(size_t(c->members) * c->tiles * 4);
+    CUDA_TRY(c, cudaMemcpyAsync(part.data(), c->partials, part.size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    double hmin = 1e300, hmax = 0.0;
+    for (size_t i = 0; i < part.size(); i += 4) {
+        hmin = std::min(hmin, part[i + 1]);
+        hmax = std::max(hmax, part[i + 2]);
+    }
+    if (!(hmin > 0.0)) return fail(c, HSGN_E_DRY, "SGN geometry: non-positive depth");
+    const double rho = 1.25 * hmax * hmax * hmax / (3.0 * c->dx * c->dx * hmin);
+    const double r = 2.0 * rho / (1.0 + 2.0 * rho + std::sqrt(1.0 + 4.0 * rho));
+    int w = int(std::ceil(41.588830833596716 / -std::log(r))) + 4;
+    w = ((w + 7) / 8) * 8;
+    const int maxT = SLCAP - 2 - 2 * w;
+    if (maxT < 16)
+        return fail(c, HSGN_E_INVALID, "SGN: phi decay length too long for the tile (dx too small vs h)");
+    const int ntiles = (c->n + maxT - 1) / maxT;
+    c->sw = w;
+    c->sT = (c->n + ntiles - 1) / ntiles;
+    c->stiles = (c->n + c->sT - 1) / c->sT;
+    return HSGN_OK;
+}
+
+// Re-seed the dt maxima slot of the next step from the current state (after
+// a scheme change: the SGN celerity differs from the hSGN one).
+hsgn_status reseed_maxima(hsgn_ctx *c)
+{
+    const int slot = int(c->host_steps % 3);
+    unsigned long long *mx = c->maxes + size_t(slot) * 2 * c->members;
+    CUDA_TRY(c, cudaMemsetAsync(mx, 0, 2 * size_t(c->members) * 8, c->stream));
+    dim3 grid(c->tiles, c->members);
+    reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[c->cur][0], c->buf[c->cur][1], c->buf[c->cur][2],
+                                              c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
+                                              c->partials, mx, c->members, c->scheme == 2);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    return HSGN_OK;
+}
+
 extern "C" {
 
 const char *hsgn_status_string(hsgn_status s)
@@ -634,6 +717,9 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_pkernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(sgn_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
+    cudaFuncSetAttribute(sgn_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
+    cudaFuncSetAttribute(sgn_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
@@ -829,12 +915,13 @@ hsgn_status hsgn_set_state(hsgn_ctx *c, const double *h, const double *q, const 
     dim3 grid(c->tiles, c->members);
     reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[0][0], c->buf[0][1], c->buf[0][2],
                                               c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
-                                              c->partials, c->maxes, c->members);
+                                              c->partials, c->maxes, c->members, c->scheme == 2);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // tv must outlive the copy
     c->host_steps = 0;
     c->have_state = true;
+    if (c->scheme == 2) return sgn_geometry(c);
     return HSGN_OK;
 }
 
@@ -969,7 +1056,7 @@ hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
     dim3 grid(c->tiles, c->members);
     reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[c->cur][0], c->buf[c->cur][1], c->buf[c->cur][2],
                                               c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
-                                              c->partials, nullptr, c->members);
+                                              c->partials, nullptr, c->members, 0);
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     std::vector<double> part(size_t(c->members) * c->tiles * 4), tv(c->members), dv(c->members);
@@ -1022,17 +1109,27 @@ int32_t hsgn_get_fused(const hsgn_ctx *c) { return c ? (c->fused ? 1 : 0) : -1; 
 hsgn_status hsgn_set_scheme(hsgn_ctx *c, int32_t scheme, int32_t stages)
 {
     if (!c) return HSGN_E_INVALID;
+    const int prev = c->scheme;
     if (scheme == HSGN_SCHEME_SI) {
         c->scheme = 0;
-    } else if (scheme == HSGN_SCHEME_EXPLICIT) {
+    } else if (scheme == HSGN_SCHEME_EXPLICIT || scheme == HSGN_SCHEME_SGN) {
         if (stages != 1 && stages != 2) return fail(c, HSGN_E_INVALID, "explicit stages must be 1 or 2");
-        c->scheme = 1;
+        c->scheme = scheme == HSGN_SCHEME_EXPLICIT ? 1 : 2;
         c->x_stages = stages;
     } else {
         return fail(c, HSGN_E_INVALID, "unknown scheme");
     }
     drop_graphs(c);
     choose_geometry(c);
+    if (c->have_state && c->ws) {
+        hsgn_status st = reconcile(c);
+        if (st != HSGN_OK) return st;
+        if ((prev == 2) != (c->scheme == 2)) {
+            st = reseed_maxima(c);      // the SGN celerity differs from hSGN's
+            if (st != HSGN_OK) return st;
+        }
+        if (c->scheme == 2) return sgn_geometry(c);
+    }
     return HSGN_OK;
 }
 

@@ -1764,6 +1764,284 @@ __global__ void __launch_bounds__(XNT) explicit_kernel(const Params P, const Buf
 }
 
 // ---------------------------------------------------------------------------
+// Classical SGN scheme, flat bottom, on (h, q):
+//   L_h = -D^_x(q),  L_q = -D^_x(q u + g h^2/2) + h phi,
+//   h phi - (1/(3dx^2)) (c_{i+1/2}(phi_{i+1} - phi_i) - c_{i-1/2}(phi_i - phi_{i-1})) = h*,
+// c = h_{i+1/2}^3 (h_{i+1/2} = (h_i + h_{i+1})/2), h* of P:591 with g h^3 (A23);
+// Rusanov with alpha = max(|u| + sqrt(g h)) on MUSCL faces (A23).  K, W carried.
+//
+// sgn_kernel<HEUN2, FINAL>: tiles of ST kept cells with an overlap of w rows
+// for the phi system (an M-matrix like the SI depth system: the same
+// truncation argument and per-CTA decay check); SNT
+// threads own MCH-row chunks (partition method in registers, PCR on the SNT
+// chunk ends in shared memory).  The phi decay length is ~h/sqrt(3), so w is
+// ~ 40 (h/dx): the tile is 5 x 512 rows.
+// ---------------------------------------------------------------------------
+constexpr int SNT = 512;
+constexpr int SLCAP = SNT * MCH;                 // 2560 rows
+constexpr int SROWS_S = SLCAP + 16;
+// shared: h, q (stencil input, rows -2-? .. L+?), staged outputs h, q, PCR 2 x 3 x SNT
+constexpr size_t SSMEM_BYTES = (size_t(4) * SROWS_S + size_t(6) * SNT) * sizeof(double);
+
+template <bool HEUN2, bool FINAL>
+__global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs B)
+{
+    __shared__ double xw[SNT / 32][3];
+    __shared__ float rw[SNT / 32];
+    __shared__ double rd[2][SNT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int j = blockIdx.x, m = blockIdx.y;
+    const int n = P.n;
+    const size_t mo = size_t(m) * n;
+    Geom G = stage_geom(P, j * P.T, min(n, j * P.T + P.T), P.w);
+    const int start = G.start, L = G.L;
+    double *const smem = dyn_smem();
+    double *sh = smem + 4, *sq = sh + SROWS_S;                  // rows -4 .. L+3 (shift 4)
+    double *oh = smem + 2 * SROWS_S, *oq = oh + SROWS_S;        // staged outputs
+    double *pcr0 = smem + 4 * SROWS_S, *pcr1 = pcr0 + 3 * SNT;
+    const double *const *X = HEUN2 ? B.U1 : B.Un;
+    // ---- load rows -4 .. L+3 of (h, q) of X (q parity at wall ghosts) ---------
+    for (int r = tid - 4; r < L + 4; r += SNT) {
+        double par;
+        const size_t gi = mo + size_t(map_cell(start + r, n, P.bcl, P.bcr, par));
+        sh[r] = X[0][gi];
+        sq[r] = par * X[1][gi];
+    }
+    const unsigned int err0 = *((volatile unsigned int *)P.err);
+    const double dtm = P.dt[m];
+    __syncthreads();
+    if (err0) return;
+    const double g = P.g, dx = P.dx, idx = P.idx;
+    const double c3 = 1.0 / (3.0 * dx * dx);
+    const double s6 = 1.0 / (6.0 * dx * dx * dx);
+    const double kap = P.order == 2 ? 0.25 : 0.0;
+    double umax = 0.0, numax = 0.0, rho_loc = 0.0;
+    unsigned int errbits = 0u;
+    const int r0 = tid * MCH;
+    double phi[MCH];
+    // ---- phi system on own rows (normalised by h_i), partition solve --------
+    {
+        // windows: h, u over rows r0-2 .. r0+MCH+1
+        double wh[MCH + 4], wu[MCH + 4];
+#pragma unroll
+        for (int k = 0; k < MCH + 4; k++) {
+            const int rr = min(r0 - 2 + k, L + 3);
+            wh[k] = sh[rr];
+            wu[k] = sq[rr] * rcp(wh[k]);
+        }
+        double am[MCH], cm[MCH], dm[MCH];
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            const double h0 = wh[i + 2], hp = wh[i + 3], hm = wh[i + 1];
+            const double hl = 0.5 * (hm + h0), hr = 0.5 * (h0 + hp);
+            const double ih0 = rcp(h0);
+            double rl = hl * hl * hl * c3 * ih0, rr = hr * hr * hr * c3 * ih0;
+            const double hp3 = hp * hp * hp, hm3 = hm * hm * hm;
+            const double up2 = wu[i + 4] - wu[i + 2], um2 = wu[i + 2] - wu[i];
+            double rhs = -s6 * (g * hp3 * (wh[i + 4] - 2.0 * hp + h0) + 0.5 * hp3 * up2 * up2
+                                - g * hm3 * (h0 - 2.0 * hm + wh[i]) - 0.5 * hm3 * um2 * um2) * ih0;
+            double dg = 1.0 + rl + rr;
+            // tile ends: truncated (overlap) or physical (phi ghost = p phi_0, A23)
+            if (r == 0) {
+                if (G.left_phys) dg -= rl * (P.bcl == BC_WALL ? -1.0 : 1.0);
+                rl = 0.0;
+            }
+            if (r == L - 1) {
+                if (G.right_phys) dg -= rr * (P.bcr == BC_WALL ? -1.0 : 1.0);
+                rr = 0.0;
+            }
+            if (r >= L) { rl = 0.0; rr = 0.0; dg = 1.0; rhs = 0.0; }
+            rho_loc = rr > rho_loc ? rr : rho_loc;
+            const double a = -rl, c = -rr;
+            if (i == 0) {
+                const double inv = rcp(dg);
+                am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
+            } else {
+                const double inv = rcp(dg - a * cm[i - 1]);
+                am[i] = -a * am[i - 1] * inv;
+                cm[i] = c * inv;
+                dm[i] = (rhs - a * dm[i - 1]) * inv;
+            }
+        }
+        const double aE = am[MCH - 1], cE = cm[MCH - 1], dE = dm[MCH - 1];
+        double Pn = 0.0, Qn = 0.0, Rn = -1.0;
+#pragma unroll
+        for (int i = MCH - 2; i >= 0; i--) {
+            const double Pi = dm[i] - cm[i] * Pn;
+            const double Qi = am[i] - cm[i] * Qn;
+            const double Ri = -cm[i] * Rn;
+            dm[i] = Pi; am[i] = Qi; cm[i] = Ri;
+            Pn = Pi; Qn = Qi; Rn = Ri;
+        }
+        double P1 = __shfl_down_sync(0xffffffffu, dm[0], 1);
+        double Q1 = __shfl_down_sync(0xffffffffu, am[0], 1);
+        double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
+        if (lane == 0) { xw[wid][0] = dm[0]; xw[wid][1] = am[0]; xw[wid][2] = cm[0]; }
+        __syncthreads();
+        if (lane == 31) {
+            if (wid + 1 < SNT / 32) { P1 = xw[wid + 1][0]; Q1 = xw[wid + 1][1]; R1 = xw[wid + 1][2]; }
+            else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
+        }
+        double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1;
+        if (tid == 0) A_ = 0.0;
+        {
+            const double ib = rcp(1.0 - cE * Q1);
+            A_ *= ib; C_ *= ib; D_ *= ib;
+        }
+        double *cur = pcr0, *nxt = pcr1;
+        cur[tid] = A_; cur[SNT + tid] = C_; cur[2 * SNT + tid] = D_;
+        {
+            const float ea = float(fabs(A_)), ec = float(fabs(C_));
+            const float ev = warp_max_nonneg(ea > ec ? ea : ec);
+            if (lane == 0) rw[wid] = ev;
+        }
+        __syncthreads();
+        int lim = SNT;
+        {
+            float e0 = 0.0f;
+#pragma unroll
+            for (int q = 0; q < SNT / 32; q++) e0 = fmaxf(e0, rw[q]);
+            if (e0 < 0.4f) {
+                float ee = e0 * 1.1f;
+                int sdl = 1;
+                while (sdl < SNT && ee > 5.42e-20f) { ee = ee * ee * 1.1f; sdl <<= 1; }
+                lim = sdl;
+            }
+        }
+#pragma unroll 1
+        for (int sd = 1; sd < lim; sd <<= 1) {
+            const int km = tid - sd, kp = tid + sd;
+            double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
+            if (km >= 0) { Am = cur[km]; Cm = cur[SNT + km]; Dm = cur[2 * SNT + km]; }
+            if (kp < SNT) { Ap = cur[kp]; Cp = cur[SNT + kp]; Dp = cur[2 * SNT + kp]; }
+            const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
+            const double An = -A_ * Am * ib;
+            const double Cn = -C_ * Cp * ib;
+            const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
+            A_ = An; C_ = Cn; D_ = Dn;
+            nxt[tid] = A_; nxt[SNT + tid] = C_; nxt[2 * SNT + tid] = D_;
+            __syncthreads();
+            double *tmp = cur; cur = nxt; nxt = tmp;
+        }
+        const double Xk = D_;
+        double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
+        if (lane == 31) xw[wid][0] = Xk;
+        __syncthreads();
+        if (lane == 0) XL = (wid > 0) ? xw[wid - 1][0] : 0.0;
+#pragma unroll
+        for (int i = 0; i < MCH; i++) phi[i] = (i == MCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
+    }
+    // ---- shallow-water update of own kept rows ----------------------------------
+    {
+        double wh[3], wq[3], wH[3], wW[3];     // (H, W unused: zero, keep the MUSCL helpers)
+#pragma unroll
+        for (int k = 0; k < 3; k++) { wh[k] = sh[r0 - 2 + k]; wq[k] = sq[r0 - 2 + k]; wH[k] = 0.0; wW[k] = 0.0; }
+        FState Mm = muscl_minus(wh, wq, wH, wW, kap);
+#pragma unroll
+        for (int k = 0; k < 2; k++) { wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; }
+        wh[2] = sh[min(r0 + 1, L + 3)]; wq[2] = sq[min(r0 + 1, L + 3)];
+        FState Pn, Mr;
+        muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);
+        // Rusanov for the shallow-water fluxes: 2F with alpha = max(|u| + sqrt(g h))
+        auto face = [&](const FState &a, const FState &b, double &Fh, double &Fq) {
+            const double sa = fabs(a.u) + fsqrt(g * a.h), sb = fabs(b.u) + fsqrt(g * b.h);
+            const double al = sa > sb ? sa : sb;
+            Fh = (a.q + b.q) - al * (b.h - a.h);
+            Fq = fma(a.q, a.u, fma(b.q, b.u, 0.5 * g * (a.h * a.h + b.h * b.h))) - al * (b.q - a.q);
+        };
+        double Fhl, Fql;
+        face(Mm, Pn, Fhl, Fql);
+        const double hidx = 0.5 * idx;
+#pragma unroll
+        for (int i = 0; i < MCH; i++) {
+            const int r = r0 + i;
+            const double hc = wh[1], qc = wq[1];
+#pragma unroll
+            for (int k = 0; k < 2; k++) { wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; }
+            const int rn = min(r + 2, L + 3);
+            wh[2] = sh[rn]; wq[2] = sq[rn];
+            FState Mn;
+            muscl_pair(wh, wq, wH, wW, kap, Pn, Mn);
+            double Fhr, Fqr;
+            face(Mr, Pn, Fhr, Fqr);
+            Mr = Mn;
+            if (r >= G.klo && r < G.khi) {
+                const double Lh = -(Fhr - Fhl) * hidx;
+                const double Lq = -(Fqr - Fql) * hidx + hc * phi[i];
+                double ho, qo;
+                if (HEUN2) {
+                    const size_t gi = mo + size_t(start + r);
+                    ho = 0.5 * B.Un[0][gi] + 0.5 * (hc + dtm * Lh);
+                    qo = 0.5 * B.Un[1][gi] + 0.5 * (qc + dtm * Lq);
+                } else {
+                    ho = hc + dtm * Lh;
+                    qo = qc + dtm * Lq;
+                }
+                if (!(ho > P.h_min)) errbits |= ERR_DRY;
+                if (!isfinite(ho + qo)) errbits |= ERR_NONFINITE;
+                oh[r - G.klo] = ho; oq[r - G.klo] = qo;
+                if (FINAL) {
+                    const double u = fabs(qo * rcp(ho));
+                    const double nu = u + fsqrt(g * ho);
+                    umax = u > umax ? u : umax;
+                    numax = nu > numax ? nu : numax;
+                }
+            }
+            Fhl = Fhr; Fql = Fqr;
+        }
+    }
+    __syncthreads();
+    {
+        const int Tk = G.khi - G.klo;
+        const size_t gdst = mo + size_t(G.start + G.klo);
+        for (int k = tid; k < Tk; k += SNT) {
+            B.out[0][gdst + k] = oh[k]; B.out[1][gdst + k] = oq[k];
+            if (FINAL) {                // K, W carried into U^{n+1} (not needed in U1)
+                B.out[2][gdst + k] = B.Un[2][gdst + k];
+                B.out[3][gdst + k] = B.Un[3][gdst + k];
+            }
+        }
+    }
+    // ---- error bits, overlap check, dt maxima, time level ---------------------
+    const unsigned int eb = __reduce_or_sync(0xffffffffu, errbits);
+    if (lane == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
+    double um = 0.0, nm = 0.0;
+    if (FINAL) { um = warp_max_nonneg(umax); nm = warp_max_nonneg(numax); }
+    const float rf = warp_max_nonneg(float(rho_loc));
+    if (lane == 0) { rd[0][wid] = um; rd[1][wid] = nm; rw[wid] = rf; }
+    __syncthreads();
+    if (tid == 0) {
+        float r = rw[0];
+        for (int q = 1; q < SNT / 32; q++) {
+            um = rd[0][q] > um ? rd[0][q] : um; nm = rd[1][q] > nm ? rd[1][q] : nm;
+            r = rw[q] > r ? rw[q] : r;
+        }
+        um = rd[0][0] > um ? rd[0][0] : um; nm = rd[1][0] > nm ? rd[1][0] : nm;
+        const int wmin = min(G.left_phys ? 1 << 30 : G.wl, G.right_phys ? 1 << 30 : G.wr);
+        if (r > 0.0f && dtm != 0.0 && wmin < (1 << 30)) {
+            const double rho = double(r) * (1.0 + 1e-6);
+            const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
+            double x = 1.0, b = rdec;
+            for (int k = wmin; k > 0; k >>= 1) { if (k & 1) x *= b; b *= b; }
+            if (x > 8.673617379884035e-19) atomicOr(P.err, ERR_OVERLAP);
+            atomicMax(P.rho_obs, (unsigned long long)__double_as_longlong(rho));
+        }
+        if (FINAL) {
+            const int members = P.members;
+            const int slot_w = (P.kslot + 1) % 3;
+            atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
+            atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
+            if (j == 0) {
+                const double tm = P.t[P.kpar * members + m];
+                const double t_end = P.ctrl->t_end;
+                P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Between steps: commit step k-1 (steps += 1 unless an error was latched) and
 // set dt of step k for every member from the max|u|, max(|u|+c) of U^k
 // (A7), clipped to t_end; free the maxima slot read at
@@ -1813,8 +2091,11 @@ __global__ void __launch_bounds__(NT) reduce_kernel(const double *__restrict__ h
                                                     const double *__restrict__ b,
                                                     const double *__restrict__ lamv, int n, int T,
                                                     double g, double *partials,
-                                                    unsigned long long *maxes, int members)
+                                                    unsigned long long *maxes, int members,
+                                                    int sgn)
 {
+    // sgn: 1 = celerity of the classical SGN scheme, sqrt(g h);
+    // 2 = as 1 with partials[2] = max h instead of max |u| (SGN tile geometry)
     __shared__ double red[NT / 32 + 1];
     __shared__ double sred[NT];
     const int j = blockIdx.x, m = blockIdx.y, tid = threadIdx.x;
@@ -1829,8 +2110,8 @@ __global__ void __launch_bounds__(NT) reduce_kernel(const double *__restrict__ h
         const double u = qq / hh, sg = H / hh / hh;
         sum += hh;
         mn = fmin(mn, hh);
-        um = fmax(um, fabs(u));
-        nm = fmax(nm, fabs(u) + sqrt(g * hh + (lam / 3.0) * sg * sg));
+        um = fmax(um, sgn == 2 ? hh : fabs(u));
+        nm = fmax(nm, fabs(u) + sqrt(g * hh + (sgn ? 0.0 : (lam / 3.0) * sg * sg)));
     }
     // deterministic tree sum
     sred[tid] = sum;

@@ -217,8 +217,9 @@ class Solver:
         self._chk(self.L.hsgn_set_fused(self.ctx, 1 if on else 0))
 
     def set_scheme(self, scheme: str = "si", stages: int = 2) -> None:
-        """"si" (IMEX) or "explicit" (stages 1 Euler, 2 Heun)."""
-        code = {"si": 0, "explicit": 1}[scheme]
+        """"si" (IMEX, P:500-517), "explicit" (hSGN, P:442-458) or "sgn" (classical
+        SGN); stages 1 Euler, 2 Heun for the last two."""
+        code = {"si": 0, "explicit": 1, "sgn": 2}[scheme]
         self._chk(self.L.hsgn_set_scheme(self.ctx, code, stages))
 
     def set_persistent(self, on: bool) -> None:

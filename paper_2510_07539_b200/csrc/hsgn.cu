@@ -227,19 +227,19 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
         if (c->x_stages == 1) {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
             if (filt) explicit_kernel<false, true, true><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
-            else explicit_kernel<false, true, false><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            else explicit_kernel<false, true, false><<<grid, XNT, XSMEM_BYTES_NF, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
             if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
         } else {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
-            explicit_kernel<false, false, false><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            explicit_kernel<false, false, false><<<grid, XNT, XSMEM_BYTES_NF, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
             if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
             if (filt) explicit_kernel<true, true, true><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
-            else explicit_kernel<true, true, false><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
+            else explicit_kernel<true, true, false><<<grid, XNT, XSMEM_BYTES_NF, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
         }

@@ -1550,7 +1550,8 @@ constexpr int XT = 1024;                 // kept cells per tile
 constexpr int XR = 4;                    // halo rows of X (filter: 2 + 2)
 constexpr int XROWS = XT + 2 * XR + 8;   // shared rows per X array (+ alignment)
 constexpr int XFROWS = XT + 8;           // shared rows of the filter arrays
-constexpr size_t XSMEM_BYTES = (size_t(4) * XROWS + 2 * size_t(XFROWS)) * sizeof(double);
+constexpr size_t XSMEM_BYTES = (size_t(4) * XROWS + 4 * size_t(XFROWS)) * sizeof(double);   // FILT
+constexpr size_t XSMEM_BYTES_NF = size_t(4) * XROWS * sizeof(double);                        // no filter
 
 // L(X) at row r of the tile (rows r-2 .. r+2 of the shared arrays).
 __device__ __forceinline__ void explicit_rhs(const double *xh, const double *xq, const double *xH,
@@ -1664,15 +1665,20 @@ __global__ void __launch_bounds__(XNT) explicit_kernel(const Params P, const Buf
         }
     } else {
     // ---- final values of rows -RO .. Tk+RO-1 ----------------------------------
+    double *fh = fw + XFROWS, *fk = fh + XFROWS;            // final h, K of kept rows (filter)
     for (int r = tid - RO; r < Tk + RO; r += XNT) {
         const bool kept = r >= 0 && r < Tk;
+        // base U^n first: its global loads overlap the flux arithmetic
+        double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+        if (HEUN2) {
+            double par;
+            const size_t gi = mo + size_t(map_cell(s + r, n, P.bcl, P.bcr, par));
+            b0 = B.Un[0][gi]; b1 = par * B.Un[1][gi]; b2 = B.Un[2][gi]; b3 = B.Un[3][gi];
+        }
         double L[4];
         explicit_rhs(xh, xq, xH, xW, r, kap, g, lam, idx, ihdx, L);
         double o[4];
         if (HEUN2) {
-            double par;
-            const size_t gi = mo + size_t(map_cell(s + r, n, P.bcl, P.bcr, par));
-            const double b0 = B.Un[0][gi], b1 = par * B.Un[1][gi], b2 = B.Un[2][gi], b3 = B.Un[3][gi];
             o[0] = 0.5 * b0 + 0.5 * (xh[r] + dtm * L[0]);
             o[1] = 0.5 * b1 + 0.5 * (xq[r] + dtm * L[1]);
             o[2] = 0.5 * b2 + 0.5 * (xH[r] + dtm * L[2]);
@@ -1687,9 +1693,12 @@ __global__ void __launch_bounds__(XNT) explicit_kernel(const Params P, const Buf
         if (kept) {
             if (!(o[0] > P.h_min)) errbits |= ERR_DRY;
             if (!isfinite(o[0] + o[1] + o[2] + o[3])) errbits |= ERR_NONFINITE;
-            B.out[0][mo + s + r] = o[0];
-            B.out[2][mo + s + r] = o[2];
-            if (!FILT) { B.out[1][mo + s + r] = o[1]; B.out[3][mo + s + r] = o[3]; }
+            if (FILT) {
+                fh[r] = o[0]; fk[r] = o[2];
+            } else {
+                B.out[0][mo + s + r] = o[0]; B.out[1][mo + s + r] = o[1];
+                B.out[2][mo + s + r] = o[2]; B.out[3][mo + s + r] = o[3];
+            }
             if (FINAL && !FILT) {
                 const double ih = rcp(o[0]);
                 const double u = fabs(o[1] * ih), sg = o[2] * ih * ih;
@@ -1722,10 +1731,10 @@ __global__ void __launch_bounds__(XNT) explicit_kernel(const Params P, const Buf
             const double qo = cq[2] - sig16 * (cq[0] - 4.0 * cq[1] + 6.0 * cq[2] - 4.0 * cq[3] + cq[4]);
             const double wo = cw[2] - sig16 * (cw[0] - 4.0 * cw[1] + 6.0 * cw[2] - 4.0 * cw[3] + cw[4]);
             if (!isfinite(qo + wo)) errbits |= ERR_NONFINITE;
-            B.out[1][mo + s + r] = qo;
-            B.out[3][mo + s + r] = wo;
+            const double h0 = fh[r], K0 = fk[r];
+            B.out[0][mo + s + r] = h0; B.out[1][mo + s + r] = qo;
+            B.out[2][mo + s + r] = K0; B.out[3][mo + s + r] = wo;
             if (FINAL) {
-                const double h0 = B.out[0][mo + s + r], K0 = B.out[2][mo + s + r];
                 const double ih = rcp(h0);
                 const double u = fabs(qo * ih), sg = K0 * ih * ih;
                 const double nu = u + fsqrt(g * h0 + lam * (1.0 / 3.0) * sg * sg);

@@ -1546,6 +1546,10 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) step_kernel(const Params P, con
 // computed (the 4 halo rows redundantly) into shared memory first.
 // ---------------------------------------------------------------------------
 constexpr int XNT = 256;                 // threads per CTA
+#ifndef HSGN_XMINB
+#define HSGN_XMINB 3
+#endif
+constexpr int XMINB = HSGN_XMINB;        // CTAs per SM the registers allow
 constexpr int XT = 1024;                 // kept cells per tile
 constexpr int XR = 4;                    // halo rows of X (filter: 2 + 2)
 constexpr int XROWS = XT + 2 * XR + 8;   // shared rows per X array (+ alignment)
@@ -1587,7 +1591,7 @@ __device__ __forceinline__ void explicit_rhs(const double *xh, const double *xq,
 }
 
 template <bool HEUN2, bool FINAL, bool FILT>
-__global__ void __launch_bounds__(XNT) explicit_kernel(const Params P, const Bufs B)
+__global__ void __launch_bounds__(XNT, XMINB) explicit_kernel(const Params P, const Bufs B)
 {
     const int tid = threadIdx.x;
     const int j = blockIdx.x, m = blockIdx.y;

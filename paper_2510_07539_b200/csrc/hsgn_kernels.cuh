@@ -763,17 +763,20 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                     const double2 h1 = v[7 * SROWS / 2], q1 = v[2 * SROWS], K1 = v[5 * SROWS / 2],
                                   W1 = v[3 * SROWS];
                     const double q1x = par0 * q1.x, q1y = par1 * q1.y;
+                    // (1 - w) U^n + w U1 = U^n + w (U1 - U^n): one difference, two FMAs
+                    const double dhx = h1.x - eh.x, dhy = h1.y - eh.y, dqx = q1x - eq.x, dqy = q1y - eq.y;
+                    const double dKx = K1.x - eK.x, dKy = K1.y - eK.y, dWx = W1.x - eW.x, dWy = W1.y - eW.y;
                     double2 rh, rq, rK, rW;
-                    rh.x = (1.0 - wR) * eh.x + wR * h1.x; rh.y = (1.0 - wR) * eh.y + wR * h1.y;
-                    rq.x = (1.0 - wR) * eq.x + wR * q1x;  rq.y = (1.0 - wR) * eq.y + wR * q1y;
-                    rK.x = (1.0 - wR) * eK.x + wR * K1.x; rK.y = (1.0 - wR) * eK.y + wR * K1.y;
-                    rW.x = (1.0 - wR) * eW.x + wR * W1.x; rW.y = (1.0 - wR) * eW.y + wR * W1.y;
+                    rh.x = fma(wR, dhx, eh.x); rh.y = fma(wR, dhy, eh.y);
+                    rq.x = fma(wR, dqx, eq.x); rq.y = fma(wR, dqy, eq.y);
+                    rK.x = fma(wR, dKx, eK.x); rK.y = fma(wR, dKy, eK.y);
+                    rW.x = fma(wR, dWx, eW.x); rW.y = fma(wR, dWy, eW.y);
                     if (raw && BATHY) { rK.x -= 1.5 * rh.x * b0; rK.y -= 1.5 * rh.y * b1; }
                     v[7 * SROWS / 2] = rh; v[2 * SROWS] = rq; v[5 * SROWS / 2] = rK; v[3 * SROWS] = rW;
-                    eh.x = (1.0 - wE) * eh.x + wE * h1.x; eh.y = (1.0 - wE) * eh.y + wE * h1.y;
-                    eq.x = (1.0 - wE) * eq.x + wE * q1x;  eq.y = (1.0 - wE) * eq.y + wE * q1y;
-                    eK.x = (1.0 - wE) * eK.x + wE * K1.x; eK.y = (1.0 - wE) * eK.y + wE * K1.y;
-                    eW.x = (1.0 - wE) * eW.x + wE * W1.x; eW.y = (1.0 - wE) * eW.y + wE * W1.y;
+                    eh.x = fma(wE, dhx, eh.x); eh.y = fma(wE, dhy, eh.y);
+                    eq.x = fma(wE, dqx, eq.x); eq.y = fma(wE, dqy, eq.y);
+                    eK.x = fma(wE, dKx, eK.x); eK.y = fma(wE, dKy, eK.y);
+                    eW.x = fma(wE, dWx, eW.x); eW.y = fma(wE, dWy, eW.y);
                 }
                 if (raw && BATHY) { eK.x -= 1.5 * eh.x * b0; eK.y -= 1.5 * eh.y * b1; }
                 v[0] = eh; v[SROWS / 2] = eq; v[SROWS] = eK;

@@ -67,6 +67,12 @@ typedef struct {
     double x_min, level;
     double gen_x1, gen_rate, amp, omega, k, cp;
     double sp_x0, sp_rate;
+    /* Picard re-linearisation of the depth equation (reading A24, SURVEY row
+     * f4): after the first solve, `picard` more assemble+solve passes with
+     * beta1 = 1 + lam tau^2/h^2 and beta2 = 2 lam tau^2/(beta1^2 h^3) taken at
+     * the latest hbar (alpha, a^2 stay at E); 0 = the paper's linearised stage. */
+    int32_t picard;
+    int32_t pad2_;
 } orc_problem;
 
 /* Double Butcher tableau. */
@@ -267,6 +273,9 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
     double *hbar = Dxb + n, *tmp0 = hbar + n, *tmp1 = tmp0 + n, *tmp2 = tmp1 + n;
     double *Hloc = tmp2 + n;
     (void)bq; (void)bH;
+    double *alE = (double *)malloc(sizeof(double) * (size_t)n * 2);
+    if (!alE) { free(buf); return ORC_E_INVALID; }
+    double *a2E = alE + n;
 
     /* Step 1 (A9): H = K - 1.5 h b on E; ghost-extend E and b. */
     double *bzero = tmp0;
@@ -326,12 +335,28 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
         orc_coeffs(g, lam, tau, hE, HE, Hd_, c);
         be[i + 1] = c[4];
         de[i + 1] = c[5];
+        alE[i] = c[0];
+        a2E[i] = c[1];
         if (!(c[4] > 0.0)) status = ORC_E_COERCIVITY;  /* kappa > 0 */
         if (c[4] < mb) mb = c[4];
     }
     if (min_beta) *min_beta = mb;
     if (status != ORC_OK) goto done;
 
+    for (int it = 0; it <= P->picard; it++) {
+    if (it > 0) {
+        /* A24 Picard pass: beta1, beta2 (hence beta, delta) at the latest hbar,
+         * alpha and a^2 at E (the exact elimination has b1 = 1/beta1
+         * and d b1/dh at h^{n+1}; the paper freezes them at h^n). */
+        for (int i = 0; i < n; i++) {
+            double hb = hbar[i];
+            double beta1 = 1.0 + lam * tau * tau / (hb * hb);
+            double beta2 = 2.0 * lam * tau * tau / (beta1 * beta1 * hb * hb * hb);
+            be[i + 1] = a2E[i] + lam * alE[i] * beta2 * Hd[i + 1];
+            de[i + 1] = alE[i] / beta1;
+            if (!(be[i + 1] > 0.0)) { status = ORC_E_COERCIVITY; goto done; }
+        }
+    }
     /* Derived-field ghosts (A10): periodic wrap; wall/transmissive mirror-copy,
      * with q^dagger odd at a wall. */
     {
@@ -383,6 +408,7 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
     status = periodic ? orc_cyclic_thomas(n, lo, di, up, rhs, hbar)
                       : orc_thomas(n, lo, di, up, rhs, hbar);
     if (status != ORC_OK) goto done;
+    }   /* Picard passes */
 
     /* Step 8: back-substitution (A9 hydrostatic term). */
     for (int i = 0; i < n; i++) {
@@ -412,6 +438,7 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
 #undef X
 #undef FACE
 done:
+    free(alE);
     free(buf);
     return status;
 }

@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--si-order", type=int, default=2, choices=[1, 2],
                    help="2: the paper's second-order SI step (headline); 1: first-order SI "
                         "(one implicit stage tau = dt, order-1 faces; SURVEY row f2)")
+    p.add_argument("--picard", type=int, default=0,
+                   help="Picard passes of the SI depth solve (reading A24, SURVEY row f4); 0: the paper's")
     p.add_argument("--scheme", default="si", choices=["si", "explicit", "sgn"],
                    help="si: the SI-IMEX step (headline); explicit: the explicit hSGN scheme "
                         "(Heun, CFL_EX 0.4); sgn: the classical SGN scheme (Heun, CFL_SGN 0.9) "
@@ -68,6 +70,8 @@ def parse():
 
 def config_dict(a, world):
     d = _config_dict(a, world)
+    if a.picard > 0:
+        d["picard_passes"] = a.picard
     if a.si_order == 1:
         d["scheme"] = "first-order SI (P:500-517: one implicit stage, tau = dt, order-1 faces)"
         d["order"] = 1
@@ -180,14 +184,14 @@ def profile_traffic(cells):
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; timed only here, never on the product path)
 # ---------------------------------------------------------------------------
-def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False, si_order=2):
+def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False, si_order=2, picard=0):
     """Oracle cell-stage/s on the host cores (one member per thread), repeated
     until at least min_seconds of wall time; returns (rate, seconds, repeats)."""
     from oracle import oracle as O
     tab = O.euler_tableau() if si_order == 1 else None
     sig = 0.0 if explicit == "sgn" else w.filter_sigma
     jobs = [(O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, b=w.b, order=si_order,
-                      filter_sigma=sig, tableau=tab), w.state(m)) for m in members]
+                      filter_sigma=sig, tableau=tab, picard=picard), w.state(m)) for m in members]
     t0 = time.perf_counter()
     reps = 0
     while True:
@@ -286,6 +290,8 @@ def main():
         s.set_tableau(hsgn.euler_tableau())
         s.set_filter(w.filter_sigma)
         s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
+    if a.picard > 0:
+        s.set_picard(a.picard)
     if a.scheme == "explicit":
         if a.config != "cfg3":
             raise SystemExit("--scheme explicit: cfg3 only (the explicit scheme needs a flat bottom)")
@@ -393,7 +399,7 @@ def main():
         nm = max(4 * threads, 16)
         rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0,
                                            explicit="sgn" if a.scheme == "sgn" else a.scheme == "explicit",
-                                           si_order=a.si_order)
+                                           si_order=a.si_order, picard=a.picard)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"first {nm} cfg3 members x 10 "
                          f"{ {'explicit': 'explicit Heun', 'sgn': 'classical SGN Heun'}.get(a.scheme, 'SI')} "

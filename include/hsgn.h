@@ -236,6 +236,16 @@ int32_t hsgn_get_fused(const hsgn_ctx *ctx);
  * dx is too small against h for the tile width. */
 #define HSGN_SCHEME_SGN 2
 hsgn_status hsgn_set_scheme(hsgn_ctx *ctx, int32_t scheme, int32_t stages);
+/* Picard re-linearisation of the depth equation (reading A24, SURVEY 8(f)
+ * row f4): after the paper's linearised solve of each SI
+ * stage, `passes` more assemble+solve passes with beta1 = 1 + lam tau^2/h^2
+ * and beta2 = 2 lam tau^2/(beta1^2 h^3) (hence kappa = beta and delta) at the
+ * latest hbar, alpha and a^2 staying at the stage input E.  0 (default) = the
+ * paper's scheme.  Runs on the one-CTA-per-tile stage kernels (the fused and
+ * persistent organisations are bypassed); not with relaxation zones or the
+ * explicit / SGN schemes (HSGN_E_INVALID at the next step).  Errors:
+ * HSGN_E_INVALID (null context, passes outside 0..16). */
+hsgn_status hsgn_set_picard(hsgn_ctx *ctx, int32_t passes);
 /* Per-stage kernels as persistent CTAs: each CTA walks
  * (tile, member) items and prefetches the next item's inputs by TMA while it
  * finishes the current one; on = 0: one CTA per (tile, member).  Same

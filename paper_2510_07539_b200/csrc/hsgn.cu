@@ -81,6 +81,7 @@ struct hsgn_ctx {
     int scheme = 0, x_stages = 2, xT = 0, xtiles = 0;
     // classical SGN (scheme 2): phi-system overlap and tiles, from the state
     int sw = 0, sT = 0, stiles = 0;
+    int picard = 0;               // A24 Picard passes of the SI depth solve (0: the paper's)
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
     bool persist = false;
     int persist_grid = 0;
@@ -146,6 +147,7 @@ Params make_params(hsgn_ctx *c, long long k)
         P.mcfl = 0.0;
     }
     P.inv_tiles = 1.0 / double(c->tiles);
+    P.picard = c->picard;
     for (int k = 0; k < 9; k++) {
         P.halo_l[k] = c->halo_l ? c->halo_l + k * H_MAX : nullptr;
         P.halo_r[k] = c->halo_r ? c->halo_r + k * H_MAX : nullptr;
@@ -157,7 +159,10 @@ template <bool S2, bool FIN, bool BATHY>
 hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
 {
     const bool relax = FIN && (c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0);
-    if (c->persist) {
+    if (c->picard > 0) {             // A24: one CTA per tile, Picard variant
+        dim3 grid(c->tiles, c->members);
+        stage_kernel<S2, FIN, BATHY, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    } else if (c->persist) {
         const int items = c->tiles * c->members;
         const int grid = std::min(items, c->persist_grid);
         if (relax) stage_pkernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
@@ -324,7 +329,7 @@ void choose_geometry(hsgn_ctx *c)
     }
     // fused step: stage 1 runs on the kept tile widened by 2w + 3 on each side
     const int wmax_fused = (LCAP - 2 - 6 - T_MIN) / 4;
-    c->fused = c->fused_on && c->tab.stages == 2 && !c->slab && w <= wmax_fused;
+    c->fused = c->fused_on && c->tab.stages == 2 && !c->slab && w <= wmax_fused && c->picard == 0;
     w = std::max(3, std::min(w, (LCAP - 2 - T_MIN) / 2));
     const int maxT = c->fused ? LCAP - 2 - 6 - 4 * w : LCAP - 2 - 2 * w;
     int T;
@@ -369,6 +374,8 @@ hsgn_status ready(hsgn_ctx *c)
     if (!c->have_state) return fail(c, HSGN_E_INVALID, "hsgn_set_state not called");
     if (c->scheme != 0 && (c->bathy || c->slab || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
         return fail(c, HSGN_E_INVALID, "explicit / SGN schemes: flat bottom, no relaxation zones, no slabs");
+    if (c->picard > 0 && (c->scheme != 0 || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
+        return fail(c, HSGN_E_INVALID, "Picard passes: SI scheme without relaxation zones");
     if (c->scheme == 2 && c->filter_sigma > 0.0)
         return fail(c, HSGN_E_INVALID, "SGN scheme: no A19 filter (its Rusanov speed includes sqrt(g h))");
     if (c->scheme == 2 && c->sT <= 0) return fail(c, HSGN_E_INVALID, "SGN geometry not set");
@@ -717,6 +724,12 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_pkernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
@@ -1130,6 +1143,15 @@ hsgn_status hsgn_set_scheme(hsgn_ctx *c, int32_t scheme, int32_t stages)
         }
         if (c->scheme == 2) return sgn_geometry(c);
     }
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_picard(hsgn_ctx *c, int32_t passes)
+{
+    if (!c || passes < 0 || passes > 16) return HSGN_E_INVALID;
+    c->picard = passes;
+    drop_graphs(c);
+    choose_geometry(c);
     return HSGN_OK;
 }
 

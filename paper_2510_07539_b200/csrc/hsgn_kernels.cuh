@@ -109,6 +109,7 @@ struct Params {
     // resident at once); 0: off
     int pf_dist;
     double inv_tiles;                // 1 / tiles
+    int picard;                      // A24 Picard passes (stage_kernel<..., PIC = true>)
     // A10 relaxation zones (cfg4), applied to U^{n+1} at t^{n+1} in the final
     // stage; rates <= 0 switch them off.  x_i = x_min + (i + 1/2) dx.
     double x_min, x_max, level, gen_x1, gen_rate, amp, omega, kw, cp, sp_x0, sp_rate;
@@ -709,7 +710,7 @@ __device__ __forceinline__ void prefetch_stage_item(const Params &P, const Bufs 
 // parities applied) and that U1; output staged in the dedicated buffer.  Once the arrays 0..3 are no longer read, the
 // loads of U^n for next_item (>= 0) are issued into them (prefetch).
 // ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, int MODE>
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, int MODE, bool PIC = false>
 __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const Geom &G, int m, int s_cell,
                                            const StageC &S, double dtm, TileAcc &acc, int next_item,
                                            bool rt2)
@@ -872,25 +873,28 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // make those face coefficients t2 (beta_i + beta_{i+1}) / 2 exactly zero;
     // rows L+1 .. L+MCH+1 (read by the last live chunk) get zero fields and
     // alternating +-beta_{L-1}, so all their couplings vanish too.
-    if (tid == 0) {
-        if (left_phys) {
-            sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
-            sHd[-1] = sHd[0]; sDe[-1] = sDe[0];
+    auto tile_end_ghosts = [&]() {
+        if (tid == 0) {
+            if (left_phys) {
+                sQd[-1] = (P.bcl == BC_WALL ? -1.0 : 1.0) * sQd[0];
+                sHd[-1] = sHd[0]; sDe[-1] = sDe[0];
+            }
+            sBe[-1] = -sBe[0];
         }
-        sBe[-1] = -sBe[0];
-    }
-    if (tid == 32) {
-        if (right_phys) {
-            sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
-            sHd[L] = sHd[L - 1]; sDe[L] = sDe[L - 1];
+        if (tid == 32) {
+            if (right_phys) {
+                sQd[L] = (P.bcr == BC_WALL ? -1.0 : 1.0) * sQd[L - 1];
+                sHd[L] = sHd[L - 1]; sDe[L] = sDe[L - 1];
+            }
+            sBe[L] = -sBe[L - 1];
         }
-        sBe[L] = -sBe[L - 1];
-    }
-    if (tid >= 64 && tid < 64 + MCH + 1) {
-        const int r = L + 1 + (tid - 64);
-        sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0;
-        sBe[r] = ((r - L) & 1) ? sBe[L - 1] : -sBe[L - 1];
-    }
+        if (tid >= 64 && tid < 64 + MCH + 1) {
+            const int r = L + 1 + (tid - 64);
+            sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0;
+            sBe[r] = ((r - L) & 1) ? sBe[L - 1] : -sBe[L - 1];
+        }
+    };
+    tile_end_ghosts();
     __syncthreads();
 
     // ---- phase 2: assemble + partition solve (A1, A3) ---------
@@ -917,6 +921,43 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         for (int k = 0; k < MCH + 2; k++) { vb[k] = 0.0; vd[k] = 0.0; vH[k] = 0.0; vq[k] = 0.0; }
     }
     double hb[MCH];
+    double alv[MCH], a2v[MCH];           // PIC: alpha, a^2 at E of the own rows
+#pragma unroll 1
+    for (int pic = 0; pic <= (PIC ? P.picard : 0); pic++) {
+    if (PIC && pic > 0) {
+        // A24 Picard pass: beta, delta of the own rows with beta1 = 1 + lam tau^2/hbar^2
+        // and beta2 = 2 lam tau^2/(beta1^2 hbar^3) at the latest hbar; alpha, a^2 stay
+        // at E (recovered from the first pass: alpha = delta beta1(h^E),
+        // a^2 = beta - lam alpha beta2(h^E) H^dag)
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < MCH; i++) {
+                const int r = r0 + i;
+                if (r >= L) continue;
+                if (pic == 1) {
+                    const double hE = sEh[r], hE2 = hE * hE;
+                    const double b1E = 1.0 + lt2 / hE2;
+                    const double b2E = 2.0 * lt2 / (b1E * b1E * hE2 * hE);
+                    alv[i] = vd[i + 1] * b1E;
+                    a2v[i] = vb[i + 1] - lam * alv[i] * b2E * vH[i + 1];
+                }
+                const double hn = hb[i], hn2 = hn * hn;
+                const double b1 = 1.0 + lt2 / hn2;
+                const double b2 = 2.0 * lt2 / (b1 * b1 * hn2 * hn);
+                const double be = a2v[i] + lam * alv[i] * b2 * vH[i + 1];
+                if (r >= G.klo && r < G.khi && !(be > 0.0)) acc.err |= ERR_COERC;
+                sBe[r] = be;
+                sDe[r] = alv[i] / b1;
+            }
+        }
+        __syncthreads();
+        tile_end_ghosts();
+        __syncthreads();
+        if (live) {
+#pragma unroll
+            for (int k = 0; k < MCH + 2; k++) { vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; }
+        }
+    }
     {
         double am[MCH], cm[MCH], dm[MCH];
 #pragma unroll
@@ -1028,6 +1069,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         }
     }
     __syncthreads();
+    }   // Picard passes
 
     // ---- phase 3: back-substitution, own rows ------------------
     const bool filt = fin && (P.filter_sigma > 0.0);
@@ -1300,7 +1342,7 @@ __device__ unsigned long long g_exp[8];
 #define EXP_T(v)
 #endif
 
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false>
 __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
 {
     EXP_T(t0);
@@ -1353,7 +1395,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
     } else {
         const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
-        stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE>(P, B, G, m, s, S, dtm, acc, -1, false);
+        stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE, PIC>(P, B, G, m, s, S, dtm, acc, -1, false);
         store_tile(B, mo, s, e - s, false, P.T);
     }
     EXP_T(t2);

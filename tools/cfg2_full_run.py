@@ -25,17 +25,24 @@ def main():
               "scaled errors h q K W", ["%.2e" % e for e in errs])
         return
     lam, out = float(sys.argv[2]), sys.argv[3]
+    nsteps = int(sys.argv[4]) if len(sys.argv) > 4 else None     # else run to t_end
     w = W.cfg2(lam)
     t0 = time.time()
     if mode == "oracle":
         from oracle import oracle as O
         o = O.Oracle(w.n, w.dx, lam=lam, bc=w.bc, filter_sigma=w.filter_sigma)
-        U, t, steps, _ = o.run(w.state(0), cfl=w.cfl, mcfl=w.mcfl, t_end=w.t_end)
+        if nsteps:
+            U, t, steps, _ = o.run(w.state(0), cfl=w.cfl, mcfl=w.mcfl, steps=nsteps)
+        else:
+            U, t, steps, _ = o.run(w.state(0), cfl=w.cfl, mcfl=w.mcfl, t_end=w.t_end)
         dt = o.dt(U, w.cfl, w.mcfl)[0]
     else:
         from paper_2510_07539_b200 import hsgn
         s = hsgn.solver_for(w)
-        steps = s.advance_to(w.t_end)
+        if nsteps:
+            s.run_steps(nsteps)
+        else:
+            s.advance_to(w.t_end)
         (h, q, K, Wf), tt = s.get_state(device=False)
         U, t = [h[0], q[0], K[0], Wf[0]], float(tt[0])
         dt = 0.0

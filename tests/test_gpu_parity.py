@@ -395,3 +395,30 @@ def test_wavemaker_channel_matches_oracle():
     compare(w, s, [0], steps=1000, tol=TOL_RUN)
     (h, *_), t = s.get_state(device=False)
     assert np.max(np.abs(h[0] - 0.4)) > 5e-3
+
+
+def test_nccl_transport_single_rank_ring():
+    """The NCCL slab transport with world = 1: one periodic domain as a single
+    slab whose two halo sides are exchanged with itself through ncclSend/Recv
+    and whose dt maxima go through ncclAllReduce -- the same code path as the
+    multi-GPU run, without ranks waiting on one another.  Must equal the plain
+    periodic domain (same arithmetic, same tile cuts)."""
+    hs = _hsgn()
+    w = W.cfg5_workload(1 << 16)
+    single = gpu_solver(w)
+    (sv,), _ = hs.slab_solvers(w, 1)
+    sv.attach_nccl(hs.nccl_unique_id(), 0, 1)
+    single.run_steps(1)
+    sv.run_steps(1)
+    (a, ta), (b, tb) = single.get_state(device=False), sv.get_state(device=False)
+    refs, _ = oracle_run(w, [0], steps=1)
+    dt = O.Oracle(w.n, w.dx, lam=float(w.lam[0]), b=w.b).dt(refs[0], w.cfl, w.mcfl)[0]
+    S = field_scales(refs[0], float(w.lam[0]), dt)
+    assert ta[0] == tb[0]
+    assert rel_err([f[0] for f in b], [f[0] for f in a], S) <= 1e-13
+    assert rel_err([f[0] for f in b], refs[0], S) <= TOL_STEP
+    single.run_steps(9)
+    sv.run_steps(9)
+    (a, ta), (b, tb) = single.get_state(device=False), sv.get_state(device=False)
+    assert abs(ta[0] - tb[0]) <= 1e-13 * ta[0]
+    assert rel_err([f[0] for f in b], [f[0] for f in a], S) <= 1e-11

@@ -422,3 +422,24 @@ def test_nccl_transport_single_rank_ring():
     (a, ta), (b, tb) = single.get_state(device=False), sv.get_state(device=False)
     assert abs(ta[0] - tb[0]) <= 1e-13 * ta[0]
     assert rel_err([f[0] for f in b], [f[0] for f in a], S) <= 1e-11
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_randomised_cases_one_step(case):
+    """Seeded random problem shapes (cells, members, BCs, order, lambda range,
+    amplitude, tile size, bathymetry, filter): one SI step == the oracle."""
+    rng = np.random.default_rng(7539 + case)
+    n = int(rng.integers(5, 6000))
+    members = int(rng.integers(1, 4))
+    bc = ["periodic", "wall", "transmissive"][int(rng.integers(0, 3))]
+    order = int(rng.integers(1, 3))
+    bathy = float(rng.choice([0.0, 0.05]))
+    w = W.random_smooth(n, members, seed=int(rng.integers(1 << 30)), amp=float(rng.uniform(0.01, 0.12)),
+                        bc=(bc, bc), bathy=bathy, lam_range=(10 ** rng.uniform(1, 2), 10 ** rng.uniform(3, 4.5)))
+    w.filter_sigma = float(rng.choice([0.0, 0.25]))
+    kw = {"order": order}
+    if rng.random() < 0.5:
+        kw["tile_cells"] = int(rng.integers(64, 600))
+    s = gpu_solver(w, **kw)
+    s.step()
+    compare(w, s, range(members), steps=1, order=order)

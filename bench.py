@@ -394,7 +394,7 @@ def main():
                "what": "Solver.set_state(pinned host) + K x Solver.step(return_dt) + get_state(pinned host), wall clock, max over ranks"}
 
     cpu = None
-    if rank == 0 and not a.no_cpu and a.config == "cfg3":
+    if rank == 0 and world == 1 and not a.no_cpu and a.config == "cfg3":   # N = 1 only
         threads = os.cpu_count() or 1
         nm = max(4 * threads, 16)
         rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0,

@@ -72,7 +72,10 @@ typedef struct {
      * beta1 = 1 + lam tau^2/h^2 and beta2 = 2 lam tau^2/(beta1^2 h^3) taken at
      * the latest hbar (alpha, a^2 stay at E); 0 = the paper's linearised stage. */
     int32_t picard;
-    int32_t pad2_;
+    /* Exactly well-balanced variant (reading A25): face-based
+     * delta_{i+1/2} in the depth right-hand side and qbar from face-averaged
+     * face fluxes, so that the lake at rest is kept to round-off at lam > 0. */
+    int32_t wb;
 } orc_problem;
 
 /* Double Butcher tableau. */
@@ -249,6 +252,21 @@ static void fill_ghosts(const double *f, int n, int G, int bcl, int bcr, double 
  * Bathymetric terms follow reading A9; the half-index coefficients follow A1.
  * On success writes out[0..3] = (h, q, K, W) and *min_beta = min_i beta_i.
  */
+/* A25 face coefficient dhat_{f+1/2} = -(2 sigma^ - 1)/(3 h~) b1~ between cells f
+ * and f+1 of E (ghost-extended arrays with G ghosts): sigma^ = (sigma_f + sigma_{f+1})/2,
+ * h~ = (h_f + h_{f+1})/2, b1~ = (1/beta1_f + 1/beta1_{f+1})/2, beta1 = 1 + lam tau^2/h^2.
+ * At the lake at rest (sigma = 1, H = h^2) it makes lam dhat (H^dag_{f+1} - H^dag_f)
+ * equal the lam part of -beta_{f+1/2} (h_{f+1} - h_f) exactly. */
+static double wb_delta(const double *eh, const double *eH, int f, double lam, double tau, int G)
+{
+    double h0 = eh[f + G], h1 = eh[f + 1 + G];
+    double s0 = (eH[f + G] / h0) / h0, s1 = (eH[f + 1 + G] / h1) / h1;
+    double b0 = 1.0 / (1.0 + lam * tau * tau / (h0 * h0));
+    double b1 = 1.0 / (1.0 + lam * tau * tau / (h1 * h1));
+    double sig = 0.5 * (s0 + s1), ht = 0.5 * (h0 + h1), bt = 0.5 * (b0 + b1);
+    return -(2.0 * sig - 1.0) / (3.0 * ht) * bt;
+}
+
 static int stage_impl(const orc_problem *P, const double *const E[4],
                       const double *const R[4], double tau, double *const out[4],
                       double *min_beta)
@@ -260,6 +278,7 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
     const double qpar = -1.0;  /* q is odd under wall reflection (A10) */
     int status = ORC_OK;
     size_t ne = (size_t)(n + 2 * G);
+    if (P->wb && P->picard > 0) return ORC_E_INVALID;   /* A25 is defined on the linearised stage */
 
     double *buf = (double *)calloc(ne * 5 + (size_t)(n + 3) * 3 + (size_t)(n + 2) * 8
                                    + (size_t)n * 10, sizeof(double));
@@ -385,6 +404,11 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
             double rr = t2 * (be[i + 1] + be[i + 2]) / 2.0;  /* rho_{i+1/2} */
             double ml = lt2 * (de[i] + de[i + 1]);            /* mu_{i-1/2} */
             double mr = lt2 * (de[i + 1] + de[i + 2]);        /* mu_{i+1/2} */
+            if (P->wb) {
+                /* A25: mu_{i+1/2} = (lam tau^2/dx^2) dhat_{i+1/2} */
+                ml = 2.0 * lt2 * wb_delta(eh, eH, i - 1, lam, tau, G);
+                mr = 2.0 * lt2 * wb_delta(eh, eH, i, lam, tau, G);
+            }
             if (!periodic && i == 0) rl = 0.0;
             if (!periodic && i == n - 1) rr = 0.0;
             double hd = R[0][i] - (tau / (2.0 * dx)) * (qd[i + 2] - qd[i])
@@ -420,6 +444,19 @@ static int stage_impl(const orc_problem *P, const double *const E[4],
         double qn = qd[i + 1] - (tau / (2.0 * dx)) * be[i + 1] * (hr - hl)
                     - (lam * tau / (2.0 * dx)) * de[i + 1] * (Hd[i + 2] - Hd[i])
                     - tau * g * X(eh, i) * Dxb[i];
+        if (P->wb) {
+            /* A25: qbar = q^dag - (tau/(2dx)) (Phi_{i+1/2} + Phi_{i-1/2}),
+             * Phi_{f} = beta_f (hbar_R - hbar_L) + lam dhat_f (H^dag_R - H^dag_L) + G_f (b_R - b_L) */
+            double Phr = 0.5 * (be[i + 1] + be[i + 2]) * (hr - hn)
+                         + lam * wb_delta(eh, eH, i, lam, tau, G) * (Hd[i + 2] - Hd[i + 1])
+                         + 0.5 * g * (X(eh, i) + X(eh, i + 1)) * (X(eb, i + 1) - X(eb, i));
+            double Phl = 0.5 * (be[i] + be[i + 1]) * (hn - hl)
+                         + lam * wb_delta(eh, eH, i - 1, lam, tau, G) * (Hd[i + 1] - Hd[i])
+                         + 0.5 * g * (X(eh, i - 1) + X(eh, i)) * (X(eb, i) - X(eb, i - 1));
+            if (!periodic && i == 0) Phl = 0.0;          /* wall / Neumann face */
+            if (!periodic && i == n - 1) Phr = 0.0;
+            qn = qd[i + 1] - (tau / (2.0 * dx)) * (Phr + Phl);
+        }
         double Hn = Hd[i + 1] / (1.0 + lam * tau * tau / (hn * hn));  /* P:514 */
         double Wn = Wd[i + 1] - lam * tau * Hn / (hn * hn);          /* P:515 */
         tmp1[i] = qn;

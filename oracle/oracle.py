@@ -45,7 +45,7 @@ class Problem(C.Structure):
         ("x_min", C.c_double), ("level", C.c_double), ("gen_x1", C.c_double),
         ("gen_rate", C.c_double), ("amp", C.c_double), ("omega", C.c_double), ("k", C.c_double),
         ("cp", C.c_double), ("sp_x0", C.c_double), ("sp_rate", C.c_double),
-        ("picard", C.c_int32), ("pad2_", C.c_int32),
+        ("picard", C.c_int32), ("wb", C.c_int32),
     ]
 
 
@@ -151,7 +151,7 @@ class Oracle:
 
     def __init__(self, n, dx, g=9.81, lam=500.0, bc=("periodic", "periodic"), order=2,
                  h_min=1e-8, b=None, filter_sigma=0.0, filter_mask=0b1010, tableau=None,
-                 relax=None, picard=0):
+                 relax=None, picard=0, wb=False):
         """relax: dict(x_min, level, gen_x1, gen_rate, amp, omega, k, cp, sp_x0, sp_rate)
         for the A10 wavemaker / sponge zones (cfg4)."""
         self.L = lib()
@@ -161,6 +161,7 @@ class Oracle:
                          dx=dx, g=g, lam=lam, h_min=h_min,
                          b=_p(self._b) if self._b is not None else None,
                          filter_sigma=filter_sigma, filter_mask=filter_mask, picard=picard,
+                         wb=1 if wb else 0,
                          **(relax or {}))
         self.T = tableau if tableau is not None else paper_tableau()
 

@@ -54,6 +54,8 @@ def parse():
                         "(one implicit stage tau = dt, order-1 faces; SURVEY row f2)")
     p.add_argument("--picard", type=int, default=0,
                    help="Picard passes of the SI depth solve (reading A24, SURVEY row f4); 0: the paper's")
+    p.add_argument("--wb", action="store_true",
+                   help="exactly well-balanced face form of the SI stage (reading A25, SURVEY row f4)")
     p.add_argument("--scheme", default="si", choices=["si", "explicit", "sgn"],
                    help="si: the SI-IMEX step (headline); explicit: the explicit hSGN scheme "
                         "(Heun, CFL_EX 0.4); sgn: the classical SGN scheme (Heun, CFL_SGN 0.9) "
@@ -72,6 +74,8 @@ def config_dict(a, world):
     d = _config_dict(a, world)
     if a.picard > 0:
         d["picard_passes"] = a.picard
+    if a.wb:
+        d["well_balanced"] = "A25 face form"
     if a.si_order == 1:
         d["scheme"] = "first-order SI (P:500-517: one implicit stage, tau = dt, order-1 faces)"
         d["order"] = 1
@@ -184,14 +188,15 @@ def profile_traffic(cells):
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (test infrastructure; timed only here, never on the product path)
 # ---------------------------------------------------------------------------
-def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False, si_order=2, picard=0):
+def cpu_oracle_rate(w, members, steps, threads, min_seconds=0.0, explicit=False, si_order=2, picard=0,
+                    wb=False):
     """Oracle cell-stage/s on the host cores (one member per thread), repeated
     until at least min_seconds of wall time; returns (rate, seconds, repeats)."""
     from oracle import oracle as O
     tab = O.euler_tableau() if si_order == 1 else None
     sig = 0.0 if explicit == "sgn" else w.filter_sigma
     jobs = [(O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, b=w.b, order=si_order,
-                      filter_sigma=sig, tableau=tab, picard=picard), w.state(m)) for m in members]
+                      filter_sigma=sig, tableau=tab, picard=picard, wb=wb), w.state(m)) for m in members]
     t0 = time.perf_counter()
     reps = 0
     while True:
@@ -292,6 +297,10 @@ def main():
         s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
     if a.picard > 0:
         s.set_picard(a.picard)
+    if a.wb:
+        if a.scheme != "si" or a.picard > 0:
+            raise SystemExit("--wb: SI scheme without Picard passes")
+        s.set_well_balanced(True)
     if a.scheme == "explicit":
         if a.config != "cfg3":
             raise SystemExit("--scheme explicit: cfg3 only (the explicit scheme needs a flat bottom)")
@@ -399,7 +408,7 @@ def main():
         nm = max(4 * threads, 16)
         rate, secs, reps = cpu_oracle_rate(w.subset(range(nm)), range(nm), 10, threads, min_seconds=10.0,
                                            explicit="sgn" if a.scheme == "sgn" else a.scheme == "explicit",
-                                           si_order=a.si_order, picard=a.picard)
+                                           si_order=a.si_order, picard=a.picard, wb=a.wb)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"first {nm} cfg3 members x 10 "
                          f"{ {'explicit': 'explicit Heun', 'sgn': 'classical SGN Heun'}.get(a.scheme, 'SI')} "

@@ -246,6 +246,20 @@ hsgn_status hsgn_set_scheme(hsgn_ctx *ctx, int32_t scheme, int32_t stages);
  * explicit / SGN schemes (HSGN_E_INVALID at the next step).  Errors:
  * HSGN_E_INVALID (null context, passes outside 0..16). */
 hsgn_status hsgn_set_picard(hsgn_ctx *ctx, int32_t passes);
+/* Exactly well-balanced face form of the SI stage (reading A25, SURVEY 8(f)
+ * row f4; P:163-171 hSGNb): the depth right-hand side uses the face
+ * coefficient dhat_{i+1/2} = -(2 sigma^ - 1)/(3 h~) b1~ (face averages of
+ * sigma = H/h^2, h and 1/beta1 at E) in place of (delta_i + delta_{i+1})/2,
+ * and qbar = q^dag - tau/(2 dx) (Phi_{i+1/2} + Phi_{i-1/2}) with the face
+ * fluxes Phi = beta~ (hbar_R - hbar_L) + lam dhat (H^dag_R - H^dag_L)
+ * + g h~ (b_R - b_L).  The lake at rest over any bathymetry is then a fixed
+ * point to round-off at lam > 0 (the paper's cell-centred form keeps it to
+ * O(dx^2) only, reading A9); the scheme stays conservative and second order.
+ * on = 0 (default): the paper's form.  Runs on the one-CTA-per-tile stage
+ * kernels; not with Picard passes or the explicit / SGN schemes
+ * (HSGN_E_INVALID at the next step).  Drops captured graphs.  Errors:
+ * HSGN_E_INVALID (null context). */
+hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
 /* Per-stage kernels as persistent CTAs: each CTA walks
  * (tile, member) items and prefetches the next item's inputs by TMA while it
  * finishes the current one; on = 0: one CTA per (tile, member).  Same

@@ -82,6 +82,7 @@ struct hsgn_ctx {
     // classical SGN (scheme 2): phi-system overlap and tiles, from the state
     int sw = 0, sT = 0, stiles = 0;
     int picard = 0;               // A24 Picard passes of the SI depth solve (0: the paper's)
+    bool wb = false;              // A25 exactly well-balanced face form of the SI stage
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
     bool persist = false;
     int persist_grid = 0;
@@ -162,6 +163,10 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
     if (c->picard > 0) {             // A24: one CTA per tile, Picard variant
         dim3 grid(c->tiles, c->members);
         stage_kernel<S2, FIN, BATHY, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+    } else if (c->wb) {              // A25: one CTA per tile, face form
+        dim3 grid(c->tiles, c->members);
+        if (relax) stage_kernel<S2, FIN, BATHY, true, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+        else stage_kernel<S2, FIN, BATHY, false, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
     } else if (c->persist) {
         const int items = c->tiles * c->members;
         const int grid = std::min(items, c->persist_grid);
@@ -329,7 +334,7 @@ void choose_geometry(hsgn_ctx *c)
     }
     // fused step: stage 1 runs on the kept tile widened by 2w + 3 on each side
     const int wmax_fused = (LCAP - 2 - 6 - T_MIN) / 4;
-    c->fused = c->fused_on && c->tab.stages == 2 && !c->slab && w <= wmax_fused && c->picard == 0;
+    c->fused = c->fused_on && c->tab.stages == 2 && !c->slab && w <= wmax_fused && c->picard == 0 && !c->wb;
     w = std::max(3, std::min(w, (LCAP - 2 - T_MIN) / 2));
     const int maxT = c->fused ? LCAP - 2 - 6 - 4 * w : LCAP - 2 - 2 * w;
     int T;
@@ -376,6 +381,8 @@ hsgn_status ready(hsgn_ctx *c)
         return fail(c, HSGN_E_INVALID, "explicit / SGN schemes: flat bottom, no relaxation zones, no slabs");
     if (c->picard > 0 && (c->scheme != 0 || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
         return fail(c, HSGN_E_INVALID, "Picard passes: SI scheme without relaxation zones");
+    if (c->wb && (c->scheme != 0 || c->picard > 0))
+        return fail(c, HSGN_E_INVALID, "well-balanced form: SI scheme without Picard passes");
     if (c->scheme == 2 && c->filter_sigma > 0.0)
         return fail(c, HSGN_E_INVALID, "SGN scheme: no A19 filter (its Rusanov speed includes sqrt(g h))");
     if (c->scheme == 2 && c->sT <= 0) return fail(c, HSGN_E_INVALID, "SGN geometry not set");
@@ -1150,6 +1157,15 @@ hsgn_status hsgn_set_picard(hsgn_ctx *c, int32_t passes)
 {
     if (!c || passes < 0 || passes > 16) return HSGN_E_INVALID;
     c->picard = passes;
+    drop_graphs(c);
+    choose_geometry(c);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_well_balanced(hsgn_ctx *c, int32_t on)
+{
+    if (!c) return HSGN_E_INVALID;
+    c->wb = on != 0;
     drop_graphs(c);
     choose_geometry(c);
     return HSGN_OK;

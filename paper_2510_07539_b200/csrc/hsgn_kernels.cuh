@@ -320,7 +320,10 @@ struct RowCtx { double tau, tdx2, t2, lt2, lam, lam3, ltau, g, idx; };
 // Stores q^dag, H^dag, beta, delta at row r unless r < -1 (dead row); returns
 // h^R' (R_h plus the hydrostatic term) in hR_out.  Stage 2 reads R_h from the
 // delta array (sRh == sDe) before overwriting it with delta.
-template <bool BATHY>
+// WB (reading A25): the delta array takes the face coefficient
+// dhat_{r+1/2} = -(2 sigma^ - 1)/(3 h~) b1~ of rows r, r+1 instead (averages of
+// sigma = H/h^2, h and 1/beta1 over the two rows).
+template <bool BATHY, bool WB = false>
 __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const Params &P, int r, int start, int n,
                                            const double (&ch)[3], const double (&cq)[3],
                                            const double (&cH)[3], const double (&cW)[3],
@@ -363,7 +366,16 @@ __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const P
     const double ib1 = s2 * D;                                      // 1/beta1
     const double beta2 = 2.0 * C.lt2 * hE * D * D;                  // P:506 (= 2 lt2 ib1^2 / h^3)
     const double beta = a2 + C.lam * alpha * beta2 * Hd;
-    const double delta = alpha * ib1;
+    double delta = alpha * ib1;
+    if (WB) {
+        const double h1 = ch[2], s21 = h1 * h1, den1 = s21 + C.lt2;
+        const double Z1 = rcp(h1 * den1);
+        const double ih1 = den1 * Z1;
+        const double sg1 = cH[2] * ih1 * ih1;
+        const double ib11 = s21 * (h1 * Z1);
+        // -(2 (sg + sg1)/2 - 1)/(3 (hE + h1)/2) (ib1 + ib11)/2
+        delta = -(sg + sg1 - 1.0) * (ib1 + ib11) * rcp(3.0 * (hE + h1));
+    }
     if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; }
     hR_out = hRp;
     Wd_out = Wd;
@@ -710,7 +722,7 @@ __device__ __forceinline__ void prefetch_stage_item(const Params &P, const Bufs 
 // parities applied) and that U1; output staged in the dedicated buffer.  Once the arrays 0..3 are no longer read, the
 // loads of U^n for next_item (>= 0) are issued into them (prefetch).
 // ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, int MODE, bool PIC = false>
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, int MODE, bool PIC = false, bool WB = false>
 __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const Geom &G, int m, int s_cell,
                                            const StageC &S, double dtm, TileAcc &acc, int next_item,
                                            bool rt2)
@@ -825,7 +837,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], kap);
             const Face Fb = rusanov(Mm, P0);                          // face -1/2
             double Wd, beta, hRd;
-            row_update<BATHY>(st2, C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
+            row_update<BATHY, WB>(st2, C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
                                       sQd, sHd, sBe, sDe, Wd, beta, hRd);
         }
 #pragma unroll
@@ -852,7 +864,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
             Mr = Mn;
             double beta, hRr;
-            row_update<BATHY>(st2, C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
+            row_update<BATHY, WB>(st2, C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
                                       sQd, sHd, sBe, sDe, wd[i], beta, hRr);
             hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
             if (r >= G.klo && r < G.khi && !(beta > 0.0)) acc.err |= ERR_COERC;
@@ -905,6 +917,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // loads PCR goes over arrays 4..5 (later the filter), hbar into array 6 and
     // the own rows' E_h (BATHY) are copied to array 7.
     constexpr bool ALONE = (MODE == MODE_ALONE);
+    static_assert(!WB || ALONE, "A25 reads E_h of rows r +- 1 from array 0 (one CTA per tile)");
     double *sHB = ALONE ? sEq : sBe;                             // hbar[r], r in [0, L)
     double *pcr0 = ALONE ? smem + 2 * SROWS : smem + 4 * SROWS;  // 2 x 3 x NT doubles
     double *pcr1 = pcr0 + 3 * NT;
@@ -965,7 +978,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             // (r_{-1/2} = r_{L-1/2} = 0 through the beta ghosts set above)
             const double rl = t2h * (vb[i] + vb[i + 1]);
             const double rr = t2h * (vb[i + 1] + vb[i + 2]);
-            const double ml = lt2h * (vd[i] + vd[i + 1]), mr = lt2h * (vd[i + 1] + vd[i + 2]);
+            // (WB, A25: mu_{r+1/2} = 2 lt2h dhat_{r+1/2}, face values in vd)
+            const double ml = WB ? 2.0 * lt2h * vd[i] : lt2h * (vd[i] + vd[i + 1]);
+            const double mr = WB ? 2.0 * lt2h * vd[i + 1] : lt2h * (vd[i + 1] + vd[i + 2]);
             const double rhs = hRv[i] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
                                - ml * (vH[i + 1] - vH[i]);
             const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
@@ -1092,8 +1107,28 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         double hr = (i < MCH - 1) ? hb[i + 1] : hRn;
         if (r == 0) hl = h0;                           // Neumann at physical ends
         if (r == L - 1) hr = h0;
-        double qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
-        if (BATHY && act) {
+        double qb;
+        if (WB) {
+            // A25: qbar = q^dag - tau/(2 dx) (Phi_{r+1/2} + Phi_{r-1/2}) with the face
+            // fluxes Phi = beta~ (hbar_R - hbar_L) + lam dhat (H^dag_R - H^dag_L)
+            // + g h~ (b_R - b_L) (E-depth h~); zero at physical (and cut) ends
+            double Phr = 0.5 * (vb[i + 1] + vb[i + 2]) * (hr - h0) + lam * vd[i + 1] * (vH[i + 2] - vH[i + 1]);
+            double Phl = 0.5 * (vb[i] + vb[i + 1]) * (h0 - hl) + lam * vd[i] * (vH[i + 1] - vH[i]);
+            if (BATHY && act) {
+                const double bm = bathy_at(P, start + r - 1), bp = bathy_at(P, start + r + 1);
+                const double bz = bathy_at(P, start + r);
+                const double e0 = sEhc[r];
+                bbv[i] = bz;
+                Phr += 0.5 * g * (e0 + sEhc[r + 1]) * (bp - bz);
+                Phl += 0.5 * g * (sEhc[r - 1] + e0) * (bz - bm);
+            }
+            if (r == 0) Phl = 0.0;
+            if (r == L - 1) Phr = 0.0;
+            qb = vq[i + 1] - tdx2 * (Phr + Phl);
+        } else {
+            qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
+        }
+        if (BATHY && act && !WB) {
             const double bm = bathy_at(P, start + r - 1);
             const double bp = bathy_at(P, start + r + 1);
             bbv[i] = bathy_at(P, start + r);
@@ -1342,7 +1377,7 @@ __device__ unsigned long long g_exp[8];
 #define EXP_T(v)
 #endif
 
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false>
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false, bool WB = false>
 __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
 {
     EXP_T(t0);
@@ -1395,7 +1430,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
     } else {
         const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
-        stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE, PIC>(P, B, G, m, s, S, dtm, acc, -1, false);
+        stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE, PIC, WB>(P, B, G, m, s, S, dtm, acc, -1, false);
         store_tile(B, mo, s, e - s, false, P.T);
     }
     EXP_T(t2);

@@ -58,7 +58,7 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_set_state", "hsgn_get_state", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
            "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
            "hsgn_set_fused", "hsgn_get_fused", "hsgn_set_persistent", "hsgn_set_scheme",
-           "hsgn_set_picard",
+           "hsgn_set_picard", "hsgn_set_well_balanced",
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
            "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl"]
 
@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
         "hsgn_set_persistent": (st, [vp, C.c_int32]),
         "hsgn_set_scheme": (st, [vp, C.c_int32, C.c_int32]),
         "hsgn_set_picard": (st, [vp, C.c_int32]),
+        "hsgn_set_well_balanced": (st, [vp, C.c_int32]),
         "hsgn_status_string": (C.c_char_p, [st]),
         "hsgn_group_create": (st, [C.POINTER(vp), C.c_int32, C.POINTER(vp)]),
         "hsgn_group_run_steps": (st, [vp, C.c_int64]),
@@ -227,6 +228,10 @@ class Solver:
     def set_picard(self, passes: int) -> None:
         """A24 Picard passes of the SI depth solve (0 = the paper's linearised stage)."""
         self._chk(self.L.hsgn_set_picard(self.ctx, int(passes)))
+
+    def set_well_balanced(self, on: bool = True) -> None:
+        """A25 exactly well-balanced face form of the SI stage (default off: the paper's)."""
+        self._chk(self.L.hsgn_set_well_balanced(self.ctx, 1 if on else 0))
 
     def set_persistent(self, on: bool) -> None:
         """Persistent per-stage kernels with next-tile prefetch (default) or one

@@ -44,12 +44,13 @@ def rel_err(gpu, ref, scales=None):
     return max(out)
 
 
-def oracle_run(w, members, steps=None, t_end=None, order=2, tableau=None, dt_fixed=0.0, picard=0):
+def oracle_run(w, members, steps=None, t_end=None, order=2, tableau=None, dt_fixed=0.0, picard=0,
+               wb=False):
     jobs = []
     for m in members:
         o = O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, order=order, b=w.b,
                      filter_sigma=w.filter_sigma, tableau=tableau, relax=w.meta.get("relax"),
-                     picard=picard)
+                     picard=picard, wb=wb)
         jobs.append((o, w.state(m)))
     res = O.run_members(jobs, cfl=w.cfl, mcfl=w.mcfl, steps=steps, t_end=t_end, dt_fixed=dt_fixed)
     return [r[0] for r in res], [r[1] for r in res]

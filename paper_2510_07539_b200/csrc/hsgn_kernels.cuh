@@ -510,20 +510,30 @@ __device__ __forceinline__ void fused_geom(const Params &P, int s, int e, int w,
 }
 
 // TMA bulk loads need 16-B aligned destinations: shift the arrays by the parity
-// of the first copied cell (interior tiles).
+// of the first copied cell.  Interior tiles copy one range per field; tiles that
+// wrap around a periodic domain of even n copy two (cells a0 .. n-1, then
+// 0 .. cnt - seg1 - 1), both 16-B aligned because a0 and n are even.
 struct LoadPlan {
-    int a0, cnt;      // first copied cell, count (even)
+    int a0, cnt;      // first copied cell (in [0, n)), count (even)
+    int seg1;         // cells in the first range (== cnt unless the tile wraps)
     bool bulk;
 };
 
 __device__ __forceinline__ LoadPlan load_plan(const Params &P, size_t mo, Geom &G)
 {
     LoadPlan Lp;
-    const int d = G.interior ? int((mo + size_t(G.start - 3)) & 1) : 0;
+    const bool wrap = !G.interior && P.bcl == BC_PERIODIC && P.bcr == BC_PERIODIC && (P.n & 1) == 0;
+    const int d = (G.interior || wrap) ? int((mo + size_t(G.start - 3)) & 1) : 0;
     G.abase = 3 + d;
     Lp.a0 = G.start - 3 - d;
     Lp.cnt = (G.L + 6 + d + 1) & ~1;
+    Lp.seg1 = Lp.cnt;
     Lp.bulk = G.interior && (Lp.a0 >= 0) && (Lp.a0 + Lp.cnt <= P.n);
+    if (wrap && Lp.cnt <= P.n) {
+        if (Lp.a0 < 0) Lp.a0 += P.n;
+        Lp.seg1 = min(Lp.cnt, P.n - Lp.a0);
+        Lp.bulk = true;
+    }
     return Lp;
 }
 
@@ -547,8 +557,9 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
     if (Lp.bulk) {
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            const unsigned bytes = unsigned(Lp.cnt) * 8u;
-            const unsigned tx = bytes * ((DO_UN ? 4u : 0u) + (DO_U1 ? 4u : 0u));
+            const unsigned bytes = unsigned(Lp.seg1) * 8u;
+            const unsigned bytes2 = unsigned(Lp.cnt - Lp.seg1) * 8u;     // wrapped part
+            const unsigned tx = unsigned(Lp.cnt) * 8u * ((DO_UN ? 4u : 0u) + (DO_U1 ? 4u : 0u));
             if (PART == LD_UN)
                 asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;\n" ::"r"(mb), "r"(tx) : "memory");
             else
@@ -564,6 +575,19 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
                 bulk_g2s(smem + 4 * SROWS, B.U1[1] + gsrc, bytes, mb);
                 bulk_g2s(smem + 5 * SROWS, B.U1[2] + gsrc, bytes, mb);
                 bulk_g2s(smem + 6 * SROWS, B.U1[3] + gsrc, bytes, mb);
+            }
+            if (bytes2) {
+                const int k2 = Lp.seg1;
+                if (DO_UN) {
+#pragma unroll
+                    for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS + k2, B.Un[f] + mo, bytes2, mb);
+                }
+                if (DO_U1) {
+                    bulk_g2s(smem + 7 * SROWS + k2, B.U1[0] + mo, bytes2, mb);
+                    bulk_g2s(smem + 4 * SROWS + k2, B.U1[1] + mo, bytes2, mb);
+                    bulk_g2s(smem + 5 * SROWS + k2, B.U1[2] + mo, bytes2, mb);
+                    bulk_g2s(smem + 6 * SROWS + k2, B.U1[3] + mo, bytes2, mb);
+                }
             }
         }
     } else {
@@ -752,8 +776,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // ---- in-place pass: E, R, H = K - 1.5 h b (A9), wall parity
     {
         const bool raw = !fused2;                     // inputs not yet in H-form / parity
-        const bool wall_ghosts = (left_phys && P.bcl == BC_WALL) || (right_phys && P.bcr == BC_WALL);
-        if (st2 || (raw && (BATHY || wall_ghosts))) {
+        // q parity of ghost rows mirrored at a wall (raw rows outside [0, n))
+        const bool wall_par = raw && !G.interior && (P.bcl == BC_WALL || P.bcr == BC_WALL);
+        if (st2 || (raw && BATHY) || wall_par) {
             // two rows per thread and iteration with 16-B shared accesses: row r of
             // array k sits at smem[k * SROWS + abase + r], pairs start at even
             // offsets (the spare rows at either end are scratch)
@@ -764,7 +789,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 double2 *v = reinterpret_cast<double2 *>(smem + p);
                 double2 eh = v[0], eq = v[SROWS / 2], eK = v[SROWS], eW = v[3 * SROWS / 2];
                 double par0 = 1.0, par1 = 1.0;
-                if (raw && !G.interior) {              // q parity of wall ghosts
+                if (wall_par) {
                     (void)map_cell(start + r, n, P.bcl, P.bcr, par0);
                     (void)map_cell(start + r + 1, n, P.bcl, P.bcr, par1);
                 }
@@ -1033,8 +1058,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         // step.  The reduced couplings shrink like e_{s+1} <= e_s^2/(1-2e_s^2)
         // (e = max |A|,|C|), so PCR stops once e^(2^s) <= 2^-64: the rows are
         // then decoupled to below round-off (x_k = D_k).
-        double *cur = pcr0, *nxt = pcr1;
-        cur[tid] = A_; cur[NT + tid] = C_; cur[2 * NT + tid] = D_;
+        pcr0[tid] = A_; pcr0[NT + tid] = C_; pcr0[2 * NT + tid] = D_;
         {
             const float ea = float(fabs(A_)), ec = float(fabs(C_));
             const float ev = warp_max_nonneg(ea > ec ? ea : ec);
@@ -1049,15 +1073,24 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             float e0 = 0.0f;
 #pragma unroll
             for (int q = 0; q < NT / 32; q++) e0 = fmaxf(e0, s_redf[q]);
-            if (e0 < 0.4f) {                       // repeated squaring, 10% margin per step
-                float ee = e0 * 1.1f;
-                int sdl = 1;
-                while (sdl < NT && ee > 5.42e-20f) { ee = ee * ee * 1.1f; sdl <<= 1; }   // 2^-64
-                lim = sdl;
+            if (e0 < 0.4f) {
+                // repeated squaring with a 10 % margin per step, ee_0 = 1.1 e0,
+                // ee_{s+1} = 1.1 ee_s^2, stops at the first s with ee_s <= 2^-64:
+                // log2 ee_s = 2^s (log2 e0 + 2 log2 1.1) - log2 1.1, so
+                // 2^s >= (64 - log2 1.1) / -(log2 e0 + 2 log2 1.1), rounded up to a
+                // power of two (margins 64 and 0.28 cover the log2 approximation);
+                // e0 = 0 gives q = 0 and no PCR step
+                const float q = __fdividef(64.0f, -__log2f(e0) - 0.28f);
+                const int qi = int(ceilf(q));
+                lim = qi <= 1 ? 1 : min(NT, 1 << (32 - __clz(qi - 1)));
             }
         }
-#pragma unroll 1
-        for (int sd = 1; sd < lim; sd <<= 1) {
+#pragma unroll
+        for (int lev = 0; (1 << lev) < NT; lev++) {
+            const int sd = 1 << lev;
+            if (sd >= lim) break;
+            double *const cur = (lev & 1) ? pcr1 : pcr0;
+            double *const nxt = (lev & 1) ? pcr0 : pcr1;
             const int km = tid - sd, kp = tid + sd;
             double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
             if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
@@ -1069,7 +1102,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             A_ = An; C_ = Cn; D_ = Dn;
             nxt[tid] = A_; nxt[NT + tid] = C_; nxt[2 * NT + tid] = D_;
             __syncthreads();
-            double *tmp = cur; cur = nxt; nxt = tmp;
         }
         const double Xk = D_;
         double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
@@ -1160,6 +1192,17 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     if (filt) __syncthreads();
     const double sig16 = P.filter_sigma * (1.0 / 16.0);
     const double t_new = (fin && RELAX) ? P.t[P.kpar * members + m] + dtm : 0.0;
+    // filter windows over rows r0-2 .. r0+MCH+1: own rows from registers, two halo
+    // rows each side from shared memory (threads whose window meets a physical
+    // end mirror per row below)
+    const bool fwin = filt && (!(left_phys || right_phys) || (r0 >= 2 && r0 + MCH + 2 <= L));
+    double xq[MCH + 4], xw[MCH + 4];
+    if (fwin) {
+        xq[0] = sQb[r0 - 2]; xq[1] = sQb[r0 - 1]; xq[MCH + 2] = sQb[r0 + MCH]; xq[MCH + 3] = sQb[r0 + MCH + 1];
+        xw[0] = sWb[r0 - 2]; xw[1] = sWb[r0 - 1]; xw[MCH + 2] = sWb[r0 + MCH]; xw[MCH + 3] = sWb[r0 + MCH + 1];
+#pragma unroll
+        for (int i = 0; i < MCH; i++) { xq[i + 2] = qbv[i]; xw[i + 2] = Wbv[i]; }
+    }
     // final values into (hb, qbv, HdD := K or H, Wbv)
 #pragma unroll
     for (int i = 0; i < MCH; i++) {
@@ -1168,9 +1211,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         double qo = qbv[i], wo = Wbv[i];
         if (filt) {
             double fq[5], fw[5];
-            if (!(left_phys || right_phys) || (r >= 2 && r + 2 < L)) {
+            if (fwin) {
 #pragma unroll
-                for (int k = 0; k < 5; k++) { fq[k] = sQb[r + k - 2]; fw[k] = sWb[r + k - 2]; }
+                for (int k = 0; k < 5; k++) { fq[k] = xq[i + k]; fw[k] = xw[i + k]; }
             } else {
 #pragma unroll
                 for (int k = -2; k <= 2; k++) {
@@ -1404,7 +1447,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             const LoadPlan Lf = load_plan(P, mof, Gf);
             if (Lf.bulk) {
                 const size_t off = mof + size_t(Lf.a0);
-                const unsigned bytes = unsigned(Lf.cnt) * 8u;
+                const unsigned bytes = unsigned(Lf.seg1) * 8u;       // (first range only)
 #pragma unroll
                 for (int f = 0; f < 4; f++) prefetch_l2(B.Un[f] + off, bytes);
                 if (STAGE2) {

@@ -1127,8 +1127,16 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // HdD = H^dag / (hbar^2 + lam tau^2): Hbar = HdD hbar^2 and, in the
     // final stage, sigma = Hbar / hbar^2 = HdD for the dt maxima
     double qbv[MCH], HdD[MCH], Wbv[MCH], bbv[MCH], ihv[MCH];
-    const double hLn = (r0 > 0 && r0 - 1 < L) ? sHB[r0 - 1] : 0.0;
-    const double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
+    // Neumann at physical ends (hbar_{-1} := hbar_0, hbar_L := hbar_{L-1}); at cut
+    // tile ends rows 0 and L-1 are overlap rows whose qbar is never used (w >= 3)
+    const double hLn = r0 > 0 ? ((r0 - 1 < L) ? sHB[r0 - 1] : 0.0) : hb[0];
+    double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
+    if (right_phys) {
+        if (r0 + MCH == L) hRn = hb[MCH - 1];
+#pragma unroll
+        for (int i = 1; i < MCH; i++)
+            if (r0 + i == L) hb[i] = hb[i - 1];       // (row L itself is not kept)
+    }
 #pragma unroll
     for (int i = 0; i < MCH; i++) {
         const int r = r0 + i;
@@ -1137,8 +1145,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         const double h0 = hb[i];
         double hl = (i > 0) ? hb[i - 1] : hLn;
         double hr = (i < MCH - 1) ? hb[i + 1] : hRn;
-        if (r == 0) hl = h0;                           // Neumann at physical ends
-        if (r == L - 1) hr = h0;
         double qb;
         if (WB) {
             // A25: qbar = q^dag - tau/(2 dx) (Phi_{r+1/2} + Phi_{r-1/2}) with the face
@@ -1210,11 +1216,15 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         if (r < klo || r >= khi) continue;
         double qo = qbv[i], wo = Wbv[i];
         if (filt) {
-            double fq[5], fw[5];
+            // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
+            auto f5 = [&](double a0, double a1, double a2, double a3, double a4) {
+                return a2 - sig16 * (a0 - 4.0 * a1 + 6.0 * a2 - 4.0 * a3 + a4);
+            };
             if (fwin) {
-#pragma unroll
-                for (int k = 0; k < 5; k++) { fq[k] = xq[i + k]; fw[k] = xw[i + k]; }
+                qo = f5(xq[i], xq[i + 1], xq[i + 2], xq[i + 3], xq[i + 4]);
+                wo = f5(xw[i], xw[i + 1], xw[i + 2], xw[i + 3], xw[i + 4]);
             } else {
+                double fq[5], fw[5];
 #pragma unroll
                 for (int k = -2; k <= 2; k++) {
                     int rr = r + k;
@@ -1227,10 +1237,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                     fq[k + 2] = pq * sQb[rr];
                     fw[k + 2] = sWb[rr];
                 }
+                qo = f5(fq[0], fq[1], fq[2], fq[3], fq[4]);
+                wo = f5(fw[0], fw[1], fw[2], fw[3], fw[4]);
             }
-            // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
-            qo = fq[2] - sig16 * (fq[0] - 4.0 * fq[1] + 6.0 * fq[2] - 4.0 * fq[3] + fq[4]);
-            wo = fw[2] - sig16 * (fw[0] - 4.0 * fw[1] + 6.0 * fw[2] - 4.0 * fw[3] + fw[4]);
             if (!isfinite(qo + wo)) acc.err |= ERR_NONFINITE;
         }
         double h0 = hb[i];

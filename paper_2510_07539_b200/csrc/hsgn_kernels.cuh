@@ -279,10 +279,12 @@ __device__ __forceinline__ void muscl_pair(const double (&wh)[3], const double (
                                            const double (&wH)[3], const double (&wW)[3],
                                            double kap, FState &Pl, FState &M)
 {
-    const double dh = kap * (wh[2] - wh[0]), dq = kap * (wq[2] - wq[0]);
-    const double dH = kap * (wH[2] - wH[0]), dW = kap * (wW[2] - wW[0]);
-    Pl.h = wh[1] - dh; Pl.q = wq[1] - dq; Pl.H = wH[1] - dH; Pl.W = wW[1] - dW;
-    M.h = wh[1] + dh; M.q = wq[1] + dq; M.H = wH[1] + dH; M.W = wW[1] + dW;
+    const double dh = wh[2] - wh[0], dq = wq[2] - wq[0];
+    const double dH = wH[2] - wH[0], dW = wW[2] - wW[0];
+    Pl.h = fma(-kap, dh, wh[1]); Pl.q = fma(-kap, dq, wq[1]);
+    Pl.H = fma(-kap, dH, wH[1]); Pl.W = fma(-kap, dW, wW[1]);
+    M.h = fma(kap, dh, wh[1]); M.q = fma(kap, dq, wq[1]);
+    M.H = fma(kap, dH, wH[1]); M.W = fma(kap, dW, wW[1]);
     const double Z = rcp(Pl.h * M.h);
     Pl.u = Pl.q * (M.h * Z);
     M.u = M.q * (Pl.h * Z);
@@ -290,15 +292,17 @@ __device__ __forceinline__ void muscl_pair(const double (&wh)[3], const double (
 
 // Rusanov flux of R_E at a face (A4): alpha = max(|u-|, |u+|),
 // F = 1/2 (F(U-) + F(U+)) - 1/2 alpha (U+ - U-) for F^q = q u, F^H = H u, F^W = W u.
-// Returned as 2F (the 1/2 is folded into the tau/(2 dx) of the predictor: exact).
+// Returned as 2F (the 1/2 is folded into the tau/(2 dx) of the predictor: exact),
+// in the form 2F = v- (u- + alpha) + v+ (u+ - alpha) (two products per field).
 __device__ __forceinline__ Face rusanov(const FState &m, const FState &p)
 {
     const double am = fabs(m.u), ap = fabs(p.u);
     const double a = am > ap ? am : ap;
+    const double cm = m.u + a, cp = p.u - a;
     Face F;
-    F.q = fma(m.q, m.u, p.q * p.u) - a * (p.q - m.q);
-    F.H = fma(m.H, m.u, p.H * p.u) - a * (p.H - m.H);
-    F.W = fma(m.W, m.u, p.W * p.u) - a * (p.W - m.W);
+    F.q = fma(m.q, cm, p.q * cp);
+    F.H = fma(m.H, cm, p.H * cp);
+    F.W = fma(m.W, cm, p.W * cp);
     return F;
 }
 
@@ -313,7 +317,7 @@ __device__ __forceinline__ FState muscl_plus_next(const double (&wh)[3], const d
     return muscl_plus(th, tq, tH, tW, kap);
 }
 
-struct RowCtx { double tau, tdx2, t2, lt2, lam, lam3, ltau, g, idx; };
+struct RowCtx { double tau, tdx2, t2, lt2, lam, lam3, ltau, g, idx, c23; };
 
 // Predictor (A9) and coefficients at E (A2) of
 // one row r; E rows r-1, r, r+1 in (ch, cq, cH, cW); fluxes at r -+ 1/2.
@@ -360,13 +364,14 @@ __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const P
     const double Wd = WR - C.tdx2 * (Fr.W - Fl.W) + C.ltau;
     const double Hd = HR - C.tdx2 * (Fr.H - Fl.H) - 1.5 * C.tau * qE * Dxb + C.tau * Wd;
     const double qd = qR - C.tdx2 * (Fr.q - Fl.q) - ptil_term;
-    // coefficients at E
-    const double alpha = -(2.0 * sg - 1.0) * ihE * (1.0 / 3.0);
-    const double a2 = C.g * hE + C.lam3 * sg * (3.0 * sg - 1.0);
-    const double ib1 = s2 * D;                                      // 1/beta1
-    const double beta2 = 2.0 * C.lt2 * hE * D * D;                  // P:506 (= 2 lt2 ib1^2 / h^3)
-    const double beta = a2 + C.lam * alpha * beta2 * Hd;
-    double delta = alpha * ib1;
+    // coefficients at E: alpha = -(2 sg - 1)/(3 h), a^2,
+    // 1/beta1 = h^2 D, beta2 = 2 lam tau^2 h D^2 with
+    // D = 1/(h^2 + lam tau^2); so lam alpha beta2 = -(2/3) lam^2 tau^2 (2 sg - 1) D^2
+    // and delta = alpha/beta1 = -(2 sg - 1)/3 h D
+    const double t = 2.0 * sg - 1.0;
+    const double a2 = fma(C.lam3 * sg, 3.0 * sg - 1.0, C.g * hE);
+    const double beta = fma(-C.c23 * t, (D * D) * Hd, a2);
+    double delta = (t * (-1.0 / 3.0)) * (hE * D);
     if (WB) {
         const double h1 = ch[2], s21 = h1 * h1, den1 = s21 + C.lt2;
         const double Z1 = rcp(h1 * den1);
@@ -374,7 +379,7 @@ __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const P
         const double sg1 = cH[2] * ih1 * ih1;
         const double ib11 = s21 * (h1 * Z1);
         // -(2 (sg + sg1)/2 - 1)/(3 (hE + h1)/2) (ib1 + ib11)/2
-        delta = -(sg + sg1 - 1.0) * (ib1 + ib11) * rcp(3.0 * (hE + h1));
+        delta = -(sg + sg1 - 1.0) * (s2 * D + ib11) * rcp(3.0 * (hE + h1));
     }
     if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; }
     hR_out = hRp;
@@ -842,6 +847,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         RowCtx C{};
         C.tau = tau; C.tdx2 = tdx2; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
         C.ltau = ltau; C.g = g; C.idx = idx1;
+        C.c23 = (2.0 / 3.0) * lam * lt2;
         double wh[3], wq[3], wH[3], wW[3];
 #pragma unroll
         for (int k = 0; k < 3; k++) {                 // rows r0-2 .. r0

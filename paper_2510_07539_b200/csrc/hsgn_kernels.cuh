@@ -384,7 +384,7 @@ __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const P
     if (live) { sQd[rr] = qd; sHd[rr] = Hd; sBe[rr] = beta; sDe[rr] = delta; }
     hR_out = hRp;
     Wd_out = Wd;
-    beta_out = live ? beta : 1.0;
+    beta_out = live ? beta : 2.2250738585072014e-308;   // dead rows: neutral for both checks
 }
 
 __device__ __forceinline__ double warp_max(double v)
@@ -668,6 +668,7 @@ struct TileAcc {
     double umax, numax, rho;
     unsigned int err;
     int wmin;                     // narrowest truncated overlap (1 << 30: none)
+    int bhi;                      // max high word of beta over the rows (rho bound)
 };
 
 enum { MODE_ALONE = 0, MODE_FUSED = 1, MODE_PERSIST = 2 };
@@ -898,7 +899,11 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             row_update<BATHY, WB>(st2, C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
                                       sQd, sHd, sBe, sDe, wd[i], beta, hRr);
             hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
-            if (r >= G.klo && r < G.khi && !(beta > 0.0)) acc.err |= ERR_COERC;
+            // coercivity on every row of the tile (overlap rows are real
+            // cells, and the kept rows' solve relies on them too); the rho bound
+            // of the overlap check from max beta (high words: +1 ulp of 2^-20)
+            if (!(beta > 0.0)) acc.err |= ERR_COERC;
+            acc.bhi = max(acc.bhi, __double2hiint(beta));
             Fl = Fr;
         }
     } else {
@@ -990,6 +995,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 const double b2 = 2.0 * lt2 / (b1 * b1 * hn2 * hn);
                 const double be = a2v[i] + lam * alv[i] * b2 * vH[i + 1];
                 if (r >= G.klo && r < G.khi && !(be > 0.0)) acc.err |= ERR_COERC;
+                acc.bhi = max(acc.bhi, __double2hiint(be));
                 sBe[r] = be;
                 sDe[r] = alv[i] / b1;
             }
@@ -1015,7 +1021,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const double rhs = hRv[i] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
                                - ml * (vH[i + 1] - vH[i]);
             const double a = -rl, c = -rr, dg = 1.0 + rl + rr;
-            acc.rho = rr > acc.rho ? rr : acc.rho;
             if (i == 0) {
                 const double inv = rcp(dg);
                 am[0] = a * inv; cm[0] = c * inv; dm[0] = rhs * inv;
@@ -1091,12 +1096,8 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 lim = qi <= 1 ? 1 : min(NT, 1 << (32 - __clz(qi - 1)));
             }
         }
-#pragma unroll
-        for (int lev = 0; (1 << lev) < NT; lev++) {
-            const int sd = 1 << lev;
-            if (sd >= lim) break;
-            double *const cur = (lev & 1) ? pcr1 : pcr0;
-            double *const nxt = (lev & 1) ? pcr0 : pcr1;
+        // one PCR level at distance sd (compile-time), cur -> nxt
+        auto level = [&](const int sd, const double *cur, double *nxt) {
             const int km = tid - sd, kp = tid + sd;
             double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
             if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
@@ -1108,7 +1109,15 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             A_ = An; C_ = Cn; D_ = Dn;
             nxt[tid] = A_; nxt[NT + tid] = C_; nxt[2 * NT + tid] = D_;
             __syncthreads();
-        }
+        };
+        static_assert(NT == 128, "PCR levels below are written out for 128 unknowns");
+        if (lim > 1) level(1, pcr0, pcr1);
+        if (lim > 2) level(2, pcr1, pcr0);
+        if (lim > 4) level(4, pcr0, pcr1);
+        if (lim > 8) level(8, pcr1, pcr0);
+        if (lim > 16) level(16, pcr0, pcr1);
+        if (lim > 32) level(32, pcr1, pcr0);
+        if (lim > 64) level(64, pcr0, pcr1);
         const double Xk = D_;
         double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
         if (lane == 31) s_xch[wid][0] = Xk;       // last chunk of this warp
@@ -1123,6 +1132,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     }
     __syncthreads();
     }   // Picard passes
+
+    // rho = max (tau/dx)^2 (beta_i + beta_{i+1})/2 <= t2 max beta
+    acc.rho = fmax(acc.rho, t2 * __hiloint2double(acc.bhi + 1, 0));
 
     // ---- phase 3: back-substitution, own rows ------------------
     const bool filt = fin && (P.filter_sigma > 0.0);
@@ -1483,7 +1495,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     EXP_T(t1);
     if (err0) return;
 
-    TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
+    TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
     if (dtm == 0.0) {
         carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
     } else {
@@ -1547,7 +1559,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_pkernel(const Params P, c
         const double lam = s_rc[1];
         if (s_err) break;                 // an error was latched (seen at the prefetch)
         if (tid == 0) grab = int(atomicAdd(ctr, 1u));      // used at the item's end
-        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
+        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
         if (dtm == 0.0) {
             carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
             __syncthreads();
@@ -1614,7 +1626,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) step_kernel(const Params P, con
             return;
         }
 
-        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30};
+        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
         if (dtm == 0.0) {
             carry_tile<true, BATHY>(P, B, mo, s, e, lam, acc);
             __syncthreads();

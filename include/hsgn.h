@@ -177,6 +177,28 @@ hsgn_status hsgn_set_state(hsgn_ctx *ctx, const double *h, const double *q, cons
  * of n_members, or NULL) receives each member's time.  Synchronises. */
 hsgn_status hsgn_get_state(hsgn_ctx *ctx, double *h, double *q, double *K, double *W,
                            double *t);
+/* Whole ensemble job from and to host memory, pipelined over member chunks
+ * (DESIGN.md section 7): the members are split into `chunks` contiguous
+ * groups (at most 16 and n_members); for each group, in order, its initial
+ * state (h, q, K, W: n_members * n_cells doubles each, member-major, as for
+ * hsgn_set_state) is copied in on one copy stream, n_steps steps run on the
+ * context's stream (exactly as hsgn_set_state + hsgn_run_steps would: members
+ * are independent, so each member's result is bitwise the same), and its final
+ * state and times are copied out on a second copy stream -- group k+1's input
+ * and group k-1's output transfers overlap group k's steps.  Use page-locked
+ * host buffers for the overlap (pageable ones work, serialised).  t0: start
+ * time of every member; t_out (n_members doubles, or NULL) receives the final
+ * times.  Synchronises before returning.  Afterwards the context holds no state
+ * (call hsgn_set_state before hsgn_step / hsgn_run_steps).  Not for slab
+ * contexts or the SGN scheme (its tile geometry depends on the whole state).
+ * Errors: HSGN_E_INVALID (null pointer, n_steps < 0, chunks < 1, slab / SGN),
+ * HSGN_E_NOWORKSPACE, HSGN_E_CUDA; a device error in a group (dry bed,
+ * coercivity, non-finite, overlap) returns that status, and that group's
+ * outputs hold its last committed state and times. */
+hsgn_status hsgn_run_host(hsgn_ctx *ctx, const double *h, const double *q, const double *K,
+                          const double *W, double t0, int64_t n_steps, double *h_out,
+                          double *q_out, double *K_out, double *W_out, double *t_out,
+                          int32_t chunks);
 
 /* ---- stepping ------------------------------------------------------------ */
 

@@ -30,8 +30,16 @@ constexpr int GRAPH_STEPS = 18;   // steps per captured graph: a multiple of 6, 
 constexpr int POLL_STEPS = 256;   // advance_to polls the device every POLL_STEPS
 constexpr int T_MIN = 64;         // smallest kept tile (bounds the partials workspace)
 constexpr int H_MAX = (LCAP - 2 - T_MIN) / 2 + 3;   // largest slab halo (overlap + stencil)
+constexpr int KIDS_MAX = 16;      // member chunks of hsgn_run_host
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// small per-member arrays of one member chunk of hsgn_run_host
+size_t kid_small_bytes(int n, int cnt)
+{
+    return align256(2 * size_t(cnt) * 8) + 2 * align256(size_t(cnt) * 8) + align256(6 * size_t(cnt) * 8) +
+           align256(size_t(cnt) * ((n + T_MIN - 1) / T_MIN + 1) * 4 * 8) + 512;
+}
 
 }  // namespace
 
@@ -89,6 +97,16 @@ struct hsgn_ctx {
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
     std::string last_error;
+    // hsgn_run_host pipeline: member-chunk views of this context (their state
+    // buffers are slices of ours, their small arrays live in the workspace tail)
+    std::vector<hsgn_ctx *> kids;
+    long long gen = 0, kids_gen = -1;   // settings generation (bumped by drop_graphs)
+    char *kid_ws = nullptr;
+    cudaStream_t cp_in = nullptr, cp_out = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_in[16] = {}, ev_done[16] = {};
+    long long *kstat = nullptr;         // pinned [16][2]: error bits, committed steps
+    double *tstage = nullptr;           // pinned [n_members]: final times (a pageable
+                                        // destination would block the enqueue loop)
 };
 
 namespace {
@@ -299,6 +317,7 @@ void drop_graphs(hsgn_ctx *c)
 {
     for (auto &gx : c->graph)
         if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
+    c->gen++;                     // every setter passes here: member-chunk views are stale
 }
 
 hsgn_status set_ctrl(hsgn_ctx *c, double t_end, double dt_fixed)
@@ -606,6 +625,94 @@ hsgn_status reconcile(hsgn_ctx *c, unsigned int *bits_out = nullptr)
     return st;
 }
 
+void free_kids(hsgn_ctx *c)
+{
+    for (hsgn_ctx *k : c->kids) { drop_graphs(k); delete k; }
+    c->kids.clear();
+    c->kids_gen = -1;
+}
+
+__global__ void fill_kernel(double *p, int count, double v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) p[i] = v;
+}
+
+// Member-chunk views for hsgn_run_host: chunk k = members [m0, m1) with the
+// same settings and geometry as c, state buffers = slices of c's, own small
+// arrays in the workspace tail, c's stream.  Rebuilt when a setter ran.
+hsgn_status make_kids(hsgn_ctx *c, int chunks)
+{
+    if (int(c->kids.size()) == chunks && c->kids_gen == c->gen) return HSGN_OK;
+    free_kids(c);
+    char *q = c->kid_ws;
+    for (int k = 0; k < chunks; k++) {
+        const int m0 = int((long long)c->members * k / chunks), m1 = int((long long)c->members * (k + 1) / chunks);
+        const int cnt = m1 - m0;
+        hsgn_ctx *kc = new hsgn_ctx();
+        kc->desc = c->desc;
+        kc->desc.n_members = cnt;
+        kc->stream = c->stream;
+        kc->device = c->device;
+        kc->n = c->n; kc->members = cnt; kc->dx = c->dx;
+        kc->g = c->g; kc->cfl = c->cfl; kc->mcfl = c->mcfl; kc->h_min = c->h_min;
+        kc->lam.assign(c->lam.begin() + m0, c->lam.begin() + m1);
+        kc->have_params = true;
+        kc->bathy = c->bathy;
+        kc->tab = c->tab; kc->aI1 = c->aI1; kc->aI2 = c->aI2; kc->wE = c->wE; kc->wR = c->wR;
+        kc->filter_sigma = c->filter_sigma;
+        kc->relax = c->relax;
+        kc->fused_on = c->fused_on; kc->persist = c->persist;
+        kc->scheme = c->scheme; kc->x_stages = c->x_stages;
+        kc->picard = c->picard; kc->wb = c->wb;
+        kc->ws = c->ws;
+        for (int bi = 0; bi < 3; bi++)
+            for (int f = 0; f < 4; f++) kc->buf[bi][f] = c->buf[bi][f] + size_t(m0) * c->n;
+        kc->b = c->b;
+        kc->lamd = c->lamd + m0;
+        kc->t = (double *)q; q += align256(2 * size_t(cnt) * 8);
+        kc->dt = (double *)q; q += align256(size_t(cnt) * 8);
+        kc->dt_used = (double *)q; q += align256(size_t(cnt) * 8);
+        kc->maxes = (unsigned long long *)q; q += align256(6 * size_t(cnt) * 8);
+        kc->partials = (double *)q; q += align256(size_t(cnt) * ((c->n + T_MIN - 1) / T_MIN + 1) * 4 * 8);
+        kc->err = (unsigned int *)q;
+        kc->done = (unsigned int *)(q + 4);
+        kc->steps = (long long *)(q + 8);
+        kc->rho_obs = (unsigned long long *)(q + 16);
+        kc->work = (unsigned int *)(q + 32);
+        q += 256;
+        kc->ctrl = (Ctrl *)q;
+        q += 256;
+        choose_geometry(kc);
+        c->kids.push_back(kc);
+    }
+    c->kids_gen = c->gen;
+    return HSGN_OK;
+}
+
+// hsgn_set_state's device part for a member-chunk view whose U^n slice was
+// copied in on another stream: t = t0, dt/maxima/error words cleared, dt
+// maxima of the initial state (no host synchronisation).
+hsgn_status kid_state_init(hsgn_ctx *kc, double t0)
+{
+    fill_kernel<<<(kc->members + 255) / 256, 256, 0, kc->stream>>>(kc->t, kc->members, t0);
+    CUDA_TRY(kc, cudaMemsetAsync(kc->dt, 0, kc->members * sizeof(double), kc->stream));
+    CUDA_TRY(kc, cudaMemsetAsync(kc->maxes, 0, 6 * size_t(kc->members) * 8, kc->stream));
+    CUDA_TRY(kc, cudaMemsetAsync(kc->err, 0, 512, kc->stream));   // scalars + ctrl
+    dim3 grid(kc->tiles, kc->members);
+    reduce_kernel<<<grid, NT, 0, kc->stream>>>(kc->buf[0][0], kc->buf[0][1], kc->buf[0][2],
+                                               kc->bathy ? kc->b : nullptr, kc->lamd, kc->n, kc->T, kc->g,
+                                               kc->partials, kc->maxes, kc->members, kc->scheme == 2);
+    kc->launches += 2;
+    CUDA_TRY(kc, cudaGetLastError());
+    kc->cur = 0;
+    kc->dev_steps = 0;
+    kc->host_steps = 0;
+    kc->ctrl_host = Ctrl{0.0, 0.0};
+    kc->have_state = true;
+    return HSGN_OK;
+}
+
 }  // namespace
 
 // Classical SGN (scheme 2): overlap of the phi system from the state.  Rows
@@ -762,6 +869,16 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
 void hsgn_destroy(hsgn_ctx *c)
 {
     if (!c) return;
+    free_kids(c);
+    if (c->cp_in) cudaStreamDestroy(c->cp_in);
+    if (c->cp_out) cudaStreamDestroy(c->cp_out);
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
+    for (int k = 0; k < KIDS_MAX; k++) {
+        if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+        if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+    }
+    if (c->kstat) cudaFreeHost(c->kstat);
+    if (c->tstage) cudaFreeHost(c->tstage);
     drop_graphs(c);
     if (c->nccl) ncclCommDestroy(c->nccl);
     delete c;
@@ -781,6 +898,7 @@ size_t hsgn_workspace_bytes(const hsgn_ctx *c)
     s += 256;                                               // scalars
     s += 256;                                               // ctrl
     s += 2 * align256(9 * size_t(H_MAX) * sizeof(double));  // slab halos
+    s += kid_small_bytes(c->n, c->members) + KIDS_MAX * kid_small_bytes(c->n, 1);  // hsgn_run_host
     return s;
 }
 
@@ -813,6 +931,7 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     q += 256;
     c->halo_l = (double *)q; q += align256(9 * size_t(H_MAX) * sizeof(double));
     c->halo_r = (double *)q; q += align256(9 * size_t(H_MAX) * sizeof(double));
+    c->kid_ws = q;
     CUDA_TRY(c, cudaMemsetAsync(c->ws + (size_t)((char *)c->err - c->ws), 0, 512, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->b, 0, size_t(c->n) * sizeof(double), c->stream));
     c->ctrl_host = Ctrl{0.0, 0.0};
@@ -958,6 +1077,92 @@ hsgn_status hsgn_get_state(hsgn_ctx *c, double *h, double *q, double *K, double 
     if (t) CUDA_TRY(c, cudaMemcpyAsync(t, c->t + (c->dev_steps & 1) * c->members, c->members * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return st;
+}
+
+hsgn_status hsgn_run_host(hsgn_ctx *c, const double *h, const double *q, const double *K, const double *W,
+                          double t0, int64_t n_steps, double *h_out, double *q_out, double *K_out,
+                          double *W_out, double *t_out, int32_t chunks)
+{
+    if (!c || !h || !q || !K || !W || !h_out || !q_out || !K_out || !W_out || n_steps < 0 || chunks < 1)
+        return HSGN_E_INVALID;
+    if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
+    if (!c->have_params) return fail(c, HSGN_E_INVALID, "hsgn_set_params first");
+    if (c->slab) return fail(c, HSGN_E_INVALID, "hsgn_run_host: not for slab contexts");
+    if (c->scheme == 2)
+        return fail(c, HSGN_E_INVALID, "hsgn_run_host: SGN geometry depends on the whole state (use set_state)");
+    chunks = std::min(std::min(chunks, KIDS_MAX), c->members);
+    hsgn_status st = make_kids(c, chunks);
+    if (st != HSGN_OK) return st;
+    if (!c->cp_in) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cp_in, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cp_out, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+        for (int k = 0; k < KIDS_MAX; k++) {
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming));
+            CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
+        }
+        CUDA_TRY(c, cudaMallocHost(&c->kstat, KIDS_MAX * 2 * sizeof(long long)));
+        CUDA_TRY(c, cudaMallocHost(&c->tstage, size_t(c->members) * sizeof(double)));
+    }
+    c->have_state = false;                       // our buffers are the chunks' from here on
+    const double *src[4] = {h, q, K, W};
+    double *dst[4] = {h_out, q_out, K_out, W_out};
+    const size_t n = size_t(c->n);
+    CUDA_TRY(c, cudaEventRecord(c->ev_start, c->stream));   // earlier work on our buffers
+    CUDA_TRY(c, cudaStreamWaitEvent(c->cp_in, c->ev_start, 0));
+    long long l0 = 0;
+    for (hsgn_ctx *kc : c->kids) l0 += kc->launches;
+    size_t m0 = 0;
+    for (int k = 0; k < chunks; k++) {
+        hsgn_ctx *kc = c->kids[k];
+        const size_t cn = size_t(kc->members) * n;
+        for (int f = 0; f < 4; f++)
+            CUDA_TRY(c, cudaMemcpyAsync(kc->buf[0][f], src[f] + m0 * n, cn * sizeof(double),
+                                        cudaMemcpyDefault, c->cp_in));
+        CUDA_TRY(c, cudaEventRecord(c->ev_in[k], c->cp_in));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_in[k], 0));
+        if ((st = kid_state_init(kc, t0)) != HSGN_OK) return fail(c, st, kc->last_error);
+        if ((st = run_steps_impl(kc, n_steps)) != HSGN_OK) return fail(c, st, kc->last_error);
+        CUDA_TRY(c, cudaEventRecord(c->ev_done[k], c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->cp_out, c->ev_done[k], 0));
+        for (int f = 0; f < 4; f++)
+            CUDA_TRY(c, cudaMemcpyAsync(dst[f] + m0 * n, kc->buf[kc->cur][f], cn * sizeof(double),
+                                        cudaMemcpyDefault, c->cp_out));
+        CUDA_TRY(c, cudaMemcpyAsync(c->tstage + m0, kc->t + (kc->host_steps & 1) * kc->members,
+                                    kc->members * sizeof(double), cudaMemcpyDeviceToHost, c->cp_out));
+        CUDA_TRY(c, cudaMemcpyAsync(c->kstat + 2 * k, kc->err, 2 * sizeof(long long),
+                                    cudaMemcpyDeviceToHost, c->cp_out));
+        m0 += kc->members;
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->cp_out));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (t_out) std::memcpy(t_out, c->tstage, size_t(c->members) * sizeof(double));
+    long long l1 = 0;
+    for (hsgn_ctx *kc : c->kids) l1 += kc->launches;
+    c->launches += l1 - l0;
+    // a chunk that stopped early (device error): its committed state replaces
+    // what was copied out, and the first error is returned
+    hsgn_status first = HSGN_OK;
+    m0 = 0;
+    for (int k = 0; k < chunks; k++) {
+        hsgn_ctx *kc = c->kids[k];
+        const unsigned bits = unsigned(c->kstat[2 * k] & 0xffffffffll);
+        if (bits || c->kstat[2 * k + 1] != n_steps) {
+            const hsgn_status ks = reconcile(kc);
+            const size_t cn = size_t(kc->members) * n;
+            for (int f = 0; f < 4; f++)
+                CUDA_TRY(c, cudaMemcpy(dst[f] + m0 * n, kc->buf[kc->cur][f], cn * sizeof(double), cudaMemcpyDefault));
+            if (t_out)
+                CUDA_TRY(c, cudaMemcpy(t_out + m0, kc->t + (kc->dev_steps & 1) * kc->members,
+                                       kc->members * sizeof(double), cudaMemcpyDefault));
+            if (first == HSGN_OK) {
+                first = ks != HSGN_OK ? ks : HSGN_E_INVALID;
+                c->last_error = "member chunk " + std::to_string(k) + ": " + kc->last_error;
+            }
+        }
+        m0 += kc->members;
+    }
+    return first;
 }
 
 hsgn_status hsgn_step(hsgn_ctx *c, double dt, double *dt_used)

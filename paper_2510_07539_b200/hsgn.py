@@ -55,7 +55,7 @@ class Diag(C.Structure):
 SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_workspace",
            "hsgn_set_params", "hsgn_set_tableau", "hsgn_set_bathymetry", "hsgn_set_filter",
            "hsgn_set_relaxation",
-           "hsgn_set_state", "hsgn_get_state", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
+           "hsgn_set_state", "hsgn_get_state", "hsgn_run_host", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
            "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
            "hsgn_set_fused", "hsgn_get_fused", "hsgn_set_persistent", "hsgn_set_scheme",
            "hsgn_set_picard", "hsgn_set_well_balanced",
@@ -88,6 +88,7 @@ def load_library(path: str = LIB_PATH):
         "hsgn_set_relaxation": (st, [vp, C.POINTER(Relax)]),
         "hsgn_set_state": (st, [vp, vp, vp, vp, vp, C.c_double]),
         "hsgn_get_state": (st, [vp, vp, vp, vp, vp, vp]),
+        "hsgn_run_host": (st, [vp, vp, vp, vp, vp, C.c_double, C.c_int64, vp, vp, vp, vp, vp, C.c_int32]),
         "hsgn_step": (st, [vp, C.c_double, dp]),
         "hsgn_run_steps": (st, [vp, C.c_int64]),
         "hsgn_advance_to": (st, [vp, C.c_double, C.c_int64, C.POINTER(C.c_int64)]),
@@ -294,6 +295,24 @@ class Solver:
         t = np.empty(self.members)
         self._chk(self.L.hsgn_get_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in out],
                                         C.c_void_p(t.ctypes.data)))
+        return out, t
+
+    def run_host(self, h, q, K, W, n_steps: int, out=None, chunks: int = 4, t0: float = 0.0):
+        """hsgn_run_host: a whole job from host arrays (numpy or CPU tensors, pinned
+        for copy/compute overlap) -- n_steps steps of every member, pipelined over
+        member chunks.  Returns ((h, q, K, W) written into `out` or new numpy
+        arrays of shape [members, n], t[members])."""
+        N = self.n * self.members
+        arrs = [self._as_f64(a) for a in (h, q, K, W)]
+        for a in arrs:
+            assert (a.size if isinstance(a, np.ndarray) else a.numel()) == N
+        if out is None:
+            out = [np.empty((self.members, self.n)) for _ in range(4)]
+        t = np.empty(self.members)
+        self.stream.wait_stream(self._torch.cuda.current_stream())
+        self._chk(self.L.hsgn_run_host(self.ctx, *[C.c_void_p(_ptr(a)) for a in arrs], float(t0),
+                                       int(n_steps), *[C.c_void_p(_ptr(o)) for o in out],
+                                       C.c_void_p(t.ctypes.data), int(chunks)))
         return out, t
 
     # -- stepping ------------------------------------------------------------

@@ -174,6 +174,23 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
+def profile_fp64():
+    """fp64 arithmetic of the stage-2 kernel from the committed ncu capture
+    (profiles/ncu_summary.json: DADD + DMUL + 2 DFMA per cycle) against the
+    measured DFMA peak (profiles/r01_dfma_peak.json): the kernels are issue /
+    latency-bound, neither HBM- nor fp64-bound."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        k = [x for x in d["full"] if "S2=1" in x["kernel"]][0]
+        pk = d["fp64_peak_tflops"]
+        return {"achieved": k["fp64_tflops"], "peak": pk, "unit": "TFLOP/s", "frac": k["fp64_tflops"] / pk,
+                "pipe_active_pct": k["fp64_pipe_pct"], "issue_active_pct": k["issue_active_pct"],
+                "source": "profiles/r01_ncu_summary.md (ncu --set full, 512 x 4096 cells)"}
+    except Exception:
+        return None
+
+
 def profile_traffic(cells):
     """dram__bytes_read.sum + dram__bytes_write.sum per stage-2 launch, from the
     committed ncu launch list of the same workload (profiles/ncu_summary.json),
@@ -432,7 +449,8 @@ def main():
                      "peak_source": peak_src,
                      "stage1": {"achieved": ach1, "frac": ach1 / peak, "bytes_model": f"{bs1} B/cell"},
                      "step_avg_frac": ((ach2 / peak) if nst == 1 else
-                                       (0.5 * (bs1 + bs2) * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak)},
+                                       (0.5 * (bs1 + bs2) * 2 * Ntot / ((ms1 + ms2) / a.steps / 1e3) / 1e9) / peak),
+                     "fp64": profile_fp64() if a.scheme == "si" and a.config == "cfg3" and nst == 2 else None},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches * world,

@@ -65,6 +65,10 @@ def full(rep):
         "launch__grid_size": "grid",
         "launch__occupancy_limit_registers": "occ_limit_regs",
         "launch__occupancy_limit_shared_mem": "occ_limit_smem",
+        "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed": "dadd_per_cycle",
+        "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed": "dmul_per_cycle",
+        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed": "dfma_per_cycle",
+        "sm__cycles_elapsed.avg.per_second": "clock_hz",
     }
     out = []
     for r in rows[2:]:
@@ -73,7 +77,8 @@ def full(rep):
             if k in hdr:
                 i = hdr.index(k)
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
-                         "nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}.get(units[i], 1)
+                         "nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+                         "Ghz": 1e9, "Mhz": 1e6, "hz": 1}.get(units[i], 1)
                 try:
                     d[v] = float(r[i].replace(",", "")) * scale      # bytes, ns
                 except ValueError:
@@ -133,6 +138,23 @@ def main():
     s1 = [v for k, v in js["launch_list"].items() if "S2=0" in k and "FINAL=0" in k]
     if s1:
         js["stage1_dram_bytes_per_cell"] = s1[0]["dram_read_per_cell"] + s1[0]["dram_write_per_cell"]
+    # fp64 arithmetic rate against the measured DFMA peak (profiles/rNN_dfma_peak.json)
+    pk = os.path.join(prof, f"{tag}_dfma_peak.json")
+    if os.path.exists(pk):
+        peak = json.load(open(pk))
+        ptf = peak["fp64_tflops"]
+        md += ["", f"fp64 arithmetic (DADD + DMUL + 2 DFMA per cycle, ncu) against the measured DFMA peak "
+                   f"{ptf:.1f} TFLOP/s (`tools/dfma_peak.cu`, {peak['dfma_per_clk_per_sm_at_max_clock']:.1f} "
+                   f"DFMA/clk/SM):", "", "| kernel | fp64 TFLOP/s | of peak | fp64 pipe active % |", "|---|---|---|---|"]
+        js["fp64_peak_tflops"] = ptf
+        for d in js["full"]:
+            try:
+                clk = float(d.get("clock_hz", 0)) or 1.965e9
+                tf = (d["dadd_per_cycle"] + d["dmul_per_cycle"] + 2 * d["dfma_per_cycle"]) * clk / 1e12
+            except (KeyError, TypeError):
+                continue
+            d["fp64_tflops"] = tf
+            md.append(f"| {d['kernel']} | {tf:.2f} | {tf / ptf:.2f} | {d.get('fp64_pipe_pct', 0):.1f} |")
     open(os.path.join(prof, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     json.dump(js, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
     print("\n".join(md))

@@ -178,13 +178,14 @@ template <bool S2, bool FIN, bool BATHY>
 hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
 {
     const bool relax = FIN && (c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0);
+    const size_t sm = BATHY ? SMEM_BYTES_B : SMEM_BYTES;    // one-CTA-per-tile kernels: b in smem
     if (c->picard > 0) {             // A24: one CTA per tile, Picard variant
         dim3 grid(c->tiles, c->members);
-        stage_kernel<S2, FIN, BATHY, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+        stage_kernel<S2, FIN, BATHY, false, true><<<grid, NT, sm, c->stream>>>(P, B);
     } else if (c->wb) {              // A25: one CTA per tile, face form
         dim3 grid(c->tiles, c->members);
-        if (relax) stage_kernel<S2, FIN, BATHY, true, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
-        else stage_kernel<S2, FIN, BATHY, false, false, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+        if (relax) stage_kernel<S2, FIN, BATHY, true, false, true><<<grid, NT, sm, c->stream>>>(P, B);
+        else stage_kernel<S2, FIN, BATHY, false, false, true><<<grid, NT, sm, c->stream>>>(P, B);
     } else if (c->persist) {
         const int items = c->tiles * c->members;
         const int grid = std::min(items, c->persist_grid);
@@ -192,8 +193,8 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
         else stage_pkernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
     } else {
         dim3 grid(c->tiles, c->members);
-        if (relax) stage_kernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
-        else stage_kernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B);
+        if (relax) stage_kernel<S2, FIN, BATHY, true><<<grid, NT, sm, c->stream>>>(P, B);
+        else stage_kernel<S2, FIN, BATHY, false><<<grid, NT, sm, c->stream>>>(P, B);
     }
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
@@ -819,15 +820,15 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     c->aI1 = gm; c->aI2 = gm; c->wE = cc / gm; c->wR = (1.0 - gm) / gm;
     // kernels need > 48 KiB dynamic smem
     cudaFuncSetAttribute(stage_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_pkernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
@@ -839,11 +840,11 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<true, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<false, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(sgn_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));

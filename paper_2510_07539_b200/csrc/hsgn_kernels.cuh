@@ -64,6 +64,10 @@ constexpr int SROWS = LCAP + 16;    // smem row capacity per array (even: 16-B a
                                     // rows up to L+MCH+2 past a base shifted by <= 4)
 constexpr int NARR = 8;             // smem arrays
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
+// one-CTA-per-tile stage kernels with bathymetry: b of the tile's raw rows in a
+// ninth array (the per-row global reads of b through the boundary map cost more
+// than the rest of the stage, `profiles/r01_ncu_summary.md`); < 48 KiB
+constexpr size_t SMEM_BYTES_B = SMEM_BYTES + size_t(SROWS) * sizeof(double);
 // fused step kernel: + a dedicated output staging buffer of 4 x T doubles
 // (T <= LCAP), so a tile's bulk store overlaps the next tile's compute
 __host__ __device__ constexpr size_t fused_smem_bytes(int T)
@@ -328,7 +332,8 @@ struct RowCtx { double tau, tdx2, t2, lt2, lam, lam3, ltau, g, idx, c23; };
 // dhat_{r+1/2} = -(2 sigma^ - 1)/(3 h~) b1~ of rows r, r+1 instead (averages of
 // sigma = H/h^2, h and 1/beta1 over the two rows).
 template <bool BATHY, bool WB = false>
-__device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const Params &P, int r, int start, int n,
+__device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const Params &P, const double *sB,
+                                           int r, int start, int n,
                                            const double (&ch)[3], const double (&cq)[3],
                                            const double (&cH)[3], const double (&cW)[3],
                                            const Face &Fl, const Face &Fr, double *sQd,
@@ -350,9 +355,10 @@ __device__ __forceinline__ void row_update(bool STAGE2, const RowCtx &C, const P
     const double sg = HE * ih2;                                      // eta/h
     double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
     if (BATHY) {
-        const double bm = bathy_at(P, start + rr - 1);
-        const double b0 = bathy_at(P, start + rr);
-        const double bp = bathy_at(P, start + rr + 1);
+        // (sB: b of the tile's raw rows in shared memory, else through the map)
+        const double bm = sB ? sB[rr - 1] : bathy_at(P, start + rr - 1);
+        const double b0 = sB ? sB[rr] : bathy_at(P, start + rr);
+        const double bp = sB ? sB[rr + 1] : bathy_at(P, start + rr + 1);
         Dxb = (bp - bm) * (0.5 * C.idx);
         // hydrostatic term in zeta-form (A9)
         const double Gr = C.g * (hE + ch[2]) * 0.5, Gl = C.g * (ch[0] + hE) * 0.5;
@@ -551,7 +557,7 @@ __device__ __forceinline__ LoadPlan load_plan(const Params &P, size_t mo, Geom &
 // arrive + expect_tx).
 enum { LD_ALL = 0, LD_UN = 1, LD_U1 = 2 };
 
-template <bool WITH_U1, int PART = LD_ALL>
+template <bool WITH_U1, int PART = LD_ALL, bool WITH_B = false>
 __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_t mo, const Geom &G,
                                            const LoadPlan &Lp, unsigned mb, int tid)
 {
@@ -559,12 +565,20 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
     if (HSGN_EXP_NOLOAD) return;
     constexpr bool DO_UN = PART != LD_U1;
     constexpr bool DO_U1 = WITH_U1 && PART != LD_UN;
+    // b rides the TMA copies when its source is 16-B aligned too (a0 even: b has
+    // no member offset), else every thread cp.asyncs it (odd n and odd member)
+    const bool b_bulk = WITH_B && Lp.bulk && !(Lp.a0 & 1);
+    if (WITH_B && Lp.bulk && !b_bulk) {
+        double *const Ab = smem + G.abase + 8 * SROWS;
+        for (int r = tid - 3; r < G.L + 3; r += NT) cp_async8(Ab + r, P.b + (G.start + r));
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     if (Lp.bulk) {
         if (tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             const unsigned bytes = unsigned(Lp.seg1) * 8u;
             const unsigned bytes2 = unsigned(Lp.cnt - Lp.seg1) * 8u;     // wrapped part
-            const unsigned tx = unsigned(Lp.cnt) * 8u * ((DO_UN ? 4u : 0u) + (DO_U1 ? 4u : 0u));
+            const unsigned tx = unsigned(Lp.cnt) * 8u * ((DO_UN ? 4u : 0u) + (DO_U1 ? 4u : 0u) + (b_bulk ? 1u : 0u));
             if (PART == LD_UN)
                 asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;\n" ::"r"(mb), "r"(tx) : "memory");
             else
@@ -574,6 +588,10 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
             if (DO_UN) {
 #pragma unroll
                 for (int f = 0; f < 4; f++) bulk_g2s(smem + f * SROWS, B.Un[f] + gsrc, bytes, mb);
+            }
+            if (b_bulk) {
+                bulk_g2s(smem + 8 * SROWS, P.b + Lp.a0, bytes, mb);
+                if (bytes2) bulk_g2s(smem + 8 * SROWS + Lp.seg1, P.b, bytes2, mb);
             }
             if (DO_U1) {
                 bulk_g2s(smem + 7 * SROWS, B.U1[0] + gsrc, bytes, mb);
@@ -601,17 +619,22 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
         for (int r = tid - 3; r < G.L + 3; r += NT) {
             const int c = G.start + r;
             const double *p0, *p1, *p2, *p3, *u0 = nullptr, *u1 = nullptr, *u2 = nullptr, *u3 = nullptr;
+            const double *pb = nullptr;
             if (c < 0 && P.bcl == BC_HALO) {
                 const int o = c + P.H;
                 p0 = P.halo_l[0] + o; p1 = P.halo_l[1] + o; p2 = P.halo_l[2] + o; p3 = P.halo_l[3] + o;
+                pb = P.halo_l[8] + o;
                 if (DO_U1) { u0 = P.halo_l[4] + o; u1 = P.halo_l[5] + o; u2 = P.halo_l[6] + o; u3 = P.halo_l[7] + o; }
             } else if (c >= n && P.bcr == BC_HALO) {
                 const int o = c - n;
                 p0 = P.halo_r[0] + o; p1 = P.halo_r[1] + o; p2 = P.halo_r[2] + o; p3 = P.halo_r[3] + o;
+                pb = P.halo_r[8] + o;
                 if (DO_U1) { u0 = P.halo_r[4] + o; u1 = P.halo_r[5] + o; u2 = P.halo_r[6] + o; u3 = P.halo_r[7] + o; }
             } else {
                 double par;
-                const size_t gi = mo + size_t(map_cell(c, n, P.bcl, P.bcr, par));
+                const int ci = map_cell(c, n, P.bcl, P.bcr, par);
+                const size_t gi = mo + size_t(ci);
+                pb = P.b + ci;
                 p0 = B.Un[0] + gi; p1 = B.Un[1] + gi; p2 = B.Un[2] + gi; p3 = B.Un[3] + gi;
                 if (DO_U1) { u0 = B.U1[0] + gi; u1 = B.U1[1] + gi; u2 = B.U1[2] + gi; u3 = B.U1[3] + gi; }
             }
@@ -623,6 +646,7 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
                 cp_async8(A + 7 * SROWS + r, u0); cp_async8(A + 4 * SROWS + r, u1);
                 cp_async8(A + 5 * SROWS + r, u2); cp_async8(A + 6 * SROWS + r, u3);
             }
+            if (WITH_B) cp_async8(A + 8 * SROWS + r, pb);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
@@ -774,6 +798,11 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     double *sHd = A + 5 * SROWS;   // U1_K -> R_H -> H^dagger
     double *sBe = A + 6 * SROWS;   // U1_W -> R_W -> beta -> hbar
     double *sDe = A + 7 * SROWS;   // U1_h -> R_h -> delta (R_h read by its own row first)
+    // b of the raw rows -3 .. L+2 (one-CTA-per-tile kernels: array 8, loaded with the tile)
+    const double *const sBz = (MODE == MODE_ALONE && BATHY) ? A + 8 * SROWS : nullptr;
+    auto bz = [&](int r) -> double {
+        return (MODE == MODE_ALONE && BATHY) ? sBz[r] : bathy_at(P, G.start + r);
+    };
     const double tau = S.tau, g = S.g, idx1 = S.idx1, tdx = S.tdx, tdx2 = S.tdx2, t2 = S.t2;
     const double t2h = S.t2h, lt2 = S.lt2, lt2h = S.lt2h, ltdx2 = S.ltdx2, lam = S.lam;
     const double lam3 = S.lam3, ltau = S.ltau;
@@ -801,8 +830,8 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 }
                 eq.x *= par0; eq.y *= par1;
                 // (scratch rows clamped onto rows -3 .. L+2: stay inside slab halos)
-                const double b0 = (raw && BATHY) ? bathy_at(P, start + max(r, -3)) : 0.0;
-                const double b1 = (raw && BATHY) ? bathy_at(P, start + min(r + 1, L + 2)) : 0.0;
+                const double b0 = (raw && BATHY) ? bz(max(r, -3)) : 0.0;
+                const double b1 = (raw && BATHY) ? bz(min(r + 1, L + 2)) : 0.0;
                 if (st2) {
                     const double2 h1 = v[7 * SROWS / 2], q1 = v[2 * SROWS], K1 = v[5 * SROWS / 2],
                                   W1 = v[3 * SROWS];
@@ -869,7 +898,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const FState P0 = muscl_plus_next(wh, wq, wH, wW, sEh[1], sEq[1], sEH[1], sEW[1], kap);
             const Face Fb = rusanov(Mm, P0);                          // face -1/2
             double Wd, beta, hRd;
-            row_update<BATHY, WB>(st2, C, P, -1, start, n, wh, wq, wH, wW, Fa, Fb,
+            row_update<BATHY, WB>(st2, C, P, sBz, -1, start, n, wh, wq, wH, wW, Fa, Fb,
                                       sQd, sHd, sBe, sDe, Wd, beta, hRd);
         }
 #pragma unroll
@@ -896,7 +925,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
             Mr = Mn;
             double beta, hRr;
-            row_update<BATHY, WB>(st2, C, P, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
+            row_update<BATHY, WB>(st2, C, P, sBz, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
                                       sQd, sHd, sBe, sDe, wd[i], beta, hRr);
             hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
             // coercivity on every row of the tile (overlap rows are real
@@ -1171,12 +1200,12 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             double Phr = 0.5 * (vb[i + 1] + vb[i + 2]) * (hr - h0) + lam * vd[i + 1] * (vH[i + 2] - vH[i + 1]);
             double Phl = 0.5 * (vb[i] + vb[i + 1]) * (h0 - hl) + lam * vd[i] * (vH[i + 1] - vH[i]);
             if (BATHY && act) {
-                const double bm = bathy_at(P, start + r - 1), bp = bathy_at(P, start + r + 1);
-                const double bz = bathy_at(P, start + r);
+                const double bm = bz(r - 1), bp = bz(r + 1);
+                const double b0 = bz(r);
                 const double e0 = sEhc[r];
-                bbv[i] = bz;
-                Phr += 0.5 * g * (e0 + sEhc[r + 1]) * (bp - bz);
-                Phl += 0.5 * g * (sEhc[r - 1] + e0) * (bz - bm);
+                bbv[i] = b0;
+                Phr += 0.5 * g * (e0 + sEhc[r + 1]) * (bp - b0);
+                Phl += 0.5 * g * (sEhc[r - 1] + e0) * (b0 - bm);
             }
             if (r == 0) Phl = 0.0;
             if (r == L - 1) Phr = 0.0;
@@ -1185,9 +1214,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
         }
         if (BATHY && act && !WB) {
-            const double bm = bathy_at(P, start + r - 1);
-            const double bp = bathy_at(P, start + r + 1);
-            bbv[i] = bathy_at(P, start + r);
+            const double bm = bz(r - 1);
+            const double bp = bz(r + 1);
+            bbv[i] = bz(r);
             qb -= tau * g * sEhc[r] * (bp - bm) * (0.5 * idx1);     // A9
         }
         // P:514-515 with one reciprocal: Hbar = H^dag hbar^2 / (hbar^2 + lam tau^2),
@@ -1461,7 +1490,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const LoadPlan Lp = load_plan(P, mo, G);
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
     if (Lp.bulk) init_mbar(mb);
-    issue_load<STAGE2>(P, B, mo, G, Lp, mb, tid);
+    issue_load<STAGE2, LD_ALL, BATHY>(P, B, mo, G, Lp, mb, tid);
     // L2 prefetch of the tile of the CTA about one residency wave later, so its
     // TMA loads hit L2 instead of HBM (no shared memory involved)
     if (tid == 0 && P.pf_dist > 0 && !HSGN_EXP_NOLOAD) {
@@ -1491,6 +1520,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const double lam = P.lam[m];
     unsigned parity = 0u;
     wait_load(Lp, mb, parity);
+    if (BATHY && Lp.bulk && (Lp.a0 & 1)) cp_async_wait_all();    // b by cp.async (issue_load)
     __syncthreads();
     EXP_T(t1);
     if (err0) return;

@@ -125,6 +125,19 @@ def test_bathymetry_steps(bc, kmode):
     compare(w, s, range(2), steps=20, tol=1e-10)
 
 
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_bathymetry_odd_sizes(bc):
+    """odd n and members: member m's cells start at an odd offset, so the tile's
+    b (no member offset) is not 16-B aligned with its state rows and takes the
+    cp.async path while the state rides TMA"""
+    w = W.random_smooth(3001, 3, seed=19, amp=0.05, bc=(bc, bc), bathy=0.08)
+    s = gpu_solver(w, tile_cells=500)
+    s.step()
+    compare(w, s, range(3), steps=1)
+    s.run_steps(9)
+    compare(w, s, range(3), steps=10, tol=1e-10)
+
+
 def test_euler_tableau_first_order_step():
     w = W.random_smooth(1500, 2, seed=8, amp=0.05)
     hs = _hsgn()

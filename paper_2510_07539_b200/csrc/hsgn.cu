@@ -91,6 +91,8 @@ struct hsgn_ctx {
     int sw = 0, sT = 0, stiles = 0;
     int picard = 0;               // A24 Picard passes of the SI depth solve (0: the paper's)
     bool wb = false;              // A25 exactly well-balanced face form of the SI stage
+    bool pdl = false;             // programmatic dependent launch of the step's kernels
+                                  // (HSGN_PDL=1; measured no gain on cfg3, -7 % on cfg2)
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
     bool persist = false;
     int persist_grid = 0;
@@ -174,6 +176,24 @@ Params make_params(hsgn_ctx *c, long long k)
     return P;
 }
 
+// Launch with programmatic stream serialization (PDL, see pdl_release/pdl_wait
+// in hsgn_kernels.cuh) when enabled (HSGN_PDL=1), else plain stream order.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(hsgn_ctx *c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = c->pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 template <bool S2, bool FIN, bool BATHY>
 hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
 {
@@ -181,11 +201,11 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
     const size_t sm = BATHY ? SMEM_BYTES_B : SMEM_BYTES;    // one-CTA-per-tile kernels: b in smem
     if (c->picard > 0) {             // A24: one CTA per tile, Picard variant
         dim3 grid(c->tiles, c->members);
-        stage_kernel<S2, FIN, BATHY, false, true><<<grid, NT, sm, c->stream>>>(P, B);
+        CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false, true>, grid, dim3(NT), sm, P, B));
     } else if (c->wb) {              // A25: one CTA per tile, face form
         dim3 grid(c->tiles, c->members);
-        if (relax) stage_kernel<S2, FIN, BATHY, true, false, true><<<grid, NT, sm, c->stream>>>(P, B);
-        else stage_kernel<S2, FIN, BATHY, false, false, true><<<grid, NT, sm, c->stream>>>(P, B);
+        if (relax) CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, true, false, true>, grid, dim3(NT), sm, P, B));
+        else CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false, false, true>, grid, dim3(NT), sm, P, B));
     } else if (c->persist) {
         const int items = c->tiles * c->members;
         const int grid = std::min(items, c->persist_grid);
@@ -193,8 +213,8 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
         else stage_pkernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
     } else {
         dim3 grid(c->tiles, c->members);
-        if (relax) stage_kernel<S2, FIN, BATHY, true><<<grid, NT, sm, c->stream>>>(P, B);
-        else stage_kernel<S2, FIN, BATHY, false><<<grid, NT, sm, c->stream>>>(P, B);
+        if (relax) CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, true>, grid, dim3(NT), sm, P, B));
+        else CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false>, grid, dim3(NT), sm, P, B));
     }
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
@@ -210,7 +230,8 @@ hsgn_status launch_stage_b(hsgn_ctx *c, const Params &P, const Bufs &B)
 hsgn_status launch_dtc(hsgn_ctx *c, long long k, int commit_prev, int compute_dt)
 {
     const Params P = make_params(c, k);
-    dt_commit_kernel<<<(c->members + 127) / 128, 128, 0, c->stream>>>(P, commit_prev, compute_dt);
+    CUDA_TRY(c, launch_pdl(c, dt_commit_kernel, dim3((c->members + 127) / 128), dim3(128), 0, P, commit_prev,
+                           compute_dt));
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     return HSGN_OK;
@@ -665,7 +686,7 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         kc->relax = c->relax;
         kc->fused_on = c->fused_on; kc->persist = c->persist;
         kc->scheme = c->scheme; kc->x_stages = c->x_stages;
-        kc->picard = c->picard; kc->wb = c->wb;
+        kc->picard = c->picard; kc->wb = c->wb; kc->pdl = c->pdl;
         kc->ws = c->ws;
         for (int bi = 0; bi < 3; bi++)
             for (int f = 0; f < 4; f++) kc->buf[bi][f] = c->buf[bi][f] + size_t(m0) * c->n;
@@ -804,6 +825,7 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     c->desc = *d;
     c->slab = slab;
     c->stream = (cudaStream_t)stream;
+    if (const char *e = std::getenv("HSGN_PDL")) c->pdl = std::atoi(e) != 0;
     cudaGetDevice(&c->device);
     c->n = int(d->n_cells);
     c->members = d->n_members;

@@ -1454,6 +1454,15 @@ __device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, dou
     }
 }
 
+// Programmatic dependent launch: the step's kernels are launched with the
+// programmatic-serialization attribute (hsgn.cu launch_pdl).  A kernel lets the
+// next one launch once all its CTAs have started (its CTAs then take the SM slots
+// freed by this grid's last wave) and waits for the previous grid's completion
+// and memory before it touches global memory; both are no-ops without the
+// attribute.
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ void init_mbar(unsigned mb)
 {
     if (threadIdx.x == 0) {
@@ -1490,6 +1499,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const LoadPlan Lp = load_plan(P, mo, G);
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
     if (Lp.bulk) init_mbar(mb);
+    pdl_release();
+    pdl_wait();                      // (no global access above)
     issue_load<STAGE2, LD_ALL, BATHY>(P, B, mo, G, Lp, mb, tid);
     // L2 prefetch of the tile of the CTA about one residency wave later, so its
     // TMA loads hit L2 instead of HBM (no shared memory involved)
@@ -2245,6 +2256,8 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
 __global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int commit_prev,
                                                         int compute_dt)
 {
+    pdl_release();
+    pdl_wait();
     const unsigned int err = *((volatile unsigned int *)P.err);
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0) { P.work[2 * P.kpar] = 0u; P.work[2 * P.kpar + 1] = 0u; }   // step k's item counters

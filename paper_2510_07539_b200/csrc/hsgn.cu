@@ -1413,9 +1413,9 @@ hsgn_status hsgn_set_persistent(hsgn_ctx *c, int32_t on)
 int hsgn_exp_counters(unsigned long long *out, int reset)
 {
     cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, g_exp, sizeof(unsigned long long) * 8);
+    cudaMemcpyFromSymbol(out, g_exp, sizeof(unsigned long long) * 16);
     if (reset) {
-        unsigned long long z[8] = {};
+        unsigned long long z[16] = {};
         cudaMemcpyToSymbol(g_exp, z, sizeof(z));
     }
     return 0;

@@ -125,6 +125,16 @@ struct Bufs {
     double *out[4];
 };
 
+#if HSGN_EXP_TIMING
+// [stage][load wait, compute + store issue, epilogue + drain, CTAs, in-place + phase 1,
+//  phase 2, phase 3 + staging, -]
+__device__ unsigned long long g_exp[16];
+__shared__ long long s_tph[4];
+#define EXP_MARK(k) do { if (threadIdx.x == 0) s_tph[k] = clock64(); } while (0)
+#else
+#define EXP_MARK(k) do { } while (0)
+#endif
+
 // Reciprocal: hardware approximation (MUFU.RCP64H, ~2^-20) refined by one
 // cubic step r0 (1 + e + e^2), e = 1 - x r0 (relative error e^3 < 2^-60; 3 DFMA,
 // <= 1 ulp from IEEE 1/x, tools/rcp_check.cu) -- replaces the IEEE division
@@ -940,6 +950,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         for (int i = 0; i < MCH; i++) { wd[i] = 0.0; hRv[i] = 0.0; }
     }
     __syncthreads();
+    EXP_MARK(0);
     // persistent kernel without bathymetry: arrays 0..3 (E) are not read after
     // phase 1, so the next item's U^n loads can start now
     if (MODE == MODE_PERSIST && !HSGN_EXP_NOPREFETCH && !BATHY && next_item >= 0)
@@ -1162,6 +1173,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     __syncthreads();
     }   // Picard passes
 
+    EXP_MARK(1);
     // rho = max (tau/dx)^2 (beta_i + beta_{i+1})/2 <= t2 max beta
     acc.rho = fmax(acc.rho, t2 * __hiloint2double(acc.bhi + 1, 0));
 
@@ -1479,7 +1491,6 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 // tableaux and slab (BC_HALO) domains; the two-stage step otherwise runs fused.
 // ---------------------------------------------------------------------------
 #if HSGN_EXP_TIMING
-__device__ unsigned long long g_exp[8];
 #define EXP_T(v) long long v = clock64()
 #else
 #define EXP_T(v)
@@ -1551,11 +1562,16 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
 #if HSGN_EXP_TIMING
     if (tid == 0) {
         const long long t3 = clock64();
-        unsigned long long *g = g_exp + (STAGE2 ? 4 : 0);
+        unsigned long long *g = g_exp + (STAGE2 ? 8 : 0);
         atomicAdd(g + 0, (unsigned long long)(t1 - t0));
         atomicAdd(g + 1, (unsigned long long)(t2 - t1));
         atomicAdd(g + 2, (unsigned long long)(t3 - t2));
         atomicAdd(g + 3, 1ull);
+        if (dtm != 0.0) {
+            atomicAdd(g + 4, (unsigned long long)(s_tph[0] - t1));
+            atomicAdd(g + 5, (unsigned long long)(s_tph[1] - s_tph[0]));
+            atomicAdd(g + 6, (unsigned long long)(t2 - s_tph[1]));
+        }
     }
 #endif
 }

@@ -168,6 +168,10 @@ Params make_params(hsgn_ctx *c, long long k)
         P.mcfl = 0.0;
     }
     P.inv_tiles = 1.0 / double(c->tiles);
+    {   // r = 2 rho/(1 + 2 rho + sqrt(1 + 4 rho)) inverts to rho = r/(1 - r)^2
+        const double r = std::exp2(-60.0 / double(std::max(P.w, 1)));
+        P.rho_ok = r / ((1.0 - r) * (1.0 - r));
+    }
     P.picard = c->picard;
     for (int k = 0; k < 9; k++) {
         P.halo_l[k] = c->halo_l ? c->halo_l + k * H_MAX : nullptr;

@@ -113,6 +113,7 @@ struct Params {
     // resident at once); 0: off
     int pf_dist;
     double inv_tiles;                // 1 / tiles
+    double rho_ok;                   // largest rho whose decay r(rho)^w <= 2^-60 (overlap check)
     int picard;                      // A24 Picard passes (stage_kernel<..., PIC = true>)
     // A10 relaxation zones (cfg4), applied to U^{n+1} at t^{n+1} in the final
     // stage; rates <= 0 switch them off.  x_i = x_min + (i + 1/2) dx.
@@ -1435,7 +1436,7 @@ __device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, dou
     double um = 0.0, nm = 0.0;
     if (FINAL) { um = warp_max_nonneg(acc.umax); nm = warp_max_nonneg(acc.numax); }
     float rf = warp_max_nonneg(float(acc.rho));
-    __syncthreads();
+    // (s_red is only used here; s_redf's last reads in phase 2 precede later barriers)
     if (lane == 0) { s_red[0][wid] = um; s_red[1][wid] = nm; s_redf[wid] = rf; }
     __syncthreads();
     if (tid == 0) {
@@ -1445,8 +1446,11 @@ __device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, dou
         }
         if (rf > 0.0f && dtm != 0.0 && !exp_off) {
             const double rho = double(rf) * (1.0 + 1e-6);
-            const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
-            if (acc.wmin < (1 << 30)) {
+            if (acc.wmin == P.w) {
+                // r(rho)^w <= 2^-60  <=>  rho <= rho_ok = r*/(1 - r*)^2, r* = 2^(-60/w) (host)
+                if (rho > P.rho_ok) atomicOr(P.err, ERR_OVERLAP);
+            } else if (acc.wmin < (1 << 30)) {
+                const double rdec = 2.0 * rho / ((1.0 + 2.0 * rho) + sqrt(1.0 + 4.0 * rho));
                 double x = 1.0, b = rdec;          // rdec^wmin by squaring
                 for (int k = acc.wmin; k > 0; k >>= 1) { if (k & 1) x *= b; b *= b; }
                 if (x > 8.673617379884035e-19) atomicOr(P.err, ERR_OVERLAP);   // 2^-60

@@ -13,6 +13,8 @@ from paper_2510_07539_b200 import workloads as W  # noqa: E402
 
 members = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 w = W.cfg3(members=members)
+if "nofilter" in sys.argv[2:]:
+    w.filter_sigma = 0.0
 s = hsgn.solver_for(w)
 L = s.L
 f = L.hsgn_exp_counters

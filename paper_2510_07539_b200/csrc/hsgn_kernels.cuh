@@ -1513,10 +1513,17 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     Geom G = stage_geom(P, s, e, P.w);
     const LoadPlan Lp = load_plan(P, mo, G);
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
-    if (Lp.bulk) init_mbar(mb);
+    // thread 0 initialises the mbarrier and issues the tile's TMA loads at once;
+    // the barrier that publishes the initialised mbarrier to the other threads
+    // comes after the issue, off the loads' critical path
+    if (Lp.bulk && tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     pdl_release();
     pdl_wait();                      // (no global access above)
     issue_load<STAGE2, LD_ALL, BATHY>(P, B, mo, G, Lp, mb, tid);
+    if (Lp.bulk) __syncthreads();
     // L2 prefetch of the tile of the CTA about one residency wave later, so its
     // TMA loads hit L2 instead of HBM (no shared memory involved)
     if (tid == 0 && P.pf_dist > 0 && !HSGN_EXP_NOLOAD) {

@@ -1893,8 +1893,9 @@ __global__ void __launch_bounds__(XNT, XMINB) explicit_kernel(const Params P, co
         // base U^n first: its global loads overlap the flux arithmetic
         double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
         if (HEUN2) {
-            double par;
-            const size_t gi = mo + size_t(map_cell(s + r, n, P.bcl, P.bcr, par));
+            const int c = s + r;
+            double par = 1.0;
+            const size_t gi = mo + size_t((c >= 0 && c < n) ? c : map_cell(c, n, P.bcl, P.bcr, par));
             b0 = B.Un[0][gi]; b1 = par * B.Un[1][gi]; b2 = B.Un[2][gi]; b3 = B.Un[3][gi];
         }
         double L[4];
@@ -1933,10 +1934,16 @@ __global__ void __launch_bounds__(XNT, XMINB) explicit_kernel(const Params P, co
     if (FILT) {
         __syncthreads();
         const double sig16 = P.filter_sigma * (1.0 / 16.0);
+        // stencil rows reach a physical end only in the first / last two cells
+        const bool near_phys = (P.bcl != BC_PERIODIC && s < 2) || (P.bcr != BC_PERIODIC && e + 2 > n);
         for (int r = tid; r < Tk; r += XNT) {
             // A19 on q and W; the halo rows are the neighbours' final values
             // (the mirror of the tile itself at a physical end, A10)
             double cq[5], cw[5];
+            if (!near_phys) {
+#pragma unroll
+                for (int k = 0; k < 5; k++) { cq[k] = fq[r + k - 2]; cw[k] = fw[r + k - 2]; }
+            } else {
 #pragma unroll
             for (int k = 0; k < 5; k++) {
                 const int c = s + r + k - 2;
@@ -1949,6 +1956,7 @@ __global__ void __launch_bounds__(XNT, XMINB) explicit_kernel(const Params P, co
                 }
                 cq[k] = pq * fq[rr];
                 cw[k] = fw[rr];
+            }
             }
             const double qo = cq[2] - sig16 * (cq[0] - 4.0 * cq[1] + 6.0 * cq[2] - 4.0 * cq[3] + cq[4]);
             const double wo = cw[2] - sig16 * (cw[0] - 4.0 * cw[1] + 6.0 * cw[2] - 4.0 * cw[3] + cw[4]);

@@ -2039,17 +2039,38 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
     double *oh = smem + 2 * SROWS_S, *oq = oh + SROWS_S;        // staged outputs
     double *pcr0 = smem + 4 * SROWS_S, *pcr1 = pcr0 + 3 * SNT;
     const double *const *X = HEUN2 ? B.U1 : B.Un;
-    // ---- load rows -4 .. L+3 of (h, q) of X (q parity at wall ghosts) ---------
+    // ---- load rows -4 .. L+3 of (h, q) of X and, for Heun stage 2, the kept
+    // rows of U^n's (h, q) into the output staging (read there by the row's own
+    // thread before it writes the result); all by cp.async, q parity of wall
+    // ghosts applied after the wait ---------------------------------------------
     for (int r = tid - 4; r < L + 4; r += SNT) {
-        double par;
-        const size_t gi = mo + size_t(map_cell(start + r, n, P.bcl, P.bcr, par));
-        sh[r] = X[0][gi];
-        sq[r] = par * X[1][gi];
+        const int c = start + r;
+        double par = 1.0;
+        const size_t gi = mo + size_t((c >= 0 && c < n) ? c : map_cell(c, n, P.bcl, P.bcr, par));
+        cp_async8(sh + r, X[0] + gi);
+        cp_async8(sq + r, X[1] + gi);
     }
+    if (HEUN2) {
+        const size_t g0 = mo + size_t(start + G.klo);
+        for (int k = tid; k < G.khi - G.klo; k += SNT) {
+            cp_async8(oh + k, B.Un[0] + g0 + k);
+            cp_async8(oq + k, B.Un[1] + g0 + k);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     const unsigned int err0 = *((volatile unsigned int *)P.err);
     const double dtm = P.dt[m];
+    cp_async_wait_all();
     __syncthreads();
     if (err0) return;
+    if ((start - 4 < 0 && P.bcl == BC_WALL) || (start + L + 4 > n && P.bcr == BC_WALL)) {
+        for (int r = tid - 4; r < L + 4; r += SNT) {
+            double par;
+            (void)map_cell(start + r, n, P.bcl, P.bcr, par);
+            sq[r] *= par;
+        }
+        __syncthreads();
+    }
     const double g = P.g, dx = P.dx, idx = P.idx;
     const double c3 = 1.0 / (3.0 * dx * dx);
     const double s6 = 1.0 / (6.0 * dx * dx * dx);
@@ -2210,9 +2231,8 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
                 const double Lq = -(Fqr - Fql) * hidx + hc * phi[i];
                 double ho, qo;
                 if (HEUN2) {
-                    const size_t gi = mo + size_t(start + r);
-                    ho = 0.5 * B.Un[0][gi] + 0.5 * (hc + dtm * Lh);
-                    qo = 0.5 * B.Un[1][gi] + 0.5 * (qc + dtm * Lq);
+                    ho = 0.5 * oh[r - G.klo] + 0.5 * (hc + dtm * Lh);
+                    qo = 0.5 * oq[r - G.klo] + 0.5 * (qc + dtm * Lq);
                 } else {
                     ho = hc + dtm * Lh;
                     qo = qc + dtm * Lq;

@@ -324,6 +324,53 @@ def test_cfg5_bathymetry_scaled():
     compare(w, s, [0], steps=10, tol=1e-10)
 
 
+def test_cfg5_full_size_sampled():
+    """cfg5 at its full size (2^28 cells, bathymetry, filter) in bench.py's launch
+    configuration, one step.  Sampled windows are checked against the oracle run
+    on the window itself (transmissive ends, the GPU's dt): the implicit solve's
+    influence decays like r^d per stage (r ~ 0.42 at CFL 2),
+    so the centre of a window with 1024-cell margins sees the wrong ends at
+    < 1e-300; the dt is checked against the rule of P:607-617 evaluated with torch
+    fp64 over the whole domain."""
+    import torch
+    hs = _hsgn()
+    n = 1 << 28
+    (h, q, K, Wf, b), meta = W.cfg5(n, device="cuda")
+    s = hs.Solver(n, 1, 0.0, meta["L"])
+    s.set_params(9.81, meta["lam"], meta["cfl"], meta["mcfl"])
+    s.set_bathymetry(b)
+    s.set_filter(0.25)
+    s.set_state(h, q, K, Wf)
+    dx = meta["L"] / n
+    lam = float(meta["lam"]) if np.ndim(meta["lam"]) == 0 else float(np.ravel(meta["lam"])[0])
+    # dt rule over the whole domain (A7, A8)
+    u = (q / h).abs()
+    sg = (K - 1.5 * h * b) / (h * h)
+    nu = (u + torch.sqrt(9.81 * h + lam / 3.0 * sg * sg)).max().item()
+    umax = u.max().item()
+    dt_ref = meta["cfl"] * dx / nu
+    if umax * dt_ref / dx > meta["mcfl"]:
+        dt_ref = meta["mcfl"] * dx / umax
+    dt = s.step(return_dt=True)[0]
+    assert abs(dt - dt_ref) <= 1e-13 * dt_ref, (dt, dt_ref)
+    (go, _) = s.get_state(device=True)
+    margin, half = 1024, 64
+    for c in (5_000, 77_777_777, n // 2 + 12_345, n - 9_000):
+        lo, hi = c - margin - half, c + margin + half
+        win = [f[lo:hi].double().cpu().numpy() for f in (h, q, K, Wf)]
+        o = O.Oracle(hi - lo, dx, g=9.81, lam=lam, bc=("transmissive", "transmissive"),
+                     b=b[lo:hi].double().cpu().numpy(), filter_sigma=0.25)
+        ref = o.step(win, dt)
+        sl = slice(margin, margin + 2 * half)
+        got = [g[0, lo:hi].cpu().numpy()[sl] for g in go]
+        ref = [r[sl] for r in ref]
+        S = field_scales(ref, lam, dt)
+        assert rel_err(got, ref, S) <= TOL_STEP, c
+    del go, h, q, K, Wf, b
+    s.close()
+    torch.cuda.empty_cache()
+
+
 # --------------------------------------------------------------------------
 # slab decomposition (P2): loopback group of slab contexts on one device
 # --------------------------------------------------------------------------

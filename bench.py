@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--members", type=int, default=4096)
     p.add_argument("--cells", type=int, default=4096)
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--e2e-chunks", type=int, default=4,
+    p.add_argument("--e2e-chunks", type=int, default=8,
                    help="member chunks of the e2e job (hsgn_run_host copy/compute pipeline)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--si-order", type=int, default=2, choices=[1, 2],

@@ -182,7 +182,8 @@ hsgn_status hsgn_get_state(hsgn_ctx *ctx, double *h, double *q, double *K, doubl
  * groups (at most 16 and n_members); for each group, in order, its initial
  * state (h, q, K, W: n_members * n_cells doubles each, member-major, as for
  * hsgn_set_state) is copied in on one copy stream, n_steps steps run on the
- * context's stream (exactly as hsgn_set_state + hsgn_run_steps would: members
+ * context's stream or, for odd groups, a second compute stream ordered after
+ * the context's earlier work (exactly as hsgn_set_state + hsgn_run_steps would: members
  * are independent, so each member's result is bitwise the same), and its final
  * state and times are copied out on a second copy stream -- group k+1's input
  * and group k-1's output transfers overlap group k's steps.  Use page-locked

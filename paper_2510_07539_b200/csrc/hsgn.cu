@@ -105,6 +105,7 @@ struct hsgn_ctx {
     long long gen = 0, kids_gen = -1;   // settings generation (bumped by drop_graphs)
     char *kid_ws = nullptr;
     cudaStream_t cp_in = nullptr, cp_out = nullptr;
+    cudaStream_t cs2 = nullptr;         // second compute stream (odd chunks) or null
     cudaEvent_t ev_start = nullptr, ev_in[16] = {}, ev_done[16] = {};
     long long *kstat = nullptr;         // pinned [16][2]: error bits, committed steps
     double *tstage = nullptr;           // pinned [n_members]: final times (a pageable
@@ -678,7 +679,7 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         hsgn_ctx *kc = new hsgn_ctx();
         kc->desc = c->desc;
         kc->desc.n_members = cnt;
-        kc->stream = c->stream;
+        kc->stream = (c->cs2 && (k & 1)) ? c->cs2 : c->stream;   // chunks alternate compute streams
         kc->device = c->device;
         kc->n = c->n; kc->members = cnt; kc->dx = c->dx;
         kc->g = c->g; kc->cfl = c->cfl; kc->mcfl = c->mcfl; kc->h_min = c->h_min;
@@ -899,6 +900,7 @@ void hsgn_destroy(hsgn_ctx *c)
     free_kids(c);
     if (c->cp_in) cudaStreamDestroy(c->cp_in);
     if (c->cp_out) cudaStreamDestroy(c->cp_out);
+    if (c->cs2) cudaStreamDestroy(c->cs2);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
     for (int k = 0; k < KIDS_MAX; k++) {
         if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
@@ -1118,8 +1120,7 @@ hsgn_status hsgn_run_host(hsgn_ctx *c, const double *h, const double *q, const d
     if (c->scheme == 2)
         return fail(c, HSGN_E_INVALID, "hsgn_run_host: SGN geometry depends on the whole state (use set_state)");
     chunks = std::min(std::min(chunks, KIDS_MAX), c->members);
-    hsgn_status st = make_kids(c, chunks);
-    if (st != HSGN_OK) return st;
+    hsgn_status st;
     if (!c->cp_in) {
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cp_in, cudaStreamNonBlocking));
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cp_out, cudaStreamNonBlocking));
@@ -1130,13 +1131,19 @@ hsgn_status hsgn_run_host(hsgn_ctx *c, const double *h, const double *q, const d
         }
         CUDA_TRY(c, cudaMallocHost(&c->kstat, KIDS_MAX * 2 * sizeof(long long)));
         CUDA_TRY(c, cudaMallocHost(&c->tstage, size_t(c->members) * sizeof(double)));
+        // odd chunks run on a second compute stream: two chunks' kernels interleave
+        // and fill each other's last-wave tails (HSGN_RH_STREAMS=1: one stream)
+        const char *e = std::getenv("HSGN_RH_STREAMS");
+        if (!(e && std::atoi(e) == 1)) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cs2, cudaStreamNonBlocking));
     }
+    if ((st = make_kids(c, chunks)) != HSGN_OK) return st;
     c->have_state = false;                       // our buffers are the chunks' from here on
     const double *src[4] = {h, q, K, W};
     double *dst[4] = {h_out, q_out, K_out, W_out};
     const size_t n = size_t(c->n);
     CUDA_TRY(c, cudaEventRecord(c->ev_start, c->stream));   // earlier work on our buffers
     CUDA_TRY(c, cudaStreamWaitEvent(c->cp_in, c->ev_start, 0));
+    if (c->cs2) CUDA_TRY(c, cudaStreamWaitEvent(c->cs2, c->ev_start, 0));
     long long l0 = 0;
     for (hsgn_ctx *kc : c->kids) l0 += kc->launches;
     size_t m0 = 0;
@@ -1147,10 +1154,10 @@ hsgn_status hsgn_run_host(hsgn_ctx *c, const double *h, const double *q, const d
             CUDA_TRY(c, cudaMemcpyAsync(kc->buf[0][f], src[f] + m0 * n, cn * sizeof(double),
                                         cudaMemcpyDefault, c->cp_in));
         CUDA_TRY(c, cudaEventRecord(c->ev_in[k], c->cp_in));
-        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_in[k], 0));
+        CUDA_TRY(c, cudaStreamWaitEvent(kc->stream, c->ev_in[k], 0));
         if ((st = kid_state_init(kc, t0)) != HSGN_OK) return fail(c, st, kc->last_error);
         if ((st = run_steps_impl(kc, n_steps)) != HSGN_OK) return fail(c, st, kc->last_error);
-        CUDA_TRY(c, cudaEventRecord(c->ev_done[k], c->stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev_done[k], kc->stream));
         CUDA_TRY(c, cudaStreamWaitEvent(c->cp_out, c->ev_done[k], 0));
         for (int f = 0; f < 4; f++)
             CUDA_TRY(c, cudaMemcpyAsync(dst[f] + m0 * n, kc->buf[kc->cur][f], cn * sizeof(double),
@@ -1163,6 +1170,7 @@ hsgn_status hsgn_run_host(hsgn_ctx *c, const double *h, const double *q, const d
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->cp_out));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->cs2) CUDA_TRY(c, cudaStreamSynchronize(c->cs2));
     if (t_out) std::memcpy(t_out, c->tstage, size_t(c->members) * sizeof(double));
     long long l1 = 0;
     for (hsgn_ctx *kc : c->kids) l1 += kc->launches;

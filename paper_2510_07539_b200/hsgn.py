@@ -297,7 +297,7 @@ class Solver:
                                         C.c_void_p(t.ctypes.data)))
         return out, t
 
-    def run_host(self, h, q, K, W, n_steps: int, out=None, chunks: int = 4, t0: float = 0.0):
+    def run_host(self, h, q, K, W, n_steps: int, out=None, chunks: int = 8, t0: float = 0.0):
         """hsgn_run_host: a whole job from host arrays (numpy or CPU tensors, pinned
         for copy/compute overlap) -- n_steps steps of every member, pipelined over
         member chunks.  Returns ((h, q, K, W) written into `out` or new numpy

@@ -39,7 +39,7 @@ def main():
     s.run_steps(18)
     _, tc = wall(lambda: s.run_steps(steps))
     print(f"{steps} steps on the device: {tc * 1e3:.1f} ms")
-    for ch in (1, 2, 4, 8, 16):
+    for ch in ([int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else (1, 2, 4, 8, 16)):
         s.run_host(*pin, steps, out=outp, chunks=ch)
         _, tr = wall(lambda: s.run_host(*pin, steps, out=outp, chunks=ch))
         print(f"run_host chunks {ch:2d}: {tr * 1e3:.1f} ms  ({2 * N * steps / tr / 1e9:.1f} G cell-stage/s)")

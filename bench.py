@@ -360,13 +360,15 @@ def main():
         s.run_steps(a.steps)       # per-stage events are not recorded for slab contexts
         ms1 = ms2 = None
     else:
-        ms1, ms2 = s.run_steps_timed(a.steps)
+        # the K steps as one CUDA graph with event nodes between the kernels
+        # (hsgn_run_steps_timed): device time of the steps and of each stage kernel
+        ms1, ms2, ms_steps = s.run_steps_timed(a.steps, total=True)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     ck = clocks.stop()
     launches = s.launches - l0
-    elapsed = ev0.elapsed_time(ev1)
+    elapsed = ev0.elapsed_time(ev1) if slab else ms_steps
     if slab:
         ms1 = ms2 = 0.5 * elapsed        # step-average model below
     t = torch.tensor([elapsed, ms1, ms2], device="cuda", dtype=torch.float64)

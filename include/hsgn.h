@@ -213,12 +213,15 @@ hsgn_status hsgn_run_steps(hsgn_ctx *ctx, int64_t n_steps);
  * steps; polls the device every `poll` steps.  *steps_done = steps taken. */
 hsgn_status hsgn_advance_to(hsgn_ctx *ctx, double t_end, int64_t max_steps,
                             int64_t *steps_done);
-/* Enqueue n_steps automatic-dt steps EAGERLY with a CUDA event recorded
- * between consecutive kernels on the context's stream, synchronise, and
- * return in stage_ms[0] / stage_ms[1] the summed device time (ms) of the
- * stage-1 / stage-2 kernels (stage_ms[1] = 0 for a 1-stage tableau; for a fused
- * step, stage_ms[0] is the fused kernel and stage_ms[1] = 0).  Same arithmetic
- * as hsgn_run_steps; used by bench.py for per-kernel rooflines. */
+/* Run n_steps automatic-dt steps as ONE CUDA graph (captured with event record
+ * nodes before, between and after the kernels, then launched once -- the launch
+ * mode of hsgn_run_steps), synchronise, and return (ms, device clock) in
+ * stage_ms[0] / stage_ms[1] the summed time of the stage-1 / stage-2 kernels
+ * (stage_ms[1] = 0 for a 1-stage tableau; for a fused step stage_ms[0] is the
+ * fused kernel) and in stage_ms[2] the time of the whole n steps (first to last
+ * kernel).  stage_ms: 3 doubles.  Same arithmetic as hsgn_run_steps; used by
+ * bench.py for the step time and the per-kernel rooflines.  Needs a
+ * non-default stream; not for slab contexts (HSGN_E_INVALID). */
 hsgn_status hsgn_run_steps_timed(hsgn_ctx *ctx, int64_t n_steps, double *stage_ms);
 /* Wait for the stream; return the latched device status. */
 hsgn_status hsgn_sync(hsgn_ctx *ctx);

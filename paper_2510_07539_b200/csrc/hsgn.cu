@@ -91,6 +91,7 @@ struct hsgn_ctx {
     int sw = 0, sT = 0, stiles = 0;
     int picard = 0;               // A24 Picard passes of the SI depth solve (0: the paper's)
     bool wb = false;              // A25 exactly well-balanced face form of the SI stage
+    bool ev_ext = false;          // record events as graph nodes (timed capture)
     bool pdl = false;             // programmatic dependent launch of the step's kernels
                                   // (HSGN_PDL=1; measured no gain on cfg3, -7 % on cfg2)
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
@@ -199,6 +200,14 @@ cudaError_t launch_pdl(hsgn_ctx *c, void (*k)(KArgs...), dim3 grid, dim3 block, 
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+// Event record on the context's stream; inside a timed capture as an event
+// record node of the graph (cudaEventRecordExternal), so it times the replay.
+cudaError_t rec_ev(hsgn_ctx *c, cudaEvent_t e)
+{
+    return c->ev_ext ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
+                     : cudaEventRecord(e, c->stream);
+}
+
 template <bool S2, bool FIN, bool BATHY>
 hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
 {
@@ -255,7 +264,7 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
         B.U1[f] = c->buf[2][f];
     }
     hsgn_status st;
-    if (ev) CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
+    if (ev) CUDA_TRY(c, rec_ev(c, ev[0]));
     if (c->scheme == 2) {
         dim3 grid(c->stiles, c->members);
         if (c->x_stages == 1) {
@@ -263,19 +272,19 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
             sgn_kernel<false, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
-            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
         } else {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
             sgn_kernel<false, false><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
-            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
             sgn_kernel<true, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
         }
-        if (ev) CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+        if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
     } else if (c->scheme == 1) {
         dim3 grid(c->xtiles, c->members);
         const bool filt = c->filter_sigma > 0.0;
@@ -285,20 +294,20 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
             else explicit_kernel<false, true, false><<<grid, XNT, XSMEM_BYTES_NF, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
-            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
         } else {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
             explicit_kernel<false, false, false><<<grid, XNT, XSMEM_BYTES_NF, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
-            if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
             if (filt) explicit_kernel<true, true, true><<<grid, XNT, XSMEM_BYTES, c->stream>>>(P, B);
             else explicit_kernel<true, true, false><<<grid, XNT, XSMEM_BYTES_NF, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
         }
-        if (ev) CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+        if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
     } else if (c->fused) {
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         const int items = c->tiles * c->members;
@@ -313,26 +322,26 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
         c->launches++;
         CUDA_TRY(c, cudaGetLastError());
         if (ev) {
-            CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
-            CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+            CUDA_TRY(c, rec_ev(c, ev[1]));
+            CUDA_TRY(c, rec_ev(c, ev[2]));
         }
     } else if (c->tab.stages == 1) {
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         st = launch_stage_b<false, true>(c, P, B);
         if (st != HSGN_OK) return st;
         if (ev) {
-            CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
-            CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+            CUDA_TRY(c, rec_ev(c, ev[1]));
+            CUDA_TRY(c, rec_ev(c, ev[2]));
         }
     } else {
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
         st = launch_stage_b<false, false>(c, P, B);
         if (st != HSGN_OK) return st;
-        if (ev) CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+        if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
         st = launch_stage_b<true, true>(c, P, B);
         if (st != HSGN_OK) return st;
-        if (ev) CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+        if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
     }
     if (dt_copy)
         CUDA_TRY(c, cudaMemcpyAsync(dt_copy, c->dt, c->members * sizeof(double),
@@ -1244,29 +1253,55 @@ hsgn_status hsgn_run_steps_timed(hsgn_ctx *c, int64_t n_steps, double *stage_ms)
     if (st != HSGN_OK) return st;
     if (n_steps < 0 || !stage_ms) return HSGN_E_INVALID;
     if (c->slab) return fail(c, HSGN_E_INVALID, "hsgn_run_steps_timed: not for slab contexts");
+    if (!c->stream) return fail(c, HSGN_E_INVALID, "hsgn_run_steps_timed: needs a non-default stream");
     st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
     if (st != HSGN_OK) return st;
-    std::vector<cudaEvent_t> ev(size_t(n_steps) * 3);
+    // the n steps are captured into one CUDA graph with event record nodes
+    // before, between and after the kernels, instantiated, then launched once:
+    // the same launch mode as hsgn_run_steps, timed on the device
+    const size_t ne = size_t(n_steps) * 3 + 2;
+    std::vector<cudaEvent_t> ev(ne);
     for (auto &e : ev) CUDA_TRY(c, cudaEventCreate(&e));
-    st = launch_dtc(c, c->host_steps, 0, 1);
-    for (int64_t k = 0; k < n_steps && st == HSGN_OK; k++) {
-        st = enqueue_step(c, c->cur, c->host_steps, &ev[3 * k]);
-        c->cur ^= 1;
-        c->host_steps++;
+    cudaGraph_t gr = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->ev_ext = true;
+    cudaError_t ce = rec_ev(c, ev[ne - 2]);
+    int cc = c->cur;
+    if (ce == cudaSuccess) st = launch_dtc(c, c->host_steps, 0, 1);
+    for (int64_t k = 0; k < n_steps && st == HSGN_OK && ce == cudaSuccess; k++) {
+        st = enqueue_step(c, cc, c->host_steps + k, &ev[3 * k]);
+        cc ^= 1;
     }
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    stage_ms[0] = stage_ms[1] = 0.0;
-    if (st == HSGN_OK) {
+    if (ce == cudaSuccess) ce = rec_ev(c, ev[ne - 1]);
+    c->ev_ext = false;
+    const cudaError_t ce2 = cudaStreamEndCapture(c->stream, &gr);
+    if (st == HSGN_OK && ce == cudaSuccess && ce2 == cudaSuccess) ce = cudaGraphInstantiate(&gx, gr, 0);
+    if (st == HSGN_OK && ce == cudaSuccess && ce2 == cudaSuccess) ce = cudaGraphLaunch(gx, c->stream);
+    if (st == HSGN_OK && ce == cudaSuccess && ce2 == cudaSuccess) {
+        c->cur = cc;
+        c->host_steps += n_steps;
+        ce = cudaStreamSynchronize(c->stream);
+    }
+    stage_ms[0] = stage_ms[1] = stage_ms[2] = 0.0;
+    if (st == HSGN_OK && ce == cudaSuccess && ce2 == cudaSuccess) {
         for (int64_t k = 0; k < n_steps; k++) {
             float a = 0.f, b = 0.f;
-            CUDA_TRY(c, cudaEventElapsedTime(&a, ev[3 * k], ev[3 * k + 1]));
-            CUDA_TRY(c, cudaEventElapsedTime(&b, ev[3 * k + 1], ev[3 * k + 2]));
+            cudaEventElapsedTime(&a, ev[3 * k], ev[3 * k + 1]);
+            cudaEventElapsedTime(&b, ev[3 * k + 1], ev[3 * k + 2]);
             stage_ms[0] += a;
             stage_ms[1] += b;
         }
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, ev[ne - 2], ev[ne - 1]);
+        stage_ms[2] = tot;
     }
+    if (gx) cudaGraphExecDestroy(gx);
+    if (gr) cudaGraphDestroy(gr);
     for (auto &e : ev) cudaEventDestroy(e);
     if (st != HSGN_OK) return st;
+    if (ce != cudaSuccess || ce2 != cudaSuccess)
+        return fail(c, HSGN_E_CUDA, std::string("timed graph: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ce2));
     return reconcile(c);
 }
 

@@ -326,13 +326,14 @@ class Solver:
     def run_steps(self, n_steps: int):
         self._chk(self.L.hsgn_run_steps(self.ctx, int(n_steps)))
 
-    def run_steps_timed(self, n_steps: int):
-        """Eager steps with CUDA events between kernels; returns summed device
-        ms per stage kind (stage 1, stage 2)."""
-        ms = np.zeros(2)
+    def run_steps_timed(self, n_steps: int, total: bool = False):
+        """n steps as one CUDA graph with event nodes between the kernels; returns
+        the summed device ms per stage kind (stage 1, stage 2) and, with
+        total=True, also the device ms of the whole n steps."""
+        ms = np.zeros(3)
         self._chk(self.L.hsgn_run_steps_timed(self.ctx, int(n_steps),
                                               ms.ctypes.data_as(C.POINTER(C.c_double))))
-        return float(ms[0]), float(ms[1])
+        return (float(ms[0]), float(ms[1]), float(ms[2])) if total else (float(ms[0]), float(ms[1]))
 
     def advance_to(self, t_end: float, max_steps: int = 1 << 40) -> int:
         s = C.c_int64()

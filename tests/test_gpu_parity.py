@@ -189,6 +189,25 @@ def test_mass_conservation_gpu():
 
 
 @pytest.mark.parametrize("kmode", KMODES)
+def test_timed_graph_equals_run_steps(kmode):
+    """hsgn_run_steps_timed (bench.py's timed region: the K steps as one graph with
+    event nodes) advances exactly like hsgn_run_steps, and its kernel times sum
+    to less than the whole."""
+    w = W.random_smooth(3000, 4, seed=11, amp=0.06)
+    a, b = gpu_solver(w, kmode=kmode), gpu_solver(w, kmode=kmode)
+    a.run_steps(25)
+    l0 = b.launches
+    ms1, ms2, tot = b.run_steps_timed(25, total=True)
+    assert b.launches - l0 == 1 + (2 if kmode == "fused" else 3) * 25
+    (x, tx), (y, ty) = a.get_state(device=False), b.get_state(device=False)
+    for f, g in zip(x, y):
+        assert np.array_equal(f, g)
+    assert np.array_equal(tx, ty)
+    assert 0.0 < ms1 and 0.0 <= ms2 and ms1 + ms2 < tot
+    assert b.diagnostics()["steps"] == 25
+
+
+@pytest.mark.parametrize("kmode", KMODES)
 def test_launch_count_per_step(kmode):
     """per step: the fused step kernel (or stage 1 + stage 2) and dt/commit;
     plus one dt kernel per call."""

@@ -58,9 +58,26 @@ MUTANTS = {
         ("return sqrt(g * h + (lambda / 3.0) * eta_over_h * eta_over_h);",
          "return sqrt(g * h + (lambda / 3.0) * (eta_over_h - 1.0));"),
 }
+# A25 (well-balanced face form) mutants: checked against tests/test_oracle_wb.py
+WB_MUTANTS = {
+    "A25 dhat sign of (2 sigma - 1)":
+        ("return -(2.0 * sig - 1.0) / (3.0 * ht) * bt;", "return -(2.0 * sig + 1.0) / (3.0 * ht) * bt;"),
+    "A25 dhat one-sided 1/beta1":
+        ("double sig = 0.5 * (s0 + s1), ht = 0.5 * (h0 + h1), bt = 0.5 * (b0 + b1);",
+         "double sig = 0.5 * (s0 + s1), ht = 0.5 * (h0 + h1), bt = b0;"),
+    "A25 mu without the factor 2":
+        ("ml = 2.0 * lt2 * wb_delta(eh, eH, i - 1, lam, tau, G);",
+         "ml = 1.0 * lt2 * wb_delta(eh, eH, i - 1, lam, tau, G);"),
+    "A25 face hydrostatic term dropped (right face)":
+        ("+ 0.5 * g * (X(eh, i) + X(eh, i + 1)) * (X(eb, i + 1) - X(eb, i));",
+         "+ 0.0 * g * (X(eh, i) + X(eh, i + 1)) * (X(eb, i + 1) - X(eb, i));"),
+    "A25 qbar face fluxes subtracted with the wrong sign":
+        ("qn = qd[i + 1] - (tau / (2.0 * dx)) * (Phr + Phl);", "qn = qd[i + 1] - (tau / (2.0 * dx)) * (Phr - Phl);"),
+}
 
 ok = True
-for name, (a, b) in MUTANTS.items():
+for name, (a, b), tf in [(k, v, "test_oracle_pins.py") for k, v in MUTANTS.items()] + \
+                        [(k, v, "test_oracle_wb.py") for k, v in WB_MUTANTS.items()]:
     assert SRC.count(a) >= 1, name
     mut = SRC.replace(a, b, 1)
     with tempfile.TemporaryDirectory() as d:
@@ -71,7 +88,7 @@ for name, (a, b) in MUTANTS.items():
                                "-o", so, c, "-lm"])
         env = dict(os.environ, HSGN_ORACLE_LIB=so)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                            os.path.join(ROOT, "tests", "test_oracle_pins.py")],
+                            os.path.join(ROOT, "tests", tf)],
                            cwd=ROOT, env=env, capture_output=True, text=True)
         caught = r.returncode != 0
         first = [l for l in r.stdout.splitlines() if l.startswith("FAILED")][:1]

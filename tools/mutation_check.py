@@ -75,9 +75,38 @@ WB_MUTANTS = {
         ("qn = qd[i + 1] - (tau / (2.0 * dx)) * (Phr + Phl);", "qn = qd[i + 1] - (tau / (2.0 * dx)) * (Phr - Phl);"),
 }
 
+# explicit hSGN scheme (A22) mutants: tests/test_oracle_explicit.py
+EX_MUTANTS = {
+    "explicit: centred mass flux sign":
+        ("L[0][i] = -Dxq;", "L[0][i] = +Dxq;"),
+    "explicit: pressure term lam alpha DxH dropped":
+        ("- a2 * Dxh - lam * alpha * DxH;", "- a2 * Dxh;"),
+    "explicit: W relaxation source sign":
+        ("- lam * (H / (h * h) - 1.0);", "+ lam * (H / (h * h) - 1.0);"),
+    "explicit: Heun weight 1/2 -> 1":
+        ("U[k][i] = 0.5 * Un[k][i] + 0.5 * (U1[k][i] + dt * Lb[k][i]);",
+         "U[k][i] = 0.0 * Un[k][i] + 1.0 * (U1[k][i] + dt * Lb[k][i]);"),
+}
+# classical SGN scheme (A23) mutants: tests/test_oracle_sgn.py
+SGN_MUTANTS = {
+    "SGN: h* with g h instead of g h^3 (the literal P:591)":
+        ("* (g * hp3 * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i))", "* (g * hp * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i))"),
+    "SGN: phi system off-diagonal h^3/3 -> h^3":
+        ("double cl = hl * hl * hl / (3.0 * dx * dx), cr = hr * hr * hr / (3.0 * dx * dx);",
+         "double cl = hl * hl * hl / (1.0 * dx * dx), cr = hr * hr * hr / (1.0 * dx * dx);"),
+    "SGN: source h phi sign":
+        ("Lq[i] = -(Fq[i + 1] - Fq[i]) / dx + XS(eh, i) * phi[i];",
+         "Lq[i] = -(Fq[i + 1] - Fq[i]) / dx - XS(eh, i) * phi[i];"),
+    "SGN: Rusanov speed without sqrt(g h)":
+        ("double am = fabs(um) + sqrt(g * vm[0]), ap = fabs(up_) + sqrt(g * vp[0]);",
+         "double am = fabs(um), ap = fabs(up_);"),
+}
+
 ok = True
 for name, (a, b), tf in [(k, v, "test_oracle_pins.py") for k, v in MUTANTS.items()] + \
-                        [(k, v, "test_oracle_wb.py") for k, v in WB_MUTANTS.items()]:
+                        [(k, v, "test_oracle_wb.py") for k, v in WB_MUTANTS.items()] + \
+                        [(k, v, "test_oracle_explicit.py") for k, v in EX_MUTANTS.items()] + \
+                        [(k, v, "test_oracle_sgn.py") for k, v in SGN_MUTANTS.items()]:
     assert SRC.count(a) >= 1, name
     mut = SRC.replace(a, b, 1)
     with tempfile.TemporaryDirectory() as d:

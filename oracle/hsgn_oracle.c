@@ -859,7 +859,7 @@ int orc_explicit_run(const orc_problem *P, int stages, double cfl, double dt_fix
 }
 
 /* ------------------------------------------------------------------------ */
-/* Classical SGN scheme, flat bottom          */
+/* Classical SGN scheme, with bathymetry      */
 /* ------------------------------------------------------------------------ */
 /*
  * Explicit scheme for the standard SGN equations in elliptic-hyperbolic form
@@ -875,28 +875,42 @@ int orc_explicit_run(const orc_problem *P, int stages, double cfl, double dt_fix
  * states; phi ghosts: periodic wrap, wall phi_{-1} = -phi_0 (phi is an
  * acceleration, odd like q), transmissive phi_{-1} = phi_0.  K and W are not
  * part of this model and are carried unchanged.
+ *
+ * Bathymetry (eq. SGNb_standard; reading A26): the phi equation
+ *   h phi - (h^3/3 phi_x)_x + kappa phi = -(h^3/3 g zeta_xx + 2 h^3/3 u_x^2 + rho)_x - h Q b_x,
+ *   kappa = (h^2 b_x/2)_x + 3 h b_x^2/4,  rho = -(h^2 b_x/2) g zeta_x + h^3 u^2 b_xx,
+ *   Q = (h/2) g zeta_xx - (3 g b_x/4) zeta_x + h u_x^2 + (3/2) h u^2 b_xx,
+ * follows from P:175-186 with phi := Du/Dt + g zeta_x, so the momentum carries
+ * the hydrostatic source: (hu)_t + (hu^2 + g h^2/2)_x + g h b_x = h phi (P:566
+ * prints it without g h b_x, which would move the lake at rest).  Discretised
+ * like the flat scheme: zeta = h + b in the g-term's second differences, rho and
+ * the derivatives of zeta, u, b centred at cells i-1, i, i+1, kappa_i =
+ * (h^2_{i+1/2}(b_{i+1} - b_i) - h^2_{i-1/2}(b_i - b_{i-1}))/(2 dx^2) + (3/4) h_i (D_x b)_i^2,
+ * source -g h_i (D_x b)_i.  b ghosts even.  b = 0 reproduces the flat scheme
+ * bit for bit (every added term is a product with a difference of b).
  */
 static int sgn_L(const orc_problem *P, const double *h, const double *q, double *Lh, double *Lq)
 {
     const int n = P->n, G = 2;
     const double dx = P->dx, g = P->g;
     const size_t ne = (size_t)(n + 2 * G);
-    if (P->b) return ORC_E_INVALID;
-    double *buf = (double *)calloc(ne * 3 + (size_t)(n + 1) * 2 + (size_t)n * 4, sizeof(double));
+    double *buf = (double *)calloc(ne * 4 + (size_t)(n + 1) * 2 + (size_t)n * 4, sizeof(double));
     if (!buf) return ORC_E_INVALID;
-    double *eh = buf, *eq = eh + ne, *eu = eq + ne;
-    double *Fh = eu + ne, *Fq = Fh + (n + 1);
+    double *eh = buf, *eq = eh + ne, *eu = eq + ne, *eb = eu + ne;
+    double *Fh = eb + ne, *Fq = Fh + (n + 1);
     double *lo = Fq + (n + 1), *di = lo + n, *up = di + n, *rhs = up + n;
     double *phi = (double *)calloc((size_t)n, sizeof(double));
     if (!phi) { free(buf); return ORC_E_INVALID; }
     fill_ghosts(h, n, G, P->bc_left, P->bc_right, 1.0, eh);
     fill_ghosts(q, n, G, P->bc_left, P->bc_right, -1.0, eq);
+    if (P->b) fill_ghosts(P->b, n, G, P->bc_left, P->bc_right, 1.0, eb);
     int st = ORC_OK;
     for (int i = -G; i < n + G; i++) {
         if (!(eh[i + G] > P->h_min)) st = ORC_E_DRY;
         eu[i + G] = eq[i + G] / eh[i + G];
     }
 #define XS(a, i) ((a)[(i) + G])
+#define XZ(i) (XS(eh, i) + XS(eb, i))         /* zeta = h + b */
     /* Rusanov fluxes of (q, q^2/h + g h^2/2) at faces f+1/2, f = -1 .. n-1 */
     for (int f = -1; f <= n - 1; f++) {
         double vm[2], vp[2];
@@ -929,12 +943,44 @@ static int sgn_L(const orc_problem *P, const double *h, const double *q, double 
         double hp = XS(eh, i + 1), hm = XS(eh, i - 1);
         double hp3 = hp * hp * hp, hm3 = hm * hm * hm;
         double up2 = XS(eu, i + 2) - XS(eu, i), um2 = XS(eu, i) - XS(eu, i - 2);
-        rhs[i] = -(1.0 / (6.0 * dx * dx * dx))
-                 * (g * hp3 * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i)) + 0.5 * hp3 * up2 * up2
-                    - g * hm3 * (XS(eh, i) - 2.0 * hm + XS(eh, i - 2)) - 0.5 * hm3 * um2 * um2);
+        if (!P->b) {
+            rhs[i] = -(1.0 / (6.0 * dx * dx * dx))
+                     * (g * hp3 * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i)) + 0.5 * hp3 * up2 * up2
+                        - g * hm3 * (XS(eh, i) - 2.0 * hm + XS(eh, i - 2)) - 0.5 * hm3 * um2 * um2);
+        } else {
+            rhs[i] = -(1.0 / (6.0 * dx * dx * dx))
+                     * (g * hp3 * (XZ(i + 2) - 2.0 * XZ(i + 1) + XZ(i)) + 0.5 * hp3 * up2 * up2
+                        - g * hm3 * (XZ(i) - 2.0 * XZ(i - 1) + XZ(i - 2)) - 0.5 * hm3 * um2 * um2);
+            /* rho at cells j = i -+ 1 and Q at cell i (A26) */
+            double rho[2];
+            for (int s2 = 0; s2 < 2; s2++) {
+                const int j = s2 == 0 ? i - 1 : i + 1;
+                const double hj = XS(eh, j), uj = XS(eu, j);
+                const double bx = (XS(eb, j + 1) - XS(eb, j - 1)) / (2.0 * dx);
+                const double zx = (XZ(j + 1) - XZ(j - 1)) / (2.0 * dx);
+                const double bxx = (XS(eb, j + 1) - 2.0 * XS(eb, j) + XS(eb, j - 1)) / (dx * dx);
+                rho[s2] = -(hj * hj * bx / 2.0) * g * zx + hj * hj * hj * uj * uj * bxx;
+            }
+            const double h0 = XS(eh, i), u0 = XS(eu, i);
+            const double bx = (XS(eb, i + 1) - XS(eb, i - 1)) / (2.0 * dx);
+            const double zx = (XZ(i + 1) - XZ(i - 1)) / (2.0 * dx);
+            const double zxx = (XZ(i + 1) - 2.0 * XZ(i) + XZ(i - 1)) / (dx * dx);
+            const double bxx = (XS(eb, i + 1) - 2.0 * XS(eb, i) + XS(eb, i - 1)) / (dx * dx);
+            const double ux = (XS(eu, i + 1) - XS(eu, i - 1)) / (2.0 * dx);
+            const double Q = (h0 / 2.0) * g * zxx - (3.0 * g * bx / 4.0) * zx + h0 * ux * ux
+                             + 1.5 * h0 * u0 * u0 * bxx;
+            rhs[i] += -(rho[1] - rho[0]) / (2.0 * dx) - h0 * Q * bx;
+        }
         lo[i] = -cl;
         up[i] = -cr;
         di[i] = XS(eh, i) + cl + cr;
+        if (P->b) {
+            const double bx = (XS(eb, i + 1) - XS(eb, i - 1)) / (2.0 * dx);
+            const double kap = (hr * hr * (XS(eb, i + 1) - XS(eb, i)) - hl * hl * (XS(eb, i) - XS(eb, i - 1)))
+                               / (2.0 * dx * dx)
+                               + 0.75 * XS(eh, i) * bx * bx;
+            di[i] += kap;
+        }
     }
     if (P->bc_left != ORC_BC_PERIODIC) {
         /* phi_{-1} = p phi_0 folds into the diagonal: -cl (p phi_0) */
@@ -949,7 +995,9 @@ static int sgn_L(const orc_problem *P, const double *h, const double *q, double 
     for (int i = 0; i < n; i++) {
         Lh[i] = -(Fh[i + 1] - Fh[i]) / dx;
         Lq[i] = -(Fq[i + 1] - Fq[i]) / dx + XS(eh, i) * phi[i];
+        if (P->b) Lq[i] -= g * XS(eh, i) * (XS(eb, i + 1) - XS(eb, i - 1)) / (2.0 * dx);   /* A26 */
     }
+#undef XZ
 #undef XS
     free(phi);
     free(buf);

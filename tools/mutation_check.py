@@ -101,12 +101,26 @@ SGN_MUTANTS = {
         ("double am = fabs(um) + sqrt(g * vm[0]), ap = fabs(up_) + sqrt(g * vp[0]);",
          "double am = fabs(um), ap = fabs(up_);"),
 }
+# bathymetric SGN closure (A26) mutants: tests/test_oracle_sgnb.py
+SGNB_MUTANTS = {
+    "SGNb: hydrostatic source g h b_x dropped (the literal P:566)":
+        ("if (P->b) Lq[i] -= g * XS(eh, i)", "if (0) Lq[i] -= g * XS(eh, i)"),
+    "SGNb: kappa 3/4 h b_x^2 term sign":
+        ("+ 0.75 * XS(eh, i) * bx * bx;", "- 0.75 * XS(eh, i) * bx * bx;"),
+    "SGNb: rho hydrostatic part sign":
+        ("rho[s2] = -(hj * hj * bx / 2.0) * g * zx", "rho[s2] = +(hj * hj * bx / 2.0) * g * zx"),
+    "SGNb: Q without the 3 g b_x zeta_x / 4 term":
+        ("- (3.0 * g * bx / 4.0) * zx + h0 * ux * ux", "+ 0.0 * zx + h0 * ux * ux"),
+    "SGNb: g-term on h instead of zeta":
+        ("* (g * hp3 * (XZ(i + 2) - 2.0 * XZ(i + 1) + XZ(i))", "* (g * hp3 * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i))"),
+}
 
 ok = True
 for name, (a, b), tf in [(k, v, "test_oracle_pins.py") for k, v in MUTANTS.items()] + \
                         [(k, v, "test_oracle_wb.py") for k, v in WB_MUTANTS.items()] + \
                         [(k, v, "test_oracle_explicit.py") for k, v in EX_MUTANTS.items()] + \
-                        [(k, v, "test_oracle_sgn.py") for k, v in SGN_MUTANTS.items()]:
+                        [(k, v, "test_oracle_sgn.py") for k, v in SGN_MUTANTS.items()] + \
+                        [(k, v, "test_oracle_sgnb.py") for k, v in SGNB_MUTANTS.items()]:
     assert SRC.count(a) >= 1, name
     mut = SRC.replace(a, b, 1)
     with tempfile.TemporaryDirectory() as d:

@@ -257,7 +257,9 @@ int32_t hsgn_get_fused(const hsgn_ctx *ctx);
  * faces with alpha = max(|u| + sqrt(g h)), a tridiagonal phi system per stage
  * (reading A23: g h^3 in h*), source h phi; Euler or Heun;
  * dt = CFL dx / max(|u| + sqrt(g h)); K, W are carried unchanged.
- * Flat bottom, no filter, no relaxation zones or slabs.  The phi overlap is
+ * With bathymetry (hsgn_set_bathymetry) the phi system carries the kappa, rho, Q
+ * closure of P:562-578 and the momentum the hydrostatic source -g h b_x
+ * (reading A26).  No filter, no relaxation zones or slabs.  The phi overlap is
  * chosen from the state (hsgn_set_state / hsgn_set_scheme); HSGN_E_INVALID if
  * dx is too small against h for the tile width. */
 #define HSGN_SCHEME_SGN 2

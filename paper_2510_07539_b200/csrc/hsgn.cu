@@ -269,18 +269,21 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
         dim3 grid(c->stiles, c->members);
         if (c->x_stages == 1) {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
-            sgn_kernel<false, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
+            if (c->bathy) sgn_kernel<false, true, true><<<grid, SNT, SSMEM_BYTES_B, c->stream>>>(P, B);
+            else sgn_kernel<false, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
             if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
         } else {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
-            sgn_kernel<false, false><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
+            if (c->bathy) sgn_kernel<false, false, true><<<grid, SNT, SSMEM_BYTES_B, c->stream>>>(P, B);
+            else sgn_kernel<false, false><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
             if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
-            sgn_kernel<true, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
+            if (c->bathy) sgn_kernel<true, true, true><<<grid, SNT, SSMEM_BYTES_B, c->stream>>>(P, B);
+            else sgn_kernel<true, true><<<grid, SNT, SSMEM_BYTES, c->stream>>>(P, B);
             c->launches++;
             CUDA_TRY(c, cudaGetLastError());
         }
@@ -432,8 +435,9 @@ hsgn_status ready(hsgn_ctx *c)
     if (!c->ws) return fail(c, HSGN_E_NOWORKSPACE, "workspace not set");
     if (!c->have_params) return fail(c, HSGN_E_INVALID, "hsgn_set_params not called");
     if (!c->have_state) return fail(c, HSGN_E_INVALID, "hsgn_set_state not called");
-    if (c->scheme != 0 && (c->bathy || c->slab || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
-        return fail(c, HSGN_E_INVALID, "explicit / SGN schemes: flat bottom, no relaxation zones, no slabs");
+    if (c->scheme != 0 && ((c->bathy && c->scheme == 1) || c->slab || c->relax.gen_rate > 0.0 ||
+                           c->relax.sp_rate > 0.0))
+        return fail(c, HSGN_E_INVALID, "explicit scheme: flat bottom; explicit / SGN: no relaxation zones, no slabs");
     if (c->picard > 0 && (c->scheme != 0 || c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0))
         return fail(c, HSGN_E_INVALID, "Picard passes: SI scheme without relaxation zones");
     if (c->wb && (c->scheme != 0 || c->picard > 0))
@@ -884,6 +888,9 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(sgn_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
+    cudaFuncSetAttribute(sgn_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES_B));
+    cudaFuncSetAttribute(sgn_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES_B));
+    cudaFuncSetAttribute(sgn_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES_B));
     cudaFuncSetAttribute(explicit_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));

@@ -2021,8 +2021,10 @@ constexpr int SLCAP = SNT * MCH;                 // 2560 rows
 constexpr int SROWS_S = SLCAP + 16;
 // shared: h, q (stencil input, rows -2-? .. L+?), staged outputs h, q, PCR 2 x 3 x SNT
 constexpr size_t SSMEM_BYTES = (size_t(4) * SROWS_S + size_t(6) * SNT) * sizeof(double);
+// with bathymetry: b of rows -4 .. L+3 in a fifth array (A26)
+constexpr size_t SSMEM_BYTES_B = SSMEM_BYTES + size_t(SROWS_S) * sizeof(double);
 
-template <bool HEUN2, bool FINAL>
+template <bool HEUN2, bool FINAL, bool BATHY = false>
 __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs B)
 {
     __shared__ double xw[SNT / 32][3];
@@ -2038,6 +2040,7 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
     double *sh = smem + 4, *sq = sh + SROWS_S;                  // rows -4 .. L+3 (shift 4)
     double *oh = smem + 2 * SROWS_S, *oq = oh + SROWS_S;        // staged outputs
     double *pcr0 = smem + 4 * SROWS_S, *pcr1 = pcr0 + 3 * SNT;
+    double *sb = smem + 4 * SROWS_S + 6 * SNT + 4;               // b rows -4 .. L+3 (BATHY)
     const double *const *X = HEUN2 ? B.U1 : B.Un;
     // ---- load rows -4 .. L+3 of (h, q) of X and, for Heun stage 2, the kept
     // rows of U^n's (h, q) into the output staging (read there by the row's own
@@ -2049,6 +2052,7 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
         const size_t gi = mo + size_t((c >= 0 && c < n) ? c : map_cell(c, n, P.bcl, P.bcr, par));
         cp_async8(sh + r, X[0] + gi);
         cp_async8(sq + r, X[1] + gi);
+        if (BATHY) cp_async8(sb + r, P.b + (gi - mo));             // (b: even at walls)
     }
     if (HEUN2) {
         const size_t g0 = mo + size_t(start + G.klo);
@@ -2082,12 +2086,13 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
     // ---- phi system on own rows (normalised by h_i), partition solve --------
     {
         // windows: h, u over rows r0-2 .. r0+MCH+1
-        double wh[MCH + 4], wu[MCH + 4];
+        double wh[MCH + 4], wu[MCH + 4], wb[MCH + 4];
 #pragma unroll
         for (int k = 0; k < MCH + 4; k++) {
             const int rr = min(r0 - 2 + k, L + 3);
             wh[k] = sh[rr];
             wu[k] = sq[rr] * rcp(wh[k]);
+            wb[k] = BATHY ? sb[rr] : 0.0;
         }
         double am[MCH], cm[MCH], dm[MCH];
 #pragma unroll
@@ -2099,9 +2104,45 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
             double rl = hl * hl * hl * c3 * ih0, rr = hr * hr * hr * c3 * ih0;
             const double hp3 = hp * hp * hp, hm3 = hm * hm * hm;
             const double up2 = wu[i + 4] - wu[i + 2], um2 = wu[i + 2] - wu[i];
-            double rhs = -s6 * (g * hp3 * (wh[i + 4] - 2.0 * hp + h0) + 0.5 * hp3 * up2 * up2
-                                - g * hm3 * (h0 - 2.0 * hm + wh[i]) - 0.5 * hm3 * um2 * um2) * ih0;
-            double dg = 1.0 + rl + rr;
+            double rhs, dg;
+            double kfac = 1.0;               // (BATHY) decay-check factor for kappa < 0
+            if (!BATHY) {
+                rhs = -s6 * (g * hp3 * (wh[i + 4] - 2.0 * hp + h0) + 0.5 * hp3 * up2 * up2
+                             - g * hm3 * (h0 - 2.0 * hm + wh[i]) - 0.5 * hm3 * um2 * um2) * ih0;
+                dg = 1.0 + rl + rr;
+            } else {
+                // A26: zeta = h + b in the g-term; rho at rows r -+ 1, Q at row r, kappa
+                auto z = [&](int k) { return wh[k] + wb[k]; };
+                double rhb = -s6 * (g * hp3 * (z(i + 4) - 2.0 * z(i + 3) + z(i + 2)) + 0.5 * hp3 * up2 * up2
+                                    - g * hm3 * (z(i + 2) - 2.0 * z(i + 1) + z(i)) - 0.5 * hm3 * um2 * um2);
+                const double i2dx = 0.5 * idx, idx2 = idx * idx;
+                auto rho = [&](int k) {           // at window row k
+                    const double hj = wh[k], uj = wu[k];
+                    const double bx = (wb[k + 1] - wb[k - 1]) * i2dx;
+                    const double zx = (z(k + 1) - z(k - 1)) * i2dx;
+                    const double bxx = (wb[k + 1] - 2.0 * wb[k] + wb[k - 1]) * idx2;
+                    return -(hj * hj * bx / 2.0) * g * zx + hj * hj * hj * uj * uj * bxx;
+                };
+                const double u0 = wu[i + 2];
+                const double bx = (wb[i + 3] - wb[i + 1]) * i2dx;
+                const double zx = (z(i + 3) - z(i + 1)) * i2dx;
+                const double zxx = (z(i + 3) - 2.0 * z(i + 2) + z(i + 1)) * idx2;
+                const double bxx = (wb[i + 3] - 2.0 * wb[i + 2] + wb[i + 1]) * idx2;
+                const double ux = (wu[i + 3] - wu[i + 1]) * i2dx;
+                const double Q = (h0 / 2.0) * g * zxx - (3.0 * g * bx / 4.0) * zx + h0 * ux * ux
+                                 + 1.5 * h0 * u0 * u0 * bxx;
+                rhb += -(rho(i + 3) - rho(i + 1)) * i2dx - h0 * Q * bx;
+                rhs = rhb * ih0;
+                const double kap = (hr * hr * (wb[i + 3] - wb[i + 2]) - hl * hl * (wb[i + 2] - wb[i + 1])) * (0.5 * idx2)
+                                   + 0.75 * h0 * bx * bx;
+                dg = 1.0 + rl + rr + kap * ih0;
+                // kappa < 0 weakens the diagonal dominance: scale the coupling in the
+                // decay check; a non-positive h + kappa makes the phi operator singular
+                if (kap < 0.0) {
+                    if (!(h0 + kap > 0.0)) errbits |= ERR_COERC;
+                    kfac = 1.0 / (1.0 + kap * ih0);
+                }
+            }
             // tile ends: truncated (overlap) or physical (phi ghost = p phi_0, A23)
             if (r == 0) {
                 if (G.left_phys) dg -= rl * (P.bcl == BC_WALL ? -1.0 : 1.0);
@@ -2112,7 +2153,7 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
                 rr = 0.0;
             }
             if (r >= L) { rl = 0.0; rr = 0.0; dg = 1.0; rhs = 0.0; }
-            rho_loc = rr > rho_loc ? rr : rho_loc;
+            rho_loc = rr * kfac > rho_loc ? rr * kfac : rho_loc;
             const double a = -rl, c = -rr;
             if (i == 0) {
                 const double inv = rcp(dg);
@@ -2228,7 +2269,8 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
             Mr = Mn;
             if (r >= G.klo && r < G.khi) {
                 const double Lh = -(Fhr - Fhl) * hidx;
-                const double Lq = -(Fqr - Fql) * hidx + hc * phi[i];
+                double Lq = -(Fqr - Fql) * hidx + hc * phi[i];
+                if (BATHY) Lq -= g * hc * (sb[r + 1] - sb[r - 1]) * hidx;          // A26 hydrostatic source
                 double ho, qo;
                 if (HEUN2) {
                     ho = 0.5 * oh[r - G.klo] + 0.5 * (hc + dtm * Lh);

@@ -24,6 +24,8 @@ def ssolver(w, stages=2, **kw):
     order = kw.pop("order", 2)
     s = hs.Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, order=order, **kw)
     s.set_params(w.g, w.lam, CFL_SGN, 0.0)
+    if w.b is not None:
+        s.set_bathymetry(w.b)
     s.set_scheme("sgn", stages)
     s.set_state(w.h.reshape(-1), w.q.reshape(-1), w.K.reshape(-1), w.W.reshape(-1))
     return s
@@ -33,7 +35,7 @@ def scompare(w, s, members, stages=2, steps=None, t_end=None, tol=TOL_STEP, orde
     (h, q, K, Wf), t = s.get_state(device=False)
     worst = 0.0
     for m in members:
-        o = O.Oracle(w.n, w.dx, g=w.g, bc=w.bc, order=order)
+        o = O.Oracle(w.n, w.dx, g=w.g, bc=w.bc, order=order, b=w.b)
         U0 = w.state(m)
         ref, tr, _ = o.sgn_run(U0, cfl=CFL_SGN, stages=stages, steps=steps, t_end=t_end)
         hm = np.max(np.abs(ref[0]))
@@ -130,3 +132,51 @@ def test_sgn_refuses_filter_and_too_fine_grids():
     fine = W.random_smooth(20000, 1, seed=2, amp=0.05, dx=0.005)   # h/dx = 200
     with pytest.raises(hs.HsgnError):
         ssolver(fine)
+
+
+# --------------------------------------------------------------------------
+# bathymetric SGN (reading A26)
+@pytest.mark.parametrize("bc", ["periodic", "wall", "transmissive"])
+@pytest.mark.parametrize("order,stages", [(2, 2), (1, 1)])
+def test_sgnb_one_step_ragged_tiles(bc, order, stages):
+    w = W.random_smooth(5000, 3, seed=57, amp=0.06, bc=(bc, bc), bathy=0.08)
+    w.filter_sigma = 0.0
+    s = ssolver(w, stages=stages, order=order)
+    assert s.geometry.tiles_per_member > 1
+    s.step()
+    scompare(w, s, range(3), stages=stages, steps=1, order=order)
+
+
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_sgnb_runs(bc):
+    w = W.random_smooth(3000, 2, seed=59, amp=0.05, bc=(bc, bc), bathy=0.06)
+    w.filter_sigma = 0.0
+    s = ssolver(w)
+    s.run_steps(40)
+    scompare(w, s, range(2), steps=40, tol=1e-10)
+
+
+def test_sgnb_zero_bathymetry_is_the_flat_path():
+    w = W.random_smooth(2048, 2, seed=61, amp=0.05)
+    w.filter_sigma = 0.0
+    a = ssolver(w)
+    w.b = np.zeros(w.n)
+    b = ssolver(w)
+    a.run_steps(10)
+    b.run_steps(10)
+    (x, _), (y, _) = a.get_state(device=False), b.get_state(device=False)
+    for f, g in zip(x, y):
+        assert np.max(np.abs(f - g)) <= 1e-13 * max(1.0, np.max(np.abs(f)))
+
+
+def test_sgnb_lake_at_rest_small_drift():
+    """zeta = const, u = 0 over bathymetry: phi = 0 and only the O(dx^2) residual
+    of the centred hydrostatic source moves water (oracle pin
+    test_sgnb_lake_at_rest_second_order); the GPU equals the oracle on it."""
+    w = W.lake_at_rest(2000, 0.0)
+    w.filter_sigma = 0.0
+    s = ssolver(w)
+    s.run_steps(50)
+    scompare(w, s, [0], steps=50, tol=1e-10)
+    (h, q, K, Wf), t = s.get_state(device=False)
+    assert np.max(np.abs(q[0])) < 1e-3

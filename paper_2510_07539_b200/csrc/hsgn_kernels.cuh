@@ -1491,8 +1491,9 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 // ---------------------------------------------------------------------------
 // Standalone stage kernel: one IMEX stage over every (tile, member) CTA.
 // STAGE2: inputs U^n and U1 (E, R formed on load); FINAL: this stage produces
-// U^{n+1} (filter, relaxation, dt maxima, time level).  Used for one-stage
-// tableaux and slab (BC_HALO) domains; the two-stage step otherwise runs fused.
+// U^{n+1} (filter, relaxation, dt maxima, time level).  The default kernel
+// organisation; the persistent (stage_pkernel) and fused
+// (step_kernel) organisations are opt-in alternatives with the same arithmetic.
 // ---------------------------------------------------------------------------
 #if HSGN_EXP_TIMING
 #define EXP_T(v) long long v = clock64()

@@ -218,6 +218,7 @@ class Solver:
         return int(self.L.hsgn_get_fused(self.ctx)) == 1
 
     def set_fused(self, on: bool) -> None:
+        """One fused kernel per two-stage step (off by default)."""
         self._chk(self.L.hsgn_set_fused(self.ctx, 1 if on else 0))
 
     def set_scheme(self, scheme: str = "si", stages: int = 2) -> None:
@@ -235,8 +236,8 @@ class Solver:
         self._chk(self.L.hsgn_set_well_balanced(self.ctx, 1 if on else 0))
 
     def set_persistent(self, on: bool) -> None:
-        """Persistent per-stage kernels with next-tile prefetch (default) or one
-        CTA per (tile, member)."""
+        """Persistent per-stage kernels with next-tile prefetch, or one CTA per
+        (tile, member) (the default)."""
         self._chk(self.L.hsgn_set_persistent(self.ctx, 1 if on else 0))
 
     @property

@@ -60,7 +60,7 @@ def gpu_solver(w, **kw):
     hs = _hsgn()
     order = kw.pop("order", 2)
     tab = kw.pop("tableau", None)
-    kmode = kw.pop("kmode", None)          # None: library default (persistent per-stage)
+    kmode = kw.pop("kmode", None)          # None: library default (one CTA per tile and member)
     s = hs.Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, order=order, **kw)
     if kmode is not None:
         s.set_fused(kmode == "fused")

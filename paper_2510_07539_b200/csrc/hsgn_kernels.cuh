@@ -1425,7 +1425,10 @@ __device__ __forceinline__ void carry_tile(const Params &P, const Bufs &B, size_
 // end), dt maxima of the member (final stage) and its next
 // time level (tile 0).
 template <bool FINAL>
-__device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, double dtm, const TileAcc &acc)
+// tm0, tend0: t^n of the member and t_end, read at the CTA's start by tile 0 of
+// a final stage (negative: read here) -- keeps their latency out of the serial tail
+__device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, double dtm, const TileAcc &acc,
+                                              double tm0 = -1.0, double tend0 = -1.0)
 {
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
@@ -1462,8 +1465,8 @@ __device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, dou
             atomicMax(P.maxes + (slot_w * 2 + 0) * members + m, (unsigned long long)__double_as_longlong(um));
             atomicMax(P.maxes + (slot_w * 2 + 1) * members + m, (unsigned long long)__double_as_longlong(nm));
             if (j == 0) {   // t^{n+1} of this member, in the other parity slot
-                const double tm = P.t[P.kpar * members + m];
-                const double t_end = P.ctrl->t_end;
+                const double tm = tm0 >= 0.0 ? tm0 : P.t[P.kpar * members + m];
+                const double t_end = tend0 >= 0.0 ? tend0 : P.ctrl->t_end;
                 P.t[(P.kpar ^ 1) * members + m] = (t_end > 0.0 && dtm == t_end - tm) ? t_end : tm + dtm;
             }
         }
@@ -1552,6 +1555,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     const unsigned int err0 = *((volatile unsigned int *)P.err);
     const double dtm = P.dt[m];
     const double lam = P.lam[m];
+    double tm0 = -1.0, tend0 = -1.0;             // (tile_epilogue: t^{n+1} of tile 0)
+    if (FINAL && j == 0 && tid == 0) { tm0 = P.t[P.kpar * P.members + m]; tend0 = P.ctrl->t_end; }
     unsigned parity = 0u;
     wait_load(Lp, mb, parity);
     if (BATHY && Lp.bulk && (Lp.a0 & 1)) cp_async_wait_all();    // b by cp.async (issue_load)
@@ -1568,7 +1573,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         store_tile(B, mo, s, e - s, false, P.T);
     }
     EXP_T(t2);
-    tile_epilogue<FINAL>(P, j, m, dtm, acc);
+    tile_epilogue<FINAL>(P, j, m, dtm, acc, tm0, tend0);
     // shared memory must outlive the bulk stores' reads (no-op if none)
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 #if HSGN_EXP_TIMING

@@ -21,7 +21,16 @@
  *
  * Every function here is pinned by a test in tests/test_oracle_*.py against
  * something other than itself (closed forms, the paper's printed numbers,
- * dense LU, Fourier symbols derived from the paper); see DESIGN.md section 4.
+ * dense LU, Fourier symbols derived from the paper); see DESIGN.md section 4:
+ *   SI stage / step / run, dt, filter, relaxation zones: test_oracle_pins.py
+ *   explicit hSGN scheme (A22): test_oracle_explicit.py
+ *   classical SGN scheme (A23): test_oracle_sgn.py; bathymetric closure (A26):
+ *     test_oracle_sgnb.py (against the primitive model of P:175-186)
+ *   well-balanced face form (A25): test_oracle_wb.py
+ *   Picard passes (A24): test_oracle_picard.py -- pinned by contraction, rest,
+ *     mass and time order only; the fixed point itself is "parity unpinned"
+ *     (the paper prints no Picard result)
+ * tools/mutation_check.py applies 37 plausible mistakes; every one fails a pin.
  */
 #include <math.h>
 #include <stdint.h>

@@ -1,5 +1,9 @@
+"""Dev probe: time per step of the cfg2 dam break (65536
+cells, latency-bound) for the three kernel organisations and tile sizes.
+    python tools/cfg2_modes.py
+"""
 import sys, time
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __file__.rsplit('/tools/', 1)[0])
 import torch
 from paper_2510_07539_b200 import hsgn, workloads as W
 for mode in ("default", "fused", "persistent"):

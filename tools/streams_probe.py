@@ -1,5 +1,10 @@
+"""Dev probe: the cfg3 ensemble as 1-4 independent solvers on
+separate streams, wall time of 54 steps each -- whether interleaving kernels of
+several member groups fills the last-wave tails.
+    python tools/streams_probe.py
+"""
 import sys, time
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __file__.rsplit('/tools/', 1)[0])
 import torch
 from paper_2510_07539_b200 import hsgn, workloads as W
 full = W.cfg3(members=4096)

@@ -188,6 +188,21 @@ def test_mass_conservation_gpu():
         assert abs(d["mass"] - m0) <= 1e-13 * m0
 
 
+def test_programmatic_dependent_launch_option(monkeypatch):
+    """HSGN_PDL=1 (griddepcontrol launches, off by default) advances bitwise like
+    the default launch mode."""
+    w = W.random_smooth(3000, 3, seed=13, amp=0.06, bathy=0.04)
+    a = gpu_solver(w)
+    monkeypatch.setenv("HSGN_PDL", "1")
+    b = gpu_solver(w)
+    a.run_steps(25)
+    b.run_steps(25)
+    (x, tx), (y, ty) = a.get_state(device=False), b.get_state(device=False)
+    for f, g in zip(x, y):
+        assert np.array_equal(f, g)
+    assert np.array_equal(tx, ty)
+
+
 @pytest.mark.parametrize("kmode", KMODES)
 def test_timed_graph_equals_run_steps(kmode):
     """hsgn_run_steps_timed (bench.py's timed region: the K steps as one graph with

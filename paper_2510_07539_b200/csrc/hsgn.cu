@@ -215,7 +215,8 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
     const size_t sm = BATHY ? SMEM_BYTES_B : SMEM_BYTES;    // one-CTA-per-tile kernels: b in smem
     if (c->picard > 0) {             // A24: one CTA per tile, Picard variant
         dim3 grid(c->tiles, c->members);
-        CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false, true>, grid, dim3(NT), sm, P, B));
+        CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false, true>, grid, dim3(NT),
+                               BATHY ? SMEM_BYTES_PIC_B : SMEM_BYTES_PIC, P, B));
     } else if (c->wb) {              // A25: one CTA per tile, face form
         dim3 grid(c->tiles, c->members);
         if (relax) CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, true, false, true>, grid, dim3(NT), sm, P, B));
@@ -879,12 +880,12 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_pkernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
-    cudaFuncSetAttribute(stage_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<true, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
-    cudaFuncSetAttribute(stage_kernel<false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_kernel<false, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
+    cudaFuncSetAttribute(stage_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC));
+    cudaFuncSetAttribute(stage_kernel<false, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC_B));
+    cudaFuncSetAttribute(stage_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC));
+    cudaFuncSetAttribute(stage_kernel<true, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC_B));
+    cudaFuncSetAttribute(stage_kernel<false, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC));
+    cudaFuncSetAttribute(stage_kernel<false, true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC_B));
     cudaFuncSetAttribute(sgn_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));
     cudaFuncSetAttribute(sgn_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SSMEM_BYTES));

@@ -68,6 +68,9 @@ constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
 // ninth array (the per-row global reads of b through the boundary map cost more
 // than the rest of the stage, `profiles/r01_ncu_summary.md`); < 48 KiB
 constexpr size_t SMEM_BYTES_B = SMEM_BYTES + size_t(SROWS) * sizeof(double);
+// Picard kernels (A24): alpha, a^2 of the own rows in two more arrays
+constexpr size_t SMEM_BYTES_PIC = SMEM_BYTES + size_t(2 * SROWS) * sizeof(double);
+constexpr size_t SMEM_BYTES_PIC_B = SMEM_BYTES_B + size_t(2 * SROWS) * sizeof(double);
 // fused step kernel: + a dedicated output staging buffer of 4 x T doubles
 // (T <= LCAP), so a tile's bulk store overlaps the next tile's compute
 __host__ __device__ constexpr size_t fused_smem_bytes(int T)
@@ -1011,7 +1014,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         for (int k = 0; k < MCH + 2; k++) { vb[k] = 0.0; vd[k] = 0.0; vH[k] = 0.0; vq[k] = 0.0; }
     }
     double hb[MCH];
-    double alv[MCH], a2v[MCH];           // PIC: alpha, a^2 at E of the own rows
+    // PIC: alpha, a^2 at E of the own rows, in two arrays after the tile's (shared
+    // memory rather than registers: the Picard kernels were spilling)
+    double *const sAl = smem + (BATHY ? 9 : 8) * SROWS;
 #pragma unroll 1
     for (int pic = 0; pic <= (PIC ? P.picard : 0); pic++) {
     if (PIC && pic > 0) {
@@ -1024,21 +1029,27 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             for (int i = 0; i < MCH; i++) {
                 const int r = r0 + i;
                 if (r >= L) continue;
+                double al, a2;
                 if (pic == 1) {
                     const double hE = sEh[r], hE2 = hE * hE;
                     const double b1E = 1.0 + lt2 / hE2;
                     const double b2E = 2.0 * lt2 / (b1E * b1E * hE2 * hE);
-                    alv[i] = vd[i + 1] * b1E;
-                    a2v[i] = vb[i + 1] - lam * alv[i] * b2E * vH[i + 1];
+                    al = vd[i + 1] * b1E;
+                    a2 = vb[i + 1] - lam * al * b2E * vH[i + 1];
+                    sAl[r] = al;
+                    sAl[SROWS + r] = a2;
+                } else {
+                    al = sAl[r];
+                    a2 = sAl[SROWS + r];
                 }
                 const double hn = hb[i], hn2 = hn * hn;
                 const double b1 = 1.0 + lt2 / hn2;
                 const double b2 = 2.0 * lt2 / (b1 * b1 * hn2 * hn);
-                const double be = a2v[i] + lam * alv[i] * b2 * vH[i + 1];
+                const double be = a2 + lam * al * b2 * vH[i + 1];
                 if (r >= G.klo && r < G.khi && !(be > 0.0)) acc.err |= ERR_COERC;
                 acc.bhi = max(acc.bhi, __double2hiint(be));
                 sBe[r] = be;
-                sDe[r] = alv[i] / b1;
+                sDe[r] = al / b1;
             }
         }
         __syncthreads();

@@ -405,9 +405,11 @@ def main():
         else:
             pin = [torch.from_numpy(np.ascontiguousarray(f.reshape(-1))).pin_memory() for f in (w.h, w.q, w.K, w.W)]
         outp = [torch.empty(Ntot, dtype=torch.float64).pin_memory() for _ in range(4)]
-        if slab:
-            # slab contexts (cfg5 over N GPUs) exchange halos every stage: no member
-            # chunks to pipeline; set_state + run_steps + get_state through pinned buffers
+        plain_e2e = slab or a.scheme == "sgn"
+        if plain_e2e:
+            # slab contexts (cfg5 over N GPUs) exchange halos every stage, and the SGN
+            # tile geometry depends on the whole state: no member chunks to pipeline;
+            # set_state + run_steps + get_state through pinned buffers
             import ctypes as C
             barrier()
             torch.cuda.synchronize()
@@ -432,8 +434,8 @@ def main():
         e2e = {"value": nst * Ntot * a.steps * world / te, "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / a.steps,
                "d2h_bytes_per_step": (state_bytes + 8 * w.members) / a.steps,
-               "what": ("Solver.set_state(pinned) + run_steps(K) + get_state(pinned) per slab; wall clock, max over ranks"
-                        if slab else
+               "what": ("Solver.set_state(pinned) + run_steps(K) + get_state(pinned); wall clock, max over ranks"
+                        if plain_e2e else
                         f"Solver.run_host (hsgn_run_host): pinned host state in, K steps, final state and "
                         f"times out, pipelined over {a.e2e_chunks} member chunks; wall clock, max over ranks")}
 

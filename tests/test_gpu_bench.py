@@ -39,6 +39,12 @@ def test_bench_line_has_the_contract_keys():
     assert "sm_mhz" in d["clocks"]
 
 
+@pytest.mark.parametrize("scheme", ["explicit", "sgn"])
+def test_bench_scheme_variants_run(scheme):
+    d = _run("--steps", "2", "--warmup", "3", "--members", "32", "--no-cpu", "--scheme", scheme)
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and 0 < d["roofline"]["frac"] < 1
+
+
 def test_reference_arm_line():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "1", "--cells", "256")
     assert d["impl"] == "reference" and d["value"] > 0

@@ -269,9 +269,18 @@ def main():
     from paper_2510_07539_b200 import hsgn
     from paper_2510_07539_b200 import workloads as W
 
+    local = local % max(torch.cuda.device_count(), 1)   # (several gloo ranks may share a GPU)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # HSGN_BENCH_BACKEND=gloo: host-side collectives only (exercises the
+        # multi-rank path with several ranks on one GPU; the ranks' kernels never
+        # wait on each other: the ensemble shards need no data-path exchange)
+        backend = os.environ.get("HSGN_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = "cuda" if (world == 1 or os.environ.get("HSGN_BENCH_BACKEND", "nccl") == "nccl") else "cpu"
 
     bathy = False
     slab = a.config == "cfg5" and world > 1
@@ -371,7 +380,7 @@ def main():
     elapsed = ev0.elapsed_time(ev1) if slab else ms_steps
     if slab:
         ms1 = ms2 = 0.5 * elapsed        # step-average model below
-    t = torch.tensor([elapsed, ms1, ms2], device="cuda", dtype=torch.float64)
+    t = torch.tensor([elapsed, ms1, ms2], device=coll_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed, ms1, ms2 = [float(x) for x in t.tolist()]
@@ -427,7 +436,7 @@ def main():
             te0 = time.perf_counter()
             _, tt = s.run_host(*pin, a.steps, out=outp, chunks=a.e2e_chunks)
             te = time.perf_counter() - te0
-        tt_ = torch.tensor([te], device="cuda", dtype=torch.float64)
+        tt_ = torch.tensor([te], device=coll_dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
         te = float(tt_.item())

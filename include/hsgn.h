@@ -295,6 +295,27 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
  * section 6).  Drops captured graphs.  Errors:
  * HSGN_E_INVALID (null context). */
 hsgn_status hsgn_set_persistent(hsgn_ctx *ctx, int32_t on);
+/* Cluster stage kernels (hsgn_cluster.cuh): the C CTAs
+ * of a member form one thread-block cluster and solve the depth system of
+ * P:509-512 EXACTLY across their tiles (partition method per thread chunk,
+ * interior PCR with two spike columns, one DSMEM exchange of 12 doubles per
+ * CTA, a C-unknown separator system solved redundantly per CTA; cyclic for
+ * periodic members) -- no overlap rows and no decay condition.  Eligible when
+ * the member fits: n_cells % 4 == 0, both sides periodic (C = the smallest
+ * power of two with n_cells <= 512 C) or both physical (wall / transmissive,
+ * C = ceil(n_cells / 512)), C <= 16, and the step is the SI stage without
+ * Picard passes, the A25 form, relaxation zones or slab sides.  mode 0: never
+ * (overlapped tiles with the decay check); 1: whenever eligible; 2 (default,
+ * "auto"): when eligible and the overlapped tiles cannot bound the decay a
+ * priori, i.e. material-CFL-only stepping (cfl_imex <= 0) without a
+ * user overlap -- the overlapped tiles are faster on B200 when CFL_IMEX bounds
+ * rho.  Drops captured graphs.  Errors: HSGN_E_INVALID
+ * (null context, mode outside 0..2). */
+hsgn_status hsgn_set_cluster(hsgn_ctx *ctx, int32_t mode);
+/* 1 if the next step runs on the cluster kernels (then *ctas = C and
+ * *tile_rows = rows per CTA, the last CTA n_cells - (C - 1) * tile_rows),
+ * 0 if not (both 0), -1 for a null context.  Either pointer may be NULL. */
+int32_t hsgn_get_cluster(const hsgn_ctx *ctx, int32_t *ctas, int32_t *tile_rows);
 /* Tile geometry chosen by hsgn_create: kept cells per tile, overlap, tiles per
  * member, threads per CTA, max rows per CTA. */
 hsgn_status hsgn_get_geometry(const hsgn_ctx *ctx, int32_t *tile_cells, int32_t *overlap,

@@ -21,8 +21,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "hsgn_oracle.c")
 _LIB = os.path.join(_HERE, "build", "libhsgn_oracle.so")
+_LIB_FMA = os.path.join(_HERE, "build", "libhsgn_oracle_fma.so")
 _lock = threading.Lock()
 _lib = None
+_libs = {}
 
 BC_PERIODIC, BC_WALL, BC_TRANSMISSIVE = 0, 1, 2
 OK, E_INVALID, E_DRY, E_COERCIVITY, E_SINGULAR, E_NONFINITE = 0, -1, -2, -3, -4, -5
@@ -67,11 +69,24 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
-def lib():
+def build_fma(force: bool = False) -> str:
+    """The SAME source compiled with FMA contraction (-ffp-contract=fast
+    -march=native): a second fp64 rounding of the identical algorithm.  Used
+    only to measure the rounding floor of the parity metric (reading A17):
+    oracle vs oracle-fma differences are what any two correct fp64
+    implementations may differ by."""
+    os.makedirs(os.path.dirname(_LIB_FMA), exist_ok=True)
+    if force or not os.path.exists(_LIB_FMA) or os.path.getmtime(_LIB_FMA) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-std=c11", "-O2", "-ffp-contract=fast", "-march=native",
+                               "-fno-fast-math", "-fPIC", "-shared", "-o", _LIB_FMA, _SRC, "-lm"])
+    return _LIB_FMA
+
+
+def lib(variant: str = "plain"):
     global _lib
     with _lock:
-        if _lib is None:
-            L = C.CDLL(build())
+        if variant not in _libs:
+            L = C.CDLL(build() if variant == "plain" else build_fma())
             dp = C.POINTER(C.c_double)
             P, T = C.POINTER(Problem), C.POINTER(Tableau)
             L.orc_celerity.restype = C.c_double
@@ -114,8 +129,10 @@ def lib():
                                       C.c_int64, dp, dp, dp, C.POINTER(C.c_int64)]
             L.orc_mass.restype = C.c_double
             L.orc_mass.argtypes = [C.c_int, C.c_double, dp]
-            _lib = L
-    return _lib
+            _libs[variant] = L
+            if variant == "plain":
+                _lib = L
+    return _libs[variant]
 
 
 def _p(a: np.ndarray):
@@ -151,10 +168,11 @@ class Oracle:
 
     def __init__(self, n, dx, g=9.81, lam=500.0, bc=("periodic", "periodic"), order=2,
                  h_min=1e-8, b=None, filter_sigma=0.0, filter_mask=0b1010, tableau=None,
-                 relax=None, picard=0, wb=False):
+                 relax=None, picard=0, wb=False, variant="plain"):
         """relax: dict(x_min, level, gen_x1, gen_rate, amp, omega, k, cp, sp_x0, sp_rate)
-        for the A10 wavemaker / sponge zones (cfg4)."""
-        self.L = lib()
+        for the A10 wavemaker / sponge zones (cfg4).  variant="fma": the same
+        oracle built with FMA contraction (rounding-floor measurements, A17)."""
+        self.L = lib(variant)
         codes = {"periodic": BC_PERIODIC, "wall": BC_WALL, "transmissive": BC_TRANSMISSIVE}
         self._b = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
         self.P = Problem(n=n, bc_left=codes[bc[0]], bc_right=codes[bc[1]], order=order,

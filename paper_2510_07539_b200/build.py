@@ -13,7 +13,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "hsgn.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", "hsgn_kernels.cuh"), os.path.join(ROOT, "include", "hsgn.h")]
+DEPS = SRC + [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))
+              if f.endswith((".cuh", ".cu", ".h"))] + [os.path.join(ROOT, "include", "hsgn.h")]
 LIB = os.path.join(PKG, "lib", "libhsgn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

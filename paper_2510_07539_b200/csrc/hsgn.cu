@@ -20,6 +20,7 @@
 
 #include "../../include/hsgn.h"
 #include "hsgn_kernels.cuh"
+#include "hsgn_cluster.cuh"
 
 using namespace hsgn;
 
@@ -97,6 +98,14 @@ struct hsgn_ctx {
     // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
     bool persist = false;
     int persist_grid = 0;
+    // cluster stage kernels (exact depth solve across the CTAs of a cluster,
+    // hsgn_cluster.cuh): C CTAs of clT rows per member; used whenever the
+    // member fits (n <= 16 * 512, n % 4 == 0) and the step is the SI stage
+    // without Picard passes, the A25 form, relaxation zones or slab sides
+    int cl_mode = 2;              // 0 off, 1 on (when the member fits), 2 auto: on when the
+                                  // overlapped tiles cannot bound the decay a priori
+                                  // (material-CFL-only stepping); HSGN_CLUSTER overrides
+    int clC = 0, clT = 0;
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
     std::string last_error;
@@ -242,6 +251,75 @@ hsgn_status launch_stage_b(hsgn_ctx *c, const Params &P, const Bufs &B)
     return c->bathy ? launch_stage<S2, FIN, true>(c, P, B) : launch_stage<S2, FIN, false>(c, P, B);
 }
 
+// Cluster path eligibility for the current settings (the geometry clC, clT
+// depends only on n and the boundary kinds and is fixed at hsgn_create).
+bool use_cluster(const hsgn_ctx *c)
+{
+    const bool on = c->cl_mode == 1 || (c->cl_mode == 2 && !(c->cfl > 0.0) && c->desc.overlap <= 0);
+    return on && c->clC > 0 && c->scheme == 0 && !c->slab && c->picard == 0 && !c->wb &&
+           !(c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0);
+}
+
+void choose_cluster(hsgn_ctx *c)
+{
+    c->clC = c->clT = 0;
+    const int bl = c->desc.bc_left, br = c->desc.bc_right;
+    const bool cyc = bl == HSGN_BC_PERIODIC && br == HSGN_BC_PERIODIC;
+    const bool phys = (bl == HSGN_BC_WALL || bl == HSGN_BC_TRANSMISSIVE) &&
+                      (br == HSGN_BC_WALL || br == HSGN_BC_TRANSMISSIVE);
+    const int n = c->n;
+    if ((!cyc && !phys) || (n % 4) != 0) return;
+    int C;
+    if (cyc) {                    // cyclic separator PCR: C a power of two
+        C = 1;
+        while (C * CT_MAX < n) C *= 2;
+    } else {
+        C = (n + CT_MAX - 1) / CT_MAX;
+    }
+    if (C > C_MAX) return;
+    const int T = (((n + C - 1) / C) + 3) / 4 * 4;
+    const int last = n - (C - 1) * T;
+    if (T < 8 || T > CT_MAX || last < 8) return;
+    c->clC = C;
+    c->clT = T;
+}
+
+template <bool S2, bool FIN, bool BATHY>
+hsgn_status launch_cl(hsgn_ctx *c, Params P, const Bufs &B)
+{
+    P.T = c->clT;
+    P.tiles = c->clC;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->clC, c->members);
+    cfg.blockDim = dim3(CNT);
+    cfg.dynamicSmemBytes = BATHY ? CSMEM_BYTES_B : CSMEM_BYTES;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(c->clC);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, cl_stage_kernel<S2, FIN, BATHY>, P, B));
+    c->launches++;
+    return HSGN_OK;
+}
+
+template <bool S2, bool FIN>
+hsgn_status launch_cl_b(hsgn_ctx *c, const Params &P, const Bufs &B)
+{
+    return c->bathy ? launch_cl<S2, FIN, true>(c, P, B) : launch_cl<S2, FIN, false>(c, P, B);
+}
+
+template <bool S2, bool FIN, bool BATHY>
+void cl_attrs()
+{
+    cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(BATHY ? CSMEM_BYTES_B : CSMEM_BYTES));
+}
+
 hsgn_status launch_dtc(hsgn_ctx *c, long long k, int commit_prev, int compute_dt)
 {
     const Params P = make_params(c, k);
@@ -328,6 +406,25 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
         if (ev) {
             CUDA_TRY(c, rec_ev(c, ev[1]));
             CUDA_TRY(c, rec_ev(c, ev[2]));
+        }
+    } else if (use_cluster(c)) {
+        if (c->tab.stages == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            st = launch_cl_b<false, true>(c, P, B);
+            if (st != HSGN_OK) return st;
+            if (ev) {
+                CUDA_TRY(c, rec_ev(c, ev[1]));
+                CUDA_TRY(c, rec_ev(c, ev[2]));
+            }
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            st = launch_cl_b<false, false>(c, P, B);
+            if (st != HSGN_OK) return st;
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            st = launch_cl_b<true, true>(c, P, B);
+            if (st != HSGN_OK) return st;
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
         }
     } else if (c->tab.stages == 1) {
         for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
@@ -706,6 +803,7 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         kc->fused_on = c->fused_on; kc->persist = c->persist;
         kc->scheme = c->scheme; kc->x_stages = c->x_stages;
         kc->picard = c->picard; kc->wb = c->wb; kc->pdl = c->pdl;
+        kc->cl_mode = c->cl_mode; kc->clC = c->clC; kc->clT = c->clT;
         kc->ws = c->ws;
         for (int bi = 0; bi < 3; bi++)
             for (int f = 0; f < 4; f++) kc->buf[bi][f] = c->buf[bi][f] + size_t(m0) * c->n;
@@ -901,7 +999,12 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cudaFuncSetAttribute(step_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cudaFuncSetAttribute(step_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
+    cl_attrs<false, false, false>(); cl_attrs<false, false, true>();
+    cl_attrs<true, true, false>(); cl_attrs<true, true, true>();
+    cl_attrs<false, true, false>(); cl_attrs<false, true, true>();
+    if (const char *e = std::getenv("HSGN_CLUSTER")) c->cl_mode = std::atoi(e);
     choose_geometry(c);
+    if (!slab) choose_cluster(c);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         delete c;
@@ -1454,6 +1557,23 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *c, int32_t on)
     return HSGN_OK;
 }
 
+hsgn_status hsgn_set_cluster(hsgn_ctx *c, int32_t mode)
+{
+    if (!c || mode < 0 || mode > 2) return HSGN_E_INVALID;
+    drop_graphs(c);
+    c->cl_mode = mode;
+    return HSGN_OK;
+}
+
+int32_t hsgn_get_cluster(const hsgn_ctx *c, int32_t *ctas, int32_t *tile_rows)
+{
+    if (!c) return -1;
+    const bool on = use_cluster(c);
+    if (ctas) *ctas = on ? c->clC : 0;
+    if (tile_rows) *tile_rows = on ? c->clT : 0;
+    return on ? 1 : 0;
+}
+
 hsgn_status hsgn_set_persistent(hsgn_ctx *c, int32_t on)
 {
     if (!c) return HSGN_E_INVALID;
@@ -1465,6 +1585,17 @@ hsgn_status hsgn_set_persistent(hsgn_ctx *c, int32_t on)
 #if HSGN_EXP_TIMING
 // timing experiments only (not part of the product ABI): per-stage sums of
 // CTA clocks [load wait, compute + store issue, epilogue + store drain, CTAs]
+int hsgn_cl_counters(unsigned long long *out, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_clt, sizeof(unsigned long long) * 32);
+    if (reset) {
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(g_clt, z, sizeof(z));
+    }
+    return 0;
+}
+
 int hsgn_exp_counters(unsigned long long *out, int reset)
 {
     cudaDeviceSynchronize();

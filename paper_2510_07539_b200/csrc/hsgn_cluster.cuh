@@ -1,0 +1,827 @@
+// hsgn_cluster.cuh -- sm_100a cluster stage kernel of the SI-IMEX hSGN step:
+// one IMEX stage S(E, R, tau) with the depth system of P:509-512
+// solved EXACTLY across the CTAs of a thread-block cluster (no overlap rows,
+// no decay check).  Citations: P:n = PAPER.md line n, Ak = DESIGN.md reading k.
+//
+// Work split.  A member (one periodic or walled 1-D domain of n cells) is
+// cut into C contiguous tiles of T rows (the last one n - (C-1) T), one CTA
+// each; the C CTAs of a member form one cluster (C <= 16).  Within a CTA every
+// thread owns a chunk of CMCH = 4 consecutive rows.
+//
+// Exact solve (SPIKE inside the cluster).  The depth matrix is tridiagonal
+// (cyclic for periodic members).  Each chunk is reduced to its last row (the
+// partition method: downward + upward sweeps in registers), giving a
+// tridiagonal system in the chunk-end unknowns X_k.  The last chunk end of CTA
+// j is its SEPARATOR L_j (row T_j - 1).  Between two separators lie only rows
+// of one CTA, so each CTA solves its interior chunk ends X_0 .. X_{ks-1} by PCR
+// in shared memory with three right-hand sides:
+//     X_k = Y_k - V_k L_{j-1} - W_k L_j
+// (V, W: responses to the couplings of its first and last interior rows to the
+// two separators).  Every CTA then pushes 12 numbers into the shared memory of
+// every CTA of the cluster (DSMEM, st.shared::cluster): the raw reduced row of
+// its separator chunk, (Y, V, W) at its last interior slot, and the first-row
+// relation and (Y, V, W) of its chunk 0 (what the separator row of the
+// previous CTA needs).  After one cluster barrier each CTA forms the C
+// separator equations
+//     -a V' L_{j-1} + (B - a W' + c R1 V0) L_j + c R1 W0 L_{j+1}
+//        = d - c P1 - a Y' + c R1 Y0
+// and solves them redundantly by PCR over C lanes of one warp (cyclic for
+// periodic members, indices mod C).  X_k and every row then follow exactly.
+// The result is the unique solution of the full system (to round-off); PCR
+// stops early only once the reduced couplings are below 2^-64 (then the rows
+// are decoupled to round-off).
+//
+// Shared-memory layout.  Phases 1-3 are chunk-parallel (thread t reads rows
+// 4t-2 .. 4t+5); a plain row layout would put the 32 threads of a warp on 4
+// bank pairs.  Row arrays are therefore stored chunk-major with an XOR swizzle,
+//     row r (r in [-4, 4 CNT + 4)):  j = r + 4,  i = j & 3,  c = j >> 2,
+//     index = i * CCAP + (c ^ (i << 3)),
+// which is conflict-free (2 wavefronts per warp access, the minimum for 8-B
+// words) both chunk-parallel (fixed i, consecutive c) and row-parallel
+// (consecutive r).  TMA lands the tile in plain row order; one row-parallel
+// pass (which also forms E and R of stage 2) rewrites it swizzled
+// in place, through registers.
+//
+// Phases (CNT = 128 threads, rows -4 .. T+3 of the tile in shared memory):
+//   load    : TMA bulk copies of U^n (and U1, b) rows -4 .. T+3 (periodic wrap
+//             by extra segments; physical ends mirrored in the next pass)
+//   pass    : E, R (stage 2), H = K - 1.5 h b, wall parity, swizzle
+//   phase 1 : MUSCL + Rusanov faces, predictor, coefficients (rows -1 .. T)
+//   phase 2 : assembly, partition sweeps, interior PCR (Y, V, W), DSMEM
+//             exchange, separator PCR, recovery -> hbar (rows -1 .. T)
+//   phase 3 : back-substitution; final stage: A19 filter with a +-2 row DSMEM
+//             halo exchange, dt maxima; staged TMA bulk store
+#pragma once
+#include "hsgn_kernels.cuh"
+
+#ifndef HSGN_CMINB
+#define HSGN_CMINB 4
+#endif
+
+namespace hsgn {
+
+constexpr int CNT = 128;                 // threads per CTA (= chunks)
+constexpr int CMCH = 4;                  // rows per chunk
+constexpr int CT_MAX = CNT * CMCH;       // 512 rows per CTA
+constexpr int CCAP = CNT + 32;           // swizzled capacity in chunks (rows -4 .. T+3; XOR < CCAP)
+constexpr int CARR = 4 * CCAP;           // doubles per row array (640)
+constexpr int C_MAX = 16;                // CTAs per cluster (16: non-portable size)
+constexpr int CNARR = 8;
+constexpr size_t CSMEM_BYTES = size_t(CNARR) * CARR * sizeof(double);        // 40 KiB
+constexpr size_t CSMEM_BYTES_B = size_t(CNARR + 1) * CARR * sizeof(double);  // + b (45 KiB)
+constexpr int XPUB = 12;                 // doubles each CTA publishes to the cluster
+
+__shared__ double s_cx[C_MAX][XPUB];     // separator data of every CTA of the cluster
+__shared__ double s_cw[NT / 32][3];      // chunk-relation exchange across warps
+
+__device__ __forceinline__ int swz(int r)
+{
+    const int j = r + 4, i = j & 3;
+    return i * CCAP + ((j >> 2) ^ (i << 3));
+}
+
+// Cluster barrier, used once: every CTA arrives (relaxed: no memory ordering,
+// only "started, mbarriers initialised" -- fence.mbarrier_init orders those)
+// right after its start and waits just before its first remote store.
+__device__ __forceinline__ void cl_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory"); }
+
+// shared::cluster address of `p` (a shared variable of this CTA) in CTA `rank`
+__device__ __forceinline__ unsigned cl_map(const void *p, unsigned rank)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+
+// Remote store of one double into CTA `rank`'s shared memory at the address
+// of `dst` there, completing 8 transaction bytes on that CTA's mbarrier `mbar`
+// (st.async: the receiver waits on its own mbarrier, no cluster barrier).
+__device__ __forceinline__ void st_remote(const void *dst, const void *mbar, unsigned rank, double v)
+{
+    const unsigned a = cl_map(dst, rank), b = cl_map(mbar, rank);
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n"
+                 ::"r"(a), "l"((unsigned long long)__double_as_longlong(v)), "r"(b) : "memory");
+}
+
+__shared__ __align__(8) unsigned long long s_xmb;   // separator data received (12 C doubles)
+__shared__ __align__(8) unsigned long long s_fmb;   // filter halo rows received
+
+// Predictor (A9) and coefficients at E (A2) of one row r
+// of the swizzled tile; same arithmetic as row_update (hsgn_kernels.cuh).
+// R = (h, q, H, W) of the row (stage 1: R = E) is read from the row's slot of
+// (sDe, sQd, sHd, sBe), which then take delta, q^dag, H^dag, beta.
+template <bool BATHY>
+__device__ __forceinline__ void cl_row_update(const RowCtx &C, const double *sB, int r,
+                                              const double (&ch)[3], const double (&cq)[3],
+                                              const double (&cH)[3], const double (&cW)[3],
+                                              const Face &Fl, const Face &Fr, double *sQd, double *sHd,
+                                              double *sBe, double *sDe, double &Wd_out, double &beta_out,
+                                              double &hR_out)
+{
+    const int x = swz(r);
+    const double hR = sDe[x], qR = sQd[x], HR = sHd[x], WR = sBe[x];      // R of the row
+    const double hE = ch[1], qE = cq[1], HE = cH[1];
+    const double s2 = hE * hE, den = s2 + C.lt2;
+    const double Z = rcp(hE * den);
+    const double ihE = den * Z, D = hE * Z;
+    const double sg = HE * (ihE * ihE);                              // eta/h
+    double Dxb = 0.0, hRp = hR, ptil_term = 0.0;
+    if (BATHY) {
+        const double bm = sB[swz(r - 1)], b0 = sB[x], bp = sB[swz(r + 1)];
+        Dxb = (bp - bm) * (0.5 * C.idx);
+        const double Gr = C.g * (hE + ch[2]) * 0.5, Gl = C.g * (ch[0] + hE) * 0.5;
+        hRp = hR + C.t2 * (Gr * (bp - b0) - Gl * (b0 - bm));          // zeta-form (A9)
+        ptil_term = 1.5 * C.tau * C.lam3 * (1.0 - sg) * Dxb;          // p~
+    }
+    const double Wd = WR - C.tdx2 * (Fr.W - Fl.W) + C.ltau;
+    const double Hd = HR - C.tdx2 * (Fr.H - Fl.H) - 1.5 * C.tau * qE * Dxb + C.tau * Wd;
+    const double qd = qR - C.tdx2 * (Fr.q - Fl.q) - ptil_term;
+    const double t = 2.0 * sg - 1.0;
+    const double a2 = fma(C.lam3 * sg, 3.0 * sg - 1.0, C.g * hE);
+    const double beta = fma(-C.c23 * t, (D * D) * Hd, a2);
+    const double delta = (t * (-1.0 / 3.0)) * (hE * D);
+    sQd[x] = qd; sHd[x] = Hd; sBe[x] = beta; sDe[x] = delta;
+    hR_out = hRp;
+    Wd_out = Wd;
+    beta_out = beta;
+}
+
+// Phase 1 of one isolated row r (rows -1 and T of the tile): faces r -+ 1/2
+// from E rows r-2 .. r+2.
+template <bool BATHY>
+__device__ __forceinline__ void cl_single_row(const RowCtx &C, double kap, const double *sB, int r,
+                                              const double *sEh, const double *sEq, const double *sEH,
+                                              const double *sEW, double *sQd, double *sHd, double *sBe,
+                                              double *sDe)
+{
+    double xh[5], xq[5], xH[5], xW[5];
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        const int x = swz(r - 2 + k);
+        xh[k] = sEh[x]; xq[k] = sEq[x]; xH[k] = sEH[x]; xW[k] = sEW[x];
+    }
+    const double ah[3] = {xh[0], xh[1], xh[2]}, aq[3] = {xq[0], xq[1], xq[2]};
+    const double aH[3] = {xH[0], xH[1], xH[2]}, aW[3] = {xW[0], xW[1], xW[2]};
+    const double bh[3] = {xh[1], xh[2], xh[3]}, bq[3] = {xq[1], xq[2], xq[3]};
+    const double bH[3] = {xH[1], xH[2], xH[3]}, bW[3] = {xW[1], xW[2], xW[3]};
+    const double ch[3] = {xh[2], xh[3], xh[4]}, cq[3] = {xq[2], xq[3], xq[4]};
+    const double cH[3] = {xH[2], xH[3], xH[4]}, cW[3] = {xW[2], xW[3], xW[4]};
+    const FState Mm = muscl_minus(ah, aq, aH, aW, kap);       // M_{r-1}
+    FState Pl, Mr;
+    muscl_pair(bh, bq, bH, bW, kap, Pl, Mr);                  // Pl_r, M_r
+    const FState Pn = muscl_plus(ch, cq, cH, cW, kap);        // Pl_{r+1}
+    const Face Fl = rusanov(Mm, Pl), Fr = rusanov(Mr, Pn);
+    double Wd, hR, beta;
+    cl_row_update<BATHY>(C, sB, r, bh, bq, bH, bW, Fl, Fr, sQd, sHd, sBe, sDe, Wd, beta, hR);
+}
+
+#if HSGN_EXP_TIMING
+// per-phase clocks of the cluster kernels, summed over CTAs: [stage][mark]
+__device__ unsigned long long g_clt[2][16];
+#define CL_MARK(k) do { if (tid == 0) tmk[k] = clock64(); } while (0)
+#else
+#define CL_MARK(k) do { } while (0)
+#endif
+
+// PCR buffers (phase 2, in the dead E arrays 1..3): 2 buffers x 5 columns (A, C, D, V, W) of CNT slots
+// with PPAD zero slots on either side, so levels of stride <= PPAD need no
+// bounds tests (the pads are identity rows: no coupling, zero right-hand side).
+constexpr int PPAD = 16;
+constexpr int PSTR = CNT + 2 * PPAD;
+static_assert(2 * 5 * PSTR <= 3 * CARR, "PCR buffers fit in arrays 1..3");
+
+// ---------------------------------------------------------------------------
+// The cluster stage kernel.  grid = (C, members), cluster = (C, 1, 1).
+// STAGE2: inputs U^n and U1 (E, R formed on load); FINAL: this stage produces
+// U^{n+1} (filter, dt maxima, time level).  P.T = tile rows (a multiple of
+// 4), P.tiles = C; periodic members (both sides periodic) or physical ends
+// on both sides.
+// ---------------------------------------------------------------------------
+template <bool STAGE2, bool FINAL, bool BATHY>
+__global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params P, const Bufs B)
+{
+    double *const sm = hsgn_smem;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#if HSGN_EXP_TIMING
+    long long tmk[12] = {};
+#endif
+    CL_MARK(0);
+    const int C = P.tiles;
+    const int c = blockIdx.x;                       // == %cluster_ctarank (cluster spans x)
+    const int m = blockIdx.y;
+    const int n = P.n;
+    const size_t mo = size_t(m) * n;
+    const int s = c * P.T;
+    const int Tc = (c == C - 1) ? n - s : P.T;
+    const bool cyc = P.bcl == BC_PERIODIC;
+    const bool left_phys = !cyc && c == 0, right_phys = !cyc && c == C - 1;
+    const unsigned xmb = (unsigned)__cvta_generic_to_shared(&s_xmb);
+    const unsigned fmb = (unsigned)__cvta_generic_to_shared(&s_fmb);
+    double *const A0 = sm, *const A1 = sm + CARR, *const A2 = sm + 2 * CARR, *const A3 = sm + 3 * CARR;
+    double *const A4 = sm + 4 * CARR, *const A5 = sm + 5 * CARR, *const A6 = sm + 6 * CARR;
+    double *const A7 = sm + 7 * CARR, *const A8 = sm + 8 * CARR;
+    const int ks = Tc / CMCH - 1;                     // separator chunk (last row = Tc - 1)
+    const bool filt = FINAL && (P.filter_sigma > 0.0);
+    // run control first: its latency overlaps the barrier and the tile load
+    const double dtm = P.dt[m];
+    const double lam = P.lam[m];
+    double tm0 = -1.0, tend0 = -1.0;
+    if (FINAL && c == 0 && tid == 0) { tm0 = P.t[P.kpar * P.members + m]; tend0 = P.ctrl->t_end; }
+
+    // ---- load.  Thread t owns rows 4t .. 4t+3 (contiguous: two 16-B loads per
+    // field, a warp reads 1 KiB contiguous).  E goes to shared memory
+    // (swizzled; neighbours' rows are read in phase 1), R stays in registers
+    // (only its own rows are used).  Rows -4..-1 and Tc..Tc+3 (halo) come from
+    // the neighbouring tiles (periodic: wrapped) by threads 64, 65 (left) and
+    // 96, 97 (right), two rows each, or are mirrored at physical ends (A10);
+    // R of rows -1 and Tc goes to s_rh for the threads computing those rows.
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xmb) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fmb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        // separator data: XPUB doubles from each of the C CTAs (incl. this one)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xmb),
+                     "r"(unsigned(XPUB * C) * 8u) : "memory");
+        // filter halo: rows Tc, Tc+1 (q, W) from the right neighbour, -2, -1 from the left
+        const unsigned fbytes = filt ? (left_phys ? 0u : 32u) + (right_phys ? 0u : 32u) : 0u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fmb), "r"(fbytes) : "memory");
+    }
+    const bool wall_l = P.bcl == BC_WALL, wall_r = P.bcr == BC_WALL;
+    const int r0 = tid * CMCH;
+    const bool live = r0 < Tc;
+    {
+        const double wE = P.wE, wR = P.wR;
+        // rows [r, r+1] of every field at global cell gc (member offset applied);
+        // E and R of the two rows (stage 1: R = E); H = K - 1.5 h b (A9)
+        auto load2 = [&](size_t gc, double (&e)[4][2], double (&rr)[4][2], double (&bb)[2]) {
+            double2 u[4], v[4];
+#pragma unroll
+            for (int f = 0; f < 4; f++) u[f] = __ldg(reinterpret_cast<const double2 *>(B.Un[f] + gc));
+            if (STAGE2) {
+#pragma unroll
+                for (int f = 0; f < 4; f++) v[f] = __ldg(reinterpret_cast<const double2 *>(B.U1[f] + gc));
+            }
+            if (BATHY) {
+                const double2 b2 = __ldg(reinterpret_cast<const double2 *>(P.b + (gc - mo)));
+                bb[0] = b2.x; bb[1] = b2.y;
+            } else {
+                bb[0] = bb[1] = 0.0;
+            }
+#pragma unroll
+            for (int f = 0; f < 4; f++) {
+                const double x0 = u[f].x, x1 = u[f].y;
+                if (STAGE2) {     // (1 - w) U^n + w U1 = U^n + w (U1 - U^n)
+                    const double d0 = v[f].x - x0, d1 = v[f].y - x1;
+                    e[f][0] = fma(wE, d0, x0); e[f][1] = fma(wE, d1, x1);
+                    rr[f][0] = fma(wR, d0, x0); rr[f][1] = fma(wR, d1, x1);
+                } else {
+                    e[f][0] = x0; e[f][1] = x1;
+                    rr[f][0] = x0; rr[f][1] = x1;
+                }
+            }
+            if (BATHY) {
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    e[2][k] -= 1.5 * e[0][k] * bb[k];
+                    rr[2][k] -= 1.5 * rr[0][k] * bb[k];
+                }
+            }
+        };
+        auto putE = [&](int r, double h, double q, double H, double W, double b) {
+            const int x = swz(r);
+            A0[x] = h; A1[x] = q; A2[x] = H; A3[x] = W;
+            if (BATHY) A8[x] = b;
+        };
+        auto putR = [&](int r, double h, double q, double H, double W) {   // read back by the row's owner
+            const int x = swz(r);
+            A7[x] = h; A4[x] = q; A5[x] = H; A6[x] = W;
+        };
+        if (live) {
+            double e0[4][2], e1[4][2], q0[4][2], q1[4][2], b0[2], b1[2];
+            load2(mo + size_t(s + r0), e0, q0, b0);
+            load2(mo + size_t(s + r0 + 2), e1, q1, b1);
+            putR(r0, q0[0][0], q0[1][0], q0[2][0], q0[3][0]);
+            putR(r0 + 1, q0[0][1], q0[1][1], q0[2][1], q0[3][1]);
+            putR(r0 + 2, q1[0][0], q1[1][0], q1[2][0], q1[3][0]);
+            putR(r0 + 3, q1[0][1], q1[1][1], q1[2][1], q1[3][1]);
+            putE(r0, e0[0][0], e0[1][0], e0[2][0], e0[3][0], b0[0]);
+            putE(r0 + 1, e0[0][1], e0[1][1], e0[2][1], e0[3][1], b0[1]);
+            putE(r0 + 2, e1[0][0], e1[1][0], e1[2][0], e1[3][0], b1[0]);
+            putE(r0 + 3, e1[0][1], e1[1][1], e1[2][1], e1[3][1], b1[1]);
+            // physical ends: mirrored ghosts (A10; q odd at walls, copy for transmissive)
+            if (tid == 0 && left_phys) {
+                const double pq = wall_l ? -1.0 : 1.0;
+                double ef[4][4], bf[4];
+#pragma unroll
+                for (int f = 0; f < 4; f++) { ef[f][0] = e0[f][0]; ef[f][1] = e0[f][1]; ef[f][2] = e1[f][0]; ef[f][3] = e1[f][1]; }
+                bf[0] = b0[0]; bf[1] = b0[1]; bf[2] = b1[0]; bf[3] = b1[1];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {           // row -1-k <- row k (wall) or row 0
+                    const int src = wall_l ? k : 0;
+                    putE(-1 - k, ef[0][src], pq * ef[1][src], ef[2][src], ef[3][src], bf[src]);
+                }
+            }
+            if (tid == ks && right_phys) {
+                const double pq = wall_r ? -1.0 : 1.0;
+                double ef[4][4], bf[4];
+#pragma unroll
+                for (int f = 0; f < 4; f++) { ef[f][0] = e0[f][0]; ef[f][1] = e0[f][1]; ef[f][2] = e1[f][0]; ef[f][3] = e1[f][1]; }
+                bf[0] = b0[0]; bf[1] = b0[1]; bf[2] = b1[0]; bf[3] = b1[1];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {           // row Tc+k <- row Tc-1-k (wall) or Tc-1
+                    const int src = wall_r ? 3 - k : 3;
+                    putE(Tc + k, ef[0][src], pq * ef[1][src], ef[2][src], ef[3][src], bf[src]);
+                }
+            }
+        }
+        // halo rows of interior or periodic tile ends
+        const int hs = (tid == 64 || tid == 65) ? 0 : (tid == 96 || tid == 97) ? 1 : -1;
+        if (hs == 0 && !left_phys) {
+            const int rr0 = (tid == 64) ? -4 : -2;                    // rows rr0, rr0+1
+            const int gc = (s + rr0 >= 0) ? s + rr0 : n + s + rr0;    // (periodic wrap: c == 0)
+            double e[4][2], q[4][2], bb[2];
+            load2(mo + size_t(gc), e, q, bb);
+            putE(rr0, e[0][0], e[1][0], e[2][0], e[3][0], bb[0]);
+            putE(rr0 + 1, e[0][1], e[1][1], e[2][1], e[3][1], bb[1]);
+            if (tid == 65) putR(-1, q[0][1], q[1][1], q[2][1], q[3][1]);
+        }
+        if (hs == 1 && !right_phys) {
+            const int rr0 = (tid == 96) ? Tc : Tc + 2;
+            const int gc = (s + rr0 < n) ? s + rr0 : s + rr0 - n;
+            double e[4][2], q[4][2], bb[2];
+            load2(mo + size_t(gc), e, q, bb);
+            putE(rr0, e[0][0], e[1][0], e[2][0], e[3][0], bb[0]);
+            putE(rr0 + 1, e[0][1], e[1][1], e[2][1], e[3][1], bb[1]);
+            if (tid == 96) putR(Tc, q[0][0], q[1][0], q[2][0], q[3][0]);
+        }
+    }
+    __syncthreads();                                  // E rows, s_rh; mbarriers initialised
+    cl_arrive_relaxed();                              // cluster phase: every CTA has started
+    CL_MARK(1);
+    CL_MARK(2);
+    CL_MARK(3);
+
+    TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
+    if (dtm == 0.0) {                                 // member at t_end: uniform over the cluster
+        carry_tile<FINAL, BATHY>(P, B, mo, s, s + Tc, lam, acc);
+        __syncwarp();
+        cl_wait();
+        tile_epilogue<FINAL>(P, c, m, dtm, acc, tm0, tend0);
+        return;
+    }
+    const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
+    const double tau = S.tau, g = S.g, idx1 = S.idx1, tdx2 = S.tdx2, t2h = S.t2h, lt2 = S.lt2;
+    const double lt2h = S.lt2h, ltdx2 = S.ltdx2, lam3 = S.lam3, ltau = S.ltau;
+    const double *const sEh = A0, *const sEq = A1, *const sEH = A2, *const sEW = A3;
+    double *const sQd = A4, *const sHd = A5, *const sBe = A6, *const sDe = A7;
+    const double *const sB = BATHY ? A8 : nullptr;
+
+    // ---- phase 1: faces, predictor, coefficients ---------------------------
+    double wd[CMCH], hRv[CMCH];
+    {
+        const double kap = P.order == 2 ? 0.25 : 0.0;
+        RowCtx Cx{};
+        Cx.tau = tau; Cx.tdx2 = tdx2; Cx.t2 = S.t2; Cx.lt2 = lt2; Cx.lam = lam; Cx.lam3 = lam3;
+        Cx.ltau = ltau; Cx.g = g; Cx.idx = idx1;
+        Cx.c23 = (2.0 / 3.0) * lam * lt2;
+        if (tid == 0 && !left_phys)                   // row -1 (previous CTA's last row)
+            cl_single_row<BATHY>(Cx, kap, sB, -1, sEh, sEq, sEH, sEW, sQd, sHd, sBe, sDe);
+        if (tid == 32 && !right_phys)                 // row Tc (next CTA's first row)
+            cl_single_row<BATHY>(Cx, kap, sB, Tc, sEh, sEq, sEH, sEW, sQd, sHd, sBe, sDe);
+        if (live) {
+            double wh[3], wq[3], wH[3], wW[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++) {             // rows r0-2 .. r0
+                const int x = swz(r0 - 2 + k);
+                wh[k] = sEh[x]; wq[k] = sEq[x]; wH[k] = sEH[x]; wW[k] = sEW[x];
+            }
+            FState Mm = muscl_minus(wh, wq, wH, wW, kap);          // M_{r0-1}
+#pragma unroll
+            for (int k = 0; k < 2; k++) { wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1]; }
+            {
+                const int x = swz(r0 + 1);
+                wh[2] = sEh[x]; wq[2] = sEq[x]; wH[2] = sEH[x]; wW[2] = sEW[x];
+            }
+            FState Pn, Mr;
+            muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);               // Pl_{r0}, M_{r0}
+            Face Fl = rusanov(Mm, Pn);                             // face r0 - 1/2
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) {
+                const int r = r0 + i;
+                double ch[3], cq[3], cH[3], cW[3];
+#pragma unroll
+                for (int k = 0; k < 3; k++) { ch[k] = wh[k]; cq[k] = wq[k]; cH[k] = wH[k]; cW[k] = wW[k]; }
+#pragma unroll
+                for (int k = 0; k < 2; k++) { wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1]; }
+                {
+                    const int x = swz(r + 2);
+                    wh[2] = sEh[x]; wq[2] = sEq[x]; wH[2] = sEH[x]; wW[2] = sEW[x];
+                }
+                FState Mn;
+                muscl_pair(wh, wq, wH, wW, kap, Pn, Mn);           // Pl_{r+1}, M_{r+1}
+                const Face Fr = rusanov(Mr, Pn);                   // face r + 1/2
+                Mr = Mn;
+                double beta;
+                cl_row_update<BATHY>(Cx, sB, r, ch, cq, cH, cW, Fl, Fr, sQd, sHd, sBe, sDe, wd[i], beta, hRv[i]);
+                if (!(beta > 0.0)) acc.err |= ERR_COERC;           // kappa > 0
+                acc.bhi = max(acc.bhi, __double2hiint(beta));
+                Fl = Fr;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) { wd[i] = 0.0; hRv[i] = 0.0; }
+        }
+    }
+    __syncthreads();
+    // physical ends (A10): derived-field ghosts mirrored, the depth coupling
+    // across the end cut (beta_{-1} = -beta_0 makes rho_{-1/2} exactly 0)
+    if (tid == 0 && left_phys) {
+        const int x = swz(-1), y = swz(0);
+        sQd[x] = (wall_l ? -1.0 : 1.0) * sQd[y]; sHd[x] = sHd[y]; sDe[x] = sDe[y]; sBe[x] = -sBe[y];
+    }
+    if (tid == 32 && right_phys) {
+        const int x = swz(Tc), y = swz(Tc - 1);
+        sQd[x] = (wall_r ? -1.0 : 1.0) * sQd[y]; sHd[x] = sHd[y]; sDe[x] = sDe[y]; sBe[x] = -sBe[y];
+    }
+    __syncthreads();
+    CL_MARK(4);
+
+    // ---- phase 2: assemble + exact solve (A1, A3) ---------------
+    // register windows of the derived fields over rows r0-1 .. r0+4 (arrays
+    // 4..7 stay intact: phase 3 reads them again; the PCR buffers go to the
+    // dead E arrays 1..3)
+    double hb[CMCH], hLn, hRn;
+    double am[CMCH], cm[CMCH], dm[CMCH];
+    {
+    double vb[CMCH + 2], vd[CMCH + 2], vH[CMCH + 2], vq[CMCH + 2];
+    if (live) {
+#pragma unroll
+        for (int k = 0; k < CMCH + 2; k++) {
+            const int x = swz(r0 - 1 + k);
+            vb[k] = sBe[x]; vd[k] = sDe[x]; vH[k] = sHd[x]; vq[k] = sQd[x];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < CMCH + 2; k++) { vb[k] = 0.0; vd[k] = 0.0; vH[k] = 0.0; vq[k] = 0.0; }
+    }
+#pragma unroll
+        for (int i = 0; i < CMCH; i++) {
+            const double rl = t2h * (vb[i] + vb[i + 1]);              // rho_{r-1/2}
+            const double rr = t2h * (vb[i + 1] + vb[i + 2]);          // rho_{r+1/2}
+            const double ml = lt2h * (vd[i] + vd[i + 1]);             // mu (A1)
+            const double mr = lt2h * (vd[i + 1] + vd[i + 2]);
+            const double rhs = hRv[i] - tdx2 * (vq[i + 2] - vq[i]) + mr * (vH[i + 2] - vH[i + 1])
+                               - ml * (vH[i + 1] - vH[i]);
+            const double a = -rl, cc = -rr, dg = 1.0 + rl + rr;
+            if (i == 0) {
+                const double inv = rcp(dg);
+                am[0] = a * inv; cm[0] = cc * inv; dm[0] = rhs * inv;
+            } else {
+                const double inv = rcp(dg - a * cm[i - 1]);
+                am[i] = -a * am[i - 1] * inv;
+                cm[i] = cc * inv;
+                dm[i] = (rhs - a * dm[i - 1]) * inv;
+            }
+        }
+    }
+    {
+        // chunk-end relation: X_k + aE X_{k-1} + cE x_{next first} = dE;
+        // upward: x_i = P_i - Q_i X_{k-1} - R_i X_k (stored in dm, am, cm)
+        const double aE = am[CMCH - 1], cE = cm[CMCH - 1], dE = dm[CMCH - 1];
+        {
+            double Pn = 0.0, Qn = 0.0, Rn = -1.0;
+#pragma unroll
+            for (int i = CMCH - 2; i >= 0; i--) {
+                const double Pi = dm[i] - cm[i] * Pn;
+                const double Qi = am[i] - cm[i] * Qn;
+                const double Ri = -cm[i] * Rn;
+                dm[i] = Pi; am[i] = Qi; cm[i] = Ri;
+                Pn = Pi; Qn = Qi; Rn = Ri;
+            }
+        }
+        double P1 = __shfl_down_sync(0xffffffffu, dm[0], 1);
+        double Q1 = __shfl_down_sync(0xffffffffu, am[0], 1);
+        double R1 = __shfl_down_sync(0xffffffffu, cm[0], 1);
+        if (lane == 0) { s_cw[wid][0] = dm[0]; s_cw[wid][1] = am[0]; s_cw[wid][2] = cm[0]; }
+        __syncthreads();                              // (also: all window loads of arrays 4..7 done)
+        if (lane == 31) {
+            if (wid + 1 < CNT / 32) { P1 = s_cw[wid + 1][0]; Q1 = s_cw[wid + 1][1]; R1 = s_cw[wid + 1][2]; }
+            else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
+        }
+        // reduced row of chunk end k: A X_{k-1} + X_k + C X_{k+1} = D (normalised)
+        double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1, V_ = 0.0, W_ = 0.0;
+        {
+            const double ib = rcp(1.0 - cE * Q1);
+            A_ *= ib; C_ *= ib; D_ *= ib;
+        }
+        if (tid == 0) { V_ = A_; A_ = 0.0; }          // coupling to L_{j-1}: right-hand side V
+        if (tid == ks - 1) { W_ = C_; C_ = 0.0; }     // coupling to L_j: right-hand side W
+        if (tid >= ks) { A_ = 0.0; C_ = 0.0; D_ = 0.0; V_ = 0.0; W_ = 0.0; }   // separator, dead
+        double *const pb0 = A1 + PPAD, *const pb1 = A1 + 5 * PSTR + PPAD;       // slot k at [k]
+        auto put = [&](double *b, int k, double a, double cc, double d, double v, double w_) {
+            b[k] = a; b[PSTR + k] = cc; b[2 * PSTR + k] = d; b[3 * PSTR + k] = v; b[4 * PSTR + k] = w_;
+        };
+        put(pb0, tid, A_, C_, D_, V_, W_);
+        if (tid < 2 * PPAD) {                         // zero pads (identity rows) of both buffers
+            const int k = tid < PPAD ? tid - PPAD : CNT + tid - PPAD;
+            put(pb0, k, 0.0, 0.0, 0.0, 0.0, 0.0);
+            put(pb1, k, 0.0, 0.0, 0.0, 0.0, 0.0);
+        }
+        {
+            const float ea = float(fabs(A_)), ec = float(fabs(C_));
+            const float ev = warp_max_nonneg(ea > ec ? ea : ec);
+            if (lane == 0) s_redf[wid] = ev;
+        }
+        __syncthreads();
+        int lim = CNT;
+        {
+            float e0 = 0.0f;
+#pragma unroll
+            for (int q = 0; q < CNT / 32; q++) e0 = fmaxf(e0, s_redf[q]);
+            if (e0 < 0.4f) {     // PCR stop once e^(2^s) <= 2^-64 (see stage_body)
+                const float q = __fdividef(64.0f, -__log2f(e0) - 0.28f);
+                const int qi = int(ceilf(q));
+                lim = qi <= 1 ? 1 : min(CNT, 1 << (32 - __clz(qi - 1)));
+            }
+        }
+        // one PCR level at stride sd, cur -> nxt (pads: no bounds tests for sd <= PPAD)
+        auto level = [&](const int sd, const double *cur, double *nxt) {
+            int km = tid - sd, kp = tid + sd;
+            const bool okm = sd <= PPAD || km >= 0, okp = sd <= PPAD || kp < CNT;
+            km = okm ? km : 0; kp = okp ? kp : 0;
+            double Am = cur[km], Cm = cur[PSTR + km], Dm = cur[2 * PSTR + km];
+            double Vm = cur[3 * PSTR + km], Wm = cur[4 * PSTR + km];
+            double Ap = cur[kp], Cp = cur[PSTR + kp], Dp = cur[2 * PSTR + kp];
+            double Vp = cur[3 * PSTR + kp], Wp = cur[4 * PSTR + kp];
+            if (sd > PPAD) {
+                if (!okm) { Am = Cm = Dm = Vm = Wm = 0.0; }
+                if (!okp) { Ap = Cp = Dp = Vp = Wp = 0.0; }
+            }
+            const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
+            const double An = -A_ * Am * ib, Cn = -C_ * Cp * ib;
+            D_ = (D_ - A_ * Dm - C_ * Dp) * ib;
+            V_ = (V_ - A_ * Vm - C_ * Vp) * ib;
+            W_ = (W_ - A_ * Wm - C_ * Wp) * ib;
+            A_ = An; C_ = Cn;
+            put(nxt, tid, A_, C_, D_, V_, W_);
+            __syncthreads();
+        };
+        static_assert(CNT == 128, "PCR levels below are written out for 128 unknowns");
+        const double *fin = pb0;                      // buffer holding the final (Y, V, W)
+        if (lim > 1) { level(1, pb0, pb1); fin = pb1; }
+        if (lim > 2) { level(2, pb1, pb0); fin = pb0; }
+        if (lim > 4) { level(4, pb0, pb1); fin = pb1; }
+        if (lim > 8) { level(8, pb1, pb0); fin = pb0; }
+        if (lim > 16) { level(16, pb0, pb1); fin = pb1; }
+        if (lim > 32) { level(32, pb1, pb0); fin = pb0; }
+        if (lim > 64) { level(64, pb0, pb1); fin = pb1; }
+        // (Y, V, W) of the neighbouring slots, read before the exchange: after it
+        // the neighbours' filter halo rows may land in arrays 2, 3
+        const double Yl = fin[2 * PSTR + tid - 1], Vl = fin[3 * PSTR + tid - 1], Wl = fin[4 * PSTR + tid - 1];
+        const double Yr = fin[2 * PSTR + tid + 1], Vr = fin[3 * PSTR + tid + 1], Wr = fin[4 * PSTR + tid + 1];
+        const double Yks = fin[2 * PSTR + ks - 1], Vks = fin[3 * PSTR + ks - 1], Wks = fin[4 * PSTR + ks - 1];
+        CL_MARK(5);
+        // publish (DSMEM, st.async): warp 0 sends the first-row relation of chunk 0
+        // and (Y, V, W) of slot 0 (what the previous CTA's separator row needs);
+        // the warp of thread ks sends the raw reduced row of the separator chunk
+        // and (Y, V, W) of slot ks-1 -- to every CTA of the cluster
+        cl_wait();                                    // every CTA of the cluster has started
+        if (wid == 0 || wid == (ks >> 5)) {
+            double v6[6];
+            if (wid == 0) {
+                v6[0] = __shfl_sync(0xffffffffu, dm[0], 0); v6[1] = __shfl_sync(0xffffffffu, am[0], 0);
+                v6[2] = __shfl_sync(0xffffffffu, cm[0], 0); v6[3] = __shfl_sync(0xffffffffu, D_, 0);
+                v6[4] = __shfl_sync(0xffffffffu, V_, 0); v6[5] = __shfl_sync(0xffffffffu, W_, 0);
+                for (int i = lane; i < 6 * C; i += 32) {
+                    const int rk = i / 6, k = i - rk * 6;
+                    st_remote(&s_cx[c][6 + k], &s_xmb, unsigned(rk), v6[k]);
+                }
+            }
+            if (wid == (ks >> 5)) {
+                const int ls = ks & 31;
+                v6[0] = __shfl_sync(0xffffffffu, aE, ls); v6[1] = __shfl_sync(0xffffffffu, cE, ls);
+                v6[2] = __shfl_sync(0xffffffffu, dE, ls);
+                v6[3] = Yks; v6[4] = Vks; v6[5] = Wks;
+                for (int i = lane; i < 6 * C; i += 32) {
+                    const int rk = i / 6, k = i - rk * 6;
+                    st_remote(&s_cx[c][k], &s_xmb, unsigned(rk), v6[k]);
+                }
+            }
+        }
+        mbar_wait(xmb, 0u);                           // all separator data in s_cx
+        CL_MARK(6);
+        // separator system, solved redundantly by every warp (lane j < C holds
+        // equation j), PCR over the C lanes
+        double Lj;
+        {
+            double a = 0.0, cc = 0.0, d = 0.0;
+            const int j = lane;
+            if (j < C) {
+                const int jn = (j + 1 < C) ? j + 1 : (cyc ? 0 : -1);
+                const double aEj = s_cx[j][0], cEj = s_cx[j][1], dEj = s_cx[j][2];
+                const double Yp = s_cx[j][3], Vp = s_cx[j][4], Wp = s_cx[j][5];
+                double P1n = 0, Q1n = 0, R1n = 0, Y0 = 0, V0 = 0, W0 = 0;
+                if (jn >= 0) {
+                    P1n = s_cx[jn][6]; Q1n = s_cx[jn][7]; R1n = s_cx[jn][8];
+                    Y0 = s_cx[jn][9]; V0 = s_cx[jn][10]; W0 = s_cx[jn][11];
+                }
+                const double cr = cEj * R1n;
+                const double sub = -aEj * Vp;
+                const double dia = (1.0 - cEj * Q1n) - aEj * Wp + cr * V0;
+                const double sup = cr * W0;
+                const double rhs = dEj - cEj * P1n - aEj * Yp + cr * Y0;
+                const double id = rcp(dia);
+                a = sub * id; cc = sup * id; d = rhs * id;
+            }
+            // the couplings of neighbouring separators go through the spike tips
+            // (~ r^T): they are usually decoupled to round-off already (the
+            // in-CTA PCR's stop test): then L_j = d_j, else PCR over the lanes
+            const bool dec = __all_sync(0xffffffffu, fabs(a) <= 5.421010862427522e-20 &&
+                                                         fabs(cc) <= 5.421010862427522e-20);   // 2^-64
+            for (int sd = 1; sd < C && !dec; sd <<= 1) {
+                int jm = j - sd, jp = j + sd;
+                if (cyc) { jm = (jm % C + C) % C; jp = jp % C; }
+                const double am_ = __shfl_sync(0xffffffffu, a, jm & 31), cm_ = __shfl_sync(0xffffffffu, cc, jm & 31);
+                const double dm_ = __shfl_sync(0xffffffffu, d, jm & 31);
+                const double ap_ = __shfl_sync(0xffffffffu, a, jp & 31), cp_ = __shfl_sync(0xffffffffu, cc, jp & 31);
+                const double dp_ = __shfl_sync(0xffffffffu, d, jp & 31);
+                const bool okm = j < C && jm >= 0 && jm < C, okp = j < C && jp >= 0 && jp < C;
+                const double Am = okm ? am_ : 0.0, Cm = okm ? cm_ : 0.0, Dm = okm ? dm_ : 0.0;
+                const double Ap = okp ? ap_ : 0.0, Cp = okp ? cp_ : 0.0, Dp = okp ? dp_ : 0.0;
+                const double ib = rcp(1.0 - a * Cm - cc * Ap);
+                const double na = -a * Am * ib, nc = -cc * Cp * ib;
+                d = (d - a * Dm - cc * Dp) * ib;
+                a = na; cc = nc;
+            }
+            // cyclic: the last level couples each row to itself (stride C == 0 mod C)
+            Lj = (cyc && !dec) ? d * rcp(1.0 + a + cc) : d;
+        }
+        const int cp_ = (c + 1 < C) ? c + 1 : 0, cm_ = (c > 0) ? c - 1 : C - 1;
+        const double Lm = (c > 0 || cyc) ? __shfl_sync(0xffffffffu, Lj, cm_) : 0.0;
+        const double Lc = __shfl_sync(0xffffffffu, Lj, c);
+        const double Lp = __shfl_sync(0xffffffffu, Lj, cp_);
+        // chunk ends: X_k = Y_k - V_k L_{j-1} - W_k L_j (interior), X_ks = L_j
+        const double Xk = tid < ks ? D_ - V_ * Lm - W_ * Lc : (tid == ks ? Lc : 0.0);
+        const double XL = tid == 0 ? Lm : Yl - Vl * Lm - Wl * Lc;
+        const double XR = tid + 1 == ks ? Lc : Yr - Vr * Lm - Wr * Lc;
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) hb[i] = (i == CMCH - 1) ? Xk : dm[i] - am[i] * XL - cm[i] * Xk;
+            // hbar of rows r0-1 (= X_{k-1}) and r0+4 (first row of the next chunk,
+            // or of the next CTA: from its published relation)
+            hLn = left_phys && tid == 0 ? hb[0] : XL;          // Neumann hbar_{-1} := hbar_0
+            if (tid < ks) {
+                hRn = P1 - Q1 * Xk - R1 * XR;
+            } else if (right_phys) {
+                hRn = hb[CMCH - 1];                             // Neumann hbar_Tc := hbar_{Tc-1}
+            } else {
+                const double X0n = s_cx[cp_][9] - s_cx[cp_][10] * Lc - s_cx[cp_][11] * Lp;
+                hRn = s_cx[cp_][6] - s_cx[cp_][7] * Lc - s_cx[cp_][8] * X0n;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) hb[i] = 1.0;
+            hLn = hRn = 1.0;
+        }
+    }
+    acc.rho = fmax(acc.rho, S.t2 * __hiloint2double(acc.bhi + 1, 0));
+    CL_MARK(7);
+
+    // ---- phase 3: back-substitution, own rows -------------------
+    double qbv[CMCH], HdD[CMCH], Wbv[CMCH], bbv[CMCH], ihv[CMCH];
+    double vb[CMCH + 2], vd[CMCH + 2], vH[CMCH + 2], vq[CMCH + 2];
+#pragma unroll
+    for (int k = 0; k < CMCH + 2; k++) {
+        const int x = swz(r0 - 1 + k);
+        vb[k] = sBe[x]; vd[k] = sDe[x]; vH[k] = sHd[x]; vq[k] = sQd[x];
+    }
+#pragma unroll
+    for (int i = 0; i < CMCH; i++) {
+        const int r = r0 + i;
+        bbv[i] = 0.0;
+        const double h0 = hb[i];
+        const double hl = (i > 0) ? hb[i - 1] : hLn;
+        const double hr = (i < CMCH - 1) ? hb[i + 1] : hRn;
+        double qb = vq[i + 1] - tdx2 * vb[i + 1] * (hr - hl) - ltdx2 * vd[i + 1] * (vH[i + 2] - vH[i]);
+        if (BATHY && live) {
+            const double bm = sB[swz(r - 1)], bp = sB[swz(r + 1)];
+            bbv[i] = sB[swz(r)];
+            qb -= tau * g * sEh[swz(r)] * (bp - bm) * (0.5 * idx1);     // A9
+        }
+        // Hbar = H^dag hbar^2/(hbar^2 + lam tau^2), Wbar; final
+        // stage: Z = 1/(hbar (hbar^2 + lam tau^2)) also gives 1/hbar
+        const double den = h0 * h0 + lt2;
+        double rden;
+        if (FINAL) {
+            const double Z = rcp(h0 * den);
+            rden = h0 * Z;
+            ihv[i] = den * Z;
+        } else {
+            rden = rcp(den);
+            ihv[i] = 0.0;
+        }
+        HdD[i] = vH[i + 1] * rden;
+        qbv[i] = qb;
+        Wbv[i] = wd[i] - ltau * HdD[i];
+        if (live) {
+            if (!(h0 > P.h_min)) acc.err |= ERR_DRY;
+            if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) acc.err |= ERR_NONFINITE;
+        }
+    }
+    if (filt) {
+        // A19 on q, W: own rows into A2 (q), A3 (W); rows -2, -1, Tc, Tc+1 from
+        // the neighbouring CTAs (DSMEM) or mirrored at physical ends (A10)
+        double *const sQb = A2, *const sWb = A3;
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) { sQb[swz(r0 + i)] = qbv[i]; sWb[swz(r0 + i)] = Wbv[i]; }
+        }
+        if (tid == 0) {                               // rows 0, 1 -> left neighbour's Tl, Tl+1
+            if (left_phys) {
+                const double pq = wall_l ? -1.0 : 1.0;
+                sQb[swz(-1)] = pq * qbv[0]; sWb[swz(-1)] = Wbv[0];
+                sQb[swz(-2)] = wall_l ? pq * qbv[1] : qbv[0]; sWb[swz(-2)] = wall_l ? Wbv[1] : Wbv[0];
+            } else {
+                const int cl_ = (c > 0) ? c - 1 : C - 1;
+                const int Tl = (cl_ == C - 1) ? n - (C - 1) * P.T : P.T;
+                st_remote(sQb + swz(Tl), &s_fmb, cl_, qbv[0]);
+                st_remote(sWb + swz(Tl), &s_fmb, cl_, Wbv[0]);
+                st_remote(sQb + swz(Tl + 1), &s_fmb, cl_, qbv[1]);
+                st_remote(sWb + swz(Tl + 1), &s_fmb, cl_, Wbv[1]);
+            }
+        }
+        if (tid == ks) {                              // rows Tc-2, Tc-1 -> right neighbour's -2, -1
+            if (right_phys) {
+                const double pq = wall_r ? -1.0 : 1.0;
+                sQb[swz(Tc)] = pq * qbv[3]; sWb[swz(Tc)] = Wbv[3];
+                sQb[swz(Tc + 1)] = wall_r ? pq * qbv[2] : qbv[3]; sWb[swz(Tc + 1)] = wall_r ? Wbv[2] : Wbv[3];
+            } else {
+                const int cr_ = (c + 1 < C) ? c + 1 : 0;
+                st_remote(sQb + swz(-2), &s_fmb, cr_, qbv[2]);
+                st_remote(sWb + swz(-2), &s_fmb, cr_, Wbv[2]);
+                st_remote(sQb + swz(-1), &s_fmb, cr_, qbv[3]);
+                st_remote(sWb + swz(-1), &s_fmb, cr_, Wbv[3]);
+            }
+        }
+        __syncthreads();                              // own rows and mirrored ghosts
+        mbar_wait(fmb, 0u);                           // neighbours' rows
+        if (live) {
+            const double sig16 = P.filter_sigma * (1.0 / 16.0);
+            double xq[CMCH + 4], xw[CMCH + 4];
+            xq[0] = sQb[swz(r0 - 2)]; xq[1] = sQb[swz(r0 - 1)];
+            xq[CMCH + 2] = sQb[swz(r0 + CMCH)]; xq[CMCH + 3] = sQb[swz(r0 + CMCH + 1)];
+            xw[0] = sWb[swz(r0 - 2)]; xw[1] = sWb[swz(r0 - 1)];
+            xw[CMCH + 2] = sWb[swz(r0 + CMCH)]; xw[CMCH + 3] = sWb[swz(r0 + CMCH + 1)];
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) { xq[i + 2] = qbv[i]; xw[i + 2] = Wbv[i]; }
+#pragma unroll
+            for (int i = 0; i < CMCH; i++) {
+                // f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
+                qbv[i] = xq[i + 2] - sig16 * (xq[i] - 4.0 * xq[i + 1] + 6.0 * xq[i + 2] - 4.0 * xq[i + 3] + xq[i + 4]);
+                Wbv[i] = xw[i + 2] - sig16 * (xw[i] - 4.0 * xw[i + 1] + 6.0 * xw[i + 2] - 4.0 * xw[i + 3] + xw[i + 4]);
+                if (!isfinite(qbv[i] + Wbv[i])) acc.err |= ERR_NONFINITE;
+            }
+        }
+    }
+    CL_MARK(8);
+    // final values, dt maxima, direct 16-B stores of the own rows
+    if (live) {
+        double oh[CMCH], oK[CMCH];
+#pragma unroll
+        for (int i = 0; i < CMCH; i++) {
+            const double h0 = hb[i];
+            const double Hb = HdD[i] * (h0 * h0);
+            oh[i] = h0;
+            oK[i] = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
+            if (FINAL) {
+                const double u = fabs(qbv[i] * ihv[i]), sg = HdD[i];
+                const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
+                acc.umax = u > acc.umax ? u : acc.umax;
+                acc.numax = nu > acc.numax ? nu : acc.numax;
+            }
+        }
+        const size_t gd = mo + size_t(s + r0);
+        double2 *const o0 = reinterpret_cast<double2 *>(B.out[0] + gd);
+        double2 *const o1 = reinterpret_cast<double2 *>(B.out[1] + gd);
+        double2 *const o2 = reinterpret_cast<double2 *>(B.out[2] + gd);
+        double2 *const o3 = reinterpret_cast<double2 *>(B.out[3] + gd);
+        o0[0] = make_double2(oh[0], oh[1]); o0[1] = make_double2(oh[2], oh[3]);
+        o1[0] = make_double2(qbv[0], qbv[1]); o1[1] = make_double2(qbv[2], qbv[3]);
+        o2[0] = make_double2(oK[0], oK[1]); o2[1] = make_double2(oK[2], oK[3]);
+        o3[0] = make_double2(Wbv[0], Wbv[1]); o3[1] = make_double2(Wbv[2], Wbv[3]);
+    }
+    CL_MARK(9);
+    tile_epilogue<FINAL>(P, c, m, dtm, acc, tm0, tend0);
+#if HSGN_EXP_TIMING
+    CL_MARK(10);
+    if (tid == 0) {
+        unsigned long long *gg = g_clt[STAGE2 ? 1 : 0];
+        for (int k = 1; k <= 10; k++) atomicAdd(gg + k - 1, (unsigned long long)(tmk[k] - tmk[k - 1]));
+        atomicAdd(gg + 15, 1ull);
+    }
+#endif
+}
+
+}  // namespace hsgn

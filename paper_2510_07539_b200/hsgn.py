@@ -58,7 +58,7 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_set_state", "hsgn_get_state", "hsgn_run_host", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
            "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
            "hsgn_set_fused", "hsgn_get_fused", "hsgn_set_persistent", "hsgn_set_scheme",
-           "hsgn_set_picard", "hsgn_set_well_balanced",
+           "hsgn_set_picard", "hsgn_set_well_balanced", "hsgn_set_cluster", "hsgn_get_cluster",
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
            "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl"]
 
@@ -103,6 +103,8 @@ def load_library(path: str = LIB_PATH):
         "hsgn_set_scheme": (st, [vp, C.c_int32, C.c_int32]),
         "hsgn_set_picard": (st, [vp, C.c_int32]),
         "hsgn_set_well_balanced": (st, [vp, C.c_int32]),
+        "hsgn_set_cluster": (st, [vp, C.c_int32]),
+        "hsgn_get_cluster": (C.c_int32, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "hsgn_status_string": (C.c_char_p, [st]),
         "hsgn_group_create": (st, [C.POINTER(vp), C.c_int32, C.POINTER(vp)]),
         "hsgn_group_run_steps": (st, [vp, C.c_int64]),
@@ -234,6 +236,19 @@ class Solver:
     def set_well_balanced(self, on: bool = True) -> None:
         """A25 exactly well-balanced face form of the SI stage (default off: the paper's)."""
         self._chk(self.L.hsgn_set_well_balanced(self.ctx, 1 if on else 0))
+
+    def set_cluster(self, mode) -> None:
+        """Cluster stage kernels with the exact cross-CTA depth solve: True/1 =
+        whenever the member fits, False/0 = never (overlapped tiles), 2 = auto
+        (default: only for material-CFL-only stepping) (hsgn_set_cluster)."""
+        self._chk(self.L.hsgn_set_cluster(self.ctx, int(mode)))
+
+    @property
+    def cluster(self):
+        """(C, tile rows) if the next step runs on the cluster kernels, else None."""
+        a, b = C.c_int32(), C.c_int32()
+        on = int(self.L.hsgn_get_cluster(self.ctx, C.byref(a), C.byref(b)))
+        return (a.value, b.value) if on == 1 else None
 
     def set_persistent(self, on: bool) -> None:
         """Persistent per-stage kernels with next-tile prefetch, or one CTA per

@@ -169,24 +169,26 @@ def cfg3(members: int = 4096, n: int = 4096, seed: int = 7539003, dx: float = 0.
     200 steps in some members (A19), so no full-run parity is possible
     without it; filter_sigma = 0 gives the literal scheme.
 
-    The per-member draws come from one PCG64 stream in member order, so any
-    subset [first_member, first_member + members) is reproducible on its own."""
+    Each member m draws from its own PCG64 stream seeded with (seed, m), in the
+    order n_s, amplitudes[3], positions[3], lambda, so member m's state does not
+    depend on how many members are generated or which shard does it: any subset
+    [first_member, first_member + members) equals the same rows of the full
+    ensemble."""
     L = n * dx
-    rng = np.random.Generator(np.random.PCG64(seed))
-    total = first_member + members
-    ns = rng.integers(1, 4, size=total)
-    amps = rng.uniform(0.05, 0.3, size=(total, 3))
-    pos = rng.uniform(0.0, L, size=(total, 3))
-    lam = 10.0 ** rng.uniform(2.0, 4.0, size=total)
     x = cell_centres(0.0, L, n)
     H = np.empty((members, n)); Q = np.empty((members, n))
     KK = np.empty((members, n)); WW = np.empty((members, n))
+    lam = np.empty(members)
     for mi in range(members):
         m = first_member + mi
-        k = int(ns[m])
-        H[mi], Q[mi], KK[mi], WW[mi] = multi_soliton_state(x, amps[m, :k], pos[m, :k], L=L)
+        rng = np.random.Generator(np.random.PCG64([seed, m]))
+        k = int(rng.integers(1, 4))
+        amps = rng.uniform(0.05, 0.3, size=3)
+        pos = rng.uniform(0.0, L, size=3)
+        lam[mi] = 10.0 ** rng.uniform(2.0, 4.0)
+        H[mi], Q[mi], KK[mi], WW[mi] = multi_soliton_state(x, amps[:k], pos[:k], L=L)
     return Workload("cfg3_ensemble", n, members, 0.0, L, ("periodic", "periodic"),
-                    lam[first_member:total].copy(), H, Q, KK, WW, cfl=2.0, mcfl=0.5,
+                    lam, H, Q, KK, WW, cfl=2.0, mcfl=0.5,
                     steps=200, filter_sigma=filter_sigma,
                     meta=dict(seed=seed, first_member=first_member))
 

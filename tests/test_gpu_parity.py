@@ -5,7 +5,17 @@ after a full run (north_star), with S_f the magnitude of the field's state and
 update terms: S_h = max|h|, S_K = max|K|, S_q = max(max|q|, sqrt(g h_max) h_max)
 (the momentum of an O(1) shallow-water wave), S_W = max(max|W|, lam dt) (P:502
 adds lam dt to W and P:515 removes ~lam dt again, so W's rounding floor is
-eps * lam dt, not eps * max|W|, which is ~0 near rest)."""
+eps * lam dt, not eps * max|W|, which is ~0 near rest).
+
+The plain normwise form (S_f = max|f_ref|) is printed beside it for every
+comparison.  Its rounding floor was measured oracle against oracle -- the same
+source built with FMA contraction, tools/a17_floor.py,
+profiles/r02_a17_floor.json: cfg5 after one step 1.8e-10 (q) and 1.4e-8 (W),
+i.e. above 1e-11 for two fp64 implementations of the same algorithm.  Where a
+test asks for it (floor=True) the floor is measured live on the same members
+and every field must also satisfy plain <= max(tol, FLOOR_K * plain floor): an
+error confined to q or W is bounded by the rounding of the algorithm itself,
+not by the looser scaled form."""
 import math
 
 import numpy as np
@@ -18,6 +28,7 @@ pytestmark = pytest.mark.gpu
 
 TOL_STEP = 1e-11
 TOL_RUN = 1e-8
+FLOOR_K = 30.0
 
 
 def _hsgn():
@@ -30,6 +41,17 @@ def field_scales(ref, lam, dt, g=9.81):
     hm = np.max(np.abs(h))
     return [hm, max(np.max(np.abs(q)), np.sqrt(g * hm) * hm), np.max(np.abs(K)),
             max(np.max(np.abs(Wf)), lam * dt)]
+
+
+def field_errs(gpu, ref, scales=None):
+    """per field: max_i |gpu - ref| / S_f (S_f = max|ref| if scales is None)"""
+    out = []
+    for k, (fg, fr) in enumerate(zip(gpu, ref)):
+        fg = np.asarray(fg)
+        fr = np.asarray(fr)
+        S = scales[k] if scales is not None else np.max(np.abs(fr))
+        out.append(float(np.max(np.abs(fg - fr)) / max(S, 1e-300)))
+    return out
 
 
 def rel_err(gpu, ref, scales=None):
@@ -45,12 +67,12 @@ def rel_err(gpu, ref, scales=None):
 
 
 def oracle_run(w, members, steps=None, t_end=None, order=2, tableau=None, dt_fixed=0.0, picard=0,
-               wb=False):
+               wb=False, variant="plain"):
     jobs = []
     for m in members:
         o = O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, order=order, b=w.b,
                      filter_sigma=w.filter_sigma, tableau=tableau, relax=w.meta.get("relax"),
-                     picard=picard, wb=wb)
+                     picard=picard, wb=wb, variant=variant)
         jobs.append((o, w.state(m)))
     res = O.run_members(jobs, cfl=w.cfl, mcfl=w.mcfl, steps=steps, t_end=t_end, dt_fixed=dt_fixed)
     return [r[0] for r in res], [r[1] for r in res]
@@ -78,9 +100,10 @@ def gpu_solver(w, **kw):
     return s
 
 
-def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, **okw):
+def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, floor=False, **okw):
     (h, q, K, Wf), t = s.get_state(device=False)
     refs, trefs = oracle_run(w, members, steps=steps, t_end=t_end, **okw)
+    frefs = oracle_run(w, members, steps=steps, t_end=t_end, variant="fma", **okw)[0] if floor else None
     worst = 0.0
     for i, m in enumerate(members):
         o = O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[m]), bc=w.bc, b=w.b)
@@ -88,7 +111,18 @@ def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, **okw):
             dt = o.dt(refs[i], w.cfl, w.mcfl)[0]
         except O.OracleError:
             dt = 0.0
-        e = rel_err([h[m], q[m], K[m], Wf[m]], refs[i], field_scales(refs[i], float(w.lam[m]), dt, w.g))
+        got = [h[m], q[m], K[m], Wf[m]]
+        sc = field_errs(got, refs[i], field_scales(refs[i], float(w.lam[m]), dt, w.g))
+        pl = field_errs(got, refs[i])
+        e = max(sc)
+        msg = f"parity {w.name} m={m} steps={steps} scaled={e:.2e} plain(h,q,K,W)=" + \
+              ",".join(f"{x:.1e}" for x in pl)
+        if floor:
+            fl = field_errs(frefs[i], refs[i])
+            msg += " floor=" + ",".join(f"{x:.1e}" for x in fl)
+            for k in range(4):
+                assert pl[k] <= max(tol, FLOOR_K * fl[k]), (m, k, pl, fl)
+        print(msg)
         worst = max(worst, e)
         # t accumulates dt's computed from states that agree to ~tol
         assert abs(t[m] - trefs[i]) <= max(tol, 1e-13) * max(1.0, abs(trefs[i])), (m, t[m], trefs[i])
@@ -314,9 +348,9 @@ def test_cfg3_subset_200_steps(kmode):
     w = W.cfg3(members=6)
     s = gpu_solver(w, kmode=kmode)
     s.run_steps(1)
-    compare(w, s, range(6), steps=1)
+    compare(w, s, range(6), steps=1, floor=True)
     s.run_steps(199)
-    compare(w, s, range(6), steps=200, tol=TOL_RUN)
+    compare(w, s, range(6), steps=200, tol=TOL_RUN, floor=True)
 
 
 @pytest.mark.slow
@@ -340,9 +374,9 @@ def test_cfg2_dam_break_walls_scaled():
         w = W.cfg2(lam, n=1 << 14)
         s = gpu_solver(w)
         s.step()
-        compare(w, s, [0], steps=1)
+        compare(w, s, [0], steps=1, floor=True)
         s.run_steps(199)
-        compare(w, s, [0], steps=200, tol=TOL_RUN)
+        compare(w, s, [0], steps=200, tol=TOL_RUN, floor=True)
         d = s.diagnostics()
         m0 = np.sum(w.h[0]) * w.dx
         assert abs(d["mass"] - m0) <= 1e-13 * m0
@@ -353,9 +387,9 @@ def test_cfg5_bathymetry_scaled():
     w = W.cfg5_workload(1 << 20)
     s = gpu_solver(w)
     s.step()
-    compare(w, s, [0], steps=1)
+    compare(w, s, [0], steps=1, floor=True)
     s.run_steps(9)
-    compare(w, s, [0], steps=10, tol=1e-10)
+    compare(w, s, [0], steps=10, tol=1e-10, floor=True)
 
 
 def test_cfg5_full_size_sampled():
@@ -537,4 +571,4 @@ def test_randomised_cases_one_step(case):
         kw["tile_cells"] = int(rng.integers(64, 600))
     s = gpu_solver(w, **kw)
     s.step()
-    compare(w, s, range(members), steps=1, order=order)
+    compare(w, s, range(members), steps=1, order=order, floor=True)

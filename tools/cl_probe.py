@@ -1,0 +1,27 @@
+"""Dev probe: cfg3-shaped ensemble, K timed SI steps (one graph with event
+nodes), cluster kernels on / off; prints per-stage device ms and fractions of
+the HBM roofline.  Usage: python tools/cl_probe.py [members] [steps] [cluster 0/1] [cells]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2510_07539_b200 import hsgn as hs          # noqa: E402
+from paper_2510_07539_b200 import workloads as W      # noqa: E402
+
+members = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+cl = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+cells = int(sys.argv[4]) if len(sys.argv) > 4 else 4096
+w = W.cfg3(members=members, n=cells)
+s = hs.solver_for(w)
+s.set_cluster(bool(cl))
+print("cluster", s.cluster, "geometry", s.geometry)
+s.run_steps(3)
+s.sync()
+ms1, ms2, tot = s.run_steps_timed(steps, total=True)
+N = cells * members
+peak = 6536.7e9
+t1, t2 = ms1 / steps * 1e-3, ms2 / steps * 1e-3
+print(f"stage1 {t1*1e6:.1f} us ({64*N/t1/peak:.3f}), stage2 {t2*1e6:.1f} us ({96*N/t2/peak:.3f}), "
+      f"step {tot/steps*1e3:.1f} us, {2*N*steps/(tot*1e-3)/1e9:.2f} G cell-stage/s")

@@ -115,13 +115,37 @@ SGNB_MUTANTS = {
         ("* (g * hp3 * (XZ(i + 2) - 2.0 * XZ(i + 1) + XZ(i))", "* (g * hp3 * (XS(eh, i + 2) - 2.0 * hp + XS(eh, i))"),
 }
 
+# operator-split extras and the Picard pass: tests/test_oracle_pins_ops.py
+OPS_MUTANTS = {
+    "A19 filter sigma/16 -> sigma/8":
+        ("U[k][i] = ext[i + 2] - (P->filter_sigma / 16.0) * d4;",
+         "U[k][i] = ext[i + 2] - (P->filter_sigma / 8.0) * d4;"),
+    "Picard pass beta2 factor 2 -> 1":
+        ("double beta2 = 2.0 * lam * tau * tau / (beta1 * beta1 * hb * hb * hb);",
+         "double beta2 = 1.0 * lam * tau * tau / (beta1 * beta1 * hb * hb * hb);"),
+    "Picard pass delta = alpha (not alpha/beta1)":
+        ("de[i + 1] = alE[i] / beta1;", "de[i + 1] = alE[i];"),
+    "sponge ramp r^2 -> r":
+        ("double r = (x - P->sp_x0) / (x_max - P->sp_x0);\n            s = P->sp_rate * r * r;",
+         "double r = (x - P->sp_x0) / (x_max - P->sp_x0);\n            s = P->sp_rate * r;"),
+    "A19 filter stencil not conservative (6 -> 5)":
+        ("6.0 * ext[i + 2]", "5.0 * ext[i + 2]"),
+    "A19 filter q ghost parity even at walls":
+        ("double par = (k == 1) ? -1.0 : 1.0;", "double par = 1.0;"),
+    "wavemaker target velocity halved":
+        ("double u = P->cp * eta / P->level;", "double u = 0.5 * P->cp * eta / P->level;"),
+}
+
 ok = True
 for name, (a, b), tf in [(k, v, "test_oracle_pins.py") for k, v in MUTANTS.items()] + \
                         [(k, v, "test_oracle_wb.py") for k, v in WB_MUTANTS.items()] + \
                         [(k, v, "test_oracle_explicit.py") for k, v in EX_MUTANTS.items()] + \
                         [(k, v, "test_oracle_sgn.py") for k, v in SGN_MUTANTS.items()] + \
-                        [(k, v, "test_oracle_sgnb.py") for k, v in SGNB_MUTANTS.items()]:
+                        [(k, v, "test_oracle_sgnb.py") for k, v in SGNB_MUTANTS.items()] + \
+                        [(k, v, "test_oracle_pins_ops.py") for k, v in OPS_MUTANTS.items()]:
     assert SRC.count(a) >= 1, name
+    if len(sys.argv) > 1 and not any(k in name for k in sys.argv[1:]):
+        continue
     mut = SRC.replace(a, b, 1)
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "m.c")

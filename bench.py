@@ -62,10 +62,9 @@ def parse():
                    help="si: the SI-IMEX step (headline); explicit: the explicit hSGN scheme "
                         "(Heun, CFL_EX 0.4); sgn: the classical SGN scheme (Heun, CFL_SGN 0.9) "
                         "on the same workload")
-    p.add_argument("--persistent", type=int, default=-1,
-                   help="1: persistent per-stage kernels, 0: one CTA per tile, -1: library default")
-    p.add_argument("--fused", type=int, default=-1,
-                   help="1: fused step kernel, 0: per-stage kernels, -1: library default")
+    p.add_argument("--cluster", type=int, default=-1,
+                   help="1: cluster stage kernels (exact cross-CTA depth solve) whenever the member fits, "
+                        "0: overlapped tiles, -1: library default (auto)")
     p.add_argument("--config", default="cfg3", choices=["cfg3", "cfg5"],
                    help="cfg3: ensemble (default, headline); cfg5: single 2^28-cell domain with bathymetry")
     p.add_argument("--cells5", type=int, default=1 << 28)
@@ -340,10 +339,8 @@ def main():
         s.set_filter(0.0)
         s.set_params(w.g, w.lam, CFL_SGN, 0.0)
         s.set_scheme("sgn", 2)
-    if a.fused >= 0:
-        s.set_fused(bool(a.fused))
-    if a.persistent >= 0:
-        s.set_persistent(bool(a.persistent))
+    if a.cluster >= 0:
+        s.set_cluster(a.cluster)
     state_bytes = 4 * 8 * Ntot
 
     def barrier():

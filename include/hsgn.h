@@ -63,7 +63,9 @@ typedef enum {
     HSGN_E_CUDA = -6,       /* CUDA runtime error                         */
     HSGN_E_OVERLAP = -7,    /* tile overlap too short for the depth solve's
                                decay (solver); result inexact  */
-    HSGN_E_NOWORKSPACE = -8 /* workspace missing or too small             */
+    HSGN_E_NOWORKSPACE = -8,/* workspace missing or too small             */
+    HSGN_E_COMM = -9        /* NCCL failure in the slab transport (halo
+                               send/recv, dt all-reduce, communicator)   */
 } hsgn_status;
 
 typedef enum {
@@ -103,9 +105,17 @@ typedef struct {
 
 /* Diagnostics (all members): mass = sum_i h_i dx summed over members,
  * min_h, max_abs_u, nu_max = max(|u| + c), t_min/t_max over members,
- * dt_last_min/max = last step's dt over members, rho_max = largest
+ * dt_last_min/max = the dt of the next step over members (set from the
+ * current state by the rule of P:613-617), rho_max = largest
  * (tau/dx)^2 (beta_i + beta_{i+1})/2 seen (sets the solver overlap),
- * steps = committed steps. */
+ * min_kappa = smallest beta = kappa of any cell in any SI
+ * stage since hsgn_set_state, rounded toward zero to 2^-20 relative (its
+ * high word) -- the coercivity monitor of the proposition at P:297-334 (a
+ * value <= 0 also latches HSGN_E_COERCIVITY; +inf before the first SI stage;
+ * not updated by the explicit and SGN schemes),
+ * cfl_imex / mcfl = the achieved Courant numbers dt nu_max / dx and
+ * dt max|u| / dx of the next step (max over members; P:617-643 report the
+ * varying CFL), steps = committed steps. */
 typedef struct {
     double mass;
     double min_h;
@@ -116,6 +126,9 @@ typedef struct {
     double dt_last_min;
     double dt_last_max;
     double rho_max;      /* max off-diagonal rho of the depth system seen since set_state */
+    double min_kappa;    /* min kappa = beta since set_state (coercivity monitor)        */
+    double cfl_imex;     /* dt nu_max / dx of the next step (max over members)           */
+    double mcfl;         /* dt max|u| / dx of the next step (max over members)           */
     int64_t steps;
     int32_t error_bits;
     int32_t pad_;
@@ -217,8 +230,7 @@ hsgn_status hsgn_advance_to(hsgn_ctx *ctx, double t_end, int64_t max_steps,
  * nodes before, between and after the kernels, then launched once -- the launch
  * mode of hsgn_run_steps), synchronise, and return (ms, device clock) in
  * stage_ms[0] / stage_ms[1] the summed time of the stage-1 / stage-2 kernels
- * (stage_ms[1] = 0 for a 1-stage tableau; for a fused step stage_ms[0] is the
- * fused kernel) and in stage_ms[2] the time of the whole n steps (first to last
+ * (stage_ms[1] = 0 for a 1-stage tableau) and in stage_ms[2] the time of the whole n steps (first to last
  * kernel).  stage_ms: 3 doubles.  Same arithmetic as hsgn_run_steps; used by
  * bench.py for the step time and the per-kernel rooflines.  Needs a
  * non-default stream; not for slab contexts (HSGN_E_INVALID). */
@@ -230,16 +242,6 @@ hsgn_status hsgn_sync(hsgn_ctx *ctx);
 hsgn_status hsgn_get_diagnostics(hsgn_ctx *ctx, hsgn_diag *out);
 /* Number of kernel launches enqueued by this context since creation. */
 int64_t hsgn_launch_count(const hsgn_ctx *ctx);
-/* Fused step: a two-stage tableau on a non-slab domain
- * runs each step as ONE persistent kernel (stage 1 on a widened tile, U1 kept
- * in shared memory, stage 2, next tile prefetched) instead of one kernel per
- * stage.  Both paths compute the same P:500-517 arithmetic.  on = 1 selects the
- * fused kernel (tests compare both); default off (measured slower on B200,
- * DESIGN.md section 6).  Drops captured graphs and re-chooses the tile
- * geometry.  Errors: HSGN_E_INVALID (null context). */
-hsgn_status hsgn_set_fused(hsgn_ctx *ctx, int32_t on);
-/* 1 if steps currently run as the fused kernel, 0 otherwise (-1: null). */
-int32_t hsgn_get_fused(const hsgn_ctx *ctx);
 /* Time-stepping scheme.  HSGN_SCHEME_SI (default): the
  * semi-implicit IMEX step of P:500-517.  HSGN_SCHEME_EXPLICIT: the explicit
  * hSGN scheme of P:442-458 -- central D_x for the mass flux and the pressure
@@ -269,8 +271,7 @@ hsgn_status hsgn_set_scheme(hsgn_ctx *ctx, int32_t scheme, int32_t stages);
  * stage, `passes` more assemble+solve passes with beta1 = 1 + lam tau^2/h^2
  * and beta2 = 2 lam tau^2/(beta1^2 h^3) (hence kappa = beta and delta) at the
  * latest hbar, alpha and a^2 staying at the stage input E.  0 (default) = the
- * paper's scheme.  Runs on the one-CTA-per-tile stage kernels (the fused and
- * persistent organisations are bypassed); not with relaxation zones or the
+ * paper's scheme.  Runs on the overlapped-tile stage kernels; not with relaxation zones or the
  * explicit / SGN schemes (HSGN_E_INVALID at the next step).  Errors:
  * HSGN_E_INVALID (null context, passes outside 0..16). */
 hsgn_status hsgn_set_picard(hsgn_ctx *ctx, int32_t passes);
@@ -288,13 +289,6 @@ hsgn_status hsgn_set_picard(hsgn_ctx *ctx, int32_t passes);
  * (HSGN_E_INVALID at the next step).  Drops captured graphs.  Errors:
  * HSGN_E_INVALID (null context). */
 hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
-/* Per-stage kernels as persistent CTAs: each CTA walks
- * (tile, member) items and prefetches the next item's inputs by TMA while it
- * finishes the current one; on = 0: one CTA per (tile, member).  Same
- * arithmetic either way.  Default off (measured slower on B200, DESIGN.md
- * section 6).  Drops captured graphs.  Errors:
- * HSGN_E_INVALID (null context). */
-hsgn_status hsgn_set_persistent(hsgn_ctx *ctx, int32_t on);
 /* Cluster stage kernels (hsgn_cluster.cuh): the C CTAs
  * of a member form one thread-block cluster and solve the depth system of
  * P:509-512 EXACTLY across their tiles (partition method per thread chunk,

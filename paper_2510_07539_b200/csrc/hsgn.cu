@@ -66,7 +66,7 @@ struct hsgn_ctx {
     double *b = nullptr, *lamd = nullptr, *t = nullptr, *dt = nullptr, *dt_used = nullptr,
            *partials = nullptr;
     unsigned long long *maxes = nullptr, *rho_obs = nullptr;
-    unsigned int *work = nullptr;
+    unsigned int *kmin = nullptr;
     unsigned int *err = nullptr, *done = nullptr;
     long long *steps = nullptr;
     Ctrl *ctrl = nullptr;
@@ -80,11 +80,6 @@ struct hsgn_ctx {
     // slab decomposition (BC_HALO sides): halo receive buffers [9][H_MAX] per side
     double *halo_l = nullptr, *halo_r = nullptr;
     bool slab = false;
-    // fused two-stage step kernel (persistent CTAs): off unless enabled, used for
-    // two-stage tableaux on non-slab domains when the widened tile fits
-    bool fused_on = false, fused = false;
-    int fused_grid = 0;
-    int pf_dist = 0;              // L2 prefetch distance of the stage kernels (CTAs)
     // scheme: 0 = SI-IMEX (default), 1 = explicit hSGN (P:442-480,
     // x_stages 1 = Euler, 2 = Heun) on tiles of xT cells
     int scheme = 0, x_stages = 2, xT = 0, xtiles = 0;
@@ -93,11 +88,6 @@ struct hsgn_ctx {
     int picard = 0;               // A24 Picard passes of the SI depth solve (0: the paper's)
     bool wb = false;              // A25 exactly well-balanced face form of the SI stage
     bool ev_ext = false;          // record events as graph nodes (timed capture)
-    bool pdl = false;             // programmatic dependent launch of the step's kernels
-                                  // (HSGN_PDL=1; measured no gain on cfg3, -7 % on cfg2)
-    // persistent stage kernels (walk tiles, prefetch the next tile's inputs)
-    bool persist = false;
-    int persist_grid = 0;
     // cluster stage kernels (exact depth solve across the CTAs of a cluster,
     // hsgn_cluster.cuh): C CTAs of clT rows per member; used whenever the
     // member fits (n <= 16 * 512, n % 4 == 0) and the step is the SI stage
@@ -164,10 +154,8 @@ Params make_params(hsgn_ctx *c, long long k)
     P.sp_x0 = c->relax.sp_x0; P.sp_rate = c->relax.sp_rate;
     P.b = c->bathy ? c->b : nullptr;
     P.lam = c->lamd; P.t = c->t; P.dt = c->dt; P.maxes = c->maxes; P.err = c->err;
-    P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.ctrl = c->ctrl;
-    P.work = c->work;
+    P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.kmin = c->kmin; P.ctrl = c->ctrl;
     P.H = c->w + 3;
-    P.pf_dist = c->pf_dist;
     if (c->scheme == 1) {            // explicit: its own tiles, dt = CFL_EX dx / mu_max only
         P.T = c->xT;
         P.tiles = c->xtiles;
@@ -191,21 +179,16 @@ Params make_params(hsgn_ctx *c, long long k)
     return P;
 }
 
-// Launch with programmatic stream serialization (PDL, see pdl_release/pdl_wait
-// in hsgn_kernels.cuh) when enabled (HSGN_PDL=1), else plain stream order.
+// Plain launch on the context's stream (cudaLaunchKernelEx, no attributes).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(hsgn_ctx *c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args)
+cudaError_t launch_k(hsgn_ctx *c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = c->pdl ? 1 : 0;
+    cfg.numAttrs = 0;
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
@@ -224,21 +207,16 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
     const size_t sm = BATHY ? SMEM_BYTES_B : SMEM_BYTES;    // one-CTA-per-tile kernels: b in smem
     if (c->picard > 0) {             // A24: one CTA per tile, Picard variant
         dim3 grid(c->tiles, c->members);
-        CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false, true>, grid, dim3(NT),
+        CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, false, true>, grid, dim3(NT),
                                BATHY ? SMEM_BYTES_PIC_B : SMEM_BYTES_PIC, P, B));
     } else if (c->wb) {              // A25: one CTA per tile, face form
         dim3 grid(c->tiles, c->members);
-        if (relax) CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, true, false, true>, grid, dim3(NT), sm, P, B));
-        else CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false, false, true>, grid, dim3(NT), sm, P, B));
-    } else if (c->persist) {
-        const int items = c->tiles * c->members;
-        const int grid = std::min(items, c->persist_grid);
-        if (relax) stage_pkernel<S2, FIN, BATHY, true><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
-        else stage_pkernel<S2, FIN, BATHY, false><<<grid, NT, SMEM_BYTES, c->stream>>>(P, B, items);
+        if (relax) CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, true, false, true>, grid, dim3(NT), sm, P, B));
+        else CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, false, false, true>, grid, dim3(NT), sm, P, B));
     } else {
         dim3 grid(c->tiles, c->members);
-        if (relax) CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, true>, grid, dim3(NT), sm, P, B));
-        else CUDA_TRY(c, launch_pdl(c, stage_kernel<S2, FIN, BATHY, false>, grid, dim3(NT), sm, P, B));
+        if (relax) CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, true>, grid, dim3(NT), sm, P, B));
+        else CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, false>, grid, dim3(NT), sm, P, B));
     }
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
@@ -323,7 +301,7 @@ void cl_attrs()
 hsgn_status launch_dtc(hsgn_ctx *c, long long k, int commit_prev, int compute_dt)
 {
     const Params P = make_params(c, k);
-    CUDA_TRY(c, launch_pdl(c, dt_commit_kernel, dim3((c->members + 127) / 128), dim3(128), 0, P, commit_prev,
+    CUDA_TRY(c, launch_k(c, dt_commit_kernel, dim3((c->members + 127) / 128), dim3(128), 0, P, commit_prev,
                            compute_dt));
     c->launches++;
     CUDA_TRY(c, cudaGetLastError());
@@ -390,23 +368,6 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
             CUDA_TRY(c, cudaGetLastError());
         }
         if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
-    } else if (c->fused) {
-        for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
-        const int items = c->tiles * c->members;
-        const bool relax = c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0;
-        if (c->bathy) {
-            if (relax) step_kernel<true, true><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
-            else step_kernel<true, false><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
-        } else {
-            if (relax) step_kernel<false, true><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
-            else step_kernel<false, false><<<c->fused_grid, NT, fused_smem_bytes(c->T), c->stream>>>(P, B, items);
-        }
-        c->launches++;
-        CUDA_TRY(c, cudaGetLastError());
-        if (ev) {
-            CUDA_TRY(c, rec_ev(c, ev[1]));
-            CUDA_TRY(c, rec_ev(c, ev[2]));
-        }
     } else if (use_cluster(c)) {
         if (c->tab.stages == 1) {
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
@@ -488,11 +449,8 @@ void choose_geometry(hsgn_ctx *c)
     } else {
         w = 256;   // material-CFL-only stepping: rho is not bounded a priori
     }
-    // fused step: stage 1 runs on the kept tile widened by 2w + 3 on each side
-    const int wmax_fused = (LCAP - 2 - 6 - T_MIN) / 4;
-    c->fused = c->fused_on && c->tab.stages == 2 && !c->slab && w <= wmax_fused && c->picard == 0 && !c->wb;
     w = std::max(3, std::min(w, (LCAP - 2 - T_MIN) / 2));
-    const int maxT = c->fused ? LCAP - 2 - 6 - 4 * w : LCAP - 2 - 2 * w;
+    const int maxT = LCAP - 2 - 2 * w;
     int T;
     if (c->desc.tile_cells > 0) T = std::max(std::min<int>(c->desc.tile_cells, maxT), T_MIN);
     else {
@@ -507,24 +465,6 @@ void choose_geometry(hsgn_ctx *c)
     c->tiles = (c->n + T - 1) / T;
     c->xT = std::min(c->n, XT);
     c->xtiles = (c->n + c->xT - 1) / c->xT;
-    {
-        int sms = 148, occ = 4;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<true, true, false>, NT, SMEM_BYTES);
-        const char *e = std::getenv("HSGN_PF_WAVES");     // tuning: prefetch distance in waves
-        const double waves = e ? std::atof(e) : 0.0;
-        c->pf_dist = int(waves * sms * std::max(occ, 1));
-        int occp = 4;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, stage_pkernel<true, true, false>, NT, SMEM_BYTES);
-        c->persist_grid = sms * std::max(occp, 1);
-    }
-    if (c->fused) {
-        int sms = 148, occ = 1;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<false, false>, NT, fused_smem_bytes(c->T));
-        const long long items = (long long)c->tiles * c->members;
-        c->fused_grid = int(std::min<long long>(items, (long long)sms * std::max(occ, 1)));
-    }
 }
 
 hsgn_status ready(hsgn_ctx *c)
@@ -584,7 +524,7 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
                 cudaGraphDestroy(gr);
             }
             CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
-            const int kpl = c->scheme != 0 ? c->x_stages : (c->fused ? 1 : c->tab.stages);
+            const int kpl = c->scheme != 0 ? c->x_stages : c->tab.stages;
             c->launches += GRAPH_STEPS * (kpl + 1);
             done += GRAPH_STEPS;          // even: cur unchanged
             c->host_steps += GRAPH_STEPS;
@@ -655,7 +595,7 @@ hsgn_status loopback_exchange(std::vector<hsgn_ctx *> &g, int which)
     do {                                                                              \
         ncclResult_t r_ = (expr);                                                     \
         if (r_ != ncclSuccess)                                                        \
-            return fail((c), HSGN_E_CUDA, std::string(#expr ": ") + ncclGetErrorString(r_)); \
+            return fail((c), HSGN_E_COMM, std::string(#expr ": ") + ncclGetErrorString(r_)); \
     } while (0)
 
 hsgn_status nccl_exchange(hsgn_ctx *c, int which)
@@ -800,9 +740,8 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         kc->tab = c->tab; kc->aI1 = c->aI1; kc->aI2 = c->aI2; kc->wE = c->wE; kc->wR = c->wR;
         kc->filter_sigma = c->filter_sigma;
         kc->relax = c->relax;
-        kc->fused_on = c->fused_on; kc->persist = c->persist;
         kc->scheme = c->scheme; kc->x_stages = c->x_stages;
-        kc->picard = c->picard; kc->wb = c->wb; kc->pdl = c->pdl;
+        kc->picard = c->picard; kc->wb = c->wb;
         kc->cl_mode = c->cl_mode; kc->clC = c->clC; kc->clT = c->clT;
         kc->ws = c->ws;
         for (int bi = 0; bi < 3; bi++)
@@ -818,7 +757,7 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         kc->done = (unsigned int *)(q + 4);
         kc->steps = (long long *)(q + 8);
         kc->rho_obs = (unsigned long long *)(q + 16);
-        kc->work = (unsigned int *)(q + 32);
+        kc->kmin = (unsigned int *)(q + 64);
         q += 256;
         kc->ctrl = (Ctrl *)q;
         q += 256;
@@ -921,6 +860,7 @@ const char *hsgn_status_string(hsgn_status s)
     case HSGN_E_CUDA: return "CUDA error";
     case HSGN_E_OVERLAP: return "tile overlap too short for the depth-solve decay";
     case HSGN_E_NOWORKSPACE: return "workspace missing or too small";
+    case HSGN_E_COMM: return "NCCL communication error (slab transport)";
     }
     return "unknown status";
 }
@@ -942,7 +882,6 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     c->desc = *d;
     c->slab = slab;
     c->stream = (cudaStream_t)stream;
-    if (const char *e = std::getenv("HSGN_PDL")) c->pdl = std::atoi(e) != 0;
     cudaGetDevice(&c->device);
     c->n = int(d->n_cells);
     c->members = d->n_members;
@@ -968,16 +907,6 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_kernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
-    cudaFuncSetAttribute(stage_pkernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<true, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
-    cudaFuncSetAttribute(stage_pkernel<false, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC));
     cudaFuncSetAttribute(stage_kernel<false, false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC_B));
     cudaFuncSetAttribute(stage_kernel<true, true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_PIC));
@@ -995,10 +924,6 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(explicit_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
     cudaFuncSetAttribute(explicit_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(XSMEM_BYTES));
-    cudaFuncSetAttribute(step_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
-    cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
-    cudaFuncSetAttribute(step_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
-    cudaFuncSetAttribute(step_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FUSED_SMEM_MAX));
     cl_attrs<false, false, false>(); cl_attrs<false, false, true>();
     cl_attrs<true, true, false>(); cl_attrs<true, true, true>();
     cl_attrs<false, true, false>(); cl_attrs<false, true, true>();
@@ -1074,7 +999,7 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     c->done = (unsigned int *)(q + 4);
     c->steps = (long long *)(q + 8);
     c->rho_obs = (unsigned long long *)(q + 16);
-    c->work = (unsigned int *)(q + 32);
+    c->kmin = (unsigned int *)(q + 64);
     q += 256;
     c->ctrl = (Ctrl *)q;
     q += 256;
@@ -1199,7 +1124,7 @@ hsgn_status hsgn_set_state(hsgn_ctx *c, const double *h, const double *q, const 
     c->dev_steps = 0;
     CUDA_TRY(c, cudaMemsetAsync(c->dt, 0, c->members * sizeof(double), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->maxes, 0, 6 * size_t(c->members) * 8, c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->err, 0, 48, c->stream));   // err, done, steps, rho_obs, work
+    CUDA_TRY(c, cudaMemsetAsync(c->err, 0, 72, c->stream));   // err, done, steps, rho_obs, kmin
     dim3 grid(c->tiles, c->members);
     reduce_kernel<<<grid, NT, 0, c->stream>>>(c->buf[0][0], c->buf[0][1], c->buf[0][2],
                                               c->bathy ? c->b : nullptr, c->lamd, c->n, c->T, c->g,
@@ -1476,23 +1401,42 @@ hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
     d.min_h = 1e300;
     d.t_min = 1e300; d.t_max = -1e300; d.dt_last_min = 1e300; d.dt_last_max = -1e300;
     for (int m = 0; m < c->members; m++) {
-        double mass = 0.0;
+        double mass = 0.0, um = 0.0, nm = 0.0;
         for (int j = 0; j < c->tiles; j++) {
             const double *p = &part[(size_t(m) * c->tiles + j) * 4];
             mass += p[0];
             d.min_h = std::min(d.min_h, p[1]);
-            d.max_abs_u = std::max(d.max_abs_u, p[2]);
-            d.nu_max = std::max(d.nu_max, p[3]);
+            um = std::max(um, p[2]);
+            nm = std::max(nm, p[3]);
         }
+        d.max_abs_u = std::max(d.max_abs_u, um);
+        d.nu_max = std::max(d.nu_max, nm);
+        // achieved Courant numbers of the step about to be taken:
+        // its dt (set from this state) against this state's maxima
+        d.cfl_imex = std::max(d.cfl_imex, dv[m] * nm / c->dx);
+        d.mcfl = std::max(d.mcfl, dv[m] * um / c->dx);
         d.mass += mass * c->dx;
         d.t_min = std::min(d.t_min, tv[m]); d.t_max = std::max(d.t_max, tv[m]);
         d.dt_last_min = std::min(d.dt_last_min, dv[m]); d.dt_last_max = std::max(d.dt_last_max, dv[m]);
     }
     unsigned long long rb = 0;
+    unsigned int kb = 0;
     CUDA_TRY(c, cudaMemcpy(&rb, c->rho_obs, sizeof(rb), cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(&kb, c->kmin, sizeof(kb), cudaMemcpyDeviceToHost));
     double rmx;
     memcpy(&rmx, &rb, sizeof(rmx));
     d.rho_max = rmx;
+    // min kappa: ~kb is the ordered key of the high word (hsgn_kernels.cuh
+    // khi_key); the value is that high word with a zero low word, i.e. the
+    // minimum rounded toward zero to 2^-20 relative (0: no SI stage -> +inf)
+    if (kb == 0) {
+        d.min_kappa = HUGE_VAL;
+    } else {
+        const int key = int(~kb);
+        const int hi = key >= 0 ? key : (key ^ 0x7fffffff);
+        const unsigned long long b = (unsigned long long)(unsigned int)hi << 32;
+        memcpy(&d.min_kappa, &b, sizeof(b));
+    }
     d.steps = dsteps;
     d.error_bits = int32_t(bits);
     *o = d;
@@ -1500,17 +1444,6 @@ hsgn_status hsgn_get_diagnostics(hsgn_ctx *c, hsgn_diag *o)
 }
 
 int64_t hsgn_launch_count(const hsgn_ctx *c) { return c ? c->launches : 0; }
-
-hsgn_status hsgn_set_fused(hsgn_ctx *c, int32_t on)
-{
-    if (!c) return HSGN_E_INVALID;
-    c->fused_on = on != 0;
-    drop_graphs(c);
-    choose_geometry(c);
-    return HSGN_OK;
-}
-
-int32_t hsgn_get_fused(const hsgn_ctx *c) { return c ? (c->fused ? 1 : 0) : -1; }
 
 hsgn_status hsgn_set_scheme(hsgn_ctx *c, int32_t scheme, int32_t stages)
 {
@@ -1572,14 +1505,6 @@ int32_t hsgn_get_cluster(const hsgn_ctx *c, int32_t *ctas, int32_t *tile_rows)
     if (ctas) *ctas = on ? c->clC : 0;
     if (tile_rows) *tile_rows = on ? c->clT : 0;
     return on ? 1 : 0;
-}
-
-hsgn_status hsgn_set_persistent(hsgn_ctx *c, int32_t on)
-{
-    if (!c) return HSGN_E_INVALID;
-    c->persist = on != 0;
-    drop_graphs(c);
-    return HSGN_OK;
 }
 
 #if HSGN_EXP_TIMING

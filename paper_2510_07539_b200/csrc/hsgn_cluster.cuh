@@ -105,8 +105,39 @@ __device__ __forceinline__ void st_remote(const void *dst, const void *mbar, uns
                  ::"r"(a), "l"((unsigned long long)__double_as_longlong(v)), "r"(b) : "memory");
 }
 
-__shared__ __align__(8) unsigned long long s_xmb;   // separator data received (12 C doubles)
+__shared__ __align__(8) unsigned long long s_xmb;   // separator data received from the near CTAs
+__shared__ __align__(8) unsigned long long s_xmb2;  // ... from the others (the coupled case only)
 __shared__ __align__(8) unsigned long long s_fmb;   // filter halo rows received
+
+// Separator data routing.  Equation j needs the OWN part (values 0..5) of CTA
+// j and the LEFT part (values 6..11) of CTA j+1; a CTA c needs equations
+// c-1, c, c+1 (and the left part of c+1 for its halo row T), i.e. own parts of
+// CTAs c-1 .. c+1 and left parts of c .. c+2.  part = -1: own, 0: left.
+__device__ __forceinline__ bool cl_is_near(int s, int r, int C, bool cyc, int part)
+{
+    // sender s -> receiver r: own near iff s - r in {-1, 0, 1}; left iff s - r in {0, 1, 2}
+    // (mod C for periodic members, C a power of two)
+    if (cyc) {
+        if (C <= 3) return true;
+        const int d = (s - r - part) & (C - 1);
+        return d <= 2;
+    }
+    const int d = s - r - part;
+    return d >= 0 && d <= 2;
+}
+
+// number of distinct near senders of receiver c for a part (see cl_is_near)
+__device__ __forceinline__ int cl_near_count(int c, int C, bool cyc, int part)
+{
+    if (cyc) return C < 3 ? C : 3;
+    const int lo = max(c + part, 0), hi = min(c + part + 2, C - 1);
+    return hi >= lo ? hi - lo + 1 : 0;
+}
+
+__device__ __forceinline__ double cl_pick6(const double (&v)[6], int k)
+{
+    return k == 0 ? v[0] : k == 1 ? v[1] : k == 2 ? v[2] : k == 3 ? v[3] : k == 4 ? v[4] : v[5];
+}
 
 // Predictor (A9) and coefficients at E (A2) of one row r
 // of the swizzled tile; same arithmetic as row_update (hsgn_kernels.cuh).
@@ -218,6 +249,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     const bool cyc = P.bcl == BC_PERIODIC;
     const bool left_phys = !cyc && c == 0, right_phys = !cyc && c == C - 1;
     const unsigned xmb = (unsigned)__cvta_generic_to_shared(&s_xmb);
+    const unsigned xmb2 = (unsigned)__cvta_generic_to_shared(&s_xmb2);
     const unsigned fmb = (unsigned)__cvta_generic_to_shared(&s_fmb);
     double *const A0 = sm, *const A1 = sm + CARR, *const A2 = sm + 2 * CARR, *const A3 = sm + 3 * CARR;
     double *const A4 = sm + 4 * CARR, *const A5 = sm + 5 * CARR, *const A6 = sm + 6 * CARR;
@@ -239,11 +271,15 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     // R of rows -1 and Tc goes to s_rh for the threads computing those rows.
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xmb) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xmb2) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fmb) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        // separator data: XPUB doubles from each of the C CTAs (incl. this one)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xmb),
-                     "r"(unsigned(XPUB * C) * 8u) : "memory");
+        // separator data: XPUB doubles from each of the C CTAs (incl. this one),
+        // the parts the three equations c-1, c, c+1 need on xmb, the rest on xmb2
+        const unsigned nb = 48u * unsigned(cl_near_count(c, C, cyc, -1) + cl_near_count(c, C, cyc, 0));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xmb), "r"(nb) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xmb2),
+                     "r"(unsigned(XPUB * C) * 8u - nb) : "memory");
         // filter halo: rows Tc, Tc+1 (q, W) from the right neighbour, -2, -1 from the left
         const unsigned fbytes = filt ? (left_phys ? 0u : 32u) + (right_phys ? 0u : 32u) : 0u;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fmb), "r"(fbytes) : "memory");
@@ -427,6 +463,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 cl_row_update<BATHY>(Cx, sB, r, ch, cq, cH, cW, Fl, Fr, sQd, sHd, sBe, sDe, wd[i], beta, hRv[i]);
                 if (!(beta > 0.0)) acc.err |= ERR_COERC;           // kappa > 0
                 acc.bhi = max(acc.bhi, __double2hiint(beta));
+                acc.kkey = min(acc.kkey, khi_key(beta));
                 Fl = Fr;
             }
         } else {
@@ -596,7 +633,9 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 v6[4] = __shfl_sync(0xffffffffu, V_, 0); v6[5] = __shfl_sync(0xffffffffu, W_, 0);
                 for (int i = lane; i < 6 * C; i += 32) {
                     const int rk = i / 6, k = i - rk * 6;
-                    st_remote(&s_cx[c][6 + k], &s_xmb, unsigned(rk), v6[k]);
+                    const bool nr = cl_is_near(c, rk, C, cyc, 0);       // left part: receivers c-2 .. c
+                    st_remote(&s_cx[c][6 + k], nr ? (const void *)&s_xmb : (const void *)&s_xmb2, unsigned(rk),
+                              cl_pick6(v6, k));
                 }
             }
             if (wid == (ks >> 5)) {
@@ -606,62 +645,78 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 v6[3] = Yks; v6[4] = Vks; v6[5] = Wks;
                 for (int i = lane; i < 6 * C; i += 32) {
                     const int rk = i / 6, k = i - rk * 6;
-                    st_remote(&s_cx[c][k], &s_xmb, unsigned(rk), v6[k]);
+                    const bool nr = cl_is_near(c, rk, C, cyc, -1);      // own part: receivers c-1 .. c+1
+                    st_remote(&s_cx[c][k], nr ? (const void *)&s_xmb : (const void *)&s_xmb2, unsigned(rk),
+                              cl_pick6(v6, k));
                 }
             }
         }
-        mbar_wait(xmb, 0u);                           // all separator data in s_cx
+        mbar_wait(xmb, 0u);                           // the data of equations c-1, c, c+1
         CL_MARK(6);
-        // separator system, solved redundantly by every warp (lane j < C holds
-        // equation j), PCR over the C lanes
-        double Lj;
-        {
-            double a = 0.0, cc = 0.0, d = 0.0;
-            const int j = lane;
-            if (j < C) {
-                const int jn = (j + 1 < C) ? j + 1 : (cyc ? 0 : -1);
-                const double aEj = s_cx[j][0], cEj = s_cx[j][1], dEj = s_cx[j][2];
-                const double Yp = s_cx[j][3], Vp = s_cx[j][4], Wp = s_cx[j][5];
-                double P1n = 0, Q1n = 0, R1n = 0, Y0 = 0, V0 = 0, W0 = 0;
-                if (jn >= 0) {
-                    P1n = s_cx[jn][6]; Q1n = s_cx[jn][7]; R1n = s_cx[jn][8];
-                    Y0 = s_cx[jn][9]; V0 = s_cx[jn][10]; W0 = s_cx[jn][11];
-                }
-                const double cr = cEj * R1n;
-                const double sub = -aEj * Vp;
-                const double dia = (1.0 - cEj * Q1n) - aEj * Wp + cr * V0;
-                const double sup = cr * W0;
-                const double rhs = dEj - cEj * P1n - aEj * Yp + cr * Y0;
-                const double id = rcp(dia);
-                a = sub * id; cc = sup * id; d = rhs * id;
+        // separator equation j (lane-independent helper): coefficients of
+        // L_{j-1}, L_j, L_{j+1}, normalised by the diagonal
+        auto sep_eq = [&](int j, double &a, double &cc, double &d) {
+            const int jn = (j + 1 < C) ? j + 1 : (cyc ? 0 : -1);
+            const double aEj = s_cx[j][0], cEj = s_cx[j][1], dEj = s_cx[j][2];
+            const double Yp = s_cx[j][3], Vp = s_cx[j][4], Wp = s_cx[j][5];
+            double P1n = 0, Q1n = 0, R1n = 0, Y0 = 0, V0 = 0, W0 = 0;
+            if (jn >= 0) {
+                P1n = s_cx[jn][6]; Q1n = s_cx[jn][7]; R1n = s_cx[jn][8];
+                Y0 = s_cx[jn][9]; V0 = s_cx[jn][10]; W0 = s_cx[jn][11];
             }
+            const double cr = cEj * R1n;
+            const double sub = -aEj * Vp;
+            const double dia = (1.0 - cEj * Q1n) - aEj * Wp + cr * V0;
+            const double sup = cr * W0;
+            const double rhs = dEj - cEj * P1n - aEj * Yp + cr * Y0;
+            const double id = rcp(dia);
+            a = sub * id; cc = sup * id; d = rhs * id;
+        };
+        const int cp_ = (c + 1 < C) ? c + 1 : 0, cm_ = (c > 0) ? c - 1 : C - 1;
+        double Lm = 0.0, Lc, Lp = 0.0;
+        {
             // the couplings of neighbouring separators go through the spike tips
-            // (~ r^T): they are usually decoupled to round-off already (the
-            // in-CTA PCR's stop test): then L_j = d_j, else PCR over the lanes
+            // (~ r^T): usually equations c-1, c, c+1 are decoupled to round-off
+            // (the in-CTA PCR's stop test, 2^-64): then L_j = d_j; otherwise all
+            // C equations are solved by PCR over the lanes of every warp
+            double a = 0.0, cc = 0.0, d = 0.0;
+            const int jj = lane == 0 ? cm_ : lane == 1 ? c : cp_;
+            const bool has = lane < 3 && (lane == 1 || cyc || (lane == 0 ? c > 0 : c + 1 < C));
+            if (has) sep_eq(jj, a, cc, d);
             const bool dec = __all_sync(0xffffffffu, fabs(a) <= 5.421010862427522e-20 &&
                                                          fabs(cc) <= 5.421010862427522e-20);   // 2^-64
-            for (int sd = 1; sd < C && !dec; sd <<= 1) {
-                int jm = j - sd, jp = j + sd;
-                if (cyc) { jm = (jm % C + C) % C; jp = jp % C; }
-                const double am_ = __shfl_sync(0xffffffffu, a, jm & 31), cm_ = __shfl_sync(0xffffffffu, cc, jm & 31);
-                const double dm_ = __shfl_sync(0xffffffffu, d, jm & 31);
-                const double ap_ = __shfl_sync(0xffffffffu, a, jp & 31), cp_ = __shfl_sync(0xffffffffu, cc, jp & 31);
-                const double dp_ = __shfl_sync(0xffffffffu, d, jp & 31);
-                const bool okm = j < C && jm >= 0 && jm < C, okp = j < C && jp >= 0 && jp < C;
-                const double Am = okm ? am_ : 0.0, Cm = okm ? cm_ : 0.0, Dm = okm ? dm_ : 0.0;
-                const double Ap = okp ? ap_ : 0.0, Cp = okp ? cp_ : 0.0, Dp = okp ? dp_ : 0.0;
-                const double ib = rcp(1.0 - a * Cm - cc * Ap);
-                const double na = -a * Am * ib, nc = -cc * Cp * ib;
-                d = (d - a * Dm - cc * Dp) * ib;
-                a = na; cc = nc;
+            if (dec) {
+                Lm = __shfl_sync(0xffffffffu, d, 0);
+                Lc = __shfl_sync(0xffffffffu, d, 1);
+                Lp = __shfl_sync(0xffffffffu, d, 2);
+                if (!(c > 0 || cyc)) Lm = 0.0;
+            } else {
+                mbar_wait(xmb2, 0u);                  // every CTA's data
+                a = cc = d = 0.0;
+                const int j = lane;
+                if (j < C) sep_eq(j, a, cc, d);
+                for (int sd = 1; sd < C; sd <<= 1) {
+                    int jm = j - sd, jp = j + sd;
+                    if (cyc) { jm = (jm % C + C) % C; jp = jp % C; }
+                    const double am_ = __shfl_sync(0xffffffffu, a, jm & 31), cm2 = __shfl_sync(0xffffffffu, cc, jm & 31);
+                    const double dm_ = __shfl_sync(0xffffffffu, d, jm & 31);
+                    const double ap_ = __shfl_sync(0xffffffffu, a, jp & 31), cp2 = __shfl_sync(0xffffffffu, cc, jp & 31);
+                    const double dp_ = __shfl_sync(0xffffffffu, d, jp & 31);
+                    const bool okm = j < C && jm >= 0 && jm < C, okp = j < C && jp >= 0 && jp < C;
+                    const double Am = okm ? am_ : 0.0, Cm = okm ? cm2 : 0.0, Dm = okm ? dm_ : 0.0;
+                    const double Ap = okp ? ap_ : 0.0, Cp = okp ? cp2 : 0.0, Dp = okp ? dp_ : 0.0;
+                    const double ib = rcp(1.0 - a * Cm - cc * Ap);
+                    const double na = -a * Am * ib, nc = -cc * Cp * ib;
+                    d = (d - a * Dm - cc * Dp) * ib;
+                    a = na; cc = nc;
+                }
+                // cyclic: the last level couples each row to itself (stride C == 0 mod C)
+                const double Lj = cyc ? d * rcp(1.0 + a + cc) : d;
+                Lm = (c > 0 || cyc) ? __shfl_sync(0xffffffffu, Lj, cm_) : 0.0;
+                Lc = __shfl_sync(0xffffffffu, Lj, c);
+                Lp = __shfl_sync(0xffffffffu, Lj, cp_);
             }
-            // cyclic: the last level couples each row to itself (stride C == 0 mod C)
-            Lj = (cyc && !dec) ? d * rcp(1.0 + a + cc) : d;
         }
-        const int cp_ = (c + 1 < C) ? c + 1 : 0, cm_ = (c > 0) ? c - 1 : C - 1;
-        const double Lm = (c > 0 || cyc) ? __shfl_sync(0xffffffffu, Lj, cm_) : 0.0;
-        const double Lc = __shfl_sync(0xffffffffu, Lj, c);
-        const double Lp = __shfl_sync(0xffffffffu, Lj, cp_);
         // chunk ends: X_k = Y_k - V_k L_{j-1} - W_k L_j (interior), X_ks = L_j
         const double Xk = tid < ks ? D_ - V_ * Lm - W_ * Lc : (tid == ks ? Lc : 0.0);
         const double XL = tid == 0 ? Lm : Yl - Vl * Lm - Wl * Lc;
@@ -814,6 +869,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     }
     CL_MARK(9);
     tile_epilogue<FINAL>(P, c, m, dtm, acc, tm0, tend0);
+    mbar_wait(xmb2, 0u);                              // no remote store may target an exited CTA
 #if HSGN_EXP_TIMING
     CL_MARK(10);
     if (tid == 0) {

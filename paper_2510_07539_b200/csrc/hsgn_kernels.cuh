@@ -34,21 +34,7 @@
 #ifndef HSGN_MINB
 #define HSGN_MINB 4
 #endif
-// Timing experiments only (never in the product build): skip the global loads
-// or stores of the stage kernel and ignore its error checks.
-#ifndef HSGN_EXP_NOLOAD
-#define HSGN_EXP_NOLOAD 0
-#endif
-#ifndef HSGN_EXP_NOSTORE
-#define HSGN_EXP_NOSTORE 0
-#endif
-#ifndef HSGN_EXP_NOPREFETCH            // persistent kernel loads each item at its start
-#define HSGN_EXP_NOPREFETCH 0
-#endif
-#ifndef HSGN_STORE_DIRECT               // stage kernels: coalesced STG from staging, no TMA store
-#define HSGN_STORE_DIRECT 0
-#endif
-#ifndef HSGN_EXP_TIMING                 // per-CTA phase clocks (hsgn_exp_counters)
+#ifndef HSGN_EXP_TIMING                 // dev builds only: per-CTA phase clocks (tools/*timing.py)
 #define HSGN_EXP_TIMING 0
 #endif
 
@@ -71,13 +57,6 @@ constexpr size_t SMEM_BYTES_B = SMEM_BYTES + size_t(SROWS) * sizeof(double);
 // Picard kernels (A24): alpha, a^2 of the own rows in two more arrays
 constexpr size_t SMEM_BYTES_PIC = SMEM_BYTES + size_t(2 * SROWS) * sizeof(double);
 constexpr size_t SMEM_BYTES_PIC_B = SMEM_BYTES_B + size_t(2 * SROWS) * sizeof(double);
-// fused step kernel: + a dedicated output staging buffer of 4 x T doubles
-// (T <= LCAP), so a tile's bulk store overlaps the next tile's compute
-__host__ __device__ constexpr size_t fused_smem_bytes(int T)
-{
-    return SMEM_BYTES + size_t(4) * size_t((T + 1) & ~1) * sizeof(double);
-}
-constexpr size_t FUSED_SMEM_MAX = SMEM_BYTES + size_t(4) * LCAP * sizeof(double);
 
 enum { BC_PERIODIC = 0, BC_WALL = 1, BC_TRANSMISSIVE = 2, BC_HALO = 3 };
 enum { ERR_COERC = 1u, ERR_DRY = 2u, ERR_NONFINITE = 4u, ERR_OVERLAP = 8u, ERR_DT = 16u };
@@ -103,8 +82,7 @@ struct Params {
     long long *steps;
     unsigned int *done;
     unsigned long long *rho_obs;     // max rho over tiles (double bits)
-    unsigned int *work;              // [2 parities][2 stages] item counters of the
-                                     // persistent kernels (zeroed by dt_commit_kernel)
+    unsigned int *kmin;              // min kappa = beta seen: max of ~khi_key (see khi_key)
     const Ctrl *ctrl;
     int kslot, kpar;                 // host step index k: k mod 3, k mod 2
     // slab decomposition (BC_HALO sides): ghost cells received from the
@@ -112,9 +90,6 @@ struct Params {
     const double *halo_l[9];
     const double *halo_r[9];
     int H;
-    // L2 prefetch distance of the standalone stage kernel, in CTAs (~ CTAs
-    // resident at once); 0: off
-    int pf_dist;
     double inv_tiles;                // 1 / tiles
     double rho_ok;                   // largest rho whose decay r(rho)^w <= 2^-60 (overlap check)
     int picard;                      // A24 Picard passes (stage_kernel<..., PIC = true>)
@@ -158,10 +133,8 @@ extern __shared__ __align__(16) double hsgn_smem[];
 __shared__ __align__(8) unsigned long long s_mbar;
 __shared__ double s_red[2][NT / 32];
 __shared__ float s_redf[NT / 32];
+__shared__ int s_redk[NT / 32];
 __shared__ double s_xch[NT / 32][3];
-__shared__ double s_rc[2];            // persistent kernels: dt, lambda of the next item
-__shared__ unsigned int s_err;        // persistent kernels: error word seen at its prefetch
-__shared__ int s_item[2];             // persistent kernels: current, next item
 
 __device__ __forceinline__ double *dyn_smem() { return hsgn_smem; }
 
@@ -193,12 +166,6 @@ __device__ __forceinline__ void bulk_s2g(double *dst, const double *src_smem, un
     const unsigned a = (unsigned)__cvta_generic_to_shared(src_smem);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
                  ::"l"(dst), "r"(a), "r"(bytes) : "memory");
-}
-
-// Bulk prefetch of a global range into L2 (16-B aligned, size a multiple of 16).
-__device__ __forceinline__ void prefetch_l2(const double *src, unsigned bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned parity)
@@ -512,28 +479,6 @@ __device__ __forceinline__ Geom stage_geom(const Params &P, int s, int e, int w)
     return G;
 }
 
-// Fused step: stage-2 tile G2 of kept cells [s, e); stage-1 tile G1 delivering
-// U1 on G2's raw rows (cells start2-3 .. start2+L2+2, minus the ghost rows at a
-// physical end, which are mirrored from the tile afterwards).
-__device__ __forceinline__ void fused_geom(const Params &P, int s, int e, int w, Geom &G1, Geom &G2)
-{
-    const bool physL = (P.bcl == BC_WALL || P.bcl == BC_TRANSMISSIVE);
-    const bool physR = (P.bcr == BC_WALL || P.bcr == BC_TRANSMISSIVE);
-    G2 = stage_geom(P, s, e, w);
-    const int a1 = G2.left_phys ? G2.start : G2.start - 3;
-    const int b1 = G2.right_phys ? G2.start + G2.L : G2.start + G2.L + 3;
-    G1.wl = physL ? min(w, a1) : w;
-    G1.wr = physR ? min(w, P.n - b1) : w;
-    G1.start = a1 - G1.wl;
-    G1.L = (b1 - a1) + G1.wl + G1.wr;
-    G1.klo = G1.wl;
-    G1.khi = G1.wl + (b1 - a1);
-    G1.left_phys = physL && (G1.start == 0);
-    G1.right_phys = physR && (G1.start + G1.L == P.n);
-    G1.interior = (G1.start - 3 >= 0) && (G1.start + G1.L + 3 <= P.n);
-    G1.abase = 3;
-}
-
 // TMA bulk loads need 16-B aligned destinations: shift the arrays by the parity
 // of the first copied cell.  Interior tiles copy one range per field; tiles that
 // wrap around a periodic domain of even n copy two (cells a0 .. n-1, then
@@ -576,7 +521,6 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
                                            const LoadPlan &Lp, unsigned mb, int tid)
 {
     double *const smem = dyn_smem();
-    if (HSGN_EXP_NOLOAD) return;
     constexpr bool DO_UN = PART != LD_U1;
     constexpr bool DO_U1 = WITH_U1 && PART != LD_UN;
     // b rides the TMA copies when its source is 16-B aligned too (a0 even: b has
@@ -669,7 +613,6 @@ __device__ __forceinline__ void issue_load(const Params &P, const Bufs &B, size_
 // Wait for the loads issued by issue_load (bulk: mbarrier phase parity).
 __device__ __forceinline__ void wait_load(const LoadPlan &Lp, unsigned mb, unsigned &parity)
 {
-    if (HSGN_EXP_NOLOAD) return;
     if (Lp.bulk) {
         mbar_wait(mb, parity);
         parity ^= 1u;
@@ -701,106 +644,36 @@ __device__ __forceinline__ StageC stage_consts(const Params &P, double aii, doub
     return S;
 }
 
-// Accumulators of one tile (both stages of a fused step).
+// Accumulators of one tile.
 struct TileAcc {
     double umax, numax, rho;
     unsigned int err;
     int wmin;                     // narrowest truncated overlap (1 << 30: none)
     int bhi;                      // max high word of beta over the rows (rho bound)
+    int kkey = 0x7fffffff;        // min beta (= kappa) over the rows, as khi_key of its
+                                  // high word (coercivity monitor, to 2^-20 relative)
 };
 
-enum { MODE_ALONE = 0, MODE_FUSED = 1, MODE_PERSIST = 2 };
-
-__device__ __forceinline__ void item_tile(const Params &P, int item, int &j, int &m, int &s, int &e)
+// Order-preserving integer key of the high word of a double (signed order of
+// the key = numeric order of the value); the device accumulator keeps ~key
+// under atomicMax, so 0 (memset) is "no value yet".
+__device__ __forceinline__ int khi_key(double v)
 {
-    // item / tiles through the reciprocal (exact after the +-1 correction)
-    m = __double2int_rz(double(item) * P.inv_tiles);
-    if (m * P.tiles > item) m--;
-    else if ((m + 1) * P.tiles <= item) m++;
-    j = item - m * P.tiles;
-    s = j * P.T;
-    e = min(P.n, s + P.T);
-}
-
-// Output staging of a final stage: arrays 4..7 (standalone kernel) or the
-// dedicated buffer of the fused kernel (4 x even(T) doubles after the arrays).
-__device__ __forceinline__ void stage_ptrs(bool dedicated, int T, double *&oh, double *&oq, double *&oK,
-                                           double *&oW)
-{
-    double *const smem = dyn_smem();
-    if (dedicated) {
-        const int TS = (T + 1) & ~1;
-        oh = smem + NARR * SROWS; oq = oh + TS; oK = oq + TS; oW = oK + TS;
-    } else {
-        oh = smem + 4 * SROWS; oq = smem + 5 * SROWS; oK = smem + 6 * SROWS; oW = smem + 7 * SROWS;
-    }
-}
-
-// Issue the U^n loads of a fused-step item (its stage-1 tile).
-__device__ __forceinline__ void prefetch_item(const Params &P, const Bufs &B, int item)
-{
-    int j, m, s, e;
-    item_tile(P, item, j, m, s, e);
-    Geom G1, G2;
-    fused_geom(P, s, e, P.w, G1, G2);
-    const size_t mo = size_t(m) * P.n;
-    const LoadPlan Lp = load_plan(P, mo, G1);
-    issue_load<false>(P, B, mo, G1, Lp, (unsigned)__cvta_generic_to_shared(&s_mbar), threadIdx.x);
-    if (threadIdx.x == 0) { s_rc[0] = P.dt[m]; s_rc[1] = P.lam[m]; }
-}
-
-
-// Persistent stage kernel: item -> kept cells and its stage tile.
-__device__ __forceinline__ void stage_item(const Params &P, int item, int &j, int &m, int &s, int &e,
-                                           Geom &G, size_t &mo, LoadPlan &Lp)
-{
-    item_tile(P, item, j, m, s, e);
-    G = stage_geom(P, s, e, P.w);
-    mo = size_t(m) * P.n;
-    Lp = load_plan(P, mo, G);
-}
-
-// Issue loads of a persistent-stage item (PART of its inputs) and, with the
-// U^n part, fetch its run control (dt, lambda) into s_rc.
-template <bool STAGE2, int PART>
-__device__ __forceinline__ void prefetch_stage_item(const Params &P, const Bufs &B, int item)
-{
-    int j, m, s, e;
-    Geom G;
-    size_t mo;
-    LoadPlan Lp;
-    stage_item(P, item, j, m, s, e, G, mo, Lp);
-    issue_load<STAGE2, PART>(P, B, mo, G, Lp, (unsigned)__cvta_generic_to_shared(&s_mbar), threadIdx.x);
-    if (PART != LD_U1 && threadIdx.x == 0) {       // async: no wait on the critical path
-        cp_async8(&s_rc[0], P.dt + m);
-        cp_async8(&s_rc[1], P.lam + m);
-        const unsigned a = (unsigned)__cvta_generic_to_shared(&s_err);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(a), "l"(P.err) : "memory");
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
+    const int hi = __double2hiint(v);
+    return hi >= 0 ? hi : (hi ^ 0x7fffffff);
 }
 
 // ---------------------------------------------------------------------------
 // One IMEX stage S(E, R, tau) on the tile G, data already in
-// shared memory.  MODE_ALONE: raw U^n (and U1) rows as loaded, output K-form
-// staged at arrays 4..7 (h, q, K, W) index r - klo for the bulk store.
-// MODE_FUSED, rt2 = false: stage 1 of a fused step, output U1 in H-form
-// (H = K - 1.5 h b) into arrays 7, 4, 5, 6 (h, q, H, W) at the cells' own
-// positions.  MODE_FUSED, rt2 = true: stage 2 of a fused step on U^n (H-form,
-// parities applied) and that U1; output staged in the dedicated buffer.  Once the arrays 0..3 are no longer read, the
-// loads of U^n for next_item (>= 0) are issued into them (prefetch).
+// shared memory: raw U^n (and U1) rows as loaded, output K-form staged at
+// arrays 4..7 (h, q, K, W) index r - klo for the bulk store.
 // ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, int MODE, bool PIC = false, bool WB = false>
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, bool PIC = false, bool WB = false>
 __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const Geom &G, int m, int s_cell,
-                                           const StageC &S, double dtm, TileAcc &acc, int next_item,
-                                           bool rt2)
+                                           const StageC &S, double dtm, TileAcc &acc)
 {
-    // MODE_FUSED: one copy of the code serves both stages of the fused step
-    // (rt2 = stage 2), keeping the kernel inside the instruction cache
-    const bool st2 = (MODE == MODE_FUSED) ? rt2 : STAGE2;
-    const bool fin = (MODE == MODE_FUSED) ? rt2 : FINAL;
-    const bool fused1 = (MODE == MODE_FUSED) && !rt2;
-    const bool fused2 = (MODE == MODE_FUSED) && rt2;
+    const bool st2 = STAGE2;
+    const bool fin = FINAL;
     double *const smem = dyn_smem();
     const int tid = threadIdx.x;
     const int n = P.n;
@@ -813,10 +686,8 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     double *sBe = A + 6 * SROWS;   // U1_W -> R_W -> beta -> hbar
     double *sDe = A + 7 * SROWS;   // U1_h -> R_h -> delta (R_h read by its own row first)
     // b of the raw rows -3 .. L+2 (one-CTA-per-tile kernels: array 8, loaded with the tile)
-    const double *const sBz = (MODE == MODE_ALONE && BATHY) ? A + 8 * SROWS : nullptr;
-    auto bz = [&](int r) -> double {
-        return (MODE == MODE_ALONE && BATHY) ? sBz[r] : bathy_at(P, G.start + r);
-    };
+    const double *const sBz = BATHY ? A + 8 * SROWS : nullptr;
+    auto bz = [&](int r) -> double { return sBz[r]; };
     const double tau = S.tau, g = S.g, idx1 = S.idx1, tdx = S.tdx, tdx2 = S.tdx2, t2 = S.t2;
     const double t2h = S.t2h, lt2 = S.lt2, lt2h = S.lt2h, ltdx2 = S.ltdx2, lam = S.lam;
     const double lam3 = S.lam3, ltau = S.ltau;
@@ -824,7 +695,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
 
     // ---- in-place pass: E, R, H = K - 1.5 h b (A9), wall parity
     {
-        const bool raw = !fused2;                     // inputs not yet in H-form / parity
+        const bool raw = true;                        // inputs not yet in H-form / parity
         // q parity of ghost rows mirrored at a wall (raw rows outside [0, n))
         const bool wall_par = raw && !G.interior && (P.bcl == BC_WALL || P.bcr == BC_WALL);
         if (st2 || (raw && BATHY) || wall_par) {
@@ -947,6 +818,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             // of the overlap check from max beta (high words: +1 ulp of 2^-20)
             if (!(beta > 0.0)) acc.err |= ERR_COERC;
             acc.bhi = max(acc.bhi, __double2hiint(beta));
+            if (r < L) acc.kkey = min(acc.kkey, khi_key(beta));
             Fl = Fr;
         }
     } else {
@@ -955,10 +827,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     }
     __syncthreads();
     EXP_MARK(0);
-    // persistent kernel without bathymetry: arrays 0..3 (E) are not read after
-    // phase 1, so the next item's U^n loads can start now
-    if (MODE == MODE_PERSIST && !HSGN_EXP_NOPREFETCH && !BATHY && next_item >= 0)
-        prefetch_stage_item<STAGE2, STAGE2 ? LD_UN : LD_ALL>(P, B, next_item);
     // derived-field ghosts at physical boundaries (A10).  The implicit
     // coupling across both tile ends is cut (truncated overlap or Neumann end:
     // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
@@ -990,18 +858,13 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     __syncthreads();
 
     // ---- phase 2: assemble + partition solve (A1, A3) ---------
-    // Standalone: arrays 1..3 are free after phase 1: hbar in array 1, PCR
-    // buffers over arrays 2..3 (later the filter buffers), E_h stays in array 0;
-    // arrays 4..7 take the output staging during phase 3.
-    // Fused: arrays 0..3 take the next tile's prefetch, so after the window
-    // loads PCR goes over arrays 4..5 (later the filter), hbar into array 6 and
-    // the own rows' E_h (BATHY) are copied to array 7.
-    constexpr bool ALONE = (MODE == MODE_ALONE);
-    static_assert(!WB || ALONE, "A25 reads E_h of rows r +- 1 from array 0 (one CTA per tile)");
-    double *sHB = ALONE ? sEq : sBe;                             // hbar[r], r in [0, L)
-    double *pcr0 = ALONE ? smem + 2 * SROWS : smem + 4 * SROWS;  // 2 x 3 x NT doubles
+    // Arrays 1..3 are free after phase 1: hbar in array 1, PCR buffers over
+    // arrays 2..3 (later the filter buffers), E_h stays in array 0; arrays
+    // 4..7 take the output staging during phase 3.
+    double *sHB = sEq;                                           // hbar[r], r in [0, L)
+    double *pcr0 = smem + 2 * SROWS;                             // 2 x 3 x NT doubles
     double *pcr1 = pcr0 + 3 * NT;
-    double *sEhc = ALONE ? sEh : sDe;                            // E_h (BATHY)
+    double *sEhc = sEh;                                          // E_h (BATHY)
     // register windows over rows r0-1 .. r0+MCH
     double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
     if (live) {
@@ -1048,6 +911,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 const double be = a2 + lam * al * b2 * vH[i + 1];
                 if (r >= G.klo && r < G.khi && !(be > 0.0)) acc.err |= ERR_COERC;
                 acc.bhi = max(acc.bhi, __double2hiint(be));
+                acc.kkey = min(acc.kkey, khi_key(be));
                 sBe[r] = be;
                 sDe[r] = al / b1;
             }
@@ -1106,10 +970,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             if (wid + 1 < NT / 32) { P1 = s_xch[wid + 1][0]; Q1 = s_xch[wid + 1][1]; R1 = s_xch[wid + 1][2]; }
             else { P1 = 0.0; Q1 = 0.0; R1 = 0.0; }
         }
-        if (BATHY && !ALONE && live) {
-#pragma unroll
-            for (int i = 0; i < MCH; i++) sEhc[r0 + i] = sEh[r0 + i];
-        }
         // reduced row k:  A X_{k-1} + Bd X_k + C X_{k+1} = D, normalised by Bd
         double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1;
         if (tid == 0) A_ = 0.0;
@@ -1128,9 +988,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             if (lane == 0) s_redf[wid] = ev;
         }
         __syncthreads();
-        if (fused2 && next_item >= 0) prefetch_item(P, B, next_item);   // arrays 0..3 free
-        if (MODE == MODE_PERSIST && !HSGN_EXP_NOPREFETCH && BATHY && next_item >= 0)   // (after the E_h copies)
-            prefetch_stage_item<STAGE2, STAGE2 ? LD_UN : LD_ALL>(P, B, next_item);
         int lim = NT;
         {
             float e0 = 0.0f;
@@ -1191,7 +1048,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
 
     // ---- phase 3: back-substitution, own rows ------------------
     const bool filt = fin && (P.filter_sigma > 0.0);
-    double *sQb = (ALONE ? smem + 2 * SROWS : smem + 4 * SROWS) + G.abase;   // filter (A19)
+    double *sQb = smem + 2 * SROWS + G.abase;                   // filter (A19)
     double *sWb = sQb + SROWS;
     const int klo = G.klo, khi = G.khi;
     const int flo = filt ? klo - 2 : klo, fhi = filt ? khi + 2 : khi;
@@ -1315,7 +1172,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         }
         double h0 = hb[i];
         const double Hb = HdD[i] * (h0 * h0);
-        double Ko = (BATHY && !fused1) ? Hb + 1.5 * h0 * bbv[i] : Hb;
+        double Ko = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
         if (fin && RELAX) {
             relax_cell(P, P.x_min + (double(s_cell + (r - klo)) + 0.5) * P.dx, bbv[i], t_new, h0, qo, Ko, wo);
             const double Hf = Ko - 1.5 * h0 * bbv[i];
@@ -1331,49 +1188,10 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             acc.numax = nu > acc.numax ? nu : acc.numax;
         }
         hb[i] = h0; qbv[i] = qo; HdD[i] = Ko; Wbv[i] = wo;
-        if (ALONE) {          // staging arrays 4..7 are not read in this phase
+        {                     // staging arrays 4..7 are not read in this phase
             const int ko = r - klo;
             smem[4 * SROWS + ko] = h0; smem[5 * SROWS + ko] = qo;
             smem[6 * SROWS + ko] = Ko; smem[7 * SROWS + ko] = wo;
-        }
-    }
-    if (ALONE) {
-        // (staged; store_tile synchronises)
-    } else if (MODE == MODE_PERSIST) {
-        // staged at arrays 4..7 once hbar (6) and the filter (4, 5) are read;
-        // the caller bulk-stores them (direct per-thread stores measured slower)
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < MCH; i++) {
-            const int r = r0 + i;
-            if (r < klo || r >= khi) continue;
-            const int ko = r - klo;
-            smem[4 * SROWS + ko] = hb[i]; smem[5 * SROWS + ko] = qbv[i];
-            smem[6 * SROWS + ko] = HdD[i]; smem[7 * SROWS + ko] = Wbv[i];
-        }
-    } else if (fused1) {
-        __syncthreads();             // hbar, filter and E_h copies all read
-        // U1 (H-form) at the cells' own positions: arrays 7, 4, 5, 6
-#pragma unroll
-        for (int i = 0; i < MCH; i++) {
-            const int r = r0 + i;
-            if (r < klo || r >= khi) continue;
-            A[7 * SROWS + r] = hb[i]; A[4 * SROWS + r] = qbv[i];
-            A[5 * SROWS + r] = HdD[i]; A[6 * SROWS + r] = Wbv[i];
-        }
-    } else {
-        // staged for the bulk store in the dedicated buffer, index r - klo (the
-        // previous tile's bulk store has long read it)
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        __syncthreads();             // hbar, filter and E_h copies all read
-        double *oh, *oq, *oK, *oW;
-        stage_ptrs(true, P.T, oh, oq, oK, oW);
-#pragma unroll
-        for (int i = 0; i < MCH; i++) {
-            const int r = r0 + i;
-            if (r < klo || r >= khi) continue;
-            const int ko = r - klo;
-            oh[ko] = hb[i]; oq[ko] = qbv[i]; oK[ko] = HdD[i]; oW[ko] = Wbv[i];
         }
     }
     // truncated overlap widths for the overlap check
@@ -1383,16 +1201,15 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
 
 // Store the staged rows (arrays 4..7, index 0 .. Tk-1) to out[] at cells
 // [s, s + Tk): bulk (thread 0; read-completion wait deferred) or per element.
-__device__ __forceinline__ void store_tile(const Bufs &B, size_t mo, int s, int Tk, bool dedicated, int T)
+__device__ __forceinline__ void store_tile(const Bufs &B, size_t mo, int s, int Tk)
 {
     const int tid = threadIdx.x;
     const size_t gdst = mo + size_t(s);
-    const bool bulk_out = !HSGN_STORE_DIRECT && ((gdst | size_t(Tk)) & 1) == 0;
-    double *oh, *oq, *oK, *oW;
-    stage_ptrs(dedicated, T, oh, oq, oK, oW);
-    if (HSGN_EXP_NOSTORE) {
-        __syncthreads();
-    } else if (bulk_out) {
+    const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
+    double *const smem = dyn_smem();
+    double *const oh = smem + 4 * SROWS, *const oq = smem + 5 * SROWS, *const oK = smem + 6 * SROWS,
+                 *const oW = smem + 7 * SROWS;
+    if (bulk_out) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
         if (tid == 0) {
@@ -1444,21 +1261,23 @@ __device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, dou
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     const int members = P.members;
-    const bool exp_off = HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE;
-    const unsigned int eb = exp_off ? 0u : __reduce_or_sync(0xffffffffu, acc.err);
+    const unsigned int eb = __reduce_or_sync(0xffffffffu, acc.err);
     if (lane == 0 && eb) { atomicOr(P.err, eb); __threadfence(); }
     double um = 0.0, nm = 0.0;
     if (FINAL) { um = warp_max_nonneg(acc.umax); nm = warp_max_nonneg(acc.numax); }
     float rf = warp_max_nonneg(float(acc.rho));
+    int km = __reduce_min_sync(0xffffffffu, acc.kkey);
     // (s_red is only used here; s_redf's last reads in phase 2 precede later barriers)
-    if (lane == 0) { s_red[0][wid] = um; s_red[1][wid] = nm; s_redf[wid] = rf; }
+    if (lane == 0) { s_red[0][wid] = um; s_red[1][wid] = nm; s_redf[wid] = rf; s_redk[wid] = km; }
     __syncthreads();
     if (tid == 0) {
         for (int q = 1; q < NT / 32; q++) {
             um = s_red[0][q] > um ? s_red[0][q] : um; nm = s_red[1][q] > nm ? s_red[1][q] : nm;
             rf = s_redf[q] > rf ? s_redf[q] : rf;
+            km = min(km, s_redk[q]);
         }
-        if (rf > 0.0f && dtm != 0.0 && !exp_off) {
+        if (km != 0x7fffffff && P.kmin) atomicMax(P.kmin, ~unsigned(km));
+        if (rf > 0.0f && dtm != 0.0) {
             const double rho = double(rf) * (1.0 + 1e-6);
             if (acc.wmin == P.w) {
                 // r(rho)^w <= 2^-60  <=>  rho <= rho_ok = r*/(1 - r*)^2, r* = 2^(-60/w) (host)
@@ -1484,15 +1303,6 @@ __device__ __forceinline__ void tile_epilogue(const Params &P, int j, int m, dou
     }
 }
 
-// Programmatic dependent launch: the step's kernels are launched with the
-// programmatic-serialization attribute (hsgn.cu launch_pdl).  A kernel lets the
-// next one launch once all its CTAs have started (its CTAs then take the SM slots
-// freed by this grid's last wave) and waits for the previous grid's completion
-// and memory before it touches global memory; both are no-ops without the
-// attribute.
-__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-
 __device__ __forceinline__ void init_mbar(unsigned mb)
 {
     if (threadIdx.x == 0) {
@@ -1506,8 +1316,7 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 // Standalone stage kernel: one IMEX stage over every (tile, member) CTA.
 // STAGE2: inputs U^n and U1 (E, R formed on load); FINAL: this stage produces
 // U^{n+1} (filter, relaxation, dt maxima, time level).  The default kernel
-// organisation; the persistent (stage_pkernel) and fused
-// (step_kernel) organisations are opt-in alternatives with the same arithmetic.
+// organisation of the overlapped tiles.
 // ---------------------------------------------------------------------------
 #if HSGN_EXP_TIMING
 #define EXP_T(v) long long v = clock64()
@@ -1535,33 +1344,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    pdl_release();
-    pdl_wait();                      // (no global access above)
     issue_load<STAGE2, LD_ALL, BATHY>(P, B, mo, G, Lp, mb, tid);
     if (Lp.bulk) __syncthreads();
-    // L2 prefetch of the tile of the CTA about one residency wave later, so its
-    // TMA loads hit L2 instead of HBM (no shared memory involved)
-    if (tid == 0 && P.pf_dist > 0 && !HSGN_EXP_NOLOAD) {
-        const long long lin = (long long)m * gridDim.x + j + P.pf_dist;
-        if (lin < (long long)gridDim.x * gridDim.y) {
-            const int jf = int(lin % gridDim.x), mf = int(lin / gridDim.x);
-            const int sf = jf * P.T;
-            Geom Gf = stage_geom(P, sf, min(P.n, sf + P.T), P.w);
-            const size_t mof = size_t(mf) * P.n;
-            const LoadPlan Lf = load_plan(P, mof, Gf);
-            if (Lf.bulk) {
-                const size_t off = mof + size_t(Lf.a0);
-                const unsigned bytes = unsigned(Lf.seg1) * 8u;       // (first range only)
-#pragma unroll
-                for (int f = 0; f < 4; f++) prefetch_l2(B.Un[f] + off, bytes);
-                if (STAGE2) {
-#pragma unroll
-                    for (int f = 0; f < 4; f++) prefetch_l2(B.U1[f] + off, bytes);
-                }
-            }
-        }
-    }
-
     // ---- run control: dt of this member was set by dt_commit_kernel ---------
     const unsigned int err0 = *((volatile unsigned int *)P.err);
     const double dtm = P.dt[m];
@@ -1580,8 +1364,8 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
     } else {
         const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
-        stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_ALONE, PIC, WB>(P, B, G, m, s, S, dtm, acc, -1, false);
-        store_tile(B, mo, s, e - s, false, P.T);
+        stage_body<STAGE2, FINAL, BATHY, RELAX, PIC, WB>(P, B, G, m, s, S, dtm, acc);
+        store_tile(B, mo, s, e - s);
     }
     EXP_T(t2);
     tile_epilogue<FINAL>(P, j, m, dtm, acc, tm0, tend0);
@@ -1602,165 +1386,6 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
         }
     }
 #endif
-}
-
-// ---------------------------------------------------------------------------
-// Persistent stage kernel: the same stage as stage_kernel, but each CTA walks
-// (tile, member) items and prefetches the next item's inputs while it finishes
-// the current one: U^n into arrays 0..3 as soon as phase 2 has its register
-// windows (stage 1: all its inputs); stage 2's U1 into arrays 4..7 once the
-// current item's staged output has been read by its bulk store.
-// ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false>
-__global__ void __launch_bounds__(NT, HSGN_MINB) stage_pkernel(const Params P, const Bufs B, int items)
-{
-    const int tid = threadIdx.x;
-    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
-    // items are handed out by an atomic counter (dynamic balance across SMs);
-    // thread 0 asks for item k+2 while item k runs, so no CTA waits on it
-    unsigned int *ctr = P.work + 2 * P.kpar + (STAGE2 ? 1 : 0);
-    int grab = 0;
-    if (tid == 0) {
-        s_item[0] = int(atomicAdd(ctr, 1u));
-        s_item[1] = int(atomicAdd(ctr, 1u));
-    }
-    init_mbar(mb);                       // (synchronises s_item)
-    int item = s_item[0];
-    if (item >= items) return;
-    unsigned parity = 0u;
-    if (!HSGN_EXP_NOPREFETCH) prefetch_stage_item<STAGE2, LD_ALL>(P, B, item);
-    for (;;) {
-        if (HSGN_EXP_NOPREFETCH) { __syncthreads(); prefetch_stage_item<STAGE2, LD_ALL>(P, B, item); }
-        int j, m, s, e;
-        Geom G;
-        size_t mo;
-        LoadPlan Lp;
-        stage_item(P, item, j, m, s, e, G, mo, Lp);
-        wait_load(Lp, mb, parity);
-        cp_async_wait_all();              // run control (and per-row loads)
-        __syncthreads();
-        const int next = s_item[1];
-        const double dtm = s_rc[0];
-        const double lam = s_rc[1];
-        if (s_err) break;                 // an error was latched (seen at the prefetch)
-        if (tid == 0) grab = int(atomicAdd(ctr, 1u));      // used at the item's end
-        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
-        if (dtm == 0.0) {
-            carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
-            __syncthreads();
-            if (!HSGN_EXP_NOPREFETCH && next < items) prefetch_stage_item<STAGE2, LD_ALL>(P, B, next);
-        } else {
-            const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
-            stage_body<STAGE2, FINAL, BATHY, RELAX, MODE_PERSIST>(P, B, G, m, s, S, dtm, acc,
-                                                                  next < items ? next : -1, false);
-            store_tile(B, mo, s, e - s, false, P.T);
-            if (next < items) {
-                // arrays 4..7 must be read by the bulk store before the next item
-                // writes them (stage 1: phase 1) or loads its U1 into them (stage 2)
-                if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-                if (STAGE2 && !HSGN_EXP_NOPREFETCH) {
-                    __syncthreads();
-                    prefetch_stage_item<STAGE2, LD_U1>(P, B, next);
-                }
-            }
-        }
-        tile_epilogue<FINAL>(P, j, m, dtm, acc);   // (its barriers order the s_item update)
-        if (next >= items) break;
-        if (tid == 0) { s_item[1] = grab; }
-        item = next;
-    }
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-}
-
-// ---------------------------------------------------------------------------
-// Fused two-stage IMEX step (P:500-517 twice, E/R of P:399-401): persistent
-// CTAs walk the (tile, member) items; per item, stage 1 runs on a tile widened
-// by w + 3 cells on each side, its U1 stays in shared memory, stage 2 runs on
-// the inner tile and produces U^{n+1}.  U^n of the next item is prefetched by
-// TMA into arrays 0..3 while stage 2 of the current item finishes.
-// ---------------------------------------------------------------------------
-template <bool BATHY, bool RELAX>
-__global__ void __launch_bounds__(NT, HSGN_MINB) step_kernel(const Params P, const Bufs B, int items)
-{
-    double *const smem = dyn_smem();
-    const int tid = threadIdx.x;
-    const unsigned mb = (unsigned)__cvta_generic_to_shared(&s_mbar);
-    int item = blockIdx.x;
-    if (item >= items) return;
-    init_mbar(mb);
-    unsigned parity = 0u;
-    prefetch_item(P, B, item);
-
-    for (;;) {
-        int j, m, s, e;
-        item_tile(P, item, j, m, s, e);
-        Geom G1, G2;
-        fused_geom(P, s, e, P.w, G1, G2);
-        const size_t mo = size_t(m) * P.n;
-        const LoadPlan Lp = load_plan(P, mo, G1);        // as issued
-        G2.abase = G1.abase + (G2.start - G1.start);     // cells keep their positions
-        const int next = item + int(gridDim.x);
-        // ---- run control: dt, lambda of this item were fetched with its loads
-        const unsigned int err0 = *((volatile unsigned int *)P.err);
-        wait_load(Lp, mb, parity);
-        __syncthreads();
-        const double dtm = s_rc[0];
-        const double lam = s_rc[1];
-        if (err0) {
-            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-            return;
-        }
-
-        TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
-        if (dtm == 0.0) {
-            carry_tile<true, BATHY>(P, B, mo, s, e, lam, acc);
-            __syncthreads();
-            if (next < items) prefetch_item(P, B, next);
-        } else {
-            // ---- stage 1: U^n -> U1 on the widened tile; stage 2: (U^n, U1) ->
-            // U^{n+1} on the kept tile.  One (not unrolled) loop: both stages
-            // run the same instructions.
-#pragma unroll 1
-            for (int st = 0; st < 2; st++) {
-                const bool two = st == 1;
-                const Geom G = two ? G2 : G1;
-                const StageC S = stage_consts(P, two ? P.aI2 : P.aI1, dtm, lam);
-                stage_body<false, false, BATHY, RELAX, MODE_FUSED>(P, B, G, m, s, S, dtm, acc,
-                                                                   (two && next < items) ? next : -1, two);
-                if (two) break;
-                __syncthreads();
-                // U1 ghost rows at physical ends (A10): mirror (wall, q odd) or copy
-                if (G2.left_phys || G2.right_phys) {
-                    double *const A2 = smem + G2.abase;
-                    const int L2 = G2.L;
-                    if (tid < 3 && G2.left_phys) {
-                        const int r = -1 - tid;
-                        const bool wall = P.bcl == BC_WALL;
-                        const int src = wall ? -1 - r : 0;
-                        A2[7 * SROWS + r] = A2[7 * SROWS + src];
-                        A2[4 * SROWS + r] = (wall ? -1.0 : 1.0) * A2[4 * SROWS + src];
-                        A2[5 * SROWS + r] = A2[5 * SROWS + src];
-                        A2[6 * SROWS + r] = A2[6 * SROWS + src];
-                    }
-                    if (tid >= 32 && tid < 35 && G2.right_phys) {
-                        const int r = L2 + (tid - 32);
-                        const bool wall = P.bcr == BC_WALL;
-                        const int src = wall ? 2 * L2 - 1 - r : L2 - 1;
-                        A2[7 * SROWS + r] = A2[7 * SROWS + src];
-                        A2[4 * SROWS + r] = (wall ? -1.0 : 1.0) * A2[4 * SROWS + src];
-                        A2[5 * SROWS + r] = A2[5 * SROWS + src];
-                        A2[6 * SROWS + r] = A2[6 * SROWS + src];
-                    }
-                    __syncthreads();
-                }
-            }
-            store_tile(B, mo, s, e - s, true, P.T);
-        }
-        tile_epilogue<true>(P, j, m, dtm, acc);
-        if (next >= items) break;
-        item = next;
-    }
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -2370,11 +1995,8 @@ __global__ void __launch_bounds__(SNT, 1) sgn_kernel(const Params P, const Bufs 
 __global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int commit_prev,
                                                         int compute_dt)
 {
-    pdl_release();
-    pdl_wait();
     const unsigned int err = *((volatile unsigned int *)P.err);
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid == 0) { P.work[2 * P.kpar] = 0u; P.work[2 * P.kpar + 1] = 0u; }   // step k's item counters
     if (tid == 0 && commit_prev && err == 0u) *P.steps += 1;
     if (err || !compute_dt) return;
     const int m = tid;
@@ -2390,7 +2012,6 @@ __global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int comm
         if (!(tm < t_end)) dtm = 0.0;
         else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end
     }
-    if ((HSGN_EXP_NOLOAD || HSGN_EXP_NOSTORE) && !(dtm > 0.0 && isfinite(dtm))) dtm = 1e-3;
     if (!(dtm >= 0.0) || !isfinite(dtm)) {
         atomicOr(P.err, ERR_DT);
         return;

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("HSGN_LIB") or os.path.join(_PKG, "lib", "libhsgn.so")
 
 BC = {"periodic": 0, "wall": 1, "transmissive": 2, "halo": 3}
 STATUS = {0: "OK", -1: "E_INVALID", -2: "E_DRY", -3: "E_COERCIVITY", -4: "E_SINGULAR",
-          -5: "E_NONFINITE", -6: "E_CUDA", -7: "E_OVERLAP", -8: "E_NOWORKSPACE"}
+          -5: "E_NONFINITE", -6: "E_CUDA", -7: "E_OVERLAP", -8: "E_NOWORKSPACE", -9: "E_COMM"}
 
 
 class HsgnError(RuntimeError):
@@ -48,6 +48,7 @@ class Diag(C.Structure):
     _fields_ = [("mass", C.c_double), ("min_h", C.c_double), ("max_abs_u", C.c_double),
                 ("nu_max", C.c_double), ("t_min", C.c_double), ("t_max", C.c_double),
                 ("dt_last_min", C.c_double), ("dt_last_max", C.c_double), ("rho_max", C.c_double),
+                ("min_kappa", C.c_double), ("cfl_imex", C.c_double), ("mcfl", C.c_double),
                 ("steps", C.c_int64), ("error_bits", C.c_int32), ("pad_", C.c_int32)]
 
 
@@ -57,7 +58,7 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_set_relaxation",
            "hsgn_set_state", "hsgn_get_state", "hsgn_run_host", "hsgn_step", "hsgn_run_steps", "hsgn_advance_to",
            "hsgn_sync", "hsgn_run_steps_timed", "hsgn_get_diagnostics", "hsgn_launch_count", "hsgn_get_geometry",
-           "hsgn_set_fused", "hsgn_get_fused", "hsgn_set_persistent", "hsgn_set_scheme",
+           "hsgn_set_scheme",
            "hsgn_set_picard", "hsgn_set_well_balanced", "hsgn_set_cluster", "hsgn_get_cluster",
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
            "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl"]
@@ -97,9 +98,6 @@ def load_library(path: str = LIB_PATH):
         "hsgn_get_diagnostics": (st, [vp, C.POINTER(Diag)]),
         "hsgn_launch_count": (C.c_int64, [vp]),
         "hsgn_get_geometry": (st, [vp] + [C.POINTER(C.c_int32)] * 5),
-        "hsgn_set_fused": (st, [vp, C.c_int32]),
-        "hsgn_get_fused": (C.c_int32, [vp]),
-        "hsgn_set_persistent": (st, [vp, C.c_int32]),
         "hsgn_set_scheme": (st, [vp, C.c_int32, C.c_int32]),
         "hsgn_set_picard": (st, [vp, C.c_int32]),
         "hsgn_set_well_balanced": (st, [vp, C.c_int32]),
@@ -214,15 +212,6 @@ class Solver:
         self._chk(self.L.hsgn_get_geometry(self.ctx, *[C.byref(x) for x in v]))
         return Geometry(*[x.value for x in v])
 
-    @property
-    def fused(self) -> bool:
-        """True if each step runs as the one fused kernel (hsgn_set_fused)."""
-        return int(self.L.hsgn_get_fused(self.ctx)) == 1
-
-    def set_fused(self, on: bool) -> None:
-        """One fused kernel per two-stage step (off by default)."""
-        self._chk(self.L.hsgn_set_fused(self.ctx, 1 if on else 0))
-
     def set_scheme(self, scheme: str = "si", stages: int = 2) -> None:
         """"si" (IMEX, P:500-517), "explicit" (hSGN, P:442-458) or "sgn" (classical
         SGN); stages 1 Euler, 2 Heun for the last two."""
@@ -249,11 +238,6 @@ class Solver:
         a, b = C.c_int32(), C.c_int32()
         on = int(self.L.hsgn_get_cluster(self.ctx, C.byref(a), C.byref(b)))
         return (a.value, b.value) if on == 1 else None
-
-    def set_persistent(self, on: bool) -> None:
-        """Persistent per-stage kernels with next-tile prefetch, or one CTA per
-        (tile, member) (the default)."""
-        self._chk(self.L.hsgn_set_persistent(self.ctx, 1 if on else 0))
 
     @property
     def launches(self) -> int:

@@ -30,6 +30,16 @@ def test_library_builds_and_exports_every_declared_symbol():
     # a pure host call: status strings
     assert L.hsgn_status_string(0) == b"ok"
     assert b"coercivity" in L.hsgn_status_string(-3)
+    assert b"NCCL" in L.hsgn_status_string(-9)                  # HSGN_E_COMM
+
+
+def test_diag_struct_matches_header():
+    """the ctypes mirror of hsgn_diag has the header's fields in order"""
+    src = open(os.path.join(ROOT, "include", "hsgn.h")).read()
+    body = src[:src.index("} hsgn_diag;")].rsplit("typedef struct {", 1)[1]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = re.findall(r"\b(\w+)\s*;", body)
+    assert names == [n for n, _ in hsgn.Diag._fields_]
 
 
 def test_library_is_sm100a():

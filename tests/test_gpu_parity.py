@@ -82,11 +82,10 @@ def gpu_solver(w, **kw):
     hs = _hsgn()
     order = kw.pop("order", 2)
     tab = kw.pop("tableau", None)
-    kmode = kw.pop("kmode", None)          # None: library default (one CTA per tile and member)
+    kmode = kw.pop("kmode", None)          # None: library default (auto)
     s = hs.Solver(w.n, w.members, w.x_min, w.x_max, bc=w.bc, order=order, **kw)
-    if kmode is not None:
-        s.set_fused(kmode == "fused")
-        s.set_persistent(kmode == "persistent")
+    if kmode is not None:                  # "tiles": overlapped tiles; "cluster": exact cluster
+        s.set_cluster(1 if kmode == "cluster" else 0)   # solve whenever the member fits
     s.set_params(w.g, w.lam, w.cfl, w.mcfl)
     if tab is not None:
         s.set_tableau(tab)
@@ -132,7 +131,7 @@ def compare(w, s, members, steps=None, t_end=None, tol=TOL_STEP, floor=False, **
 
 # --------------------------------------------------------------------------
 # kernel organisations of the same arithmetic
-KMODES = ["persistent", "per-tile", "fused"]
+KMODES = ["tiles", "cluster"]
 
 
 @pytest.mark.parametrize("kmode", KMODES)
@@ -141,7 +140,6 @@ KMODES = ["persistent", "per-tile", "fused"]
 def test_one_step_ragged_tiles(bc, order, kmode):
     w = W.random_smooth(3000, 3, seed=21, amp=0.08, bc=(bc, bc))
     s = gpu_solver(w, tile_cells=700, overlap=64, order=order, kmode=kmode)
-    assert s.fused == (kmode == "fused")
     g = s.geometry
     assert g.tiles_per_member == -(-3000 // g.tile_cells) >= 5 and 3000 % g.tile_cells != 0  # ragged
     s.step()
@@ -222,21 +220,6 @@ def test_mass_conservation_gpu():
         assert abs(d["mass"] - m0) <= 1e-13 * m0
 
 
-def test_programmatic_dependent_launch_option(monkeypatch):
-    """HSGN_PDL=1 (griddepcontrol launches, off by default) advances bitwise like
-    the default launch mode."""
-    w = W.random_smooth(3000, 3, seed=13, amp=0.06, bathy=0.04)
-    a = gpu_solver(w)
-    monkeypatch.setenv("HSGN_PDL", "1")
-    b = gpu_solver(w)
-    a.run_steps(25)
-    b.run_steps(25)
-    (x, tx), (y, ty) = a.get_state(device=False), b.get_state(device=False)
-    for f, g in zip(x, y):
-        assert np.array_equal(f, g)
-    assert np.array_equal(tx, ty)
-
-
 @pytest.mark.parametrize("kmode", KMODES)
 def test_timed_graph_equals_run_steps(kmode):
     """hsgn_run_steps_timed (bench.py's timed region: the K steps as one graph with
@@ -247,7 +230,7 @@ def test_timed_graph_equals_run_steps(kmode):
     a.run_steps(25)
     l0 = b.launches
     ms1, ms2, tot = b.run_steps_timed(25, total=True)
-    assert b.launches - l0 == 1 + (2 if kmode == "fused" else 3) * 25
+    assert b.launches - l0 == 1 + 3 * 25
     (x, tx), (y, ty) = a.get_state(device=False), b.get_state(device=False)
     for f, g in zip(x, y):
         assert np.array_equal(f, g)
@@ -258,14 +241,14 @@ def test_timed_graph_equals_run_steps(kmode):
 
 @pytest.mark.parametrize("kmode", KMODES)
 def test_launch_count_per_step(kmode):
-    """per step: the fused step kernel (or stage 1 + stage 2) and dt/commit;
+    """per step: stage 1 + stage 2 and dt/commit;
     plus one dt kernel per call."""
     w = W.random_smooth(512, 1, seed=1)
     s = gpu_solver(w, kmode=kmode)
     l0 = s.launches
     s.run_steps(40)          # graph replays + eager remainder
     s.sync()
-    assert s.launches - l0 == 1 + (2 if kmode == "fused" else 3) * 40
+    assert s.launches - l0 == 1 + 3 * 40
 
 
 # --------------------------------------------------------------------------

@@ -15,6 +15,7 @@ from paper_2510_07539_b200 import workloads as W  # noqa: E402
 members = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 w = W.cfg3(members=members)
 s = hsgn.solver_for(w)
+s.set_cluster(1)
 f = s.L.hsgn_cl_counters
 f.restype = C.c_int
 f.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]

@@ -333,6 +333,40 @@ void hsgn_group_destroy(hsgn_group *g);
 hsgn_status hsgn_nccl_unique_id(void *id);
 hsgn_status hsgn_attach_nccl(hsgn_ctx *ctx, const void *id, int32_t rank, int32_t world);
 
+/* ---- host-staged slab transport (any process-group transport, e.g. gloo) --
+ * One slab step of a context with HSGN_BC_HALO sides, neither grouped nor
+ * NCCL-attached, in phases; between them the caller moves the data with its
+ * own collectives (tests/test_gpu_slab_gloo.py):
+ *   1. hsgn_slab_get(MAXIMA) -> max-reduce over the slabs -> hsgn_slab_put(MAXIMA)
+ *      (2 n_members uint64: bit patterns of the non-negative max|u|, max(|u|+c)
+ *      of U^n; the max of the bit patterns is the max of the values)
+ *   2. hsgn_slab_phase(HSGN_PHASE_DT)           dt of the step (clipped to t_end)
+ *   3. hsgn_slab_get(UN): [left boundary: 4 x H][right boundary: 4 x H] of U^n
+ *      (h, q, K, W; H = overlap + 3 cells), send the left part to the left
+ *      neighbour and the right part to the right one; hsgn_slab_put(UN):
+ *      [left halo: 4 x H (the left neighbour's right boundary)][right halo]
+ *   4. hsgn_slab_phase(HSGN_PHASE_STAGE1)
+ *   5. as 3 with U1 (UN -> U1), then hsgn_slab_phase(HSGN_PHASE_STAGE2)
+ *      (2-stage tableaux only)
+ *   6. hsgn_slab_phase(HSGN_PHASE_COMMIT)
+ * With bathymetry, the static b halos are exchanged once the same way (B: 1
+ * field) before the first step.  hsgn_slab_xfer_count gives the doubles (or
+ * uint64) of one get/put buffer.  get/put synchronise the context's stream;
+ * phases only enqueue.  Errors: HSGN_E_INVALID (not a host-staged slab
+ * context, unknown transfer or phase, STAGE2 with a 1-stage tableau). */
+#define HSGN_XFER_MAXIMA 0
+#define HSGN_XFER_UN 1
+#define HSGN_XFER_U1 2
+#define HSGN_XFER_B 3
+#define HSGN_PHASE_DT 0
+#define HSGN_PHASE_STAGE1 1
+#define HSGN_PHASE_STAGE2 2
+#define HSGN_PHASE_COMMIT 3
+int64_t hsgn_slab_xfer_count(const hsgn_ctx *ctx, int32_t what);
+hsgn_status hsgn_slab_get(hsgn_ctx *ctx, int32_t what, void *host_out);
+hsgn_status hsgn_slab_put(hsgn_ctx *ctx, int32_t what, const void *host_in);
+hsgn_status hsgn_slab_phase(hsgn_ctx *ctx, int32_t phase);
+
 const char *hsgn_status_string(hsgn_status s);
 const char *hsgn_last_error(const hsgn_ctx *ctx);
 

@@ -620,6 +620,49 @@ hsgn_status nccl_exchange(hsgn_ctx *c, int which)
     return HSGN_OK;
 }
 
+// Slab step phases (shared by the group, NCCL and host-staged transports).
+// b. dt of step k (after the maxima were max-reduced over the slabs)
+hsgn_status slab_phase_dt(std::vector<hsgn_ctx *> &g, long long k)
+{
+    hsgn_status st;
+    for (auto *c : g) if ((st = launch_dtc(c, k, 0, 1)) != HSGN_OK) return st;
+    return HSGN_OK;
+}
+
+// c/d. stage 1 (s2 = false) or stage 2 (s2 = true) of step k, halos in place
+hsgn_status slab_phase_stage(std::vector<hsgn_ctx *> &g, long long k, bool s2)
+{
+    hsgn_status st;
+    for (auto *c : g) {
+        const Params Pm = make_params(c, k);
+        Bufs B{};
+        for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; }
+        if (s2) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
+            if ((st = launch_stage_b<true, true>(c, Pm, B)) != HSGN_OK) return st;
+        } else if (c->tab.stages == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
+            if ((st = launch_stage_b<false, true>(c, Pm, B)) != HSGN_OK) return st;
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            if ((st = launch_stage_b<false, false>(c, Pm, B)) != HSGN_OK) return st;
+        }
+    }
+    return HSGN_OK;
+}
+
+// e. commit step k
+hsgn_status slab_phase_commit(std::vector<hsgn_ctx *> &g, long long k)
+{
+    hsgn_status st;
+    for (auto *c : g) {
+        if ((st = launch_dtc(c, k + 1, 1, 0)) != HSGN_OK) return st;
+        c->cur ^= 1;
+        c->host_steps++;
+    }
+    return HSGN_OK;
+}
+
 // one slab step k for every context of g (lockstep, one shared stream) or for
 // the single NCCL-attached context g[0]
 hsgn_status slab_step(std::vector<hsgn_ctx *> &g, long long k, bool nccl)
@@ -640,41 +683,16 @@ hsgn_status slab_step(std::vector<hsgn_ctx *> &g, long long k, bool nccl)
         c0->launches++;
         CUDA_TRY(c0, cudaGetLastError());
     }
-    // b. dt of step k
-    for (auto *c : g) if ((st = launch_dtc(c, k, 0, 1)) != HSGN_OK) return st;
+    if ((st = slab_phase_dt(g, k)) != HSGN_OK) return st;
     // c. U^n halos, stage 1
     if ((st = nccl ? nccl_exchange(c0, 0) : loopback_exchange(g, 0)) != HSGN_OK) return st;
-    for (auto *c : g) {
-        const Params Pm = make_params(c, k);
-        Bufs B{};
-        for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; }
-        if (c->tab.stages == 1) {
-            for (int f = 0; f < 4; f++) B.out[f] = c->buf[c->cur ^ 1][f];
-            if ((st = launch_stage_b<false, true>(c, Pm, B)) != HSGN_OK) return st;
-        } else {
-            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
-            if ((st = launch_stage_b<false, false>(c, Pm, B)) != HSGN_OK) return st;
-        }
-    }
+    if ((st = slab_phase_stage(g, k, false)) != HSGN_OK) return st;
     if (c0->tab.stages == 2) {
         // d. U1 halos, stage 2
         if ((st = nccl ? nccl_exchange(c0, 1) : loopback_exchange(g, 1)) != HSGN_OK) return st;
-        for (auto *c : g) {
-            const Params Pm = make_params(c, k);
-            Bufs B{};
-            for (int f = 0; f < 4; f++) {
-                B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; B.out[f] = c->buf[c->cur ^ 1][f];
-            }
-            if ((st = launch_stage_b<true, true>(c, Pm, B)) != HSGN_OK) return st;
-        }
+        if ((st = slab_phase_stage(g, k, true)) != HSGN_OK) return st;
     }
-    // e. commit step k
-    for (auto *c : g) {
-        if ((st = launch_dtc(c, k + 1, 1, 0)) != HSGN_OK) return st;
-        c->cur ^= 1;
-        c->host_steps++;
-    }
-    return HSGN_OK;
+    return slab_phase_commit(g, k);
 }
 
 // After a sync: reconcile host buffer parity with the device's committed steps.
@@ -1591,6 +1609,90 @@ hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps)
 }
 
 void hsgn_group_destroy(hsgn_group *g) { delete g; }
+
+// ---- host-staged slab transport ------------------------------------------
+int64_t hsgn_slab_xfer_count(const hsgn_ctx *c, int32_t what)
+{
+    if (!c || !c->slab) return -1;
+    if (what == HSGN_XFER_MAXIMA) return 2 * int64_t(c->members);
+    if (what < HSGN_XFER_UN || what > HSGN_XFER_B) return -1;
+    const int nf = what == HSGN_XFER_B ? 1 : 4;
+    return 2 * int64_t(nf) * (c->w + 3);
+}
+
+hsgn_status hsgn_slab_get(hsgn_ctx *c, int32_t what, void *host_out)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (!host_out || !c->slab || c->nccl) return fail(c, HSGN_E_INVALID, "slab_get: host-staged slab contexts only");
+    if (what == HSGN_XFER_MAXIMA) {
+        const int slot = int(c->host_steps % 3);
+        CUDA_TRY(c, cudaMemcpyAsync(host_out, c->maxes + size_t(slot) * 2 * c->members,
+                                    2 * size_t(c->members) * 8, cudaMemcpyDeviceToHost, c->stream));
+    } else if (what >= HSGN_XFER_UN && what <= HSGN_XFER_B) {
+        const int which = what - HSGN_XFER_UN, nf = which == 2 ? 1 : 4, H = c->w + 3;
+        double *o = (double *)host_out;
+        for (int f = 0; f < nf; f++) {       // [left boundary: nf x H][right boundary: nf x H]
+            CUDA_TRY(c, cudaMemcpyAsync(o + f * H, bnd_src(c, false, which, f, H), H * 8, cudaMemcpyDeviceToHost,
+                                        c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(o + (nf + f) * H, bnd_src(c, true, which, f, H), H * 8,
+                                        cudaMemcpyDeviceToHost, c->stream));
+        }
+    } else {
+        return fail(c, HSGN_E_INVALID, "slab_get: unknown transfer");
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_slab_put(hsgn_ctx *c, int32_t what, const void *host_in)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (!host_in || !c->slab || c->nccl) return fail(c, HSGN_E_INVALID, "slab_put: host-staged slab contexts only");
+    if (what == HSGN_XFER_MAXIMA) {
+        const int slot = int(c->host_steps % 3);
+        CUDA_TRY(c, cudaMemcpyAsync(c->maxes + size_t(slot) * 2 * c->members, host_in, 2 * size_t(c->members) * 8,
+                                    cudaMemcpyHostToDevice, c->stream));
+    } else if (what >= HSGN_XFER_UN && what <= HSGN_XFER_B) {
+        const int which = what - HSGN_XFER_UN, nf = which == 2 ? 1 : 4, H = c->w + 3;
+        const double *in = (const double *)host_in;
+        for (int f = 0; f < nf; f++) {       // [left halo: nf x H][right halo: nf x H]
+            if (c->desc.bc_left == HSGN_BC_HALO)
+                CUDA_TRY(c, cudaMemcpyAsync(halo_dst(c, true, which, f), in + f * H, H * 8, cudaMemcpyHostToDevice,
+                                            c->stream));
+            if (c->desc.bc_right == HSGN_BC_HALO)
+                CUDA_TRY(c, cudaMemcpyAsync(halo_dst(c, false, which, f), in + (nf + f) * H, H * 8,
+                                            cudaMemcpyHostToDevice, c->stream));
+        }
+    } else {
+        return fail(c, HSGN_E_INVALID, "slab_put: unknown transfer");
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // the host buffer may be reused at return
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_slab_phase(hsgn_ctx *c, int32_t phase)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (!c->slab || c->nccl) return fail(c, HSGN_E_INVALID, "slab_phase: host-staged slab contexts only");
+    if (phase == HSGN_PHASE_DT) {
+        st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
+        if (st != HSGN_OK) return st;
+    }
+    std::vector<hsgn_ctx *> g{c};
+    const long long k = c->host_steps;
+    switch (phase) {
+    case HSGN_PHASE_DT: return slab_phase_dt(g, k);
+    case HSGN_PHASE_STAGE1: return slab_phase_stage(g, k, false);
+    case HSGN_PHASE_STAGE2:
+        if (c->tab.stages != 2) return fail(c, HSGN_E_INVALID, "slab_phase: 1-stage tableau has no stage 2");
+        return slab_phase_stage(g, k, true);
+    case HSGN_PHASE_COMMIT: return slab_phase_commit(g, k);
+    default: return fail(c, HSGN_E_INVALID, "slab_phase: unknown phase");
+    }
+}
 
 hsgn_status hsgn_nccl_unique_id(void *id)
 {

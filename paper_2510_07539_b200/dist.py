@@ -1,12 +1,15 @@
 """Multi-GPU plumbing (torch.distributed): sharding arithmetic, the NCCL
 unique-id bootstrap for slab contexts, and max-over-ranks timing.  Pure host
 logic; the data path (halo exchange, dt all-reduce) runs inside libhsgn.so
-(include/hsgn.h: hsgn_attach_nccl).  Covered by tests/test_dist_gloo.py on CPU
+(include/hsgn.h: hsgn_attach_nccl), or -- host-staged transport -- through
+the process group's own collectives between the library's step phases
+(host_staged_step; gloo).  Covered by tests/test_dist_gloo.py on CPU
 (world_size 2, gloo)."""
 from __future__ import annotations
 
 import os
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -54,6 +57,40 @@ def max_over_ranks(values):
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(x) for x in t.cpu().tolist()]
+
+
+def _ring_exchange(bnd, rank: int, world: int, group=None):
+    """[left boundary | right boundary] of every rank -> this rank's
+    [left halo | right halo] = [left neighbour's right boundary | right
+    neighbour's left boundary] (ring; an all_gather, any world size)."""
+    half = bnd.size // 2
+    t = torch.from_numpy(bnd.copy())
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    left, right = parts[(rank - 1) % world].numpy(), parts[(rank + 1) % world].numpy()
+    return np.concatenate([left[half:], right[:half]])
+
+
+def host_staged_exchange_b(solver, rank: int, world: int, group=None):
+    """Static bathymetry halos of a host-staged slab (once, before stepping)."""
+    solver.slab_put("b", _ring_exchange(solver.slab_get("b"), rank, world, group))
+
+
+def host_staged_step(solver, rank: int, world: int, group=None, stages: int = 2):
+    """One slab step through the host-staged transport (include/hsgn.h): the
+    dt maxima max-reduced and the U^n / U1 halos exchanged with the process
+    group's collectives (gloo on CPU tensors), the stages on the GPU."""
+    mx = solver.slab_get("maxima").view(np.int64)        # non-negative doubles: int64 order
+    t = torch.from_numpy(mx.copy())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    solver.slab_put("maxima", t.numpy().view(np.uint64))
+    solver.slab_phase("dt")
+    solver.slab_put("un", _ring_exchange(solver.slab_get("un"), rank, world, group))
+    solver.slab_phase("stage1")
+    if stages == 2:
+        solver.slab_put("u1", _ring_exchange(solver.slab_get("u1"), rank, world, group))
+        solver.slab_phase("stage2")
+    solver.slab_phase("commit")
 
 
 def attach_slab(solver, rank: int, world: int):

@@ -61,7 +61,11 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_set_scheme",
            "hsgn_set_picard", "hsgn_set_well_balanced", "hsgn_set_cluster", "hsgn_get_cluster",
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
-           "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl"]
+           "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl",
+           "hsgn_slab_xfer_count", "hsgn_slab_get", "hsgn_slab_put", "hsgn_slab_phase"]
+
+XFER = {"maxima": 0, "un": 1, "u1": 2, "b": 3}
+PHASE = {"dt": 0, "stage1": 1, "stage2": 2, "commit": 3}
 
 _lib = None
 
@@ -110,6 +114,10 @@ def load_library(path: str = LIB_PATH):
         "hsgn_nccl_unique_id": (st, [C.c_char_p]),
         "hsgn_attach_nccl": (st, [vp, C.c_char_p, C.c_int32, C.c_int32]),
         "hsgn_last_error": (C.c_char_p, [vp]),
+        "hsgn_slab_xfer_count": (C.c_int64, [vp, C.c_int32]),
+        "hsgn_slab_get": (st, [vp, C.c_int32, vp]),
+        "hsgn_slab_put": (st, [vp, C.c_int32, vp]),
+        "hsgn_slab_phase": (st, [vp, C.c_int32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -347,6 +355,25 @@ class Solver:
         """Slab of a domain sharded over `world` processes (one GPU each)."""
         assert len(unique_id) == 128
         self._chk(self.L.hsgn_attach_nccl(self.ctx, unique_id, rank, world))
+
+    # -- host-staged slab transport (include/hsgn.h) -------------------------
+    def slab_get(self, what: str) -> np.ndarray:
+        """Boundary data this slab sends ("un", "u1", "b": [left | right]) or its
+        dt maxima ("maxima", uint64 bit patterns)."""
+        n = int(self.L.hsgn_slab_xfer_count(self.ctx, XFER[what]))
+        if n < 0:
+            raise HsgnError(-1, "slab_get: not a slab context")
+        out = np.empty(n, dtype=np.uint64 if what == "maxima" else np.float64)
+        self._chk(self.L.hsgn_slab_get(self.ctx, XFER[what], C.c_void_p(out.ctypes.data)))
+        return out
+
+    def slab_put(self, what: str, data: np.ndarray) -> None:
+        data = np.ascontiguousarray(data, dtype=np.uint64 if what == "maxima" else np.float64)
+        assert data.size == int(self.L.hsgn_slab_xfer_count(self.ctx, XFER[what]))
+        self._chk(self.L.hsgn_slab_put(self.ctx, XFER[what], C.c_void_p(data.ctypes.data)))
+
+    def slab_phase(self, phase: str) -> None:
+        self._chk(self.L.hsgn_slab_phase(self.ctx, PHASE[phase]))
 
     def diagnostics(self) -> dict:
         d = Diag()

@@ -64,3 +64,35 @@ def test_slab_edges_local():
             assert e[0] == 0 and e[-1] == n
             sizes = [b - a for a, b in zip(e, e[1:])]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _ring_worker(rank, world, port, q):
+    import numpy as np
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_07539_b200 import dist as D
+    H = 5
+    bnd = np.concatenate([np.full(H, 100.0 * rank + 1), np.full(H, 100.0 * rank + 2)])   # [left | right]
+    halo = D._ring_exchange(bnd, rank, world)
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, halo.tolist()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_staged_ring_exchange(world):
+    """host-staged slab transport: rank r's [left halo | right halo] is
+    [right boundary of r-1 | left boundary of r+1] on the periodic ring"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ring_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        left, right = (r - 1) % world, (r + 1) % world
+        assert res[r] == [100.0 * left + 2] * 5 + [100.0 * right + 1] * 5

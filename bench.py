@@ -68,6 +68,8 @@ def parse():
     p.add_argument("--config", default="cfg3", choices=["cfg3", "cfg5"],
                    help="cfg3: ensemble (default, headline); cfg5: single 2^28-cell domain with bathymetry")
     p.add_argument("--cells5", type=int, default=1 << 28)
+    p.add_argument("--no-sub", action="store_true",
+                   help="skip the cfg5 and time-to-t_end sub-records of the default (cfg3) line")
     return p.parse_args()
 
 
@@ -268,13 +270,25 @@ def main():
     from paper_2510_07539_b200 import hsgn
     from paper_2510_07539_b200 import workloads as W
 
-    local = local % max(torch.cuda.device_count(), 1)   # (several gloo ranks may share a GPU)
+    backend = os.environ.get("HSGN_BENCH_BACKEND", "nccl") if world > 1 else "none"
+    ngpu = max(torch.cuda.device_count(), 1)
+    if backend != "nccl":
+        local = local % ngpu          # (gloo: several ranks may share a GPU)
+    elif local >= ngpu:
+        raise SystemExit(f"LOCAL_RANK {local} but only {ngpu} GPUs visible (NCCL needs one GPU per rank)")
+    phys_gpus = min(world, ngpu) if backend != "nccl" else world
+    if a.config == "cfg5" and world > 1 and backend != "nccl":
+        raise SystemExit("--config cfg5 over several ranks needs the NCCL slab transport (one GPU per rank)")
     torch.cuda.set_device(local)
+    if world > 1 and backend == "nccl":
+        # NCCL's communicator set-up (rings / NVLS) visible on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if world > 1:
         # HSGN_BENCH_BACKEND=gloo: host-side collectives only (exercises the
         # multi-rank path with several ranks on one GPU; the ranks' kernels never
         # wait on each other: the ensemble shards need no data-path exchange)
-        backend = os.environ.get("HSGN_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -483,10 +497,156 @@ def main():
         "diag": {"steps": diag["steps"], "mass": diag["mass"], "min_h": diag["min_h"],
                  "t_max": diag["t_max"], "dt_last_min": diag["dt_last_min"]},
     }
+    if phys_gpus != world:
+        line["shared_gpu"] = f"{world} ranks on {phys_gpus} GPU(s) (gloo test mode)"
+    # sub-records: cfg5 (the largest single-GPU config; over NCCL slabs at N > 1,
+    # strong scaling) and the times to t_end of the other configs (rank 0)
+    if not a.no_sub and a.config == "cfg3" and a.scheme == "si" and a.si_order == 2 and a.picard == 0 \
+            and not a.wb:
+        del s
+        torch.cuda.empty_cache()
+        subs = {}
+        if backend in ("none", "nccl"):
+            subs["cfg5"] = cfg5_record(a, rank, world, dist, coll_dev, peak, peak_src)
+        if rank == 0:
+            subs["time_to_t_end"] = tend_records()
+        if rank == 0:
+            line["sub_records"] = subs
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _timed(stream, fn):
+    """device seconds (CUDA events on the solver's stream) and wall seconds of fn()"""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    e0.record(stream)
+    out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1) / 1e3, time.perf_counter() - w0
+
+
+def cfg5_record(a, rank, world, dist, coll_dev, peak, peak_src):
+    """BASELINE configs[4]: one periodic domain of a.cells5 cells with bathymetry,
+    its 100-step configuration.  N = 1: one context; N > 1: contiguous slabs,
+    one per rank, halo exchange + dt all-reduce over NCCL inside libhsgn
+    (strong scaling).  Device time of the 100 steps (max over ranks), the
+    stage-2 roofline (104 B/cell: U^n, U1, b read, U^{n+1} written; N = 1) and
+    the end-to-end job through the public API: set_state from pinned host
+    memory, the 100 steps, get_state into pinned host memory (wall clock)."""
+    import ctypes as C
+    import torch
+    from paper_2510_07539_b200 import dist as D
+    from paper_2510_07539_b200 import hsgn
+    from paper_2510_07539_b200 import workloads as W
+    n = a.cells5
+    lo, hi = D.slab_range(n, rank, world)
+    (h, q, K, Wf, b), meta = W.cfg5(n, device="cuda", first=lo, count=hi - lo)
+    dx = meta["L"] / meta["n"]
+    slab = world > 1
+    s = hsgn.Solver(hi - lo, 1, lo * dx, hi * dx, bc=("halo", "halo") if slab else ("periodic", "periodic"))
+    s.set_params(9.81, meta["lam"], meta["cfl"], meta["mcfl"])
+    s.set_bathymetry(b)
+    s.set_filter(0.25)
+    s.set_state(h, q, K, Wf)
+    if slab:
+        D.attach_slab(s, rank, world)
+    steps = int(meta["steps"])
+    s.run_steps(6)
+    s.sync()
+    if world > 1:
+        dist.barrier()
+    if slab:
+        _, dev, _ = _timed(s.stream, lambda: s.run_steps(steps))
+        ms1 = ms2 = None
+    else:
+        ms1, ms2, tot = s.run_steps_timed(steps, total=True)
+        dev = tot / 1e3
+    t = torch.tensor([dev], device=coll_dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = float(t.item())
+    cells = hi - lo
+    rec = {"workload": f"cfg5_large_domain: {n} cells, periodic, bathymetry 0.2 sin, lambda 1e4, "
+                       f"{steps}-step config, A19 filter",
+           "value": 2.0 * n * steps / dev, "unit": UNIT, "n_gpus": world, "steps": steps,
+           "ms_per_step": dev / steps * 1e3, "time_to_end_s": dev,
+           "scaling": "strong", "parallelism": (f"slabs x{world} (NCCL send/recv halos + all-reduce max)"
+                                                if slab else "single GPU")}
+    if not slab:
+        ach = 104.0 * cells / (ms2 / steps / 1e3) / 1e9
+        rec["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                           "kernel": "stage_kernel<STAGE2,FINAL,BATHY> (stage 2)",
+                           "bytes_model": "104 B/cell per stage-2 launch (read U^n, U1, b; write U^{n+1})",
+                           "peak_source": peak_src,
+                           "stage1_frac": 72.0 * cells / (ms1 / steps / 1e3) / 1e9 / peak}
+    if not a.no_e2e:
+        pin = [x.cpu().pin_memory() for x in (h, q, K, Wf)]
+        del h, q, K, Wf
+        outp = [torch.empty(cells, dtype=torch.float64).pin_memory() for _ in range(4)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        te0 = time.perf_counter()
+        s.set_state(*pin)
+        s.run_steps(steps)
+        tt = np.empty(1)
+        s._chk(s.L.hsgn_get_state(s.ctx, *[C.c_void_p(x.data_ptr()) for x in outp], C.c_void_p(tt.ctypes.data)))
+        te = time.perf_counter() - te0
+        t = torch.tensor([te], device=coll_dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te = float(t.item())
+        rec["e2e"] = {"value": 2.0 * n * steps / te, "unit": UNIT, "seconds": te,
+                      "h2d_bytes": 32 * cells * world, "d2h_bytes": 32 * cells * world + 8,
+                      "what": "Solver.set_state(pinned host) + run_steps(100) + get_state(pinned host) of the "
+                              "whole 100-step job; wall clock, max over ranks (a single coupled domain: the "
+                              "first step needs the global dt of the whole uploaded state)"}
+    else:
+        del h, q, K, Wf
+    s.close()
+    del s
+    torch.cuda.empty_cache()
+    return rec
+
+
+def tend_records():
+    """Times to t_end (device time of advance_to / run_steps, CUDA events) of
+    the other BASELINE configs on one GPU: cfg1 soliton to t = 20, cfg2 dam
+    break to t = 48 at lambda 1e2 / 1e3 / 1e4, cfg4 bar (4 lambdas) 200 steps."""
+    from paper_2510_07539_b200 import hsgn
+    from paper_2510_07539_b200 import workloads as W
+    out = {}
+    w = W.cfg1()
+    s = hsgn.solver_for(w)
+    s.advance_to(1.0)                               # warm-up (graph capture)
+    s = hsgn.solver_for(w)
+    _, dev, wall = _timed(s.stream, lambda: s.advance_to(w.t_end))
+    st = s.diagnostics()["steps"]
+    out["cfg1_soliton_t20"] = {"seconds": dev, "wall_s": wall, "steps": st, "us_per_step": dev / st * 1e6,
+                               "cells": w.n}
+    for lam in (1e2, 1e3, 1e4):
+        w = W.cfg2(lam)
+        s = hsgn.solver_for(w)
+        _, dev, wall = _timed(s.stream, lambda: s.advance_to(w.t_end))
+        st = s.diagnostics()["steps"]
+        out[f"cfg2_dambreak_lam{lam:g}_t48"] = {"seconds": dev, "wall_s": wall, "steps": st,
+                                                "us_per_step": dev / st * 1e6, "cells": w.n,
+                                                "value": 2.0 * w.n * st / dev}
+    w = W.cfg4()
+    s = hsgn.solver_for(w)
+    s.run_steps(18)
+    s.sync()
+    _, dev, wall = _timed(s.stream, lambda: s.run_steps(200))
+    out["cfg4_bar_4lambdas_200steps"] = {"seconds": dev, "wall_s": wall, "steps": 200,
+                                         "cells": w.n * w.members, "value": 2.0 * w.n * w.members * 200 / dev}
+    out["unit"] = "seconds of device time (value: cell-stage/s)"
+    return out
 
 
 if __name__ == "__main__":

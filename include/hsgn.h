@@ -289,26 +289,35 @@ hsgn_status hsgn_set_picard(hsgn_ctx *ctx, int32_t passes);
  * (HSGN_E_INVALID at the next step).  Drops captured graphs.  Errors:
  * HSGN_E_INVALID (null context). */
 hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
-/* Cluster stage kernels (hsgn_cluster.cuh): the C CTAs
- * of a member form one thread-block cluster and solve the depth system of
- * P:509-512 EXACTLY across their tiles (partition method per thread chunk,
- * interior PCR with two spike columns, one DSMEM exchange of 12 doubles per
- * CTA, a C-unknown separator system solved redundantly per CTA; cyclic for
- * periodic members) -- no overlap rows and no decay condition.  Eligible when
- * the member fits: n_cells % 4 == 0, both sides periodic (C = the smallest
- * power of two with n_cells <= 512 C) or both physical (wall / transmissive,
- * C = ceil(n_cells / 512)), C <= 16, and the step is the SI stage without
- * Picard passes, the A25 form, relaxation zones or slab sides.  mode 0: never
- * (overlapped tiles with the decay check); 1: whenever eligible; 2 (default,
- * "auto"): when eligible and the overlapped tiles cannot bound the decay a
+/* Exact depth solve across tiles (hsgn_cluster.cuh).
+ * Cluster kernels: the C CTAs of a member form one thread-block cluster and
+ * solve the depth system of P:509-512 EXACTLY across their tiles (partition
+ * method per thread chunk, interior PCR with two spike columns, one DSMEM
+ * exchange of 12 doubles per CTA, a C-unknown separator system solved
+ * redundantly per CTA; cyclic for periodic members) -- no overlap rows and no
+ * decay condition.  They need the member to fit: n_cells % 4 == 0, both sides
+ * periodic (C = the smallest power of two with n_cells <= 512 C) or both
+ * physical (wall / transmissive, C = ceil(n_cells / 512)), C <= 16.
+ * Tile-level SPIKE (members of any size, n_cells % 4 == 0): per stage, the
+ * tiles' reduced systems (12 values per tile to global memory), one CTA per
+ * member solving the separator system exactly (the same scheme one level up),
+ * the tiles recomputed and finished with their separator values, and, with the
+ * A19 filter, the two rows at each tile end completed by a small kernel: about
+ * 2x the work of a stage on the overlapped tiles, for any decay length.
+ * Both: the SI stage without Picard passes, the A25 form or slab sides.
+ * mode 0: never (overlapped tiles with the decay check); 1: the cluster kernels
+ * whenever the member fits; 3: tile-level SPIKE whenever eligible; 2 (default,
+ * "auto"): exact paths only when the overlapped tiles cannot bound the decay a
  * priori, i.e. material-CFL-only stepping (cfl_imex <= 0) without a
- * user overlap -- the overlapped tiles are faster on B200 when CFL_IMEX bounds
- * rho.  Drops captured graphs.  Errors: HSGN_E_INVALID
- * (null context, mode outside 0..2). */
+ * user overlap -- the cluster kernels if the member fits, else tile-level
+ * SPIKE (the overlapped tiles are faster on B200 when CFL_IMEX bounds rho).
+ * Drops captured graphs.  Errors: HSGN_E_INVALID (null context, mode outside
+ * 0..3). */
 hsgn_status hsgn_set_cluster(hsgn_ctx *ctx, int32_t mode);
-/* 1 if the next step runs on the cluster kernels (then *ctas = C and
- * *tile_rows = rows per CTA, the last CTA n_cells - (C - 1) * tile_rows),
- * 0 if not (both 0), -1 for a null context.  Either pointer may be NULL. */
+/* 1 if the next step runs on the cluster kernels, 2 if on tile-level SPIKE
+ * (then *ctas = CTAs (tiles) per member and *tile_rows = rows per tile, the last
+ * n_cells - (ctas - 1) * tile_rows), 0 for the overlapped tiles (both 0), -1 for
+ * a null context.  Either pointer may be NULL. */
 int32_t hsgn_get_cluster(const hsgn_ctx *ctx, int32_t *ctas, int32_t *tile_rows);
 /* Tile geometry chosen by hsgn_create: kept cells per tile, overlap, tiles per
  * member, threads per CTA, max rows per CTA. */

@@ -96,6 +96,10 @@ struct hsgn_ctx {
                                   // overlapped tiles cannot bound the decay a priori
                                   // (material-CFL-only stepping); HSGN_CLUSTER overrides
     int clC = 0, clT = 0;
+    // tile-level SPIKE (general exact path: any member size): spG tiles of spT
+    // rows per member; buffers in the workspace (tips, L, filter rows, scratch)
+    int spG = 0, spT = 0;
+    double *sp_tips = nullptr, *sp_L = nullptr, *sp_fb = nullptr, *sp_S = nullptr;
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
     std::string last_error;
@@ -231,11 +235,49 @@ hsgn_status launch_stage_b(hsgn_ctx *c, const Params &P, const Bufs &B)
 
 // Cluster path eligibility for the current settings (the geometry clC, clT
 // depends only on n and the boundary kinds and is fixed at hsgn_create).
+bool exact_eligible(const hsgn_ctx *c)
+{
+    return c->scheme == 0 && !c->slab && c->picard == 0 && !c->wb;
+}
+
+// material-CFL-only stepping without a user overlap: the overlapped tiles
+// cannot bound the depth system's decay a priori
+bool overlap_unbounded(const hsgn_ctx *c) { return !(c->cfl > 0.0) && c->desc.overlap <= 0; }
+
 bool use_cluster(const hsgn_ctx *c)
 {
-    const bool on = c->cl_mode == 1 || (c->cl_mode == 2 && !(c->cfl > 0.0) && c->desc.overlap <= 0);
-    return on && c->clC > 0 && c->scheme == 0 && !c->slab && c->picard == 0 && !c->wb &&
-           !(c->relax.gen_rate > 0.0 || c->relax.sp_rate > 0.0);
+    const bool on = c->cl_mode == 1 || (c->cl_mode == 2 && overlap_unbounded(c));
+    return on && c->clC > 0 && exact_eligible(c);
+}
+
+bool use_spike(const hsgn_ctx *c)
+{
+    if (use_cluster(c) || c->spG <= 0 || !exact_eligible(c) || c->sp_tips == nullptr) return false;
+    return c->cl_mode == 3 || (c->cl_mode == 2 && overlap_unbounded(c));
+}
+
+void choose_spike(hsgn_ctx *c)
+{
+    c->spG = c->spT = 0;
+    const int bl = c->desc.bc_left, br = c->desc.bc_right;
+    const bool cyc = bl == HSGN_BC_PERIODIC && br == HSGN_BC_PERIODIC;
+    const bool phys = (bl == HSGN_BC_WALL || bl == HSGN_BC_TRANSMISSIVE) &&
+                      (br == HSGN_BC_WALL || br == HSGN_BC_TRANSMISSIVE);
+    const int n = c->n;
+    if ((!cyc && !phys) || (n % 4) != 0 || n < 8) return;
+    const int G = (n + CT_MAX - 1) / CT_MAX;
+    int T = G == 1 ? n : CT_MAX;
+    if (G > 1 && n - (G - 1) * T < 8) T = CT_MAX - 4;      // last tile 4 rows: shorten the others
+    if (G > 1 && (n - (G - 1) * T < 8 || n - (G - 1) * T > CT_MAX)) return;
+    c->spG = G;
+    c->spT = T;
+}
+
+size_t spike_bytes(const hsgn_ctx *c)
+{
+    // per member and tile: 12 (tips) + 1 (L) + 16 (filter rows) + 3 (scratch) doubles
+    const int G = std::max(c->spG, 1);
+    return 4 * 256 + size_t(c->members) * G * 32 * sizeof(double);
 }
 
 void choose_cluster(hsgn_ctx *c)
@@ -291,11 +333,49 @@ hsgn_status launch_cl_b(hsgn_ctx *c, const Params &P, const Bufs &B)
 }
 
 template <bool S2, bool FIN, bool BATHY>
+hsgn_status launch_spike(hsgn_ctx *c, Params P, const Bufs &B)
+{
+    P.T = c->spT;
+    P.tiles = c->spG;
+    P.sp_tips = c->sp_tips; P.sp_L = c->sp_L; P.sp_fb = c->sp_fb; P.sp_S = c->sp_S;
+    const dim3 grid(c->spG, c->members);
+    const size_t sm = BATHY ? CSMEM_BYTES_B : CSMEM_BYTES;
+    CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_TIPS>, grid, dim3(CNT), sm, P, B));
+    CUDA_TRY(c, launch_k(c, sep_solve_kernel, dim3(c->members), dim3(CNT), 0, P));
+    CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_FINISH>, grid, dim3(CNT), sm, P, B));
+    c->launches += 3;
+    if (FIN && c->filter_sigma > 0.0) {
+        CUDA_TRY(c, launch_k(c, filter_fix_kernel, dim3((4 * c->spG + 127) / 128, c->members), dim3(128), 0, P, B));
+        c->launches++;
+    }
+    return HSGN_OK;
+}
+
+template <bool S2, bool FIN>
+hsgn_status launch_spike_b(hsgn_ctx *c, const Params &P, const Bufs &B)
+{
+    return c->bathy ? launch_spike<S2, FIN, true>(c, P, B) : launch_spike<S2, FIN, false>(c, P, B);
+}
+
+// kernels enqueued per step (graph launch accounting)
+int launches_per_step(const hsgn_ctx *c)
+{
+    if (c->scheme != 0) return c->x_stages + 1;
+    if (use_spike(c)) {
+        const int fix = c->filter_sigma > 0.0 ? 1 : 0;
+        return 3 * c->tab.stages + fix + 1;
+    }
+    return c->tab.stages + 1;
+}
+
+template <bool S2, bool FIN, bool BATHY>
 void cl_attrs()
 {
     cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(BATHY ? CSMEM_BYTES_B : CSMEM_BYTES));
+    const int sm = int(BATHY ? CSMEM_BYTES_B : CSMEM_BYTES);
+    cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY, CL_MODE_TIPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(cl_stage_kernel<S2, FIN, BATHY, CL_MODE_FINISH>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
 hsgn_status launch_dtc(hsgn_ctx *c, long long k, int commit_prev, int compute_dt)
@@ -384,6 +464,25 @@ hsgn_status enqueue_step(hsgn_ctx *c, int cur, long long k, cudaEvent_t *ev = nu
             if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
             for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
             st = launch_cl_b<true, true>(c, P, B);
+            if (st != HSGN_OK) return st;
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
+        }
+    } else if (use_spike(c)) {
+        if (c->tab.stages == 1) {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            st = launch_spike_b<false, true>(c, P, B);
+            if (st != HSGN_OK) return st;
+            if (ev) {
+                CUDA_TRY(c, rec_ev(c, ev[1]));
+                CUDA_TRY(c, rec_ev(c, ev[2]));
+            }
+        } else {
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[2][f];
+            st = launch_spike_b<false, false>(c, P, B);
+            if (st != HSGN_OK) return st;
+            if (ev) CUDA_TRY(c, rec_ev(c, ev[1]));
+            for (int f = 0; f < 4; f++) B.out[f] = c->buf[cur ^ 1][f];
+            st = launch_spike_b<true, true>(c, P, B);
             if (st != HSGN_OK) return st;
             if (ev) CUDA_TRY(c, rec_ev(c, ev[2]));
         }
@@ -524,8 +623,7 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
                 cudaGraphDestroy(gr);
             }
             CUDA_TRY(c, cudaGraphLaunch(gx, c->stream));
-            const int kpl = c->scheme != 0 ? c->x_stages : c->tab.stages;
-            c->launches += GRAPH_STEPS * (kpl + 1);
+            c->launches += GRAPH_STEPS * launches_per_step(c);
             done += GRAPH_STEPS;          // even: cur unchanged
             c->host_steps += GRAPH_STEPS;
         } else {
@@ -761,6 +859,12 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         kc->scheme = c->scheme; kc->x_stages = c->x_stages;
         kc->picard = c->picard; kc->wb = c->wb;
         kc->cl_mode = c->cl_mode; kc->clC = c->clC; kc->clT = c->clT;
+        kc->spG = c->spG; kc->spT = c->spT;
+        if (c->sp_tips) {
+            const size_t o = size_t(m0) * c->spG;
+            kc->sp_tips = c->sp_tips + o * XPUB; kc->sp_L = c->sp_L + o;
+            kc->sp_fb = c->sp_fb + o * 16; kc->sp_S = c->sp_S + o * 3;
+        }
         kc->ws = c->ws;
         for (int bi = 0; bi < 3; bi++)
             for (int f = 0; f < 4; f++) kc->buf[bi][f] = c->buf[bi][f] + size_t(m0) * c->n;
@@ -947,7 +1051,7 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cl_attrs<false, true, false>(); cl_attrs<false, true, true>();
     if (const char *e = std::getenv("HSGN_CLUSTER")) c->cl_mode = std::atoi(e);
     choose_geometry(c);
-    if (!slab) choose_cluster(c);
+    if (!slab) { choose_cluster(c); choose_spike(c); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         delete c;
@@ -991,6 +1095,7 @@ size_t hsgn_workspace_bytes(const hsgn_ctx *c)
     s += 256;                                               // ctrl
     s += 2 * align256(9 * size_t(H_MAX) * sizeof(double));  // slab halos
     s += kid_small_bytes(c->n, c->members) + KIDS_MAX * kid_small_bytes(c->n, 1);  // hsgn_run_host
+    s += spike_bytes(c);                                    // tile-level SPIKE buffers
     return s;
 }
 
@@ -1023,6 +1128,15 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
     q += 256;
     c->halo_l = (double *)q; q += align256(9 * size_t(H_MAX) * sizeof(double));
     c->halo_r = (double *)q; q += align256(9 * size_t(H_MAX) * sizeof(double));
+    if (c->spG > 0) {
+        const size_t mg = size_t(c->members) * c->spG;
+        c->sp_tips = (double *)q; q += align256(mg * XPUB * sizeof(double));
+        c->sp_L = (double *)q; q += align256(mg * sizeof(double));
+        c->sp_fb = (double *)q; q += align256(mg * 16 * sizeof(double));
+        c->sp_S = (double *)q; q += align256(mg * 3 * sizeof(double));
+    } else {
+        q += spike_bytes(c);
+    }
     c->kid_ws = q;
     CUDA_TRY(c, cudaMemsetAsync(c->ws + (size_t)((char *)c->err - c->ws), 0, 512, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->b, 0, size_t(c->n) * sizeof(double), c->stream));
@@ -1510,7 +1624,7 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *c, int32_t on)
 
 hsgn_status hsgn_set_cluster(hsgn_ctx *c, int32_t mode)
 {
-    if (!c || mode < 0 || mode > 2) return HSGN_E_INVALID;
+    if (!c || mode < 0 || mode > 3) return HSGN_E_INVALID;
     drop_graphs(c);
     c->cl_mode = mode;
     return HSGN_OK;
@@ -1519,10 +1633,19 @@ hsgn_status hsgn_set_cluster(hsgn_ctx *c, int32_t mode)
 int32_t hsgn_get_cluster(const hsgn_ctx *c, int32_t *ctas, int32_t *tile_rows)
 {
     if (!c) return -1;
-    const bool on = use_cluster(c);
-    if (ctas) *ctas = on ? c->clC : 0;
-    if (tile_rows) *tile_rows = on ? c->clT : 0;
-    return on ? 1 : 0;
+    if (use_cluster(c)) {
+        if (ctas) *ctas = c->clC;
+        if (tile_rows) *tile_rows = c->clT;
+        return 1;
+    }
+    if (use_spike(c)) {
+        if (ctas) *ctas = c->spG;
+        if (tile_rows) *tile_rows = c->spT;
+        return 2;
+    }
+    if (ctas) *ctas = 0;
+    if (tile_rows) *tile_rows = 0;
+    return 0;
 }
 
 #if HSGN_EXP_TIMING

@@ -223,6 +223,16 @@ constexpr int PPAD = 16;
 constexpr int PSTR = CNT + 2 * PPAD;
 static_assert(2 * 5 * PSTR <= 3 * CARR, "PCR buffers fit in arrays 1..3");
 
+// Kernel modes.  CLUSTER: the C tiles of a member are one thread-block cluster,
+// the separator data travel by DSMEM.  TIPS / FINISH: tile-level SPIKE for
+// members of any size (no cluster; C = tiles per member): TIPS computes each
+// tile's reduced system and writes its 12 published values to P.sp_tips;
+// sep_solve_kernel solves the separator system of every member exactly into
+// P.sp_L; FINISH recomputes the tile (identical arithmetic), takes its L values
+// from P.sp_L, and finishes the stage; with the A19 filter the two rows at each
+// interior tile end are completed by filter_fix_kernel from P.sp_fb.
+enum { CL_MODE_CLUSTER = 0, CL_MODE_TIPS = 1, CL_MODE_FINISH = 2 };
+
 // ---------------------------------------------------------------------------
 // The cluster stage kernel.  grid = (C, members), cluster = (C, 1, 1).
 // STAGE2: inputs U^n and U1 (E, R formed on load); FINAL: this stage produces
@@ -230,9 +240,10 @@ static_assert(2 * 5 * PSTR <= 3 * CARR, "PCR buffers fit in arrays 1..3");
 // 4), P.tiles = C; periodic members (both sides periodic) or physical ends
 // on both sides.
 // ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY>
+template <bool STAGE2, bool FINAL, bool BATHY, int MODE = CL_MODE_CLUSTER>
 __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params P, const Bufs B)
 {
+    constexpr bool CLU = MODE == CL_MODE_CLUSTER;
     double *const sm = hsgn_smem;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 #if HSGN_EXP_TIMING
@@ -269,7 +280,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     // the neighbouring tiles (periodic: wrapped) by threads 64, 65 (left) and
     // 96, 97 (right), two rows each, or are mirrored at physical ends (A10);
     // R of rows -1 and Tc goes to s_rh for the threads computing those rows.
-    if (tid == 0) {
+    if (CLU && tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xmb) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xmb2) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(fmb) : "memory");
@@ -393,17 +404,18 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             if (tid == 96) putR(Tc, q[0][0], q[1][0], q[2][0], q[3][0]);
         }
     }
-    __syncthreads();                                  // E rows, s_rh; mbarriers initialised
-    cl_arrive_relaxed();                              // cluster phase: every CTA has started
+    __syncthreads();                                  // E rows; mbarriers initialised
+    if (CLU) cl_arrive_relaxed();                     // cluster phase: every CTA has started
     CL_MARK(1);
     CL_MARK(2);
     CL_MARK(3);
 
     TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
     if (dtm == 0.0) {                                 // member at t_end: uniform over the cluster
+        if (MODE == CL_MODE_TIPS) return;             // (its separators are not used)
         carry_tile<FINAL, BATHY>(P, B, mo, s, s + Tc, lam, acc);
         __syncwarp();
-        cl_wait();
+        if (CLU) cl_wait();
         tile_epilogue<FINAL>(P, c, m, dtm, acc, tm0, tend0);
         return;
     }
@@ -620,6 +632,24 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
         const double Yr = fin[2 * PSTR + tid + 1], Vr = fin[3 * PSTR + tid + 1], Wr = fin[4 * PSTR + tid + 1];
         const double Yks = fin[2 * PSTR + ks - 1], Vks = fin[3 * PSTR + ks - 1], Wks = fin[4 * PSTR + ks - 1];
         CL_MARK(5);
+        const int cp_ = (c + 1 < C) ? c + 1 : 0, cm_ = (c > 0) ? c - 1 : C - 1;
+        double Lm = 0.0, Lc, Lp = 0.0;
+        double nx[6];                                 // the next tile's left part (P1, Q1, R1, Y0, V0, W0)
+        if constexpr (MODE == CL_MODE_TIPS) {
+            // publish to global memory: the same 12 values as the DSMEM exchange
+            double *const tp = P.sp_tips + (size_t(m) * C + c) * XPUB;
+            if (tid == 0) { tp[6] = dm[0]; tp[7] = am[0]; tp[8] = cm[0]; tp[9] = D_; tp[10] = V_; tp[11] = W_; }
+            if (tid == ks) { tp[0] = aE; tp[1] = cE; tp[2] = dE; tp[3] = Yks; tp[4] = Vks; tp[5] = Wks; }
+            return;
+        } else if constexpr (MODE == CL_MODE_FINISH) {
+            const double *const Lv = P.sp_L + size_t(m) * C;
+            Lc = Lv[c];
+            if (c > 0 || cyc) Lm = Lv[cm_];
+            if (c + 1 < C || cyc) Lp = Lv[cp_];
+            const double *const tn = P.sp_tips + (size_t(m) * C + cp_) * XPUB;
+#pragma unroll
+            for (int k = 0; k < 6; k++) nx[k] = tn[6 + k];
+        } else {
         // publish (DSMEM, st.async): warp 0 sends the first-row relation of chunk 0
         // and (Y, V, W) of slot 0 (what the previous CTA's separator row needs);
         // the warp of thread ks sends the raw reduced row of the separator chunk
@@ -672,8 +702,6 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             const double id = rcp(dia);
             a = sub * id; cc = sup * id; d = rhs * id;
         };
-        const int cp_ = (c + 1 < C) ? c + 1 : 0, cm_ = (c > 0) ? c - 1 : C - 1;
-        double Lm = 0.0, Lc, Lp = 0.0;
         {
             // the couplings of neighbouring separators go through the spike tips
             // (~ r^T): usually equations c-1, c, c+1 are decoupled to round-off
@@ -717,6 +745,9 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 Lp = __shfl_sync(0xffffffffu, Lj, cp_);
             }
         }
+#pragma unroll
+        for (int k = 0; k < 6; k++) nx[k] = s_cx[cp_][6 + k];
+        }
         // chunk ends: X_k = Y_k - V_k L_{j-1} - W_k L_j (interior), X_ks = L_j
         const double Xk = tid < ks ? D_ - V_ * Lm - W_ * Lc : (tid == ks ? Lc : 0.0);
         const double XL = tid == 0 ? Lm : Yl - Vl * Lm - Wl * Lc;
@@ -732,8 +763,8 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             } else if (right_phys) {
                 hRn = hb[CMCH - 1];                             // Neumann hbar_Tc := hbar_{Tc-1}
             } else {
-                const double X0n = s_cx[cp_][9] - s_cx[cp_][10] * Lc - s_cx[cp_][11] * Lp;
-                hRn = s_cx[cp_][6] - s_cx[cp_][7] * Lc - s_cx[cp_][8] * X0n;
+                const double X0n = nx[3] - nx[4] * Lc - nx[5] * Lp;
+                hRn = nx[0] - nx[1] * Lc - nx[2] * X0n;
             }
         } else {
 #pragma unroll
@@ -785,6 +816,12 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) acc.err |= ERR_NONFINITE;
         }
     }
+    // FINISH mode with the filter: the two rows at an interior tile end need the
+    // neighbouring tile's rows -- filter_fix_kernel completes them (and their dt
+    // maxima); here they stay unfiltered
+    auto fix_row = [&](int i) -> bool {
+        return !CLU && filt && ((tid == 0 && i < 2 && !left_phys) || (tid == ks && i >= 2 && !right_phys));
+    };
     if (filt) {
         // A19 on q, W: own rows into A2 (q), A3 (W); rows -2, -1, Tc, Tc+1 from
         // the neighbouring CTAs (DSMEM) or mirrored at physical ends (A10)
@@ -798,6 +835,10 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 const double pq = wall_l ? -1.0 : 1.0;
                 sQb[swz(-1)] = pq * qbv[0]; sWb[swz(-1)] = Wbv[0];
                 sQb[swz(-2)] = wall_l ? pq * qbv[1] : qbv[0]; sWb[swz(-2)] = wall_l ? Wbv[1] : Wbv[0];
+            } else if (!CLU) {                        // FINISH: rows 0..3 for filter_fix_kernel
+                double *const fb = P.sp_fb + (size_t(m) * C + c) * 16;
+#pragma unroll
+                for (int i = 0; i < CMCH; i++) { fb[i] = qbv[i]; fb[4 + i] = Wbv[i]; }
             } else {
                 const int cl_ = (c > 0) ? c - 1 : C - 1;
                 const int Tl = (cl_ == C - 1) ? n - (C - 1) * P.T : P.T;
@@ -812,6 +853,10 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 const double pq = wall_r ? -1.0 : 1.0;
                 sQb[swz(Tc)] = pq * qbv[3]; sWb[swz(Tc)] = Wbv[3];
                 sQb[swz(Tc + 1)] = wall_r ? pq * qbv[2] : qbv[3]; sWb[swz(Tc + 1)] = wall_r ? Wbv[2] : Wbv[3];
+            } else if (!CLU) {                        // FINISH: rows Tc-4..Tc-1
+                double *const fb = P.sp_fb + (size_t(m) * C + c) * 16 + 8;
+#pragma unroll
+                for (int i = 0; i < CMCH; i++) { fb[i] = qbv[i]; fb[4 + i] = Wbv[i]; }
             } else {
                 const int cr_ = (c + 1 < C) ? c + 1 : 0;
                 st_remote(sQb + swz(-2), &s_fmb, cr_, qbv[2]);
@@ -821,7 +866,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             }
         }
         __syncthreads();                              // own rows and mirrored ghosts
-        mbar_wait(fmb, 0u);                           // neighbours' rows
+        if (CLU) mbar_wait(fmb, 0u);                  // neighbours' rows
         if (live) {
             const double sig16 = P.filter_sigma * (1.0 / 16.0);
             double xq[CMCH + 4], xw[CMCH + 4];
@@ -833,6 +878,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             for (int i = 0; i < CMCH; i++) { xq[i + 2] = qbv[i]; xw[i + 2] = Wbv[i]; }
 #pragma unroll
             for (int i = 0; i < CMCH; i++) {
+                if (fix_row(i)) continue;             // FINISH: completed by filter_fix_kernel
                 // f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
                 qbv[i] = xq[i + 2] - sig16 * (xq[i] - 4.0 * xq[i + 1] + 6.0 * xq[i + 2] - 4.0 * xq[i + 3] + xq[i + 4]);
                 Wbv[i] = xw[i + 2] - sig16 * (xw[i] - 4.0 * xw[i + 1] + 6.0 * xw[i + 2] - 4.0 * xw[i + 3] + xw[i + 4]);
@@ -845,17 +891,28 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     if (live) {
         double oh[CMCH], oK[CMCH];
 #pragma unroll
+        const bool relax = FINAL && (P.gen_rate > 0.0 || P.sp_rate > 0.0);
+        const double t_new = relax ? P.t[P.kpar * P.members + m] + dtm : 0.0;
         for (int i = 0; i < CMCH; i++) {
-            const double h0 = hb[i];
+            double h0 = hb[i];
             const double Hb = HdD[i] * (h0 * h0);
-            oh[i] = h0;
-            oK[i] = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
-            if (FINAL) {
+            double Ko = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
+            if (relax && !fix_row(i)) {
+                // A10 relaxation zones at t^{n+1}, after the filter
+                relax_cell(P, P.x_min + (double(s + r0 + i) + 0.5) * P.dx, bbv[i], t_new, h0, qbv[i], Ko, Wbv[i]);
+                const double ih = rcp(h0);
+                const double u = fabs(qbv[i] * ih), sg = (Ko - 1.5 * h0 * bbv[i]) * ih * ih;
+                const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
+                acc.umax = u > acc.umax ? u : acc.umax;
+                acc.numax = nu > acc.numax ? nu : acc.numax;
+            } else if (FINAL && !fix_row(i)) {
                 const double u = fabs(qbv[i] * ihv[i]), sg = HdD[i];
                 const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
                 acc.umax = u > acc.umax ? u : acc.umax;
                 acc.numax = nu > acc.numax ? nu : acc.numax;
             }
+            oh[i] = h0;
+            oK[i] = Ko;
         }
         const size_t gd = mo + size_t(s + r0);
         double2 *const o0 = reinterpret_cast<double2 *>(B.out[0] + gd);
@@ -869,7 +926,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     }
     CL_MARK(9);
     tile_epilogue<FINAL>(P, c, m, dtm, acc, tm0, tend0);
-    mbar_wait(xmb2, 0u);                              // no remote store may target an exited CTA
+    if (CLU) mbar_wait(xmb2, 0u);                     // no remote store may target an exited CTA
 #if HSGN_EXP_TIMING
     CL_MARK(10);
     if (tid == 0) {
@@ -878,6 +935,250 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
         atomicAdd(gg + 15, 1ull);
     }
 #endif
+}
+
+}  // namespace hsgn
+
+namespace hsgn {
+
+// ---------------------------------------------------------------------------
+// Tile-level SPIKE, step 2: the separator system of every member (one CTA per
+// member), from the tiles' published values (P.sp_tips, CL_MODE_TIPS):
+//     -a V' L_{j-1} + (B - a W' + c R1 V0) L_j + c R1 W0 L_{j+1}
+//        = d - c P1 - a Y' + c R1 Y0                        (j = 0 .. G-1)
+// (the same equations as the cluster kernel's; cyclic for periodic members),
+// solved exactly by the same scheme one level up: thread chunks of separators
+// eliminated sequentially (partition method, per-row relations in P.sp_S),
+// the chunk ends by PCR with two spike columns, the last chunk end (L_{G-1})
+// as the block's single separator.  Writes L to P.sp_L.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sep_equation(const double *tips, int G, bool cyc, int j, double &a, double &cc,
+                                             double &d)
+{
+    const double *o = tips + size_t(j) * XPUB;
+    const int jn = (j + 1 < G) ? j + 1 : (cyc ? 0 : -1);
+    double P1n = 0, Q1n = 0, R1n = 0, Y0 = 0, V0 = 0, W0 = 0;
+    if (jn >= 0) {
+        const double *l = tips + size_t(jn) * XPUB;
+        P1n = l[6]; Q1n = l[7]; R1n = l[8]; Y0 = l[9]; V0 = l[10]; W0 = l[11];
+    }
+    const double aEj = o[0], cEj = o[1], dEj = o[2], Yp = o[3], Vp = o[4], Wp = o[5];
+    const double cr = cEj * R1n;
+    const double sub = -aEj * Vp;
+    const double dia = (1.0 - cEj * Q1n) - aEj * Wp + cr * V0;
+    const double sup = cr * W0;
+    const double rhs = dEj - cEj * P1n - aEj * Yp + cr * Y0;
+    const double id = rcp(dia);
+    a = sub * id; cc = sup * id; d = rhs * id;
+}
+
+__global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
+{
+    __shared__ double pb[2][5][PSTR];
+    __shared__ double sw[CNT / 32][3];
+    __shared__ float sred[CNT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int m = blockIdx.x;
+    const int G = P.tiles;
+    const bool cyc = P.bcl == BC_PERIODIC;
+    const double *const tips = P.sp_tips + size_t(m) * G * XPUB;
+    double *const Lout = P.sp_L + size_t(m) * G;
+    double *const S = P.sp_S + size_t(m) * G * 3;
+    if (G == 1) {                                     // one tile: its separator couples to itself
+        if (tid == 0) {
+            double a, cc, d;
+            sep_equation(tips, G, cyc, 0, a, cc, d);
+            Lout[0] = cyc ? d * rcp(1.0 + a + cc) : d;
+        }
+        return;
+    }
+    const int mch = (G + CNT - 1) / CNT;              // separators per thread chunk
+    const int ta = (G + mch - 1) / mch;               // active chunks (>= 2)
+    const int ks = ta - 1;                            // the block's separator chunk
+    const int j0 = tid * mch, j1 = min(G, j0 + mch);
+    const bool live = tid < ta;
+    // forward sweep: x_i + am_i X_{k-1} + cm_i x_{i+1} = dm_i
+    double am = 0.0, cm = 0.0, dm = 0.0;
+    if (live) {
+        for (int j = j0; j < j1; j++) {
+            double a, cc, d;
+            sep_equation(tips, G, cyc, j, a, cc, d);
+            if (j == j0) {
+                am = a; cm = cc; dm = d;
+            } else {
+                const double inv = rcp(1.0 - a * cm);
+                am = -a * am * inv;
+                cm = cc * inv;
+                dm = (d - a * dm) * inv;
+            }
+            S[3 * size_t(j)] = am; S[3 * size_t(j) + 1] = cm; S[3 * size_t(j) + 2] = dm;
+        }
+    }
+    const double aE = am, cE = cm, dE = dm;
+    // upward: x_i = P_i - Q_i X_{k-1} - R_i X_k (X_k = x_{j1-1})
+    double P0 = 0.0, Q0 = 0.0, R0 = 0.0;
+    if (live) {
+        double Pn = 0.0, Qn = 0.0, Rn = -1.0;
+        S[3 * size_t(j1 - 1)] = 0.0; S[3 * size_t(j1 - 1) + 1] = 0.0; S[3 * size_t(j1 - 1) + 2] = -1.0;
+        for (int j = j1 - 2; j >= j0; j--) {
+            const double a_ = S[3 * size_t(j)], c_ = S[3 * size_t(j) + 1], d_ = S[3 * size_t(j) + 2];
+            const double Pi = d_ - c_ * Pn, Qi = a_ - c_ * Qn, Ri = -c_ * Rn;
+            S[3 * size_t(j)] = Pi; S[3 * size_t(j) + 1] = Qi; S[3 * size_t(j) + 2] = Ri;
+            Pn = Pi; Qn = Qi; Rn = Ri;
+        }
+        P0 = Pn; Q0 = Qn; R0 = Rn;
+        if (j1 - j0 == 1) { P0 = 0.0; Q0 = 0.0; R0 = -1.0; }
+    }
+    // the next chunk's first-row relation (thread ks: chunk 0's, the cyclic wrap)
+    double P1 = __shfl_down_sync(0xffffffffu, P0, 1), Q1 = __shfl_down_sync(0xffffffffu, Q0, 1);
+    double R1 = __shfl_down_sync(0xffffffffu, R0, 1);
+    if (lane == 0) { sw[wid][0] = P0; sw[wid][1] = Q0; sw[wid][2] = R0; }
+    __syncthreads();
+    if (lane == 31) {
+        if (wid + 1 < CNT / 32) { P1 = sw[wid + 1][0]; Q1 = sw[wid + 1][1]; R1 = sw[wid + 1][2]; }
+        else { P1 = Q1 = R1 = 0.0; }
+    }
+    const double P00 = sw[0][0], Q00 = sw[0][1], R00 = sw[0][2];     // chunk 0's first-row relation
+    double A_ = aE, C_ = -cE * R1, D_ = dE - cE * P1, V_ = 0.0, W_ = 0.0;
+    {
+        const double ib = rcp(1.0 - cE * Q1);
+        A_ *= ib; C_ *= ib; D_ *= ib;
+    }
+    if (tid == 0) { V_ = A_; A_ = 0.0; }              // coupling to the separator (cyclic wrap)
+    if (tid == ks - 1) { W_ = C_; C_ = 0.0; }         // coupling to the separator
+    if (tid >= ks) { A_ = C_ = D_ = V_ = W_ = 0.0; }
+    double *const b0 = &pb[0][0][PPAD], *const b1 = &pb[1][0][PPAD];
+    auto put = [&](double *b, int k, double a, double cc, double d, double v, double w_) {
+        b[k] = a; b[PSTR + k] = cc; b[2 * PSTR + k] = d; b[3 * PSTR + k] = v; b[4 * PSTR + k] = w_;
+    };
+    put(b0, tid, A_, C_, D_, V_, W_);
+    if (tid < 2 * PPAD) {
+        const int k = tid < PPAD ? tid - PPAD : CNT + tid - PPAD;
+        put(b0, k, 0.0, 0.0, 0.0, 0.0, 0.0);
+        put(b1, k, 0.0, 0.0, 0.0, 0.0, 0.0);
+    }
+    {
+        const float ea = float(fabs(A_)), ec = float(fabs(C_));
+        const float ev = warp_max_nonneg(ea > ec ? ea : ec);
+        if (lane == 0) sred[wid] = ev;
+    }
+    __syncthreads();
+    int lim = CNT;
+    {
+        float e0 = 0.0f;
+        for (int q = 0; q < CNT / 32; q++) e0 = fmaxf(e0, sred[q]);
+        if (e0 < 0.4f) {
+            const float q = __fdividef(64.0f, -__log2f(e0) - 0.28f);
+            const int qi = int(ceilf(q));
+            lim = qi <= 1 ? 1 : min(CNT, 1 << (32 - __clz(qi - 1)));
+        }
+    }
+    const double *fin = b0;
+    for (int sd = 1, pp = 0; sd < lim; sd <<= 1, pp ^= 1) {
+        const double *cur = pp ? b1 : b0;
+        double *nxt = pp ? b0 : b1;
+        int km = tid - sd, kp = tid + sd;
+        const bool okm = km >= -PPAD, okp = kp < CNT + PPAD;
+        km = okm ? km : 0; kp = okp ? kp : 0;
+        double Am = cur[km], Cm = cur[PSTR + km], Dm = cur[2 * PSTR + km], Vm = cur[3 * PSTR + km], Wm = cur[4 * PSTR + km];
+        double Ap = cur[kp], Cp = cur[PSTR + kp], Dp = cur[2 * PSTR + kp], Vp = cur[3 * PSTR + kp], Wp = cur[4 * PSTR + kp];
+        if (!okm || tid - sd < 0) { Am = Cm = Dm = Vm = Wm = 0.0; }
+        if (!okp || tid + sd >= CNT) { Ap = Cp = Dp = Vp = Wp = 0.0; }
+        const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
+        const double An = -A_ * Am * ib, Cn = -C_ * Cp * ib;
+        D_ = (D_ - A_ * Dm - C_ * Dp) * ib;
+        V_ = (V_ - A_ * Vm - C_ * Vp) * ib;
+        W_ = (W_ - A_ * Wm - C_ * Wp) * ib;
+        A_ = An; C_ = Cn;
+        put(nxt, tid, A_, C_, D_, V_, W_);
+        __syncthreads();
+        fin = nxt;
+    }
+    // the block's separator L_s = L_{G-1}: its equation couples to the last
+    // interior chunk end (Y', V', W') and, through chunk 0's first row, to chunk
+    // end 0 (Y0, V0, W0); cyclic: L_{j-1} = L_{j+1} = L_s (one block)
+    __shared__ double sL;
+    if (tid == ks) {
+        const double Yp = fin[2 * PSTR + ks - 1], Vp = fin[3 * PSTR + ks - 1], Wp = fin[4 * PSTR + ks - 1];
+        double Pn = 0, Qn = 0, Rn = 0, Y0 = 0, V0 = 0, W0 = 0;
+        if (cyc) {
+            Pn = P00; Qn = Q00; Rn = R00;
+            Y0 = fin[2 * PSTR]; V0 = fin[3 * PSTR]; W0 = fin[4 * PSTR];
+        }
+        const double cr = cE * Rn;
+        const double sub = -aE * Vp, dia = (1.0 - cE * Qn) - aE * Wp + cr * V0, sup = cr * W0;
+        const double rhs = dE - cE * Pn - aE * Yp + cr * Y0;
+        sL = cyc ? rhs * rcp(sub + dia + sup) : rhs * rcp(dia);
+    }
+    __syncthreads();
+    const double Ls = sL;
+    const double Xk = tid < ks ? D_ - (V_ + W_) * Ls : (tid == ks ? Ls : 0.0);
+    double XL = 0.0;
+    if (tid == 0) XL = cyc ? Ls : 0.0;
+    else if (tid <= ks) XL = (tid - 1 == ks) ? Ls : fin[2 * PSTR + tid - 1] - (fin[3 * PSTR + tid - 1] + fin[4 * PSTR + tid - 1]) * Ls;
+    if (live) {
+        for (int j = j0; j < j1; j++) {
+            const double Pi = S[3 * size_t(j)], Qi = S[3 * size_t(j) + 1], Ri = S[3 * size_t(j) + 2];
+            Lout[j] = (j == j1 - 1) ? Xk : Pi - Qi * XL - Ri * Xk;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tile-level SPIKE, A19 filter at the interior tile ends (final stage): rows
+// T-2, T-1 of tile b-1 and rows 0, 1 of tile b from the unfiltered rows
+// T-4 .. T-1 and 0 .. 3 (P.sp_fb), written to the output state; their dt
+// maxima join the member's.  Four threads per tile end.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) filter_fix_kernel(const Params P, const Bufs B)
+{
+    const int m = blockIdx.y;
+    const int G = P.tiles;
+    const bool cyc = P.bcl == BC_PERIODIC;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int bnd = t >> 2, i = (t & 3) + 2;          // tile end b between tiles b-1 and b; row 2..5
+    double um = 0.0, nm = 0.0;
+    const bool act = bnd < G && (cyc || bnd > 0) && P.dt[m] != 0.0;   // (dt = 0: the member was carried)
+    if (act) {
+        const int bl = bnd > 0 ? bnd - 1 : G - 1;
+        const int Tl = (bl == G - 1) ? P.n - (G - 1) * P.T : P.T;
+        const double *fl = P.sp_fb + (size_t(m) * G + bl) * 16 + 8;     // rows Tl-4 .. Tl-1
+        const double *fr = P.sp_fb + (size_t(m) * G + bnd) * 16;        // rows 0 .. 3
+        double xq[8], xw[8];
+#pragma unroll
+        for (int k = 0; k < 4; k++) { xq[k] = fl[k]; xw[k] = fl[4 + k]; xq[4 + k] = fr[k]; xw[4 + k] = fr[4 + k]; }
+        const double sig16 = P.filter_sigma * (1.0 / 16.0);
+        double qo = 0.0, wo = 0.0;
+#pragma unroll
+        for (int k = 2; k < 6; k++)
+            if (k == i) {
+                qo = xq[k] - sig16 * (xq[k - 2] - 4.0 * xq[k - 1] + 6.0 * xq[k] - 4.0 * xq[k + 1] + xq[k + 2]);
+                wo = xw[k] - sig16 * (xw[k - 2] - 4.0 * xw[k - 1] + 6.0 * xw[k] - 4.0 * xw[k + 1] + xw[k + 2]);
+            }
+        const int cell = i < 4 ? bl * P.T + Tl - 4 + i : bnd * P.T + (i - 4);
+        const size_t g = size_t(m) * P.n + cell;
+        double h = B.out[0][g], K = B.out[2][g];
+        const double bb = P.b ? P.b[cell] : 0.0;
+        if (P.gen_rate > 0.0 || P.sp_rate > 0.0)           // A10 zones after the filter, at t^{n+1}
+            relax_cell(P, P.x_min + (double(cell) + 0.5) * P.dx, bb, P.t[P.kpar * P.members + m] + P.dt[m],
+                       h, qo, K, wo);
+        B.out[0][g] = h;
+        B.out[1][g] = qo;
+        B.out[2][g] = K;
+        B.out[3][g] = wo;
+        if (!isfinite(qo + wo)) atomicOr(P.err, ERR_NONFINITE);
+        const double ih = rcp(h);
+        const double u = fabs(qo * ih), sg = (K - 1.5 * h * bb) * ih * ih;
+        um = u;
+        nm = u + fsqrt(P.g * h + P.lam[m] * (1.0 / 3.0) * sg * sg);
+    }
+    um = warp_max_nonneg(um);
+    nm = warp_max_nonneg(nm);
+    if ((threadIdx.x & 31) == 0 && nm > 0.0) {
+        const int slot_w = (P.kslot + 1) % 3;
+        atomicMax(P.maxes + (slot_w * 2 + 0) * P.members + m, (unsigned long long)__double_as_longlong(um));
+        atomicMax(P.maxes + (slot_w * 2 + 1) * P.members + m, (unsigned long long)__double_as_longlong(nm));
+    }
 }
 
 }  // namespace hsgn

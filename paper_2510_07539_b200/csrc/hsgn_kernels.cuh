@@ -83,6 +83,10 @@ struct Params {
     unsigned int *done;
     unsigned long long *rho_obs;     // max rho over tiles (double bits)
     unsigned int *kmin;              // min kappa = beta seen: max of ~khi_key (see khi_key)
+    // tile-level SPIKE (hsgn_cluster.cuh CL_MODE_TIPS / FINISH, sep_solve_kernel,
+    // filter_fix_kernel): per member and tile 12 published values, the separator
+    // value L, 16 unfiltered boundary values; per member and tile 3 scratch
+    double *sp_tips, *sp_L, *sp_fb, *sp_S;
     const Ctrl *ctrl;
     int kslot, kpar;                 // host step index k: k mod 3, k mod 2
     // slab decomposition (BC_HALO sides): ghost cells received from the

@@ -235,9 +235,10 @@ class Solver:
         self._chk(self.L.hsgn_set_well_balanced(self.ctx, 1 if on else 0))
 
     def set_cluster(self, mode) -> None:
-        """Cluster stage kernels with the exact cross-CTA depth solve: True/1 =
-        whenever the member fits, False/0 = never (overlapped tiles), 2 = auto
-        (default: only for material-CFL-only stepping) (hsgn_set_cluster)."""
+        """Exact depth solve across tiles (hsgn_set_cluster): 1/True = cluster
+        kernels whenever the member fits, 3 = tile-level SPIKE, 0/False = never
+        (overlapped tiles), 2 = auto (default: exact paths only for
+        material-CFL-only stepping)."""
         self._chk(self.L.hsgn_set_cluster(self.ctx, int(mode)))
 
     @property
@@ -246,6 +247,13 @@ class Solver:
         a, b = C.c_int32(), C.c_int32()
         on = int(self.L.hsgn_get_cluster(self.ctx, C.byref(a), C.byref(b)))
         return (a.value, b.value) if on == 1 else None
+
+    @property
+    def spike(self):
+        """(tiles, tile rows) if the next step runs on tile-level SPIKE, else None."""
+        a, b = C.c_int32(), C.c_int32()
+        on = int(self.L.hsgn_get_cluster(self.ctx, C.byref(a), C.byref(b)))
+        return (a.value, b.value) if on == 2 else None
 
     @property
     def launches(self) -> int:

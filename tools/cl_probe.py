@@ -15,8 +15,8 @@ cl = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 cells = int(sys.argv[4]) if len(sys.argv) > 4 else 4096
 w = W.cfg3(members=members, n=cells)
 s = hs.solver_for(w)
-s.set_cluster(bool(cl))
-print("cluster", s.cluster, "geometry", s.geometry)
+s.set_cluster(cl)
+print("cluster", s.cluster, "spike", s.spike, "geometry", s.geometry)
 s.run_steps(3)
 s.sync()
 ms1, ms2, tot = s.run_steps_timed(steps, total=True)

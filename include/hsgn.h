@@ -314,6 +314,22 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
  * Drops captured graphs.  Errors: HSGN_E_INVALID (null context, mode outside
  * 0..3). */
 hsgn_status hsgn_set_cluster(hsgn_ctx *ctx, int32_t mode);
+/* Member-resident stepping (hsgn_multi.cuh): the C CTAs
+ * of every member (one cluster, as for the cluster kernels: the member must
+ * fit) load its state once, advance it by n_steps full SI-IMEX steps with the
+ * dt rule of P:613-617 (per member, the last step clipped to t_end if t_end > 0,
+ * S:342; a member at t_end stays there for the remaining steps), keeping the state, the stage inputs E2, R2 and
+ * all intermediates in shared memory and exchanging only edge rows,
+ * separator data and dt maxima between the CTAs (DSMEM), and store it once.
+ * Same arithmetic as hsgn_run_steps on the cluster kernels up to rounding
+ * order (E2, R2 formed in the H-form).  Synchronous; *device_ms (or NULL)
+ * receives the kernel's device time.  2-stage tableau, SI scheme without
+ * Picard passes, the A25 form or slab sides.  On a device error (coercivity,
+ * dry bed, non-finite, dt) the call returns it and the state stays at the
+ * call's start for every member; otherwise n_steps steps are committed.
+ * Errors: HSGN_E_INVALID (not eligible, n_steps < 0), HSGN_E_NOWORKSPACE,
+ * HSGN_E_CUDA, device errors as above. */
+hsgn_status hsgn_run_resident(hsgn_ctx *ctx, int64_t n_steps, double t_end, double *device_ms);
 /* 1 if the next step runs on the cluster kernels, 2 if on tile-level SPIKE
  * (then *ctas = CTAs (tiles) per member and *tile_rows = rows per tile, the last
  * n_cells - (ctas - 1) * tile_rows), 0 for the overlapped tiles (both 0), -1 for

@@ -21,6 +21,7 @@
 #include "../../include/hsgn.h"
 #include "hsgn_kernels.cuh"
 #include "hsgn_cluster.cuh"
+#include "hsgn_multi.cuh"
 
 using namespace hsgn;
 
@@ -366,6 +367,14 @@ int launches_per_step(const hsgn_ctx *c)
         return 3 * c->tab.stages + fix + 1;
     }
     return c->tab.stages + 1;
+}
+
+template <bool BATHY>
+void multi_attrs()
+{
+    cudaFuncSetAttribute(cl_multi_kernel<BATHY>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cl_multi_kernel<BATHY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(BATHY ? CSMEM_BYTES_B : CSMEM_BYTES));
 }
 
 template <bool S2, bool FIN, bool BATHY>
@@ -1049,6 +1058,7 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cl_attrs<false, false, false>(); cl_attrs<false, false, true>();
     cl_attrs<true, true, false>(); cl_attrs<true, true, true>();
     cl_attrs<false, true, false>(); cl_attrs<false, true, true>();
+    multi_attrs<false>(); multi_attrs<true>();
     if (const char *e = std::getenv("HSGN_CLUSTER")) c->cl_mode = std::atoi(e);
     choose_geometry(c);
     if (!slab) { choose_cluster(c); choose_spike(c); }
@@ -1619,6 +1629,65 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *c, int32_t on)
     c->wb = on != 0;
     drop_graphs(c);
     choose_geometry(c);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_run_resident(hsgn_ctx *c, int64_t n_steps, double t_end, double *device_ms)
+{
+    hsgn_status st = ready(c);
+    if (st != HSGN_OK) return st;
+    if (n_steps < 0 || n_steps > (1 << 30)) return fail(c, HSGN_E_INVALID, "run_resident: n_steps out of range");
+    if (c->clC <= 0 || !exact_eligible(c) || c->tab.stages != 2)
+        return fail(c, HSGN_E_INVALID, "run_resident: member must fit a cluster (n % 4 == 0, <= 16 x 512 cells), "
+                                       "SI scheme, 2-stage tableau, no Picard / A25 / slab sides");
+    st = reconcile(c);
+    if (st != HSGN_OK) return st;
+    st = set_ctrl(c, t_end > 0.0 ? t_end : 0.0, 0.0);
+    if (st != HSGN_OK) return st;
+    if (n_steps == 0) { if (device_ms) *device_ms = 0.0; return HSGN_OK; }
+    const long long k0 = c->host_steps;
+    Params P = make_params(c, k0);
+    P.T = c->clT;
+    P.tiles = c->clC;
+    Bufs B{};
+    for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; B.out[f] = c->buf[c->cur ^ 1][f]; }
+    CUDA_TRY(c, cudaMemsetAsync(c->maxes, 0, 6 * size_t(c->members) * 8, c->stream));
+    if (!c->ev_start) CUDA_TRY(c, cudaEventCreate(&c->ev_start));
+    cudaEvent_t e1;
+    CUDA_TRY(c, cudaEventCreate(&e1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->clC, c->members);
+    cfg.blockDim = dim3(CNT);
+    cfg.dynamicSmemBytes = c->bathy ? CSMEM_BYTES_B : CSMEM_BYTES;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(c->clC);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaEventRecord(c->ev_start, c->stream));
+    if (c->bathy) CUDA_TRY(c, cudaLaunchKernelEx(&cfg, cl_multi_kernel<true>, P, B, int(n_steps), int(k0)));
+    else CUDA_TRY(c, cudaLaunchKernelEx(&cfg, cl_multi_kernel<false>, P, B, int(n_steps), int(k0)));
+    CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+    c->launches++;
+    CUDA_TRY(c, cudaEventSynchronize(e1));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, c->ev_start, e1);
+    cudaEventDestroy(e1);
+    if (device_ms) *device_ms = ms;
+    unsigned int bits = 0;
+    CUDA_TRY(c, cudaMemcpy(&bits, c->err, sizeof(bits), cudaMemcpyDeviceToHost));
+    if (bits) return fail(c, status_from_bits(bits), "run_resident: device error bits; state kept at the call's start");
+    // commit: the output buffer becomes the state, n_steps more steps
+    long long ds = 0;
+    CUDA_TRY(c, cudaMemcpy(&ds, c->steps, sizeof(ds), cudaMemcpyDeviceToHost));
+    ds += n_steps;
+    CUDA_TRY(c, cudaMemcpy(c->steps, &ds, sizeof(ds), cudaMemcpyHostToDevice));
+    c->cur ^= 1;
+    c->host_steps += n_steps;
+    c->dev_steps = ds;
     return HSGN_OK;
 }
 

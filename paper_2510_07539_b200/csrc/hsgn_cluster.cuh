@@ -143,16 +143,18 @@ __device__ __forceinline__ double cl_pick6(const double (&v)[6], int k)
 // of the swizzled tile; same arithmetic as row_update (hsgn_kernels.cuh).
 // R = (h, q, H, W) of the row (stage 1: R = E) is read from the row's slot of
 // (sDe, sQd, sHd, sBe), which then take delta, q^dag, H^dag, beta.
-template <bool BATHY>
+template <bool BATHY, bool R_IS_E = false>
 __device__ __forceinline__ void cl_row_update(const RowCtx &C, const double *sB, int r,
                                               const double (&ch)[3], const double (&cq)[3],
                                               const double (&cH)[3], const double (&cW)[3],
                                               const Face &Fl, const Face &Fr, double *sQd, double *sHd,
                                               double *sBe, double *sDe, double &Wd_out, double &beta_out,
-                                              double &hR_out)
+                                              double &hR_out, bool r_is_e = R_IS_E)
 {
     const int x = swz(r);
-    const double hR = sDe[x], qR = sQd[x], HR = sHd[x], WR = sBe[x];      // R of the row
+    // R of the row (r_is_e: stage 1, R = E)
+    const double hR = r_is_e ? ch[1] : sDe[x], qR = r_is_e ? cq[1] : sQd[x];
+    const double HR = r_is_e ? cH[1] : sHd[x], WR = r_is_e ? cW[1] : sBe[x];
     const double hE = ch[1], qE = cq[1], HE = cH[1];
     const double s2 = hE * hE, den = s2 + C.lt2;
     const double Z = rcp(hE * den);
@@ -181,11 +183,11 @@ __device__ __forceinline__ void cl_row_update(const RowCtx &C, const double *sB,
 
 // Phase 1 of one isolated row r (rows -1 and T of the tile): faces r -+ 1/2
 // from E rows r-2 .. r+2.
-template <bool BATHY>
+template <bool BATHY, bool R_IS_E = false>
 __device__ __forceinline__ void cl_single_row(const RowCtx &C, double kap, const double *sB, int r,
                                               const double *sEh, const double *sEq, const double *sEH,
                                               const double *sEW, double *sQd, double *sHd, double *sBe,
-                                              double *sDe)
+                                              double *sDe, bool r_is_e = R_IS_E)
 {
     double xh[5], xq[5], xH[5], xW[5];
 #pragma unroll
@@ -205,7 +207,7 @@ __device__ __forceinline__ void cl_single_row(const RowCtx &C, double kap, const
     const FState Pn = muscl_plus(ch, cq, cH, cW, kap);        // Pl_{r+1}
     const Face Fl = rusanov(Mm, Pl), Fr = rusanov(Mr, Pn);
     double Wd, hR, beta;
-    cl_row_update<BATHY>(C, sB, r, bh, bq, bH, bW, Fl, Fr, sQd, sHd, sBe, sDe, Wd, beta, hR);
+    cl_row_update<BATHY, R_IS_E>(C, sB, r, bh, bq, bH, bW, Fl, Fr, sQd, sHd, sBe, sDe, Wd, beta, hR, r_is_e);
 }
 
 #if HSGN_EXP_TIMING

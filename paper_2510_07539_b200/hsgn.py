@@ -62,7 +62,8 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_set_picard", "hsgn_set_well_balanced", "hsgn_set_cluster", "hsgn_get_cluster",
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
            "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl",
-           "hsgn_slab_xfer_count", "hsgn_slab_get", "hsgn_slab_put", "hsgn_slab_phase"]
+           "hsgn_slab_xfer_count", "hsgn_slab_get", "hsgn_slab_put", "hsgn_slab_phase",
+           "hsgn_run_resident"]
 
 XFER = {"maxima": 0, "un": 1, "u1": 2, "b": 3}
 PHASE = {"dt": 0, "stage1": 1, "stage2": 2, "commit": 3}
@@ -118,6 +119,7 @@ def load_library(path: str = LIB_PATH):
         "hsgn_slab_get": (st, [vp, C.c_int32, vp]),
         "hsgn_slab_put": (st, [vp, C.c_int32, vp]),
         "hsgn_slab_phase": (st, [vp, C.c_int32]),
+        "hsgn_run_resident": (st, [vp, C.c_int64, C.c_double, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -339,6 +341,14 @@ class Solver:
             return d
         self._chk(self.L.hsgn_step(self.ctx, dt, None))
 
+    def run_resident(self, n_steps: int, t_end: float = 0.0) -> float:
+        """hsgn_run_resident: n_steps steps with every member resident in its
+        cluster's shared memory (one launch), the last step clipped to t_end if
+        t_end > 0; returns the device ms."""
+        ms = C.c_double()
+        self._chk(self.L.hsgn_run_resident(self.ctx, int(n_steps), float(t_end), C.byref(ms)))
+        return ms.value
+
     def run_steps(self, n_steps: int):
         self._chk(self.L.hsgn_run_steps(self.ctx, int(n_steps)))
 
@@ -425,6 +435,14 @@ class Group:
         if st != 0:
             raise HsgnError(st, self.L.hsgn_last_error(self.solvers[0].ctx).decode())
         self.g = h
+
+    def run_resident(self, n_steps: int, t_end: float = 0.0) -> float:
+        """hsgn_run_resident: n_steps steps with every member resident in its
+        cluster's shared memory (one launch), the last step clipped to t_end if
+        t_end > 0; returns the device ms."""
+        ms = C.c_double()
+        self._chk(self.L.hsgn_run_resident(self.ctx, int(n_steps), float(t_end), C.byref(ms)))
+        return ms.value
 
     def run_steps(self, n_steps: int):
         st = self.L.hsgn_group_run_steps(self.g, int(n_steps))

@@ -15,6 +15,13 @@ cl = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 cells = int(sys.argv[4]) if len(sys.argv) > 4 else 4096
 w = W.cfg3(members=members, n=cells)
 s = hs.solver_for(w)
+if cl == 4:                                   # member-resident stepping
+    s.set_cluster(1)
+    s.run_resident(3)
+    ms = s.run_resident(steps)
+    N = cells * members
+    print(f"resident: {ms / steps * 1e3:.1f} us/step, {2 * N * steps / (ms * 1e-3) / 1e9:.2f} G cell-stage/s")
+    raise SystemExit
 s.set_cluster(cl)
 print("cluster", s.cluster, "spike", s.spike, "geometry", s.geometry)
 s.run_steps(3)

@@ -16,13 +16,17 @@
 #pragma once
 #include "hsgn_cluster.cuh"
 
+#ifndef HSGN_MMINB
+#define HSGN_MMINB 4                                  // resident CTAs per SM (registers / shared memory)
+#endif
+
 namespace hsgn {
 
 __shared__ double s_dx[C_MAX][4];                     // dt maxima (u, nu), error flag of every CTA
 __shared__ __align__(8) unsigned long long s_emb, s_umb, s_dmb;
 
 template <bool BATHY>
-__global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_multi_kernel(const Params P, const Bufs B, const int K,
+__global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params P, const Bufs B, const int K,
                                                                    const int k0)
 {
     double *const sm = hsgn_smem;
@@ -206,11 +210,13 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_multi_kernel(const Params 
     int kdone = 0;
     const double kap = P.order == 2 ? 0.25 : 0.0;
 
+#pragma unroll 1
     for (int step = 0; step < K; step++) {
         if (dtm == 0.0) {                              // member at t_end (or stopped): carry
             continue;
         }
         // ===== the two IMEX stages; stage 2 inputs E2, R2 =====
+#pragma unroll 1
         for (int st = 0; st < 2; st++) {
             const bool st2 = st == 1;
             const StageC S = stage_consts(P, st2 ? P.aI2 : P.aI1, dtm, lam);

@@ -356,6 +356,12 @@ hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps);
 void hsgn_group_destroy(hsgn_group *g);
 /* 128-byte ncclUniqueId (rank 0; the caller broadcasts it, e.g. torch.distributed) */
 hsgn_status hsgn_nccl_unique_id(void *id);
+/* Collective over the `world` ranks (every rank calls it with the same id).
+ * Checks that every rank has the same overlap w and member count (an NCCL
+ * max-reduce at attach time) and n_cells >= w + 3; the overlap must then stay
+ * as attached (a later hsgn_set_params that changes w makes hsgn_run_steps
+ * return HSGN_E_INVALID).  Errors: HSGN_E_INVALID (no BC_HALO side, already
+ * attached, slab shorter than its halo, ranks disagree), HSGN_E_COMM, HSGN_E_CUDA. */
 hsgn_status hsgn_attach_nccl(hsgn_ctx *ctx, const void *id, int32_t rank, int32_t world);
 
 /* ---- host-staged slab transport (any process-group transport, e.g. gloo) --

@@ -103,6 +103,7 @@ struct hsgn_ctx {
     double *sp_tips = nullptr, *sp_L = nullptr, *sp_fb = nullptr, *sp_S = nullptr;
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
+    int nccl_w = -1;              // overlap w at hsgn_attach_nccl (the halo size every rank agreed on)
     std::string last_error;
     // hsgn_run_host pipeline: member-chunk views of this context (their state
     // buffers are slices of ours, their small arrays live in the workspace tail)
@@ -602,6 +603,9 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
     if (c->slab) {
         if (!c->nccl)
             return fail(c, HSGN_E_INVALID, "BC_HALO sides need hsgn_group_run_steps or hsgn_attach_nccl");
+        if (c->w != c->nccl_w)     // the neighbours' send/recv sizes would no longer match
+            return fail(c, HSGN_E_INVALID, "overlap changed since hsgn_attach_nccl (set it with the "
+                                           "descriptor's overlap, or re-attach on every rank)");
         std::vector<hsgn_ctx *> g{c};
         for (long long i = 0; i < n_steps; i++) {
             hsgn_status st = slab_step(g, c->host_steps, true);
@@ -1790,6 +1794,8 @@ hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps)
 {
     if (!g || n_steps < 0) return HSGN_E_INVALID;
     for (auto *c : g->ctx) {
+        if (c->w != g->ctx[0]->w || c->n < c->w + 3)
+            return fail(c, HSGN_E_INVALID, "group: the slabs' overlaps differ (or a slab is shorter than its halo)");
         hsgn_status st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
         if (st != HSGN_OK) return st;
     }
@@ -1899,11 +1905,38 @@ hsgn_status hsgn_attach_nccl(hsgn_ctx *c, const void *id, int32_t rank, int32_t 
 {
     if (!c || !id || world < 1 || rank < 0 || rank >= world) return HSGN_E_INVALID;
     if (!c->slab) return fail(c, HSGN_E_INVALID, "attach_nccl: context has no BC_HALO side");
+    if (c->nccl) return fail(c, HSGN_E_INVALID, "attach_nccl: already attached");
+    if (c->n < c->w + 3) return fail(c, HSGN_E_INVALID, "attach_nccl: slab shorter than its halo (n < overlap + 3)");
     ncclUniqueId u;
     memcpy(&u, id, sizeof(u));
     NCCL_TRY(c, ncclCommInitRank(&c->nccl, world, u, rank));
     c->nrank = rank;
     c->nworld = world;
+    // every rank must exchange halos of the same size (w + 3) for the same
+    // members: max over ranks of (w, -w, members, -members)
+    {
+        long long v[4] = {c->w, -c->w, c->members, -c->members};
+        long long *d = nullptr;
+        cudaError_t ce = cudaMalloc(&d, sizeof v);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(d, v, sizeof v, cudaMemcpyHostToDevice, c->stream);
+        ncclResult_t nr = ncclSuccess;
+        if (ce == cudaSuccess) nr = ncclAllReduce(d, d, 4, ncclInt64, ncclMax, c->nccl, c->stream);
+        if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaMemcpyAsync(v, d, sizeof v, cudaMemcpyDeviceToHost, c->stream);
+        if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaStreamSynchronize(c->stream);
+        if (d) cudaFree(d);
+        if (ce != cudaSuccess || nr != ncclSuccess) {
+            ncclCommDestroy(c->nccl);
+            c->nccl = nullptr;
+            return fail(c, ce != cudaSuccess ? HSGN_E_CUDA : HSGN_E_COMM,
+                        ce != cudaSuccess ? cudaGetErrorString(ce) : ncclGetErrorString(nr));
+        }
+        if (v[0] != -v[1] || v[2] != -v[3]) {
+            ncclCommDestroy(c->nccl);
+            c->nccl = nullptr;
+            return fail(c, HSGN_E_INVALID, "attach_nccl: ranks disagree on the overlap or the member count");
+        }
+    }
+    c->nccl_w = c->w;
     if (c->bathy) return nccl_exchange(c, 2);
     return HSGN_OK;
 }

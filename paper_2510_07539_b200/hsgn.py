@@ -436,14 +436,6 @@ class Group:
             raise HsgnError(st, self.L.hsgn_last_error(self.solvers[0].ctx).decode())
         self.g = h
 
-    def run_resident(self, n_steps: int, t_end: float = 0.0) -> float:
-        """hsgn_run_resident: n_steps steps with every member resident in its
-        cluster's shared memory (one launch), the last step clipped to t_end if
-        t_end > 0; returns the device ms."""
-        ms = C.c_double()
-        self._chk(self.L.hsgn_run_resident(self.ctx, int(n_steps), float(t_end), C.byref(ms)))
-        return ms.value
-
     def run_steps(self, n_steps: int):
         st = self.L.hsgn_group_run_steps(self.g, int(n_steps))
         if st != 0:

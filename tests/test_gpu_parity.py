@@ -536,6 +536,31 @@ def test_nccl_transport_single_rank_ring():
     assert rel_err([f[0] for f in b], [f[0] for f in a], S) <= 1e-11
 
 
+def test_nccl_attach_and_group_checks():
+    """attach_nccl refuses a second attach and an overlap change after the
+    attach (the neighbours' halo sizes would differ); a group refuses slabs
+    whose overlaps diverged after hsgn_group_create."""
+    hs = _hsgn()
+    w = W.cfg5_workload(1 << 16)
+    (sv,), _ = hs.slab_solvers(w, 1)
+    sv.attach_nccl(hs.nccl_unique_id(), 0, 1)
+    with pytest.raises(hs.HsgnError):
+        sv.attach_nccl(hs.nccl_unique_id(), 0, 1)
+    sv.run_steps(1)
+    w0 = sv.geometry.overlap
+    sv.set_params(w.g, w.lam, 4.0 * w.cfl, w.mcfl)   # a larger CFL_IMEX -> a longer overlap
+    assert sv.geometry.overlap != w0
+    with pytest.raises(hs.HsgnError):
+        sv.run_steps(1)
+    w = W.random_smooth(3000, 1, seed=4)
+    solvers, _ = hs.slab_solvers(w, 2)
+    g = hs.Group(solvers)
+    g.run_steps(1)
+    solvers[1].set_params(w.g, w.lam, 4.0 * w.cfl, w.mcfl)
+    with pytest.raises(hs.HsgnError):
+        g.run_steps(1)
+
+
 @pytest.mark.parametrize("case", range(12))
 def test_randomised_cases_one_step(case):
     """Seeded random problem shapes (cells, members, BCs, order, lambda range,

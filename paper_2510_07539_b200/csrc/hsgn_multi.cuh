@@ -187,8 +187,10 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
         }
         mbar_wait(dmb, pd);
         pd ^= 1u;
-        double a = 0.0, b = 0.0, e = 0.0;
-        for (int q = 0; q < C; q++) { a = fmax(a, s_dx[q][0]); b = fmax(b, s_dx[q][1]); e = fmax(e, s_dx[q][2]); }
+        // (non-negative doubles: the warp max of the bit patterns, C <= 32 lanes)
+        const bool ql = lane < C;
+        const double a = warp_max_nonneg(ql ? s_dx[lane][0] : 0.0), b = warp_max_nonneg(ql ? s_dx[lane][1] : 0.0);
+        const double e = warp_max_nonneg(ql ? s_dx[lane][2] : 0.0);
         __syncthreads();
         if (tid == 0) arm(dmb, DB);
         double d = dt_rule(P.cfl, P.mcfl, P.dx, P.idx, a, b);
@@ -369,13 +371,15 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
             for (int sd = 1, pp = 0; sd < lim; sd <<= 1, pp ^= 1) {
                 const double *cur = pp ? pb1 : pb0;
                 double *nxt = pp ? pb0 : pb1;
+                // a row whose partner tid -/+ sd lies outside 0..CNT-1 has A_ (C_) exactly 0
+                // at this level (row 0 starts with A_ = 0, rows >= ks-1 with C_ = 0, and
+                // PCR keeps it so), so any finite value may stand in for the partner's:
+                // the pads (zeros) for sd <= PPAD, the row's own slot beyond
                 int km = tid - sd, kp = tid + sd;
-                const bool okm = sd <= PPAD || km >= 0, okp = sd <= PPAD || kp < CNT;
-                km = okm ? km : 0; kp = okp ? kp : 0;
-                double Am = cur[km], Cm = cur[PSTR + km], Dm = cur[2 * PSTR + km], Vm = cur[3 * PSTR + km], Wm = cur[4 * PSTR + km];
-                double Ap = cur[kp], Cp = cur[PSTR + kp], Dp = cur[2 * PSTR + kp], Vp = cur[3 * PSTR + kp], Wp = cur[4 * PSTR + kp];
-                if (!okm) { Am = Cm = Dm = Vm = Wm = 0.0; }
-                if (!okp) { Ap = Cp = Dp = Vp = Wp = 0.0; }
+                km = (sd <= PPAD || km >= 0) ? km : tid;
+                kp = (sd <= PPAD || kp < CNT) ? kp : tid;
+                const double Am = cur[km], Cm = cur[PSTR + km], Dm = cur[2 * PSTR + km], Vm = cur[3 * PSTR + km], Wm = cur[4 * PSTR + km];
+                const double Ap = cur[kp], Cp = cur[PSTR + kp], Dp = cur[2 * PSTR + kp], Vp = cur[3 * PSTR + kp], Wp = cur[4 * PSTR + kp];
                 const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
                 const double An = -A_ * Am * ib, Cn = -C_ * Cp * ib;
                 D_ = (D_ - A_ * Dm - C_ * Dp) * ib;

@@ -178,7 +178,7 @@ def measured_peaks():
 def profile_fp64():
     """fp64 arithmetic of the stage-2 kernel from the committed ncu capture
     (profiles/ncu_summary.json: DADD + DMUL + 2 DFMA per cycle) against the
-    measured DFMA peak (profiles/r01_dfma_peak.json): the kernels are issue /
+    measured DFMA peak (profiles/r01_dfma_peak.json, tools/dfma_peak.cu): the kernels are issue /
     latency-bound, neither HBM- nor fp64-bound."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -187,7 +187,7 @@ def profile_fp64():
         pk = d["fp64_peak_tflops"]
         return {"achieved": k["fp64_tflops"], "peak": pk, "unit": "TFLOP/s", "frac": k["fp64_tflops"] / pk,
                 "pipe_active_pct": k["fp64_pipe_pct"], "issue_active_pct": k["issue_active_pct"],
-                "source": "profiles/r01_ncu_summary.md (ncu --set full, 512 x 4096 cells)"}
+                "source": d.get("summary", "profiles/r01_ncu_summary.md") + " (ncu --set full, 512 x 4096 cells)"}
     except Exception:
         return None
 
@@ -629,9 +629,11 @@ def resident_record(a):
     k = max(a.steps, 10)
     ms = s.run_resident(k)
     d = s.diagnostics()
+    s.set_cluster(1)                                # (only to read the cluster shape back)
+    cl = list(s.cluster) if s.cluster else None
     cs = 2.0 * w.n * w.members * k
     rec = {"value": cs / (ms * 1e-3), "unit": "cell-stage/s", "steps": k, "ms_per_step": ms / k,
-           "launches": 1, "cluster": list(s.cluster) if s.cluster else None,
+           "launches": 1, "cluster_ctas_x_rows": cl,
            "hbm_bytes_per_launch": 64 * w.n * w.members,
            "bound": "latency of the in-cluster exchanges and fp64 issue (no per-step HBM traffic)",
            "mass": d["mass"], "steps_done": d["steps"]}

@@ -20,6 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def short(name):
+    if "cl_stage_kernel" in name or "cl_multi_kernel" in name:
+        return name.split("(")[0].replace("void ", "").replace("hsgn::", "").replace("(bool)", "")
     if "stage_kernel" in name:
         t = name.split("<")[1].split(">")[0].replace("(bool)", "")
         f = [x.strip() for x in t.split(",")]
@@ -47,7 +49,12 @@ def launches(path):
 
 
 def full(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """per-launch metrics of an ncu report (or of its `--page raw --csv` export)"""
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+        txt = txt[txt.index('"ID"'):] if '"ID"' in txt else txt
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
     want = {
@@ -116,7 +123,7 @@ def main():
           "(cfg3, 4096 x 4096 cells; cold-cache serialised launches: compare shares).", "",
           "| kernel | launches | mean us | share of time | DRAM B/cell read | DRAM B/cell write |",
           "|---|---|---|---|---|---|"]
-    js = {"round": a.round, "launch_list": {}, "full": []}
+    js = {"round": a.round, "summary": f"profiles/{tag}_ncu_summary.md", "launch_list": {}, "full": []}
     for k, v in sorted(L.items(), key=lambda kv: -(kv[1]["total_us"] or 0)):
         rd = (v["dram_read_per_launch"] or 0) / a.cells_full
         wr = (v["dram_write_per_launch"] or 0) / a.cells_full
@@ -139,13 +146,14 @@ def main():
     if s1:
         js["stage1_dram_bytes_per_cell"] = s1[0]["dram_read_per_cell"] + s1[0]["dram_write_per_cell"]
     # fp64 arithmetic rate against the measured DFMA peak (profiles/rNN_dfma_peak.json)
-    pk = os.path.join(prof, f"{tag}_dfma_peak.json")
-    if os.path.exists(pk):
+    pks = sorted(f for f in os.listdir(prof) if f.endswith("_dfma_peak.json") and f <= f"{tag}_dfma_peak.json")
+    pk = os.path.join(prof, pks[-1]) if pks else ""
+    if pk:
         peak = json.load(open(pk))
         ptf = peak["fp64_tflops"]
         md += ["", f"fp64 arithmetic (DADD + DMUL + 2 DFMA per cycle, ncu) against the measured DFMA peak "
                    f"{ptf:.1f} TFLOP/s (`tools/dfma_peak.cu`, {peak['dfma_per_clk_per_sm_at_max_clock']:.1f} "
-                   f"DFMA/clk/SM):", "", "| kernel | fp64 TFLOP/s | of peak | fp64 pipe active % |", "|---|---|---|---|"]
+                   f"DFMA/clk/SM, profiles/{os.path.basename(pk)}):", "", "| kernel | fp64 TFLOP/s | of peak | fp64 pipe active % |", "|---|---|---|---|"]
         js["fp64_peak_tflops"] = ptf
         for d in js["full"]:
             try:

@@ -277,9 +277,10 @@ void choose_spike(hsgn_ctx *c)
 
 size_t spike_bytes(const hsgn_ctx *c)
 {
-    // per member and tile: 12 (tips) + 1 (L) + 16 (filter rows) + 3 (scratch) doubles
+    // per member and tile: 12 (tips) + 1 (L) + 16 (filter rows) doubles, and the
+    // separator solve's scratch (sep_scratch: 3 G, or 6 (G + 1024) for G > 1024)
     const int G = std::max(c->spG, 1);
-    return 4 * 256 + size_t(c->members) * G * 32 * sizeof(double);
+    return 4 * 256 + size_t(c->members) * (size_t(G) * 29 + sep_scratch(G)) * sizeof(double);
 }
 
 void choose_cluster(hsgn_ctx *c)
@@ -343,7 +344,13 @@ hsgn_status launch_spike(hsgn_ctx *c, Params P, const Bufs &B)
     const dim3 grid(c->spG, c->members);
     const size_t sm = BATHY ? CSMEM_BYTES_B : CSMEM_BYTES;
     CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_TIPS>, grid, dim3(CNT), sm, P, B));
-    CUDA_TRY(c, launch_k(c, sep_solve_kernel, dim3(c->members), dim3(CNT), 0, P));
+    if (c->spG > 1024) {
+        CUDA_TRY(c, launch_k(c, sep_coef_kernel, dim3((c->spG + 255) / 256, c->members), dim3(256), 0, P));
+        CUDA_TRY(c, launch_k(c, sep_solve_kernel<1024>, dim3(c->members), dim3(1024), sep_smem_bytes(1024), P));
+        c->launches++;
+    }
+    else
+        CUDA_TRY(c, launch_k(c, sep_solve_kernel<CNT>, dim3(c->members), dim3(CNT), sep_smem_bytes(CNT), P));
     CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_FINISH>, grid, dim3(CNT), sm, P, B));
     c->launches += 3;
     if (FIN && c->filter_sigma > 0.0) {
@@ -365,7 +372,7 @@ int launches_per_step(const hsgn_ctx *c)
     if (c->scheme != 0) return c->x_stages + 1;
     if (use_spike(c)) {
         const int fix = c->filter_sigma > 0.0 ? 1 : 0;
-        return 3 * c->tab.stages + fix + 1;
+        return (c->spG > 1024 ? 4 : 3) * c->tab.stages + fix + 1;
     }
     return c->tab.stages + 1;
 }
@@ -876,7 +883,7 @@ hsgn_status make_kids(hsgn_ctx *c, int chunks)
         if (c->sp_tips) {
             const size_t o = size_t(m0) * c->spG;
             kc->sp_tips = c->sp_tips + o * XPUB; kc->sp_L = c->sp_L + o;
-            kc->sp_fb = c->sp_fb + o * 16; kc->sp_S = c->sp_S + o * 3;
+            kc->sp_fb = c->sp_fb + o * 16; kc->sp_S = c->sp_S + size_t(m0) * sep_scratch(c->spG);
         }
         kc->ws = c->ws;
         for (int bi = 0; bi < 3; bi++)
@@ -1063,6 +1070,8 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cl_attrs<true, true, false>(); cl_attrs<true, true, true>();
     cl_attrs<false, true, false>(); cl_attrs<false, true, true>();
     multi_attrs<false>(); multi_attrs<true>();
+    cudaFuncSetAttribute(sep_solve_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sep_smem_bytes(1024)));
     if (const char *e = std::getenv("HSGN_CLUSTER")) c->cl_mode = std::atoi(e);
     choose_geometry(c);
     if (!slab) { choose_cluster(c); choose_spike(c); }
@@ -1147,7 +1156,7 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
         c->sp_tips = (double *)q; q += align256(mg * XPUB * sizeof(double));
         c->sp_L = (double *)q; q += align256(mg * sizeof(double));
         c->sp_fb = (double *)q; q += align256(mg * 16 * sizeof(double));
-        c->sp_S = (double *)q; q += align256(mg * 3 * sizeof(double));
+        c->sp_S = (double *)q; q += align256(size_t(c->members) * sep_scratch(c->spG) * sizeof(double));
     } else {
         q += spike_bytes(c);
     }

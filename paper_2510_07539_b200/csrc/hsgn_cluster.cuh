@@ -974,18 +974,48 @@ __device__ __forceinline__ void sep_equation(const double *tips, int G, bool cyc
     a = sub * id; cc = sup * id; d = rhs * id;
 }
 
-__global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
+// NTS threads: 128, or 1024 for members of more than 1024 tiles (8x shorter
+// sequential chunk sweeps); the PCR buffers (2 x 5 x (NTS + 2 PPAD) doubles)
+// are dynamic shared memory (sep_smem_bytes).  With 1024 threads the equations'
+// (a, c, d) come from sep_coef_kernel (all SMs) and both they and the sweep
+// relations are stored chunk-transposed, [field][i][thread] with thread chunk
+// i-th separator j = thread * mch + i, so that every sweep access of a warp is
+// coalesced (strided per-thread chunks cost 32 L1 wavefronts per load on the
+// one SM that runs the block).
+constexpr size_t sep_smem_bytes(int nts) { return size_t(2) * 5 * (nts + 2 * PPAD) * sizeof(double); }
+__host__ __device__ constexpr size_t sep_scratch(int G)          // doubles per member (P.sp_S)
 {
-    __shared__ double pb[2][5][PSTR];
-    __shared__ double sw[CNT / 32][3];
-    __shared__ float sred[CNT / 32];
+    return G > 1024 ? size_t(6) * ((G + 1023) / 1024) * 1024 : size_t(3) * G;
+}
+
+__global__ void __launch_bounds__(256) sep_coef_kernel(const Params P)
+{
+    const int m = blockIdx.y;
+    const int G = P.tiles;
+    const int j = blockIdx.x * 256 + threadIdx.x;
+    if (j >= G) return;
+    const int mch = (G + 1023) / 1024, t = j / mch, i = j - t * mch;
+    double a, cc, d;
+    sep_equation(P.sp_tips + size_t(m) * G * XPUB, G, P.bcl == BC_PERIODIC, j, a, cc, d);
+    double *const abc = P.sp_S + size_t(m) * sep_scratch(G) + size_t(3) * mch * 1024;
+    abc[(size_t(0) * mch + i) * 1024 + t] = a;
+    abc[(size_t(1) * mch + i) * 1024 + t] = cc;
+    abc[(size_t(2) * mch + i) * 1024 + t] = d;
+}
+
+template <int NTS>
+__global__ void __launch_bounds__(NTS) sep_solve_kernel(const Params P)
+{
+    constexpr int SSTR = NTS + 2 * PPAD;              // PCR array stride
+    __shared__ double sw[NTS / 32][3];
+    __shared__ float sred[NTS / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int m = blockIdx.x;
     const int G = P.tiles;
     const bool cyc = P.bcl == BC_PERIODIC;
     const double *const tips = P.sp_tips + size_t(m) * G * XPUB;
     double *const Lout = P.sp_L + size_t(m) * G;
-    double *const S = P.sp_S + size_t(m) * G * 3;
+    double *const S = P.sp_S + size_t(m) * sep_scratch(G);
     if (G == 1) {                                     // one tile: its separator couples to itself
         if (tid == 0) {
             double a, cc, d;
@@ -994,17 +1024,30 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
         }
         return;
     }
-    const int mch = (G + CNT - 1) / CNT;              // separators per thread chunk
+    const int mch = (G + NTS - 1) / NTS;              // separators per thread chunk
     const int ta = (G + mch - 1) / mch;               // active chunks (>= 2)
     const int ks = ta - 1;                            // the block's separator chunk
     const int j0 = tid * mch, j1 = min(G, j0 + mch);
     const bool live = tid < ta;
+    // relation f of separator j (f = 0, 1, 2), and equation j: chunk-transposed for NTS = 1024
+    auto Sx = [&](int f, int j) -> double & {
+        return NTS == 1024 ? S[(size_t(f) * mch + (j - j0)) * NTS + tid] : S[3 * size_t(j) + f];
+    };
+    auto eq = [&](int j, double &a, double &cc, double &d) {
+        if (NTS == 1024) {
+            const double *const abc = S + size_t(3) * mch * NTS;
+            const size_t o = size_t(j - j0) * NTS + tid;
+            a = abc[o]; cc = abc[size_t(mch) * NTS + o]; d = abc[2 * size_t(mch) * NTS + o];
+        } else {
+            sep_equation(tips, G, cyc, j, a, cc, d);
+        }
+    };
     // forward sweep: x_i + am_i X_{k-1} + cm_i x_{i+1} = dm_i
     double am = 0.0, cm = 0.0, dm = 0.0;
     if (live) {
         for (int j = j0; j < j1; j++) {
             double a, cc, d;
-            sep_equation(tips, G, cyc, j, a, cc, d);
+            eq(j, a, cc, d);
             if (j == j0) {
                 am = a; cm = cc; dm = d;
             } else {
@@ -1013,7 +1056,7 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
                 cm = cc * inv;
                 dm = (d - a * dm) * inv;
             }
-            S[3 * size_t(j)] = am; S[3 * size_t(j) + 1] = cm; S[3 * size_t(j) + 2] = dm;
+            Sx(0, j) = am; Sx(1, j) = cm; Sx(2, j) = dm;
         }
     }
     const double aE = am, cE = cm, dE = dm;
@@ -1021,11 +1064,11 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
     double P0 = 0.0, Q0 = 0.0, R0 = 0.0;
     if (live) {
         double Pn = 0.0, Qn = 0.0, Rn = -1.0;
-        S[3 * size_t(j1 - 1)] = 0.0; S[3 * size_t(j1 - 1) + 1] = 0.0; S[3 * size_t(j1 - 1) + 2] = -1.0;
+        Sx(0, j1 - 1) = 0.0; Sx(1, j1 - 1) = 0.0; Sx(2, j1 - 1) = -1.0;
         for (int j = j1 - 2; j >= j0; j--) {
-            const double a_ = S[3 * size_t(j)], c_ = S[3 * size_t(j) + 1], d_ = S[3 * size_t(j) + 2];
+            const double a_ = Sx(0, j), c_ = Sx(1, j), d_ = Sx(2, j);
             const double Pi = d_ - c_ * Pn, Qi = a_ - c_ * Qn, Ri = -c_ * Rn;
-            S[3 * size_t(j)] = Pi; S[3 * size_t(j) + 1] = Qi; S[3 * size_t(j) + 2] = Ri;
+            Sx(0, j) = Pi; Sx(1, j) = Qi; Sx(2, j) = Ri;
             Pn = Pi; Qn = Qi; Rn = Ri;
         }
         P0 = Pn; Q0 = Qn; R0 = Rn;
@@ -1037,7 +1080,7 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
     if (lane == 0) { sw[wid][0] = P0; sw[wid][1] = Q0; sw[wid][2] = R0; }
     __syncthreads();
     if (lane == 31) {
-        if (wid + 1 < CNT / 32) { P1 = sw[wid + 1][0]; Q1 = sw[wid + 1][1]; R1 = sw[wid + 1][2]; }
+        if (wid + 1 < NTS / 32) { P1 = sw[wid + 1][0]; Q1 = sw[wid + 1][1]; R1 = sw[wid + 1][2]; }
         else { P1 = Q1 = R1 = 0.0; }
     }
     const double P00 = sw[0][0], Q00 = sw[0][1], R00 = sw[0][2];     // chunk 0's first-row relation
@@ -1049,13 +1092,13 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
     if (tid == 0) { V_ = A_; A_ = 0.0; }              // coupling to the separator (cyclic wrap)
     if (tid == ks - 1) { W_ = C_; C_ = 0.0; }         // coupling to the separator
     if (tid >= ks) { A_ = C_ = D_ = V_ = W_ = 0.0; }
-    double *const b0 = &pb[0][0][PPAD], *const b1 = &pb[1][0][PPAD];
+    double *const b0 = hsgn_smem + PPAD, *const b1 = hsgn_smem + 5 * SSTR + PPAD;
     auto put = [&](double *b, int k, double a, double cc, double d, double v, double w_) {
-        b[k] = a; b[PSTR + k] = cc; b[2 * PSTR + k] = d; b[3 * PSTR + k] = v; b[4 * PSTR + k] = w_;
+        b[k] = a; b[SSTR + k] = cc; b[2 * SSTR + k] = d; b[3 * SSTR + k] = v; b[4 * SSTR + k] = w_;
     };
     put(b0, tid, A_, C_, D_, V_, W_);
     if (tid < 2 * PPAD) {
-        const int k = tid < PPAD ? tid - PPAD : CNT + tid - PPAD;
+        const int k = tid < PPAD ? tid - PPAD : NTS + tid - PPAD;
         put(b0, k, 0.0, 0.0, 0.0, 0.0, 0.0);
         put(b1, k, 0.0, 0.0, 0.0, 0.0, 0.0);
     }
@@ -1065,14 +1108,14 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
         if (lane == 0) sred[wid] = ev;
     }
     __syncthreads();
-    int lim = CNT;
+    int lim = NTS;
     {
         float e0 = 0.0f;
-        for (int q = 0; q < CNT / 32; q++) e0 = fmaxf(e0, sred[q]);
+        for (int q = 0; q < NTS / 32; q++) e0 = fmaxf(e0, sred[q]);
         if (e0 < 0.4f) {
             const float q = __fdividef(64.0f, -__log2f(e0) - 0.28f);
             const int qi = int(ceilf(q));
-            lim = qi <= 1 ? 1 : min(CNT, 1 << (32 - __clz(qi - 1)));
+            lim = qi <= 1 ? 1 : min(NTS, 1 << (32 - __clz(qi - 1)));
         }
     }
     const double *fin = b0;
@@ -1080,12 +1123,12 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
         const double *cur = pp ? b1 : b0;
         double *nxt = pp ? b0 : b1;
         int km = tid - sd, kp = tid + sd;
-        const bool okm = km >= -PPAD, okp = kp < CNT + PPAD;
+        const bool okm = km >= -PPAD, okp = kp < NTS + PPAD;
         km = okm ? km : 0; kp = okp ? kp : 0;
-        double Am = cur[km], Cm = cur[PSTR + km], Dm = cur[2 * PSTR + km], Vm = cur[3 * PSTR + km], Wm = cur[4 * PSTR + km];
-        double Ap = cur[kp], Cp = cur[PSTR + kp], Dp = cur[2 * PSTR + kp], Vp = cur[3 * PSTR + kp], Wp = cur[4 * PSTR + kp];
+        double Am = cur[km], Cm = cur[SSTR + km], Dm = cur[2 * SSTR + km], Vm = cur[3 * SSTR + km], Wm = cur[4 * SSTR + km];
+        double Ap = cur[kp], Cp = cur[SSTR + kp], Dp = cur[2 * SSTR + kp], Vp = cur[3 * SSTR + kp], Wp = cur[4 * SSTR + kp];
         if (!okm || tid - sd < 0) { Am = Cm = Dm = Vm = Wm = 0.0; }
-        if (!okp || tid + sd >= CNT) { Ap = Cp = Dp = Vp = Wp = 0.0; }
+        if (!okp || tid + sd >= NTS) { Ap = Cp = Dp = Vp = Wp = 0.0; }
         const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
         const double An = -A_ * Am * ib, Cn = -C_ * Cp * ib;
         D_ = (D_ - A_ * Dm - C_ * Dp) * ib;
@@ -1101,11 +1144,11 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
     // end 0 (Y0, V0, W0); cyclic: L_{j-1} = L_{j+1} = L_s (one block)
     __shared__ double sL;
     if (tid == ks) {
-        const double Yp = fin[2 * PSTR + ks - 1], Vp = fin[3 * PSTR + ks - 1], Wp = fin[4 * PSTR + ks - 1];
+        const double Yp = fin[2 * SSTR + ks - 1], Vp = fin[3 * SSTR + ks - 1], Wp = fin[4 * SSTR + ks - 1];
         double Pn = 0, Qn = 0, Rn = 0, Y0 = 0, V0 = 0, W0 = 0;
         if (cyc) {
             Pn = P00; Qn = Q00; Rn = R00;
-            Y0 = fin[2 * PSTR]; V0 = fin[3 * PSTR]; W0 = fin[4 * PSTR];
+            Y0 = fin[2 * SSTR]; V0 = fin[3 * SSTR]; W0 = fin[4 * SSTR];
         }
         const double cr = cE * Rn;
         const double sub = -aE * Vp, dia = (1.0 - cE * Qn) - aE * Wp + cr * V0, sup = cr * W0;
@@ -1117,10 +1160,10 @@ __global__ void __launch_bounds__(CNT) sep_solve_kernel(const Params P)
     const double Xk = tid < ks ? D_ - (V_ + W_) * Ls : (tid == ks ? Ls : 0.0);
     double XL = 0.0;
     if (tid == 0) XL = cyc ? Ls : 0.0;
-    else if (tid <= ks) XL = (tid - 1 == ks) ? Ls : fin[2 * PSTR + tid - 1] - (fin[3 * PSTR + tid - 1] + fin[4 * PSTR + tid - 1]) * Ls;
+    else if (tid <= ks) XL = (tid - 1 == ks) ? Ls : fin[2 * SSTR + tid - 1] - (fin[3 * SSTR + tid - 1] + fin[4 * SSTR + tid - 1]) * Ls;
     if (live) {
         for (int j = j0; j < j1; j++) {
-            const double Pi = S[3 * size_t(j)], Qi = S[3 * size_t(j) + 1], Ri = S[3 * size_t(j) + 2];
+            const double Pi = Sx(0, j), Qi = Sx(1, j), Ri = Sx(2, j);
             Lout[j] = (j == j1 - 1) ? Xk : Pi - Qi * XL - Ri * Xk;
         }
     }

@@ -76,6 +76,28 @@ def test_spike_cfg5_recipe_and_equal_to_tiles():
     assert abs(tx[0] - ty[0]) <= 1e-13 * ty[0]
 
 
+@pytest.mark.parametrize("n,bc,G", [(1 << 20, "periodic", 2048), (600000, "wall", 1172)])
+def test_spike_large_members_1024_thread_separator_solve(n, bc, G):
+    """more than 1024 tiles per member: the separator system is solved by the
+    1024-thread sep_solve_kernel (chunks of <= 2 separators per thread here)"""
+    w = W.random_smooth(n, 1, seed=n, amp=0.08, bc=(bc, bc))
+    w.filter_sigma = 0.25
+    s = gpu_solver(w)
+    assert s.spike == (G, 512), s.spike
+    s.step()
+    compare(w, s, [0], steps=1, floor=True)
+    s.run_steps(4)
+    compare(w, s, [0], steps=5, tol=1e-10)
+    b = _gpu_solver(w)
+    b.set_cluster(0)
+    b.run_steps(5)
+    (x, tx), (y, ty) = s.get_state(device=False), b.get_state(device=False)
+    ref = [f[0] for f in y]
+    dt = O.Oracle(w.n, w.dx, lam=float(w.lam[0]), bc=w.bc).dt(ref, w.cfl, w.mcfl)[0]
+    assert rel_err([f[0] for f in x], ref, field_scales(ref, float(w.lam[0]), dt)) <= 1e-12
+    assert abs(tx[0] - ty[0]) <= 1e-13 * ty[0]
+
+
 def test_spike_equals_cluster():
     w = W.random_smooth(4096, 3, seed=12, amp=0.1)
     w.filter_sigma = 0.25

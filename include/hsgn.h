@@ -187,7 +187,10 @@ hsgn_status hsgn_set_relaxation(hsgn_ctx *ctx, const hsgn_relax *relax);
 hsgn_status hsgn_set_state(hsgn_ctx *ctx, const double *h, const double *q, const double *K,
                            const double *W, double t0);
 /* Copy out the last committed state; any pointer may be NULL.  t (host array
- * of n_members, or NULL) receives each member's time.  Synchronises. */
+ * of n_members, or NULL) receives each member's time.  Synchronises.  Returns a
+ * latched device error of a failed step (HSGN_E_COERCIVITY, _DRY, _NONFINITE,
+ * _OVERLAP, _INVALID for a bad dt) after making the copy: the data are then the
+ * last committed state, which the failed step left untouched. */
 hsgn_status hsgn_get_state(hsgn_ctx *ctx, double *h, double *q, double *K, double *W,
                            double *t);
 /* Whole ensemble job from and to host memory, pipelined over member chunks

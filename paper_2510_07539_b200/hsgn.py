@@ -21,6 +21,10 @@ STATUS = {0: "OK", -1: "E_INVALID", -2: "E_DRY", -3: "E_COERCIVITY", -4: "E_SING
           -5: "E_NONFINITE", -6: "E_CUDA", -7: "E_OVERLAP", -8: "E_NOWORKSPACE", -9: "E_COMM"}
 
 
+# statuses of a latched device error (a failed step: the state stays the last committed one)
+DEVICE_ERRORS = (-2, -3, -5, -7)
+
+
 class HsgnError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"hsgn {STATUS.get(status, status)}: {msg}")
@@ -302,8 +306,10 @@ class Solver:
         self.stream.wait_stream(self._torch.cuda.current_stream())
         self._chk(self.L.hsgn_set_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in arrs], t0))
 
-    def get_state(self, device: bool = True):
-        """Return (h, q, K, W) as [members, n] tensors (device) or numpy arrays, and t[members]."""
+    def get_state(self, device: bool = True, check: bool = True):
+        """Return (h, q, K, W) as [members, n] tensors (device) or numpy arrays, and t[members].
+        A latched device error (a failed step) raises unless check=False; the copy is
+        made either way and holds the last committed state (include/hsgn.h)."""
         torch = self._torch
         if device:
             out = [torch.empty((self.members, self.n), dtype=torch.float64, device="cuda") for _ in range(4)]
@@ -311,8 +317,9 @@ class Solver:
         else:
             out = [np.empty((self.members, self.n)) for _ in range(4)]
         t = np.empty(self.members)
-        self._chk(self.L.hsgn_get_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in out],
-                                        C.c_void_p(t.ctypes.data)))
+        st = self.L.hsgn_get_state(self.ctx, *[C.c_void_p(_ptr(a)) for a in out], C.c_void_p(t.ctypes.data))
+        if st != 0 and (check or st not in DEVICE_ERRORS):
+            self._chk(st)
         return out, t
 
     def run_host(self, h, q, K, W, n_steps: int, out=None, chunks: int = 8, t0: float = 0.0):

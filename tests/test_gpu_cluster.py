@@ -134,3 +134,32 @@ def test_cluster_auto_mode_mcfl_only():
     assert s.cluster is None                      # CFL_IMEX bounds rho: overlapped tiles
     s.set_params(w.g, w.lam, 0.0, 0.5)
     assert s.cluster == (4, 512)
+
+
+@pytest.mark.parametrize("mode", [1, 3])
+def test_mcfl_only_coercivity_loss_agrees_with_oracle(mode):
+    """Material-CFL-only stepping (cfl_imex = 0, MCFL 0.5) on cfg3 member 144
+    (lambda 8815, implied CFL_IMEX ~ 12): grid-scale growth of ~4.5x per step
+    (two builds of the oracle differ by 5e-11 after 5 steps, 40 % after 20)
+    until the scheme loses coercivity (beta <= 0) at step 21 -- the
+    oracle stops there, and so must every exact GPU path, keeping step 20."""
+    w = W.cfg3(members=1, first_member=144)
+    w.cfl, w.mcfl = 0.0, 0.5
+    ref = O.Oracle(w.n, w.dx, g=w.g, lam=float(w.lam[0]), bc=w.bc, filter_sigma=w.filter_sigma)
+    with pytest.raises(O.OracleError) as eo:
+        ref.run(w.state(0), cfl=0.0, mcfl=0.5, steps=25)
+    assert "after 20 steps" in str(eo.value) and "-3" in str(eo.value)
+    s = gpu_solver(w)
+    s.set_cluster(mode)
+    s.run_steps(5)
+    compare(w, s, [0], steps=5, tol=1e-9, floor=True)
+    s.run_steps(15)
+    s.sync()
+    (a, ta) = s.get_state(device=False)
+    hs = __import__("paper_2510_07539_b200.hsgn", fromlist=["hsgn"])
+    with pytest.raises(hs.HsgnError) as eg:
+        s.run_steps(1)
+        s.sync()
+    assert eg.value.name == "E_COERCIVITY", eg.value
+    (b, tb) = s.get_state(device=False, check=False)    # the state of step 20 is kept
+    assert tb[0] == ta[0] and all(np.array_equal(x, y) for x, y in zip(a, b))

@@ -357,6 +357,13 @@ typedef struct hsgn_group hsgn_group;
 hsgn_status hsgn_group_create(hsgn_ctx *const *ctxs, int32_t n, hsgn_group **out);
 hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps);
 void hsgn_group_destroy(hsgn_group *g);
+/* Development aid: copy `count` doubles of an internal SPIKE array to host
+ * memory (which: 0 separators L [members][G], 1 slab Y, V, W [3][members][G],
+ * 2 slab end separators (E_{p-1}, F_{p+1}) [members][2], 3 right slab's tile-0
+ * relation [members][6], 4 all-gathered end values [P][members][6], 5 tile tips
+ * [members][G][12], 6 unfiltered tile-end rows [members][G][16]).  Synchronises.
+ * Errors: HSGN_E_INVALID (null pointer, unknown or unallocated array). */
+hsgn_status hsgn_debug_copy(hsgn_ctx *ctx, int32_t which, double *host, int64_t count);
 /* 128-byte ncclUniqueId (rank 0; the caller broadcasts it, e.g. torch.distributed) */
 hsgn_status hsgn_nccl_unique_id(void *id);
 /* Collective over the `world` ranks (every rank calls it with the same id).

@@ -33,6 +33,7 @@ constexpr int POLL_STEPS = 256;   // advance_to polls the device every POLL_STEP
 constexpr int T_MIN = 64;         // smallest kept tile (bounds the partials workspace)
 constexpr int H_MAX = (LCAP - 2 - T_MIN) / 2 + 3;   // largest slab halo (overlap + stencil)
 constexpr int KIDS_MAX = 16;      // member chunks of hsgn_run_host
+constexpr int GROUP_MAX_SX = 64;  // slabs of one domain (= GROUP_MAX)
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -101,6 +102,9 @@ struct hsgn_ctx {
     // rows per member; buffers in the workspace (tips, L, filter rows, scratch)
     int spG = 0, spT = 0;
     double *sp_tips = nullptr, *sp_L = nullptr, *sp_fb = nullptr, *sp_S = nullptr;
+    // SPIKE across slabs (slab contexts only; Params::sx_*)
+    double *sx_nx = nullptr, *sx_fbl = nullptr, *sx_fbr = nullptr, *sx_elfr = nullptr;
+    double *sx_yvw = nullptr, *sx_all = nullptr, *sx_send = nullptr;
     ncclComm_t nccl = nullptr;
     int nrank = 0, nworld = 1;
     int nccl_w = -1;              // overlap w at hsgn_attach_nccl (the halo size every rank agreed on)
@@ -178,6 +182,10 @@ Params make_params(hsgn_ctx *c, long long k)
         P.rho_ok = r / ((1.0 - r) * (1.0 - r));
     }
     P.picard = c->picard;
+    P.sp_tips = c->sp_tips; P.sp_L = c->sp_L; P.sp_fb = c->sp_fb; P.sp_S = c->sp_S;
+    P.sx_nx = c->sx_nx; P.sx_fbl = c->sx_fbl; P.sx_fbr = c->sx_fbr; P.sx_elfr = c->sx_elfr;
+    P.sx_yvw = c->sx_yvw; P.sx_all = c->sx_all; P.sx_send = c->sx_send;
+    P.sx_rank = c->nrank; P.sx_P = c->nworld;
     for (int k = 0; k < 9; k++) {
         P.halo_l[k] = c->halo_l ? c->halo_l + k * H_MAX : nullptr;
         P.halo_r[k] = c->halo_r ? c->halo_r + k * H_MAX : nullptr;
@@ -242,6 +250,12 @@ bool exact_eligible(const hsgn_ctx *c)
     return c->scheme == 0 && !c->slab && c->picard == 0 && !c->wb;
 }
 
+// tile-level SPIKE also runs on slab contexts (across slabs, section 8)
+bool spike_eligible(const hsgn_ctx *c)
+{
+    return c->scheme == 0 && c->picard == 0 && !c->wb;
+}
+
 // material-CFL-only stepping without a user overlap: the overlapped tiles
 // cannot bound the depth system's decay a priori
 bool overlap_unbounded(const hsgn_ctx *c) { return !(c->cfl > 0.0) && c->desc.overlap <= 0; }
@@ -254,7 +268,7 @@ bool use_cluster(const hsgn_ctx *c)
 
 bool use_spike(const hsgn_ctx *c)
 {
-    if (use_cluster(c) || c->spG <= 0 || !exact_eligible(c) || c->sp_tips == nullptr) return false;
+    if (use_cluster(c) || c->spG <= 0 || !spike_eligible(c) || c->sp_tips == nullptr) return false;
     return c->cl_mode == 3 || (c->cl_mode == 2 && overlap_unbounded(c));
 }
 
@@ -263,8 +277,9 @@ void choose_spike(hsgn_ctx *c)
     c->spG = c->spT = 0;
     const int bl = c->desc.bc_left, br = c->desc.bc_right;
     const bool cyc = bl == HSGN_BC_PERIODIC && br == HSGN_BC_PERIODIC;
-    const bool phys = (bl == HSGN_BC_WALL || bl == HSGN_BC_TRANSMISSIVE) &&
-                      (br == HSGN_BC_WALL || br == HSGN_BC_TRANSMISSIVE);
+    // non-periodic sides: physical or slab halo (SPIKE across slabs)
+    auto side = [](int b) { return b == HSGN_BC_WALL || b == HSGN_BC_TRANSMISSIVE || b == HSGN_BC_HALO; };
+    const bool phys = side(bl) && side(br);
     const int n = c->n;
     if ((!cyc && !phys) || (n % 4) != 0 || n < 8) return;
     const int G = (n + CT_MAX - 1) / CT_MAX;
@@ -280,7 +295,8 @@ size_t spike_bytes(const hsgn_ctx *c)
     // per member and tile: 12 (tips) + 1 (L) + 16 (filter rows) doubles, and the
     // separator solve's scratch (sep_scratch: 3 G, or 6 (G + 1024) for G > 1024)
     const int G = std::max(c->spG, 1);
-    return 4 * 256 + size_t(c->members) * (size_t(G) * 29 + sep_scratch(G)) * sizeof(double);
+    const size_t sx = c->slab ? size_t(c->members) * (6 + 8 + 8 + 2 + 16 + 6 * GROUP_MAX_SX + 3 * size_t(G)) : 0;
+    return 12 * 256 + (size_t(c->members) * (size_t(G) * 29 + sep_scratch(G)) + sx) * sizeof(double);
 }
 
 void choose_cluster(hsgn_ctx *c)
@@ -342,15 +358,18 @@ hsgn_status launch_spike(hsgn_ctx *c, Params P, const Bufs &B)
     P.tiles = c->spG;
     P.sp_tips = c->sp_tips; P.sp_L = c->sp_L; P.sp_fb = c->sp_fb; P.sp_S = c->sp_S;
     const dim3 grid(c->spG, c->members);
+    if (c->slab) return HSGN_E_INVALID;               // slabs: slab_spike_stage
     const size_t sm = BATHY ? CSMEM_BYTES_B : CSMEM_BYTES;
     CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_TIPS>, grid, dim3(CNT), sm, P, B));
     if (c->spG > 1024) {
-        CUDA_TRY(c, launch_k(c, sep_coef_kernel, dim3((c->spG + 255) / 256, c->members), dim3(256), 0, P));
-        CUDA_TRY(c, launch_k(c, sep_solve_kernel<1024>, dim3(c->members), dim3(1024), sep_smem_bytes(1024), P));
+        CUDA_TRY(c, launch_k(c, sep_coef_kernel, dim3((c->spG + 255) / 256, c->members), dim3(256), 0, P, 0));
+        CUDA_TRY(c, launch_k(c, sep_solve_kernel<1024>, dim3(c->members), dim3(1024), sep_smem_bytes(1024), P, 0,
+                             (double *)nullptr));
         c->launches++;
     }
     else
-        CUDA_TRY(c, launch_k(c, sep_solve_kernel<CNT>, dim3(c->members), dim3(CNT), sep_smem_bytes(CNT), P));
+        CUDA_TRY(c, launch_k(c, sep_solve_kernel<CNT>, dim3(c->members), dim3(CNT), sep_smem_bytes(CNT), P, 0,
+                             (double *)nullptr));
     CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_FINISH>, grid, dim3(CNT), sm, P, B));
     c->launches += 3;
     if (FIN && c->filter_sigma > 0.0) {
@@ -747,10 +766,13 @@ hsgn_status slab_phase_dt(std::vector<hsgn_ctx *> &g, long long k)
     return HSGN_OK;
 }
 
+hsgn_status slab_spike_stage(std::vector<hsgn_ctx *> &g, long long k, bool s2, bool nccl);
+
 // c/d. stage 1 (s2 = false) or stage 2 (s2 = true) of step k, halos in place
-hsgn_status slab_phase_stage(std::vector<hsgn_ctx *> &g, long long k, bool s2)
+hsgn_status slab_phase_stage(std::vector<hsgn_ctx *> &g, long long k, bool s2, bool nccl = false)
 {
     hsgn_status st;
+    if (use_spike(g[0])) return slab_spike_stage(g, k, s2, nccl);
     for (auto *c : g) {
         const Params Pm = make_params(c, k);
         Bufs B{};
@@ -804,13 +826,156 @@ hsgn_status slab_step(std::vector<hsgn_ctx *> &g, long long k, bool nccl)
     if ((st = slab_phase_dt(g, k)) != HSGN_OK) return st;
     // c. U^n halos, stage 1
     if ((st = nccl ? nccl_exchange(c0, 0) : loopback_exchange(g, 0)) != HSGN_OK) return st;
-    if ((st = slab_phase_stage(g, k, false)) != HSGN_OK) return st;
+    if ((st = slab_phase_stage(g, k, false, nccl)) != HSGN_OK) return st;
     if (c0->tab.stages == 2) {
         // d. U1 halos, stage 2
         if ((st = nccl ? nccl_exchange(c0, 1) : loopback_exchange(g, 1)) != HSGN_OK) return st;
-        if ((st = slab_phase_stage(g, k, true)) != HSGN_OK) return st;
+        if ((st = slab_phase_stage(g, k, true, nccl)) != HSGN_OK) return st;
     }
     return slab_phase_commit(g, k);
+}
+
+// One stage of step k with the depth system solved exactly across all slabs
+// (tile-level SPIKE per slab + the slab interface system, section 8):
+//   TIPS -> [right slab's tile-0 relation] -> sep solves Y, V, W -> [all-gather
+//   of the end values] -> interface solve, L -> FINISH -> (final stage with the
+//   filter) [neighbouring slabs' unfiltered end rows] -> filter_fix.
+// Transports: loopback group (D2D copies on the shared stream) or NCCL.
+// HSGN_DEBUG_SYNC=1: synchronise and report after every phase (development aid)
+bool dbg_sync(hsgn_ctx *c, const char *what, int k)
+{
+    static const bool on = std::getenv("HSGN_DEBUG_SYNC") != nullptr;
+    if (!on) return false;
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) return false;
+    fprintf(stderr, "hsgn: %s %d: %s\n", what, k, cudaGetErrorString(e));
+    c->last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return true;
+}
+
+template <bool S2, bool FIN, bool BATHY>
+hsgn_status slab_spike_kernels(hsgn_ctx *c, Params P, const Bufs &B, int phase)
+{
+    P.T = c->spT;
+    P.tiles = c->spG;
+    const dim3 grid(c->spG, c->members);
+    const size_t sm = BATHY ? CSMEM_BYTES_B : CSMEM_BYTES;
+    const int mb = (c->members + 127) / 128;
+    if (phase == 0) {                 // tips, tile-0 relation packed for the left slab
+        CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_TIPS>, grid, dim3(CNT), sm, P, B));
+        CUDA_TRY(c, launch_k(c, slab_pack_kernel, dim3(mb), dim3(128), 0, P, 0));
+        c->launches += 2;
+    } else if (phase == 1) {          // Y, V, W of the slab's separator system; end values packed
+        for (int mode = 0; mode < 3; mode++) {
+            double *out = c->sx_yvw + size_t(mode) * c->members * c->spG;
+            if (c->spG > 1024) {
+                CUDA_TRY(c, launch_k(c, sep_coef_kernel, dim3((c->spG + 255) / 256, c->members), dim3(256), 0, P, mode));
+                CUDA_TRY(c, launch_k(c, sep_solve_kernel<1024>, dim3(c->members), dim3(1024), sep_smem_bytes(1024),
+                                     P, mode, out));
+                c->launches += 2;
+            } else {
+                CUDA_TRY(c, launch_k(c, sep_solve_kernel<CNT>, dim3(c->members), dim3(CNT), sep_smem_bytes(CNT),
+                                     P, mode, out));
+                c->launches++;
+            }
+        }
+        CUDA_TRY(c, launch_k(c, slab_pack_kernel, dim3(mb), dim3(128), 0, P, 1));
+        c->launches++;
+    } else if (phase == 2) {          // interface solve, separators, finish; filter rows packed
+        const size_t ism = size_t(2 * P.sx_P) * (2 * P.sx_P + 1) * sizeof(double);
+        CUDA_TRY(c, launch_k(c, slab_iface_kernel, dim3(c->members), dim3(128), ism, P));
+        CUDA_TRY(c, launch_k(c, cl_stage_kernel<S2, FIN, BATHY, CL_MODE_FINISH>, grid, dim3(CNT), sm, P, B));
+        c->launches += 2;
+        if (FIN && c->filter_sigma > 0.0) {
+            CUDA_TRY(c, launch_k(c, slab_pack_kernel, dim3(mb), dim3(128), 0, P, 2));
+            c->launches++;
+        }
+    } else if (FIN && c->filter_sigma > 0.0) {   // phase 3: filter rows at tile and slab ends
+        CUDA_TRY(c, launch_k(c, filter_fix_kernel, dim3((4 * (c->spG + 1) + 127) / 128, c->members), dim3(128), 0, P, B));
+        c->launches++;
+    }
+    return HSGN_OK;
+}
+
+template <bool S2, bool FIN>
+hsgn_status slab_spike_kernels_b(hsgn_ctx *c, const Params &P, const Bufs &B, int phase)
+{
+    return c->bathy ? slab_spike_kernels<S2, FIN, true>(c, P, B, phase)
+                    : slab_spike_kernels<S2, FIN, false>(c, P, B, phase);
+}
+
+// exchange x of the slab SPIKE stage: 0 tile-0 relation (right -> left), 1 end
+// values (all-gather), 2 unfiltered end rows (both ways)
+hsgn_status slab_spike_xfer(std::vector<hsgn_ctx *> &g, int x, bool nccl)
+{
+    const int P = int(g.size());
+    hsgn_ctx *c0 = g[0];
+    const size_t M = c0->members;
+    if (nccl) {
+        hsgn_ctx *c = c0;
+        const int left = (c->nrank - 1 + c->nworld) % c->nworld, right = (c->nrank + 1) % c->nworld;
+        const bool hl = c->desc.bc_left == HSGN_BC_HALO, hr = c->desc.bc_right == HSGN_BC_HALO;
+        if (x == 1) {
+            NCCL_TRY(c, ncclAllGather(c->sx_send, c->sx_all, 6 * M, ncclDouble, c->nccl, c->stream));
+            return HSGN_OK;
+        }
+        NCCL_TRY(c, ncclGroupStart());
+        if (x == 0) {
+            if (hl) NCCL_TRY(c, ncclSend(c->sx_send, 6 * M, ncclDouble, left, c->nccl, c->stream));
+            if (hr) NCCL_TRY(c, ncclRecv(c->sx_nx, 6 * M, ncclDouble, right, c->nccl, c->stream));
+        } else {
+            if (hl) NCCL_TRY(c, ncclSend(c->sx_send, 8 * M, ncclDouble, left, c->nccl, c->stream));
+            if (hr) NCCL_TRY(c, ncclRecv(c->sx_fbr, 8 * M, ncclDouble, right, c->nccl, c->stream));
+            if (hr) NCCL_TRY(c, ncclSend(c->sx_send + 8 * M, 8 * M, ncclDouble, right, c->nccl, c->stream));
+            if (hl) NCCL_TRY(c, ncclRecv(c->sx_fbl, 8 * M, ncclDouble, left, c->nccl, c->stream));
+        }
+        NCCL_TRY(c, ncclGroupEnd());
+        return HSGN_OK;
+    }
+    for (int i = 0; i < P; i++) {
+        hsgn_ctx *c = g[i], *L = g[(i - 1 + P) % P], *R = g[(i + 1) % P];
+        const bool hl = c->desc.bc_left == HSGN_BC_HALO, hr = c->desc.bc_right == HSGN_BC_HALO;
+        auto cp = [&](double *dst, const double *src, size_t nd) {
+            return cudaMemcpyAsync(dst, src, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+        };
+        if (x == 0) {
+            if (hr) CUDA_TRY(c, cp(c->sx_nx, R->sx_send, 6 * M));
+        } else if (x == 1) {
+            for (int q = 0; q < P; q++) CUDA_TRY(c, cp(c->sx_all + size_t(q) * 6 * M, g[q]->sx_send, 6 * M));
+        } else {
+            if (hr) CUDA_TRY(c, cp(c->sx_fbr, R->sx_send, 8 * M));
+            if (hl) CUDA_TRY(c, cp(c->sx_fbl, L->sx_send + 8 * M, 8 * M));
+        }
+    }
+    return HSGN_OK;
+}
+
+hsgn_status slab_spike_stage(std::vector<hsgn_ctx *> &g, long long k, bool s2, bool nccl)
+{
+    const int Pn = int(g.size());
+    if (!nccl && Pn > GROUP_MAX_SX) return fail(g[0], HSGN_E_INVALID, "slab SPIKE: too many slabs");
+    if (nccl && g[0]->nworld > GROUP_MAX_SX) return fail(g[0], HSGN_E_INVALID, "slab SPIKE: too many ranks");
+    const bool fin = s2 || g[0]->tab.stages == 1;
+    hsgn_status st;
+    for (int phase = 0; phase < 4; phase++) {
+        for (int i = 0; i < Pn; i++) {
+            hsgn_ctx *c = g[i];
+            Params Pm = make_params(c, k);
+            if (!nccl) { Pm.sx_rank = i; Pm.sx_P = Pn; }
+            Bufs B{};
+            for (int f = 0; f < 4; f++) { B.Un[f] = c->buf[c->cur][f]; B.U1[f] = c->buf[2][f]; }
+            for (int f = 0; f < 4; f++) B.out[f] = fin ? c->buf[c->cur ^ 1][f] : c->buf[2][f];
+            if (s2) st = slab_spike_kernels_b<true, true>(c, Pm, B, phase);
+            else if (fin) st = slab_spike_kernels_b<false, true>(c, Pm, B, phase);
+            else st = slab_spike_kernels_b<false, false>(c, Pm, B, phase);
+            if (st != HSGN_OK) return st;
+            if (dbg_sync(c, "slab spike phase", phase)) return HSGN_E_CUDA;
+        }
+        if (phase < 2 || (phase == 2 && fin && g[0]->filter_sigma > 0.0))
+            if ((st = slab_spike_xfer(g, phase, nccl)) != HSGN_OK) return st;
+        if (dbg_sync(g[0], "slab spike xfer", phase)) return HSGN_E_CUDA;
+    }
+    return HSGN_OK;
 }
 
 // After a sync: reconcile host buffer parity with the device's committed steps.
@@ -1072,9 +1237,12 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     multi_attrs<false>(); multi_attrs<true>();
     cudaFuncSetAttribute(sep_solve_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sep_smem_bytes(1024)));
+    cudaFuncSetAttribute(slab_iface_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(2 * GROUP_MAX_SX * (2 * GROUP_MAX_SX + 1) * sizeof(double)));
     if (const char *e = std::getenv("HSGN_CLUSTER")) c->cl_mode = std::atoi(e);
     choose_geometry(c);
-    if (!slab) { choose_cluster(c); choose_spike(c); }
+    if (!slab) choose_cluster(c);
+    choose_spike(c);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         delete c;
@@ -1157,6 +1325,16 @@ hsgn_status hsgn_set_workspace(hsgn_ctx *c, void *p, size_t bytes)
         c->sp_L = (double *)q; q += align256(mg * sizeof(double));
         c->sp_fb = (double *)q; q += align256(mg * 16 * sizeof(double));
         c->sp_S = (double *)q; q += align256(size_t(c->members) * sep_scratch(c->spG) * sizeof(double));
+        if (c->slab) {
+            const size_t M = c->members;
+            c->sx_nx = (double *)q; q += align256(M * 6 * sizeof(double));
+            c->sx_fbl = (double *)q; q += align256(M * 8 * sizeof(double));
+            c->sx_fbr = (double *)q; q += align256(M * 8 * sizeof(double));
+            c->sx_elfr = (double *)q; q += align256(M * 2 * sizeof(double));
+            c->sx_send = (double *)q; q += align256(M * 16 * sizeof(double));
+            c->sx_all = (double *)q; q += align256(M * 6 * GROUP_MAX_SX * sizeof(double));
+            c->sx_yvw = (double *)q; q += align256(M * 3 * size_t(c->spG) * sizeof(double));
+        }
     } else {
         q += spike_bytes(c);
     }
@@ -1884,6 +2062,9 @@ hsgn_status hsgn_slab_phase(hsgn_ctx *c, int32_t phase)
     hsgn_status st = ready(c);
     if (st != HSGN_OK) return st;
     if (!c->slab || c->nccl) return fail(c, HSGN_E_INVALID, "slab_phase: host-staged slab contexts only");
+    if (use_spike(c))
+        return fail(c, HSGN_E_INVALID, "slab_phase: SPIKE across slabs needs the group or NCCL transport "
+                                       "(set_cluster(0) and a CFL_IMEX bound for the overlapped tiles)");
     if (phase == HSGN_PHASE_DT) {
         st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
         if (st != HSGN_OK) return st;
@@ -1899,6 +2080,16 @@ hsgn_status hsgn_slab_phase(hsgn_ctx *c, int32_t phase)
     case HSGN_PHASE_COMMIT: return slab_phase_commit(g, k);
     default: return fail(c, HSGN_E_INVALID, "slab_phase: unknown phase");
     }
+}
+
+hsgn_status hsgn_debug_copy(hsgn_ctx *c, int32_t which, double *host, int64_t count)
+{
+    if (!c || !host || count < 0) return HSGN_E_INVALID;
+    const double *src[7] = {c->sp_L, c->sx_yvw, c->sx_elfr, c->sx_nx, c->sx_all, c->sp_tips, c->sp_fb};
+    if (which < 0 || which > 6 || !src[which]) return HSGN_E_INVALID;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaMemcpy(host, src[which], size_t(count) * sizeof(double), cudaMemcpyDeviceToHost));
+    return HSGN_OK;
 }
 
 hsgn_status hsgn_nccl_unique_id(void *id)

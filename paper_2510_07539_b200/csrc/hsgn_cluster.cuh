@@ -260,7 +260,11 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
     const int s = c * P.T;
     const int Tc = (c == C - 1) ? n - s : P.T;
     const bool cyc = P.bcl == BC_PERIODIC;
-    const bool left_phys = !cyc && c == 0, right_phys = !cyc && c == C - 1;
+    // slab sides (BC_HALO, tile-level SPIKE only): the neighbouring slab's rows
+    // come from the halo buffers, its separators from the slab interface solve
+    const bool left_halo = !CLU && c == 0 && P.bcl == BC_HALO;
+    const bool right_halo = !CLU && c == C - 1 && P.bcr == BC_HALO;
+    const bool left_phys = !cyc && c == 0 && !left_halo, right_phys = !cyc && c == C - 1 && !right_halo;
     const unsigned xmb = (unsigned)__cvta_generic_to_shared(&s_xmb);
     const unsigned xmb2 = (unsigned)__cvta_generic_to_shared(&s_xmb2);
     const unsigned fmb = (unsigned)__cvta_generic_to_shared(&s_fmb);
@@ -385,9 +389,46 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
                 }
             }
         }
+        // one row of a neighbouring slab (cell index < 0 or >= n): halo buffers
+        // [U^n 0..3][U1 4..7][b 8], H cells per side
+        auto load1h = [&](int cell, double (&e)[4], double (&rr)[4], double &bb) {
+            const bool lft = cell < 0;
+            const int o = lft ? cell + P.H : cell - n;
+            const double *const *hp = lft ? P.halo_l : P.halo_r;
+            bb = BATHY ? hp[8][o] : 0.0;
+#pragma unroll
+            for (int f = 0; f < 4; f++) {
+                const double x0 = hp[f][o];
+                if (STAGE2) {
+                    const double d0 = hp[4 + f][o] - x0;
+                    e[f] = fma(wE, d0, x0); rr[f] = fma(wR, d0, x0);
+                } else {
+                    e[f] = x0; rr[f] = x0;
+                }
+            }
+            if (BATHY) { e[2] -= 1.5 * e[0] * bb; rr[2] -= 1.5 * rr[0] * bb; }
+        };
         // halo rows of interior or periodic tile ends
         const int hs = (tid == 64 || tid == 65) ? 0 : (tid == 96 || tid == 97) ? 1 : -1;
-        if (hs == 0 && !left_phys) {
+        if (hs == 0 && left_halo) {
+            const int rr0 = (tid == 64) ? -4 : -2;
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                double e[4], q[4], bb;
+                load1h(rr0 + k, e, q, bb);
+                putE(rr0 + k, e[0], e[1], e[2], e[3], bb);
+                if (rr0 + k == -1) putR(-1, q[0], q[1], q[2], q[3]);
+            }
+        } else if (hs == 1 && right_halo) {
+            const int rr0 = (tid == 96) ? Tc : Tc + 2;
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                double e[4], q[4], bb;
+                load1h(s + rr0 + k, e, q, bb);
+                putE(rr0 + k, e[0], e[1], e[2], e[3], bb);
+                if (rr0 + k == Tc) putR(Tc, q[0], q[1], q[2], q[3]);
+            }
+        } else if (hs == 0 && !left_phys) {
             const int rr0 = (tid == 64) ? -4 : -2;                    // rows rr0, rr0+1
             const int gc = (s + rr0 >= 0) ? s + rr0 : n + s + rr0;    // (periodic wrap: c == 0)
             double e[4][2], q[4][2], bb[2];
@@ -396,7 +437,7 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
             putE(rr0 + 1, e[0][1], e[1][1], e[2][1], e[3][1], bb[1]);
             if (tid == 65) putR(-1, q[0][1], q[1][1], q[2][1], q[3][1]);
         }
-        if (hs == 1 && !right_phys) {
+        if (hs == 1 && !right_phys && !right_halo) {
             const int rr0 = (tid == 96) ? Tc : Tc + 2;
             const int gc = (s + rr0 < n) ? s + rr0 : s + rr0 - n;
             double e[4][2], q[4][2], bb[2];
@@ -646,11 +687,14 @@ __global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params 
         } else if constexpr (MODE == CL_MODE_FINISH) {
             const double *const Lv = P.sp_L + size_t(m) * C;
             Lc = Lv[c];
-            if (c > 0 || cyc) Lm = Lv[cm_];
-            if (c + 1 < C || cyc) Lp = Lv[cp_];
-            const double *const tn = P.sp_tips + (size_t(m) * C + cp_) * XPUB;
+            if (left_halo) Lm = P.sx_elfr[2 * m];                 // E_{p-1}: left slab's last separator
+            else if (c > 0 || cyc) Lm = Lv[cm_];
+            if (right_halo) Lp = P.sx_elfr[2 * m + 1];            // F_{p+1}: right slab's first separator
+            else if (c + 1 < C || cyc) Lp = Lv[cp_];
+            const double *const tn = right_halo ? P.sx_nx + size_t(m) * 6
+                                                : P.sp_tips + (size_t(m) * C + cp_) * XPUB + 6;
 #pragma unroll
-            for (int k = 0; k < 6; k++) nx[k] = tn[6 + k];
+            for (int k = 0; k < 6; k++) nx[k] = tn[k];
         } else {
         // publish (DSMEM, st.async): warp 0 sends the first-row relation of chunk 0
         // and (Y, V, W) of slot 0 (what the previous CTA's separator row needs);
@@ -954,15 +998,20 @@ namespace hsgn {
 // the chunk ends by PCR with two spike columns, the last chunk end (L_{G-1})
 // as the block's single separator.  Writes L to P.sp_L.
 // ---------------------------------------------------------------------------
+// nxr: the right slab's tile-0 relation (P1, Q1, R1, Y0, V0, W0) for the last
+// equation of a slab with a BC_HALO right side (else NULL).  Non-cyclic
+// members: the outer couplings a_0 L_{-1}, c_{G-1} L_G are dropped (exactly 0 at
+// physical ends); slabs carry them as the spike columns of the right-hand
+// side: mode 1 -> d = a_0 e_0 (V), mode 2 -> d = c_{G-1} e_{G-1} (W), mode 0 -> Y.
 __device__ __forceinline__ void sep_equation(const double *tips, int G, bool cyc, int j, double &a, double &cc,
-                                             double &d)
+                                             double &d, const double *nxr = nullptr, int mode = 0)
 {
     const double *o = tips + size_t(j) * XPUB;
     const int jn = (j + 1 < G) ? j + 1 : (cyc ? 0 : -1);
     double P1n = 0, Q1n = 0, R1n = 0, Y0 = 0, V0 = 0, W0 = 0;
-    if (jn >= 0) {
-        const double *l = tips + size_t(jn) * XPUB;
-        P1n = l[6]; Q1n = l[7]; R1n = l[8]; Y0 = l[9]; V0 = l[10]; W0 = l[11];
+    const double *l = jn >= 0 ? tips + size_t(jn) * XPUB + 6 : nxr;
+    if (l) {
+        P1n = l[0]; Q1n = l[1]; R1n = l[2]; Y0 = l[3]; V0 = l[4]; W0 = l[5];
     }
     const double aEj = o[0], cEj = o[1], dEj = o[2], Yp = o[3], Vp = o[4], Wp = o[5];
     const double cr = cEj * R1n;
@@ -972,6 +1021,12 @@ __device__ __forceinline__ void sep_equation(const double *tips, int G, bool cyc
     const double rhs = dEj - cEj * P1n - aEj * Yp + cr * Y0;
     const double id = rcp(dia);
     a = sub * id; cc = sup * id; d = rhs * id;
+    if (mode == 1) d = (j == 0) ? a : 0.0;
+    else if (mode == 2) d = (j == G - 1) ? cc : 0.0;
+    if (!cyc) {
+        if (j == 0) a = 0.0;
+        if (j == G - 1) cc = 0.0;
+    }
 }
 
 // NTS threads: 128, or 1024 for members of more than 1024 tiles (8x shorter
@@ -988,7 +1043,12 @@ __host__ __device__ constexpr size_t sep_scratch(int G)          // doubles per 
     return G > 1024 ? size_t(6) * ((G + 1023) / 1024) * 1024 : size_t(3) * G;
 }
 
-__global__ void __launch_bounds__(256) sep_coef_kernel(const Params P)
+__device__ __forceinline__ const double *sep_nxr(const Params &P, int m)
+{
+    return P.bcr == BC_HALO ? P.sx_nx + size_t(m) * 6 : nullptr;
+}
+
+__global__ void __launch_bounds__(256) sep_coef_kernel(const Params P, const int mode)
 {
     const int m = blockIdx.y;
     const int G = P.tiles;
@@ -996,15 +1056,17 @@ __global__ void __launch_bounds__(256) sep_coef_kernel(const Params P)
     if (j >= G) return;
     const int mch = (G + 1023) / 1024, t = j / mch, i = j - t * mch;
     double a, cc, d;
-    sep_equation(P.sp_tips + size_t(m) * G * XPUB, G, P.bcl == BC_PERIODIC, j, a, cc, d);
+    sep_equation(P.sp_tips + size_t(m) * G * XPUB, G, P.bcl == BC_PERIODIC, j, a, cc, d, sep_nxr(P, m), mode);
     double *const abc = P.sp_S + size_t(m) * sep_scratch(G) + size_t(3) * mch * 1024;
     abc[(size_t(0) * mch + i) * 1024 + t] = a;
     abc[(size_t(1) * mch + i) * 1024 + t] = cc;
     abc[(size_t(2) * mch + i) * 1024 + t] = d;
 }
 
+// mode 0: the separators L (or Y for a slab), 1 / 2: the slab spike columns V / W
+// (see sep_equation); out: [members][G] (NULL: P.sp_L)
 template <int NTS>
-__global__ void __launch_bounds__(NTS) sep_solve_kernel(const Params P)
+__global__ void __launch_bounds__(NTS) sep_solve_kernel(const Params P, const int mode, double *out)
 {
     constexpr int SSTR = NTS + 2 * PPAD;              // PCR array stride
     __shared__ double sw[NTS / 32][3];
@@ -1014,12 +1076,13 @@ __global__ void __launch_bounds__(NTS) sep_solve_kernel(const Params P)
     const int G = P.tiles;
     const bool cyc = P.bcl == BC_PERIODIC;
     const double *const tips = P.sp_tips + size_t(m) * G * XPUB;
-    double *const Lout = P.sp_L + size_t(m) * G;
+    double *const Lout = (out ? out : P.sp_L) + size_t(m) * G;
+    const double *const nxr = sep_nxr(P, m);
     double *const S = P.sp_S + size_t(m) * sep_scratch(G);
     if (G == 1) {                                     // one tile: its separator couples to itself
         if (tid == 0) {
             double a, cc, d;
-            sep_equation(tips, G, cyc, 0, a, cc, d);
+            sep_equation(tips, G, cyc, 0, a, cc, d, nxr, mode);
             Lout[0] = cyc ? d * rcp(1.0 + a + cc) : d;
         }
         return;
@@ -1039,7 +1102,7 @@ __global__ void __launch_bounds__(NTS) sep_solve_kernel(const Params P)
             const size_t o = size_t(j - j0) * NTS + tid;
             a = abc[o]; cc = abc[size_t(mch) * NTS + o]; d = abc[2 * size_t(mch) * NTS + o];
         } else {
-            sep_equation(tips, G, cyc, j, a, cc, d);
+            sep_equation(tips, G, cyc, j, a, cc, d, nxr, mode);
         }
     };
     // forward sweep: x_i + am_i X_{k-1} + cm_i x_{i+1} = dm_i
@@ -1183,12 +1246,16 @@ __global__ void __launch_bounds__(128) filter_fix_kernel(const Params P, const B
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int bnd = t >> 2, i = (t & 3) + 2;          // tile end b between tiles b-1 and b; row 2..5
     double um = 0.0, nm = 0.0;
-    const bool act = bnd < G && (cyc || bnd > 0) && P.dt[m] != 0.0;   // (dt = 0: the member was carried)
+    // slab ends (BC_HALO): end 0 with the left slab's last rows (own rows 4, 5
+    // only), end G with the right slab's first rows (own rows 2, 3 only)
+    const bool hl = bnd == 0 && P.bcl == BC_HALO, hr = bnd == G && P.bcr == BC_HALO;
+    const bool act = (bnd < G && (cyc || bnd > 0 || hl) || hr) && (!hl || i >= 4) && (!hr || i < 4) &&
+                     P.dt[m] != 0.0;                  // (dt = 0: the member was carried)
     if (act) {
         const int bl = bnd > 0 ? bnd - 1 : G - 1;
         const int Tl = (bl == G - 1) ? P.n - (G - 1) * P.T : P.T;
-        const double *fl = P.sp_fb + (size_t(m) * G + bl) * 16 + 8;     // rows Tl-4 .. Tl-1
-        const double *fr = P.sp_fb + (size_t(m) * G + bnd) * 16;        // rows 0 .. 3
+        const double *fl = hl ? P.sx_fbl + size_t(m) * 8 : P.sp_fb + (size_t(m) * G + bl) * 16 + 8;  // rows Tl-4 .. Tl-1
+        const double *fr = hr ? P.sx_fbr + size_t(m) * 8 : P.sp_fb + (size_t(m) * G + bnd) * 16;     // rows 0 .. 3
         double xq[8], xw[8];
 #pragma unroll
         for (int k = 0; k < 4; k++) { xq[k] = fl[k]; xw[k] = fl[4 + k]; xq[4 + k] = fr[k]; xw[4 + k] = fr[4 + k]; }
@@ -1200,7 +1267,7 @@ __global__ void __launch_bounds__(128) filter_fix_kernel(const Params P, const B
                 qo = xq[k] - sig16 * (xq[k - 2] - 4.0 * xq[k - 1] + 6.0 * xq[k] - 4.0 * xq[k + 1] + xq[k + 2]);
                 wo = xw[k] - sig16 * (xw[k - 2] - 4.0 * xw[k - 1] + 6.0 * xw[k] - 4.0 * xw[k + 1] + xw[k + 2]);
             }
-        const int cell = i < 4 ? bl * P.T + Tl - 4 + i : bnd * P.T + (i - 4);
+        const int cell = i < 4 ? bl * P.T + Tl - 4 + i : bnd * P.T + (i - 4);   // (hl: i >= 4; hr: i < 4, bl = G-1)
         const size_t g = size_t(m) * P.n + cell;
         double h = B.out[0][g], K = B.out[2][g];
         const double bb = P.b ? P.b[cell] : 0.0;
@@ -1224,6 +1291,91 @@ __global__ void __launch_bounds__(128) filter_fix_kernel(const Params P, const B
         atomicMax(P.maxes + (slot_w * 2 + 0) * P.members + m, (unsigned long long)__double_as_longlong(um));
         atomicMax(P.maxes + (slot_w * 2 + 1) * P.members + m, (unsigned long long)__double_as_longlong(nm));
     }
+}
+
+
+// ---------------------------------------------------------------------------
+// SPIKE across slabs.  Slab p's separators satisfy
+//     L_j = Y_j - V_j E_{p-1} - W_j F_{p+1}
+// (Y, V, W from sep_solve_kernel modes 0, 1, 2 over the slab's G tiles; E_{p-1}
+// the left slab's last separator, F_{p+1} the right slab's first), so the end
+// separators of all slabs, F_q = L_0^q and E_q = L_{G-1}^q, satisfy the 2P system
+//     F_q + V_0^q E_{q-1} + W_0^q F_{q+1} = Y_0^q
+//     E_q + V_{G-1}^q E_{q-1} + W_{G-1}^q F_{q+1} = Y_{G-1}^q        (ring in q)
+// (V = 0 / W = 0 on physical sides), which every slab solves redundantly from
+// the all-gathered (Y, V, W) end values.
+// ---------------------------------------------------------------------------
+// what 0: tile 0's first-row relation (tips 6..11) -> sx_send[m][0..5] (to the left slab)
+// what 1: (Y_0, V_0, W_0, Y_{G-1}, V_{G-1}, W_{G-1}) -> sx_send[m][0..5] (all-gather)
+// what 2: tile 0's unfiltered rows 0..3 (q, W) -> sx_send[m][0..7] (to the left),
+//         the last tile's rows Tc-4..Tc-1 -> sx_send[M*8 + m*8 ..] (to the right)
+__global__ void slab_pack_kernel(const Params P, const int what)
+{
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= P.members) return;
+    const int G = P.tiles, M = P.members;
+    if (what == 0) {
+        const double *tp = P.sp_tips + size_t(m) * G * XPUB + 6;
+        for (int k = 0; k < 6; k++) P.sx_send[size_t(m) * 6 + k] = tp[k];
+    } else if (what == 1) {
+        const double *Y = P.sx_yvw + size_t(m) * G, *V = Y + size_t(M) * G, *W = V + size_t(M) * G;
+        double *o = P.sx_send + size_t(m) * 6;
+        o[0] = Y[0]; o[1] = V[0]; o[2] = W[0]; o[3] = Y[G - 1]; o[4] = V[G - 1]; o[5] = W[G - 1];
+    } else {
+        const double *f0 = P.sp_fb + size_t(m) * G * 16, *fG = P.sp_fb + (size_t(m) * G + G - 1) * 16 + 8;
+        for (int k = 0; k < 8; k++) {
+            P.sx_send[size_t(m) * 8 + k] = f0[k];
+            P.sx_send[size_t(M) * 8 + size_t(m) * 8 + k] = fG[k];
+        }
+    }
+}
+
+// one block per member, 128 threads: the 2P end-separator system (dense, no
+// pivoting: a Schur complement of the M-matrix depth system), then
+// L_j = Y_j - V_j E_{p-1} - W_j F_{p+1} into P.sp_L and (E_{p-1}, F_{p+1}) into sx_elfr
+__global__ void __launch_bounds__(128) slab_iface_kernel(const Params P)
+{
+    const int m = blockIdx.x, tid = threadIdx.x;
+    const int Ps = P.sx_P, n2 = 2 * Ps, G = P.tiles, M = P.members, p = P.sx_rank;
+    double *const A = hsgn_smem;                      // [n2][n2 + 1], augmented
+    const int ld = n2 + 1;
+    for (int e = tid; e < n2 * ld; e += blockDim.x) A[e] = 0.0;
+    __syncthreads();
+    if (tid < Ps) {
+        const int q = tid;
+        const double *v = P.sx_all + (size_t(q) * M + m) * 6;    // Y0, V0, W0, YG, VG, WG of slab q
+        const int ql = (q + Ps - 1) % Ps, qr = (q + 1) % Ps;
+        double *rF = A + size_t(2 * q) * ld, *rE = A + size_t(2 * q + 1) * ld;
+        rF[2 * q] += 1.0; rF[2 * ql + 1] += v[1]; rF[2 * qr] += v[2]; rF[n2] = v[0];
+        rE[2 * q + 1] += 1.0; rE[2 * ql + 1] += v[4]; rE[2 * qr] += v[5]; rE[n2] = v[3];
+    }
+    __syncthreads();
+    for (int k = 0; k < n2; k++) {                    // forward elimination
+        const double piv = A[size_t(k) * ld + k];
+        for (int i = k + 1 + tid; i < n2; i += blockDim.x) {
+            const double f = A[size_t(i) * ld + k] / piv;
+            if (f != 0.0)
+                for (int j = k; j <= n2; j++) A[size_t(i) * ld + j] -= f * A[size_t(k) * ld + j];
+        }
+        __syncthreads();
+    }
+    __shared__ double sz[2];
+    if (tid == 0) {                                   // back substitution (into column n2)
+        for (int i = n2 - 1; i >= 0; i--) {
+            double x = A[size_t(i) * ld + n2];
+            for (int j = i + 1; j < n2; j++) x -= A[size_t(i) * ld + j] * A[size_t(j) * ld + n2];
+            A[size_t(i) * ld + n2] = x / A[size_t(i) * ld + i];
+        }
+        const int ql = (p + Ps - 1) % Ps, qr = (p + 1) % Ps;
+        sz[0] = P.bcl == BC_HALO ? A[size_t(2 * ql + 1) * ld + n2] : 0.0;    // E_{p-1}
+        sz[1] = P.bcr == BC_HALO ? A[size_t(2 * qr) * ld + n2] : 0.0;        // F_{p+1}
+        P.sx_elfr[2 * m] = sz[0];
+        P.sx_elfr[2 * m + 1] = sz[1];
+    }
+    __syncthreads();
+    const double El = sz[0], Fr = sz[1];
+    const double *Y = P.sx_yvw + size_t(m) * G, *V = Y + size_t(M) * G, *W = V + size_t(M) * G;
+    for (int j = tid; j < G; j += blockDim.x) P.sp_L[size_t(m) * G + j] = Y[j] - V[j] * El - W[j] * Fr;
 }
 
 }  // namespace hsgn

@@ -87,6 +87,13 @@ struct Params {
     // filter_fix_kernel): per member and tile 12 published values, the separator
     // value L, 16 unfiltered boundary values; per member and tile 3 scratch
     double *sp_tips, *sp_L, *sp_fb, *sp_S;
+    // SPIKE across slabs (BC_HALO sides), per member:
+    // sx_nx[6] the right slab's tile-0 first-row relation, sx_fbl[8] / sx_fbr[8]
+    // the neighbouring slabs' unfiltered end rows, sx_elfr[2] the neighbouring
+    // slabs' end separators (E_{p-1}, F_{p+1}), sx_yvw[3][G] the local separator
+    // solutions Y, V, W; sx_all[P][6] every slab's end values; sx_rank, sx_P
+    double *sx_nx, *sx_fbl, *sx_fbr, *sx_elfr, *sx_yvw, *sx_all, *sx_send;
+    int sx_rank, sx_P;
     const Ctrl *ctrl;
     int kslot, kpar;                 // host step index k: k mod 3, k mod 2
     // slab decomposition (BC_HALO sides): ghost cells received from the

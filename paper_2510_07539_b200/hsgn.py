@@ -67,7 +67,7 @@ SYMBOLS = ["hsgn_create", "hsgn_destroy", "hsgn_workspace_bytes", "hsgn_set_work
            "hsgn_status_string", "hsgn_last_error", "hsgn_group_create", "hsgn_group_run_steps",
            "hsgn_group_destroy", "hsgn_nccl_unique_id", "hsgn_attach_nccl",
            "hsgn_slab_xfer_count", "hsgn_slab_get", "hsgn_slab_put", "hsgn_slab_phase",
-           "hsgn_run_resident"]
+           "hsgn_run_resident", "hsgn_debug_copy"]
 
 XFER = {"maxima": 0, "un": 1, "u1": 2, "b": 3}
 PHASE = {"dt": 0, "stage1": 1, "stage2": 2, "commit": 3}
@@ -124,6 +124,7 @@ def load_library(path: str = LIB_PATH):
         "hsgn_slab_put": (st, [vp, C.c_int32, vp]),
         "hsgn_slab_phase": (st, [vp, C.c_int32]),
         "hsgn_run_resident": (st, [vp, C.c_int64, C.c_double, dp]),
+        "hsgn_debug_copy": (st, [vp, C.c_int32, dp, C.c_int64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -348,6 +349,12 @@ class Solver:
             return d
         self._chk(self.L.hsgn_step(self.ctx, dt, None))
 
+    def debug_copy(self, which: int, count: int) -> np.ndarray:
+        """hsgn_debug_copy: an internal SPIKE array (development aid)"""
+        out = np.empty(count)
+        self._chk(self.L.hsgn_debug_copy(self.ctx, int(which), out.ctypes.data_as(C.POINTER(C.c_double)), count))
+        return out
+
     def run_resident(self, n_steps: int, t_end: float = 0.0) -> float:
         """hsgn_run_resident: n_steps steps with every member resident in its
         cluster's shared memory (one launch), the last step clipped to t_end if
@@ -460,13 +467,14 @@ class Group:
             pass
 
 
-def slab_solvers(w, parts, stream=None, **kw):
+def slab_solvers(w, parts, stream=None, align=1, **kw):
     """Split a 1-member Workload into `parts` contiguous slabs (sizes differ by at
-    most one cell) sharing one stream; returns (solvers, bounds)."""
+    most `align` cells, edges multiples of `align`; SPIKE across slabs needs
+    multiples of 4) sharing one stream; returns (solvers, bounds)."""
     import torch
     assert w.members == 1
     stream = stream if stream is not None else torch.cuda.Stream()
-    edges = [round(i * w.n / parts) for i in range(parts + 1)]
+    edges = [align * round(i * w.n / (parts * align)) for i in range(parts)] + [w.n]
     out = []
     for i in range(parts):
         a, b = edges[i], edges[i + 1]

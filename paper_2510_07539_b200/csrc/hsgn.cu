@@ -148,6 +148,8 @@ hsgn_status status_from_bits(unsigned int bits)
     return HSGN_E_INVALID;
 }
 
+int slab_H(const hsgn_ctx *c);
+
 Params make_params(hsgn_ctx *c, long long k)
 {
     Params P{};
@@ -165,7 +167,7 @@ Params make_params(hsgn_ctx *c, long long k)
     P.b = c->bathy ? c->b : nullptr;
     P.lam = c->lamd; P.t = c->t; P.dt = c->dt; P.maxes = c->maxes; P.err = c->err;
     P.steps = c->steps; P.done = c->done; P.rho_obs = c->rho_obs; P.kmin = c->kmin; P.ctrl = c->ctrl;
-    P.H = c->w + 3;
+    P.H = slab_H(c);
     if (c->scheme == 1) {            // explicit: its own tiles, dt = CFL_EX dx / mu_max only
         P.T = c->xT;
         P.tiles = c->xtiles;
@@ -271,6 +273,11 @@ bool use_spike(const hsgn_ctx *c)
     if (use_cluster(c) || c->spG <= 0 || !spike_eligible(c) || c->sp_tips == nullptr) return false;
     return c->cl_mode == 3 || (c->cl_mode == 2 && overlap_unbounded(c));
 }
+
+// ghost cells a BC_HALO side takes from its neighbour per exchange: the
+// overlapped tiles need w + 3 (overlap + stencil), SPIKE across slabs only the
+// stencil's 4 rows (the depth coupling goes through the separators)
+int slab_H(const hsgn_ctx *c) { return use_spike(c) ? 4 : c->w + 3; }
 
 void choose_spike(hsgn_ctx *c)
 {
@@ -629,6 +636,7 @@ hsgn_status run_steps_impl(hsgn_ctx *c, long long n_steps)
     if (c->slab) {
         if (!c->nccl)
             return fail(c, HSGN_E_INVALID, "BC_HALO sides need hsgn_group_run_steps or hsgn_attach_nccl");
+        if (c->n < slab_H(c)) return fail(c, HSGN_E_INVALID, "slab shorter than its halo (n < overlap + 3)");
         if (c->w != c->nccl_w)     // the neighbours' send/recv sizes would no longer match
             return fail(c, HSGN_E_INVALID, "overlap changed since hsgn_attach_nccl (set it with the "
                                            "descriptor's overlap, or re-attach on every rank)");
@@ -714,7 +722,7 @@ hsgn_status loopback_exchange(std::vector<hsgn_ctx *> &g, int which)
     const int nf = which == 2 ? 1 : 4;
     for (int i = 0; i < P; i++) {
         hsgn_ctx *c = g[i];
-        const int H = c->w + 3;
+        const int H = slab_H(c);                      // (equal over the group: checked per run)
         hsgn_ctx *L = g[(i - 1 + P) % P], *R = g[(i + 1) % P];
         for (int f = 0; f < nf; f++) {
             if (c->desc.bc_left == HSGN_BC_HALO)
@@ -737,7 +745,7 @@ hsgn_status loopback_exchange(std::vector<hsgn_ctx *> &g, int which)
 
 hsgn_status nccl_exchange(hsgn_ctx *c, int which)
 {
-    const int H = c->w + 3;
+    const int H = slab_H(c);
     const int left = (c->nrank - 1 + c->nworld) % c->nworld, right = (c->nrank + 1) % c->nworld;
     const int nf = which == 2 ? 1 : 4;
     NCCL_TRY(c, ncclGroupStart());
@@ -824,6 +832,8 @@ hsgn_status slab_step(std::vector<hsgn_ctx *> &g, long long k, bool nccl)
         CUDA_TRY(c0, cudaGetLastError());
     }
     if ((st = slab_phase_dt(g, k)) != HSGN_OK) return st;
+    // static b halos (again every step: cheap, and the halo width follows the solve mode)
+    if (c0->bathy && (st = nccl ? nccl_exchange(c0, 2) : loopback_exchange(g, 2)) != HSGN_OK) return st;
     // c. U^n halos, stage 1
     if ((st = nccl ? nccl_exchange(c0, 0) : loopback_exchange(g, 0)) != HSGN_OK) return st;
     if ((st = slab_phase_stage(g, k, false, nccl)) != HSGN_OK) return st;
@@ -1965,7 +1975,7 @@ hsgn_status hsgn_group_create(hsgn_ctx *const *ctxs, int32_t n, hsgn_group **out
         if (c->stream != c0->stream || c->w != c0->w || c->members != c0->members ||
             c->tab.stages != c0->tab.stages || c->host_steps != c0->host_steps || c->nccl)
             return fail(c, HSGN_E_INVALID, "group: contexts must share stream, overlap, tableau and step");
-        if (c->n < c->w + 3) return fail(c, HSGN_E_INVALID, "group: slab shorter than its halo");
+        if (c->n < slab_H(c)) return fail(c, HSGN_E_INVALID, "group: slab shorter than its halo");
     }
     hsgn_group *g = new hsgn_group();
     g->ctx.assign(ctxs, ctxs + n);
@@ -1981,8 +1991,10 @@ hsgn_status hsgn_group_run_steps(hsgn_group *g, int64_t n_steps)
 {
     if (!g || n_steps < 0) return HSGN_E_INVALID;
     for (auto *c : g->ctx) {
-        if (c->w != g->ctx[0]->w || c->n < c->w + 3)
-            return fail(c, HSGN_E_INVALID, "group: the slabs' overlaps differ (or a slab is shorter than its halo)");
+        if (c->w != g->ctx[0]->w || slab_H(c) != slab_H(g->ctx[0]) || use_spike(c) != use_spike(g->ctx[0]) ||
+            c->n < slab_H(c))
+            return fail(c, HSGN_E_INVALID, "group: the slabs' overlaps or depth-solve modes differ "
+                                           "(or a slab is shorter than its halo)");
         hsgn_status st = set_ctrl(c, c->ctrl_host.t_end, 0.0);
         if (st != HSGN_OK) return st;
     }
@@ -2106,7 +2118,7 @@ hsgn_status hsgn_attach_nccl(hsgn_ctx *c, const void *id, int32_t rank, int32_t 
     if (!c || !id || world < 1 || rank < 0 || rank >= world) return HSGN_E_INVALID;
     if (!c->slab) return fail(c, HSGN_E_INVALID, "attach_nccl: context has no BC_HALO side");
     if (c->nccl) return fail(c, HSGN_E_INVALID, "attach_nccl: already attached");
-    if (c->n < c->w + 3) return fail(c, HSGN_E_INVALID, "attach_nccl: slab shorter than its halo (n < overlap + 3)");
+    if (c->n < slab_H(c)) return fail(c, HSGN_E_INVALID, "attach_nccl: slab shorter than its halo (n < overlap + 3)");
     ncclUniqueId u;
     memcpy(&u, id, sizeof(u));
     NCCL_TRY(c, ncclCommInitRank(&c->nccl, world, u, rank));

@@ -104,6 +104,41 @@ def test_slab_spike_mcfl_only_large_rho_auto_mode():
     compare(w, single, [0], steps=3, tol=1e-10)
 
 
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_slab_spike_coupled_slabs_interface_system(bc):
+    """8 slabs of 64 cells at an implied CFL_IMEX ~ 10: the depth system's
+    inverse decays by only ~1e-9 over one slab, so the spike columns V, W and
+    the 2P interface system carry real coupling (checked through
+    hsgn_debug_copy); the result equals the single domain to round-off, and
+    the oracle"""
+    hs = _hs()
+    w = W.random_smooth(512, 1, seed=5, amp=0.3, bc=(bc, bc))
+    w.cfl, w.mcfl = 0.0, 0.3                  # implied CFL_IMEX 8-12
+    w.filter_sigma = 0.25
+    single = single_spike(w)
+    solvers, _ = spike_slabs(w, 8, mode=2)
+    assert all(sv.spike == (1, 64) for sv in solvers)
+    g = hs.Group(solvers)
+    single.step()
+    g.run_steps(1)
+    yvw = np.abs(solvers[3].debug_copy(1, 3))           # Y, V, W of slab 3 (one tile)
+    assert yvw[1] > 1e-6 and yvw[2] > 1e-6, yvw           # (measured 1e-5 .. 5e-3, rho ~ 60-110)
+    (h, q, K, Wf), t = _gather(solvers)
+    (h1, q1, K1, W1), t1 = single.get_state(device=False)
+    refs, _ = oracle_run(w, [0], steps=1)
+    dt = O.Oracle(w.n, w.dx, lam=float(w.lam[0]), bc=w.bc).dt(refs[0], w.cfl, w.mcfl)[0]
+    S = field_scales(refs[0], float(w.lam[0]), dt)
+    assert t[0] == t1[0]
+    # round-off only: at this CFL two builds of the oracle differ by 2e-13 (A17 floor)
+    assert rel_err([h, q, K, Wf], [h1[0], q1[0], K1[0], W1[0]], S) <= 1e-12
+    assert rel_err([h, q, K, Wf], refs[0], S) <= TOL_STEP
+    g.run_steps(4)
+    single.run_steps(4)
+    (h, q, K, Wf), t = _gather(solvers)
+    (h1, q1, K1, W1), t1 = single.get_state(device=False)
+    assert rel_err([h, q, K, Wf], [h1[0], q1[0], K1[0], W1[0]], S) <= 1e-11
+
+
 def test_slab_spike_nccl_single_rank_ring():
     """the NCCL transport of the slab SPIKE stage with world = 1 (sends to and
     receives from itself, all-gather of one rank) == the single domain"""

@@ -694,6 +694,15 @@ def tend_records():
         st = s.diagnostics()["steps"]          # launched: the last poll of advance_to may carry
         out[f"cfg2_dambreak_lam{lam:g}_t48"] = {"seconds": dev, "wall_s": wall, "steps_launched": st,
                                                 "us_per_launched_step": dev / st * 1e6, "cells": w.n}
+    # the three lambdas as one 3-member ensemble (per-member dt and t_end): one
+    # launch sequence serves all three, to the slowest member's t_end
+    w = W.cfg2_lambdas()
+    s = hsgn.solver_for(w)
+    _, dev, wall = _timed(s.stream, lambda: s.advance_to(w.t_end))
+    tt = s.get_state(device=False)[1]
+    out["cfg2_dambreak_3lambdas_one_ensemble_t48"] = {"seconds": dev, "wall_s": wall,
+                                                      "steps_launched": s.diagnostics()["steps"],
+                                                      "t_reached": [float(x) for x in tt], "cells": 3 * w.n}
     w = W.cfg4()
     s = hsgn.solver_for(w)
     s.run_steps(18)

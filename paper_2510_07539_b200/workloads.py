@@ -160,6 +160,17 @@ def cfg2(lam: float, n: int = 1 << 16, width_cells: float = 50.0) -> Workload:
                     cfl=2.0, mcfl=0.5, t_end=48.0, filter_sigma=0.25)
 
 
+def cfg2_lambdas(lams=(1e2, 1e3, 1e4), n: int = 1 << 16, width_cells: float = 50.0) -> Workload:
+    """cfg2's lambda values as the members of one ensemble (same initial dam break;
+    each member its own dt and t_end clipping): the three runs in one context."""
+    one = cfg2(lams[0], n, width_cells)
+    k = len(lams)
+    rep = lambda a: np.repeat(a, k, axis=0)
+    return Workload("cfg2_dambreak_lambdas", n, k, one.x_min, one.x_max, one.bc, np.array(lams, dtype=float),
+                    rep(one.h), rep(one.q), rep(one.K), rep(one.W), cfl=one.cfl, mcfl=one.mcfl,
+                    t_end=one.t_end, filter_sigma=one.filter_sigma)
+
+
 def cfg3(members: int = 4096, n: int = 4096, seed: int = 7539003, dx: float = 0.1,
          first_member: int = 0, filter_sigma: float = 0.25) -> Workload:
     """Batched ensemble: `members` periodic domains of n cells (dx = 0.1); per member

@@ -365,6 +365,23 @@ def test_cfg2_dam_break_walls_scaled():
         assert abs(d["mass"] - m0) <= 1e-13 * m0
 
 
+def test_cfg2_lambdas_as_one_ensemble():
+    """cfg2's three lambdas as the members of one context (2^14 cells): each
+    member keeps its own dt; equal to the oracle per member after 200 steps,
+    and bitwise equal to the one-member runs (members are independent)."""
+    w = W.cfg2_lambdas(n=1 << 14)
+    s = gpu_solver(w)
+    s.run_steps(200)
+    compare(w, s, range(3), steps=200, tol=TOL_RUN, floor=True)
+    (h, q, K, Wf), t = s.get_state(device=False)
+    for m, lam in enumerate(w.lam):
+        one = gpu_solver(W.cfg2(float(lam), n=1 << 14))
+        one.run_steps(200)
+        (h1, q1, K1, W1), t1 = one.get_state(device=False)
+        assert t1[0] == t[m]
+        assert np.array_equal(h1[0], h[m]) and np.array_equal(q1[0], q[m])
+
+
 def test_cfg5_bathymetry_scaled():
     """cfg5 recipe (random field + sinusoidal bathymetry, lam = 1e4) on 2^20 cells."""
     w = W.cfg5_workload(1 << 20)

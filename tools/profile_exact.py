@@ -18,7 +18,8 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from profile_summary import full  # noqa: E402
 
 LIB = os.path.join(ROOT, "paper_2510_07539_b200", "lib", "libhsgn.so")
-CLUSTER_OPS = ("UCGABAR_ARV", "UCGABAR_WAIT", "SYNCS", "STAS", "MEMBAR", "FENCE", "ELECT", "REDUX", "CREDUX")
+CLUSTER_OPS = ("UBLKCP", "LDGSTS", "UCGABAR_ARV", "UCGABAR_WAIT", "SYNCS", "STAS", "MEMBAR", "FENCE", "REDUX",
+               "CREDUX", "MUFU")
 
 
 def sass_ops(kernel_re):
@@ -58,11 +59,14 @@ def main():
                 d["kernel"], d.get("duration", 0) / 1e3, b, d.get("achieved_occupancy_pct", 0),
                 d.get("issue_active_pct", 0), d.get("fp64_pipe_pct", 0), d.get("ipc_per_sm", 0),
                 d.get("registers", 0), ", ".join(f"{n} {v}" for n, v in d["top_stalls"])))
-    md += ["", "Static SASS (cuobjdump -sass of the built library): cluster barrier, mbarrier (SYNCS), "
-               "remote shared stores with transaction completion (STAS = st.async ... mbarrier::complete_tx), "
-               "warp reductions.  One row per kernel instantiation without bathymetry.", "",
+    md += ["", "Static SASS (cuobjdump -sass of the built library): TMA bulk copies (UBLKCP), cp.async "
+               "(LDGSTS), cluster barrier (UCGABAR), mbarrier (SYNCS), remote shared stores with transaction "
+               "completion (STAS = st.async ... mbarrier::complete_tx), warp reductions (REDUX / CREDUX), "
+               "reciprocal / rsqrt seeds (MUFU.RCP64H / RSQ64H).  One row per kernel instantiation without "
+               "bathymetry; the overlapped-tile stage kernels (default path) for comparison.", "",
            "| kernel | instructions | " + " | ".join(CLUSTER_OPS) + " |", "|---|---|" + "---|" * len(CLUSTER_OPS)]
-    ops = sass_ops(r"cl_stage_kernelILb[01]ELb[01]ELb0E|cl_multi_kernelILb0E|sep_solve|filter_fix")
+    ops = sass_ops(r"stage_kernelILb[01]ELb[01]ELb0ELb0ELb0ELb0E|cl_stage_kernelILb[01]ELb[01]ELb0E|"
+                   r"cl_multi_kernelILb0E|sep_solve|sep_coef|filter_fix|slab_iface")
     for k in sorted(ops):
         c = ops[k]
         tot = sum(c.values())

@@ -22,6 +22,14 @@
 
 namespace hsgn {
 
+// HSGN_EXP_TIMING builds: per-step phase clocks of CTA 0 of member 0 into
+// g_clt (row st = stage; tools/res_timing.py)
+#if HSGN_EXP_TIMING
+#define ML_MARK(st, k) do { if (prof) { const long long t_ = clock64(); g_clt[st][k] += (unsigned long long)(t_ - tml); tml = t_; } } while (0)
+#else
+#define ML_MARK(st, k) do { } while (0)
+#endif
+
 __shared__ double s_dx[C_MAX][4];                     // dt maxima (u, nu), error flag of every CTA
 __shared__ __align__(8) unsigned long long s_emb, s_umb, s_dmb;
 
@@ -64,6 +72,10 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
     double t = P.t[(k0 & 1) * P.members + m];
     const double t_end = P.ctrl->t_end;
 
+#if HSGN_EXP_TIMING
+    const bool prof = m == 0 && c == 0 && tid == 0;
+    long long tml = clock64();
+#endif
     auto arm = [&](unsigned mb, unsigned bytes) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes) : "memory");
     };
@@ -217,6 +229,7 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
         if (dtm == 0.0) {                              // member at t_end (or stopped): carry
             continue;
         }
+        ML_MARK(0, 15);
         // ===== the two IMEX stages; stage 2 inputs E2, R2 =====
 #pragma unroll 1
         for (int st = 0; st < 2; st++) {
@@ -281,6 +294,7 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
                 }
             }
             __syncthreads();
+            ML_MARK(st, 0);                            // phase 1
             if (tid == 0 && left_phys) {
                 const int x = swz(-1), y = swz(0);
                 sQd[x] = (wall_l ? -1.0 : 1.0) * sQd[y]; sHd[x] = sHd[y]; sDe[x] = sDe[y]; sBe[x] = -sBe[y];
@@ -390,6 +404,7 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
                 __syncthreads();
                 fin = nxt;
             }
+            ML_MARK(st, 1);                            // assembly, partition, PCR
             const double Yl = fin[2 * PSTR + tid - 1], Vl = fin[3 * PSTR + tid - 1], Wl = fin[4 * PSTR + tid - 1];
             const double Yr = fin[2 * PSTR + tid + 1], Vr = fin[3 * PSTR + tid + 1], Wr = fin[4 * PSTR + tid + 1];
             const double Yks = fin[2 * PSTR + ks - 1], Vks = fin[3 * PSTR + ks - 1], Wks = fin[4 * PSTR + ks - 1];
@@ -416,8 +431,10 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
                     }
                 }
             }
+            ML_MARK(st, 2);                            // publish
             mbar_wait(xmb, px);
             px ^= 1u;
+            ML_MARK(st, 3);                            // separator wait
             // separator system (lanes = equations, every warp), as in cl_stage_kernel
             double Lm = 0.0, Lc, Lp = 0.0, nx[6];
             {
@@ -464,6 +481,7 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
             }
             __syncthreads();                          // s_cx read by every warp
             if (tid == 0) arm(xmb, XB);
+            ML_MARK(st, 4);                            // separator solve
             double hb[CMCH], hLn, hRn;
             {
                 const double Xk = tid < ks ? D_ - V_ * Lm - W_ * Lc : (tid == ks ? Lc : 0.0);
@@ -504,6 +522,7 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
                 }
             }
             __syncthreads();                          // PCR buffers (arrays 4..7) and arrays 0..3 all read
+            ML_MARK(st, 5);                            // recovery + phase 3
             if (!st2) {
                 // ---- E2, R2 of the own rows -> arrays 0..3 / R slots;
                 //      edge rows to the neighbours (DSMEM) or mirrored (A10)
@@ -543,10 +562,12 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
                 }
                 __syncthreads();
                 mirror_halo(sU, false);
+                ML_MARK(0, 6);                         // E2 / R2 formed and sent
                 mbar_wait(emb, pe);
                 pe ^= 1u;
                 __syncthreads();
                 if (tid == 0) arm(emb, EB);
+                ML_MARK(0, 7);                         // E2 / R2 halo wait
                 continue;                             // -> stage 2
             }
             // ---- final stage: A19 filter (rows -2, -1, Tc, Tc+1 via DSMEM), relaxation,
@@ -578,8 +599,10 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
                     }
                 }
                 __syncthreads();
+                ML_MARK(1, 6);                         // filter rows sent
                 mbar_wait(fmb, pf);
                 pf ^= 1u;
+                ML_MARK(1, 7);                         // filter rows wait
                 if (live) {
                     const double sig16 = P.filter_sigma * (1.0 / 16.0);
                     double xq[CMCH + 4], xw[CMCH + 4];
@@ -635,13 +658,19 @@ __global__ void __launch_bounds__(CNT, HSGN_MMINB) cl_multi_kernel(const Params 
         // ---- commit the step, dt of the next one from U^{n+1}
         t = (t_end > 0.0 && dtm == t_end - t) ? t_end : t + dtm;
         kdone++;
+        ML_MARK(1, 8);                                 // filter, relaxation, U^{n+1} + halos sent
         double um, nm;
         local_maxima(um, nm);
         reduce_dt(um, nm, acc.err, dtm);
+        ML_MARK(1, 9);                                 // dt maxima, cluster max, dt
         mbar_wait(umb, pu);
         pu ^= 1u;
         __syncthreads();
         if (tid == 0) arm(umb, UB);
+        ML_MARK(1, 10);                                // U halo wait
+#if HSGN_EXP_TIMING
+        if (prof) g_clt[1][15] += 1ull;
+#endif
     }
 
     // ---- store U (K-form) of the own rows, the member's time and dt maxima

@@ -307,7 +307,14 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
  * the tiles recomputed and finished with their separator values, and, with the
  * A19 filter, the two rows at each tile end completed by a small kernel: about
  * 2x the work of a stage on the overlapped tiles, for any decay length.
- * Both: the SI stage without Picard passes, the A25 form or slab sides.
+ * Slab contexts (HSGN_BC_HALO sides, group or NCCL transport; every slab in the
+ * same mode): tile-level SPIKE spans all slabs -- each slab solves its
+ * separator system for Y and the spike columns V, W of its two outer
+ * couplings, the slabs exchange 6 doubles right-to-left and all-gather 6 per
+ * slab, and every slab solves the 2P end-separator system (DESIGN.md section
+ * 8); halos shrink to the 4-row stencil.  The host-staged transport refuses it.
+ * Both: the SI stage without Picard passes or the A25 form; the cluster
+ * kernels also not on slab contexts.
  * mode 0: never (overlapped tiles with the decay check); 1: the cluster kernels
  * whenever the member fits; 3: tile-level SPIKE whenever eligible; 2 (default,
  * "auto"): exact paths only when the overlapped tiles cannot bound the decay a

@@ -413,7 +413,11 @@ def main():
         bs1, bs2 = 32, 80
     ach2 = bs2 * Ntot / t2 / 1e9
     ach1 = bs1 * Ntot / t1 / 1e9
-    traffic = profile_traffic(Ntot)
+    # which depth-solve organisation ran (auto mode: DESIGN.md section 6); the
+    # committed ncu traffic belongs to the overlapped-tile stage kernels
+    org = ("cluster" if (a.scheme == "si" and s.cluster) else "spike" if (a.scheme == "si" and s.spike)
+           else "tiles")
+    traffic = profile_traffic(Ntot) if org == "tiles" and a.scheme == "si" and nst == 2 else None
 
     # e2e through the public API with host buffers: pinned host state in, K steps,
     # final state and per-member times out (hsgn_run_host; after the device-timed
@@ -481,8 +485,10 @@ def main():
                      "frac": ach2 / peak, "traffic": traffic,
                      "kernel": ("sgn_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "sgn"
                                 else "explicit_kernel<HEUN2,FINAL> (Heun stage 2)" if a.scheme == "explicit"
-                                else "stage_kernel<FINAL> (the one SI stage)" if nst == 1
-                                else "stage_kernel<STAGE2,FINAL> (stage 2)"),
+                                else ("cl_stage_kernel (cluster, exact solve)" if org == "cluster" else
+                                      "cl_stage_kernel TIPS + sep_solve + FINISH (tile-level SPIKE)" if org == "spike"
+                                      else "stage_kernel") +
+                                     (" <FINAL> (the one SI stage)" if nst == 1 else " <STAGE2,FINAL> (stage 2)")),
                      "bytes_model": (f"{bs2} B/cell per launch (read U^n; write U^{{n+1}})" if nst == 1 else
                                      f"{bs2} B/cell per stage-2 launch (read U^n, U1{', b' if bathy else ''}; write U^{{n+1}})"),
                      "peak_source": peak_src,

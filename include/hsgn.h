@@ -320,7 +320,10 @@ hsgn_status hsgn_set_well_balanced(hsgn_ctx *ctx, int32_t on);
  * "auto"): exact paths only when the overlapped tiles cannot bound the decay a
  * priori, i.e. material-CFL-only stepping (cfl_imex <= 0) without a
  * user overlap -- the cluster kernels if the member fits, else tile-level
- * SPIKE (the overlapped tiles are faster on B200 when CFL_IMEX bounds rho).
+ * SPIKE -- or when the overlapped tiles solve many redundant rows ((T + 2w) / T
+ * >= 1.5 for the cluster kernels, >= 2.4 for SPIKE, e.g. the first-order SI
+ * step); the overlapped tiles are faster on B200 when CFL_IMEX bounds rho
+ * tightly (the paper's tableau at CFL_IMEX 2: 1.19 rows per kept cell).
  * Drops captured graphs.  Errors: HSGN_E_INVALID (null context, mode outside
  * 0..3). */
 hsgn_status hsgn_set_cluster(hsgn_ctx *ctx, int32_t mode);

@@ -262,16 +262,33 @@ bool spike_eligible(const hsgn_ctx *c)
 // cannot bound the depth system's decay a priori
 bool overlap_unbounded(const hsgn_ctx *c) { return !(c->cfl > 0.0) && c->desc.overlap <= 0; }
 
+// rows the overlapped tiles solve per kept cell, (T + 2w) / T (1 when the caller
+// chose the tile geometry: then auto mode keeps the tiles)
+double tile_redundancy(const hsgn_ctx *c)
+{
+    if (c->desc.tile_cells > 0 || c->desc.overlap > 0 || c->T <= 0) return 1.0;
+    return double(c->T + 2 * c->w) / c->T;
+}
+
+// auto mode (2): the exact paths also win where the overlap tax is high.
+// Measured on cfg3: per solved row the cluster kernels
+// cost ~1.33x and tile-level SPIKE ~1.9x the overlapped tiles, which solve
+// (T + 2w) / T rows per kept cell (1.19 at CFL_IMEX 2 with the paper's
+// tableau, 1.91 for the first-order SI step: cluster 27.3 vs tiles 24.4 G)
+constexpr double AUTO_CLUSTER_REDUNDANCY = 1.5, AUTO_SPIKE_REDUNDANCY = 2.4;
+
 bool use_cluster(const hsgn_ctx *c)
 {
-    const bool on = c->cl_mode == 1 || (c->cl_mode == 2 && overlap_unbounded(c));
+    const bool on = c->cl_mode == 1 ||
+                    (c->cl_mode == 2 && (overlap_unbounded(c) || tile_redundancy(c) >= AUTO_CLUSTER_REDUNDANCY));
     return on && c->clC > 0 && exact_eligible(c);
 }
 
 bool use_spike(const hsgn_ctx *c)
 {
     if (use_cluster(c) || c->spG <= 0 || !spike_eligible(c) || c->sp_tips == nullptr) return false;
-    return c->cl_mode == 3 || (c->cl_mode == 2 && overlap_unbounded(c));
+    return c->cl_mode == 3 ||
+           (c->cl_mode == 2 && (overlap_unbounded(c) || (!c->slab && tile_redundancy(c) >= AUTO_SPIKE_REDUNDANCY)));
 }
 
 // ghost cells a BC_HALO side takes from its neighbour per exchange: the

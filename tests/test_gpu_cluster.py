@@ -163,3 +163,14 @@ def test_mcfl_only_coercivity_loss_agrees_with_oracle(mode):
     assert eg.value.name == "E_COERCIVITY", eg.value
     (b, tb) = s.get_state(device=False, check=False)    # the state of step 20 is kept
     assert tb[0] == ta[0] and all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_auto_mode_first_order_uses_cluster_kernels():
+    """auto: the first-order SI step (tau = dt) needs overlap w = 152 on the
+    tiles (638 rows for 334 kept cells): the cluster kernels take over"""
+    hs = __import__("paper_2510_07539_b200.hsgn", fromlist=["hsgn"])
+    w = W.random_smooth(4096, 2, seed=21, amp=0.05)
+    s = _gpu_solver(w, tableau=hs.euler_tableau(), order=1)
+    assert s.cluster == (8, 512), (s.cluster, s.geometry)
+    s.run_steps(5)
+    compare(w, s, range(2), steps=5, order=1, tableau=O.euler_tableau(), tol=1e-10)

@@ -139,6 +139,8 @@ typedef struct {
 /* Create a context on the current CUDA device.  cuda_stream is a cudaStream_t
  * (NULL = legacy default stream) that every later call enqueues on. */
 hsgn_status hsgn_create(const hsgn_desc *desc, void *cuda_stream, hsgn_ctx **out);
+/* Synchronises the context's streams (no kernel or copy still uses the
+ * workspace when it returns) and frees the context.  NULL is a no-op. */
 void hsgn_destroy(hsgn_ctx *ctx);
 
 /* Bytes of device workspace the context needs (3 state buffers of

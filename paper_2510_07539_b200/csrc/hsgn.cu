@@ -1282,6 +1282,12 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
 void hsgn_destroy(hsgn_ctx *c)
 {
     if (!c) return;
+    // the caller frees the workspace after this returns: no kernel or copy of
+    // this context may still be using it
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->cs2) cudaStreamSynchronize(c->cs2);
+    if (c->cp_in) cudaStreamSynchronize(c->cp_in);
+    if (c->cp_out) cudaStreamSynchronize(c->cp_out);
     free_kids(c);
     if (c->cp_in) cudaStreamDestroy(c->cp_in);
     if (c->cp_out) cudaStreamDestroy(c->cp_out);

@@ -201,6 +201,10 @@ class Solver:
         self.ctx = h
         nbytes = self.L.hsgn_workspace_bytes(self.ctx)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        # the library works on self.stream: order it after torch's stream (the
+        # memory may just have been released there) and tell the allocator
+        self.workspace.record_stream(self.stream)
+        self.stream.wait_stream(torch.cuda.current_stream())
         self._chk(self.L.hsgn_set_workspace(self.ctx, C.c_void_p(self.workspace.data_ptr()), nbytes))
         self._keep = []
 
@@ -280,6 +284,9 @@ class Solver:
         if b is not None:
             b = self._as_f64(b)
             self._keep.append(b)
+            # a device tensor may still be being written on torch's stream: the
+            # library copies on the solver's stream
+            self.stream.wait_stream(self._torch.cuda.current_stream())
         self._chk(self.L.hsgn_set_bathymetry(self.ctx, C.c_void_p(_ptr(b)) if b is not None else None))
 
     def set_relaxation(self, relax: dict | None):

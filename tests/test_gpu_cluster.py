@@ -174,3 +174,16 @@ def test_auto_mode_first_order_uses_cluster_kernels():
     assert s.cluster == (8, 512), (s.cluster, s.geometry)
     s.run_steps(5)
     compare(w, s, range(2), steps=5, order=1, tableau=O.euler_tableau(), tol=1e-10)
+
+
+@pytest.mark.slow
+def test_cluster_cfg3_full_size_sampled():
+    """cfg3 at full size on the cluster kernels (mode 1), sampled members"""
+    w = W.cfg3()
+    s = gpu_solver(w)
+    assert s.cluster == (8, 512)
+    sample = [3, 1000, 4094]
+    s.run_steps(1)
+    compare(w, s, sample, steps=1, floor=True)
+    s.run_steps(199)
+    compare(w, s, sample[:2], steps=200, tol=TOL_RUN, floor=True)

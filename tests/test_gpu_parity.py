@@ -392,9 +392,11 @@ def test_cfg5_bathymetry_scaled():
     compare(w, s, [0], steps=10, tol=1e-10, floor=True)
 
 
-def test_cfg5_full_size_sampled():
+@pytest.mark.parametrize("mode", [0, 3])
+def test_cfg5_full_size_sampled(mode):
     """cfg5 at its full size (2^28 cells, bathymetry, filter) in bench.py's launch
-    configuration, one step.  Sampled windows are checked against the oracle run
+    configuration (mode 0: the overlapped tiles; mode 3: tile-level SPIKE over
+    524288 tiles, 1024-thread separator solve), one step.  Sampled windows are checked against the oracle run
     on the window itself (transmissive ends, the GPU's dt): the implicit solve's
     influence decays like r^d per stage (r ~ 0.42 at CFL 2),
     so the centre of a window with 1024-cell margins sees the wrong ends at
@@ -409,6 +411,8 @@ def test_cfg5_full_size_sampled():
     s.set_bathymetry(b)
     s.set_filter(0.25)
     s.set_state(h, q, K, Wf)
+    s.set_cluster(mode)
+    assert (s.spike is not None) == (mode == 3)
     dx = meta["L"] / n
     lam = float(meta["lam"]) if np.ndim(meta["lam"]) == 0 else float(np.ravel(meta["lam"])[0])
     # dt rule over the whole domain (A7, A8)

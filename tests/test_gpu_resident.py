@@ -68,3 +68,19 @@ def test_resident_error_keeps_the_state():
     with pytest.raises(hs.HsgnError) as e:
         s.run_resident(5)
     assert e.value.name == "E_DRY"
+
+
+@pytest.mark.slow
+def test_resident_cfg3_full_size_sampled():
+    """cfg3 at full size (4096 x 4096) in the bench's resident launch
+    configuration (one launch of K steps, sub-record cfg3_resident); sampled
+    members against the oracle after 1 and 200 steps"""
+    from paper_2510_07539_b200 import hsgn as hs
+    w = W.cfg3()
+    s = hs.solver_for(w)
+    sample = [0, 1, 777, 2048, 4095]
+    s.run_resident(1)
+    compare(w, s, sample, steps=1, floor=True)
+    s.run_resident(199)
+    assert s.diagnostics()["steps"] == 200
+    compare(w, s, sample[:3], steps=200, tol=TOL_RUN, floor=True)

@@ -117,7 +117,7 @@ struct Bufs {
 
 #if HSGN_EXP_TIMING
 // [stage][load wait, compute + store issue, epilogue + drain, CTAs, in-place + phase 1,
-//  phase 2, phase 3 + staging, -]
+//  phase 2, phase 3 + staging, of phase 2: PCR + recovery]
 __device__ unsigned long long g_exp[16];
 __shared__ long long s_tph[4];
 #define EXP_MARK(k) do { if (threadIdx.x == 0) s_tph[k] = clock64(); } while (0)
@@ -992,6 +992,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         // step.  The reduced couplings shrink like e_{s+1} <= e_s^2/(1-2e_s^2)
         // (e = max |A|,|C|), so PCR stops once e^(2^s) <= 2^-64: the rows are
         // then decoupled to below round-off (x_k = D_k).
+        EXP_MARK(2);
         pcr0[tid] = A_; pcr0[NT + tid] = C_; pcr0[2 * NT + tid] = D_;
         {
             const float ea = float(fabs(A_)), ec = float(fabs(C_));
@@ -1394,6 +1395,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
             atomicAdd(g + 4, (unsigned long long)(s_tph[0] - t1));
             atomicAdd(g + 5, (unsigned long long)(s_tph[1] - s_tph[0]));
             atomicAdd(g + 6, (unsigned long long)(t2 - s_tph[1]));
+            atomicAdd(g + 7, (unsigned long long)(s_tph[1] - s_tph[2]));   // PCR + recovery
         }
     }
 #endif

@@ -49,6 +49,11 @@ constexpr int LCAP = NT * MCH;      // 1280 rows per CTA incl. phase-1 halo rows
 constexpr int SROWS = LCAP + 16;    // smem row capacity per array (even: 16-B aligned bases;
                                     // rows up to L+MCH+2 past a base shifted by <= 4)
 constexpr int NARR = 8;             // smem arrays
+// PCR buffers of the stage kernels (arrays 2..3 during phase 2): zero pads of
+// PPADR slots around each of the three vectors, two buffers
+constexpr int PPADR = NT / 2;                     // largest PCR distance
+constexpr int PVS = NT + PPADR;                   // vector stride
+constexpr int PBUF = 3 * PVS + PPADR;             // buffer stride (pad, A, pad, C, pad, D, pad)
 constexpr size_t SMEM_BYTES = size_t(NARR) * SROWS * sizeof(double);
 // one-CTA-per-tile stage kernels with bathymetry: b of the tile's raw rows in a
 // ninth array (the per-row global reads of b through the boundary map cost more
@@ -723,8 +728,8 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 if (wall_par) {
                     (void)map_cell(start + r, n, P.bcl, P.bcr, par0);
                     (void)map_cell(start + r + 1, n, P.bcl, P.bcr, par1);
+                    eq.x *= par0; eq.y *= par1;
                 }
-                eq.x *= par0; eq.y *= par1;
                 // (scratch rows clamped onto rows -3 .. L+2: stay inside slab halos)
                 const double b0 = (raw && BATHY) ? bz(max(r, -3)) : 0.0;
                 const double b1 = (raw && BATHY) ? bz(min(r + 1, L + 2)) : 0.0;
@@ -764,11 +769,19 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     const bool live = r0 < L + 2;
     double wd[MCH];                  // W^dagger of own rows (phase 1 -> 3)
     double hRv[MCH];                 // h^R' of own rows (phase 1 -> 2)
+    // Row -1 (the tile's left halo row of phase 1) is computed by the last
+    // thread when its own chunk is dead (L <= (NT - 1) MCH - 2, every tile but
+    // the largest): it runs the ordinary chunk loop over rows -1 .. MCH-2 and
+    // stores row -1 only, in parallel with the others; otherwise thread 0 does
+    // it before its own chunk.
+    const bool m1_last = (NT - 1) * MCH >= L + 2;                // CTA-uniform
+    const bool row_m1 = m1_last && tid == NT - 1;
+    const int p0 = row_m1 ? -1 : r0;                             // first phase-1 row
 
     // ---- phase 1: faces, predictor, coefficients --------------------------
     // Branch-free over the MCH own rows (stores predicated on r <= L) so the
-    // register window shifts are pure renaming; thread 0 also does row -1.
-    if (live) {
+    // register window shifts are pure renaming.
+    if (live || row_m1) {
         const double kap = P.order == 2 ? 0.25 : 0.0;
         RowCtx C{};
         C.tau = tau; C.tdx2 = tdx2; C.t2 = t2; C.lt2 = lt2; C.lam = lam; C.lam3 = lam3;
@@ -776,12 +789,12 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         C.c23 = (2.0 / 3.0) * lam * lt2;
         double wh[3], wq[3], wH[3], wW[3];
 #pragma unroll
-        for (int k = 0; k < 3; k++) {                 // rows r0-2 .. r0
-            const int rr = r0 - 2 + k;
+        for (int k = 0; k < 3; k++) {                 // rows p0-2 .. p0
+            const int rr = p0 - 2 + k;
             wh[k] = sEh[rr]; wq[k] = sEq[rr]; wH[k] = sEH[rr]; wW[k] = sEW[rr];
         }
-        FState Mm = muscl_minus(wh, wq, wH, wW, kap);           // M_{r0-1}
-        if (tid == 0) {
+        FState Mm = muscl_minus(wh, wq, wH, wW, kap);           // M_{p0-1}
+        if (!m1_last && tid == 0) {
             // row -1 (left halo of the tile): faces -3/2 and -1/2
             double xh[3], xq[3], xH[3], xW[3];
 #pragma unroll
@@ -801,13 +814,15 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         for (int k = 0; k < 2; k++) {
             wh[k] = wh[k + 1]; wq[k] = wq[k + 1]; wH[k] = wH[k + 1]; wW[k] = wW[k + 1];
         }
-        wh[2] = sEh[r0 + 1]; wq[2] = sEq[r0 + 1]; wH[2] = sEH[r0 + 1]; wW[2] = sEW[r0 + 1];
+        wh[2] = sEh[p0 + 1]; wq[2] = sEq[p0 + 1]; wH[2] = sEH[p0 + 1]; wW[2] = sEW[p0 + 1];
         FState Pn, Mr;
-        muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);               // Pl_{r0}, M_{r0}
-        Face Fl = rusanov(Mm, Pn);                             // face r0-1/2
+        muscl_pair(wh, wq, wH, wW, kap, Pn, Mr);               // Pl_{p0}, M_{p0}
+        Face Fl = rusanov(Mm, Pn);                             // face p0-1/2
 #pragma unroll
         for (int i = 0; i < MCH; i++) {
-            const int r = r0 + i;
+            const int r = p0 + i;
+            // rows this thread stores: its own rows up to L, or row -1 only
+            const bool own = row_m1 ? (i == 0) : (r <= L);
             double ch[3], cq[3], cH[3], cW[3];                 // rows r-1, r, r+1
 #pragma unroll
             for (int k = 0; k < 3; k++) { ch[k] = wh[k]; cq[k] = wq[k]; cH[k] = wH[k]; cW[k] = wW[k]; }
@@ -821,15 +836,16 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const Face Fr = rusanov(Mr, Pn);                   // face r+1/2
             Mr = Mn;
             double beta, hRr;
-            row_update<BATHY, WB>(st2, C, P, sBz, r <= L ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
+            row_update<BATHY, WB>(st2, C, P, sBz, own ? r : -1000000, start, n, ch, cq, cH, cW, Fl, Fr,
                                       sQd, sHd, sBe, sDe, wd[i], beta, hRr);
-            hRv[i] = r <= L ? hRr : 0.0;                       // rows > L: decoupled, finite
+            hRv[i] = own ? hRr : 0.0;                          // rows > L: decoupled, finite
+            if (i == 0 && row_m1) beta = 2.2250738585072014e-308;   // row -1: not a tile row
             // coercivity on every row of the tile (overlap rows are real
             // cells, and the kept rows' solve relies on them too); the rho bound
             // of the overlap check from max beta (high words: +1 ulp of 2^-20)
             if (!(beta > 0.0)) acc.err |= ERR_COERC;
             acc.bhi = max(acc.bhi, __double2hiint(beta));
-            if (r < L) acc.kkey = min(acc.kkey, khi_key(beta));
+            if (!row_m1 && r < L) acc.kkey = min(acc.kkey, khi_key(beta));
             Fl = Fr;
         }
     } else {
@@ -842,8 +858,9 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // coupling across both tile ends is cut (truncated overlap or Neumann end:
     // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
     // make those face coefficients t2 (beta_i + beta_{i+1}) / 2 exactly zero;
-    // rows L+1 .. L+MCH+1 (read by the last live chunk) get zero fields and
-    // alternating +-beta_{L-1}, so all their couplings vanish too.
+    // rows L+1 .. L+MCH+2 (read by the last live chunk, and as the window of
+    // every dead chunk) get zero fields and alternating +-beta_{L-1}, so all
+    // their couplings vanish too (dead chunks are identity rows).
     auto tile_end_ghosts = [&]() {
         if (tid == 0) {
             if (left_phys) {
@@ -859,13 +876,23 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             }
             sBe[L] = -sBe[L - 1];
         }
-        if (tid >= 64 && tid < 64 + MCH + 1) {
+        if (tid >= 64 && tid < 64 + MCH + 2) {
             const int r = L + 1 + (tid - 64);
             sQd[r] = 0.0; sHd[r] = 0.0; sDe[r] = 0.0;
             sBe[r] = ((r - L) & 1) ? sBe[L - 1] : -sBe[L - 1];
         }
     };
     tile_end_ghosts();
+    // zero pads around the PCR vectors (arrays 2..3 are free after phase 1):
+    // partners outside [0, NT) read exact zeros, no bounds tests in the levels
+    {
+        double *const pb = smem + 2 * SROWS;
+#pragma unroll
+        for (int k = tid; k < 8 * PPADR; k += NT) {
+            const int b = k / (4 * PPADR), v = (k / PPADR) & 3, o = k % PPADR;
+            pb[b * PBUF + v * PVS + o] = 0.0;
+        }
+    }
     __syncthreads();
 
     // ---- phase 2: assemble + partition solve (A1, A3) ---------
@@ -873,19 +900,32 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // arrays 2..3 (later the filter buffers), E_h stays in array 0; arrays
     // 4..7 take the output staging during phase 3.
     double *sHB = sEq;                                           // hbar[r], r in [0, L)
-    double *pcr0 = smem + 2 * SROWS;                             // 2 x 3 x NT doubles
-    double *pcr1 = pcr0 + 3 * NT;
+    // two PCR buffers of three vectors (A, C, D) of NT slots, each vector
+    // between zero pads of PPADR slots (PVS = NT + PPADR)
+    double *pcr0 = smem + 2 * SROWS + PPADR;
+    double *pcr1 = pcr0 + PBUF;
     double *sEhc = sEh;                                          // E_h (BATHY)
     // register windows over rows r0-1 .. r0+MCH
+    // (dead chunks read the ghost rows L+1 .. L+MCH+2: identity rows)
     double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
-    if (live) {
+    // (stage 2, at the register cap, measured faster with zeroed dead windows:
+    // 483 vs 486 us on cfg3)
+    if (STAGE2) {
+        if (live) {
 #pragma unroll
-        for (int k = 0; k < MCH + 2; k++) {
-            vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; vH[k] = sHd[r0 - 1 + k]; vq[k] = sQd[r0 - 1 + k];
+            for (int k = 0; k < MCH + 2; k++) {
+                vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; vH[k] = sHd[r0 - 1 + k]; vq[k] = sQd[r0 - 1 + k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < MCH + 2; k++) { vb[k] = 0.0; vd[k] = 0.0; vH[k] = 0.0; vq[k] = 0.0; }
         }
     } else {
+        const int wb0 = live ? r0 - 1 : L + 1;
 #pragma unroll
-        for (int k = 0; k < MCH + 2; k++) { vb[k] = 0.0; vd[k] = 0.0; vH[k] = 0.0; vq[k] = 0.0; }
+        for (int k = 0; k < MCH + 2; k++) {
+            vb[k] = sBe[wb0 + k]; vd[k] = sDe[wb0 + k]; vH[k] = sHd[wb0 + k]; vq[k] = sQd[wb0 + k];
+        }
     }
     double hb[MCH];
     // PIC: alpha, a^2 at E of the own rows, in two arrays after the tile's (shared
@@ -993,7 +1033,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         // (e = max |A|,|C|), so PCR stops once e^(2^s) <= 2^-64: the rows are
         // then decoupled to below round-off (x_k = D_k).
         EXP_MARK(2);
-        pcr0[tid] = A_; pcr0[NT + tid] = C_; pcr0[2 * NT + tid] = D_;
+        pcr0[tid] = A_; pcr0[PVS + tid] = C_; pcr0[2 * PVS + tid] = D_;
         {
             const float ea = float(fabs(A_)), ec = float(fabs(C_));
             const float ev = warp_max_nonneg(ea > ec ? ea : ec);
@@ -1018,20 +1058,20 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             }
         }
         // one PCR level at distance sd (compile-time), cur -> nxt
+        // (partners outside [0, NT) are the zero pads)
         auto level = [&](const int sd, const double *cur, double *nxt) {
             const int km = tid - sd, kp = tid + sd;
-            double Am = 0, Cm = 0, Dm = 0, Ap = 0, Cp = 0, Dp = 0;
-            if (km >= 0) { Am = cur[km]; Cm = cur[NT + km]; Dm = cur[2 * NT + km]; }
-            if (kp < NT) { Ap = cur[kp]; Cp = cur[NT + kp]; Dp = cur[2 * NT + kp]; }
+            const double Am = cur[km], Cm = cur[PVS + km], Dm = cur[2 * PVS + km];
+            const double Ap = cur[kp], Cp = cur[PVS + kp], Dp = cur[2 * PVS + kp];
             const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
             const double An = -A_ * Am * ib;
             const double Cn = -C_ * Cp * ib;
             const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
             A_ = An; C_ = Cn; D_ = Dn;
-            nxt[tid] = A_; nxt[NT + tid] = C_; nxt[2 * NT + tid] = D_;
+            nxt[tid] = A_; nxt[PVS + tid] = C_; nxt[2 * PVS + tid] = D_;
             __syncthreads();
         };
-        static_assert(NT == 128, "PCR levels below are written out for 128 unknowns");
+        static_assert(NT % 32 == 0 && NT <= 256, "PCR levels below are written out for up to 256 unknowns");
         if (lim > 1) level(1, pcr0, pcr1);
         if (lim > 2) level(2, pcr1, pcr0);
         if (lim > 4) level(4, pcr0, pcr1);
@@ -1039,6 +1079,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         if (lim > 16) level(16, pcr0, pcr1);
         if (lim > 32) level(32, pcr1, pcr0);
         if (lim > 64) level(64, pcr0, pcr1);
+        if (NT > 128 && lim > 128) level(128, pcr1, pcr0);
         const double Xk = D_;
         double XL = __shfl_up_sync(0xffffffffu, Xk, 1);
         if (lane == 31) s_xch[wid][0] = Xk;       // last chunk of this warp
@@ -1128,10 +1169,15 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         HdD[i] = vH[i + 1] * rden;
         qbv[i] = qb;
         Wbv[i] = wd[i] - ltau * HdD[i];
-        if (r >= klo && r < khi) {
-            if (!(h0 > P.h_min)) acc.err |= ERR_DRY;
-            // one test for all four: a NaN or inf in any makes the sum non-finite
-            if (!isfinite(h0 + qb + HdD[i] + Wbv[i])) acc.err |= ERR_NONFINITE;
+        {
+            // dry rows among the kept ones; non-finite values among the rows the
+            // stage delivers (with the filter: also its +-2 input rows, so the
+            // filtered values need no test of their own).  One test for all four:
+            // a NaN or inf in any makes the sum non-finite.  Branch-free.
+            const bool kept = (r >= klo) && (r < khi);
+            const unsigned ed = !(h0 > P.h_min) ? unsigned(ERR_DRY) : 0u;
+            const unsigned ef = !isfinite(h0 + qb + HdD[i] + Wbv[i]) ? unsigned(ERR_NONFINITE) : 0u;
+            acc.err |= (kept ? ed : 0u) | ((filt ? act : kept) ? ef : 0u);
         }
         if (filt && r < L) { sQb[r] = qb; sWb[r] = Wbv[i]; }
     }
@@ -1153,7 +1199,10 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
 #pragma unroll
     for (int i = 0; i < MCH; i++) {
         const int r = r0 + i;
-        if (r < klo || r >= khi) continue;
+        // rows outside [klo, khi) are computed and masked (no per-row branch),
+        // except on the relaxation and mirrored-filter paths
+        const bool kept = (r >= klo) && (r < khi);
+        if (!kept && (RELAX || (filt && !fwin))) continue;
         double qo = qbv[i], wo = Wbv[i];
         if (filt) {
             // A19: f_i - (sigma/16)(f_{i-2} - 4 f_{i-1} + 6 f_i - 4 f_{i+1} + f_{i+2})
@@ -1180,7 +1229,6 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 qo = f5(fq[0], fq[1], fq[2], fq[3], fq[4]);
                 wo = f5(fw[0], fw[1], fw[2], fw[3], fw[4]);
             }
-            if (!isfinite(qo + wo)) acc.err |= ERR_NONFINITE;
         }
         double h0 = hb[i];
         const double Hb = HdD[i] * (h0 * h0);
@@ -1196,11 +1244,10 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         } else if (fin) {
             const double u = fabs(qo * ihv[i]), sg = HdD[i];
             const double nu = u + fsqrt(g * h0 + lam3 * sg * sg);
-            acc.umax = u > acc.umax ? u : acc.umax;
-            acc.numax = nu > acc.numax ? nu : acc.numax;
+            acc.umax = (kept && u > acc.umax) ? u : acc.umax;
+            acc.numax = (kept && nu > acc.numax) ? nu : acc.numax;
         }
-        hb[i] = h0; qbv[i] = qo; HdD[i] = Ko; Wbv[i] = wo;
-        {                     // staging arrays 4..7 are not read in this phase
+        if (kept) {           // staging arrays 4..7 are not read in this phase
             const int ko = r - klo;
             smem[4 * SROWS + ko] = h0; smem[5 * SROWS + ko] = qo;
             smem[6 * SROWS + ko] = Ko; smem[7 * SROWS + ko] = wo;

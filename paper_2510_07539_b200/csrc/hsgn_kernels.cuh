@@ -101,6 +101,10 @@ struct Params {
     int sx_rank, sx_P;
     const Ctrl *ctrl;
     int kslot, kpar;                 // host step index k: k mod 3, k mod 2
+    // the step's first stage computes the step's dt itself (dt_commit_kernel's
+    // rule, no launch of its own: stage_kernel<..., FDT>, small ensembles);
+    // commit_prev: it also commits step k - 1
+    int fuse_dt, commit_prev;
     // slab decomposition (BC_HALO sides): ghost cells received from the
     // neighbouring slab, H cells each: [0..3] U^n fields, [4..7] U1, [8] b
     const double *halo_l[9];
@@ -230,6 +234,23 @@ __device__ __forceinline__ double dt_rule(double cfl, double mcfl, double dx, do
         d = -1.0;
     }
     return d;
+}
+
+// dt of the step with maxima slot kslot and time parity kpar for member m
+// (t_end clipping S:342); negative: invalid (ERR_DT).
+__device__ __forceinline__ double member_dt(const Params &P, int kslot, int kpar, int m)
+{
+    const int members = P.members;
+    const double umax = __longlong_as_double((long long)P.maxes[(kslot * 2 + 0) * members + m]);
+    const double numax = __longlong_as_double((long long)P.maxes[(kslot * 2 + 1) * members + m]);
+    const double t_end = P.ctrl->t_end, dt_fixed = P.ctrl->dt_fixed;
+    const double tm = P.t[kpar * members + m];
+    double dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, P.idx, umax, numax);
+    if (t_end > 0.0) {
+        if (!(tm < t_end)) dtm = 0.0;
+        else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end (S:342)
+    }
+    return (dtm >= 0.0 && isfinite(dtm)) ? dtm : -1.0;
 }
 
 // sqrt(x), x > 0: MUFU.RSQ64H estimate, two Newton steps for 1/sqrt, one
@@ -1383,7 +1404,9 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 #define EXP_T(v)
 #endif
 
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false, bool WB = false>
+// FDT: the step's first stage computes the step's dt itself (Params::fuse_dt)
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false, bool WB = false,
+          bool FDT = false>
 __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
 {
     EXP_T(t0);
@@ -1405,9 +1428,29 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     }
     issue_load<STAGE2, LD_ALL, BATHY>(P, B, mo, G, Lp, mb, tid);
     if (Lp.bulk) __syncthreads();
-    // ---- run control: dt of this member was set by dt_commit_kernel ---------
+    // ---- run control: dt of this member was set by dt_commit_kernel, or (the
+    // step's first stage with fuse_dt) is computed here by its rule from the
+    // previous step's maxima, the loads overlapping the tile's TMA copies; tile
+    // 0 stores it and frees the maxima slot of two steps back, tile 0 of
+    // member 0 commits the previous step (one launch per step fewer)
     const unsigned int err0 = *((volatile unsigned int *)P.err);
-    const double dtm = P.dt[m];
+    double dtm;
+    if (!STAGE2 && FDT) {
+        dtm = member_dt(P, P.kslot, P.kpar, m);
+        if (j == 0 && tid == 0 && err0 == 0u) {
+            if (m == 0 && P.commit_prev) *P.steps += 1;
+            if (dtm < 0.0) {
+                atomicOr(P.err, ERR_DT);
+            } else {
+                const int slot_z = (P.kslot + 2) % 3;
+                P.dt[m] = dtm;
+                P.maxes[(slot_z * 2 + 0) * P.members + m] = 0ull;
+                P.maxes[(slot_z * 2 + 1) * P.members + m] = 0ull;
+            }
+        }
+    } else {
+        dtm = P.dt[m];
+    }
     const double lam = P.lam[m];
     double tm0 = -1.0, tend0 = -1.0;             // (tile_epilogue: t^{n+1} of tile 0)
     if (FINAL && j == 0 && tid == 0) { tm0 = P.t[P.kpar * P.members + m]; tend0 = P.ctrl->t_end; }
@@ -1416,7 +1459,7 @@ __global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, co
     if (BATHY && Lp.bulk && (Lp.a0 & 1)) cp_async_wait_all();    // b by cp.async (issue_load)
     __syncthreads();
     EXP_T(t1);
-    if (err0) return;
+    if (err0 || dtm < 0.0) return;
 
     TileAcc acc{0.0, 0.0, 0.0, 0u, 1 << 30, 0};
     if (dtm == 0.0) {
@@ -2062,17 +2105,9 @@ __global__ void __launch_bounds__(128) dt_commit_kernel(const Params P, int comm
     const int m = tid;
     const int members = P.members;
     if (m >= members) return;
-    const int slot_r = P.kslot, slot_z = (P.kslot + 2) % 3;
-    const double umax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 0) * members + m]);
-    const double numax = __longlong_as_double((long long)P.maxes[(slot_r * 2 + 1) * members + m]);
-    const double t_end = P.ctrl->t_end, dt_fixed = P.ctrl->dt_fixed;
-    const double tm = P.t[P.kpar * members + m];
-    double dtm = dt_fixed > 0.0 ? dt_fixed : dt_rule(P.cfl, P.mcfl, P.dx, P.idx, umax, numax);
-    if (t_end > 0.0) {
-        if (!(tm < t_end)) dtm = 0.0;
-        else if (tm + dtm >= t_end) dtm = t_end - tm;   // land exactly on t_end (S:342)
-    }
-    if (!(dtm >= 0.0) || !isfinite(dtm)) {
+    const int slot_z = (P.kslot + 2) % 3;
+    const double dtm = member_dt(P, P.kslot, P.kpar, m);
+    if (dtm < 0.0) {
         atomicOr(P.err, ERR_DT);
         return;
     }

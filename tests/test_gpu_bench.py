@@ -35,7 +35,9 @@ def test_bench_line_has_the_contract_keys():
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
-    assert d["gpu_launches"] == 1 + 3 * 3
+    # dt_commit, then 2 stages + dt_commit per step; small ensembles (64 x 8 tiles,
+    # <= 2 waves) fuse the dt into stage 1: 2 stages per step + one dt_commit
+    assert d["gpu_launches"] in (1 + 3 * 3, 2 * 3 + 1)
     assert "sm_mhz" in d["clocks"]
 
 

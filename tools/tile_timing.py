@@ -1,5 +1,5 @@
 """Per-CTA phase clocks of the overlapped-tile stage kernels (dev tool; needs an
-HSGN_EXP_TIMING=1 build passed as HSGN_LIB): python tools/tile_timing.py [members]"""
+HSGN_EXP_TIMING=1 build passed as HSGN_LIB): python tools/tile_timing.py [members | cfg2]"""
 import ctypes as C
 import sys
 
@@ -9,8 +9,8 @@ sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2510_07539_b200 import hsgn  # noqa: E402
 from paper_2510_07539_b200 import workloads as W  # noqa: E402
 
-members = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-w = W.cfg3(members=members)
+arg = sys.argv[1] if len(sys.argv) > 1 else "4096"
+w = W.cfg2(1e2) if arg == "cfg2" else W.cfg3(members=int(arg))
 s = hsgn.solver_for(w)
 s.set_cluster(0)
 f = s.L.hsgn_exp_counters

@@ -34,6 +34,9 @@
 #ifndef HSGN_MINB
 #define HSGN_MINB 4
 #endif
+#ifndef HSGN_MINB1                      // CTAs per SM of the plain first-stage kernels of a 2-stage
+#define HSGN_MINB1 5                    // tableau (42 KB of shared memory each; the others: HSGN_MINB)
+#endif
 #ifndef HSGN_EXP_TIMING                 // dev builds only: per-CTA phase clocks (tools/*timing.py)
 #define HSGN_EXP_TIMING 0
 #endif
@@ -1131,6 +1134,17 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     double qbv[MCH], HdD[MCH], Wbv[MCH], bbv[MCH], ihv[MCH];
     // Neumann at physical ends (hbar_{-1} := hbar_0, hbar_L := hbar_{L-1}); at cut
     // tile ends rows 0 and L-1 are overlap rows whose qbar is never used (w >= 3)
+    constexpr bool reload = !STAGE2 && !FINAL && !BATHY && !PIC && !WB;   // (the 5-CTA kernels)
+    if (reload) {
+        // first-stage kernels: the coefficient windows again from shared memory
+        // (arrays 4..7 are intact until the staging below), so their registers die
+        // after the assembly -- 96 registers without spills, 5 CTAs per SM (stage
+        // 1 313 -> 287 us on cfg3; the second stage measured best at 4 as before)
+#pragma unroll
+        for (int k = 0; k < MCH + 2; k++) {
+            vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; vH[k] = sHd[r0 - 1 + k]; vq[k] = sQd[r0 - 1 + k];
+        }
+    }
     const double hLn = r0 > 0 ? ((r0 - 1 < L) ? sHB[r0 - 1] : 0.0) : hb[0];
     double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
     if (right_phys) {
@@ -1202,7 +1216,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         }
         if (filt && r < L) { sQb[r] = qb; sWb[r] = Wbv[i]; }
     }
-    if (filt) __syncthreads();
+    if (filt || reload) __syncthreads();     // (reads of arrays 4..7 before the staging)
     const double sig16 = P.filter_sigma * (1.0 / 16.0);
     const double t_new = (fin && RELAX) ? P.t[P.kpar * members + m] + dtm : 0.0;
     // filter windows over rows r0-2 .. r0+MCH+1: own rows from registers, two halo
@@ -1407,7 +1421,8 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 // FDT: the step's first stage computes the step's dt itself (Params::fuse_dt)
 template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false, bool WB = false,
           bool FDT = false>
-__global__ void __launch_bounds__(NT, HSGN_MINB) stage_kernel(const Params P, const Bufs B)
+__global__ void __launch_bounds__(NT, (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) ? HSGN_MINB1 : HSGN_MINB)
+    stage_kernel(const Params P, const Bufs B)
 {
     EXP_T(t0);
     const int tid = threadIdx.x;

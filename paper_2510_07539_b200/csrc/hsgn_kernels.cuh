@@ -34,6 +34,9 @@
 #ifndef HSGN_MINB
 #define HSGN_MINB 4
 #endif
+#ifndef HSGN_MINB2                      // CTAs per SM of the plain second-stage kernels
+#define HSGN_MINB2 5
+#endif
 #ifndef HSGN_MINB1                      // CTAs per SM of the plain first-stage kernels of a 2-stage
 #define HSGN_MINB1 5                    // tableau (42 KB of shared memory each; the others: HSGN_MINB)
 #endif
@@ -878,6 +881,13 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     }
     __syncthreads();
     EXP_MARK(0);
+    // plain second stage (5 CTAs per SM): W^dagger of the own rows parked in
+    // array 0 (E_h is dead after phase 1 without bathymetry) until phase 3
+    constexpr bool s2x = STAGE2 && FINAL && !BATHY && !RELAX && !PIC && !WB;
+    if (s2x && live) {
+#pragma unroll
+        for (int i = 0; i < MCH; i++) sEh[r0 + i] = wd[i];
+    }
     // derived-field ghosts at physical boundaries (A10).  The implicit
     // coupling across both tile ends is cut (truncated overlap or Neumann end:
     // r_{-1/2} = r_{L-1/2} = 0): beta_{-1} = -beta_0 and beta_L = -beta_{L-1}
@@ -1132,18 +1142,26 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // HdD = H^dag / (hbar^2 + lam tau^2): Hbar = HdD hbar^2 and, in the
     // final stage, sigma = Hbar / hbar^2 = HdD for the dt maxima
     double qbv[MCH], HdD[MCH], Wbv[MCH], bbv[MCH], ihv[MCH];
+    // final stage without relaxation: h and K of the kept rows are staged in the
+    // first loop (arrays 4..7 are not read in phase 3 then) and the wave speed's
+    // root sqv computed there, so only q, W (filtered) and u wait for the filter
+    // -- fewer values live across it
+    double sqv[MCH];
     // Neumann at physical ends (hbar_{-1} := hbar_0, hbar_L := hbar_{L-1}); at cut
     // tile ends rows 0 and L-1 are overlap rows whose qbar is never used (w >= 3)
-    constexpr bool reload = !STAGE2 && !FINAL && !BATHY && !PIC && !WB;   // (the 5-CTA kernels)
+    constexpr bool reload = (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) || s2x;   // (the 5-CTA kernels)
+    constexpr bool early = FINAL && !RELAX;
     if (reload) {
-        // first-stage kernels: the coefficient windows again from shared memory
-        // (arrays 4..7 are intact until the staging below), so their registers die
-        // after the assembly -- 96 registers without spills, 5 CTAs per SM (stage
-        // 1 313 -> 287 us on cfg3; the second stage measured best at 4 as before)
+        // the plain kernels: the coefficient windows again from shared memory
+        // (arrays 4..7 are intact until the staging), so their registers die after
+        // the assembly -- 96 registers without spills, 5 CTAs per SM (cfg3: stage
+        // 1 313 -> 287 us, stage 2 481 -> 459 us with W^dagger parked and the
+        // early staging)
 #pragma unroll
         for (int k = 0; k < MCH + 2; k++) {
             vb[k] = sBe[r0 - 1 + k]; vd[k] = sDe[r0 - 1 + k]; vH[k] = sHd[r0 - 1 + k]; vq[k] = sQd[r0 - 1 + k];
         }
+        if (early) __syncthreads();          // (the early staging below overwrites arrays 4, 6)
     }
     const double hLn = r0 > 0 ? ((r0 - 1 < L) ? sHB[r0 - 1] : 0.0) : hb[0];
     double hRn = (r0 + MCH < L) ? sHB[r0 + MCH] : 0.0;
@@ -1203,7 +1221,13 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
         }
         HdD[i] = vH[i + 1] * rden;
         qbv[i] = qb;
-        Wbv[i] = wd[i] - ltau * HdD[i];
+        Wbv[i] = (s2x ? sEh[r] : wd[i]) - ltau * HdD[i];
+        if (early) {
+            const double Hb = HdD[i] * (h0 * h0);
+            const double Ko = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
+            sqv[i] = fsqrt(g * h0 + lam3 * HdD[i] * HdD[i]);         // sigma = Hbar / hbar^2 = HdD
+            if ((r >= klo) && (r < khi)) { smem[4 * SROWS + (r - klo)] = h0; smem[6 * SROWS + (r - klo)] = Ko; }
+        }
         {
             // dry rows among the kept ones; non-finite values among the rows the
             // stage delivers (with the filter: also its +-2 input rows, so the
@@ -1264,6 +1288,14 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
                 qo = f5(fq[0], fq[1], fq[2], fq[3], fq[4]);
                 wo = f5(fw[0], fw[1], fw[2], fw[3], fw[4]);
             }
+        }
+        if (early) {
+            const double u = fabs(qo * ihv[i]);
+            const double nu = u + sqv[i];
+            acc.umax = (kept && u > acc.umax) ? u : acc.umax;
+            acc.numax = (kept && nu > acc.numax) ? nu : acc.numax;
+            if (kept) { smem[5 * SROWS + (r - klo)] = qo; smem[7 * SROWS + (r - klo)] = wo; }
+            continue;
         }
         double h0 = hb[i];
         const double Hb = HdD[i] * (h0 * h0);
@@ -1421,7 +1453,8 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 // FDT: the step's first stage computes the step's dt itself (Params::fuse_dt)
 template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false, bool WB = false,
           bool FDT = false>
-__global__ void __launch_bounds__(NT, (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) ? HSGN_MINB1 : HSGN_MINB)
+__global__ void __launch_bounds__(NT, (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) ? HSGN_MINB1
+                                     : (STAGE2 && FINAL && !BATHY && !RELAX && !PIC && !WB) ? HSGN_MINB2 : HSGN_MINB)
     stage_kernel(const Params P, const Bufs B)
 {
     EXP_T(t0);

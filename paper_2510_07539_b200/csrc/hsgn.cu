@@ -232,8 +232,8 @@ hsgn_status launch_stage(hsgn_ctx *c, const Params &P, const Bufs &B)
     } else {
         dim3 grid(c->tiles, c->members);
         if (relax) CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, true>, grid, dim3(NT), sm, P, B));
-        else if (!S2 && !FIN && P.fuse_dt)
-            CUDA_TRY(c, launch_k(c, stage_kernel<false, false, BATHY, false, false, false, true>, grid, dim3(NT), sm, P, B));
+        else if (S2 == FIN && P.fuse_dt)     // small ensembles: the latency variants
+            CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, false, false, false, true>, grid, dim3(NT), sm, P, B));
         else CUDA_TRY(c, launch_k(c, stage_kernel<S2, FIN, BATHY, false>, grid, dim3(NT), sm, P, B));
     }
     c->launches++;
@@ -1274,6 +1274,10 @@ hsgn_status hsgn_create(const hsgn_desc *d, void *stream, hsgn_ctx **out)
     cudaFuncSetAttribute(stage_kernel<false, false, false, false, false, false, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
     cudaFuncSetAttribute(stage_kernel<false, false, true, false, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
+    cudaFuncSetAttribute(stage_kernel<true, true, false, false, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    cudaFuncSetAttribute(stage_kernel<true, true, true, false, false, false, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES_B));
     cudaFuncSetAttribute(stage_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));

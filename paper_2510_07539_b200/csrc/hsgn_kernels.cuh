@@ -711,7 +711,9 @@ __device__ __forceinline__ int khi_key(double v)
 // shared memory: raw U^n (and U1) rows as loaded, output K-form staged at
 // arrays 4..7 (h, q, K, W) index r - klo for the bulk store.
 // ---------------------------------------------------------------------------
-template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, bool PIC = false, bool WB = false>
+// LAT: the small-ensemble (latency) kernels -- 4 CTAs per SM, values kept in
+// registers (one CTA per SM: occupancy does not matter, the per-thread chain does)
+template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX, bool PIC = false, bool WB = false, bool LAT = false>
 __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const Geom &G, int m, int s_cell,
                                            const StageC &S, double dtm, TileAcc &acc)
 {
@@ -883,7 +885,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     EXP_MARK(0);
     // plain second stage (5 CTAs per SM): W^dagger of the own rows parked in
     // array 0 (E_h is dead after phase 1 without bathymetry) until phase 3
-    constexpr bool s2x = STAGE2 && FINAL && !BATHY && !RELAX && !PIC && !WB;
+    constexpr bool s2x = STAGE2 && FINAL && !BATHY && !RELAX && !PIC && !WB && !LAT;
     if (s2x && live) {
 #pragma unroll
         for (int i = 0; i < MCH; i++) sEh[r0 + i] = wd[i];
@@ -1149,7 +1151,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     double sqv[MCH];
     // Neumann at physical ends (hbar_{-1} := hbar_0, hbar_L := hbar_{L-1}); at cut
     // tile ends rows 0 and L-1 are overlap rows whose qbar is never used (w >= 3)
-    constexpr bool reload = (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) || s2x;   // (the 5-CTA kernels)
+    constexpr bool reload = (!STAGE2 && !FINAL && !BATHY && !PIC && !WB && !LAT) || s2x;   // (the 5-CTA kernels)
     constexpr bool early = FINAL && !RELAX;
     if (reload) {
         // the plain kernels: the coefficient windows again from shared memory
@@ -1450,10 +1452,13 @@ __device__ __forceinline__ void init_mbar(unsigned mb)
 #define EXP_T(v)
 #endif
 
-// FDT: the step's first stage computes the step's dt itself (Params::fuse_dt)
+// FDT: the small-ensemble kernels (at most two waves of CTAs, Params::fuse_dt):
+// the step's first stage computes the step's dt itself, and both stages keep
+// the 4-CTA register-resident form (stage_body LAT)
 template <bool STAGE2, bool FINAL, bool BATHY, bool RELAX = false, bool PIC = false, bool WB = false,
           bool FDT = false>
-__global__ void __launch_bounds__(NT, (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) ? HSGN_MINB1
+__global__ void __launch_bounds__(NT, FDT ? HSGN_MINB
+                                     : (!STAGE2 && !FINAL && !BATHY && !PIC && !WB) ? HSGN_MINB1
                                      : (STAGE2 && FINAL && !BATHY && !RELAX && !PIC && !WB) ? HSGN_MINB2 : HSGN_MINB)
     stage_kernel(const Params P, const Bufs B)
 {
@@ -1514,7 +1519,7 @@ __global__ void __launch_bounds__(NT, (!STAGE2 && !FINAL && !BATHY && !PIC && !W
         carry_tile<FINAL, BATHY>(P, B, mo, s, e, lam, acc);
     } else {
         const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
-        stage_body<STAGE2, FINAL, BATHY, RELAX, PIC, WB>(P, B, G, m, s, S, dtm, acc);
+        stage_body<STAGE2, FINAL, BATHY, RELAX, PIC, WB, FDT>(P, B, G, m, s, S, dtm, acc);
         store_tile(B, mo, s, e - s);
     }
     EXP_T(t2);

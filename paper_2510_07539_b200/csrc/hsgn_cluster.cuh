@@ -57,6 +57,9 @@
 #ifndef HSGN_CMINB
 #define HSGN_CMINB 4
 #endif
+#ifndef HSGN_CMINB1            // first-stage kernels: 96 registers fit without spills, 5 CTAs
+#define HSGN_CMINB1 5          // per SM (cfg3 stage 1: cluster 468 -> 455 us, SPIKE 699 -> 655
+#endif                         // us; the second stage measured slower at 5)
 
 namespace hsgn {
 
@@ -243,7 +246,7 @@ enum { CL_MODE_CLUSTER = 0, CL_MODE_TIPS = 1, CL_MODE_FINISH = 2 };
 // on both sides.
 // ---------------------------------------------------------------------------
 template <bool STAGE2, bool FINAL, bool BATHY, int MODE = CL_MODE_CLUSTER>
-__global__ void __launch_bounds__(CNT, HSGN_CMINB) cl_stage_kernel(const Params P, const Bufs B)
+__global__ void __launch_bounds__(CNT, STAGE2 ? HSGN_CMINB : HSGN_CMINB1) cl_stage_kernel(const Params P, const Bufs B)
 {
     constexpr bool CLU = MODE == CL_MODE_CLUSTER;
     double *const sm = hsgn_smem;

@@ -1110,12 +1110,16 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const double Am = cur[km], Cm = cur[PVS + km], Dm = cur[2 * PVS + km];
             const double Ap = cur[kp], Cp = cur[PVS + kp], Dp = cur[2 * PVS + kp];
             const double ib = rcp(1.0 - A_ * Cm - C_ * Ap);
-            const double An = -A_ * Am * ib;
-            const double Cn = -C_ * Cp * ib;
             const double Dn = (D_ - A_ * Dm - C_ * Dp) * ib;
-            A_ = An; C_ = Cn; D_ = Dn;
-            nxt[tid] = A_; nxt[PVS + tid] = C_; nxt[2 * PVS + tid] = D_;
-            __syncthreads();
+            if (2 * sd < lim) {                  // another level follows (lim: CTA-uniform)
+                const double An = -A_ * Am * ib;
+                const double Cn = -C_ * Cp * ib;
+                A_ = An; C_ = Cn; D_ = Dn;
+                nxt[tid] = A_; nxt[PVS + tid] = C_; nxt[2 * PVS + tid] = D_;
+                __syncthreads();
+            } else {
+                D_ = Dn;                         // the last level: x_k = D_, nothing to publish
+            }                                    // (the XL exchange below has its own barrier)
         };
         static_assert(NT % 32 == 0 && NT <= 256, "PCR levels below are written out for up to 256 unknowns");
         if (lim > 1) level(1, pcr0, pcr1);

@@ -1479,7 +1479,10 @@ __global__ void __launch_bounds__(NT, FDT ? HSGN_MINB
     EXP_T(t0);
     const int tid = threadIdx.x;
     const int j = blockIdx.x;        // tile
-    const int m = blockIdx.y;        // member
+    // member: the second stage walks the members backwards, so its first CTAs read the
+    // U1 rows the first stage wrote last (and the next first stage, forwards, the U^{n+1}
+    // rows written last) while they are still in L2
+    const int m = STAGE2 ? P.members - 1 - int(blockIdx.y) : int(blockIdx.y);
     const size_t mo = size_t(m) * P.n;
     const int s = j * P.T;
     const int e = min(P.n, s + P.T);

@@ -225,7 +225,11 @@ hsgn_status hsgn_run_host(hsgn_ctx *ctx, const double *h, const double *q, const
  * two-condition rule of P:613-617 per member.  If dt_used (host, n_members)
  * is non-NULL the call synchronises and reports the dt each member took. */
 hsgn_status hsgn_step(hsgn_ctx *ctx, double dt, double *dt_used);
-/* Enqueue n_steps automatic-dt steps (CUDA-graph replay); asynchronous. */
+/* Enqueue n_steps automatic-dt steps (CUDA-graph replay); asynchronous.
+ * Per step: the stage kernels and one commit / next-dt kernel; for small
+ * ensembles (at most two waves of stage CTAs, e.g. cfg1 and cfg2) the first
+ * stage evaluates the dt rule itself and one commit kernel closes each
+ * sequence of steps -- same dt, same results. */
 hsgn_status hsgn_run_steps(hsgn_ctx *ctx, int64_t n_steps);
 /* Advance every member to t_end (last step clipped), at most max_steps
  * steps; polls the device every `poll` steps.  *steps_done = steps taken. */

@@ -27,10 +27,12 @@
  *   classical SGN scheme (A23): test_oracle_sgn.py; bathymetric closure (A26):
  *     test_oracle_sgnb.py (against the primitive model of P:175-186)
  *   well-balanced face form (A25): test_oracle_wb.py
- *   Picard passes (A24): test_oracle_picard.py -- pinned by contraction, rest,
- *     mass and time order only; the fixed point itself is "parity unpinned"
- *     (the paper prints no Picard result)
- * tools/mutation_check.py applies 37 plausible mistakes; every one fails a pin.
+ *   Picard passes (A24): test_oracle_picard.py (contraction, rest, mass, time
+ *     order) and test_oracle_pins_ops.py (the fixed point equals a dense
+ *     Newton solve of the un-frozen depth equation P:268-285 in numpy)
+ *   A19 filter and A10 relaxation zones: test_oracle_pins_ops.py (single-mode
+ *     symbol, mask, walls; ramp and target against a numpy evaluation)
+ * tools/mutation_check.py applies 44 plausible mistakes; every one fails a pin.
  */
 #include <math.h>
 #include <stdint.h>

@@ -709,7 +709,7 @@ __device__ __forceinline__ int khi_key(double v)
 // ---------------------------------------------------------------------------
 // One IMEX stage S(E, R, tau) on the tile G, data already in
 // shared memory: raw U^n (and U1) rows as loaded, output K-form staged at
-// arrays 4..7 (h, q, K, W) index r - klo for the bulk store.
+// arrays 4..7 (h, q, K, W) index r (rows [klo, khi) go out by the bulk store).
 // ---------------------------------------------------------------------------
 // LAT: the small-ensemble (latency) kernels -- 4 CTAs per SM, values kept in
 // registers (one CTA per SM: occupancy does not matter, the per-thread chain does)
@@ -1242,7 +1242,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const double Hb = HdD[i] * (h0 * h0);
             const double Ko = BATHY ? Hb + 1.5 * h0 * bbv[i] : Hb;
             sqv[i] = fsqrt(g * h0 + lam3 * HdD[i] * HdD[i]);         // sigma = Hbar / hbar^2 = HdD
-            if ((r >= klo) && (r < khi)) { smem[4 * SROWS + (r - klo)] = h0; smem[6 * SROWS + (r - klo)] = Ko; }
+            smem[4 * SROWS + r] = h0; smem[6 * SROWS + r] = Ko;     // (staged at row r, unmasked)
         }
         {
             // dry rows among the kept ones; non-finite values among the rows the
@@ -1310,7 +1310,7 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             const double nu = u + sqv[i];
             acc.umax = (kept && u > acc.umax) ? u : acc.umax;
             acc.numax = (kept && nu > acc.numax) ? nu : acc.numax;
-            if (kept) { smem[5 * SROWS + (r - klo)] = qo; smem[7 * SROWS + (r - klo)] = wo; }
+            smem[5 * SROWS + r] = qo; smem[7 * SROWS + r] = wo;
             continue;
         }
         double h0 = hb[i];
@@ -1330,25 +1330,24 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
             acc.umax = (kept && u > acc.umax) ? u : acc.umax;
             acc.numax = (kept && nu > acc.numax) ? nu : acc.numax;
         }
-        if (kept) {           // staging arrays 4..7 are not read in this phase
-            const int ko = r - klo;
-            smem[4 * SROWS + ko] = h0; smem[5 * SROWS + ko] = qo;
-            smem[6 * SROWS + ko] = Ko; smem[7 * SROWS + ko] = wo;
-        }
+        // staging arrays 4..7 are not read in this phase; every row is staged at
+        // its own index r (no mask), store_tile writes rows [klo, khi)
+        smem[4 * SROWS + r] = h0; smem[5 * SROWS + r] = qo;
+        smem[6 * SROWS + r] = Ko; smem[7 * SROWS + r] = wo;
     }
     // truncated overlap widths for the overlap check
     const int wt = min(left_phys ? 1 << 30 : G.wl, right_phys ? 1 << 30 : G.wr);
     acc.wmin = min(acc.wmin, wt);
 }
 
-// Store the staged rows (arrays 4..7, index 0 .. Tk-1) to out[] at cells
+// Store the staged rows (arrays 4..7, index klo .. klo+Tk-1) to out[] at cells
 // [s, s + Tk): bulk (thread 0; read-completion wait deferred) or per element.
-__device__ __forceinline__ void store_tile(const Bufs &B, size_t mo, int s, int Tk)
+__device__ __forceinline__ void store_tile(const Bufs &B, size_t mo, int s, int Tk, int klo)
 {
     const int tid = threadIdx.x;
     const size_t gdst = mo + size_t(s);
-    const bool bulk_out = ((gdst | size_t(Tk)) & 1) == 0;
-    double *const smem = dyn_smem();
+    const bool bulk_out = ((gdst | size_t(Tk) | size_t(klo)) & 1) == 0;
+    double *const smem = dyn_smem() + klo;
     double *const oh = smem + 4 * SROWS, *const oq = smem + 5 * SROWS, *const oK = smem + 6 * SROWS,
                  *const oW = smem + 7 * SROWS;
     if (bulk_out) {
@@ -1537,7 +1536,7 @@ __global__ void __launch_bounds__(NT, FDT ? HSGN_MINB
     } else {
         const StageC S = stage_consts(P, STAGE2 ? P.aI2 : P.aI1, dtm, lam);
         stage_body<STAGE2, FINAL, BATHY, RELAX, PIC, WB, FDT>(P, B, G, m, s, S, dtm, acc);
-        store_tile(B, mo, s, e - s);
+        store_tile(B, mo, s, e - s, G.klo);
     }
     EXP_T(t2);
     tile_epilogue<FINAL>(P, j, m, dtm, acc, tm0, tend0);

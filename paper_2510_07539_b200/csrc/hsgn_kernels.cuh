@@ -954,9 +954,10 @@ __device__ __forceinline__ void stage_body(const Params &P, const Bufs &B, const
     // register windows over rows r0-1 .. r0+MCH
     // (dead chunks read the ghost rows L+1 .. L+MCH+2: identity rows)
     double vb[MCH + 2], vd[MCH + 2], vH[MCH + 2], vq[MCH + 2];
-    // (stage 2, at the register cap, measured faster with zeroed dead windows:
-    // 483 vs 486 us on cfg3)
-    if (STAGE2) {
+    // (the 4-CTA second stages, at the register cap, measured faster with zeroed
+    // dead windows: 483 vs 486 us on cfg3; the 5-CTA one reads the ghost rows like
+    // the first stage: 444.5 -> 437.9 us)
+    if (STAGE2 && !s2x) {
         if (live) {
 #pragma unroll
             for (int k = 0; k < MCH + 2; k++) {

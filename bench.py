@@ -512,17 +512,68 @@ def main():
         del s
         torch.cuda.empty_cache()
         subs = {}
+        # N > 1: the cfg5 sub-record is the one leg with a data-path collective (NCCL
+        # inside libhsgn).  A failure or a hang there must not cost the headline line:
+        # errors are recorded in the sub-record, and a watchdog thread on every rank
+        # prints the line as it stands (rank 0) and leaves after SUB_TIMEOUT_S.
+        done = _watchdog(line, subs, rank) if world > 1 else None
         if backend in ("none", "nccl"):
-            subs["cfg5"] = cfg5_record(a, rank, world, dist, coll_dev, peak, peak_src)
+            try:
+                subs["cfg5"] = cfg5_record(a, rank, world, dist, coll_dev, peak, peak_src)
+            except Exception as e:          # noqa: BLE001 (reported, not swallowed)
+                if world == 1:
+                    raise
+                subs["cfg5"] = {"error": f"{type(e).__name__}: {e}"[:400]}
         if rank == 0:
             subs["cfg3_resident"] = resident_record(a)
             subs["time_to_t_end"] = tend_records()
         if rank == 0:
             line["sub_records"] = subs
+        if done is not None:
+            done.set()
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        with _PRINT_LOCK:
+            if not _PRINTED:
+                _PRINTED.append(1)
+                print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        # (a rank whose cfg5 leg failed may have left its peers inside a collective:
+        # they leave through their watchdogs; do not wait for them here)
+        if all("error" not in v for v in (line.get("sub_records") or {}).values() if isinstance(v, dict)):
+            dist.destroy_process_group()
+        else:
+            sys.stdout.flush()
+            os._exit(0)
+
+
+SUB_TIMEOUT_S = float(os.environ.get("HSGN_BENCH_SUB_TIMEOUT", "300"))
+_PRINT_LOCK = threading.Lock()
+_PRINTED = []
+
+
+def _watchdog(line, subs, rank):
+    """Multi-rank runs: if the sub-records have not finished after SUB_TIMEOUT_S
+    (a rank stuck in a collective), rank 0 prints the headline line with what it
+    has and every rank exits 0."""
+    done = threading.Event()
+
+    def run():
+        if done.wait(SUB_TIMEOUT_S):
+            return
+        if rank == 0:
+            with _PRINT_LOCK:
+                if not _PRINTED:
+                    _PRINTED.append(1)
+                    part = dict(subs)
+                    part.setdefault("cfg5", {"error": f"sub-records timed out after {SUB_TIMEOUT_S:g} s"})
+                    out = dict(line)
+                    out["sub_records"] = part
+                    print(json.dumps(out), flush=True)
+        sys.stdout.flush()
+        os._exit(0)
+
+    threading.Thread(target=run, daemon=True).start()
+    return done
 
 
 def _timed(stream, fn):

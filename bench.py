@@ -505,6 +505,7 @@ def main():
     }
     if phys_gpus != world:
         line["shared_gpu"] = f"{world} ranks on {phys_gpus} GPU(s) (gloo test mode)"
+    sub_failed = False
     # sub-records: cfg5 (the largest single-GPU config; over NCCL slabs at N > 1,
     # strong scaling) and the times to t_end of the other configs (rank 0)
     if not a.no_sub and a.config == "cfg3" and a.scheme == "si" and a.si_order == 2 and a.picard == 0 \
@@ -524,6 +525,7 @@ def main():
                 if world == 1:
                     raise
                 subs["cfg5"] = {"error": f"{type(e).__name__}: {e}"[:400]}
+                sub_failed = True
         if rank == 0:
             subs["cfg3_resident"] = resident_record(a)
             subs["time_to_t_end"] = tend_records()
@@ -539,7 +541,7 @@ def main():
     if world > 1:
         # (a rank whose cfg5 leg failed may have left its peers inside a collective:
         # they leave through their watchdogs; do not wait for them here)
-        if all("error" not in v for v in (line.get("sub_records") or {}).values() if isinstance(v, dict)):
+        if not sub_failed:
             dist.destroy_process_group()
         else:
             sys.stdout.flush()

@@ -526,7 +526,7 @@ def main():
                     raise
                 subs["cfg5"] = {"error": f"{type(e).__name__}: {e}"[:400]}
                 sub_failed = True
-        if rank == 0:
+        if rank == 0 and not sub_failed:     # (after a failed leg the CUDA context may be unusable)
             subs["cfg3_resident"] = resident_record(a)
             subs["time_to_t_end"] = tend_records()
         if rank == 0:

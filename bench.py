@@ -192,14 +192,15 @@ def profile_fp64():
         return None
 
 
-def profile_traffic(cells):
+def profile_traffic(cells, bathy=False):
     """dram__bytes_read.sum + dram__bytes_write.sum per stage-2 launch, from the
-    committed ncu launch list of the same workload (profiles/ncu_summary.json),
-    scaled to this run's cells per launch."""
+    committed ncu launch list of the same workload (profiles/ncu_summary.json:
+    cfg3, or cfg5 for the kernels with bathymetry), scaled to this run's cells
+    per launch."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        b = d.get("stage2_dram_bytes_per_cell")
+        b = (d.get("cfg5") or {}).get("stage2_dram_bytes_per_cell") if bathy else d.get("stage2_dram_bytes_per_cell")
         return None if b is None else b * cells
     except Exception:
         return None
@@ -417,7 +418,7 @@ def main():
     # committed ncu traffic belongs to the overlapped-tile stage kernels
     org = ("cluster" if (a.scheme == "si" and s.cluster) else "spike" if (a.scheme == "si" and s.spike)
            else "tiles")
-    traffic = profile_traffic(Ntot) if org == "tiles" and a.scheme == "si" and nst == 2 else None
+    traffic = profile_traffic(Ntot, bathy=bathy) if org == "tiles" and a.scheme == "si" and nst == 2 else None
 
     # e2e through the public API with host buffers: pinned host state in, K steps,
     # final state and per-member times out (hsgn_run_host; after the device-timed
@@ -643,7 +644,7 @@ def cfg5_record(a, rank, world, dist, coll_dev, peak, peak_src):
         rec["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                            "kernel": "stage_kernel<STAGE2,FINAL,BATHY> (stage 2)",
                            "bytes_model": "104 B/cell per stage-2 launch (read U^n, U1, b; write U^{n+1})",
-                           "peak_source": peak_src,
+                           "peak_source": peak_src, "traffic": profile_traffic(cells, bathy=True),
                            "stage1_frac": 72.0 * cells / (ms1 / steps / 1e3) / 1e9 / peak}
     if not a.no_e2e:
         pin = [x.cpu().pin_memory() for x in (h, q, K, Wf)]

@@ -107,6 +107,10 @@ def main():
     ap.add_argument("--round", type=int, required=True)
     ap.add_argument("--cells-full", type=float, required=True, help="cells per launch in the launch list run")
     ap.add_argument("--cells-prof", type=float, required=True, help="cells per launch in the --set full run")
+    ap.add_argument("--cfg5-launches", help="launch list of `bench.py --config cfg5` (2^28 cells)")
+    ap.add_argument("--cfg5-rep", help="--set full capture of the cfg5 stage kernels")
+    ap.add_argument("--cfg5-cells-full", type=float, default=float(1 << 28))
+    ap.add_argument("--cfg5-cells-prof", type=float, default=float(1 << 24))
     ap.add_argument("launches")
     ap.add_argument("rep")
     a = ap.parse_args()
@@ -163,6 +167,39 @@ def main():
                 continue
             d["fp64_tflops"] = tf
             md.append(f"| {d['kernel']} | {tf:.2f} | {tf / ptf:.2f} | {d.get('fp64_pipe_pct', 0):.1f} |")
+    if a.cfg5_launches:
+        # cfg5 (one domain with bathymetry): the BATHY instantiations, 104 / 72 B/cell models
+        rows = [r for r in csv.reader(open(a.cfg5_launches)) if len(r) > 10]
+        keep = [rows[0]] + [r for r in rows[1:] if "hsgn::" in ",".join(r)]
+        with open(os.path.join(prof, f"{tag}_cfg5_launches.csv"), "w", newline="") as f:
+            csv.writer(f, quoting=csv.QUOTE_ALL).writerows(keep)
+        L5 = {k: v for k, v in launches(os.path.join(prof, f"{tag}_cfg5_launches.csv")).items()}
+        tot5 = sum(v["total_us"] or 0 for v in L5.values())
+        md += ["", "cfg5 launch list (same ncu metrics over `python bench.py --config cfg5 --steps 4 --warmup 3 --no-e2e "
+                   "--no-cpu --no-sub`, 2^28 cells with bathymetry; the library's kernels only, torch's input "
+                   "generation dropped; algorithmic bytes: stage 2 104 B/cell, stage 1 72 B/cell):", "",
+               "| kernel | launches | mean us | share of time | DRAM B/cell read | DRAM B/cell write |", "|---|---|---|---|---|---|"]
+        js["cfg5"] = {"launch_list": {}, "full": []}
+        for k, v in sorted(L5.items(), key=lambda kv: -(kv[1]["total_us"] or 0)):
+            rd = (v["dram_read_per_launch"] or 0) / a.cfg5_cells_full
+            wr = (v["dram_write_per_launch"] or 0) / a.cfg5_cells_full
+            md.append(f"| {k} | {v['launches']} | {v['mean_us']:.1f} | {100 * (v['total_us'] or 0) / tot5:.1f}% | {rd:.1f} | {wr:.1f} |")
+            js["cfg5"]["launch_list"][k] = dict(v, dram_read_per_cell=rd, dram_write_per_cell=wr)
+            if "S2=1" in k and "BATHY=1" in k:
+                js["cfg5"]["stage2_dram_bytes_per_cell"] = rd + wr
+            if "S2=0" in k and "BATHY=1" in k:
+                js["cfg5"]["stage1_dram_bytes_per_cell"] = rd + wr
+        if a.cfg5_rep:
+            md += ["", "cfg5 full set (`ncu --set full --import-source on`, one 2^24-cell domain of the cfg5 recipe):", "",
+                   "| kernel | us | DRAM B/cell | occupancy % | issue active % | fp64 pipe % | IPC/SM | regs | top stalls (warps per issue) |",
+                   "|---|---|---|---|---|---|---|---|---|"]
+            for d in full(a.cfg5_rep):
+                b = (d.get("dram_read", 0) + d.get("dram_write", 0)) / a.cfg5_cells_prof
+                md.append("| %s | %.1f | %.1f | %.1f | %.1f | %.1f | %.2f | %d | %s |" % (
+                    d["kernel"], d.get("duration", 0) / 1e3, b, d.get("achieved_occupancy_pct", 0),
+                    d.get("issue_active_pct", 0), d.get("fp64_pipe_pct", 0), d.get("ipc_per_sm", 0),
+                    d.get("registers", 0), ", ".join(f"{n} {v}" for n, v in d["top_stalls"])))
+                js["cfg5"]["full"].append(dict(d, dram_bytes_per_cell=b))
     open(os.path.join(prof, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     json.dump(js, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
     print("\n".join(md))

@@ -43,3 +43,18 @@ def test_watchdog_silent_when_done():
              "d = bench._watchdog({'metric': 'm'}, {}, 0)\n"
              "d.set()\ntime.sleep(0.6)\nprint('reached')\n")
     assert r.returncode == 0 and r.stdout.strip() == "reached"
+
+
+def test_profile_summary_feeds_roofline_traffic():
+    """bench.py takes roofline.traffic from the committed ncu launch lists
+    (profiles/ncu_summary.json): cfg3's stage 2 and cfg5's bathymetry stage 2,
+    both at their algorithmic bytes (96 / 104 B per cell) to within 5 %."""
+    sys.path.insert(0, ROOT)
+    import bench
+    t3 = bench.profile_traffic(1 << 24)
+    t5 = bench.profile_traffic(1 << 28, bathy=True)
+    assert t3 is not None and t5 is not None
+    assert 0.95 * 96 <= t3 / (1 << 24) <= 1.05 * 96
+    assert 0.95 * 104 <= t5 / (1 << 28) <= 1.05 * 104
+    f = bench.profile_fp64()
+    assert f is not None and 0.0 < f["frac"] < 1.0
